@@ -1,0 +1,994 @@
+// C ABI of libef200.so (declared in include/ef200.h): context, tables, records and the
+// frontier step.  All device work is issued on the context's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ef_kernels.cuh"
+
+using namespace ef;
+
+namespace {
+
+constexpr int kMatchThreads = 256;
+constexpr int kMatThreads = 256;
+constexpr int kHashThreads = 128;
+constexpr int kPriceThreads = 64;
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;  // elements
+  // grow (optionally preserving contents); returns cudaError
+  cudaError_t reserve(size_t n, cudaStream_t st, bool keep = false) {
+    if (n <= cap) return cudaSuccess;
+    size_t nc = std::max(n, cap * 2 + 16);
+    T* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, nc * sizeof(T));
+    if (e != cudaSuccess) return e;
+    if (keep && p && cap) {
+      e = cudaMemcpyAsync(q, p, cap * sizeof(T), cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) return e;
+      cudaStreamSynchronize(st);
+    }
+    if (p) cudaFree(p);
+    p = q;
+    cap = nc;
+    return cudaSuccess;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct WeightSet {
+  int32_t kind = 0, oc = 0;
+  uint64_t w_off = 0, w_n = 0, b_off = 0, b_n = 0;
+  bool has_b = false;
+  int32_t dv[4] = {0, 0, 0, 0};
+  std::string hdr_w, hdr_b;
+  bool ready = false;  // tensors present + digest computed
+};
+
+}  // namespace
+
+struct ef_ctx {
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  std::string err;
+  int n_sm = 148;
+
+  // host mirrors of the tables
+  std::vector<ef_sig_desc> sig_desc;
+  std::vector<uint8_t> sig_exact;
+  std::vector<std::string> sig_text;
+  std::vector<std::vector<int32_t>> row_alg;
+  std::vector<std::vector<double>> row_t, row_e;
+  std::vector<std::string> names;
+  std::vector<WeightSet> ws;
+  bool dirty = true;
+
+  // device tables
+  DevBuf<ef_sig_desc> d_sig_desc;
+  DevBuf<uint32_t> d_text_off, d_text_len, d_row_off, d_row_n, d_sig_ht_val, d_dv_ht_val, d_name_off, d_name_len;
+  DevBuf<uint8_t> d_text, d_names, d_input_text, d_hdr;
+  DevBuf<int32_t> d_row_alg, d_dv_tuple;
+  DevBuf<double> d_row_t, d_row_e;
+  DevBuf<unsigned long long> d_sig_ht_key, d_dv_ht_key;
+  DevBuf<uint64_t> d_ws_digest;
+  DevBuf<double> d_pool;
+  uint64_t pool_used = 0;
+  uint32_t sig_ht_mask = 0, dv_ht_mask = 0;
+  std::string input_text;
+
+  // records
+  Geo geo{};
+  bool have_geo = false;
+  std::vector<char*> chunks;
+  uint32_t slots_per_chunk = 0;
+  std::vector<uint32_t> free_slots;
+  uint32_t n_slots = 0;
+
+  // step buffers
+  DevBuf<unsigned long long> d_parent_addr, d_sites, d_step_key, d_addr_a, d_addr_b;
+  DevBuf<uint32_t> d_pscratch, d_site_count, d_cand_off, d_step_seq, d_scalars;
+  DevBuf<char> d_cand;
+  DevBuf<int32_t> d_srcpos, d_req_dv;
+  DevBuf<uint8_t> d_seed;
+  DevBuf<ef_cand_result> d_res;
+  DevBuf<ef_sig_desc> d_req_sig;
+  DevBuf<uint64_t> d_hash_out;
+  uint32_t cand_cap = 0, site_cap = 0;
+  uint32_t req_cap = 4096;
+  uint32_t last_total = 0;
+  uint32_t last_req_sig = 0, last_req_dv = 0;
+  uint32_t* h_scalars = nullptr;  // pinned: total, err, n_req_sig, n_req_dv, vis_count lo/hi
+
+  // visited set
+  DevBuf<unsigned long long> d_vis, d_vis_count;
+  uint32_t vis_mask = 0;
+
+  cudaEvent_t ev[6] = {};
+  float last_ms[5] = {0, 0, 0, 0, 0};
+};
+
+#define EF_CUDA(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t _e = (call);                                                             \
+    if (_e != cudaSuccess) {                                                             \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(_e);                     \
+      return EF_ERR_CUDA;                                                                \
+    }                                                                                    \
+  } while (0)
+
+#define EF_REQUIRE(cond, msg)  \
+  do {                         \
+    if (!(cond)) {             \
+      ctx->err = (msg);        \
+      return EF_ERR_ARG;       \
+    }                          \
+  } while (0)
+
+static Tables make_tables(ef_ctx* ctx) {
+  Tables T{};
+  T.sig_desc = ctx->d_sig_desc.p;
+  T.sig_text_off = ctx->d_text_off.p;
+  T.sig_text_len = ctx->d_text_len.p;
+  T.sig_text = ctx->d_text.p;
+  T.row_off = ctx->d_row_off.p;
+  T.row_n = ctx->d_row_n.p;
+  T.row_alg = ctx->d_row_alg.p;
+  T.row_t = ctx->d_row_t.p;
+  T.row_e = ctx->d_row_e.p;
+  T.sig_ht_key = ctx->d_sig_ht_key.p;
+  T.sig_ht_val = ctx->d_sig_ht_val.p;
+  T.sig_ht_mask = ctx->sig_ht_mask;
+  T.ws_digest = ctx->d_ws_digest.p;
+  T.dv_tuple = ctx->d_dv_tuple.p;
+  T.dv_ht_key = ctx->d_dv_ht_key.p;
+  T.dv_ht_val = ctx->d_dv_ht_val.p;
+  T.dv_ht_mask = ctx->dv_ht_mask;
+  T.name_off = ctx->d_name_off.p;
+  T.name_len = ctx->d_name_len.p;
+  T.names = ctx->d_names.p;
+  T.input_text = ctx->d_input_text.p;
+  T.input_text_len = (uint32_t)ctx->input_text.size();
+  return T;
+}
+
+static char* slot_addr(ef_ctx* ctx, uint32_t slot) {
+  return ctx->chunks[slot / ctx->slots_per_chunk] + (uint64_t)(slot % ctx->slots_per_chunk) * ctx->geo.bytes;
+}
+
+int ef_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+ef_ctx* ef_create(int device) {
+  ef_ctx* ctx = new ef_ctx();
+  ctx->dev = device;
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return nullptr;
+  }
+  cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, device);
+  cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
+  for (auto& e : ctx->ev) cudaEventCreate(&e);
+  // weight set 0 = "no weights" (digest of the empty message)
+  ctx->ws.emplace_back();
+  ctx->ws[0].dv[0] = 0;
+  return ctx;
+}
+
+void ef_destroy(ef_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->dev);
+  cudaStreamSynchronize(ctx->st);
+  for (char* c : ctx->chunks) cudaFree(c);
+  ctx->d_sig_desc.release();
+  ctx->d_text_off.release();
+  ctx->d_text_len.release();
+  ctx->d_row_off.release();
+  ctx->d_row_n.release();
+  ctx->d_sig_ht_val.release();
+  ctx->d_dv_ht_val.release();
+  ctx->d_name_off.release();
+  ctx->d_name_len.release();
+  ctx->d_text.release();
+  ctx->d_names.release();
+  ctx->d_input_text.release();
+  ctx->d_hdr.release();
+  ctx->d_row_alg.release();
+  ctx->d_dv_tuple.release();
+  ctx->d_row_t.release();
+  ctx->d_row_e.release();
+  ctx->d_sig_ht_key.release();
+  ctx->d_dv_ht_key.release();
+  ctx->d_ws_digest.release();
+  ctx->d_pool.release();
+  ctx->d_parent_addr.release();
+  ctx->d_sites.release();
+  ctx->d_step_key.release();
+  ctx->d_addr_a.release();
+  ctx->d_addr_b.release();
+  ctx->d_pscratch.release();
+  ctx->d_site_count.release();
+  ctx->d_cand_off.release();
+  ctx->d_step_seq.release();
+  ctx->d_scalars.release();
+  ctx->d_cand.release();
+  ctx->d_srcpos.release();
+  ctx->d_req_dv.release();
+  ctx->d_seed.release();
+  ctx->d_res.release();
+  ctx->d_req_sig.release();
+  ctx->d_hash_out.release();
+  ctx->d_vis.release();
+  ctx->d_vis_count.release();
+  for (auto& e : ctx->ev) cudaEventDestroy(e);
+  if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
+  cudaStreamDestroy(ctx->st);
+  delete ctx;
+}
+
+const char* ef_error(ef_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+// ---------------------------------------------------------------------------------------------
+// tables
+// ---------------------------------------------------------------------------------------------
+
+int ef_sig_put(ef_ctx* ctx, uint32_t id, const ef_sig_desc* desc, const char* text, uint32_t text_len, int exact) {
+  EF_REQUIRE(desc && text, "ef_sig_put: null argument");
+  if (id >= ctx->sig_desc.size()) {
+    ctx->sig_desc.resize(id + 1);
+    ctx->sig_exact.resize(id + 1, 0);
+    ctx->sig_text.resize(id + 1);
+    ctx->row_alg.resize(id + 1);
+    ctx->row_t.resize(id + 1);
+    ctx->row_e.resize(id + 1);
+  }
+  ctx->sig_desc[id] = *desc;
+  ctx->sig_exact[id] = exact ? 1 : 0;
+  ctx->sig_text[id].assign(text, text_len);
+  ctx->dirty = true;
+  return EF_OK;
+}
+
+int ef_sig_costs(ef_ctx* ctx, uint32_t id, uint32_t n, const int32_t* alg, const double* time_ms, const double* energy) {
+  EF_REQUIRE(id < ctx->sig_desc.size(), "ef_sig_costs: unknown signature id");
+  EF_REQUIRE(n <= 255, "ef_sig_costs: too many algorithms");
+  ctx->row_alg[id].assign(alg, alg + n);
+  ctx->row_t[id].assign(time_ms, time_ms + n);
+  ctx->row_e[id].assign(energy, energy + n);
+  ctx->dirty = true;
+  return EF_OK;
+}
+
+int ef_name_put(ef_ctx* ctx, uint32_t id, const char* name, uint32_t len) {
+  if (id >= ctx->names.size()) ctx->names.resize(id + 1);
+  ctx->names[id].assign(name, len);
+  ctx->dirty = true;
+  return EF_OK;
+}
+
+static int pool_alloc(ef_ctx* ctx, uint64_t n, uint64_t* off) {
+  uint64_t need = ctx->pool_used + n + 2;  // +2 keeps zero-length sets at distinct offsets
+  EF_CUDA(ctx->d_pool.reserve(need, ctx->st, true));
+  *off = ctx->pool_used;
+  ctx->pool_used += n;
+  return EF_OK;
+}
+
+int ef_wset_put(ef_ctx* ctx, uint32_t id, int32_t kind, int32_t oc, const double* w, uint64_t w_n, const double* b,
+                uint64_t b_n, const char* hdr_w, uint32_t hlen_w, const char* hdr_b, uint32_t hlen_b) {
+  EF_REQUIRE(id != kEmptyWset || (w_n == 0 && b_n == 0), "weight set 0 is reserved for 'no weights'");
+  if (id >= ctx->ws.size()) ctx->ws.resize(id + 1);
+  WeightSet& S = ctx->ws[id];
+  S = WeightSet();
+  S.kind = kind;
+  S.oc = oc;
+  S.w_n = w_n;
+  S.b_n = b_n;
+  S.has_b = b != nullptr;
+  if (hdr_w) S.hdr_w.assign(hdr_w, hlen_w);
+  if (hdr_b) S.hdr_b.assign(hdr_b, hlen_b);
+  int rc = pool_alloc(ctx, w_n, &S.w_off);
+  if (rc) return rc;
+  rc = pool_alloc(ctx, b_n, &S.b_off);
+  if (rc) return rc;
+  if (w_n) EF_CUDA(cudaMemcpyAsync(ctx->d_pool.p + S.w_off, w, w_n * 8, cudaMemcpyHostToDevice, ctx->st));
+  if (b_n && b) EF_CUDA(cudaMemcpyAsync(ctx->d_pool.p + S.b_off, b, b_n * 8, cudaMemcpyHostToDevice, ctx->st));
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  ctx->dirty = true;
+  return EF_OK;
+}
+
+int ef_wset_derive(ef_ctx* ctx, uint32_t id, int32_t op, uint32_t a, uint32_t b, int32_t s0, const char* hdr_w,
+                   uint32_t hlen_w, const char* hdr_b, uint32_t hlen_b) {
+  EF_REQUIRE(a < ctx->ws.size() && ctx->ws[a].kind == EF_K_CONV2D, "ef_wset_derive: source must be a conv weight set");
+  const WeightSet A = ctx->ws[a];
+  EF_REQUIRE(A.oc > 0, "ef_wset_derive: conv without out channels");
+  const uint64_t inner = A.w_n / (uint64_t)A.oc;
+  WeightSet S;
+  S.kind = EF_K_CONV2D;
+  S.has_b = true;
+  S.dv[0] = op;
+  S.dv[1] = (int32_t)a;
+  S.dv[2] = (int32_t)b;
+  S.dv[3] = s0;
+  S.hdr_w.assign(hdr_w, hlen_w);
+  S.hdr_b.assign(hdr_b, hlen_b);
+  if (op == EF_D_MERGE) {
+    EF_REQUIRE(b < ctx->ws.size() && ctx->ws[b].kind == EF_K_CONV2D, "merge needs two conv weight sets");
+    S.oc = A.oc + ctx->ws[b].oc;
+  } else if (op == EF_D_SLICE_LO) {
+    S.oc = s0;
+  } else if (op == EF_D_SLICE_HI) {
+    S.oc = A.oc - s0;
+  } else if (op == EF_D_FOLD) {
+    EF_REQUIRE(b < ctx->ws.size() && ctx->ws[b].kind == EF_K_BATCHNORM, "fold needs a batchnorm weight set");
+    S.oc = A.oc;
+  } else {
+    EF_REQUIRE(false, "ef_wset_derive: unknown op");
+  }
+  S.w_n = (uint64_t)S.oc * inner;
+  S.b_n = (uint64_t)S.oc;
+  int rc = pool_alloc(ctx, S.w_n, &S.w_off);
+  if (rc) return rc;
+  rc = pool_alloc(ctx, S.b_n, &S.b_off);
+  if (rc) return rc;
+  if (id >= ctx->ws.size()) ctx->ws.resize(id + 1);
+  ctx->ws[id] = S;
+  ctx->dirty = true;
+  return EF_OK;
+}
+
+int ef_wset_read(ef_ctx* ctx, uint32_t id, double* w, uint64_t* w_n, double* b, uint64_t* b_n) {
+  EF_REQUIRE(id < ctx->ws.size(), "ef_wset_read: unknown weight set");
+  const WeightSet& S = ctx->ws[id];
+  if (w_n) {
+    if (w) EF_CUDA(cudaMemcpyAsync(w, ctx->d_pool.p + S.w_off, std::min(*w_n, S.w_n) * 8, cudaMemcpyDeviceToHost, ctx->st));
+    *w_n = S.w_n;
+  }
+  if (b_n) {
+    uint64_t have = S.has_b ? S.b_n : 0;
+    if (b && have) EF_CUDA(cudaMemcpyAsync(b, ctx->d_pool.p + S.b_off, std::min(*b_n, have) * 8, cudaMemcpyDeviceToHost, ctx->st));
+    *b_n = have;
+  }
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+int ef_wset_digest(ef_ctx* ctx, uint32_t id, uint8_t out[16]) {
+  EF_REQUIRE(id < ctx->ws.size() && ctx->ws[id].ready, "ef_wset_digest: weight set not committed");
+  EF_CUDA(cudaMemcpyAsync(out, ctx->d_ws_digest.p + 2 * id, 16, cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+template <typename T>
+static int upload(ef_ctx* ctx, DevBuf<T>& buf, const std::vector<T>& v) {
+  EF_CUDA(buf.reserve(std::max<size_t>(v.size(), 1), ctx->st));
+  if (!v.empty()) EF_CUDA(cudaMemcpyAsync(buf.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->st));
+  return EF_OK;
+}
+
+static uint32_t pow2_at_least(uint64_t n) {
+  uint32_t m = 16;
+  while (m < n) m <<= 1;
+  return m;
+}
+
+int ef_tables_commit(ef_ctx* ctx) {
+  cudaSetDevice(ctx->dev);
+  const size_t ns = ctx->sig_desc.size();
+  // signature texts, 8-byte aligned and zero padded (the hash kernel reads them as words)
+  std::vector<uint32_t> toff(ns), tlen(ns), roff(ns), rn(ns);
+  std::vector<uint8_t> text;
+  std::vector<int32_t> ralg;
+  std::vector<double> rt, re;
+  for (size_t i = 0; i < ns; ++i) {
+    toff[i] = (uint32_t)text.size();
+    tlen[i] = (uint32_t)ctx->sig_text[i].size();
+    text.insert(text.end(), ctx->sig_text[i].begin(), ctx->sig_text[i].end());
+    while (text.size() % 8) text.push_back(0);
+    roff[i] = (uint32_t)ralg.size();
+    rn[i] = (uint32_t)ctx->row_alg[i].size();
+    ralg.insert(ralg.end(), ctx->row_alg[i].begin(), ctx->row_alg[i].end());
+    rt.insert(rt.end(), ctx->row_t[i].begin(), ctx->row_t[i].end());
+    re.insert(re.end(), ctx->row_e[i].begin(), ctx->row_e[i].end());
+  }
+  text.resize(text.size() + 8, 0);
+  int rc;
+  if ((rc = upload(ctx, ctx->d_sig_desc, ctx->sig_desc)) || (rc = upload(ctx, ctx->d_text_off, toff)) ||
+      (rc = upload(ctx, ctx->d_text_len, tlen)) || (rc = upload(ctx, ctx->d_text, text)) ||
+      (rc = upload(ctx, ctx->d_row_off, roff)) || (rc = upload(ctx, ctx->d_row_n, rn)) ||
+      (rc = upload(ctx, ctx->d_row_alg, ralg)) || (rc = upload(ctx, ctx->d_row_t, rt)) ||
+      (rc = upload(ctx, ctx->d_row_e, re)))
+    return rc;
+  // exact-signature lookup table
+  {
+    uint32_t cap = pow2_at_least(2 * ns + 2);
+    std::vector<unsigned long long> keys(cap, 0);
+    std::vector<uint32_t> vals(cap, 0);
+    for (size_t i = 0; i < ns; ++i) {
+      if (!ctx->sig_exact[i]) continue;
+      uint64_t k = desc_key(ctx->sig_desc[i]);
+      uint32_t s = (uint32_t)k & (cap - 1);
+      bool dup = false;
+      while (keys[s]) {
+        if (keys[s] == k && desc_eq(ctx->sig_desc[vals[s]], ctx->sig_desc[i])) {
+          dup = true;
+          break;
+        }
+        s = (s + 1) & (cap - 1);
+      }
+      if (dup) continue;
+      keys[s] = k;
+      vals[s] = (uint32_t)i;
+    }
+    ctx->sig_ht_mask = cap - 1;
+    if ((rc = upload(ctx, ctx->d_sig_ht_key, keys)) || (rc = upload(ctx, ctx->d_sig_ht_val, vals))) return rc;
+  }
+  // names
+  {
+    std::vector<uint32_t> off(ctx->names.size()), len(ctx->names.size());
+    std::vector<uint8_t> pool;
+    for (size_t i = 0; i < ctx->names.size(); ++i) {
+      off[i] = (uint32_t)pool.size();
+      len[i] = (uint32_t)ctx->names[i].size();
+      pool.insert(pool.end(), ctx->names[i].begin(), ctx->names[i].end());
+    }
+    pool.push_back(0);
+    if ((rc = upload(ctx, ctx->d_name_off, off)) || (rc = upload(ctx, ctx->d_name_len, len)) ||
+        (rc = upload(ctx, ctx->d_names, pool)))
+      return rc;
+    std::vector<uint8_t> it(ctx->input_text.begin(), ctx->input_text.end());
+    it.push_back(0);
+    if ((rc = upload(ctx, ctx->d_input_text, it))) return rc;
+  }
+  // derivation table
+  const size_t nw = ctx->ws.size();
+  {
+    std::vector<int32_t> tup(4 * nw, 0);
+    uint32_t cap = pow2_at_least(2 * nw + 2);
+    std::vector<unsigned long long> keys(cap, 0);
+    std::vector<uint32_t> vals(cap, 0);
+    for (size_t i = 0; i < nw; ++i) {
+      for (int k = 0; k < 4; ++k) tup[4 * i + k] = ctx->ws[i].dv[k];
+      if (ctx->ws[i].dv[0] == 0) continue;
+      const int32_t* d = ctx->ws[i].dv;
+      uint64_t k = derive_key(d[0], (uint32_t)d[1], (uint32_t)d[2], d[3]);
+      uint32_t s = (uint32_t)k & (cap - 1);
+      while (keys[s]) s = (s + 1) & (cap - 1);
+      keys[s] = k;
+      vals[s] = (uint32_t)i;
+    }
+    ctx->dv_ht_mask = cap - 1;
+    if ((rc = upload(ctx, ctx->d_dv_tuple, tup)) || (rc = upload(ctx, ctx->d_dv_ht_key, keys)) ||
+        (rc = upload(ctx, ctx->d_dv_ht_val, vals)))
+      return rc;
+  }
+  // derived tensors, in id order (a derivation may use an earlier derived set)
+  EF_CUDA(ctx->d_ws_digest.reserve(2 * nw + 2, ctx->st, true));
+  std::vector<uint32_t> pending;
+  for (size_t i = 0; i < nw; ++i)
+    if (!ctx->ws[i].ready) pending.push_back((uint32_t)i);
+  if (!pending.empty()) {
+    std::vector<DeriveJob> djobs;
+    for (uint32_t i : pending) {
+      const WeightSet& S = ctx->ws[i];
+      if (S.dv[0] == 0) continue;
+      const WeightSet& A = ctx->ws[S.dv[1]];
+      DeriveJob J{};
+      J.op = S.dv[0];
+      J.wa = ctx->d_pool.p + A.w_off;
+      J.ba = A.has_b ? ctx->d_pool.p + A.b_off : nullptr;
+      J.oc_a = (uint64_t)A.oc;
+      J.inner = A.w_n / (uint64_t)A.oc;
+      J.s0 = S.dv[3];
+      if (J.op == EF_D_MERGE || J.op == EF_D_FOLD) {
+        const WeightSet& B = ctx->ws[S.dv[2]];
+        J.wb = ctx->d_pool.p + B.w_off;
+        J.bb = B.has_b ? ctx->d_pool.p + B.b_off : nullptr;
+        J.oc_b = (uint64_t)B.oc;
+      }
+      J.w_out = ctx->d_pool.p + S.w_off;
+      J.b_out = ctx->d_pool.p + S.b_off;
+      J.w_n = S.w_n;
+      J.b_n = S.b_n;
+      djobs.push_back(J);
+    }
+    if (!djobs.empty()) {
+      // one job per launch keeps dependencies between derived sets ordered on the stream
+      DevBuf<DeriveJob> dj;
+      EF_CUDA(dj.reserve(djobs.size(), ctx->st));
+      EF_CUDA(cudaMemcpyAsync(dj.p, djobs.data(), djobs.size() * sizeof(DeriveJob), cudaMemcpyHostToDevice, ctx->st));
+      for (size_t j = 0; j < djobs.size(); ++j) k_derive<<<ctx->n_sm * 4, 256, 0, ctx->st>>>(dj.p + j, 1);
+      EF_CUDA(cudaGetLastError());
+      EF_CUDA(cudaStreamSynchronize(ctx->st));
+      dj.release();
+    }
+    // digests: headers in sorted key order (bias < weight, scale < shift)
+    std::vector<uint8_t> hdr;
+    std::vector<DigestJob> jobs;
+    std::vector<std::pair<uint32_t, uint32_t>> hofs;  // (offset of first header, offset of second)
+    for (uint32_t i : pending) {
+      const WeightSet& S = ctx->ws[i];
+      uint32_t o1 = (uint32_t)hdr.size();
+      const std::string* h0 = nullptr;
+      const std::string* h1 = nullptr;
+      if (S.kind == EF_K_CONV2D) {
+        if (S.has_b) {
+          h0 = &S.hdr_b;
+          h1 = &S.hdr_w;
+        } else {
+          h0 = &S.hdr_w;
+        }
+      } else if (S.kind == EF_K_BATCHNORM) {
+        h0 = &S.hdr_w;
+        h1 = &S.hdr_b;
+      } else if (S.kind == EF_K_MATMUL) {
+        h0 = &S.hdr_w;
+      }
+      if (h0) hdr.insert(hdr.end(), h0->begin(), h0->end());
+      uint32_t o2 = (uint32_t)hdr.size();
+      if (h1) hdr.insert(hdr.end(), h1->begin(), h1->end());
+      hofs.push_back({o1, o2});
+    }
+    hdr.push_back(0);
+    if ((rc = upload(ctx, ctx->d_hdr, hdr))) return rc;
+    for (size_t j = 0; j < pending.size(); ++j) {
+      const WeightSet& S = ctx->ws[pending[j]];
+      DigestJob J{};
+      const uint8_t* hb = ctx->d_hdr.p;
+      uint32_t o1 = hofs[j].first, o2 = hofs[j].second;
+      uint32_t o3 = (j + 1 < hofs.size()) ? hofs[j + 1].first : (uint32_t)hdr.size() - 1;
+      J.hdr0 = hb + o1;
+      J.hlen0 = o2 - o1;
+      J.hdr1 = hb + o2;
+      J.hlen1 = o3 - o2;
+      const double* pw = ctx->d_pool.p + S.w_off;
+      const double* pb = ctx->d_pool.p + S.b_off;
+      if (S.kind == EF_K_CONV2D) {
+        if (S.has_b) {
+          J.t0 = pb;
+          J.n0 = S.b_n;
+          J.t1 = pw;
+          J.n1 = S.w_n;
+        } else {
+          J.t0 = pw;
+          J.n0 = S.w_n;
+        }
+      } else if (S.kind == EF_K_BATCHNORM) {
+        J.t0 = pw;
+        J.n0 = S.w_n;
+        J.t1 = pb;
+        J.n1 = S.b_n;
+      } else if (S.kind == EF_K_MATMUL) {
+        J.t0 = pw;
+        J.n0 = S.w_n;
+      }
+      J.out = ctx->d_ws_digest.p + 2 * pending[j];
+      jobs.push_back(J);
+    }
+    DevBuf<DigestJob> dj;
+    EF_CUDA(dj.reserve(jobs.size(), ctx->st));
+    EF_CUDA(cudaMemcpyAsync(dj.p, jobs.data(), jobs.size() * sizeof(DigestJob), cudaMemcpyHostToDevice, ctx->st));
+    k_digest<<<(unsigned)((jobs.size() + 31) / 32), 32, 0, ctx->st>>>(dj.p, (uint32_t)jobs.size());
+    EF_CUDA(cudaGetLastError());
+    EF_CUDA(cudaStreamSynchronize(ctx->st));
+    dj.release();
+    for (uint32_t i : pending) ctx->ws[i].ready = true;
+  }
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  ctx->dirty = false;
+  return EF_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// records
+// ---------------------------------------------------------------------------------------------
+
+int ef_set_geometry(ef_ctx* ctx, uint32_t cap_nodes, uint32_t cap_refs, uint32_t cap_outs, const char* input_text,
+                    uint32_t input_text_len, ef_geometry* out) {
+  EF_REQUIRE(cap_nodes > 0 && cap_nodes < (1u << 24), "ef_set_geometry: cap_nodes out of range");
+  EF_REQUIRE(!ctx->have_geo || ctx->n_slots == ctx->free_slots.size(), "ef_set_geometry: records still in use");
+  for (char* c : ctx->chunks) cudaFree(c);
+  ctx->chunks.clear();
+  ctx->free_slots.clear();
+  ctx->n_slots = 0;
+  auto al = [](uint32_t x) { return (x + 15u) & ~15u; };
+  Geo& g = ctx->geo;
+  g.cap_nodes = cap_nodes;
+  g.cap_refs = std::max<uint32_t>(cap_refs, 1);
+  g.cap_outs = std::max<uint32_t>(cap_outs, 1);
+  uint32_t o = 64;
+  g.o_nid = o;
+  o = al(o + 4 * cap_nodes);
+  g.o_sig = o;
+  o = al(o + 4 * cap_nodes);
+  g.o_aux = o;
+  o = al(o + 4 * cap_nodes);
+  g.o_nin = o;
+  o = al(o + 4 * cap_nodes);
+  g.o_inoff = o;
+  o = al(o + 4 * (cap_nodes + 1));
+  g.o_topo = o;
+  o = al(o + 4 * cap_nodes);
+  g.o_refs = o;
+  o = al(o + 4 * g.cap_refs);
+  g.o_outs = o;
+  o = al(o + 4 * g.cap_outs);
+  g.o_keys = o;
+  o = al(o + 16 * cap_nodes);
+  g.o_alg = o;
+  o = al(o + cap_nodes);
+  g.bytes = o;
+  ctx->slots_per_chunk = std::max<uint32_t>(1, (uint32_t)((64ull << 20) / g.bytes));
+  ctx->input_text.assign(input_text ? input_text : "", input_text ? input_text_len : 0);
+  ctx->have_geo = true;
+  ctx->dirty = true;
+  if (out) {
+    out->cap_nodes = g.cap_nodes;
+    out->cap_refs = g.cap_refs;
+    out->cap_outs = g.cap_outs;
+    out->record_bytes = g.bytes;
+    out->off_nid = g.o_nid;
+    out->off_sig = g.o_sig;
+    out->off_aux = g.o_aux;
+    out->off_nin = g.o_nin;
+    out->off_inoff = g.o_inoff;
+    out->off_topo = g.o_topo;
+    out->off_refs = g.o_refs;
+    out->off_outs = g.o_outs;
+    out->off_keys = g.o_keys;
+    out->off_alg = g.o_alg;
+  }
+  return EF_OK;
+}
+
+int ef_record_alloc(ef_ctx* ctx, uint32_t* slot) {
+  EF_REQUIRE(ctx->have_geo, "ef_record_alloc: no geometry");
+  if (ctx->free_slots.empty()) {
+    char* chunk = nullptr;
+    EF_CUDA(cudaMalloc(&chunk, (uint64_t)ctx->slots_per_chunk * ctx->geo.bytes));
+    uint32_t base = (uint32_t)ctx->chunks.size() * ctx->slots_per_chunk;
+    ctx->chunks.push_back(chunk);
+    for (uint32_t i = ctx->slots_per_chunk; i-- > 0;) ctx->free_slots.push_back(base + i);
+    ctx->n_slots += ctx->slots_per_chunk;
+  }
+  *slot = ctx->free_slots.back();
+  ctx->free_slots.pop_back();
+  return EF_OK;
+}
+
+int ef_record_free(ef_ctx* ctx, uint32_t slot) {
+  EF_REQUIRE(slot < ctx->n_slots, "ef_record_free: bad slot");
+  ctx->free_slots.push_back(slot);
+  return EF_OK;
+}
+
+int ef_record_write(ef_ctx* ctx, uint32_t slot, const void* host, uint64_t bytes) {
+  EF_REQUIRE(slot < ctx->n_slots && bytes <= ctx->geo.bytes, "ef_record_write: bad slot/size");
+  EF_CUDA(cudaMemcpyAsync(slot_addr(ctx, slot), host, bytes, cudaMemcpyHostToDevice, ctx->st));
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+int ef_record_read(ef_ctx* ctx, uint32_t slot, void* host, uint64_t bytes) {
+  EF_REQUIRE(slot < ctx->n_slots && bytes <= ctx->geo.bytes, "ef_record_read: bad slot/size");
+  EF_CUDA(cudaMemcpyAsync(host, slot_addr(ctx, slot), bytes, cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+static uint32_t hash_smem_nodes(ef_ctx* ctx) { return pow2_at_least(ctx->geo.cap_nodes); }
+static size_t hash_smem_bytes(uint32_t nodes) { return ((nodes + 15u) & ~15u) + 16ull * nodes; }
+
+static int ensure_hash_smem(ef_ctx* ctx, size_t bytes) {
+  EF_REQUIRE(bytes <= 227 * 1024, "graph too large for the shared-memory hash path (cap_nodes > 8192)");
+  EF_CUDA(cudaFuncSetAttribute(k_hash<kHashThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return EF_OK;
+}
+
+static int stage_addrs(ef_ctx* ctx, DevBuf<unsigned long long>& buf, const uint32_t* slots, uint32_t n) {
+  std::vector<unsigned long long> a(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    EF_REQUIRE(slots[i] < ctx->n_slots, "bad record slot");
+    a[i] = (unsigned long long)slot_addr(ctx, slots[i]);
+  }
+  return upload(ctx, buf, a);
+}
+
+int ef_hash_records(ef_ctx* ctx, const uint32_t* slots, uint32_t n, uint64_t* hashes) {
+  EF_REQUIRE(!ctx->dirty, "tables not committed (call ef_tables_commit)");
+  if (n == 0) return EF_OK;
+  int rc = stage_addrs(ctx, ctx->d_addr_a, slots, n);
+  if (rc) return rc;
+  EF_CUDA(ctx->d_hash_out.reserve(n, ctx->st));
+  EF_CUDA(ctx->d_scalars.reserve(16, ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_scalars.p, 0, 16 * 4, ctx->st));
+  HashArgs H{};
+  H.g = ctx->geo;
+  H.T = make_tables(ctx);
+  H.n = n;
+  H.rec = ctx->d_addr_a.p;
+  H.hash_out = ctx->d_hash_out.p;
+  H.smem_nodes = hash_smem_nodes(ctx);
+  H.err = ctx->d_scalars.p + 1;
+  size_t sm = hash_smem_bytes(H.smem_nodes);
+  if ((rc = ensure_hash_smem(ctx, sm))) return rc;
+  k_hash<kHashThreads><<<std::min<uint32_t>(n, ctx->n_sm * 4), kHashThreads, sm, ctx->st>>>(H);
+  EF_CUDA(cudaGetLastError());
+  EF_CUDA(cudaMemcpyAsync(hashes, ctx->d_hash_out.p, n * 8, cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  EF_REQUIRE(ctx->h_scalars[1] == 0, "hash kernel capacity error");
+  return EF_OK;
+}
+
+int ef_price_records(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const ef_price_params* pp, ef_cand_result* out) {
+  EF_REQUIRE(!ctx->dirty, "tables not committed (call ef_tables_commit)");
+  if (n == 0) return EF_OK;
+  int rc = stage_addrs(ctx, ctx->d_addr_a, slots, n);
+  if (rc) return rc;
+  EF_CUDA(ctx->d_res.reserve(std::max<size_t>(n, ctx->cand_cap), ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_res.p, 0, n * sizeof(ef_cand_result), ctx->st));
+  PriceArgs Pa{};
+  Pa.g = ctx->geo;
+  Pa.T = make_tables(ctx);
+  Pa.pp = *pp;
+  Pa.n = n;
+  Pa.rec = ctx->d_addr_a.p;
+  Pa.res = ctx->d_res.p;
+  k_price<<<(n + kPriceThreads - 1) / kPriceThreads, kPriceThreads, 0, ctx->st>>>(Pa);
+  EF_CUDA(cudaGetLastError());
+  EF_CUDA(cudaMemcpyAsync(out, ctx->d_res.p, n * sizeof(ef_cand_result), cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// visited set
+// ---------------------------------------------------------------------------------------------
+
+int ef_visited_reset(ef_ctx* ctx, uint64_t capacity) {
+  uint32_t cap = pow2_at_least(std::max<uint64_t>(capacity, 1024));
+  EF_CUDA(ctx->d_vis.reserve(cap, ctx->st));
+  EF_CUDA(ctx->d_vis_count.reserve(1, ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_vis.p, 0, (size_t)cap * 8, ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_vis_count.p, 0, 8, ctx->st));
+  ctx->vis_mask = cap - 1;
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+int ef_visited_insert(ef_ctx* ctx, const uint64_t* hashes, uint32_t n) {
+  EF_REQUIRE(ctx->vis_mask, "visited set not initialised");
+  if (!n) return EF_OK;
+  EF_CUDA(ctx->d_hash_out.reserve(n, ctx->st));
+  EF_CUDA(cudaMemcpyAsync(ctx->d_hash_out.p, hashes, n * 8, cudaMemcpyHostToDevice, ctx->st));
+  k_visited_put<<<(n + 255) / 256, 256, 0, ctx->st>>>(ctx->d_vis.p, ctx->vis_mask, ctx->d_vis_count.p,
+                                                       ctx->d_hash_out.p, n);
+  EF_CUDA(cudaGetLastError());
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+int ef_visited_count(ef_ctx* ctx, uint64_t* count) {
+  EF_REQUIRE(ctx->vis_mask, "visited set not initialised");
+  EF_CUDA(cudaMemcpyAsync(count, ctx->d_vis_count.p, 8, cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// the frontier step
+// ---------------------------------------------------------------------------------------------
+
+static int ensure_step_buffers(ef_ctx* ctx, uint32_t n_parents) {
+  const Geo& g = ctx->geo;
+  if (ctx->site_cap == 0) ctx->site_cap = std::max<uint32_t>(4 * g.cap_nodes, 256);
+  if (ctx->cand_cap == 0) ctx->cand_cap = std::max<uint32_t>(1024, std::min<uint32_t>(1u << 16, (uint32_t)((1ull << 30) / g.bytes)));
+  const uint64_t pstride = 4ull * g.cap_nodes + 1 + g.cap_refs;
+  EF_CUDA(ctx->d_parent_addr.reserve(n_parents, ctx->st));
+  EF_CUDA(ctx->d_pscratch.reserve(pstride * n_parents, ctx->st));
+  EF_CUDA(ctx->d_sites.reserve((uint64_t)ctx->site_cap * n_parents, ctx->st));
+  EF_CUDA(ctx->d_site_count.reserve(n_parents, ctx->st));
+  EF_CUDA(ctx->d_cand_off.reserve(n_parents + 1, ctx->st));
+  EF_CUDA(ctx->d_cand.reserve((uint64_t)ctx->cand_cap * g.bytes, ctx->st));
+  EF_CUDA(ctx->d_srcpos.reserve((uint64_t)ctx->cand_cap * g.cap_nodes, ctx->st));
+  EF_CUDA(ctx->d_seed.reserve((uint64_t)ctx->cand_cap * g.cap_nodes, ctx->st));
+  EF_CUDA(ctx->d_res.reserve(ctx->cand_cap, ctx->st));
+  uint32_t tcap = pow2_at_least(2ull * ctx->cand_cap);
+  EF_CUDA(ctx->d_step_key.reserve(tcap, ctx->st));
+  EF_CUDA(ctx->d_step_seq.reserve(tcap, ctx->st));
+  EF_CUDA(ctx->d_req_sig.reserve(ctx->req_cap, ctx->st));
+  EF_CUDA(ctx->d_req_dv.reserve(4 * ctx->req_cap, ctx->st));
+  EF_CUDA(ctx->d_scalars.reserve(16, ctx->st));
+  return EF_OK;
+}
+
+int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, const int32_t* rules, uint32_t n_rules,
+              const ef_price_params* pp, int insert_visited) {
+  EF_REQUIRE(!ctx->dirty, "tables not committed (call ef_tables_commit)");
+  EF_REQUIRE(ctx->vis_mask, "visited set not initialised");
+  EF_REQUIRE(n_rules <= 8, "at most 8 rules");
+  cudaSetDevice(ctx->dev);
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    int rc = ensure_step_buffers(ctx, std::max<uint32_t>(n_parents, 1));
+    if (rc) return rc;
+    const Geo& g = ctx->geo;
+    if ((rc = stage_addrs(ctx, ctx->d_parent_addr, parent_slots, n_parents))) return rc;
+    EF_CUDA(cudaMemsetAsync(ctx->d_scalars.p, 0, 16 * 4, ctx->st));
+    StepArgs A{};
+    A.g = g;
+    A.T = make_tables(ctx);
+    A.parent_addr = ctx->d_parent_addr.p;
+    A.n_parents = n_parents;
+    A.pscratch = ctx->d_pscratch.p;
+    A.pstride = 4ull * g.cap_nodes + 1 + g.cap_refs;
+    for (uint32_t i = 0; i < n_rules; ++i) A.rules[i] = rules[i];
+    A.n_rules = (int32_t)n_rules;
+    A.sites = ctx->d_sites.p;
+    A.site_cap = ctx->site_cap;
+    A.site_count = ctx->d_site_count.p;
+    A.cand_off = ctx->d_cand_off.p;
+    A.total = ctx->d_scalars.p + 0;
+    A.err = ctx->d_scalars.p + 1;
+    A.n_req_sig = ctx->d_scalars.p + 2;
+    A.n_req_dv = ctx->d_scalars.p + 3;
+    A.cand_base = ctx->d_cand.p;
+    A.cand_cap = ctx->cand_cap;
+    A.cand_srcpos = ctx->d_srcpos.p;
+    A.cand_seed = ctx->d_seed.p;
+    A.res = ctx->d_res.p;
+    A.req_sig = ctx->d_req_sig.p;
+    A.req_sig_cap = ctx->req_cap;
+    A.req_dv = ctx->d_req_dv.p;
+    A.req_dv_cap = ctx->req_cap;
+
+    cudaEventRecord(ctx->ev[0], ctx->st);
+    if (n_parents) {
+      k_match<kMatchThreads><<<std::min<uint32_t>(n_parents, ctx->n_sm * 8), kMatchThreads, 0, ctx->st>>>(A);
+      EF_CUDA(cudaGetLastError());
+    }
+    k_offsets<1024><<<1, 1024, 0, ctx->st>>>(A);
+    EF_CUDA(cudaGetLastError());
+    cudaEventRecord(ctx->ev[1], ctx->st);
+    const uint32_t grid_c = std::min<uint32_t>(ctx->cand_cap, ctx->n_sm * 8);
+    k_materialise<kMatThreads><<<grid_c, kMatThreads, 0, ctx->st>>>(A);
+    EF_CUDA(cudaGetLastError());
+    cudaEventRecord(ctx->ev[2], ctx->st);
+
+    HashArgs H{};
+    H.g = g;
+    H.T = A.T;
+    H.cand_base = ctx->d_cand.p;
+    H.total = A.total;
+    H.parent_addr = A.parent_addr;
+    H.srcpos = A.cand_srcpos;
+    H.seed = A.cand_seed;
+    H.res = A.res;
+    H.incremental = 1;
+    H.smem_nodes = hash_smem_nodes(ctx);
+    H.err = A.err;
+    size_t sm = hash_smem_bytes(H.smem_nodes);
+    if ((rc = ensure_hash_smem(ctx, sm))) return rc;
+    k_hash<kHashThreads><<<std::min<uint32_t>(ctx->cand_cap, ctx->n_sm * 8), kHashThreads, sm, ctx->st>>>(H);
+    EF_CUDA(cudaGetLastError());
+    cudaEventRecord(ctx->ev[3], ctx->st);
+
+    const uint32_t tcap = pow2_at_least(2ull * ctx->cand_cap);
+    EF_CUDA(cudaMemsetAsync(ctx->d_step_key.p, 0, (size_t)tcap * 8, ctx->st));
+    EF_CUDA(cudaMemsetAsync(ctx->d_step_seq.p, 0xff, (size_t)tcap * 4, ctx->st));
+    DedupArgs D{};
+    D.res = A.res;
+    D.total = A.total;
+    D.step_key = ctx->d_step_key.p;
+    D.step_seq = ctx->d_step_seq.p;
+    D.step_mask = tcap - 1;
+    D.vis_key = ctx->d_vis.p;
+    D.vis_mask = ctx->vis_mask;
+    D.vis_count = ctx->d_vis_count.p;
+    D.insert_visited = insert_visited;
+    D.node_cap = pp->node_cap;
+    const uint32_t grid_t = std::min<uint32_t>((ctx->cand_cap + 255) / 256, ctx->n_sm * 4);
+    k_dedup_claim<<<grid_t, 256, 0, ctx->st>>>(D);
+    k_dedup_resolve<<<grid_t, 256, 0, ctx->st>>>(D);
+    EF_CUDA(cudaGetLastError());
+    cudaEventRecord(ctx->ev[4], ctx->st);
+
+    PriceArgs Pa{};
+    Pa.g = g;
+    Pa.T = A.T;
+    Pa.pp = *pp;
+    Pa.total = A.total;
+    Pa.cand_base = ctx->d_cand.p;
+    Pa.res = A.res;
+    Pa.step_mode = 1;
+    k_price<<<std::min<uint32_t>((ctx->cand_cap + kPriceThreads - 1) / kPriceThreads, ctx->n_sm * 8), kPriceThreads, 0,
+              ctx->st>>>(Pa);
+    EF_CUDA(cudaGetLastError());
+    cudaEventRecord(ctx->ev[5], ctx->st);
+    EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
+    EF_CUDA(cudaStreamSynchronize(ctx->st));
+    const uint32_t total = ctx->h_scalars[0], err = ctx->h_scalars[1];
+    ctx->last_req_sig = ctx->h_scalars[2];
+    ctx->last_req_dv = ctx->h_scalars[3];
+    for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&ctx->last_ms[k], ctx->ev[k], ctx->ev[k + 1]);
+    if (err & 1u) {  // site buffer too small
+      ctx->site_cap *= 4;
+      continue;
+    }
+    if (err & 2u) {  // candidate arena too small
+      ctx->cand_cap = std::max<uint32_t>(total, ctx->cand_cap * 2);
+      ctx->d_step_key.release();
+      ctx->d_step_seq.release();
+      continue;
+    }
+    EF_REQUIRE(!(err & 4u), "candidate exceeds record capacity (raise cap_nodes/cap_refs)");
+    EF_REQUIRE(!(err & 8u), "graph too large for the hash kernel");
+    ctx->last_total = total;
+    if (ctx->last_req_sig || ctx->last_req_dv) return EF_NEED_RESOLVE;
+    if (insert_visited) {
+      k_visited_insert<<<grid_t, 256, 0, ctx->st>>>(D);
+      EF_CUDA(cudaGetLastError());
+      EF_CUDA(cudaStreamSynchronize(ctx->st));
+    }
+    return (int)total;
+  }
+  ctx->err = "ef_expand: buffers did not converge";
+  return EF_ERR_CAPACITY;
+}
+
+int ef_pending(ef_ctx* ctx, ef_sig_desc* sigs, uint32_t sig_cap, uint32_t* n_sigs, int32_t* derives, uint32_t derive_cap,
+               uint32_t* n_derives) {
+  uint32_t ns = std::min(ctx->last_req_sig, ctx->req_cap), nd = std::min(ctx->last_req_dv, ctx->req_cap);
+  if (n_sigs) *n_sigs = ns;
+  if (n_derives) *n_derives = nd;
+  if (sigs && ns) EF_CUDA(cudaMemcpyAsync(sigs, ctx->d_req_sig.p, std::min(ns, sig_cap) * sizeof(ef_sig_desc), cudaMemcpyDeviceToHost, ctx->st));
+  if (derives && nd) EF_CUDA(cudaMemcpyAsync(derives, ctx->d_req_dv.p, std::min(nd, derive_cap) * 16, cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+int ef_results(ef_ctx* ctx, ef_cand_result* out, uint32_t n) {
+  EF_REQUIRE(n <= ctx->last_total, "ef_results: more than the last step produced");
+  if (!n) return EF_OK;
+  EF_CUDA(cudaMemcpyAsync(out, ctx->d_res.p, n * sizeof(ef_cand_result), cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+int ef_keep(ef_ctx* ctx, const uint32_t* cand_idx, uint32_t n, const uint32_t* slots) {
+  if (!n) return EF_OK;
+  std::vector<unsigned long long> src(n), dst(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    EF_REQUIRE(cand_idx[i] < ctx->last_total, "ef_keep: bad candidate index");
+    EF_REQUIRE(slots[i] < ctx->n_slots, "ef_keep: bad slot");
+    src[i] = (unsigned long long)(ctx->d_cand.p + (uint64_t)cand_idx[i] * ctx->geo.bytes);
+    dst[i] = (unsigned long long)slot_addr(ctx, slots[i]);
+  }
+  int rc;
+  if ((rc = upload(ctx, ctx->d_addr_a, src)) || (rc = upload(ctx, ctx->d_addr_b, dst))) return rc;
+  k_copy_records<<<std::min<uint32_t>(n, ctx->n_sm * 4), 256, 0, ctx->st>>>(ctx->d_addr_a.p, ctx->d_addr_b.p, n, ctx->geo.bytes);
+  EF_CUDA(cudaGetLastError());
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+int ef_last_timing(ef_ctx* ctx, float* ms5) {
+  for (int k = 0; k < 5; ++k) ms5[k] = ctx->last_ms[k];
+  return EF_OK;
+}
+

@@ -1,0 +1,1318 @@
+// Kernels of one frontier step (match -> materialise -> hash -> dedup -> price) plus the
+// table kernels (weight-set derivation and digests) and record utilities.
+//
+// Work decomposition (B200: 148 SMs, persistent grid-stride blocks):
+//   k_match        one CTA per parent graph: consumer CSR + use counts, then every rule at
+//                  every node, emitted in the reference's site order with block-wide scans.
+//   k_materialise  one CTA per candidate: copies the parent record applying the rewrite;
+//                  positions/offsets of the child are closed-form in the <= 2 dropped nodes,
+//                  so the copy is a single coalesced pass (no per-node scan needed).
+//   k_hash         one CTA per candidate: Merkle node keys in dataflow order (threads wait on
+//                  their producers' flags in shared memory; clean nodes copy the parent key),
+//                  bitonic sort of the keys in shared memory, then the graph digest.
+//   k_dedup_*      open-addressing tables: first occurrence inside the step (atomicMin on the
+//                  candidate's sequence number) and membership in the visited set.
+//   k_price        one thread per surviving candidate: the reference's first-improvement sweep
+//                  (search.py:106-153) with CPython's Neumaier sum for the start totals; every
+//                  floating-point operation in the reference's order, no FMA contraction
+//                  (the library is compiled with --fmad=false).
+#pragma once
+#include <stdint.h>
+
+#include "ef_device.cuh"
+
+namespace ef {
+
+// ------------------------------------------------------------------------------------------
+// helpers
+// ------------------------------------------------------------------------------------------
+
+template <int BT>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total, uint32_t* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t s = lane < BT / 32 ? sh[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < BT / 32) sh[lane] = s;
+    if (lane == BT / 32 - 1) sh[BT / 32] = s;
+  }
+  __syncthreads();
+  uint32_t ex = x - v + (wid > 0 ? sh[wid - 1] : 0u);
+  *total = sh[BT / 32];
+  __syncthreads();
+  return ex;
+}
+
+__device__ __forceinline__ uint32_t lookup_sig(const Tables& T, const ef_sig_desc& d) {
+  uint64_t k = desc_key(d);
+  uint32_t m = T.sig_ht_mask;
+  if (m == 0) return kNone;
+  for (uint32_t s = (uint32_t)k & m;; s = (s + 1) & m) {
+    unsigned long long kk = T.sig_ht_key[s];
+    if (kk == 0ULL) return kNone;
+    if (kk == k) {
+      uint32_t id = T.sig_ht_val[s];
+      if (desc_eq(T.sig_desc[id], d)) return id;
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t lookup_derive(const Tables& T, int32_t op, uint32_t a, uint32_t b, int32_t s0) {
+  uint64_t k = derive_key(op, a, b, s0);
+  uint32_t m = T.dv_ht_mask;
+  if (m == 0) return kNone;
+  for (uint32_t s = (uint32_t)k & m;; s = (s + 1) & m) {
+    unsigned long long kk = T.dv_ht_key[s];
+    if (kk == 0ULL) return kNone;
+    if (kk == k) {
+      uint32_t id = T.dv_ht_val[s];
+      const int32_t* t = T.dv_tuple + 4 * id;
+      if (t[0] == op && (uint32_t)t[1] == a && (uint32_t)t[2] == b && t[3] == s0) return id;
+    }
+  }
+}
+
+__device__ __forceinline__ bool conv_compatible(const ef_sig_desc& a, const ef_sig_desc& b) {
+  // rules.py:197 _CONV_MERGE_KEYS = kernel, stride, padding, has_activation
+  return a.kh == b.kh && a.kw == b.kw && a.sh == b.sh && a.sw == b.sw && a.ph == b.ph && a.pw == b.pw &&
+         a.act == b.act;
+}
+
+__device__ __forceinline__ ef_sig_desc conv_variant(const ef_sig_desc& c, int act, int oc) {
+  ef_sig_desc d = c;
+  d.act = act;
+  d.oc = oc;
+  d.out[1] = oc;
+  return d;
+}
+
+__device__ __forceinline__ ef_sig_desc relu_of(const ef_sig_desc& conv) {
+  ef_sig_desc d;
+  int32_t* w = reinterpret_cast<int32_t*>(&d);
+  for (int i = 0; i < (int)(sizeof(ef_sig_desc) / 4); ++i) w[i] = 0;
+  d.kind = EF_K_RELU;
+  d.rank = 4;
+  for (int i = 0; i < 4; ++i) d.in[i] = d.out[i] = conv.out[i];
+  return d;
+}
+
+__device__ __forceinline__ ef_sig_desc split2_of(const ef_sig_desc& merged, int s0, int s1) {
+  ef_sig_desc d;
+  int32_t* w = reinterpret_cast<int32_t*>(&d);
+  for (int i = 0; i < (int)(sizeof(ef_sig_desc) / 4); ++i) w[i] = 0;
+  d.kind = EF_K_SPLIT;
+  d.rank = 4;
+  for (int i = 0; i < 4; ++i) d.in[i] = d.out[i] = merged.out[i];
+  d.out[1] = s0;
+  d.axis = 1;
+  d.nsizes = 2;
+  d.s0 = s0;
+  d.s1 = s1;
+  return d;
+}
+
+// ------------------------------------------------------------------------------------------
+// step arguments
+// ------------------------------------------------------------------------------------------
+
+struct StepArgs {
+  Geo g;
+  Tables T;
+  const unsigned long long* parent_addr;
+  uint32_t n_parents;
+  uint32_t* pscratch;  // per parent: u0[cap] u1[cap] coff[cap+1] ccur[cap] clist[cap_refs]
+  uint64_t pstride;    // words per parent
+  int32_t rules[8];
+  int32_t n_rules;
+  unsigned long long* sites;  // per parent site_cap packed sites
+  uint32_t site_cap;
+  uint32_t* site_count;  // per parent
+  uint32_t* cand_off;    // n_parents + 1
+  uint32_t* total;       // [0] = number of candidates
+  char* cand_base;       // scratch records
+  uint32_t cand_cap;
+  int32_t* cand_srcpos;  // cap_nodes per candidate
+  uint8_t* cand_seed;    // cap_nodes per candidate
+  ef_cand_result* res;
+  ef_sig_desc* req_sig;
+  uint32_t* n_req_sig;
+  uint32_t req_sig_cap;
+  int32_t* req_dv;
+  uint32_t* n_req_dv;
+  uint32_t req_dv_cap;
+  uint32_t* err;  // bit0 site overflow, bit1 candidate overflow, bit2 record capacity, bit3 hash capacity
+};
+
+__device__ __forceinline__ unsigned long long pack_site(uint32_t rule, uint32_t a, uint32_t b) {
+  return ((unsigned long long)rule << 56) | ((unsigned long long)(a & 0xfffffffu) << 28) | (b & 0xfffffffu);
+}
+
+// ------------------------------------------------------------------------------------------
+// k_match: one CTA per parent
+// ------------------------------------------------------------------------------------------
+
+template <int BT>
+__global__ void __launch_bounds__(BT) k_match(StepArgs A) {
+  __shared__ uint32_t sh_scan[BT / 32 + 1];
+  const Geo& G = A.g;
+  const Tables& T = A.T;
+  for (uint32_t pi = blockIdx.x; pi < A.n_parents; pi += gridDim.x) {
+    Rec R{reinterpret_cast<char*>(A.parent_addr[pi])};
+    const int n = R.h().n, n_out = R.h().n_out;
+    const uint32_t* sig = R.sig(G);
+    const uint32_t* inoff = R.inoff(G);
+    const uint32_t* nin = R.nin(G);
+    const uint32_t* refs = R.refs(G);
+    const uint32_t* outs = R.outs(G);
+    uint32_t* u0 = A.pscratch + (uint64_t)pi * A.pstride;
+    uint32_t* u1 = u0 + G.cap_nodes;
+    uint32_t* coff = u1 + G.cap_nodes;
+    uint32_t* ccur = coff + G.cap_nodes + 1;
+    uint32_t* clist = ccur + G.cap_nodes;
+
+    for (int i = threadIdx.x; i < n; i += BT) u0[i] = u1[i] = ccur[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += BT) {
+      for (uint32_t r = inoff[i]; r < inoff[i] + nin[i]; ++r) {
+        uint32_t p = refs[r] >> 8, port = refs[r] & 255u;
+        atomicAdd(&ccur[p], 1u);
+        if (port == 0) atomicAdd(&u0[p], 1u);
+        else if (port == 1) atomicAdd(&u1[p], 1u);
+      }
+    }
+    for (int o = threadIdx.x; o < n_out; o += BT) {
+      uint32_t p = outs[o] >> 8, port = outs[o] & 255u;
+      if (port == 0) atomicAdd(&u0[p], kOutMark);
+      else if (port == 1) atomicAdd(&u1[p], kOutMark);
+    }
+    __syncthreads();
+    // consumer CSR: exclusive scan of per-producer counts
+    uint32_t run = 0;
+    for (int c0 = 0; c0 < n; c0 += BT) {
+      int i = c0 + threadIdx.x;
+      uint32_t v = i < n ? ccur[i] : 0u, tot;
+      uint32_t ex = block_excl_scan<BT>(v, &tot, sh_scan);
+      if (i < n) coff[i] = run + ex;
+      run += tot;
+    }
+    if (threadIdx.x == 0) coff[n] = run;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += BT) ccur[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += BT) {
+      for (uint32_t r = inoff[i]; r < inoff[i] + nin[i]; ++r) {
+        uint32_t p = refs[r] >> 8;
+        clist[coff[p] + atomicAdd(&ccur[p], 1u)] = (uint32_t)i;
+      }
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < n; p += BT) {  // consumer lists in position (= id) order
+      uint32_t b = coff[p], e = coff[p + 1];
+      for (uint32_t x = b + 1; x < e; ++x) {
+        uint32_t v = clist[x];
+        uint32_t y = x;
+        while (y > b && clist[y - 1] > v) {
+          clist[y] = clist[y - 1];
+          --y;
+        }
+        clist[y] = v;
+      }
+    }
+    __syncthreads();
+
+    unsigned long long* out = A.sites + (uint64_t)pi * A.site_cap;
+    uint32_t base = 0;
+    bool overflow = false;
+    for (int ri = 0; ri < A.n_rules; ++ri) {
+      const int rule = A.rules[ri];
+      for (int c0 = 0; c0 < n; c0 += BT) {
+        const int i = c0 + threadIdx.x;
+        uint32_t cnt = 0, a = 0, b = 0;
+        if (i < n) {
+          const ef_sig_desc& di = T.sig_desc[sig[i]];
+          const int kind = di.kind;
+          if (rule == EF_R_FUSE_CONV_RELU || rule == EF_R_FUSE_CONV_BN || rule == EF_R_SPLIT_MERGED) {
+            // rules.py:147-161 / 303-318 / 245-261: producer conv, sole consumer of its edge
+            const int want = rule == EF_R_FUSE_CONV_RELU ? EF_K_RELU : rule == EF_R_FUSE_CONV_BN ? EF_K_BATCHNORM : EF_K_SPLIT;
+            if (kind == want && (rule != EF_R_SPLIT_MERGED || (di.axis == 1 && di.nsizes == 2))) {
+              uint32_t src = refs[inoff[i]];
+              uint32_t p = src >> 8, port = src & 255u;
+              const ef_sig_desc& dp = T.sig_desc[sig[p]];
+              uint32_t uses = port == 0 ? u0[p] : (port == 1 ? u1[p] : 2u);
+              if (dp.kind == EF_K_CONV2D && (rule == EF_R_SPLIT_MERGED || dp.act == 0) && uses == 1u) {
+                cnt = 1;
+                a = p;
+                b = (uint32_t)i;
+              }
+            }
+          } else if (rule == EF_R_SPLIT_CONV_ACT) {  // rules.py:173-178
+            if (kind == EF_K_CONV2D && di.act) {
+              cnt = 1;
+              a = (uint32_t)i;
+            }
+          } else if (rule == EF_R_FOLD_IDENTITY) {  // rules.py:288-290
+            if (kind == EF_K_IDENTITY) {
+              cnt = 1;
+              a = (uint32_t)i;
+            }
+          } else if (rule == EF_R_MERGE_CONVS) {  // rules.py:200-215: partners after i on the same edge
+            if (kind == EF_K_CONV2D) {
+              uint32_t src = refs[inoff[i]];
+              uint32_t p = src >> 8;
+              for (uint32_t x = coff[p]; x < coff[p + 1]; ++x) {
+                uint32_t c = clist[x];
+                if (c <= (uint32_t)i) continue;
+                const ef_sig_desc& dc = T.sig_desc[sig[c]];
+                if (dc.kind == EF_K_CONV2D && refs[inoff[c]] == src && conv_compatible(di, dc)) ++cnt;
+              }
+              a = (uint32_t)i;
+            }
+          }
+        }
+        uint32_t tot;
+        uint32_t ex = block_excl_scan<BT>(cnt, &tot, sh_scan);
+        if (cnt) {
+          uint32_t at = base + ex;
+          if (rule == EF_R_MERGE_CONVS) {
+            uint32_t src = refs[inoff[i]];
+            uint32_t p = src >> 8;
+            const ef_sig_desc& di = T.sig_desc[sig[i]];
+            for (uint32_t x = coff[p]; x < coff[p + 1]; ++x) {
+              uint32_t c = clist[x];
+              if (c <= (uint32_t)i) continue;
+              const ef_sig_desc& dc = T.sig_desc[sig[c]];
+              if (dc.kind == EF_K_CONV2D && refs[inoff[c]] == src && conv_compatible(di, dc)) {
+                if (at < A.site_cap) out[at] = pack_site(rule, (uint32_t)i, c);
+                ++at;
+              }
+            }
+          } else if (at < A.site_cap) {
+            out[at] = pack_site(rule, a, b);
+          }
+        }
+        base += tot;
+      }
+    }
+    if (base > A.site_cap) overflow = true;
+    if (threadIdx.x == 0) {
+      A.site_count[pi] = overflow ? A.site_cap : base;
+      if (overflow) atomicOr(A.err, 1u);
+    }
+    __syncthreads();
+  }
+}
+
+// exclusive scan of per-parent site counts -> candidate offsets (single CTA)
+template <int BT>
+__global__ void __launch_bounds__(BT) k_offsets(StepArgs A) {
+  __shared__ uint32_t sh_scan[BT / 32 + 1];
+  uint32_t run = 0;
+  for (uint32_t c0 = 0; c0 < A.n_parents; c0 += BT) {
+    uint32_t i = c0 + threadIdx.x;
+    uint32_t v = i < A.n_parents ? A.site_count[i] : 0u, tot;
+    uint32_t ex = block_excl_scan<BT>(v, &tot, sh_scan);
+    if (i < A.n_parents) A.cand_off[i] = run + ex;
+    run += tot;
+  }
+  if (threadIdx.x == 0) {
+    A.cand_off[A.n_parents] = run;
+    A.total[0] = run;
+    if (run > A.cand_cap) atomicOr(A.err, 2u);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// k_materialise: one CTA per candidate
+// ------------------------------------------------------------------------------------------
+
+struct Plan {
+  int drop[2];  // ascending, -1 = none
+  int mod;      // position rewritten in place
+  uint32_t mod_sig, mod_aux;
+  int n_new;  // new nodes before pruning (ids max+1, max+2)
+  int live[2];
+  uint32_t new_sig[2], new_aux[2], new_ref[2];  // new_ref in parent space: pos >= n means new node
+  int n_rm;
+  uint32_t rm_from[2], rm_to[2];
+  int topo_node, topo_mode;  // 1 = emit node then new nodes, 2 = emit new nodes in its place
+  int slot_of[3];            // topo slots of: drop[0], drop[1], topo_node
+  int n_live;
+  uint32_t touched[2];
+  int incomplete;
+  int drop_refs[2];  // ref ranges of the dropped nodes
+  uint32_t drop_inoff[2];
+};
+
+__device__ void plan_rewrite(const StepArgs& A, Plan& P, Rec R, int n, uint32_t rule, uint32_t a, uint32_t b,
+                             const uint32_t* u0, const uint32_t* u1) {
+  const Geo& G = A.g;
+  const Tables& T = A.T;
+  const uint32_t* sig = R.sig(G);
+  const uint32_t* aux = R.aux(G);
+  const uint32_t* refs = R.refs(G);
+  const uint32_t* inoff = R.inoff(G);
+  P.drop[0] = P.drop[1] = -1;
+  P.mod = -1;
+  P.n_new = 0;
+  P.live[0] = P.live[1] = 0;
+  P.n_rm = 0;
+  P.topo_node = -1;
+  P.topo_mode = 0;
+  P.touched[0] = P.touched[1] = kNone;
+  P.incomplete = 0;
+  auto need_sig = [&](const ef_sig_desc& d) -> uint32_t {
+    uint32_t id = lookup_sig(T, d);
+    if (id == kNone) {
+      P.incomplete = 1;
+      uint32_t k = atomicAdd(A.n_req_sig, 1u);
+      if (k < A.req_sig_cap) A.req_sig[k] = d;
+    }
+    return id;
+  };
+  auto need_dv = [&](int32_t op, uint32_t x, uint32_t y, int32_t s0) -> uint32_t {
+    uint32_t id = lookup_derive(T, op, x, y, s0);
+    if (id == kNone) {
+      P.incomplete = 1;
+      uint32_t k = atomicAdd(A.n_req_dv, 1u);
+      if (k < A.req_dv_cap) {
+        A.req_dv[4 * k] = op;
+        A.req_dv[4 * k + 1] = (int32_t)x;
+        A.req_dv[4 * k + 2] = (int32_t)y;
+        A.req_dv[4 * k + 3] = s0;
+      }
+    }
+    return id;
+  };
+  const ef_sig_desc& da = T.sig_desc[sig[a]];
+  switch (rule) {
+    case EF_R_FUSE_CONV_RELU:  // rules.py:164-170
+      P.drop[0] = (int)b;
+      P.mod = (int)a;
+      P.mod_sig = need_sig(conv_variant(da, 1, da.oc));
+      P.mod_aux = aux[a];
+      P.n_rm = 1;
+      P.rm_from[0] = b << 8;
+      P.rm_to[0] = a << 8;
+      P.touched[0] = P.mod_sig;
+      break;
+    case EF_R_SPLIT_CONV_ACT: {  // rules.py:181-190
+      P.mod = (int)a;
+      P.mod_sig = need_sig(conv_variant(da, 0, da.oc));
+      P.mod_aux = aux[a];
+      P.n_new = 1;
+      P.live[0] = 1;
+      P.new_sig[0] = need_sig(relu_of(da));
+      P.new_aux[0] = kEmptyWset;
+      P.new_ref[0] = a << 8;
+      P.n_rm = 1;
+      P.rm_from[0] = a << 8;
+      P.rm_to[0] = (uint32_t)n << 8;
+      P.topo_node = (int)a;
+      P.topo_mode = 1;
+      P.touched[0] = P.mod_sig;
+      P.touched[1] = P.new_sig[0];
+      break;
+    }
+    case EF_R_MERGE_CONVS: {  // rules.py:225-242
+      const ef_sig_desc& dbb = T.sig_desc[sig[b]];
+      ef_sig_desc dm = conv_variant(da, da.act, da.oc + dbb.oc);
+      P.drop[0] = (int)a;
+      P.drop[1] = (int)b;
+      P.n_new = 2;
+      P.live[0] = P.live[1] = 1;
+      P.new_sig[0] = need_sig(dm);
+      P.new_aux[0] = need_dv(EF_D_MERGE, aux[a], aux[b], 0);
+      P.new_ref[0] = refs[inoff[a]];
+      P.new_sig[1] = need_sig(split2_of(dm, da.oc, dbb.oc));
+      P.new_aux[1] = kEmptyWset;
+      P.new_ref[1] = (uint32_t)n << 8;
+      P.n_rm = 2;
+      P.rm_from[0] = a << 8;
+      P.rm_to[0] = ((uint32_t)(n + 1) << 8);
+      P.rm_from[1] = b << 8;
+      P.rm_to[1] = ((uint32_t)(n + 1) << 8) | 1u;
+      P.topo_mode = 2;  // topo_node chosen once the slots of a and b are known
+      P.touched[0] = P.new_sig[0];
+      P.touched[1] = P.new_sig[1];
+      break;
+    }
+    case EF_R_SPLIT_MERGED: {  // rules.py:264-281
+      const ef_sig_desc& ds = T.sig_desc[sig[b]];
+      P.drop[0] = (int)a;
+      P.drop[1] = (int)b;
+      P.n_new = 2;
+      // _rebuild prunes a half whose split port feeds nothing
+      P.live[0] = u0[b] != 0u;
+      P.live[1] = u1[b] != 0u;
+      if (P.live[0]) {
+        P.new_sig[0] = need_sig(conv_variant(da, da.act, ds.s0));
+        P.new_aux[0] = need_dv(EF_D_SLICE_LO, aux[a], 0, ds.s0);
+        P.touched[0] = P.new_sig[0];
+      }
+      if (P.live[1]) {
+        P.new_sig[1] = need_sig(conv_variant(da, da.act, ds.s1));
+        P.new_aux[1] = need_dv(EF_D_SLICE_HI, aux[a], 0, ds.s0);
+        P.touched[1] = P.new_sig[1];
+      }
+      P.new_ref[0] = P.new_ref[1] = refs[inoff[a]];
+      P.n_rm = 2;
+      P.rm_from[0] = b << 8;
+      P.rm_to[0] = (uint32_t)n << 8;
+      P.rm_from[1] = (b << 8) | 1u;
+      P.rm_to[1] = (uint32_t)(n + 1) << 8;
+      P.topo_node = (int)a;
+      P.topo_mode = 2;
+      break;
+    }
+    case EF_R_FOLD_IDENTITY:  // rules.py:293-296
+      P.drop[0] = (int)a;
+      P.n_rm = 1;
+      P.rm_from[0] = a << 8;
+      P.rm_to[0] = refs[inoff[a]];
+      break;
+    case EF_R_FUSE_CONV_BN:  // rules.py:321-331
+      P.drop[0] = (int)b;
+      P.mod = (int)a;
+      P.mod_sig = sig[a];
+      P.mod_aux = need_dv(EF_D_FOLD, aux[a], aux[b], 0);
+      P.n_rm = 1;
+      P.rm_from[0] = b << 8;
+      P.rm_to[0] = a << 8;
+      break;
+  }
+  if (P.drop[0] > P.drop[1] && P.drop[1] >= 0) {
+    int t = P.drop[0];
+    P.drop[0] = P.drop[1];
+    P.drop[1] = t;
+  }
+  if (P.drop[0] < 0 && P.drop[1] >= 0) {
+    P.drop[0] = P.drop[1];
+    P.drop[1] = -1;
+  }
+  P.n_live = P.live[0] + P.live[1];
+}
+
+template <int BT>
+__global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
+  __shared__ Plan P;
+  const Geo& G = A.g;
+  const uint32_t total = min(A.total[0], A.cand_cap);
+  for (uint32_t c = blockIdx.x; c < total; c += gridDim.x) {
+    // parent of candidate c: last pi with cand_off[pi] <= c
+    uint32_t lo = 0, hi = A.n_parents;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (A.cand_off[mid] <= c) lo = mid;
+      else hi = mid;
+    }
+    const uint32_t pi = lo;
+    const unsigned long long site = A.sites[(uint64_t)pi * A.site_cap + (c - A.cand_off[pi])];
+    const uint32_t rule = (uint32_t)(site >> 56), sa = (uint32_t)(site >> 28) & 0xfffffffu, sb = (uint32_t)site & 0xfffffffu;
+    Rec R{reinterpret_cast<char*>(A.parent_addr[pi])};
+    Rec C{A.cand_base + (uint64_t)c * G.bytes};
+    const int n = R.h().n, n_refs = R.h().n_refs, n_out = R.h().n_out;
+    const uint32_t* u0 = A.pscratch + (uint64_t)pi * A.pstride;
+    const uint32_t* u1 = u0 + G.cap_nodes;
+    const uint32_t* pnin = R.nin(G);
+    const uint32_t* pinoff = R.inoff(G);
+    if (threadIdx.x == 0) {
+      plan_rewrite(A, P, R, n, rule, sa, sb, u0, u1);
+      P.slot_of[0] = P.slot_of[1] = P.slot_of[2] = -1;
+      for (int k = 0; k < 2; ++k) {
+        P.drop_refs[k] = P.drop[k] >= 0 ? (int)pnin[P.drop[k]] : 0;
+        P.drop_inoff[k] = P.drop[k] >= 0 ? pinoff[P.drop[k]] : 0xffffffffu;
+      }
+    }
+    __syncthreads();
+    // topo slots of the special nodes
+    {
+      const uint32_t* ptopo = R.topo(G);
+      for (int s = threadIdx.x; s < n; s += BT) {
+        int v = (int)ptopo[s];
+        if (v == P.drop[0]) P.slot_of[0] = s;
+        if (v == P.drop[1]) P.slot_of[1] = s;
+        if (P.topo_mode == 2 && rule == EF_R_MERGE_CONVS) {
+          // merged conv + split go where the earlier of left/right was (both are dropped)
+        } else if (v == P.topo_node) {
+          P.slot_of[2] = s;
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && rule == EF_R_MERGE_CONVS) {
+      P.topo_node = P.slot_of[0] < P.slot_of[1] ? P.drop[0] : P.drop[1];
+      P.slot_of[2] = min(P.slot_of[0], P.slot_of[1]);
+    }
+    __syncthreads();
+    const int n_keep = n - (P.drop[0] >= 0) - (P.drop[1] >= 0);
+    const int n_child = n_keep + P.n_live;
+    const int drop_ref_tot = P.drop_refs[0] + P.drop_refs[1];
+    const int n_refs_child = n_refs - drop_ref_tot + P.n_live;
+    ef_cand_result* res = A.res + c;
+    const bool fits = n_child <= (int)G.cap_nodes && n_refs_child <= (int)G.cap_refs;
+    if (!fits) {
+      if (threadIdx.x == 0) {
+        atomicOr(A.err, 4u);
+        res->flags = EF_F_INCOMPLETE;
+      }
+      __syncthreads();
+      continue;
+    }
+    const int d0 = P.drop[0], d1 = P.drop[1];
+    // child position of a parent-space ref target
+    auto cpos = [&](uint32_t ppos) -> uint32_t {
+      if (ppos >= (uint32_t)n) {
+        uint32_t k = ppos - (uint32_t)n;
+        return (uint32_t)n_keep + (k == 1 ? (uint32_t)P.live[0] : 0u);
+      }
+      return ppos - (uint32_t)(d0 >= 0 && (uint32_t)d0 < ppos) - (uint32_t)(d1 >= 0 && (uint32_t)d1 < ppos);
+    };
+    auto remap = [&](uint32_t r) -> uint32_t {
+      for (int k = 0; k < P.n_rm; ++k)
+        if (r == P.rm_from[k]) return P.rm_to[k];
+      return r;
+    };
+    auto map_ref = [&](uint32_t r) -> uint32_t { return (cpos(r >> 8) << 8) | (r & 255u); };
+    int32_t* srcpos = A.cand_srcpos + (uint64_t)c * G.cap_nodes;
+    uint8_t* seed = A.cand_seed + (uint64_t)c * G.cap_nodes;
+    // nodes
+    {
+      const int32_t* pnid = R.nid(G);
+      const uint32_t* psig = R.sig(G);
+      const uint32_t* paux = R.aux(G);
+      int32_t* cnid = C.nid(G);
+      uint32_t* csig = C.sig(G);
+      uint32_t* caux = C.aux(G);
+      uint32_t* cnin = C.nin(G);
+      uint32_t* cinoff = C.inoff(G);
+      for (int i = threadIdx.x; i < n; i += BT) {
+        if (i == d0 || i == d1) continue;
+        uint32_t j = cpos((uint32_t)i);
+        cnid[j] = pnid[i];
+        csig[j] = i == P.mod ? P.mod_sig : psig[i];
+        caux[j] = i == P.mod ? P.mod_aux : paux[i];
+        cnin[j] = pnin[i];
+        uint32_t off = pinoff[i];
+        off -= (off > P.drop_inoff[0] ? (uint32_t)P.drop_refs[0] : 0u) + (off > P.drop_inoff[1] ? (uint32_t)P.drop_refs[1] : 0u);
+        cinoff[j] = off;
+        srcpos[j] = i;
+        seed[j] = i == P.mod ? 1 : 0;
+      }
+      if (threadIdx.x < 2) {
+        const int k = threadIdx.x;
+        if (k < P.n_new && P.live[k]) {
+          uint32_t j = (uint32_t)n_keep + (k == 1 ? (uint32_t)P.live[0] : 0u);
+          cnid[j] = R.nid(G)[n - 1] + 1 + k;
+          csig[j] = P.new_sig[k];
+          caux[j] = P.new_aux[k];
+          cnin[j] = 1;
+          cinoff[j] = (uint32_t)(n_refs - drop_ref_tot) + (j - (uint32_t)n_keep);
+          srcpos[j] = -1;
+          seed[j] = 1;
+        }
+      }
+      if (threadIdx.x == 0) cinoff[n_child] = (uint32_t)n_refs_child;
+    }
+    __syncthreads();
+    // refs of kept nodes (contiguous in the parent; dropped ranges removed)
+    {
+      const uint32_t* prefs = R.refs(G);
+      uint32_t* crefs = C.refs(G);
+      for (int r = threadIdx.x; r < n_refs; r += BT) {
+        uint32_t ru = (uint32_t)r;
+        bool in0 = P.drop[0] >= 0 && ru >= P.drop_inoff[0] && ru < P.drop_inoff[0] + (uint32_t)P.drop_refs[0];
+        bool in1 = P.drop[1] >= 0 && ru >= P.drop_inoff[1] && ru < P.drop_inoff[1] + (uint32_t)P.drop_refs[1];
+        if (in0 || in1) continue;
+        uint32_t dst = ru - (ru > P.drop_inoff[0] ? (uint32_t)P.drop_refs[0] : 0u) - (ru > P.drop_inoff[1] ? (uint32_t)P.drop_refs[1] : 0u);
+        uint32_t v = prefs[r];
+        uint32_t w = remap(v);
+        crefs[dst] = map_ref(w);
+        if (w != v) {
+          // the owner of this ref now consumes a different producer: its key changes
+          uint32_t lo2 = 0, hi2 = (uint32_t)n;
+          while (hi2 - lo2 > 1) {
+            uint32_t mid = (lo2 + hi2) >> 1;
+            if (pinoff[mid] <= ru) lo2 = mid;
+            else hi2 = mid;
+          }
+          // several nodes may share an offset when some have no inputs: take the last with nin > 0
+          while (lo2 > 0 && pnin[lo2] == 0) --lo2;
+          seed[cpos(lo2)] = 1;
+        }
+      }
+      if (threadIdx.x < 2) {
+        const int k = threadIdx.x;
+        if (k < P.n_new && P.live[k]) {
+          uint32_t j = (uint32_t)n_keep + (k == 1 ? (uint32_t)P.live[0] : 0u);
+          crefs[(uint32_t)(n_refs - drop_ref_tot) + (j - (uint32_t)n_keep)] = map_ref(P.new_ref[k]);
+        }
+      }
+      const uint32_t* pouts = R.outs(G);
+      uint32_t* couts = C.outs(G);
+      for (int o = threadIdx.x; o < n_out; o += BT) couts[o] = map_ref(remap(pouts[o]));
+    }
+    // topological order: parent order with dropped slots removed and new nodes inserted
+    {
+      const uint32_t* ptopo = R.topo(G);
+      uint32_t* ctopo = C.topo(G);
+      // emission count of the <= 3 special slots
+      int sp_slot[3], sp_emit[3];
+      for (int k = 0; k < 3; ++k) {
+        sp_slot[k] = P.slot_of[k];
+        sp_emit[k] = 1;
+      }
+      // drops emit nothing unless they are the insertion point
+      for (int k = 0; k < 2; ++k)
+        if (sp_slot[k] >= 0) sp_emit[k] = 0;
+      if (P.topo_mode == 1) sp_emit[2] = 1 + P.n_live;
+      if (P.topo_mode == 2) sp_emit[2] = P.n_live;
+      // a drop that is also the insertion slot must be counted once
+      for (int k = 0; k < 2; ++k)
+        if (sp_slot[k] >= 0 && sp_slot[k] == sp_slot[2]) sp_slot[k] = -1;
+      for (int s = threadIdx.x; s < n; s += BT) {
+        int shift = 0;
+        bool special = false;
+        int emit = 1;
+        for (int k = 0; k < 3; ++k) {
+          if (sp_slot[k] < 0) continue;
+          if (sp_slot[k] < s) shift += sp_emit[k] - 1;
+          if (sp_slot[k] == s) {
+            special = true;
+            emit = sp_emit[k];
+          }
+        }
+        uint32_t at = (uint32_t)(s + shift);
+        uint32_t v = ptopo[s];
+        if (!special) {
+          ctopo[at] = cpos(v);
+        } else if (s == sp_slot[2]) {
+          int e = 0;
+          if (P.topo_mode == 1) ctopo[at + e++] = cpos(v);
+          for (int k = 0; k < P.n_new; ++k)
+            if (P.live[k]) ctopo[at + e++] = (uint32_t)n_keep + (k == 1 ? (uint32_t)P.live[0] : 0u);
+        }
+        (void)emit;
+      }
+    }
+    if (threadIdx.x == 0) {
+      ef_rec_header& H = C.h();
+      H.n = n_child;
+      H.n_refs = n_refs_child;
+      H.n_out = n_out;
+      H.n_compute = R.h().n_compute - (n - n_keep) + P.n_live;
+      res->flags = P.incomplete ? EF_F_INCOMPLETE : 0u;
+      res->parent = pi;
+      res->rule = rule;
+      res->site_a = sa;
+      res->site_b = sb;
+      res->touched_sig[0] = P.touched[0];
+      res->touched_sig[1] = P.touched[1];
+      res->n_compute = H.n_compute;
+      res->hash = 0;
+      res->cost = res->time_ms = res->energy = 0.0;
+      res->evals = 0;
+      res->sweeps = 0;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// k_hash: canonical hash (graph.py:520-549), one CTA per record
+// ------------------------------------------------------------------------------------------
+
+struct HashArgs {
+  Geo g;
+  Tables T;
+  uint32_t n;                        // records
+  const unsigned long long* rec;     // record addresses (or null: cand_base + c * bytes)
+  char* cand_base;
+  const uint32_t* total;             // optional device count (overrides n)
+  const unsigned long long* parent;  // per candidate parent record (incremental mode)
+  const StepArgs* step;              // unused on device; keeps the signature uniform
+  const uint32_t* cand_parent;       // parent index per candidate via res->parent
+  const unsigned long long* parent_addr;
+  const int32_t* srcpos;
+  const uint8_t* seed;
+  ef_cand_result* res;
+  uint64_t* hash_out;                // full mode output
+  int incremental;
+  uint32_t smem_nodes;               // flags + keys capacity in shared memory
+  uint32_t* err;
+};
+
+__device__ __forceinline__ void append_sig_text(B2b& s, const Tables& T, uint32_t sig) {
+  const uint32_t off = T.sig_text_off[sig], len = T.sig_text_len[sig];
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(T.sig_text + off);  // 8-byte aligned, zero padded
+  uint32_t full = len >> 3;
+  for (uint32_t i = 0; i < full; ++i) s.word_le(w[i]);
+  const uint8_t* tail = T.sig_text + off + 8 * full;
+  for (uint32_t i = 0; i < (len & 7u); ++i) s.byte(tail[i]);
+}
+
+template <int BT>
+__global__ void __launch_bounds__(BT) k_hash(HashArgs A) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const Geo& G = A.g;
+  const Tables& T = A.T;
+  const uint32_t total = A.total ? A.total[0] : A.n;
+  volatile uint8_t* fl = smem;                                            // [smem_nodes]
+  uint64_t* skeys = reinterpret_cast<uint64_t*>(smem + ((A.smem_nodes + 15u) & ~15u));  // [2*smem_nodes]
+  for (uint32_t c = blockIdx.x; c < total; c += gridDim.x) {
+    ef_cand_result* res = A.res ? A.res + c : nullptr;
+    if (res && (res->flags & EF_F_INCOMPLETE)) continue;
+    Rec R{A.rec ? reinterpret_cast<char*>(A.rec[c]) : A.cand_base + (uint64_t)c * G.bytes};
+    const int n = R.h().n;
+    if ((uint32_t)n > A.smem_nodes) {
+      if (threadIdx.x == 0) {
+        atomicOr(A.err, 8u);
+        if (res) res->flags |= EF_F_INCOMPLETE;
+      }
+      continue;
+    }
+    Rec P{nullptr};
+    if (A.incremental) P.p = reinterpret_cast<char*>(A.parent_addr[res->parent]);
+    const int32_t* srcpos = A.incremental ? A.srcpos + (uint64_t)c * G.cap_nodes : nullptr;
+    const uint8_t* seed = A.incremental ? A.seed + (uint64_t)c * G.cap_nodes : nullptr;
+    const uint32_t* topo = R.topo(G);
+    const uint32_t* sig = R.sig(G);
+    const uint32_t* aux = R.aux(G);
+    const uint32_t* nin = R.nin(G);
+    const uint32_t* inoff = R.inoff(G);
+    const uint32_t* refs = R.refs(G);
+    for (int i = threadIdx.x; i < n; i += BT) fl[i] = 0;
+    __syncthreads();
+    for (int s = threadIdx.x; s < n; s += BT) {
+      const uint32_t v = topo[s];
+      bool dirty = !A.incremental || seed[v];
+      const uint32_t r0 = inoff[v], r1 = r0 + nin[v];
+      for (uint32_t r = r0; r < r1; ++r) {
+        uint32_t p = refs[r] >> 8;
+        uint8_t f;
+        while (!((f = fl[p]) & 1u)) __nanosleep(32);
+        dirty |= (f & 2u) != 0;
+      }
+      __threadfence_block();
+      uint64_t k0, k1;
+      if (!dirty) {
+        const uint64_t* pk = P.keys(G) + 2 * (uint32_t)srcpos[v];
+        k0 = pk[0];
+        k1 = pk[1];
+      } else {
+        B2b st;
+        st.init(16);
+        const uint32_t sg = sig[v];
+        append_sig_text(st, T, sg);
+        const bool is_input = T.sig_desc[sg].kind == EF_K_INPUT;
+        uint32_t wsid = aux[v];
+        if (is_input) {
+          const uint8_t* nm = T.names + T.name_off[aux[v]];
+          st.bytes(nm, T.name_len[aux[v]]);
+          wsid = kEmptyWset;
+        }
+        st.word_le(T.ws_digest[2 * wsid]);
+        st.word_le(T.ws_digest[2 * wsid + 1]);
+        for (uint32_t r = r0; r < r1; ++r) {
+          uint32_t p = refs[r] >> 8, port = refs[r] & 255u;
+          st.word_le(skeys[2 * p]);
+          st.word_le(skeys[2 * p + 1]);
+          st.u16_be(port);
+        }
+        st.final();
+        k0 = st.h[0];
+        k1 = st.h[1];
+      }
+      skeys[2 * v] = k0;
+      skeys[2 * v + 1] = k1;
+      __threadfence_block();
+      fl[v] = (uint8_t)(1u | (dirty ? 2u : 0u));
+    }
+    __syncthreads();
+    // write keys back to the record (coalesced)
+    {
+      uint64_t* rk = R.keys(G);
+      for (int i = threadIdx.x; i < 2 * n; i += BT) rk[i] = skeys[i];
+    }
+    __syncthreads();
+    // sort keys as big-endian 128-bit values (bytes order of sorted(keys.values()))
+    int m = 1;
+    while (m < n) m <<= 1;
+    for (int i = threadIdx.x; i < m; i += BT) {
+      if (i < n) {
+        uint64_t a = B2b::bswap64(skeys[2 * i]), b = B2b::bswap64(skeys[2 * i + 1]);
+        skeys[2 * i] = a;
+        skeys[2 * i + 1] = b;
+      } else {
+        skeys[2 * i] = ~0ULL;
+        skeys[2 * i + 1] = ~0ULL;
+      }
+    }
+    __syncthreads();
+    for (int k = 2; k <= m; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < m; i += BT) {
+          int ixj = i ^ j;
+          if (ixj > i) {
+            uint64_t ah = skeys[2 * i], al = skeys[2 * i + 1], bh = skeys[2 * ixj], bl = skeys[2 * ixj + 1];
+            bool gt = ah > bh || (ah == bh && al > bl);
+            bool up = (i & k) == 0;
+            if (gt == up) {
+              skeys[2 * i] = bh;
+              skeys[2 * i + 1] = bl;
+              skeys[2 * ixj] = ah;
+              skeys[2 * ixj + 1] = al;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (threadIdx.x == 0) {
+      B2b st;
+      st.init(8);
+      st.bytes(T.input_text, T.input_text_len);
+      const uint32_t* outs = R.outs(G);
+      const uint64_t* rk = R.keys(G);
+      for (int o = 0; o < R.h().n_out; ++o) {
+        uint32_t p = outs[o] >> 8, port = outs[o] & 255u;
+        st.word_le(rk[2 * p]);
+        st.word_le(rk[2 * p + 1]);
+        st.u16_be(port);
+      }
+      for (int i = 0; i < n; ++i) {
+        st.word_le(B2b::bswap64(skeys[2 * i]));
+        st.word_le(B2b::bswap64(skeys[2 * i + 1]));
+      }
+      st.final();
+      uint64_t h = B2b::bswap64(st.h[0]);
+      if (res) res->hash = h;
+      if (A.hash_out) A.hash_out[c] = h;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// dedup: first occurrence in the step, then membership in the visited set
+// ------------------------------------------------------------------------------------------
+
+struct DedupArgs {
+  ef_cand_result* res;
+  const uint32_t* total;
+  unsigned long long* step_key;
+  uint32_t* step_seq;
+  uint32_t step_mask;
+  unsigned long long* vis_key;
+  uint32_t vis_mask;
+  unsigned long long* vis_count;
+  int insert_visited;
+  int node_cap;
+};
+
+__global__ void k_dedup_claim(DedupArgs A) {
+  const uint32_t total = A.total[0];
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
+    if (A.res[c].flags & EF_F_INCOMPLETE) continue;
+    unsigned long long h = A.res[c].hash;
+    unsigned long long key = h ? h : 0x8000000000000000ULL;
+    for (uint32_t s = (uint32_t)mix64(h) & A.step_mask;; s = (s + 1) & A.step_mask) {
+      unsigned long long prev = atomicCAS(&A.step_key[s], 0ULL, key);
+      if (prev == 0ULL || prev == key) {
+        atomicMin(&A.step_seq[s], c);
+        break;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ bool vis_contains(const unsigned long long* keys, uint32_t mask, unsigned long long key,
+                                             uint64_t h) {
+  for (uint32_t s = (uint32_t)mix64(h) & mask;; s = (s + 1) & mask) {
+    unsigned long long k = keys[s];
+    if (k == key) return true;
+    if (k == 0ULL) return false;
+  }
+}
+
+__global__ void k_dedup_resolve(DedupArgs A) {
+  const uint32_t total = A.total[0];
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
+    ef_cand_result& r = A.res[c];
+    if (r.flags & EF_F_INCOMPLETE) continue;
+    unsigned long long h = r.hash;
+    unsigned long long key = h ? h : 0x8000000000000000ULL;
+    uint32_t first_seq = 0xffffffffu;
+    for (uint32_t s = (uint32_t)mix64(h) & A.step_mask;; s = (s + 1) & A.step_mask) {
+      if (A.step_key[s] == key) {
+        first_seq = A.step_seq[s];
+        break;
+      }
+    }
+    uint32_t f = r.flags;
+    if (first_seq == c) f |= EF_F_FIRST;
+    bool seen = vis_contains(A.vis_key, A.vis_mask, key, h);
+    if (seen) f |= EF_F_VISITED;
+    if (r.n_compute > A.node_cap) f |= EF_F_CAPPED;
+    r.flags = f;
+  }
+}
+
+__global__ void k_visited_insert(DedupArgs A) {
+  const uint32_t total = A.total[0];
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
+    const ef_cand_result& r = A.res[c];
+    if ((r.flags & (EF_F_INCOMPLETE | EF_F_FIRST | EF_F_VISITED)) != EF_F_FIRST) continue;
+    unsigned long long h = r.hash;
+    unsigned long long key = h ? h : 0x8000000000000000ULL;
+    for (uint32_t s = (uint32_t)mix64(h) & A.vis_mask;; s = (s + 1) & A.vis_mask) {
+      unsigned long long prev = atomicCAS(&A.vis_key[s], 0ULL, key);
+      if (prev == 0ULL) {
+        atomicAdd(A.vis_count, 1ULL);
+        break;
+      }
+      if (prev == key) break;
+    }
+  }
+}
+
+__global__ void k_visited_put(unsigned long long* keys, uint32_t mask, unsigned long long* count, const uint64_t* hs,
+                              uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint64_t h = hs[i];
+    unsigned long long key = h ? h : 0x8000000000000000ULL;
+    for (uint32_t s = (uint32_t)mix64(h) & mask;; s = (s + 1) & mask) {
+      unsigned long long prev = atomicCAS(&keys[s], 0ULL, key);
+      if (prev == 0ULL) {
+        atomicAdd(count, 1ULL);
+        break;
+      }
+      if (prev == key) break;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// k_price: the inner search of search.py:106-153 (or the default assignment, 196-202)
+// ------------------------------------------------------------------------------------------
+
+struct PriceArgs {
+  Geo g;
+  Tables T;
+  ef_price_params pp;
+  const uint32_t* total;
+  uint32_t n;
+  const unsigned long long* rec;  // or null: cand_base
+  char* cand_base;
+  ef_cand_result* res;
+  int step_mode;  // 1: only first & !visited & !capped & complete candidates
+};
+
+// cost.py:234-254 in the reference's operation order
+__device__ __forceinline__ double from_totals(const ef_price_params& f, double time_ms, double energy) {
+  const double t = time_ms / f.t_ref;
+  const double e = energy / f.e_ref;
+  switch (f.kind) {
+    case EF_C_TIME: return time_ms;
+    case EF_C_ENERGY: return energy;
+    case EF_C_POWER: return time_ms != 0.0 ? energy / time_ms : time_ms * 0.0;
+    case EF_C_LINEAR: return f.w * e + (1.0 - f.w) * t;
+    case EF_C_PRODUCT: return pow(e, f.w) * pow(t, 1.0 - f.w);
+    default: {
+      const double p = (time_ms != 0.0 ? energy / time_ms : time_ms * 0.0) / f.p_ref;
+      return f.ct * t + f.ce * e + f.cp * p;
+    }
+  }
+}
+
+// CPython 3.12 builtin sum() over floats: Neumaier-compensated, start value int 0
+struct NeumaierSum {
+  double f, c;
+  bool any;
+  __device__ void init() {
+    f = 0.0;
+    c = 0.0;
+    any = false;
+  }
+  __device__ void add(double x) {
+    if (!any) {
+      f = 0.0 + x;
+      any = true;
+      return;
+    }
+    double t = f + x;
+    if (fabs(f) >= fabs(x)) c += (f - t) + x;
+    else c += (x - t) + f;
+    f = t;
+  }
+  __device__ double result() const {
+    double r = f;
+    if (c != 0.0 && isfinite(c)) r += c;
+    return r;
+  }
+};
+
+constexpr int kMaxRadius = 16;
+
+__global__ void k_price(PriceArgs A) {
+  const Geo& G = A.g;
+  const Tables& T = A.T;
+  const ef_price_params& F = A.pp;
+  const uint32_t total = A.total ? A.total[0] : A.n;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
+    ef_cand_result& res = A.res[c];
+    if (A.step_mode) {
+      if ((res.flags & (EF_F_INCOMPLETE | EF_F_FIRST | EF_F_VISITED | EF_F_CAPPED)) != EF_F_FIRST) continue;
+    }
+    Rec R{A.rec ? reinterpret_cast<char*>(A.rec[c]) : A.cand_base + (uint64_t)c * G.bytes};
+    const int n = R.h().n;
+    const uint32_t* sig = R.sig(G);
+    uint8_t* alg = R.alg(G);  // current row index per node during the sweep; alg id at the end
+    // start: lowest applicable algorithm (row 0) per compute node; Neumaier start totals
+    NeumaierSum st, se;
+    st.init();
+    se.init();
+    int ncomp = 0;
+    bool missing = false;
+    for (int i = 0; i < n; ++i) {
+      const uint32_t s = sig[i];
+      if (T.sig_desc[s].kind == EF_K_INPUT) continue;
+      ++ncomp;
+      if (T.row_n[s] == 0) {
+        missing = true;
+        break;
+      }
+      alg[i] = 0;
+      st.add(T.row_t[T.row_off[s]]);
+      se.add(T.row_e[T.row_off[s]]);
+    }
+    if (missing) {
+      res.flags |= EF_F_MISSING;
+      continue;
+    }
+    double t_tot = ncomp ? st.result() : 0.0;
+    double e_tot = ncomp ? se.result() : 0.0;
+    double cost = from_totals(F, t_tot, e_tot);
+    long long evals = 0;
+    int sweeps = 0;
+    if (A.pp.use_inner && ncomp > 0) {
+      const int radius = min(min(F.d, ncomp), kMaxRadius);
+      bool changed = true;
+      while (changed) {
+        changed = false;
+        ++sweeps;
+        // k = 1: every node, every alternative (ascending), first improvement
+        for (int i = 0; i < n; ++i) {
+          const uint32_t s = sig[i];
+          if (T.sig_desc[s].kind == EF_K_INPUT) continue;
+          const uint32_t nr = T.row_n[s];
+          if (nr < 2) continue;
+          const uint32_t ro = T.row_off[s];
+          const uint32_t start = alg[i];
+          for (uint32_t q = 0; q < nr; ++q) {
+            if (q == start) continue;
+            const uint32_t cur = alg[i];
+            double dt = 0.0, de = 0.0;
+            dt += T.row_t[ro + q] - T.row_t[ro + cur];
+            de += T.row_e[ro + q] - T.row_e[ro + cur];
+            const double cand = from_totals(F, t_tot + dt, e_tot + de);
+            ++evals;
+            if (cand < cost) {
+              alg[i] = (uint8_t)q;
+              t_tot += dt;
+              e_tot += de;
+              cost = cand;
+              changed = true;
+            }
+          }
+        }
+        // k >= 2: itertools.combinations(nids, k) x itertools.product(*alternatives)
+        for (int k = 2; k <= radius; ++k) {
+          int pos[kMaxRadius];
+          // first combination: the first k compute positions
+          int filled = 0;
+          for (int i = 0; i < n && filled < k; ++i)
+            if (T.sig_desc[sig[i]].kind != EF_K_INPUT) pos[filled++] = i;
+          while (true) {
+            uint32_t nalt[kMaxRadius], start[kMaxRadius], idx[kMaxRadius];
+            bool skip = false;
+            for (int j = 0; j < k; ++j) {
+              const uint32_t s = sig[pos[j]];
+              nalt[j] = T.row_n[s] - 1;
+              start[j] = alg[pos[j]];
+              idx[j] = 0;
+              if (nalt[j] == 0) skip = true;
+            }
+            if (!skip) {
+              while (true) {
+                double dt = 0.0, de = 0.0;
+                uint32_t choice[kMaxRadius];
+                for (int j = 0; j < k; ++j) {
+                  const uint32_t s = sig[pos[j]];
+                  const uint32_t ro = T.row_off[s];
+                  const uint32_t q = idx[j] < start[j] ? idx[j] : idx[j] + 1;
+                  choice[j] = q;
+                  const uint32_t cur = alg[pos[j]];
+                  dt += T.row_t[ro + q] - T.row_t[ro + cur];
+                  de += T.row_e[ro + q] - T.row_e[ro + cur];
+                }
+                const double cand = from_totals(F, t_tot + dt, e_tot + de);
+                ++evals;
+                if (cand < cost) {
+                  for (int j = 0; j < k; ++j) alg[pos[j]] = (uint8_t)choice[j];
+                  t_tot += dt;
+                  e_tot += de;
+                  cost = cand;
+                  changed = true;
+                }
+                // next product index: last position varies fastest
+                int j = k - 1;
+                while (j >= 0 && ++idx[j] == nalt[j]) idx[j--] = 0;
+                if (j < 0) break;
+              }
+            }
+            // next combination of compute positions (lexicographic)
+            int j = k - 1;
+            bool advanced = false;
+            while (j >= 0) {
+              // next compute position after pos[j] leaving room for the rest
+              int q = pos[j] + 1;
+              while (q < n && T.sig_desc[sig[q]].kind == EF_K_INPUT) ++q;
+              // count compute nodes from q on
+              int room = 0;
+              for (int x = q; x < n && room < k - j; ++x)
+                if (T.sig_desc[sig[x]].kind != EF_K_INPUT) ++room;
+              if (q < n && room >= k - j) {
+                pos[j] = q;
+                int f2 = j + 1;
+                for (int x = q + 1; x < n && f2 < k; ++x)
+                  if (T.sig_desc[sig[x]].kind != EF_K_INPUT) pos[f2++] = x;
+                advanced = true;
+                break;
+              }
+              --j;
+            }
+            if (!advanced) break;
+          }
+        }
+      }
+    }
+    // row index -> algorithm id
+    for (int i = 0; i < n; ++i) {
+      const uint32_t s = sig[i];
+      if (T.sig_desc[s].kind == EF_K_INPUT) continue;
+      alg[i] = (uint8_t)T.row_alg[T.row_off[s] + alg[i]];
+    }
+    res.cost = cost;
+    res.time_ms = t_tot;
+    res.energy = e_tot;
+    res.evals = A.pp.use_inner ? evals : 1;
+    res.sweeps = sweeps;
+    res.flags |= EF_F_PRICED;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// record copy (keep candidates) and weight-set kernels
+// ------------------------------------------------------------------------------------------
+
+__global__ void k_copy_records(const unsigned long long* src, const unsigned long long* dst, uint32_t n, uint32_t bytes) {
+  const uint32_t words = bytes / 16;
+  for (uint32_t r = blockIdx.x; r < n; r += gridDim.x) {
+    const uint4* s = reinterpret_cast<const uint4*>(src[r]);
+    uint4* d = reinterpret_cast<uint4*>(dst[r]);
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) d[i] = s[i];
+  }
+}
+
+// one weight set to digest: [hdr0 bytes][t0 float64s][hdr1 bytes][t1 float64s]
+struct DigestJob {
+  const uint8_t* hdr0;
+  uint32_t hlen0;
+  const double* t0;
+  uint64_t n0;
+  const uint8_t* hdr1;
+  uint32_t hlen1;
+  const double* t1;
+  uint64_t n1;
+  uint64_t* out;  // 2 words
+};
+
+__global__ void k_digest(const DigestJob* jobs, uint32_t n) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const DigestJob J = jobs[j];
+    B2b st;
+    st.init(16);
+    st.bytes(J.hdr0, J.hlen0);
+    const unsigned long long* w0 = reinterpret_cast<const unsigned long long*>(J.t0);
+    for (uint64_t i = 0; i < J.n0; ++i) st.word_le(w0[i]);
+    st.bytes(J.hdr1, J.hlen1);
+    const unsigned long long* w1 = reinterpret_cast<const unsigned long long*>(J.t1);
+    for (uint64_t i = 0; i < J.n1; ++i) st.word_le(w1[i]);
+    st.final();
+    J.out[0] = st.h[0];
+    J.out[1] = st.h[1];
+  }
+}
+
+// derived tensors (rules.py:231-232, 272-276, 326-327); every op one IEEE rounding, no FMA
+struct DeriveJob {
+  int32_t op;
+  const double* wa;  // left / source conv weight
+  const double* ba;  // its bias (null: zeros)
+  const double* wb;  // MERGE: right weight; FOLD: bn scale
+  const double* bb;  // MERGE: right bias (null: zeros); FOLD: bn shift
+  uint64_t oc_a, oc_b, inner;  // out channels (a, b) and elements per out channel
+  int32_t s0;
+  double* w_out;
+  double* b_out;
+  uint64_t w_n, b_n;
+};
+
+__global__ void k_derive(const DeriveJob* jobs, uint32_t n) {
+  for (uint32_t j = 0; j < n; ++j) {
+    const DeriveJob J = jobs[j];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (uint64_t i = t0; i < J.w_n; i += stride) {
+      double v;
+      if (J.op == EF_D_MERGE) {
+        const uint64_t na = J.oc_a * J.inner;
+        v = i < na ? J.wa[i] : J.wb[i - na];
+      } else if (J.op == EF_D_SLICE_LO) {
+        v = J.wa[i];
+      } else if (J.op == EF_D_SLICE_HI) {
+        v = J.wa[(uint64_t)J.s0 * J.inner + i];
+      } else {  // FOLD: weight * scale[:, None, None, None]
+        v = __dmul_rn(J.wa[i], J.wb[i / J.inner]);
+      }
+      J.w_out[i] = v;
+    }
+    for (uint64_t i = t0; i < J.b_n; i += stride) {
+      double v;
+      if (J.op == EF_D_MERGE) {
+        v = i < J.oc_a ? (J.ba ? J.ba[i] : 0.0) : (J.bb ? J.bb[i - J.oc_a] : 0.0);
+      } else if (J.op == EF_D_SLICE_LO) {
+        v = J.ba ? J.ba[i] : 0.0;
+      } else if (J.op == EF_D_SLICE_HI) {
+        v = J.ba ? J.ba[(uint64_t)J.s0 + i] : 0.0;
+      } else {  // FOLD: bias * scale + shift
+        v = __dadd_rn(__dmul_rn(J.ba ? J.ba[i] : 0.0, J.wb[i]), J.bb[i]);
+      }
+      J.b_out[i] = v;
+    }
+  }
+}
+
+}  // namespace ef

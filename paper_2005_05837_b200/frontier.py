@@ -1,0 +1,344 @@
+"""The two-level search with its hot path on the B200 (reference: pkg/src/enerflow/search.py).
+
+`outer_search` keeps the reference's semantics exactly (search.py:211-272):
+a best-first heap keyed by (cost, canonical hash), a visited set, the alpha
+enqueue rule against the best cost *before* each candidate, stale entries
+pruned at pop, and the same statistics.  What moved to the GPU is the
+expansion of a popped graph — every rule at every site, materialisation,
+canonical hashing, in-step and visited deduplication, and the inner search on
+every survivor — one `ef_expand` call per expansion.  The host loop below only
+replays the reference's per-candidate bookkeeping on the returned results
+(flags, costs, hashes), in the reference's order, so the explored-hash
+sequence, the optimised graph, the assignment and every statistic match the
+reference bit for bit (tests/test_gpu_parity.py).
+
+Graphs never come back to the host during the search: the frontier lives in
+HBM as records; only the final best graph is decoded.
+"""
+
+from __future__ import annotations
+
+import heapq
+import itertools
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .costmodel import Assignment, CostDatabase, CostFunction, node_cost_table, normalization_refs
+from .device import DeviceSession, price_params
+from .errors import InfeasibleConstraint, MissingEntry, SpaceTooLarge
+from .ir import Graph
+from .profiler import ProfilerSpec, ensure_profiled, profile_signature, record_line
+from .rewrite import SubstitutionRule, scratch_graph
+
+
+@dataclass
+class SearchConfig:
+    alpha: float = 1.05
+    d: int = 1
+    max_queue: int = 100_000
+    max_graph_nodes: int | None = None
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.alpha < 1.0:
+            raise ValueError(f"alpha must be >= 1, got {self.alpha}")
+        if self.d < 1:
+            raise ValueError(f"d must be >= 1, got {self.d}")
+        if self.max_queue < 1:
+            raise ValueError("max_queue must be >= 1")
+        if self.max_graph_nodes is not None and self.max_graph_nodes < 1:
+            raise ValueError("max_graph_nodes must be >= 1")
+
+
+@dataclass
+class SearchStats:
+    graphs_explored: int = 0
+    graphs_generated: int = 0
+    graphs_deduped: int = 0
+    expanded_at_best: int = 0
+    assignments_evaluated: int = 0
+    inner_sweeps: int = 0
+    best_updates: int = 0
+    queue_pruned: int = 0
+    queue_cap_hits: int = 0
+    node_cap_hits: int = 0
+    new_cost_records: int = 0
+    wall_time_ms: float = field(default=0.0, compare=False)
+
+
+@dataclass
+class OptimizationResult:
+    graph: Graph
+    assignment: Assignment
+    cost: float
+    time_ms: float
+    energy: float
+    power_w: float
+    stats: SearchStats
+
+
+def _node_cap(cfg: SearchConfig, g0: Graph) -> int:
+    return cfg.max_graph_nodes if cfg.max_graph_nodes is not None else 4 * max(1, len(g0.compute_nodes()))
+
+
+class _Visible:
+    """Replays ensure_profiled in the reference's order on the caller's database.
+
+    The device priced candidates against rows profiled eagerly (session shadow);
+    the reference profiles a candidate's new signatures only when it evaluates
+    that candidate.  This copies those rows into `db` at exactly that point and
+    counts them, so `db` contents, `new_cost_records` and the append file match.
+    """
+
+    def __init__(self, session: DeviceSession, db: CostDatabase, profiler, append_path):
+        self.s, self.db, self.profiler, self.path = session, db, profiler, append_path
+
+    def touch(self, sig_ids) -> int:
+        made = 0
+        fh = None
+        try:
+            for sid in sig_ids:
+                if sid == 0xFFFFFFFF:
+                    continue
+                sig = self.s.sig_list[sid]
+                if self.db.has_signature(sig.text):
+                    continue
+                if fh is None and self.path:
+                    fh = open(self.path, "a")
+                src = self.s.shadow
+                if not src.has_signature(sig.text):
+                    profile_signature(sig, src, self.profiler)
+                for alg, _, _ in src.rows_for(sig.text):
+                    rec = src.lookup(sig.text, alg)
+                    self.db.add(sig.text, alg, rec)
+                    made += 1
+                    if fh is not None:
+                        fh.write(record_line(sig.text, alg, rec) + "\n")
+                        fh.flush()
+        finally:
+            if fh is not None:
+                fh.close()
+        return made
+
+
+class _Run:
+    """Device state of one search: geometry, records, visited set."""
+
+    def __init__(self, session: DeviceSession, g0: Graph, node_cap: int, db, profiler):
+        self.s = session
+        n_inputs = len(g0.nodes) - len(g0.compute_nodes())
+        n_refs = sum(len(v.inputs) for v in g0.nodes.values())
+        cap_nodes = node_cap + n_inputs + 2
+        cap_refs = n_refs + max(0, cap_nodes - len(g0.nodes)) + 4
+        session.bind_costs(db, profiler)
+        session.set_geometry(g0, cap_nodes, cap_refs)
+        session.visited_reset(1 << 20)
+        self.root = session.upload(g0)
+        self.refs: dict[int, int] = {self.root: 1}
+
+    def hold(self, slot):
+        self.refs[slot] = self.refs.get(slot, 0) + 1
+
+    def drop(self, slot):
+        self.refs[slot] -= 1
+        if self.refs[slot] == 0:
+            del self.refs[slot]
+            self.s.free(slot)
+
+    def close(self):
+        for slot in list(self.refs):
+            self.s.free(slot)
+        self.refs.clear()
+
+
+def _missing_text(session: DeviceSession, r: N.CandResult, db: CostDatabase) -> str:
+    for sid in r.touched_sig:
+        if sid != 0xFFFFFFFF and not db.has_signature(session.sig_list[sid].text):
+            return session.sig_list[sid].text
+    return "?"
+
+
+def outer_search(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: CostFunction,
+                 cfg: SearchConfig, profiler: ProfilerSpec | None, use_inner: bool = True,
+                 db_append_path: str | None = None, session: DeviceSession | None = None,
+                 trace: list | None = None) -> OptimizationResult:
+    """Best-first search over the rewrite space of g0 (search.py:211-272), expanded on the GPU."""
+    started = time.perf_counter()
+    stats = SearchStats()
+    s = session or DeviceSession.default()
+    cap = _node_cap(cfg, g0)
+    if profiler is not None:
+        stats.new_cost_records += ensure_profiled(g0, db, profiler, db_append_path)
+    run = _Run(s, g0, cap, db, profiler)
+    try:
+        pp = price_params(f, cfg.d, use_inner, cap)
+        (r0,) = s.price_slots([run.root], pp)
+        if r0.flags & N.F_MISSING:
+            node_cost_table(g0, db)  # raises the reference's MissingEntry
+        stats.assignments_evaluated += r0.evals
+        stats.inner_sweeps += r0.sweeps
+        best_slot, best_cost, best_t, best_e = run.root, r0.cost, r0.time_ms, r0.energy
+        run.hold(best_slot)
+        (h0,) = s.hash_slots([run.root])
+        s.visited_insert([h0])
+        heap: list[tuple[float, int]] = [(r0.cost, h0)]
+        pending: dict[int, int] = {h0: run.root}
+        visible = _Visible(s, db, profiler, db_append_path)
+        rule_ids = [r.rule_id for r in rules]
+        while heap:
+            cost, h = heapq.heappop(heap)
+            if cost > cfg.alpha * best_cost:
+                stats.queue_pruned += 1
+                slot = pending.pop(h, None)
+                if slot is not None:
+                    run.drop(slot)
+                continue
+            slot = pending.pop(h)
+            stats.graphs_explored += 1
+            if trace is not None:
+                trace.append(h)
+            if cost == best_cost:
+                stats.expanded_at_best += 1
+            results = s.expand([slot], rule_ids, pp) if rule_ids else []
+            keep_idx: list[int] = []
+            keep_role: list[tuple[bool, bool]] = []
+            for i, r in enumerate(results):
+                if not r.flags & N.F_FIRST:
+                    continue
+                stats.graphs_generated += 1
+                if r.flags & N.F_VISITED:
+                    stats.graphs_deduped += 1
+                    continue
+                if r.flags & N.F_CAPPED:
+                    stats.node_cap_hits += 1
+                    continue
+                if profiler is not None:
+                    stats.new_cost_records += visible.touch(r.touched_sig)
+                elif r.flags & N.F_MISSING:
+                    raise MissingEntry(_missing_text(s, r, db))
+                stats.assignments_evaluated += r.evals
+                stats.inner_sweeps += r.sweeps
+                prev = best_cost
+                new_best = r.cost < prev
+                pushed = False
+                if new_best:
+                    best_cost, best_t, best_e = r.cost, r.time_ms, r.energy
+                    stats.best_updates += 1
+                if r.cost < cfg.alpha * prev:
+                    if len(heap) >= cfg.max_queue:
+                        stats.queue_cap_hits += 1
+                    else:
+                        heapq.heappush(heap, (r.cost, r.hash))
+                        pushed = True
+                if new_best or pushed:
+                    keep_idx.append(i)
+                    keep_role.append((new_best, pushed))
+            slots = s.keep(keep_idx) if keep_idx else []
+            for (new_best, pushed), sl, i in zip(keep_role, slots, keep_idx):
+                run.refs[sl] = 0
+                if pushed:
+                    pending[results[i].hash] = sl
+                    run.hold(sl)
+                if new_best:
+                    run.drop(best_slot)
+                    best_slot = sl
+                    run.hold(sl)
+                if run.refs[sl] == 0:
+                    run.drop(sl)
+            run.drop(slot)
+        graph, assign = s.decode(s.read_record(best_slot), g0)
+    finally:
+        run.close()
+    stats.wall_time_ms = (time.perf_counter() - started) * 1000.0
+    power = best_e / best_t if best_t > 0 else 0.0
+    return OptimizationResult(graph, assign, best_cost, best_t, best_e, power, stats)
+
+
+# ---------------------------------------------------------------------------
+# single-graph entry points
+# ---------------------------------------------------------------------------
+
+def _price_one(g: Graph, db: CostDatabase, f: CostFunction, d: int, use_inner: bool, session=None):
+    s = session or DeviceSession.default()
+    s.bind_costs(db, None)
+    with scratch_graph(g, s) as (s, slot):
+        s.commit()
+        (r,) = s.price_slots([slot], price_params(f, d, use_inner, 1 << 30))
+        if r.flags & N.F_MISSING:
+            node_cost_table(g, db)
+        _, assign = s.decode(s.read_record(slot), g)
+    return r, assign
+
+
+def inner_search(g: Graph, db: CostDatabase, f: CostFunction, d: int = 1, session=None) -> Assignment:
+    """d-locally optimal assignment of one graph (search.py:106-159), on the GPU."""
+    return _price_one(g, db, f, d, True, session)[1]
+
+
+def default_assignment(g: Graph, db: CostDatabase) -> Assignment:
+    table = node_cost_table(g, db)
+    return {nid: rows[0][0] for nid, (_, rows) in table.items()}
+
+
+def canonical_hash(g: Graph, session=None) -> int:
+    """Relabel-invariant 64-bit digest (graph.py:520-549), computed on the GPU."""
+    with scratch_graph(g, session) as (s, slot):
+        return s.hash_slots([slot])[0]
+
+
+def brute_force_assignment(g: Graph, db: CostDatabase, f: CostFunction, max_points: int = 10**6) -> Assignment:
+    """Exhaustive assignment oracle of the reference API (search.py:162-182)."""
+    table = node_cost_table(g, db)
+    nids = sorted(table)
+    if not nids:
+        return {}
+    rows = [table[n][1] for n in nids]
+    total = math.prod(len(r) for r in rows)
+    if total > max_points:
+        raise SpaceTooLarge(f"{total} assignments exceed the bound {max_points}")
+    t = np.array([x[1] for x in rows[0]])
+    e = np.array([x[2] for x in rows[0]])
+    for r in rows[1:]:
+        t = np.add.outer(t, np.array([x[1] for x in r]))
+        e = np.add.outer(e, np.array([x[2] for x in r]))
+    idx = np.unravel_index(int(np.argmin(f.from_totals(t, e))), t.shape)
+    return {n: rows[i][int(k)][0] for i, (n, k) in enumerate(zip(nids, idx))}
+
+
+def constrained_optimize(g0: Graph, rules, db: CostDatabase, cfg: SearchConfig, time_bound_ms: float,
+                         profiler: ProfilerSpec | None, iterations: int = 20,
+                         db_append_path: str | None = None, session=None) -> OptimizationResult:
+    """Least energy under a time bound by binary search on w (search.py:336-381)."""
+    if profiler is not None:
+        ensure_profiled(g0, db, profiler, db_append_path)
+    if not g0.compute_nodes():
+        return outer_search(g0, rules, db, CostFunction("time"), cfg, profiler,
+                            db_append_path=db_append_path, session=session)
+    t_ref, e_ref, p_ref = normalization_refs(g0, db)
+
+    def run(w: float) -> OptimizationResult:
+        f = CostFunction.linear(w).with_refs(t_ref, e_ref, p_ref)
+        return outer_search(g0, rules, db, f, cfg, profiler, db_append_path=db_append_path, session=session)
+
+    energy_opt = run(1.0)
+    if energy_opt.time_ms <= time_bound_ms:
+        return energy_opt
+    time_opt = run(0.0)
+    if time_opt.time_ms > time_bound_ms:
+        raise InfeasibleConstraint(time_opt.time_ms)
+    best = time_opt
+    lo, hi = 0.0, 1.0
+    for _ in range(iterations):
+        mid = (lo + hi) / 2.0
+        res = run(mid)
+        if res.time_ms <= time_bound_ms:
+            lo = mid
+            if res.energy < best.energy:
+                best = res
+        else:
+            hi = mid
+    return best

@@ -181,10 +181,12 @@ int ef_visited_count(ef_ctx* ctx, uint64_t* count);
  * (rules.py:61-71), materialise each rewrite (rules.py:96-331), hash it
  * (graph.py:520-549), dedup within the step and against the visited set
  * (rules.py:79-88, search.py:247-251), price survivors (search.py:189-202).
- * Returns the number of candidates (>= 0), EF_NEED_RESOLVE when new
- * signatures / weight sets must be interned first (see ef_pending), or < 0. */
+ * Returns EF_OK with the number of candidates in *n_candidates,
+ * EF_NEED_RESOLVE when new signatures / weight sets must be interned first
+ * (see ef_pending; nothing was inserted into the visited set), or < 0. */
 int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents,
-              const int32_t* rules, uint32_t n_rules, const ef_price_params* pp, int insert_visited);
+              const int32_t* rules, uint32_t n_rules, const ef_price_params* pp, int insert_visited,
+              uint32_t* n_candidates);
 /* requests behind EF_NEED_RESOLVE: new signature descriptors and weight derivations
  * (op, a, b, s0) quadruples */
 int ef_pending(ef_ctx* ctx, ef_sig_desc* sigs, uint32_t sig_cap, uint32_t* n_sigs,

@@ -88,7 +88,7 @@ _PROTOS = {
     "ef_visited_reset": (C.c_int, [_P, C.c_uint64]),
     "ef_visited_insert": (C.c_int, [_P, _U64P, C.c_uint32]),
     "ef_visited_count": (C.c_int, [_P, _U64P]),
-    "ef_expand": (C.c_int, [_P, _U32P, C.c_uint32, _I32P, C.c_uint32, C.POINTER(PriceParams), C.c_int]),
+    "ef_expand": (C.c_int, [_P, _U32P, C.c_uint32, _I32P, C.c_uint32, C.POINTER(PriceParams), C.c_int, _U32P]),
     "ef_pending": (C.c_int, [_P, C.POINTER(SigDesc), C.c_uint32, _U32P, _I32P, C.c_uint32, _U32P]),
     "ef_results": (C.c_int, [_P, C.POINTER(CandResult), C.c_uint32]),
     "ef_keep": (C.c_int, [_P, _U32P, C.c_uint32, _U32P]),

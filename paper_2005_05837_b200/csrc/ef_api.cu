@@ -819,7 +819,9 @@ static int ensure_step_buffers(ef_ctx* ctx, uint32_t n_parents) {
 }
 
 int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, const int32_t* rules, uint32_t n_rules,
-              const ef_price_params* pp, int insert_visited) {
+              const ef_price_params* pp, int insert_visited, uint32_t* n_candidates) {
+  EF_REQUIRE(n_candidates, "ef_expand: null n_candidates");
+  *n_candidates = 0;
   EF_REQUIRE(!ctx->dirty, "tables not committed (call ef_tables_commit)");
   EF_REQUIRE(ctx->vis_mask, "visited set not initialised");
   EF_REQUIRE(n_rules <= 8, "at most 8 rules");
@@ -939,13 +941,14 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     EF_REQUIRE(!(err & 4u), "candidate exceeds record capacity (raise cap_nodes/cap_refs)");
     EF_REQUIRE(!(err & 8u), "graph too large for the hash kernel");
     ctx->last_total = total;
+    *n_candidates = total;
     if (ctx->last_req_sig || ctx->last_req_dv) return EF_NEED_RESOLVE;
     if (insert_visited) {
       k_visited_insert<<<grid_t, 256, 0, ctx->st>>>(D);
       EF_CUDA(cudaGetLastError());
       EF_CUDA(cudaStreamSynchronize(ctx->st));
     }
-    return (int)total;
+    return EF_OK;
   }
   ctx->err = "ef_expand: buffers did not converge";
   return EF_ERR_CAPACITY;

@@ -280,6 +280,14 @@ class DeviceSession:
     def commit(self) -> None:
         self._check(self.L.ef_tables_commit(self.ctx), "ef_tables_commit")
 
+    def _pending_summary(self) -> str:
+        ns, nd = C.c_uint32(0), C.c_uint32(0)
+        self._check(self.L.ef_pending(self.ctx, None, 0, C.byref(ns), None, 0, C.byref(nd)), "ef_pending")
+        sigs = (N.SigDesc * max(1, ns.value))()
+        dvs = (C.c_int32 * max(4, 4 * nd.value))()
+        self._check(self.L.ef_pending(self.ctx, sigs, ns.value, C.byref(ns), dvs, nd.value, C.byref(nd)), "ef_pending")
+        return f"sigs={[sigs[i].key() for i in range(ns.value)]} known={list(self.sig_desc_key)[:8]} derives={list(dvs)[:4 * nd.value]}"
+
     def resolve_pending(self) -> None:
         """Intern what the last ef_expand asked for, then commit."""
         ns, nd = C.c_uint32(0), C.c_uint32(0)
@@ -432,17 +440,21 @@ class DeviceSession:
                insert_visited: bool = True) -> list[N.CandResult]:
         parents = N.u32_array(slots)
         rules = N.i32_array(rule_ids)
-        while True:
+        count = C.c_uint32(0)
+        for attempt in range(64):
             rc = self.L.ef_expand(self.ctx, parents, len(slots), rules, len(rule_ids), C.byref(pp),
-                                  int(insert_visited))
+                                  int(insert_visited), C.byref(count))
             if rc == N.EF_NEED_RESOLVE:
+                if attempt >= 3:
+                    raise N.NativeError(f"ef_expand keeps asking for interning: {self._pending_summary()}")
                 self.resolve_pending()
                 continue
             self._check(rc, "ef_expand")
             break
-        out = (N.CandResult * max(1, rc))()
-        self._check(self.L.ef_results(self.ctx, out, rc), "ef_results")
-        return [out[i] for i in range(rc)]
+        n = count.value
+        out = (N.CandResult * max(1, n))()
+        self._check(self.L.ef_results(self.ctx, out, n), "ef_results")
+        return [out[i] for i in range(n)]
 
     def keep(self, cand_idx: list[int]) -> list[int]:
         slots = [self.alloc() for _ in cand_idx]

@@ -74,7 +74,7 @@ typedef struct {
   uint32_t cap_nodes, cap_refs, cap_outs;
   uint32_t record_bytes;                        /* total slot size            */
   uint32_t off_nid, off_sig, off_aux, off_nin;  /* byte offsets of the arrays  */
-  uint32_t off_inoff, off_topo, off_refs, off_outs, off_keys, off_alg;
+  uint32_t off_inoff, off_topo, off_refs, off_outs, off_keys, off_alg, off_sperm;
 } ef_geometry;
 
 /* Record header (first 64 bytes of a slot). */
@@ -93,6 +93,7 @@ typedef struct {
  *   uint32 outs[cap_outs]      graph outputs, same packing
  *   uint8  keys[cap_nodes][16] Merkle node keys (graph.py:528-540)
  *   uint8  alg[cap_nodes]      algorithm per node after pricing
+ *   uint32 sperm[cap_nodes]    positions in ascending key order (sorted(keys) of graph.py:547)
  */
 
 /* Pricing parameters: cost function (cost.py:234-254) + inner search (search.py:106-153). */
@@ -165,6 +166,12 @@ int ef_record_alloc(ef_ctx* ctx, uint32_t* slot);
 int ef_record_free(ef_ctx* ctx, uint32_t slot);
 int ef_record_write(ef_ctx* ctx, uint32_t slot, const void* host, uint64_t bytes);
 int ef_record_read(ef_ctx* ctx, uint32_t slot, void* host, uint64_t bytes);
+/* batched upload: record i comes from host + i * stride (one stream sync for all) */
+int ef_records_write(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const void* host, uint64_t stride,
+                     uint64_t bytes);
+/* page-locked host staging memory for ef_records_write / ef_results */
+void* ef_host_alloc(uint64_t bytes);
+void ef_host_free(void* p);
 /* canonical hash of records (graph.py:520-549): recomputes all keys */
 int ef_hash_records(ef_ctx* ctx, const uint32_t* slots, uint32_t n, uint64_t* hashes);
 /* inner search on records (search.py:106-153); writes alg[] into the records */

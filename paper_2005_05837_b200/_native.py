@@ -39,7 +39,7 @@ class SigDesc(C.Structure):
 class Geometry(C.Structure):
     _fields_ = [(n, C.c_uint32) for n in (
         "cap_nodes", "cap_refs", "cap_outs", "record_bytes", "off_nid", "off_sig", "off_aux", "off_nin",
-        "off_inoff", "off_topo", "off_refs", "off_outs", "off_keys", "off_alg")]
+        "off_inoff", "off_topo", "off_refs", "off_outs", "off_keys", "off_alg", "off_sperm")]
 
 
 class PriceParams(C.Structure):
@@ -83,6 +83,9 @@ _PROTOS = {
     "ef_record_free": (C.c_int, [_P, C.c_uint32]),
     "ef_record_write": (C.c_int, [_P, C.c_uint32, C.c_void_p, C.c_uint64]),
     "ef_record_read": (C.c_int, [_P, C.c_uint32, C.c_void_p, C.c_uint64]),
+    "ef_records_write": (C.c_int, [_P, _U32P, C.c_uint32, C.c_void_p, C.c_uint64, C.c_uint64]),
+    "ef_host_alloc": (C.c_void_p, [C.c_uint64]),
+    "ef_host_free": (None, [C.c_void_p]),
     "ef_hash_records": (C.c_int, [_P, _U32P, C.c_uint32, _U64P]),
     "ef_price_records": (C.c_int, [_P, _U32P, C.c_uint32, C.POINTER(PriceParams), C.POINTER(CandResult)]),
     "ef_visited_reset": (C.c_int, [_P, C.c_uint64]),

@@ -100,10 +100,11 @@ struct ef_ctx {
   DevBuf<uint32_t> d_pscratch, d_site_count, d_cand_off, d_step_seq, d_scalars;
   DevBuf<char> d_cand;
   DevBuf<int32_t> d_srcpos, d_req_dv;
-  DevBuf<uint8_t> d_seed;
+  DevBuf<uint8_t> d_seed, d_pmark;
   DevBuf<ef_cand_result> d_res;
   DevBuf<ef_sig_desc> d_req_sig;
   DevBuf<uint64_t> d_hash_out;
+  DevBuf<uint32_t> d_sperm;
   uint32_t cand_cap = 0, site_cap = 0;
   uint32_t req_cap = 4096;
   uint32_t last_total = 0;
@@ -228,9 +229,11 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_srcpos.release();
   ctx->d_req_dv.release();
   ctx->d_seed.release();
+  ctx->d_pmark.release();
   ctx->d_res.release();
   ctx->d_req_sig.release();
   ctx->d_hash_out.release();
+  ctx->d_sperm.release();
   ctx->d_vis.release();
   ctx->d_vis_count.release();
   for (auto& e : ctx->ev) cudaEventDestroy(e);
@@ -632,6 +635,8 @@ int ef_set_geometry(ef_ctx* ctx, uint32_t cap_nodes, uint32_t cap_refs, uint32_t
   o = al(o + 16 * cap_nodes);
   g.o_alg = o;
   o = al(o + cap_nodes);
+  g.o_sperm = o;
+  o = al(o + 4 * cap_nodes);
   g.bytes = o;
   ctx->slots_per_chunk = std::max<uint32_t>(1, (uint32_t)((64ull << 20) / g.bytes));
   ctx->input_text.assign(input_text ? input_text : "", input_text ? input_text_len : 0);
@@ -652,6 +657,7 @@ int ef_set_geometry(ef_ctx* ctx, uint32_t cap_nodes, uint32_t cap_refs, uint32_t
     out->off_outs = g.o_outs;
     out->off_keys = g.o_keys;
     out->off_alg = g.o_alg;
+    out->off_sperm = g.o_sperm;
   }
   return EF_OK;
 }
@@ -691,13 +697,45 @@ int ef_record_read(ef_ctx* ctx, uint32_t slot, void* host, uint64_t bytes) {
   return EF_OK;
 }
 
-static uint32_t hash_smem_nodes(ef_ctx* ctx) { return pow2_at_least(ctx->geo.cap_nodes); }
-static size_t hash_smem_bytes(uint32_t nodes) { return ((nodes + 15u) & ~15u) + 16ull * nodes; }
+static size_t hash_top_smem(uint32_t sort_cap) { return 16 * 32 * 8 + 20ull * sort_cap; }
 
-static int ensure_hash_smem(ef_ctx* ctx, size_t bytes) {
-  EF_REQUIRE(bytes <= 227 * 1024, "graph too large for the shared-memory hash path (cap_nodes > 8192)");
-  EF_CUDA(cudaFuncSetAttribute(k_hash<kHashThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+// k_hash_keys (thread per record) then k_hash_top (warp per 32 records)
+static int launch_hash(ef_ctx* ctx, HashArgs& H, uint32_t max_records) {
+  H.sort_cap = pow2_at_least(ctx->geo.cap_nodes);
+  const size_t sm = hash_top_smem(H.sort_cap);
+  EF_REQUIRE(sm <= 227 * 1024, "graph too large for the shared-memory key sort (cap_nodes > 8192)");
+  EF_CUDA(ctx->d_sperm.reserve((uint64_t)max_records * ctx->geo.cap_nodes, ctx->st));
+  H.sperm = ctx->d_sperm.p;
+  EF_CUDA(cudaFuncSetAttribute(k_hash_top, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  const uint32_t g1 = std::max<uint32_t>(1, std::min<uint32_t>((max_records + kHashThreads - 1) / kHashThreads, ctx->n_sm * 16));
+  k_hash_keys<kHashThreads><<<g1, kHashThreads, 0, ctx->st>>>(H);
+  EF_CUDA(cudaGetLastError());
+  const uint32_t g2 = std::max<uint32_t>(1, std::min<uint32_t>((max_records + 31) / 32, ctx->n_sm * 16));
+  k_hash_top<<<g2, 32, sm, ctx->st>>>(H);
+  EF_CUDA(cudaGetLastError());
   return EF_OK;
+}
+
+int ef_records_write(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const void* host, uint64_t stride,
+                     uint64_t bytes) {
+  EF_REQUIRE(bytes <= ctx->geo.bytes, "ef_records_write: record too large");
+  const char* h = static_cast<const char*>(host);
+  for (uint32_t i = 0; i < n; ++i) {
+    EF_REQUIRE(slots[i] < ctx->n_slots, "ef_records_write: bad slot");
+    EF_CUDA(cudaMemcpyAsync(slot_addr(ctx, slots[i]), h + (uint64_t)i * stride, bytes, cudaMemcpyHostToDevice, ctx->st));
+  }
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+void* ef_host_alloc(uint64_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void ef_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 static int stage_addrs(ef_ctx* ctx, DevBuf<unsigned long long>& buf, const uint32_t* slots, uint32_t n) {
@@ -723,12 +761,8 @@ int ef_hash_records(ef_ctx* ctx, const uint32_t* slots, uint32_t n, uint64_t* ha
   H.n = n;
   H.rec = ctx->d_addr_a.p;
   H.hash_out = ctx->d_hash_out.p;
-  H.smem_nodes = hash_smem_nodes(ctx);
   H.err = ctx->d_scalars.p + 1;
-  size_t sm = hash_smem_bytes(H.smem_nodes);
-  if ((rc = ensure_hash_smem(ctx, sm))) return rc;
-  k_hash<kHashThreads><<<std::min<uint32_t>(n, ctx->n_sm * 4), kHashThreads, sm, ctx->st>>>(H);
-  EF_CUDA(cudaGetLastError());
+  if ((rc = launch_hash(ctx, H, n))) return rc;
   EF_CUDA(cudaMemcpyAsync(hashes, ctx->d_hash_out.p, n * 8, cudaMemcpyDeviceToHost, ctx->st));
   EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
   EF_CUDA(cudaStreamSynchronize(ctx->st));
@@ -808,6 +842,7 @@ static int ensure_step_buffers(ef_ctx* ctx, uint32_t n_parents) {
   EF_CUDA(ctx->d_cand.reserve((uint64_t)ctx->cand_cap * g.bytes, ctx->st));
   EF_CUDA(ctx->d_srcpos.reserve((uint64_t)ctx->cand_cap * g.cap_nodes, ctx->st));
   EF_CUDA(ctx->d_seed.reserve((uint64_t)ctx->cand_cap * g.cap_nodes, ctx->st));
+  EF_CUDA(ctx->d_pmark.reserve((uint64_t)ctx->cand_cap * g.cap_nodes, ctx->st));
   EF_CUDA(ctx->d_res.reserve(ctx->cand_cap, ctx->st));
   uint32_t tcap = pow2_at_least(2ull * ctx->cand_cap);
   EF_CUDA(ctx->d_step_key.reserve(tcap, ctx->st));
@@ -853,6 +888,7 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     A.cand_cap = ctx->cand_cap;
     A.cand_srcpos = ctx->d_srcpos.p;
     A.cand_seed = ctx->d_seed.p;
+    A.cand_pmark = ctx->d_pmark.p;
     A.res = ctx->d_res.p;
     A.req_sig = ctx->d_req_sig.p;
     A.req_sig_cap = ctx->req_cap;
@@ -880,14 +916,11 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     H.parent_addr = A.parent_addr;
     H.srcpos = A.cand_srcpos;
     H.seed = A.cand_seed;
+    H.pmark = A.cand_pmark;
     H.res = A.res;
     H.incremental = 1;
-    H.smem_nodes = hash_smem_nodes(ctx);
     H.err = A.err;
-    size_t sm = hash_smem_bytes(H.smem_nodes);
-    if ((rc = ensure_hash_smem(ctx, sm))) return rc;
-    k_hash<kHashThreads><<<std::min<uint32_t>(ctx->cand_cap, ctx->n_sm * 8), kHashThreads, sm, ctx->st>>>(H);
-    EF_CUDA(cudaGetLastError());
+    if ((rc = launch_hash(ctx, H, ctx->cand_cap))) return rc;
     cudaEventRecord(ctx->ev[3], ctx->st);
 
     const uint32_t tcap = pow2_at_least(2ull * ctx->cand_cap);
@@ -933,7 +966,7 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
       continue;
     }
     if (err & 2u) {  // candidate arena too small
-      ctx->cand_cap = std::max<uint32_t>(total, ctx->cand_cap * 2);
+      ctx->cand_cap = std::max<uint32_t>(ctx->h_scalars[4] + ctx->h_scalars[4] / 4, ctx->cand_cap * 2);
       ctx->d_step_key.release();
       ctx->d_step_seq.release();
       continue;

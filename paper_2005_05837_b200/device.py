@@ -366,10 +366,13 @@ class DeviceSession:
         return buf
 
     def upload(self, g: Graph) -> int:
+        """Write g as a record and compute its node keys + sorted-key order on the device
+        (every record must carry them before it can be expanded as a parent)."""
         buf = self.encode(g)
         self.commit()
         slot = self.alloc()
         self._check(self.L.ef_record_write(self.ctx, slot, buf.ctypes.data, buf.nbytes), "ef_record_write")
+        self.hash_slots([slot])
         return slot
 
     def read_record(self, slot: int) -> np.ndarray:

@@ -342,3 +342,73 @@ def constrained_optimize(g0: Graph, rules, db: CostDatabase, cfg: SearchConfig, 
         else:
             hi = mid
     return best
+
+
+# ---------------------------------------------------------------------------
+# frontier batches (bench + scaling): the real frontier of a search, resident in HBM
+# ---------------------------------------------------------------------------
+
+class Frontier:
+    """A batch of frontier graphs of g0's search, kept as device records.
+
+    Built by expanding the origin and then the cheapest level-1 graphs in the
+    reference's best-first order, keeping every candidate the search would
+    enqueue (cost < alpha * best).  `step()` expands the whole batch at once:
+    one ef_expand over all parents, i.e. every rule at every site of every
+    frontier graph, dedup, and the inner search on every survivor.
+    """
+
+    def __init__(self, g0: Graph, db: CostDatabase, profiler, f: CostFunction, cfg: SearchConfig,
+                 n_parents: int, rules=None, session: DeviceSession | None = None):
+        from .rewrite import default_rules
+
+        self.s = session or DeviceSession.default()
+        self.g0 = g0
+        self.rules = rules if rules is not None else default_rules()
+        self.rule_ids = [r.rule_id for r in self.rules]
+        cap = _node_cap(cfg, g0)
+        if profiler is not None:
+            ensure_profiled(g0, db, profiler)
+        self.run = _Run(self.s, g0, cap, db, profiler)
+        self.pp = price_params(f, cfg.d, True, cap)
+        (r0,) = self.s.price_slots([self.run.root], self.pp)
+        (h0,) = self.s.hash_slots([self.run.root])
+        self.s.visited_insert([h0])
+        best = r0.cost
+        heap = [(r0.cost, h0, self.run.root)]
+        slots: list[int] = []
+        seen = {h0}
+        while heap and len(slots) < n_parents:
+            cost, h, slot = heapq.heappop(heap)
+            slots.append(slot)
+            res = self.s.expand([slot], self.rule_ids, self.pp, insert_visited=True)
+            keep = []
+            for i, r in enumerate(res):
+                if (r.flags & (N.F_FIRST | N.F_VISITED | N.F_CAPPED)) != N.F_FIRST or r.hash in seen:
+                    continue
+                if r.cost < cfg.alpha * best:
+                    keep.append(i)
+                    seen.add(r.hash)
+                best = min(best, r.cost)
+            for i, sl in zip(keep, self.s.keep(keep)):
+                heapq.heappush(heap, (res[i].cost, res[i].hash, sl))
+        # fill the batch with the remaining enqueued graphs in heap order
+        while heap and len(slots) < n_parents:
+            slots.append(heapq.heappop(heap)[2])
+        self.leftover = [sl for _, _, sl in heap]
+        self.slots = slots
+        # the timed steps start from a visited set holding only the explored prefix
+        self.s.visited_reset(1 << 22)
+
+    def step(self, slots=None, insert_visited: bool = False):
+        return self.s.expand(slots if slots is not None else self.slots, self.rule_ids, self.pp, insert_visited)
+
+    def decode(self, slot: int) -> Graph:
+        return self.s.decode(self.s.read_record(slot), self.g0)[0]
+
+    def close(self):
+        for sl in self.slots + self.leftover:
+            if sl != self.run.root:
+                self.s.free(sl)
+        self.slots, self.leftover = [], []
+        self.run.close()

@@ -61,7 +61,7 @@ def test_models_validate():
 def test_library_exports_every_declared_symbol():
     lib = _native.load_library()
     header = open(os.path.join(ROOT, "include", "ef200.h")).read()
-    declared = set(re.findall(r"^(?:int|void|ef_ctx\*|const char\*)\s+(ef_\w+)\(", header, re.M))
+    declared = set(re.findall(r"^(?:int|void\*?|ef_ctx\*|const char\*)\s+(ef_\w+)\(", header, re.M))
     assert declared, "no declarations parsed"
     assert declared == set(_native.EXPORTED)
     for name in declared:

@@ -259,7 +259,7 @@ def run_ours(args, world, rank, local):
         res, ms = step()
         dev_ms.append(sum(ms))
         stage_ms = [a + b for a, b in zip(stage_ms, ms)]
-        priced_n += sum(1 for r in res if r.flags & N.F_PRICED)
+        priced_n += int(np.count_nonzero(res["flags"] & N.F_PRICED))
         gen_n += len(res)
     clk = clocks.stop(local)
     total_ms = sum(dev_ms)
@@ -296,7 +296,7 @@ def run_ours(args, world, rank, local):
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             e2e_times.append(dt)
-            e2e_priced += sum(1 for r in res if r.flags & N.F_PRICED)
+            e2e_priced += int(np.count_nonzero(res["flags"] & N.F_PRICED))
     n_cand = len(res)
     s.L.ef_host_free(pinned)
     e2e_total = sum(e2e_times)
@@ -345,7 +345,7 @@ def run_ours(args, world, rank, local):
         "roofline": {"bound": "hbm", "kernel": f"k_{dom_name}", "achieved": achieved, "peak": peak,
                      "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": rec_bytes * len(mine),
-                "d2h_bytes_per_step": n_cand * C.sizeof(N.CandResult)},
+                "d2h_bytes_per_step": n_cand * N.CAND_DTYPE.itemsize},
         "gpu_launches": 7 * args.steps,
         "clocks": clk,
     }

@@ -56,6 +56,15 @@ class CandResult(C.Structure):
                 ("pad", C.c_uint32)]
 
 
+import numpy as _np
+
+# numpy view of ef_cand_result (same layout; checked against ctypes at import)
+CAND_DTYPE = _np.dtype([("hash", "<u8"), ("cost", "<f8"), ("time_ms", "<f8"), ("energy", "<f8"),
+                        ("evals", "<i8"), ("sweeps", "<i4"), ("n_compute", "<i4"), ("flags", "<u4"),
+                        ("parent", "<u4"), ("rule", "<u4"), ("site_a", "<u4"), ("site_b", "<u4"),
+                        ("touched_sig", "<u4", (2,)), ("pad", "<u4")])
+assert CAND_DTYPE.itemsize == C.sizeof(CandResult)
+
 _P = C.c_void_p
 _U32P = C.POINTER(C.c_uint32)
 _I32P = C.POINTER(C.c_int32)
@@ -93,7 +102,7 @@ _PROTOS = {
     "ef_visited_count": (C.c_int, [_P, _U64P]),
     "ef_expand": (C.c_int, [_P, _U32P, C.c_uint32, _I32P, C.c_uint32, C.POINTER(PriceParams), C.c_int, _U32P]),
     "ef_pending": (C.c_int, [_P, C.POINTER(SigDesc), C.c_uint32, _U32P, _I32P, C.c_uint32, _U32P]),
-    "ef_results": (C.c_int, [_P, C.POINTER(CandResult), C.c_uint32]),
+    "ef_results": (C.c_int, [_P, C.c_void_p, C.c_uint32]),
     "ef_keep": (C.c_int, [_P, _U32P, C.c_uint32, _U32P]),
     "ef_last_timing": (C.c_int, [_P, C.POINTER(C.c_float)]),
 }

@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "ef_kernels.cuh"
 
 using namespace ef;
@@ -98,9 +100,10 @@ struct ef_ctx {
   // step buffers
   DevBuf<unsigned long long> d_parent_addr, d_sites, d_step_key, d_addr_a, d_addr_b;
   DevBuf<uint32_t> d_pscratch, d_site_count, d_cand_off, d_step_seq, d_scalars;
-  DevBuf<char> d_cand;
+  DevBuf<char> d_cand, d_stage;
   DevBuf<int32_t> d_srcpos, d_req_dv;
-  DevBuf<uint8_t> d_seed, d_pmark;
+  DevBuf<uint8_t> d_seed, d_pmark, d_sort_tmp;
+  DevBuf<uint32_t> d_first, d_first_sorted, d_iota, d_order;
   DevBuf<ef_cand_result> d_res;
   DevBuf<ef_sig_desc> d_req_sig;
   DevBuf<uint64_t> d_hash_out;
@@ -226,10 +229,16 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_step_seq.release();
   ctx->d_scalars.release();
   ctx->d_cand.release();
+  ctx->d_stage.release();
   ctx->d_srcpos.release();
   ctx->d_req_dv.release();
   ctx->d_seed.release();
   ctx->d_pmark.release();
+  ctx->d_sort_tmp.release();
+  ctx->d_first.release();
+  ctx->d_first_sorted.release();
+  ctx->d_iota.release();
+  ctx->d_order.release();
   ctx->d_res.release();
   ctx->d_req_sig.release();
   ctx->d_hash_out.release();
@@ -719,11 +728,22 @@ static int launch_hash(ef_ctx* ctx, HashArgs& H, uint32_t max_records) {
 int ef_records_write(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const void* host, uint64_t stride,
                      uint64_t bytes) {
   EF_REQUIRE(bytes <= ctx->geo.bytes, "ef_records_write: record too large");
-  const char* h = static_cast<const char*>(host);
+  EF_REQUIRE(stride % 16 == 0 && bytes % 16 == 0, "ef_records_write: stride/bytes must be multiples of 16");
+  if (!n) return EF_OK;
+  // one bulk host->device copy into a staging area, then a device-side scatter into the slots
+  EF_CUDA(ctx->d_stage.reserve((uint64_t)n * stride, ctx->st));
+  EF_CUDA(cudaMemcpyAsync(ctx->d_stage.p, host, (uint64_t)n * stride, cudaMemcpyHostToDevice, ctx->st));
+  std::vector<unsigned long long> src(n), dst(n);
   for (uint32_t i = 0; i < n; ++i) {
     EF_REQUIRE(slots[i] < ctx->n_slots, "ef_records_write: bad slot");
-    EF_CUDA(cudaMemcpyAsync(slot_addr(ctx, slots[i]), h + (uint64_t)i * stride, bytes, cudaMemcpyHostToDevice, ctx->st));
+    src[i] = (unsigned long long)(ctx->d_stage.p + (uint64_t)i * stride);
+    dst[i] = (unsigned long long)slot_addr(ctx, slots[i]);
   }
+  int rc;
+  if ((rc = upload(ctx, ctx->d_addr_a, src)) || (rc = upload(ctx, ctx->d_addr_b, dst))) return rc;
+  k_copy_records<<<std::min<uint32_t>(n, ctx->n_sm * 8), 256, 0, ctx->st>>>(ctx->d_addr_a.p, ctx->d_addr_b.p, n,
+                                                                            (uint32_t)bytes);
+  EF_CUDA(cudaGetLastError());
   EF_CUDA(cudaStreamSynchronize(ctx->st));
   return EF_OK;
 }
@@ -843,6 +863,20 @@ static int ensure_step_buffers(ef_ctx* ctx, uint32_t n_parents) {
   EF_CUDA(ctx->d_srcpos.reserve((uint64_t)ctx->cand_cap * g.cap_nodes, ctx->st));
   EF_CUDA(ctx->d_seed.reserve((uint64_t)ctx->cand_cap * g.cap_nodes, ctx->st));
   EF_CUDA(ctx->d_pmark.reserve((uint64_t)ctx->cand_cap * g.cap_nodes, ctx->st));
+  EF_CUDA(ctx->d_first.reserve(ctx->cand_cap, ctx->st));
+  EF_CUDA(ctx->d_first_sorted.reserve(ctx->cand_cap, ctx->st));
+  EF_CUDA(ctx->d_order.reserve(ctx->cand_cap, ctx->st));
+  if (ctx->d_iota.cap < ctx->cand_cap) {
+    EF_CUDA(ctx->d_iota.reserve(ctx->cand_cap, ctx->st));
+    std::vector<uint32_t> io(ctx->d_iota.cap);
+    for (size_t i = 0; i < io.size(); ++i) io[i] = (uint32_t)i;
+    EF_CUDA(cudaMemcpyAsync(ctx->d_iota.p, io.data(), io.size() * 4, cudaMemcpyHostToDevice, ctx->st));
+    EF_CUDA(cudaStreamSynchronize(ctx->st));
+  }
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)ctx->cand_cap, 0, 24);
+  EF_CUDA(ctx->d_sort_tmp.reserve(tmp, ctx->st));
   EF_CUDA(ctx->d_res.reserve(ctx->cand_cap, ctx->st));
   uint32_t tcap = pow2_at_least(2ull * ctx->cand_cap);
   EF_CUDA(ctx->d_step_key.reserve(tcap, ctx->st));
@@ -889,6 +923,7 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     A.cand_srcpos = ctx->d_srcpos.p;
     A.cand_seed = ctx->d_seed.p;
     A.cand_pmark = ctx->d_pmark.p;
+    A.cand_first = ctx->d_first.p;
     A.res = ctx->d_res.p;
     A.req_sig = ctx->d_req_sig.p;
     A.req_sig_cap = ctx->req_cap;
@@ -917,6 +952,16 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     H.srcpos = A.cand_srcpos;
     H.seed = A.cand_seed;
     H.pmark = A.cand_pmark;
+    H.first = A.cand_first;
+    {
+      // lanes take candidates in order of their first dirty slot: warps share similar dirty cones
+      size_t tmp = ctx->d_sort_tmp.cap;
+      k_first_pad<<<std::min<uint32_t>((ctx->cand_cap + 255) / 256, ctx->n_sm * 4), 256, 0, ctx->st>>>(
+          ctx->d_first.p, A.total, ctx->cand_cap);
+      EF_CUDA(cub::DeviceRadixSort::SortPairs(ctx->d_sort_tmp.p, tmp, ctx->d_first.p, ctx->d_first_sorted.p,
+                                              ctx->d_iota.p, ctx->d_order.p, (int)ctx->cand_cap, 0, 24, ctx->st));
+      H.order = ctx->d_order.p;
+    }
     H.res = A.res;
     H.incremental = 1;
     H.err = A.err;

@@ -146,6 +146,7 @@ struct StepArgs {
   int32_t* cand_srcpos;  // cap_nodes per candidate
   uint8_t* cand_seed;    // cap_nodes per candidate
   uint8_t* cand_pmark;   // cap_nodes per candidate: parent position removed (dropped or re-keyed)
+  uint32_t* cand_first;  // per candidate: first child topo slot whose key can differ from the parent
   ef_cand_result* res;
   ef_sig_desc* req_sig;
   uint32_t* n_req_sig;
@@ -509,6 +510,7 @@ __device__ void plan_rewrite(const StepArgs& A, Plan& P, Rec R, int n, uint32_t 
 template <int BT>
 __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
   __shared__ Plan P;
+  __shared__ uint32_t first_slot;
   const Geo& G = A.g;
   const uint32_t total = min(A.total[0], A.cand_cap);
   for (uint32_t c = blockIdx.x; c < total; c += gridDim.x) {
@@ -532,6 +534,7 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
     if (threadIdx.x == 0) {
       plan_rewrite(A, P, R, n, rule, sa, sb, u0, u1);
       P.slot_of[0] = P.slot_of[1] = P.slot_of[2] = -1;
+      first_slot = 0xffffffffu;
       for (int k = 0; k < 2; ++k) {
         P.drop_refs[k] = P.drop[k] >= 0 ? (int)pnin[P.drop[k]] : 0;
         P.drop_inoff[k] = P.drop[k] >= 0 ? pinoff[P.drop[k]] : 0xffffffffu;
@@ -599,12 +602,16 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
       uint32_t* caux = C.aux(G);
       uint32_t* cnin = C.nin(G);
       uint32_t* cinoff = C.inoff(G);
+      const uint64_t* pkeys = R.keys(G);
+      uint64_t* ckeys = C.keys(G);
       uint8_t* pmark = A.cand_pmark + (uint64_t)c * G.cap_nodes;
       for (int i = threadIdx.x; i < n; i += BT) {
         pmark[i] = (i == d0 || i == d1) ? 1 : 0;
         if (i == d0 || i == d1) continue;
         uint32_t j = cpos((uint32_t)i);
         cnid[j] = pnid[i];
+        ckeys[2 * j] = pkeys[2 * i];
+        ckeys[2 * j + 1] = pkeys[2 * i + 1];
         csig[j] = i == P.mod ? P.mod_sig : psig[i];
         caux[j] = i == P.mod ? P.mod_aux : paux[i];
         cnin[j] = pnin[i];
@@ -699,6 +706,7 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
         }
         uint32_t at = (uint32_t)(s + shift);
         uint32_t v = ptopo[s];
+        if (special || (int)v == P.mod) atomicMin(&first_slot, at);
         if (!special) {
           ctopo[at] = cpos(v);
         } else if (s == sp_slot[2]) {
@@ -710,6 +718,7 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
         (void)emit;
       }
     }
+    __syncthreads();  // first_slot complete
     if (threadIdx.x == 0) {
       ef_rec_header& H = C.h();
       H.n = n_child;
@@ -721,6 +730,7 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
       res->rule = rule;
       res->site_a = sa;
       res->site_b = sb;
+      A.cand_first[c] = first_slot;
       res->touched_sig[0] = P.touched[0];
       res->touched_sig[1] = P.touched[1];
       res->n_compute = H.n_compute;
@@ -731,6 +741,14 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
     }
     __syncthreads();
   }
+}
+
+// slots past the step's candidate count sort last
+__global__ void k_first_pad(uint32_t* first, const uint32_t* total, uint32_t cap) {
+  const uint32_t t = total[0];
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cap; c += gridDim.x * blockDim.x)
+    if (c >= t) first[c] = 0xFFFFFFu;
+    else first[c] = min(first[c], 0xFFFFFEu);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -758,6 +776,8 @@ struct HashArgs {
   uint8_t* seed;      // bit0 rewritten (materialise), bit1 dirty (set here)
   uint8_t* pmark;     // parent positions whose key is not in the child (dropped / dirty)
   uint32_t* sperm;    // scratch, cap_nodes per record: sorted dirty positions
+  const uint32_t* first;  // per candidate first dirty topo slot (incremental)
+  const uint32_t* order;  // lane -> candidate permutation (sorted by first slot), or null
   ef_cand_result* res;
   uint64_t* hash_out;  // full mode output
   int incremental;
@@ -851,7 +871,8 @@ __global__ void __launch_bounds__(BT) k_hash_keys(HashArgs A) {
   const Geo& G = A.g;
   const Tables& T = A.T;
   const uint32_t total = A.total ? A.total[0] : A.n;
-  for (uint32_t c = blockIdx.x * BT + threadIdx.x; c < total; c += gridDim.x * BT) {
+  for (uint32_t lc = blockIdx.x * BT + threadIdx.x; lc < total; lc += gridDim.x * BT) {
+    const uint32_t c = A.order ? A.order[lc] : lc;
     if (A.res && (A.res[c].flags & EF_F_INCOMPLETE)) continue;
     Rec R{A.rec ? reinterpret_cast<char*>(A.rec[c]) : A.cand_base + (uint64_t)c * G.bytes};
     const int n = R.h().n;
@@ -870,8 +891,8 @@ __global__ void __launch_bounds__(BT) k_hash_keys(HashArgs A) {
     const uint32_t* inoff = R.inoff(G);
     const uint32_t* refs = R.refs(G);
     uint64_t* keys = R.keys(G);
-    const uint64_t* pkeys = A.incremental ? P.keys(G) : nullptr;
-    for (int s = 0; s < n; ++s) {
+    const int s0 = A.incremental ? (int)min(A.first[c], (uint32_t)n) : 0;
+    for (int s = s0; s < n; ++s) {
       const uint32_t v = topo[s];
       const uint32_t r0 = inoff[v], r1 = r0 + nin[v];
       bool dirty = true;
@@ -884,12 +905,7 @@ __global__ void __launch_bounds__(BT) k_hash_keys(HashArgs A) {
           if (srcpos[v] >= 0) A.pmark[(uint64_t)c * G.cap_nodes + (uint32_t)srcpos[v]] = 1;
         }
       }
-      if (!dirty) {
-        const uint32_t sp = (uint32_t)srcpos[v];
-        keys[2 * v] = pkeys[2 * sp];
-        keys[2 * v + 1] = pkeys[2 * sp + 1];
-        continue;
-      }
+      if (!dirty) continue;  // inherited key already copied by k_materialise
       B2bS<BT> st;
       st.init(16, msg + threadIdx.x);
       const uint32_t sg = sig[v];

@@ -455,9 +455,10 @@ class DeviceSession:
             self._check(rc, "ef_expand")
             break
         n = count.value
-        out = (N.CandResult * max(1, n))()
-        self._check(self.L.ef_results(self.ctx, out, n), "ef_results")
-        return [out[i] for i in range(n)]
+        out = np.empty(n, dtype=N.CAND_DTYPE)
+        if n:
+            self._check(self.L.ef_results(self.ctx, out.ctypes.data, n), "ef_results")
+        return out
 
     def keep(self, cand_idx: list[int]) -> list[int]:
         slots = [self.alloc() for _ in cand_idx]

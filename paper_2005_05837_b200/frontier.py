@@ -155,8 +155,8 @@ class _Run:
         self.refs.clear()
 
 
-def _missing_text(session: DeviceSession, r: N.CandResult, db: CostDatabase) -> str:
-    for sid in r.touched_sig:
+def _missing_text(session: DeviceSession, r, db: CostDatabase) -> str:
+    for sid in r["touched_sig"].tolist():
         if sid != 0xFFFFFFFF and not db.has_signature(session.sig_list[sid].text):
             return session.sig_list[sid].text
     return "?"
@@ -176,7 +176,7 @@ def outer_search(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: 
     run = _Run(s, g0, cap, db, profiler)
     try:
         pp = price_params(f, cfg.d, use_inner, cap)
-        (r0,) = s.price_slots([run.root], pp)
+        (r0,) = s.price_slots([run.root], pp)  # ctypes CandResult
         if r0.flags & N.F_MISSING:
             node_cost_table(g0, db)  # raises the reference's MissingEntry
         stats.assignments_evaluated += r0.evals
@@ -203,36 +203,41 @@ def outer_search(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: 
                 trace.append(h)
             if cost == best_cost:
                 stats.expanded_at_best += 1
-            results = s.expand([slot], rule_ids, pp) if rule_ids else []
+            results = s.expand([slot], rule_ids, pp) if rule_ids else np.empty(0, dtype=N.CAND_DTYPE)
+            flags = results["flags"].tolist()
+            hashes = results["hash"].tolist()
+            costs = results["cost"].tolist()
             keep_idx: list[int] = []
             keep_role: list[tuple[bool, bool]] = []
-            for i, r in enumerate(results):
-                if not r.flags & N.F_FIRST:
+            for i, fl in enumerate(flags):
+                if not fl & N.F_FIRST:
                     continue
                 stats.graphs_generated += 1
-                if r.flags & N.F_VISITED:
+                if fl & N.F_VISITED:
                     stats.graphs_deduped += 1
                     continue
-                if r.flags & N.F_CAPPED:
+                if fl & N.F_CAPPED:
                     stats.node_cap_hits += 1
                     continue
+                r = results[i]
                 if profiler is not None:
-                    stats.new_cost_records += visible.touch(r.touched_sig)
-                elif r.flags & N.F_MISSING:
+                    stats.new_cost_records += visible.touch(r["touched_sig"].tolist())
+                elif fl & N.F_MISSING:
                     raise MissingEntry(_missing_text(s, r, db))
-                stats.assignments_evaluated += r.evals
-                stats.inner_sweeps += r.sweeps
+                stats.assignments_evaluated += int(r["evals"])
+                stats.inner_sweeps += int(r["sweeps"])
+                c = costs[i]
                 prev = best_cost
-                new_best = r.cost < prev
+                new_best = c < prev
                 pushed = False
                 if new_best:
-                    best_cost, best_t, best_e = r.cost, r.time_ms, r.energy
+                    best_cost, best_t, best_e = c, float(r["time_ms"]), float(r["energy"])
                     stats.best_updates += 1
-                if r.cost < cfg.alpha * prev:
+                if c < cfg.alpha * prev:
                     if len(heap) >= cfg.max_queue:
                         stats.queue_cap_hits += 1
                     else:
-                        heapq.heappush(heap, (r.cost, r.hash))
+                        heapq.heappush(heap, (c, hashes[i]))
                         pushed = True
                 if new_best or pushed:
                     keep_idx.append(i)
@@ -241,7 +246,7 @@ def outer_search(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: 
             for (new_best, pushed), sl, i in zip(keep_role, slots, keep_idx):
                 run.refs[sl] = 0
                 if pushed:
-                    pending[results[i].hash] = sl
+                    pending[hashes[i]] = sl
                     run.hold(sl)
                 if new_best:
                     run.drop(best_slot)
@@ -383,15 +388,16 @@ class Frontier:
             slots.append(slot)
             res = self.s.expand([slot], self.rule_ids, self.pp, insert_visited=True)
             keep = []
-            for i, r in enumerate(res):
-                if (r.flags & (N.F_FIRST | N.F_VISITED | N.F_CAPPED)) != N.F_FIRST or r.hash in seen:
+            fl, hs, cs = res["flags"].tolist(), res["hash"].tolist(), res["cost"].tolist()
+            for i in range(len(res)):
+                if (fl[i] & (N.F_FIRST | N.F_VISITED | N.F_CAPPED)) != N.F_FIRST or hs[i] in seen:
                     continue
-                if r.cost < cfg.alpha * best:
+                if cs[i] < cfg.alpha * best:
                     keep.append(i)
-                    seen.add(r.hash)
-                best = min(best, r.cost)
+                    seen.add(hs[i])
+                best = min(best, cs[i])
             for i, sl in zip(keep, self.s.keep(keep)):
-                heapq.heappush(heap, (res[i].cost, res[i].hash, sl))
+                heapq.heappush(heap, (cs[i], hs[i], sl))
         # fill the batch with the remaining enqueued graphs in heap order
         while heap and len(slots) < n_parents:
             slots.append(heapq.heappop(heap)[2])

@@ -93,9 +93,9 @@ def scratch_graph(g: Graph, session: DeviceSession | None = None, extra_nodes: i
         s.free(slot)
 
 
-def _site_of(rule_name: str, g_ids: list[int], r: N.CandResult) -> MatchSite:
+def _site_of(rule_name: str, g_ids: list[int], r) -> MatchSite:
     names = _SITE_NAMES[rule_name]
-    vals = (g_ids[r.site_a], g_ids[r.site_b])[: len(names)]
+    vals = (g_ids[int(r["site_a"])], g_ids[int(r["site_b"])])[: len(names)]
     return MatchSite(tuple(sorted(zip(names, vals))))
 
 
@@ -130,7 +130,7 @@ def neighbors(g: Graph, rules: list[SubstitutionRule], session=None) -> list[Gra
     """Every one-step rewrite, first graph per canonical hash (rules.py:73-89)."""
     out = []
     for s, res in _expand_one(g, rules, session):
-        keep = [i for i, r in enumerate(res) if r.flags & N.F_FIRST]
+        keep = [i for i, fl in enumerate(res["flags"].tolist()) if fl & N.F_FIRST]
         slots = s.keep(keep)
         try:
             out = [s.decode(s.read_record(sl), g)[0] for sl in slots]

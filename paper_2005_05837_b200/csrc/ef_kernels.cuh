@@ -1463,17 +1463,67 @@ struct DigestJob {
   uint64_t* out;  // 2 words
 };
 
+// Append a float64 tensor to a BLAKE2b stream.  The header in front of the tensor fixes
+// its byte misalignment s (0..7) for the whole tensor, so once the stream sits at a block
+// boundary every further 128-byte block is 16 funnel-shifted tensor words assembled in
+// registers: one compression plus 16 loads per block instead of 16 generic appends.
+__device__ __forceinline__ void digest_tensor(B2b& st, const unsigned long long* w, uint64_t n) {
+  uint64_t i = 0;
+  while (i < n) {
+    if (st.fill == 128 && n - i >= 16) {
+      // aligned: a full block is pending and at least 16 more words follow it; the next
+      // block's words are loaded before the pending block is compressed (latency hidden)
+      do {
+        uint64_t nx[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) nx[q] = __ldg(w + i + q);
+        st.t += 128;
+        b2b_compress(st.h, st.m, st.t, false);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) st.m[q] = nx[q];
+        i += 16;
+      } while (n - i >= 16);
+      continue;  // the pending block is flushed by the next append or by final()
+    }
+    if (st.fill > 0 && st.fill < 8 && n - i >= 16) {
+      // just crossed a boundary: the block holds the s carried bytes of the previous word
+      const uint32_t s8 = 8 * st.fill, r8 = 64 - s8;
+      uint64_t carry = st.m[0];
+      uint64_t cur[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) cur[q] = __ldg(w + i + q);
+      do {
+        uint64_t mw[16];
+        mw[0] = carry | (cur[0] << s8);
+#pragma unroll
+        for (int q = 1; q < 16; ++q) mw[q] = (cur[q - 1] >> r8) | (cur[q] << s8);
+        carry = cur[15] >> r8;
+        i += 16;
+        if (n - i >= 16) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) cur[q] = __ldg(w + i + q);
+        }
+        st.t += 128;
+        b2b_compress(st.h, mw, st.t, false);  // the carried bytes follow: never the last block
+      } while (n - i >= 16);
+      st.m[0] = carry;
+#pragma unroll
+      for (int q = 1; q < 16; ++q) st.m[q] = 0;
+      continue;
+    }
+    st.word_le(w[i++]);
+  }
+}
+
 __global__ void k_digest(const DigestJob* jobs, uint32_t n) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const DigestJob J = jobs[j];
     B2b st;
     st.init(16);
     st.bytes(J.hdr0, J.hlen0);
-    const unsigned long long* w0 = reinterpret_cast<const unsigned long long*>(J.t0);
-    for (uint64_t i = 0; i < J.n0; ++i) st.word_le(w0[i]);
+    digest_tensor(st, reinterpret_cast<const unsigned long long*>(J.t0), J.n0);
     st.bytes(J.hdr1, J.hlen1);
-    const unsigned long long* w1 = reinterpret_cast<const unsigned long long*>(J.t1);
-    for (uint64_t i = 0; i < J.n1; ++i) st.word_le(w1[i]);
+    digest_tensor(st, reinterpret_cast<const unsigned long long*>(J.t1), J.n1);
     st.final();
     J.out[0] = st.h[0];
     J.out[1] = st.h[1];

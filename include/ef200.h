@@ -122,7 +122,7 @@ typedef struct {
   uint32_t flags, parent;
   uint32_t rule, site_a, site_b; /* positions in the parent */
   uint32_t touched_sig[2];       /* signatures of rewritten nodes (UINT32_MAX: none) */
-  uint32_t pad;
+  uint32_t n_nodes;              /* nodes of the candidate graph */
 } ef_cand_result;
 
 typedef struct ef_ctx ef_ctx;

@@ -53,7 +53,7 @@ class CandResult(C.Structure):
                 ("evals", C.c_int64), ("sweeps", C.c_int32), ("n_compute", C.c_int32),
                 ("flags", C.c_uint32), ("parent", C.c_uint32), ("rule", C.c_uint32),
                 ("site_a", C.c_uint32), ("site_b", C.c_uint32), ("touched_sig", C.c_uint32 * 2),
-                ("pad", C.c_uint32)]
+                ("n_nodes", C.c_uint32)]
 
 
 import numpy as _np
@@ -62,7 +62,7 @@ import numpy as _np
 CAND_DTYPE = _np.dtype([("hash", "<u8"), ("cost", "<f8"), ("time_ms", "<f8"), ("energy", "<f8"),
                         ("evals", "<i8"), ("sweeps", "<i4"), ("n_compute", "<i4"), ("flags", "<u4"),
                         ("parent", "<u4"), ("rule", "<u4"), ("site_a", "<u4"), ("site_b", "<u4"),
-                        ("touched_sig", "<u4", (2,)), ("pad", "<u4")])
+                        ("touched_sig", "<u4", (2,)), ("n_nodes", "<u4")])
 assert CAND_DTYPE.itemsize == C.sizeof(CandResult)
 
 _P = C.c_void_p

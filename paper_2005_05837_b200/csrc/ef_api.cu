@@ -9,8 +9,9 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
-#include "ef_kernels.cuh"
+#include "ef_step.cuh"
 
 using namespace ef;
 
@@ -104,7 +105,7 @@ struct ef_ctx {
   DevBuf<int32_t> d_srcpos, d_req_dv;
   DevBuf<uint8_t> d_seed, d_pmark, d_sort_tmp;
   DevBuf<uint32_t> d_first, d_first_sorted, d_iota, d_order;
-  DevBuf<ef_cand_result> d_res;
+  DevBuf<ef_cand_result> d_res, d_res_aux;
   DevBuf<ef_sig_desc> d_req_sig;
   DevBuf<uint64_t> d_hash_out;
   DevBuf<uint32_t> d_sperm;
@@ -113,6 +114,18 @@ struct ef_ctx {
   uint32_t last_total = 0;
   uint32_t last_req_sig = 0, last_req_dv = 0;
   uint32_t* h_scalars = nullptr;  // pinned: total, err, n_req_sig, n_req_dv, vis_count lo/hi
+
+  // virtual-candidate step (ef_step.cuh)
+  DevBuf<VPlan> d_plan;
+  DevBuf<uint8_t> d_alg8, d_seg_tmp;
+  DevBuf<uint32_t> d_didx, d_refsrc, d_dcount, d_dorder, d_dsorted, d_sval, d_sval2;
+  DevBuf<Job> d_jobs;
+  DevBuf<uint64_t> d_fresh, d_skey, d_skey2;
+  DevBuf<int32_t> d_seg_b, d_seg_e;
+  uint32_t step_S = 0, step_Rs = 0, step_n_parents = 0;
+  StepArgs last_step{};
+  DevBuf<uint32_t> d_sel;
+  DevBuf<unsigned long long> d_dst;
 
   // visited set
   DevBuf<unsigned long long> d_vis, d_vis_count;
@@ -240,11 +253,30 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_iota.release();
   ctx->d_order.release();
   ctx->d_res.release();
+  ctx->d_res_aux.release();
   ctx->d_req_sig.release();
   ctx->d_hash_out.release();
   ctx->d_sperm.release();
   ctx->d_vis.release();
   ctx->d_vis_count.release();
+  ctx->d_plan.release();
+  ctx->d_alg8.release();
+  ctx->d_seg_tmp.release();
+  ctx->d_didx.release();
+  ctx->d_refsrc.release();
+  ctx->d_dcount.release();
+  ctx->d_dorder.release();
+  ctx->d_dsorted.release();
+  ctx->d_sval.release();
+  ctx->d_sval2.release();
+  ctx->d_jobs.release();
+  ctx->d_fresh.release();
+  ctx->d_skey.release();
+  ctx->d_skey2.release();
+  ctx->d_seg_b.release();
+  ctx->d_seg_e.release();
+  ctx->d_sel.release();
+  ctx->d_dst.release();
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
   cudaStreamDestroy(ctx->st);
@@ -464,7 +496,7 @@ int ef_tables_commit(ef_ctx* ctx) {
         (rc = upload(ctx, ctx->d_names, pool)))
       return rc;
     std::vector<uint8_t> it(ctx->input_text.begin(), ctx->input_text.end());
-    it.push_back(0);
+    it.resize(((it.size() + 7) & ~size_t(7)) + 8, 0);  // 8-byte words, zero padded (k_digest)
     if ((rc = upload(ctx, ctx->d_input_text, it))) return rc;
   }
   // derivation table
@@ -795,18 +827,18 @@ int ef_price_records(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const ef_pr
   if (n == 0) return EF_OK;
   int rc = stage_addrs(ctx, ctx->d_addr_a, slots, n);
   if (rc) return rc;
-  EF_CUDA(ctx->d_res.reserve(std::max<size_t>(n, ctx->cand_cap), ctx->st));
-  EF_CUDA(cudaMemsetAsync(ctx->d_res.p, 0, n * sizeof(ef_cand_result), ctx->st));
+  EF_CUDA(ctx->d_res_aux.reserve(n, ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_res_aux.p, 0, n * sizeof(ef_cand_result), ctx->st));
   PriceArgs Pa{};
   Pa.g = ctx->geo;
   Pa.T = make_tables(ctx);
   Pa.pp = *pp;
   Pa.n = n;
   Pa.rec = ctx->d_addr_a.p;
-  Pa.res = ctx->d_res.p;
+  Pa.res = ctx->d_res_aux.p;
   k_price<<<(n + kPriceThreads - 1) / kPriceThreads, kPriceThreads, 0, ctx->st>>>(Pa);
   EF_CUDA(cudaGetLastError());
-  EF_CUDA(cudaMemcpyAsync(out, ctx->d_res.p, n * sizeof(ef_cand_result), cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaMemcpyAsync(out, ctx->d_res_aux.p, n * sizeof(ef_cand_result), cudaMemcpyDeviceToHost, ctx->st));
   EF_CUDA(cudaStreamSynchronize(ctx->st));
   return EF_OK;
 }
@@ -849,42 +881,70 @@ int ef_visited_count(ef_ctx* ctx, uint64_t* count) {
 // the frontier step
 // ---------------------------------------------------------------------------------------------
 
-static int ensure_step_buffers(ef_ctx* ctx, uint32_t n_parents) {
+static int ensure_parent_buffers(ef_ctx* ctx, uint32_t n_parents) {
   const Geo& g = ctx->geo;
   if (ctx->site_cap == 0) ctx->site_cap = std::max<uint32_t>(4 * g.cap_nodes, 256);
-  if (ctx->cand_cap == 0) ctx->cand_cap = std::max<uint32_t>(1024, std::min<uint32_t>(1u << 16, (uint32_t)((1ull << 30) / g.bytes)));
-  const uint64_t pstride = 4ull * g.cap_nodes + 1 + g.cap_refs;
+  const uint64_t pstride = 5ull * g.cap_nodes + 1 + g.cap_refs;
   EF_CUDA(ctx->d_parent_addr.reserve(n_parents, ctx->st));
   EF_CUDA(ctx->d_pscratch.reserve(pstride * n_parents, ctx->st));
   EF_CUDA(ctx->d_sites.reserve((uint64_t)ctx->site_cap * n_parents, ctx->st));
   EF_CUDA(ctx->d_site_count.reserve(n_parents, ctx->st));
   EF_CUDA(ctx->d_cand_off.reserve(n_parents + 1, ctx->st));
-  EF_CUDA(ctx->d_cand.reserve((uint64_t)ctx->cand_cap * g.bytes, ctx->st));
-  EF_CUDA(ctx->d_srcpos.reserve((uint64_t)ctx->cand_cap * g.cap_nodes, ctx->st));
-  EF_CUDA(ctx->d_seed.reserve((uint64_t)ctx->cand_cap * g.cap_nodes, ctx->st));
-  EF_CUDA(ctx->d_pmark.reserve((uint64_t)ctx->cand_cap * g.cap_nodes, ctx->st));
-  EF_CUDA(ctx->d_first.reserve(ctx->cand_cap, ctx->st));
-  EF_CUDA(ctx->d_first_sorted.reserve(ctx->cand_cap, ctx->st));
-  EF_CUDA(ctx->d_order.reserve(ctx->cand_cap, ctx->st));
-  if (ctx->d_iota.cap < ctx->cand_cap) {
-    EF_CUDA(ctx->d_iota.reserve(ctx->cand_cap, ctx->st));
+  EF_CUDA(ctx->d_scalars.reserve(16, ctx->st));
+  return EF_OK;
+}
+
+// candidate-level buffers (whole step) and the per-chunk hashing scratch
+static int ensure_cand_buffers(ef_ctx* ctx, uint32_t total, uint32_t S, uint32_t Rs, uint32_t* chunk) {
+  const uint64_t tcap = pow2_at_least(2ull * std::max<uint32_t>(total, 1024));
+  EF_CUDA(ctx->d_res.reserve(std::max<uint32_t>(total, 1), ctx->st));
+  EF_CUDA(ctx->d_plan.reserve(std::max<uint32_t>(total, 1), ctx->st));
+  EF_CUDA(ctx->d_alg8.reserve((uint64_t)std::max<uint32_t>(total, 1) * S, ctx->st));
+  EF_CUDA(ctx->d_step_key.reserve(tcap, ctx->st));
+  EF_CUDA(ctx->d_step_seq.reserve(tcap, ctx->st));
+  EF_CUDA(ctx->d_req_sig.reserve(ctx->req_cap, ctx->st));
+  EF_CUDA(ctx->d_req_dv.reserve(4 * ctx->req_cap, ctx->st));
+  // chunk: bounded scratch (~1.5 GB) so graphs of any size stream through
+  const uint64_t per = (uint64_t)S * (4 + sizeof(Job) + 16 + 8 + 8 + 4 + 4) + 4ull * Rs + 32;
+  uint64_t ch = std::max<uint64_t>(256, (1536ull << 20) / per);
+  ch = std::min<uint64_t>(ch, std::max<uint32_t>(total, 1));
+  ch = std::min<uint64_t>(ch, (uint64_t)INT32_MAX / S);
+  *chunk = (uint32_t)ch;
+  EF_CUDA(ctx->d_didx.reserve(ch * S, ctx->st));
+  EF_CUDA(ctx->d_jobs.reserve(ch * S, ctx->st));
+  EF_CUDA(ctx->d_refsrc.reserve(ch * Rs, ctx->st));
+  EF_CUDA(ctx->d_fresh.reserve(2 * ch * S, ctx->st));
+  EF_CUDA(ctx->d_skey.reserve(ch * S, ctx->st));
+  EF_CUDA(ctx->d_skey2.reserve(ch * S, ctx->st));
+  EF_CUDA(ctx->d_sval.reserve(ch * S, ctx->st));
+  EF_CUDA(ctx->d_sval2.reserve(ch * S, ctx->st));
+  EF_CUDA(ctx->d_dcount.reserve(ch, ctx->st));
+  EF_CUDA(ctx->d_dsorted.reserve(ch, ctx->st));
+  EF_CUDA(ctx->d_dorder.reserve(ch, ctx->st));
+  EF_CUDA(ctx->d_seg_b.reserve(ch, ctx->st));
+  EF_CUDA(ctx->d_seg_e.reserve(ch, ctx->st));
+  if (ctx->d_iota.cap < ch) {
+    EF_CUDA(ctx->d_iota.reserve(ch, ctx->st));
     std::vector<uint32_t> io(ctx->d_iota.cap);
     for (size_t i = 0; i < io.size(); ++i) io[i] = (uint32_t)i;
     EF_CUDA(cudaMemcpyAsync(ctx->d_iota.p, io.data(), io.size() * 4, cudaMemcpyHostToDevice, ctx->st));
     EF_CUDA(cudaStreamSynchronize(ctx->st));
   }
-  size_t tmp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)ctx->cand_cap, 0, 24);
-  EF_CUDA(ctx->d_sort_tmp.reserve(tmp, ctx->st));
-  EF_CUDA(ctx->d_res.reserve(ctx->cand_cap, ctx->st));
-  uint32_t tcap = pow2_at_least(2ull * ctx->cand_cap);
-  EF_CUDA(ctx->d_step_key.reserve(tcap, ctx->st));
-  EF_CUDA(ctx->d_step_seq.reserve(tcap, ctx->st));
-  EF_CUDA(ctx->d_req_sig.reserve(ctx->req_cap, ctx->st));
-  EF_CUDA(ctx->d_req_dv.reserve(4 * ctx->req_cap, ctx->st));
-  EF_CUDA(ctx->d_scalars.reserve(16, ctx->st));
+  size_t t1 = 0, t2 = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, t1, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                            (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)ch, 0, 32);
+  cub::DeviceSegmentedSort::SortPairs(nullptr, t2, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                      (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)(ch * S), (int)ch,
+                                      (const int32_t*)nullptr, (const int32_t*)nullptr);
+  EF_CUDA(ctx->d_sort_tmp.reserve(t1, ctx->st));
+  EF_CUDA(ctx->d_seg_tmp.reserve(t2, ctx->st));
   return EF_OK;
+}
+
+static uint32_t bits_for(uint32_t v) {
+  uint32_t b = 1;
+  while (b < 32 && (1ull << b) <= v) ++b;
+  return b;
 }
 
 int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, const int32_t* rules, uint32_t n_rules,
@@ -896,7 +956,7 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
   EF_REQUIRE(n_rules <= 8, "at most 8 rules");
   cudaSetDevice(ctx->dev);
   for (int attempt = 0; attempt < 8; ++attempt) {
-    int rc = ensure_step_buffers(ctx, std::max<uint32_t>(n_parents, 1));
+    int rc = ensure_parent_buffers(ctx, std::max<uint32_t>(n_parents, 1));
     if (rc) return rc;
     const Geo& g = ctx->geo;
     if ((rc = stage_addrs(ctx, ctx->d_parent_addr, parent_slots, n_parents))) return rc;
@@ -907,7 +967,7 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     A.parent_addr = ctx->d_parent_addr.p;
     A.n_parents = n_parents;
     A.pscratch = ctx->d_pscratch.p;
-    A.pstride = 4ull * g.cap_nodes + 1 + g.cap_refs;
+    A.pstride = 5ull * g.cap_nodes + 1 + g.cap_refs;
     for (uint32_t i = 0; i < n_rules; ++i) A.rules[i] = rules[i];
     A.n_rules = (int32_t)n_rules;
     A.sites = ctx->d_sites.p;
@@ -918,18 +978,13 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     A.err = ctx->d_scalars.p + 1;
     A.n_req_sig = ctx->d_scalars.p + 2;
     A.n_req_dv = ctx->d_scalars.p + 3;
-    A.cand_base = ctx->d_cand.p;
-    A.cand_cap = ctx->cand_cap;
-    A.cand_srcpos = ctx->d_srcpos.p;
-    A.cand_seed = ctx->d_seed.p;
-    A.cand_pmark = ctx->d_pmark.p;
-    A.cand_first = ctx->d_first.p;
-    A.res = ctx->d_res.p;
+    A.cand_cap = 0xffffffffu;
     A.req_sig = ctx->d_req_sig.p;
     A.req_sig_cap = ctx->req_cap;
     A.req_dv = ctx->d_req_dv.p;
     A.req_dv_cap = ctx->req_cap;
 
+    // 1) match every rule at every node of every parent; candidate offsets; parent sizes
     cudaEventRecord(ctx->ev[0], ctx->st);
     if (n_parents) {
       k_match<kMatchThreads><<<std::min<uint32_t>(n_parents, ctx->n_sm * 8), kMatchThreads, 0, ctx->st>>>(A);
@@ -938,37 +993,75 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     k_offsets<1024><<<1, 1024, 0, ctx->st>>>(A);
     EF_CUDA(cudaGetLastError());
     cudaEventRecord(ctx->ev[1], ctx->st);
-    const uint32_t grid_c = std::min<uint32_t>(ctx->cand_cap, ctx->n_sm * 8);
-    k_materialise<kMatThreads><<<grid_c, kMatThreads, 0, ctx->st>>>(A);
-    EF_CUDA(cudaGetLastError());
-    cudaEventRecord(ctx->ev[2], ctx->st);
-
-    HashArgs H{};
-    H.g = g;
-    H.T = A.T;
-    H.cand_base = ctx->d_cand.p;
-    H.total = A.total;
-    H.parent_addr = A.parent_addr;
-    H.srcpos = A.cand_srcpos;
-    H.seed = A.cand_seed;
-    H.pmark = A.cand_pmark;
-    H.first = A.cand_first;
-    {
-      // lanes take candidates in order of their first dirty slot: warps share similar dirty cones
-      size_t tmp = ctx->d_sort_tmp.cap;
-      k_first_pad<<<std::min<uint32_t>((ctx->cand_cap + 255) / 256, ctx->n_sm * 4), 256, 0, ctx->st>>>(
-          ctx->d_first.p, A.total, ctx->cand_cap);
-      EF_CUDA(cub::DeviceRadixSort::SortPairs(ctx->d_sort_tmp.p, tmp, ctx->d_first.p, ctx->d_first_sorted.p,
-                                              ctx->d_iota.p, ctx->d_order.p, (int)ctx->cand_cap, 0, 24, ctx->st));
-      H.order = ctx->d_order.p;
+    EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
+    EF_CUDA(cudaStreamSynchronize(ctx->st));
+    if (ctx->h_scalars[1] & 1u) {  // site buffer too small
+      ctx->site_cap *= 4;
+      continue;
     }
-    H.res = A.res;
-    H.incremental = 1;
-    H.err = A.err;
-    if ((rc = launch_hash(ctx, H, ctx->cand_cap))) return rc;
+    const uint32_t total = ctx->h_scalars[0];
+    const uint32_t S = (std::max<uint32_t>(ctx->h_scalars[5], 1) + 2 + 3) & ~3u;
+    const uint32_t Rs = ctx->h_scalars[6] + 4;
+    uint32_t chunk = 0;
+    if ((rc = ensure_cand_buffers(ctx, total, S, Rs, &chunk))) return rc;
+    ctx->step_S = S;
+    ctx->step_Rs = Rs;
+    ctx->step_n_parents = n_parents;
+    A.res = ctx->d_res.p;
+
+    // 2) rewrite plans; 3) per chunk: dirty walk, node keys, key sort, graph digest
+    const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));
+    if (total) {
+      k_plan<<<grid_t, 256, 0, ctx->st>>>(A, ctx->d_plan.p);
+      EF_CUDA(cudaGetLastError());
+    }
+    cudaEventRecord(ctx->ev[2], ctx->st);
+    VArgs V{};
+    V.g = g;
+    V.T = A.T;
+    V.parent_addr = A.parent_addr;
+    V.plan = ctx->d_plan.p;
+    V.res = ctx->d_res.p;
+    V.S = S;
+    V.Rs = Rs;
+    V.didx = ctx->d_didx.p;
+    V.jobs = ctx->d_jobs.p;
+    V.refsrc = ctx->d_refsrc.p;
+    V.fresh = ctx->d_fresh.p;
+    V.dcount = ctx->d_dcount.p;
+    V.order = ctx->d_dorder.p;
+    V.skey = ctx->d_skey.p;
+    V.sval = ctx->d_sval.p;
+    V.skey_sorted = ctx->d_skey2.p;
+    V.sval_sorted = ctx->d_sval2.p;
+    V.seg_begin = ctx->d_seg_b.p;
+    V.seg_end = ctx->d_seg_e.p;
+    V.input_words = reinterpret_cast<const uint64_t*>(ctx->d_input_text.p);
+    V.err = A.err;
+    for (uint32_t c0 = 0; c0 < total; c0 += chunk) {
+      V.c0 = c0;
+      V.n = std::min(chunk, total - c0);
+      const uint32_t gd = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 127) / 128, ctx->n_sm * 16));
+      k_dirty<<<gd, 128, 0, ctx->st>>>(V);
+      EF_CUDA(cudaGetLastError());
+      size_t t1 = ctx->d_sort_tmp.cap;
+      EF_CUDA(cub::DeviceRadixSort::SortPairsDescending(ctx->d_sort_tmp.p, t1, ctx->d_dcount.p, ctx->d_dsorted.p,
+                                                        ctx->d_iota.p, ctx->d_dorder.p, (int)V.n, 0, bits_for(S),
+                                                        ctx->st));
+      k_keys<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+      EF_CUDA(cudaGetLastError());
+      size_t t2 = ctx->d_seg_tmp.cap;
+      EF_CUDA(cub::DeviceSegmentedSort::SortPairs(ctx->d_seg_tmp.p, t2, ctx->d_skey.p, ctx->d_skey2.p, ctx->d_sval.p,
+                                                  ctx->d_sval2.p, (int)((uint64_t)V.n * S), (int)V.n, ctx->d_seg_b.p,
+                                                  ctx->d_seg_e.p, ctx->st));
+      k_sortfix<<<gd, 128, 0, ctx->st>>>(V);
+      k_digest<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+      EF_CUDA(cudaGetLastError());
+    }
     cudaEventRecord(ctx->ev[3], ctx->st);
 
-    const uint32_t tcap = pow2_at_least(2ull * ctx->cand_cap);
+    // 4) dedup inside the step and against the visited set
+    const uint32_t tcap = pow2_at_least(2ull * std::max<uint32_t>(total, 1024));
     EF_CUDA(cudaMemsetAsync(ctx->d_step_key.p, 0, (size_t)tcap * 8, ctx->st));
     EF_CUDA(cudaMemsetAsync(ctx->d_step_seq.p, 0xff, (size_t)tcap * 4, ctx->st));
     DedupArgs D{};
@@ -982,43 +1075,36 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     D.vis_count = ctx->d_vis_count.p;
     D.insert_visited = insert_visited;
     D.node_cap = pp->node_cap;
-    const uint32_t grid_t = std::min<uint32_t>((ctx->cand_cap + 255) / 256, ctx->n_sm * 4);
     k_dedup_claim<<<grid_t, 256, 0, ctx->st>>>(D);
     k_dedup_resolve<<<grid_t, 256, 0, ctx->st>>>(D);
     EF_CUDA(cudaGetLastError());
     cudaEventRecord(ctx->ev[4], ctx->st);
 
-    PriceArgs Pa{};
-    Pa.g = g;
-    Pa.T = A.T;
-    Pa.pp = *pp;
-    Pa.total = A.total;
-    Pa.cand_base = ctx->d_cand.p;
-    Pa.res = A.res;
-    Pa.step_mode = 1;
-    k_price<<<std::min<uint32_t>((ctx->cand_cap + kPriceThreads - 1) / kPriceThreads, ctx->n_sm * 8), kPriceThreads, 0,
-              ctx->st>>>(Pa);
+    // 5) inner search on every survivor
+    VPriceArgs Pv{};
+    Pv.pa.g = g;
+    Pv.pa.T = A.T;
+    Pv.pa.pp = *pp;
+    Pv.pa.total = A.total;
+    Pv.pa.res = A.res;
+    Pv.pa.step_mode = 1;
+    Pv.plan = ctx->d_plan.p;
+    Pv.parent_addr = A.parent_addr;
+    Pv.alg8 = ctx->d_alg8.p;
+    Pv.S = S;
+    k_price_v<<<std::max<uint32_t>(1, std::min<uint32_t>((total + kPriceThreads - 1) / kPriceThreads, ctx->n_sm * 8)),
+                kPriceThreads, 0, ctx->st>>>(Pv);
     EF_CUDA(cudaGetLastError());
     cudaEventRecord(ctx->ev[5], ctx->st);
     EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
     EF_CUDA(cudaStreamSynchronize(ctx->st));
-    const uint32_t total = ctx->h_scalars[0], err = ctx->h_scalars[1];
+    const uint32_t err = ctx->h_scalars[1];
     ctx->last_req_sig = ctx->h_scalars[2];
     ctx->last_req_dv = ctx->h_scalars[3];
     for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&ctx->last_ms[k], ctx->ev[k], ctx->ev[k + 1]);
-    if (err & 1u) {  // site buffer too small
-      ctx->site_cap *= 4;
-      continue;
-    }
-    if (err & 2u) {  // candidate arena too small
-      ctx->cand_cap = std::max<uint32_t>(ctx->h_scalars[4] + ctx->h_scalars[4] / 4, ctx->cand_cap * 2);
-      ctx->d_step_key.release();
-      ctx->d_step_seq.release();
-      continue;
-    }
     EF_REQUIRE(!(err & 4u), "candidate exceeds record capacity (raise cap_nodes/cap_refs)");
-    EF_REQUIRE(!(err & 8u), "graph too large for the hash kernel");
     ctx->last_total = total;
+    ctx->last_step = A;
     *n_candidates = total;
     if (ctx->last_req_sig || ctx->last_req_dv) return EF_NEED_RESOLVE;
     if (insert_visited) {
@@ -1053,18 +1139,45 @@ int ef_results(ef_ctx* ctx, ef_cand_result* out, uint32_t n) {
 
 int ef_keep(ef_ctx* ctx, const uint32_t* cand_idx, uint32_t n, const uint32_t* slots) {
   if (!n) return EF_OK;
-  std::vector<unsigned long long> src(n), dst(n);
+  const Geo& g = ctx->geo;
+  std::vector<unsigned long long> dst(n);
   for (uint32_t i = 0; i < n; ++i) {
     EF_REQUIRE(cand_idx[i] < ctx->last_total, "ef_keep: bad candidate index");
     EF_REQUIRE(slots[i] < ctx->n_slots, "ef_keep: bad slot");
-    src[i] = (unsigned long long)(ctx->d_cand.p + (uint64_t)cand_idx[i] * ctx->geo.bytes);
     dst[i] = (unsigned long long)slot_addr(ctx, slots[i]);
   }
+  std::vector<uint32_t> sel(cand_idx, cand_idx + n);
   int rc;
-  if ((rc = upload(ctx, ctx->d_addr_a, src)) || (rc = upload(ctx, ctx->d_addr_b, dst))) return rc;
-  k_copy_records<<<std::min<uint32_t>(n, ctx->n_sm * 4), 256, 0, ctx->st>>>(ctx->d_addr_a.p, ctx->d_addr_b.p, n, ctx->geo.bytes);
+  if ((rc = upload(ctx, ctx->d_dst, dst)) || (rc = upload(ctx, ctx->d_sel, sel))) return rc;
+  EF_CUDA(ctx->d_srcpos.reserve((uint64_t)n * g.cap_nodes, ctx->st));
+  EF_CUDA(ctx->d_seed.reserve((uint64_t)n * g.cap_nodes, ctx->st));
+  EF_CUDA(ctx->d_pmark.reserve((uint64_t)n * g.cap_nodes, ctx->st));
+  // the step's parents, sites and plans are still in place: materialise the chosen candidates
+  StepArgs A = ctx->last_step;
+  A.sel = ctx->d_sel.p;
+  A.n_sel = n;
+  A.dst = ctx->d_dst.p;
+  A.cand_srcpos = ctx->d_srcpos.p;
+  A.cand_seed = ctx->d_seed.p;
+  A.cand_pmark = ctx->d_pmark.p;
+  k_materialise<kMatThreads><<<std::min<uint32_t>(n, ctx->n_sm * 8), kMatThreads, 0, ctx->st>>>(A);
   EF_CUDA(cudaGetLastError());
+  k_keep_alg<<<std::min<uint32_t>(n, ctx->n_sm * 8), 128, 0, ctx->st>>>(ctx->d_alg8.p, ctx->step_S, ctx->d_sel.p,
+                                                                      ctx->d_dst.p, n, g);
+  EF_CUDA(cudaGetLastError());
+  // node keys and sorted-key order of the new records (every parent carries them)
+  EF_CUDA(ctx->d_scalars.reserve(16, ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_scalars.p + 8, 0, 4, ctx->st));
+  HashArgs H{};
+  H.g = g;
+  H.T = make_tables(ctx);
+  H.n = n;
+  H.rec = ctx->d_dst.p;
+  H.err = ctx->d_scalars.p + 8;
+  if ((rc = launch_hash(ctx, H, n))) return rc;
+  EF_CUDA(cudaMemcpyAsync(ctx->h_scalars + 8, ctx->d_scalars.p + 8, 4, cudaMemcpyDeviceToHost, ctx->st));
   EF_CUDA(cudaStreamSynchronize(ctx->st));
+  EF_REQUIRE(ctx->h_scalars[8] == 0, "ef_keep: hash capacity error");
   return EF_OK;
 }
 

@@ -132,7 +132,7 @@ struct StepArgs {
   Tables T;
   const unsigned long long* parent_addr;
   uint32_t n_parents;
-  uint32_t* pscratch;  // per parent: u0[cap] u1[cap] coff[cap+1] ccur[cap] clist[cap_refs]
+  uint32_t* pscratch;  // per parent: u0[cap] u1[cap] coff[cap+1] ccur[cap] clist[cap_refs] tslot[cap]
   uint64_t pstride;    // words per parent
   int32_t rules[8];
   int32_t n_rules;
@@ -155,6 +155,10 @@ struct StepArgs {
   uint32_t* n_req_dv;
   uint32_t req_dv_cap;
   uint32_t* err;  // bit0 site overflow, bit1 candidate overflow, bit2 record capacity, bit3 hash capacity
+  // keep mode of k_materialise: write candidates sel[i] into the records at dst[i]
+  const uint32_t* sel;
+  uint32_t n_sel;
+  const unsigned long long* dst;
 };
 
 __device__ __forceinline__ unsigned long long pack_site(uint32_t rule, uint32_t a, uint32_t b) {
@@ -183,6 +187,11 @@ __global__ void __launch_bounds__(BT) k_match(StepArgs A) {
     uint32_t* coff = u1 + G.cap_nodes;
     uint32_t* ccur = coff + G.cap_nodes + 1;
     uint32_t* clist = ccur + G.cap_nodes;
+    uint32_t* tslot = clist + G.cap_refs;  // inverse topological order (k_plan)
+    {
+      const uint32_t* topo = R.topo(G);
+      for (int s = threadIdx.x; s < n; s += BT) tslot[topo[s]] = (uint32_t)s;
+    }
 
     for (int i = threadIdx.x; i < n; i += BT) u0[i] = u1[i] = ccur[i] = 0;
     __syncthreads();
@@ -309,6 +318,8 @@ __global__ void __launch_bounds__(BT) k_match(StepArgs A) {
     }
     if (base > A.site_cap) overflow = true;
     if (threadIdx.x == 0) {
+      atomicMax(&A.total[5], (uint32_t)n);  // step-wide maxima size the candidate scratch
+      atomicMax(&A.total[6], R.h().n_refs);
       A.site_count[pi] = overflow ? A.site_cap : base;
       if (overflow) atomicOr(A.err, 1u);
     }
@@ -512,8 +523,9 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
   __shared__ Plan P;
   __shared__ uint32_t first_slot;
   const Geo& G = A.g;
-  const uint32_t total = min(A.total[0], A.cand_cap);
-  for (uint32_t c = blockIdx.x; c < total; c += gridDim.x) {
+  const uint32_t total = A.sel ? A.n_sel : min(A.total[0], A.cand_cap);
+  for (uint32_t ci = blockIdx.x; ci < total; ci += gridDim.x) {
+    const uint32_t c = A.sel ? A.sel[ci] : ci;
     // parent of candidate c: last pi with cand_off[pi] <= c
     uint32_t lo = 0, hi = A.n_parents;
     while (hi - lo > 1) {
@@ -525,7 +537,7 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
     const unsigned long long site = A.sites[(uint64_t)pi * A.site_cap + (c - A.cand_off[pi])];
     const uint32_t rule = (uint32_t)(site >> 56), sa = (uint32_t)(site >> 28) & 0xfffffffu, sb = (uint32_t)site & 0xfffffffu;
     Rec R{reinterpret_cast<char*>(A.parent_addr[pi])};
-    Rec C{A.cand_base + (uint64_t)c * G.bytes};
+    Rec C{A.sel ? reinterpret_cast<char*>(A.dst[ci]) : A.cand_base + (uint64_t)c * G.bytes};
     const int n = R.h().n, n_refs = R.h().n_refs, n_out = R.h().n_out;
     const uint32_t* u0 = A.pscratch + (uint64_t)pi * A.pstride;
     const uint32_t* u1 = u0 + G.cap_nodes;
@@ -570,7 +582,7 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
     if (!fits) {
       if (threadIdx.x == 0) {
         atomicOr(A.err, 4u);
-        res->flags = EF_F_INCOMPLETE;
+        if (!A.sel) res->flags = EF_F_INCOMPLETE;
       }
       __syncthreads();
       continue;
@@ -590,8 +602,8 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
       return r;
     };
     auto map_ref = [&](uint32_t r) -> uint32_t { return (cpos(r >> 8) << 8) | (r & 255u); };
-    int32_t* srcpos = A.cand_srcpos + (uint64_t)c * G.cap_nodes;
-    uint8_t* seed = A.cand_seed + (uint64_t)c * G.cap_nodes;
+    int32_t* srcpos = A.cand_srcpos + (uint64_t)ci * G.cap_nodes;
+    uint8_t* seed = A.cand_seed + (uint64_t)ci * G.cap_nodes;
     // nodes
     {
       const int32_t* pnid = R.nid(G);
@@ -604,7 +616,7 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
       uint32_t* cinoff = C.inoff(G);
       const uint64_t* pkeys = R.keys(G);
       uint64_t* ckeys = C.keys(G);
-      uint8_t* pmark = A.cand_pmark + (uint64_t)c * G.cap_nodes;
+      uint8_t* pmark = A.cand_pmark + (uint64_t)ci * G.cap_nodes;
       for (int i = threadIdx.x; i < n; i += BT) {
         pmark[i] = (i == d0 || i == d1) ? 1 : 0;
         if (i == d0 || i == d1) continue;
@@ -725,6 +737,8 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
       H.n_refs = n_refs_child;
       H.n_out = n_out;
       H.n_compute = R.h().n_compute - (n - n_keep) + P.n_live;
+    }
+    if (threadIdx.x == 0 && !A.sel) {
       res->flags = P.incomplete ? EF_F_INCOMPLETE : 0u;
       res->parent = pi;
       res->rule = rule;
@@ -733,7 +747,8 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
       A.cand_first[c] = first_slot;
       res->touched_sig[0] = P.touched[0];
       res->touched_sig[1] = P.touched[1];
-      res->n_compute = H.n_compute;
+      res->n_compute = C.h().n_compute;
+      res->n_nodes = (uint32_t)n_child;
       res->hash = 0;
       res->cost = res->time_ms = res->energy = 0.0;
       res->evals = 0;
@@ -1279,10 +1294,153 @@ struct NeumaierSum {
 
 constexpr int kMaxRadius = 16;
 
-__global__ void k_price(PriceArgs A) {
-  const Geo& G = A.g;
+// the inner search on one graph given as a view: n nodes in id order, sig(i), alg row
+template <class View>
+__device__ void price_graph(const PriceArgs& A, const View& V, uint8_t* alg, ef_cand_result& res) {
   const Tables& T = A.T;
   const ef_price_params& F = A.pp;
+  const int n = V.n;
+  // start: lowest applicable algorithm (row 0) per compute node; Neumaier start totals
+  NeumaierSum st, se;
+  st.init();
+  se.init();
+  int ncomp = 0;
+  for (int i = 0; i < n; ++i) {
+    const uint32_t s = V.sig(i);
+    if (T.sig_desc[s].kind == EF_K_INPUT) continue;
+    ++ncomp;
+    if (T.row_n[s] == 0) {
+      res.flags |= EF_F_MISSING;
+      return;
+    }
+    alg[i] = 0;
+    st.add(T.row_t[T.row_off[s]]);
+    se.add(T.row_e[T.row_off[s]]);
+  }
+  double t_tot = ncomp ? st.result() : 0.0;
+  double e_tot = ncomp ? se.result() : 0.0;
+  double cost = from_totals(F, t_tot, e_tot);
+  long long evals = 0;
+  int sweeps = 0;
+  if (A.pp.use_inner && ncomp > 0) {
+    const int radius = min(min(F.d, ncomp), kMaxRadius);
+    bool changed = true;
+    while (changed) {
+      changed = false;
+      ++sweeps;
+      // k = 1: every node, every alternative (ascending), first improvement
+      for (int i = 0; i < n; ++i) {
+        const uint32_t s = V.sig(i);
+        if (T.sig_desc[s].kind == EF_K_INPUT) continue;
+        const uint32_t nr = T.row_n[s];
+        if (nr < 2) continue;
+        const uint32_t ro = T.row_off[s];
+        const uint32_t start = alg[i];
+        for (uint32_t q = 0; q < nr; ++q) {
+          if (q == start) continue;
+          const uint32_t cur = alg[i];
+          double dt = 0.0, de = 0.0;
+          dt += T.row_t[ro + q] - T.row_t[ro + cur];
+          de += T.row_e[ro + q] - T.row_e[ro + cur];
+          const double cand = from_totals(F, t_tot + dt, e_tot + de);
+          ++evals;
+          if (cand < cost) {
+            alg[i] = (uint8_t)q;
+            t_tot += dt;
+            e_tot += de;
+            cost = cand;
+            changed = true;
+          }
+        }
+      }
+      // k >= 2: itertools.combinations(nids, k) x itertools.product(*alternatives)
+      for (int k = 2; k <= radius; ++k) {
+        int pos[kMaxRadius];
+        int filled = 0;
+        for (int i = 0; i < n && filled < k; ++i)
+          if (T.sig_desc[V.sig(i)].kind != EF_K_INPUT) pos[filled++] = i;
+        while (true) {
+          uint32_t nalt[kMaxRadius], start[kMaxRadius], idx[kMaxRadius], psg[kMaxRadius];
+          bool skip = false;
+          for (int j = 0; j < k; ++j) {
+            psg[j] = V.sig(pos[j]);
+            nalt[j] = T.row_n[psg[j]] - 1;
+            start[j] = alg[pos[j]];
+            idx[j] = 0;
+            if (nalt[j] == 0) skip = true;
+          }
+          if (!skip) {
+            while (true) {
+              double dt = 0.0, de = 0.0;
+              uint32_t choice[kMaxRadius];
+              for (int j = 0; j < k; ++j) {
+                const uint32_t ro = T.row_off[psg[j]];
+                const uint32_t q = idx[j] < start[j] ? idx[j] : idx[j] + 1;
+                choice[j] = q;
+                const uint32_t cur = alg[pos[j]];
+                dt += T.row_t[ro + q] - T.row_t[ro + cur];
+                de += T.row_e[ro + q] - T.row_e[ro + cur];
+              }
+              const double cand = from_totals(F, t_tot + dt, e_tot + de);
+              ++evals;
+              if (cand < cost) {
+                for (int j = 0; j < k; ++j) alg[pos[j]] = (uint8_t)choice[j];
+                t_tot += dt;
+                e_tot += de;
+                cost = cand;
+                changed = true;
+              }
+              int j = k - 1;  // next product index: last position varies fastest
+              while (j >= 0 && ++idx[j] == nalt[j]) idx[j--] = 0;
+              if (j < 0) break;
+            }
+          }
+          // next combination of compute positions (lexicographic)
+          int j = k - 1;
+          bool advanced = false;
+          while (j >= 0) {
+            int q = pos[j] + 1;
+            while (q < n && T.sig_desc[V.sig(q)].kind == EF_K_INPUT) ++q;
+            int room = 0;
+            for (int x = q; x < n && room < k - j; ++x)
+              if (T.sig_desc[V.sig(x)].kind != EF_K_INPUT) ++room;
+            if (q < n && room >= k - j) {
+              pos[j] = q;
+              int f2 = j + 1;
+              for (int x = q + 1; x < n && f2 < k; ++x)
+                if (T.sig_desc[V.sig(x)].kind != EF_K_INPUT) pos[f2++] = x;
+              advanced = true;
+              break;
+            }
+            --j;
+          }
+          if (!advanced) break;
+        }
+      }
+    }
+  }
+  // row index -> algorithm id
+  for (int i = 0; i < n; ++i) {
+    const uint32_t s = V.sig(i);
+    if (T.sig_desc[s].kind == EF_K_INPUT) continue;
+    alg[i] = (uint8_t)T.row_alg[T.row_off[s] + alg[i]];
+  }
+  res.cost = cost;
+  res.time_ms = t_tot;
+  res.energy = e_tot;
+  res.evals = A.pp.use_inner ? evals : 1;
+  res.sweeps = sweeps;
+  res.flags |= EF_F_PRICED;
+}
+
+struct RecView {
+  const uint32_t* s;
+  int n;
+  __device__ __forceinline__ uint32_t sig(int i) const { return s[i]; }
+};
+
+__global__ void k_price(PriceArgs A) {
+  const Geo& G = A.g;
   const uint32_t total = A.total ? A.total[0] : A.n;
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
     ef_cand_result& res = A.res[c];
@@ -1290,150 +1448,8 @@ __global__ void k_price(PriceArgs A) {
       if ((res.flags & (EF_F_INCOMPLETE | EF_F_FIRST | EF_F_VISITED | EF_F_CAPPED)) != EF_F_FIRST) continue;
     }
     Rec R{A.rec ? reinterpret_cast<char*>(A.rec[c]) : A.cand_base + (uint64_t)c * G.bytes};
-    const int n = R.h().n;
-    const uint32_t* sig = R.sig(G);
-    uint8_t* alg = R.alg(G);  // current row index per node during the sweep; alg id at the end
-    // start: lowest applicable algorithm (row 0) per compute node; Neumaier start totals
-    NeumaierSum st, se;
-    st.init();
-    se.init();
-    int ncomp = 0;
-    bool missing = false;
-    for (int i = 0; i < n; ++i) {
-      const uint32_t s = sig[i];
-      if (T.sig_desc[s].kind == EF_K_INPUT) continue;
-      ++ncomp;
-      if (T.row_n[s] == 0) {
-        missing = true;
-        break;
-      }
-      alg[i] = 0;
-      st.add(T.row_t[T.row_off[s]]);
-      se.add(T.row_e[T.row_off[s]]);
-    }
-    if (missing) {
-      res.flags |= EF_F_MISSING;
-      continue;
-    }
-    double t_tot = ncomp ? st.result() : 0.0;
-    double e_tot = ncomp ? se.result() : 0.0;
-    double cost = from_totals(F, t_tot, e_tot);
-    long long evals = 0;
-    int sweeps = 0;
-    if (A.pp.use_inner && ncomp > 0) {
-      const int radius = min(min(F.d, ncomp), kMaxRadius);
-      bool changed = true;
-      while (changed) {
-        changed = false;
-        ++sweeps;
-        // k = 1: every node, every alternative (ascending), first improvement
-        for (int i = 0; i < n; ++i) {
-          const uint32_t s = sig[i];
-          if (T.sig_desc[s].kind == EF_K_INPUT) continue;
-          const uint32_t nr = T.row_n[s];
-          if (nr < 2) continue;
-          const uint32_t ro = T.row_off[s];
-          const uint32_t start = alg[i];
-          for (uint32_t q = 0; q < nr; ++q) {
-            if (q == start) continue;
-            const uint32_t cur = alg[i];
-            double dt = 0.0, de = 0.0;
-            dt += T.row_t[ro + q] - T.row_t[ro + cur];
-            de += T.row_e[ro + q] - T.row_e[ro + cur];
-            const double cand = from_totals(F, t_tot + dt, e_tot + de);
-            ++evals;
-            if (cand < cost) {
-              alg[i] = (uint8_t)q;
-              t_tot += dt;
-              e_tot += de;
-              cost = cand;
-              changed = true;
-            }
-          }
-        }
-        // k >= 2: itertools.combinations(nids, k) x itertools.product(*alternatives)
-        for (int k = 2; k <= radius; ++k) {
-          int pos[kMaxRadius];
-          // first combination: the first k compute positions
-          int filled = 0;
-          for (int i = 0; i < n && filled < k; ++i)
-            if (T.sig_desc[sig[i]].kind != EF_K_INPUT) pos[filled++] = i;
-          while (true) {
-            uint32_t nalt[kMaxRadius], start[kMaxRadius], idx[kMaxRadius];
-            bool skip = false;
-            for (int j = 0; j < k; ++j) {
-              const uint32_t s = sig[pos[j]];
-              nalt[j] = T.row_n[s] - 1;
-              start[j] = alg[pos[j]];
-              idx[j] = 0;
-              if (nalt[j] == 0) skip = true;
-            }
-            if (!skip) {
-              while (true) {
-                double dt = 0.0, de = 0.0;
-                uint32_t choice[kMaxRadius];
-                for (int j = 0; j < k; ++j) {
-                  const uint32_t s = sig[pos[j]];
-                  const uint32_t ro = T.row_off[s];
-                  const uint32_t q = idx[j] < start[j] ? idx[j] : idx[j] + 1;
-                  choice[j] = q;
-                  const uint32_t cur = alg[pos[j]];
-                  dt += T.row_t[ro + q] - T.row_t[ro + cur];
-                  de += T.row_e[ro + q] - T.row_e[ro + cur];
-                }
-                const double cand = from_totals(F, t_tot + dt, e_tot + de);
-                ++evals;
-                if (cand < cost) {
-                  for (int j = 0; j < k; ++j) alg[pos[j]] = (uint8_t)choice[j];
-                  t_tot += dt;
-                  e_tot += de;
-                  cost = cand;
-                  changed = true;
-                }
-                // next product index: last position varies fastest
-                int j = k - 1;
-                while (j >= 0 && ++idx[j] == nalt[j]) idx[j--] = 0;
-                if (j < 0) break;
-              }
-            }
-            // next combination of compute positions (lexicographic)
-            int j = k - 1;
-            bool advanced = false;
-            while (j >= 0) {
-              // next compute position after pos[j] leaving room for the rest
-              int q = pos[j] + 1;
-              while (q < n && T.sig_desc[sig[q]].kind == EF_K_INPUT) ++q;
-              // count compute nodes from q on
-              int room = 0;
-              for (int x = q; x < n && room < k - j; ++x)
-                if (T.sig_desc[sig[x]].kind != EF_K_INPUT) ++room;
-              if (q < n && room >= k - j) {
-                pos[j] = q;
-                int f2 = j + 1;
-                for (int x = q + 1; x < n && f2 < k; ++x)
-                  if (T.sig_desc[sig[x]].kind != EF_K_INPUT) pos[f2++] = x;
-                advanced = true;
-                break;
-              }
-              --j;
-            }
-            if (!advanced) break;
-          }
-        }
-      }
-    }
-    // row index -> algorithm id
-    for (int i = 0; i < n; ++i) {
-      const uint32_t s = sig[i];
-      if (T.sig_desc[s].kind == EF_K_INPUT) continue;
-      alg[i] = (uint8_t)T.row_alg[T.row_off[s] + alg[i]];
-    }
-    res.cost = cost;
-    res.time_ms = t_tot;
-    res.energy = e_tot;
-    res.evals = A.pp.use_inner ? evals : 1;
-    res.sweeps = sweeps;
-    res.flags |= EF_F_PRICED;
+    RecView V{R.sig(G), R.h().n};
+    price_graph(A, V, R.alg(G), res);
   }
 }
 

@@ -1,0 +1,617 @@
+// The frontier step on *virtual candidates*.
+//
+// A candidate is never written out as a record during the step: it is its parent record
+// (resident in HBM, shared by all of the parent's candidates, so L1/L2 serve it) plus a
+// small rewrite plan (VPlan, ~100 bytes).  Only the candidates the search keeps are
+// materialised afterwards (ef_keep).  Per step:
+//
+//   k_plan    thread/candidate  the rewrite plan of rules.py:164-331 in parent coordinates
+//   k_dirty   thread/candidate  walks the parent's topological order from the first slot the
+//                               rewrite can touch and emits one "job" per node whose Merkle key
+//                               (graph.py:530-540) changes: its signature, weight set and the
+//                               source of every producer key (parent key or fresh key j)
+//   sort      cub radix         candidates by job count, so the lanes of a warp run the same
+//                               number of compressions
+//   k_keys    thread/candidate  one BLAKE2b-128 per job; the message is assembled in a
+//                               per-thread shared-memory column, compressed at ONE call site
+//   sort      cub segmented     every candidate's fresh keys by their first 8 bytes
+//   k_sortfix thread/candidate  orders runs of equal first words by the second word
+//   k_digest  thread/candidate  BLAKE2b-64 over input text, output keys and the merge of the
+//                               parent's sorted keys (minus removed ones) with the fresh keys
+//                               (graph.py:541-549)
+// followed by the existing dedup kernels and k_price on the virtual view.
+#pragma once
+#include "ef_kernels.cuh"
+
+namespace ef {
+
+constexpr uint32_t kFresh = 0x80000000u;  // refsrc: key comes from the candidate's fresh keys
+constexpr int kKeyMaxW = 32;              // message words a job may use in the fast path (256 bytes)
+
+// rewrite plan in parent coordinates (positions >= pn are the new nodes pn, pn + 1)
+struct VPlan {
+  int32_t drop0, drop1;  // removed parent positions, ascending (-1: none)
+  int32_t mod;           // parent position rewritten in place (-1: none)
+  uint32_t mod_sig, mod_aux;
+  int32_t live[2];
+  uint32_t new_sig[2], new_aux[2], new_ref[2];
+  int32_t n_rm;
+  uint32_t rm_from[2], rm_to[2];
+  int32_t ins_slot;   // parent topo slot where the new nodes are emitted (-1: none)
+  int32_t ins_after;  // 1: after the node at ins_slot, 0: in place of it (that node is dropped)
+  int32_t first;      // first parent topo slot whose key can change
+  int32_t pn, n_keep, n_live;
+  uint32_t parent;
+};
+
+struct Job {
+  uint32_t sig, aux, roff, nin;
+};
+
+struct VArgs {
+  Geo g;
+  Tables T;
+  const unsigned long long* parent_addr;
+  const VPlan* plan;  // whole step
+  ef_cand_result* res;
+  uint32_t c0, n;     // chunk: candidates [c0, c0 + n)
+  uint32_t S, Rs;     // per-candidate strides: node slots, ref slots
+  uint32_t* didx;     // [n][S]  fresh index + 1 of a dirty node (0: key unchanged)
+  Job* jobs;          // [n][S]
+  uint32_t* refsrc;   // [n][Rs]
+  uint64_t* fresh;    // [n][S][2]
+  uint32_t* dcount;   // [n]
+  const uint32_t* order;  // [n] chunk-local candidate per lane (k_keys)
+  uint64_t* skey;     // [n][S] sort keys (first key word, big endian)
+  uint32_t* sval;     // [n][S] job index
+  const uint64_t* skey_sorted;
+  uint32_t* sval_sorted;
+  int32_t* seg_begin;  // [n]
+  int32_t* seg_end;    // [n]
+  const uint64_t* input_words;  // input text, 8-byte words, zero padded
+  uint32_t* err;
+};
+
+// ------------------------------------------------------------------------------------------
+// k_plan
+// ------------------------------------------------------------------------------------------
+
+__global__ void k_plan(StepArgs A, VPlan* plans) {
+  const Geo& G = A.g;
+  const uint32_t total = min(A.total[0], A.cand_cap);
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = A.n_parents;  // parent: last pi with cand_off[pi] <= c
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (A.cand_off[mid] <= c) lo = mid;
+      else hi = mid;
+    }
+    const uint32_t pi = lo;
+    const unsigned long long site = A.sites[(uint64_t)pi * A.site_cap + (c - A.cand_off[pi])];
+    const uint32_t rule = (uint32_t)(site >> 56), sa = (uint32_t)(site >> 28) & 0xfffffffu, sb = (uint32_t)site & 0xfffffffu;
+    Rec R{reinterpret_cast<char*>(A.parent_addr[pi])};
+    const int n = R.h().n, n_refs = R.h().n_refs;
+    const uint32_t* u0 = A.pscratch + (uint64_t)pi * A.pstride;
+    const uint32_t* u1 = u0 + G.cap_nodes;
+    const uint32_t* tslot = u0 + 4 * G.cap_nodes + 1 + G.cap_refs;
+    Plan P;
+    plan_rewrite(A, P, R, n, rule, sa, sb, u0, u1);
+    VPlan V;
+    V.drop0 = P.drop[0];
+    V.drop1 = P.drop[1];
+    V.mod = P.mod;
+    V.mod_sig = P.mod_sig;
+    V.mod_aux = P.mod_aux;
+    for (int k = 0; k < 2; ++k) {
+      V.live[k] = k < P.n_new ? P.live[k] : 0;
+      V.new_sig[k] = P.new_sig[k];
+      V.new_aux[k] = P.new_aux[k];
+      V.new_ref[k] = P.new_ref[k];
+      V.rm_from[k] = P.rm_from[k];
+      V.rm_to[k] = P.rm_to[k];
+    }
+    V.n_rm = P.n_rm;
+    // insertion point of the new nodes (same placement as k_materialise)
+    const int s0 = V.drop0 >= 0 ? (int)tslot[V.drop0] : n;
+    const int s1 = V.drop1 >= 0 ? (int)tslot[V.drop1] : n;
+    V.ins_slot = -1;
+    V.ins_after = 0;
+    if (P.n_new > 0) {
+      if (rule == EF_R_MERGE_CONVS) {
+        V.ins_slot = min(s0, s1);
+      } else if (P.topo_node >= 0) {
+        V.ins_slot = (int)tslot[P.topo_node];
+        V.ins_after = P.topo_mode == 1 ? 1 : 0;
+      }
+    }
+    int first = min(s0, s1);
+    if (V.mod >= 0) first = min(first, (int)tslot[V.mod]);
+    if (V.ins_slot >= 0) first = min(first, V.ins_slot);
+    V.first = first;
+    V.pn = n;
+    V.n_keep = n - (V.drop0 >= 0) - (V.drop1 >= 0);
+    V.n_live = V.live[0] + V.live[1];
+    V.parent = pi;
+    plans[c] = V;
+
+    int drop_refs = 0;
+    if (V.drop0 >= 0) drop_refs += (int)R.nin(G)[V.drop0];
+    if (V.drop1 >= 0) drop_refs += (int)R.nin(G)[V.drop1];
+    const int n_child = V.n_keep + V.n_live;
+    const int n_refs_child = n_refs - drop_refs + V.n_live;
+    ef_cand_result* res = A.res + c;
+    uint32_t flags = P.incomplete ? EF_F_INCOMPLETE : 0u;
+    if (n_child > (int)G.cap_nodes || n_refs_child > (int)G.cap_refs) {
+      atomicOr(A.err, 4u);
+      flags = EF_F_INCOMPLETE;
+    }
+    res->flags = flags;
+    res->parent = pi;
+    res->rule = rule;
+    res->site_a = sa;
+    res->site_b = sb;
+    res->touched_sig[0] = P.touched[0];
+    res->touched_sig[1] = P.touched[1];
+    res->n_compute = R.h().n_compute - (n - V.n_keep) + V.n_live;
+    res->n_nodes = (uint32_t)n_child;
+    res->hash = 0;
+    res->cost = res->time_ms = res->energy = 0.0;
+    res->evals = 0;
+    res->sweeps = 0;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// k_dirty
+// ------------------------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t vremap(const VPlan& P, uint32_t r) {
+  for (int k = 0; k < P.n_rm; ++k)
+    if (r == P.rm_from[k]) return P.rm_to[k];
+  return r;
+}
+
+__global__ void k_dirty(VArgs A) {
+  const Geo& G = A.g;
+  for (uint32_t lc = blockIdx.x * blockDim.x + threadIdx.x; lc < A.n; lc += gridDim.x * blockDim.x) {
+    const uint32_t c = A.c0 + lc;
+    if (A.res[c].flags & EF_F_INCOMPLETE) {
+      A.dcount[lc] = 0;
+      A.seg_begin[lc] = A.seg_end[lc] = (int32_t)((uint64_t)lc * A.S);
+      continue;
+    }
+    const VPlan P = A.plan[c];
+    Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
+    const uint32_t* topo = R.topo(G);
+    const uint32_t* psig = R.sig(G);
+    const uint32_t* paux = R.aux(G);
+    const uint32_t* pnin = R.nin(G);
+    const uint32_t* pinoff = R.inoff(G);
+    const uint32_t* prefs = R.refs(G);
+    const int pn = P.pn;
+    uint32_t* didx = A.didx + (uint64_t)lc * A.S;
+    Job* jobs = A.jobs + (uint64_t)lc * A.S;
+    uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
+    for (int i = 0; i < pn + 2; ++i) didx[i] = 0;
+    uint32_t j = 0, r = 0;
+    auto src_of = [&](uint32_t ref) -> uint32_t {
+      const uint32_t p = ref >> 8, port = ref & 255u;
+      const uint32_t fi = didx[p];
+      return fi ? (kFresh | (port << 23) | (fi - 1)) : ((port << 23) | p);
+    };
+    auto emit_new = [&]() {
+      for (int k = 0; k < 2; ++k) {
+        if (!P.live[k]) continue;
+        rs[r] = src_of(P.new_ref[k]);  // new nodes are exempt from the remap (rules.py:186-188)
+        jobs[j] = Job{P.new_sig[k], P.new_aux[k], r, 1u};
+        r += 1;
+        didx[pn + k] = ++j;
+      }
+    };
+    for (int s = P.first; s < pn; ++s) {
+      const int v = (int)topo[s];
+      if (v == P.drop0 || v == P.drop1) {
+        if (s == P.ins_slot && !P.ins_after) emit_new();
+        continue;
+      }
+      bool dirty = v == P.mod;
+      const uint32_t r0 = pinoff[v], nr = pnin[v];
+      for (uint32_t k = 0; k < nr; ++k) {
+        const uint32_t ref = prefs[r0 + k];
+        const uint32_t ref2 = vremap(P, ref);
+        const uint32_t sv = src_of(ref2);
+        dirty |= (ref2 != ref) || (sv & kFresh);
+        rs[r + k] = sv;
+      }
+      if (dirty) {
+        jobs[j] = Job{v == P.mod ? P.mod_sig : psig[v], v == P.mod ? P.mod_aux : paux[v], r, nr};
+        r += nr;
+        didx[v] = ++j;
+      }
+      if (s == P.ins_slot && P.ins_after) emit_new();
+    }
+    A.dcount[lc] = j;
+    A.seg_begin[lc] = (int32_t)((uint64_t)lc * A.S);
+    A.seg_end[lc] = (int32_t)((uint64_t)lc * A.S + j);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// message assembly: a byte stream packed into aligned 64-bit words of a per-thread column
+// (word q of thread t at col[q * BT]), so the message can be indexed dynamically while the
+// compression itself runs on registers
+// ------------------------------------------------------------------------------------------
+
+template <int BT>
+struct WordSink {
+  uint64_t* col;
+  uint64_t acc;
+  uint32_t accb;  // bytes pending in acc (0..7)
+  uint32_t q;     // words written
+  __device__ __forceinline__ void init(uint64_t* c) {
+    col = c;
+    acc = 0;
+    accb = 0;
+    q = 0;
+  }
+  // append nb (1..8) bytes given as the low bytes of w (higher bytes zero)
+  __device__ __forceinline__ void push(uint64_t w, uint32_t nb) {
+    if (accb == 0) {
+      if (nb == 8) {
+        col[(q++) * BT] = w;
+      } else {
+        acc = w;
+        accb = nb;
+      }
+      return;
+    }
+    acc |= w << (8 * accb);
+    const uint32_t tot = accb + nb;
+    if (tot >= 8) {
+      col[(q++) * BT] = acc;
+      acc = w >> (8 * (8 - accb));
+      accb = tot - 8;
+    } else {
+      accb = tot;
+    }
+  }
+  __device__ __forceinline__ void flush() {
+    if (accb) {
+      col[(q++) * BT] = acc;
+      acc = 0;
+      accb = 0;
+    }
+  }
+};
+
+__device__ __forceinline__ uint64_t port_be(uint32_t port) { return (uint64_t)((port >> 8) & 255u) | ((uint64_t)(port & 255u) << 8); }
+
+__device__ __forceinline__ void b2b_start(uint64_t* h, int outlen) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) h[i] = b2b_iv(i);
+  h[0] ^= 0x01010000ULL ^ (uint64_t)outlen;
+}
+
+// node key of a job too long for the fast path (rare: many-input concats); streaming BLAKE2b
+__device__ __noinline__ void job_key_slow(const Tables& T, const Job jb, const uint32_t* rs, const uint64_t* pkeys,
+                                          const uint64_t* fresh, uint64_t* out) {
+  B2b st;
+  st.init(16);
+  const uint32_t off = T.sig_text_off[jb.sig], len = T.sig_text_len[jb.sig];
+  const uint64_t* tw = reinterpret_cast<const uint64_t*>(T.sig_text + off);
+  for (uint32_t i = 0; i < (len >> 3); ++i) st.word_le(tw[i]);
+  const uint8_t* tail = T.sig_text + off + 8 * (len >> 3);
+  for (uint32_t i = 0; i < (len & 7u); ++i) st.byte(tail[i]);
+  st.word_le(T.ws_digest[2 * jb.aux]);
+  st.word_le(T.ws_digest[2 * jb.aux + 1]);
+  for (uint32_t k = 0; k < jb.nin; ++k) {
+    const uint32_t sv = rs[jb.roff + k];
+    const uint32_t idx = sv & 0x7fffffu, port = (sv >> 23) & 255u;
+    const uint64_t* kp = (sv & kFresh) ? fresh + 2 * idx : pkeys + 2 * idx;
+    st.word_le(kp[0]);
+    st.word_le(kp[1]);
+    st.u16_be(port);
+  }
+  st.final();
+  out[0] = st.h[0];
+  out[1] = st.h[1];
+}
+
+// ------------------------------------------------------------------------------------------
+// k_keys
+// ------------------------------------------------------------------------------------------
+
+template <int BT>
+__global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
+  __shared__ uint64_t msg[kKeyMaxW * BT];
+  const Geo& G = A.g;
+  const Tables& T = A.T;
+  uint64_t* col = msg + threadIdx.x;
+  for (uint32_t l = blockIdx.x * BT + threadIdx.x; l < A.n; l += gridDim.x * BT) {
+    const uint32_t lc = A.order[l];
+    const uint32_t d = A.dcount[lc];
+    if (d == 0) continue;
+    const uint32_t c = A.c0 + lc;
+    const uint32_t parent = A.plan[c].parent;
+    const uint64_t* pkeys = Rec{reinterpret_cast<char*>(A.parent_addr[parent])}.keys(G);
+    const Job* jobs = A.jobs + (uint64_t)lc * A.S;
+    const uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
+    uint64_t* fresh = A.fresh + 2ull * lc * A.S;
+    uint64_t* skey = A.skey + (uint64_t)lc * A.S;
+    uint32_t* sval = A.sval + (uint64_t)lc * A.S;
+    for (uint32_t jj = 0; jj < d; ++jj) {
+      const Job jb = jobs[jj];
+      const uint32_t tlen = T.sig_text_len[jb.sig];
+      const uint32_t len = tlen + 16u + 18u * jb.nin;
+      uint64_t h[8];
+      if (len > 8u * kKeyMaxW) {
+        job_key_slow(T, jb, rs, pkeys, fresh, h);
+      } else {
+        WordSink<BT> sk;
+        sk.init(col);
+        const uint64_t* tw = reinterpret_cast<const uint64_t*>(T.sig_text + T.sig_text_off[jb.sig]);
+        const uint32_t full = tlen >> 3;
+        for (uint32_t i = 0; i < full; ++i) sk.push(__ldg(tw + i), 8);
+        if (tlen & 7u) sk.push(__ldg(tw + full), tlen & 7u);
+        sk.push(__ldg(T.ws_digest + 2 * jb.aux), 8);
+        sk.push(__ldg(T.ws_digest + 2 * jb.aux + 1), 8);
+        for (uint32_t k = 0; k < jb.nin; ++k) {
+          const uint32_t sv = rs[jb.roff + k];
+          const uint32_t idx = sv & 0x7fffffu, port = (sv >> 23) & 255u;
+          const uint64_t* kp = (sv & kFresh) ? fresh + 2 * idx : pkeys + 2 * idx;
+          sk.push(kp[0], 8);
+          sk.push(kp[1], 8);
+          sk.push(port_be(port), 2);
+        }
+        sk.flush();
+        const uint32_t nb = (len + 127u) >> 7;
+        for (uint32_t q = sk.q; q < 16u * nb; ++q) col[q * BT] = 0;
+        b2b_start(h, 16);
+        for (uint32_t b = 0; b < nb; ++b) {
+          uint64_t m[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) m[i] = col[(16 * b + i) * BT];
+          b2b_compress(h, m, (uint64_t)min(len, 128u * (b + 1)), b + 1 == nb);
+        }
+      }
+      fresh[2 * jj] = h[0];
+      fresh[2 * jj + 1] = h[1];
+      skey[jj] = B2b::bswap64(h[0]);
+      sval[jj] = jj;
+    }
+  }
+}
+
+// runs of equal first words (a 2^-64 event unless the keys are identical) ordered by the second
+__global__ void k_sortfix(VArgs A) {
+  for (uint32_t lc = blockIdx.x * blockDim.x + threadIdx.x; lc < A.n; lc += gridDim.x * blockDim.x) {
+    const uint32_t d = A.dcount[lc];
+    const uint64_t* sk = A.skey_sorted + (uint64_t)lc * A.S;
+    uint32_t* sv = A.sval_sorted + (uint64_t)lc * A.S;
+    const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
+    for (uint32_t i = 0; i + 1 < d;) {
+      if (sk[i] != sk[i + 1]) {
+        ++i;
+        continue;
+      }
+      uint32_t e = i + 1;
+      while (e < d && sk[e] == sk[i]) ++e;
+      for (uint32_t x = i + 1; x < e; ++x) {  // insertion sort of [i, e) by the second word
+        const uint32_t v = sv[x];
+        const uint64_t lv = B2b::bswap64(fresh[2 * v + 1]);
+        uint32_t y = x;
+        while (y > i && B2b::bswap64(fresh[2 * sv[y - 1] + 1]) > lv) {
+          sv[y] = sv[y - 1];
+          --y;
+        }
+        sv[y] = v;
+      }
+      i = e;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// k_digest
+// ------------------------------------------------------------------------------------------
+
+template <int BT>
+__global__ void __launch_bounds__(BT) k_digest(VArgs A) {
+  __shared__ uint64_t blk[16 * BT];
+  const Geo& G = A.g;
+  const Tables& T = A.T;
+  uint64_t* col = blk + threadIdx.x;
+  for (uint32_t lc = blockIdx.x * BT + threadIdx.x; lc < A.n; lc += gridDim.x * BT) {
+    const uint32_t c = A.c0 + lc;
+    if (A.res[c].flags & EF_F_INCOMPLETE) continue;
+    const VPlan P = A.plan[c];
+    Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
+    const uint64_t* pkeys = R.keys(G);
+    const uint32_t* porder = R.sperm(G);
+    const uint32_t* pouts = R.outs(G);
+    const int n_out = R.h().n_out;
+    const int pn = P.pn;
+    const uint32_t* didx = A.didx + (uint64_t)lc * A.S;
+    const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
+    const uint32_t* fs = A.sval_sorted + (uint64_t)lc * A.S;
+    const uint32_t d = A.dcount[lc];
+    const uint32_t li = T.input_text_len;
+    const uint32_t n_child = (uint32_t)(P.n_keep + P.n_live);
+    const uint64_t len = (uint64_t)li + 18ull * n_out + 16ull * n_child;
+    const uint32_t nblk = (uint32_t)((len + 127) >> 7);
+
+    // generator state
+    int phase = 0;
+    uint32_t gi = 0, part = 0;
+    uint32_t pi = 0, fk = 0;   // merge cursors: parent sorted order, fresh sorted list
+    uint64_t cw0 = 0, cw1 = 0;  // current key's raw words
+    auto key_of = [&](uint32_t ref, uint64_t& w0, uint64_t& w1) {
+      const uint32_t p = ref >> 8;
+      const uint32_t fi = didx[p];
+      if (fi) {
+        w0 = fresh[2 * (fi - 1)];
+        w1 = fresh[2 * (fi - 1) + 1];
+      } else {
+        w0 = pkeys[2 * p];
+        w1 = pkeys[2 * p + 1];
+      }
+    };
+    WordSink<BT> sk;
+    sk.init(col);
+    uint64_t h[8];
+    b2b_start(h, 8);
+    for (uint32_t b = 0; b < nblk; ++b) {
+      sk.q = 0;
+      while (sk.q < 16 && phase < 3) {
+        if (phase == 0) {  // input declarations "name=dims;" (graph.py:542-543)
+          if (gi * 8 < li) {
+            const uint32_t nb = min(8u, li - gi * 8);
+            sk.push(__ldg(A.input_words + gi), nb);
+            ++gi;
+          } else {
+            phase = 1;
+            gi = 0;
+            part = 0;
+          }
+        } else if (phase == 1) {  // outputs: key + port (graph.py:544-546)
+          if ((int)gi < n_out) {
+            const uint32_t ref = vremap(P, pouts[gi]);
+            if (part == 0) {
+              key_of(ref, cw0, cw1);
+              sk.push(cw0, 8);
+              part = 1;
+            } else if (part == 1) {
+              sk.push(cw1, 8);
+              part = 2;
+            } else {
+              sk.push(port_be(ref & 255u), 2);
+              part = 0;
+              ++gi;
+            }
+          } else {
+            phase = 2;
+            part = 0;
+          }
+        } else {  // sorted node keys (graph.py:547-548): merge parent order with fresh keys
+          if (part == 0) {
+            while (pi < (uint32_t)pn) {
+              const uint32_t v = porder[pi];
+              if ((int)v == P.drop0 || (int)v == P.drop1 || didx[v]) {
+                ++pi;
+                continue;
+              }
+              break;
+            }
+            const bool have_p = pi < (uint32_t)pn, have_f = fk < d;
+            if (!have_p && !have_f) {
+              phase = 3;
+              continue;
+            }
+            bool take_f = !have_p;
+            uint64_t f0 = 0, f1 = 0;
+            if (have_f) {
+              const uint32_t fj = fs[fk];
+              f0 = fresh[2 * fj];
+              f1 = fresh[2 * fj + 1];
+              if (have_p) {
+                const uint32_t v = porder[pi];
+                const uint64_t a = B2b::bswap64(pkeys[2 * v]), bb = B2b::bswap64(f0);
+                take_f = bb < a || (bb == a && B2b::bswap64(f1) < B2b::bswap64(pkeys[2 * v + 1]));
+              }
+            }
+            if (take_f) {
+              cw0 = f0;
+              cw1 = f1;
+              ++fk;
+            } else {
+              const uint32_t v = porder[pi];
+              cw0 = pkeys[2 * v];
+              cw1 = pkeys[2 * v + 1];
+              ++pi;
+            }
+            sk.push(cw0, 8);
+            part = 1;
+          } else {
+            sk.push(cw1, 8);
+            part = 0;
+          }
+        }
+      }
+      if (phase == 3) {
+        sk.flush();
+        for (uint32_t q = sk.q; q < 16; ++q) col[q * BT] = 0;
+      }
+      uint64_t m[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) m[i] = col[i * BT];
+      b2b_compress(h, m, len < 128ull * (b + 1) ? len : 128ull * (b + 1), b + 1 == nblk);
+    }
+    A.res[c].hash = B2b::bswap64(h[0]);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// the inner search on a virtual candidate: child nodes in id order are the parent positions
+// minus the dropped ones (the rewritten node with its new signature), then the new nodes
+// (their ids are max + 1, max + 2: rules.py:129-131)
+// ------------------------------------------------------------------------------------------
+
+struct VirtView {
+  const uint32_t* psig;
+  int32_t drop0, drop1, mod, n_keep;
+  uint32_t mod_sig, s_new0, s_new1;
+  int n;
+  __device__ __forceinline__ uint32_t sig(int i) const {
+    if (i < n_keep) {
+      int pp = i;
+      if (drop0 >= 0 && pp >= drop0) ++pp;
+      if (drop1 >= 0 && pp >= drop1) ++pp;
+      return pp == mod ? mod_sig : psig[pp];
+    }
+    return i == n_keep ? s_new0 : s_new1;
+  }
+};
+
+struct VPriceArgs {
+  PriceArgs pa;
+  const VPlan* plan;
+  const unsigned long long* parent_addr;
+  uint8_t* alg8;  // [total][S]: assignment per child node of every priced candidate
+  uint32_t S;
+};
+
+__global__ void k_price_v(VPriceArgs A) {
+  const Geo& G = A.pa.g;
+  const uint32_t total = A.pa.total[0];
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
+    ef_cand_result& res = A.pa.res[c];
+    if ((res.flags & (EF_F_INCOMPLETE | EF_F_FIRST | EF_F_VISITED | EF_F_CAPPED)) != EF_F_FIRST) continue;
+    const VPlan& P = A.plan[c];
+    Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
+    VirtView V;
+    V.psig = R.sig(G);
+    V.drop0 = P.drop0;
+    V.drop1 = P.drop1;
+    V.mod = P.mod;
+    V.n_keep = P.n_keep;
+    V.mod_sig = P.mod_sig;
+    V.s_new0 = P.live[0] ? P.new_sig[0] : P.new_sig[1];
+    V.s_new1 = P.new_sig[1];
+    V.n = P.n_keep + P.n_live;
+    price_graph(A.pa, V, A.alg8 + (uint64_t)c * A.S, res);
+  }
+}
+
+// copy the priced assignment of kept candidates into their materialised records
+__global__ void k_keep_alg(const uint8_t* alg8, uint32_t S, const uint32_t* cand, const unsigned long long* dst,
+                           uint32_t n, Geo G) {
+  for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
+    Rec C{reinterpret_cast<char*>(dst[k])};
+    const int nn = C.h().n;
+    const uint8_t* src = alg8 + (uint64_t)cand[k] * S;
+    uint8_t* out = C.alg(G);
+    for (int i = threadIdx.x; i < nn; i += blockDim.x) out[i] = src[i];
+  }
+}
+
+}  // namespace ef

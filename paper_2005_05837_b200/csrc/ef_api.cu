@@ -979,10 +979,6 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     A.n_req_sig = ctx->d_scalars.p + 2;
     A.n_req_dv = ctx->d_scalars.p + 3;
     A.cand_cap = 0xffffffffu;
-    A.req_sig = ctx->d_req_sig.p;
-    A.req_sig_cap = ctx->req_cap;
-    A.req_dv = ctx->d_req_dv.p;
-    A.req_dv_cap = ctx->req_cap;
 
     // 1) match every rule at every node of every parent; candidate offsets; parent sizes
     cudaEventRecord(ctx->ev[0], ctx->st);
@@ -1008,6 +1004,10 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     ctx->step_Rs = Rs;
     ctx->step_n_parents = n_parents;
     A.res = ctx->d_res.p;
+    A.req_sig = ctx->d_req_sig.p;
+    A.req_sig_cap = ctx->req_cap;
+    A.req_dv = ctx->d_req_dv.p;
+    A.req_dv_cap = ctx->req_cap;
 
     // 2) rewrite plans; 3) per chunk: dirty walk, node keys, key sort, graph digest
     const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));

@@ -941,6 +941,30 @@ static int ensure_cand_buffers(ef_ctx* ctx, uint32_t total, uint32_t S, uint32_t
   return EF_OK;
 }
 
+// every candidate's fresh keys in ascending order: warp bitonic sort in shared memory for
+// rows up to 1024 keys, cub's segmented sort (plus the tie fix) beyond
+static int sort_fresh_keys(ef_ctx* ctx, const VArgs& V) {
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 7) / 8, ctx->n_sm * 32));
+  if (V.S <= 128) {
+    k_sortkeys<128, 8><<<grid, 256, 0, ctx->st>>>(V);
+  } else if (V.S <= 256) {
+    k_sortkeys<256, 8><<<grid, 256, 0, ctx->st>>>(V);
+  } else if (V.S <= 512) {
+    k_sortkeys<512, 8><<<grid, 256, 0, ctx->st>>>(V);
+  } else if (V.S <= 1024) {
+    k_sortkeys<1024, 4><<<std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 32)), 128, 0, ctx->st>>>(V);
+  } else {
+    size_t t2 = ctx->d_seg_tmp.cap;
+    EF_CUDA(cub::DeviceSegmentedSort::SortPairs(ctx->d_seg_tmp.p, t2, ctx->d_skey.p, ctx->d_skey2.p, ctx->d_sval.p,
+                                                ctx->d_sval2.p, (int)((uint64_t)V.n * V.S), (int)V.n, ctx->d_seg_b.p,
+                                                ctx->d_seg_e.p, ctx->st));
+    const uint32_t gd = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 127) / 128, ctx->n_sm * 16));
+    k_sortfix<<<gd, 128, 0, ctx->st>>>(V);
+  }
+  EF_CUDA(cudaGetLastError());
+  return EF_OK;
+}
+
 static uint32_t bits_for(uint32_t v) {
   uint32_t b = 1;
   while (b < 32 && (1ull << b) <= v) ++b;
@@ -1050,11 +1074,7 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
                                                         ctx->st));
       k_keys<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
       EF_CUDA(cudaGetLastError());
-      size_t t2 = ctx->d_seg_tmp.cap;
-      EF_CUDA(cub::DeviceSegmentedSort::SortPairs(ctx->d_seg_tmp.p, t2, ctx->d_skey.p, ctx->d_skey2.p, ctx->d_sval.p,
-                                                  ctx->d_sval2.p, (int)((uint64_t)V.n * S), (int)V.n, ctx->d_seg_b.p,
-                                                  ctx->d_seg_e.p, ctx->st));
-      k_sortfix<<<gd, 128, 0, ctx->st>>>(V);
+      if ((rc = sort_fresh_keys(ctx, V))) return rc;
       k_digest<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
       EF_CUDA(cudaGetLastError());
     }

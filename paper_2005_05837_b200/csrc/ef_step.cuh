@@ -382,6 +382,80 @@ __global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
   }
 }
 
+// Sort every candidate's fresh keys: one warp per candidate, bitonic network over M
+// (a power of two >= the step's row length) in shared memory on the keys' first word
+// (big endian), carrying the job index; runs of equal first words (a 2^-64 event unless
+// the keys are identical) are then ordered by the second word.
+template <int M, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_sortkeys(VArgs A) {
+  __shared__ uint64_t sk_all[WARPS * M];
+  __shared__ uint32_t sv_all[WARPS * M];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint64_t* sk = sk_all + w * M;
+  uint32_t* sv = sv_all + w * M;
+  for (uint32_t lc = blockIdx.x * WARPS + w; lc < A.n; lc += gridDim.x * WARPS) {
+    const uint32_t d = A.dcount[lc];
+    if (d == 0) continue;
+    uint32_t m = 2;
+    while (m < d) m <<= 1;
+    const uint64_t* src = A.skey + (uint64_t)lc * A.S;
+    for (uint32_t i = lane; i < m; i += 32) {
+      sk[i] = i < d ? src[i] : ~0ULL;
+      sv[i] = i;
+    }
+    __syncwarp();
+    for (uint32_t k = 2; k <= m; k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = lane; i < m; i += 32) {
+          const uint32_t ixj = i ^ j;
+          if (ixj > i) {
+            const uint64_t a = sk[i], b = sk[ixj];
+            const bool up = (i & k) == 0;
+            if ((a > b) == up) {
+              sk[i] = b;
+              sk[ixj] = a;
+              const uint32_t t = sv[i];
+              sv[i] = sv[ixj];
+              sv[ixj] = t;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    bool tie = false;
+    for (uint32_t i = lane; i + 1 < d; i += 32) tie |= sk[i] == sk[i + 1];
+    if (__any_sync(0xffffffffu, tie)) {
+      if (lane == 0) {
+        const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
+        for (uint32_t i = 0; i + 1 < d;) {
+          if (sk[i] != sk[i + 1]) {
+            ++i;
+            continue;
+          }
+          uint32_t e = i + 1;
+          while (e < d && sk[e] == sk[i]) ++e;
+          for (uint32_t x = i + 1; x < e; ++x) {
+            const uint32_t v = sv[x];
+            const uint64_t lv = B2b::bswap64(fresh[2 * v + 1]);
+            uint32_t y = x;
+            while (y > i && B2b::bswap64(fresh[2 * sv[y - 1] + 1]) > lv) {
+              sv[y] = sv[y - 1];
+              --y;
+            }
+            sv[y] = v;
+          }
+          i = e;
+        }
+      }
+      __syncwarp();
+    }
+    uint32_t* dst = A.sval_sorted + (uint64_t)lc * A.S;
+    for (uint32_t i = lane; i < d; i += 32) dst[i] = sv[i];
+    __syncwarp();
+  }
+}
+
 // runs of equal first words (a 2^-64 event unless the keys are identical) ordered by the second
 __global__ void k_sortfix(VArgs A) {
   for (uint32_t lc = blockIdx.x * blockDim.x + threadIdx.x; lc < A.n; lc += gridDim.x * blockDim.x) {

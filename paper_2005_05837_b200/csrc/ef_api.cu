@@ -117,6 +117,7 @@ struct ef_ctx {
 
   // virtual-candidate step (ef_step.cuh)
   DevBuf<VPlan> d_plan;
+  DevBuf<uint32_t> d_plist, d_sig_info;
   DevBuf<uint8_t> d_alg8, d_seg_tmp;
   DevBuf<uint32_t> d_didx, d_refsrc, d_dcount, d_dorder, d_dsorted, d_sval, d_sval2;
   DevBuf<Job> d_jobs;
@@ -155,6 +156,7 @@ struct ef_ctx {
 static Tables make_tables(ef_ctx* ctx) {
   Tables T{};
   T.sig_desc = ctx->d_sig_desc.p;
+  T.sig_info = reinterpret_cast<const uint2*>(ctx->d_sig_info.p);
   T.sig_text_off = ctx->d_text_off.p;
   T.sig_text_len = ctx->d_text_len.p;
   T.sig_text = ctx->d_text.p;
@@ -260,6 +262,8 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_vis.release();
   ctx->d_vis_count.release();
   ctx->d_plan.release();
+  ctx->d_plist.release();
+  ctx->d_sig_info.release();
   ctx->d_alg8.release();
   ctx->d_seg_tmp.release();
   ctx->d_didx.release();
@@ -458,6 +462,14 @@ int ef_tables_commit(ef_ctx* ctx) {
       (rc = upload(ctx, ctx->d_row_alg, ralg)) || (rc = upload(ctx, ctx->d_row_t, rt)) ||
       (rc = upload(ctx, ctx->d_row_e, re)))
     return rc;
+  {
+    std::vector<uint32_t> info(2 * std::max<size_t>(ns, 1), 0);
+    for (size_t i = 0; i < ns; ++i) {
+      info[2 * i] = roff[i];
+      info[2 * i + 1] = rn[i] | (ctx->sig_desc[i].kind == EF_K_INPUT ? 0x80000000u : 0u);
+    }
+    if ((rc = upload(ctx, ctx->d_sig_info, info))) return rc;
+  }
   // exact-signature lookup table
   {
     uint32_t cap = pow2_at_least(2 * ns + 2);
@@ -899,6 +911,7 @@ static int ensure_cand_buffers(ef_ctx* ctx, uint32_t total, uint32_t S, uint32_t
   const uint64_t tcap = pow2_at_least(2ull * std::max<uint32_t>(total, 1024));
   EF_CUDA(ctx->d_res.reserve(std::max<uint32_t>(total, 1), ctx->st));
   EF_CUDA(ctx->d_plan.reserve(std::max<uint32_t>(total, 1), ctx->st));
+  EF_CUDA(ctx->d_plist.reserve(std::max<uint32_t>(total, 1), ctx->st));
   EF_CUDA(ctx->d_alg8.reserve((uint64_t)std::max<uint32_t>(total, 1) * S, ctx->st));
   EF_CUDA(ctx->d_step_key.reserve(tcap, ctx->st));
   EF_CUDA(ctx->d_step_seq.reserve(tcap, ctx->st));
@@ -1062,6 +1075,7 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     V.seg_end = ctx->d_seg_e.p;
     V.input_words = reinterpret_cast<const uint64_t*>(ctx->d_input_text.p);
     V.err = A.err;
+    V.one = 1;
     for (uint32_t c0 = 0; c0 < total; c0 += chunk) {
       V.c0 = c0;
       V.n = std::min(chunk, total - c0);
@@ -1095,6 +1109,8 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     D.vis_count = ctx->d_vis_count.p;
     D.insert_visited = insert_visited;
     D.node_cap = pp->node_cap;
+    D.plist = ctx->d_plist.p;
+    D.plist_n = ctx->d_scalars.p + 7;
     k_dedup_claim<<<grid_t, 256, 0, ctx->st>>>(D);
     k_dedup_resolve<<<grid_t, 256, 0, ctx->st>>>(D);
     EF_CUDA(cudaGetLastError());
@@ -1112,9 +1128,18 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     Pv.parent_addr = A.parent_addr;
     Pv.alg8 = ctx->d_alg8.p;
     Pv.S = S;
-    k_price_v<<<std::max<uint32_t>(1, std::min<uint32_t>((total + kPriceThreads - 1) / kPriceThreads, ctx->n_sm * 8)),
-                kPriceThreads, 0, ctx->st>>>(Pv);
-    EF_CUDA(cudaGetLastError());
+    {
+      const uint32_t gp = std::max<uint32_t>(1, std::min<uint32_t>((total + kPriceThreads - 1) / kPriceThreads, ctx->n_sm * 16));
+      const uint32_t* pl = ctx->d_plist.p;
+      const uint32_t* pn = ctx->d_scalars.p + 7;
+      const bool fast = pp->use_inner && pp->d == 1;
+      if (fast && pp->kind == EF_C_ENERGY) k_price_v<EF_C_ENERGY><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
+      else if (fast && pp->kind == EF_C_TIME) k_price_v<EF_C_TIME><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
+      else if (fast && pp->kind == EF_C_LINEAR) k_price_v<EF_C_LINEAR><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
+      else if (fast) k_price_v<EF_C_MIX + 1><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
+      else k_price_v<-1><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
+      EF_CUDA(cudaGetLastError());
+    }
     cudaEventRecord(ctx->ev[5], ctx->st);
     EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
     EF_CUDA(cudaStreamSynchronize(ctx->st));

@@ -36,6 +36,7 @@ struct Rec {
 // read-only tables, passed by value to kernels
 struct Tables {
   const ef_sig_desc* sig_desc;
+  const uint2* sig_info;  // per signature: {row_off, row_n | is_input << 31} (pricing)
   const uint32_t* sig_text_off;
   const uint32_t* sig_text_len;
   const uint8_t* sig_text;

@@ -1141,6 +1141,8 @@ struct DedupArgs {
   unsigned long long* vis_count;
   int insert_visited;
   int node_cap;
+  uint32_t* plist;    // survivors to price (appended in k_dedup_resolve), may be null
+  uint32_t* plist_n;
 };
 
 __global__ void k_dedup_claim(DedupArgs A) {
@@ -1170,24 +1172,41 @@ __device__ __forceinline__ bool vis_contains(const unsigned long long* keys, uin
 
 __global__ void k_dedup_resolve(DedupArgs A) {
   const uint32_t total = A.total[0];
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
-    ef_cand_result& r = A.res[c];
-    if (r.flags & EF_F_INCOMPLETE) continue;
-    unsigned long long h = r.hash;
-    unsigned long long key = h ? h : 0x8000000000000000ULL;
-    uint32_t first_seq = 0xffffffffu;
-    for (uint32_t s = (uint32_t)mix64(h) & A.step_mask;; s = (s + 1) & A.step_mask) {
-      if (A.step_key[s] == key) {
-        first_seq = A.step_seq[s];
-        break;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t span = (total + blockDim.x - 1) / blockDim.x * blockDim.x;  // whole warps iterate together
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < span; c += gridDim.x * blockDim.x) {
+    bool survivor = false;
+    if (c < total) {
+      ef_cand_result& r = A.res[c];
+      if (!(r.flags & EF_F_INCOMPLETE)) {
+        unsigned long long h = r.hash;
+        unsigned long long key = h ? h : 0x8000000000000000ULL;
+        uint32_t first_seq = 0xffffffffu;
+        for (uint32_t s = (uint32_t)mix64(h) & A.step_mask;; s = (s + 1) & A.step_mask) {
+          if (A.step_key[s] == key) {
+            first_seq = A.step_seq[s];
+            break;
+          }
+        }
+        uint32_t f = r.flags;
+        if (first_seq == c) f |= EF_F_FIRST;
+        bool seen = vis_contains(A.vis_key, A.vis_mask, key, h);
+        if (seen) f |= EF_F_VISITED;
+        if (r.n_compute > A.node_cap) f |= EF_F_CAPPED;
+        r.flags = f;
+        survivor = (f & (EF_F_FIRST | EF_F_VISITED | EF_F_CAPPED)) == EF_F_FIRST;
       }
     }
-    uint32_t f = r.flags;
-    if (first_seq == c) f |= EF_F_FIRST;
-    bool seen = vis_contains(A.vis_key, A.vis_mask, key, h);
-    if (seen) f |= EF_F_VISITED;
-    if (r.n_compute > A.node_cap) f |= EF_F_CAPPED;
-    r.flags = f;
+    if (A.plist) {  // warp-aggregated append keeps neighbouring candidates (same parent) together
+      const unsigned m = __ballot_sync(__activemask(), survivor);
+      if (m) {
+        uint32_t base = 0;
+        const int leader = __ffs(m) - 1;
+        if ((int)lane == leader) base = atomicAdd(A.plist_n, (uint32_t)__popc(m));
+        base = __shfl_sync(__activemask(), base, leader);
+        if (survivor) A.plist[base + __popc(m & ((1u << lane) - 1u))] = c;
+      }
+    }
   }
 }
 
@@ -1429,6 +1448,93 @@ __device__ void price_graph(const PriceArgs& A, const View& V, uint8_t* alg, ef_
   res.time_ms = t_tot;
   res.energy = e_tot;
   res.evals = A.pp.use_inner ? evals : 1;
+  res.sweeps = sweeps;
+  res.flags |= EF_F_PRICED;
+}
+
+template <int KIND>
+__device__ __forceinline__ double cost_of(const ef_price_params& f, double time_ms, double energy) {
+  if (KIND == EF_C_TIME) return time_ms;
+  if (KIND == EF_C_ENERGY) return energy;
+  if (KIND == EF_C_LINEAR) {
+    const double t = time_ms / f.t_ref, e = energy / f.e_ref;
+    return f.w * e + (1.0 - f.w) * t;
+  }
+  return from_totals(f, time_ms, energy);
+}
+
+// the d = 1 sweep (search.py:106-153 with radius 1) specialised on the cost kind; same
+// floating-point operations in the same order as price_graph / the reference
+template <int KIND, class View>
+__device__ void price_d1(const PriceArgs& A, const View& V, uint8_t* alg, ef_cand_result& res) {
+  const Tables& T = A.T;
+  const ef_price_params& F = A.pp;
+  const int n = V.n;
+  NeumaierSum st, se;
+  st.init();
+  se.init();
+  int ncomp = 0;
+  for (int i = 0; i < n; ++i) {
+    const uint2 info = T.sig_info[V.sig(i)];
+    if (info.y >> 31) continue;
+    ++ncomp;
+    if (info.y == 0) {
+      res.flags |= EF_F_MISSING;
+      return;
+    }
+    alg[i] = 0;
+    st.add(T.row_t[info.x]);
+    se.add(T.row_e[info.x]);
+  }
+  double t_tot = ncomp ? st.result() : 0.0;
+  double e_tot = ncomp ? se.result() : 0.0;
+  double cost = cost_of<KIND>(F, t_tot, e_tot);
+  long long evals = 0;
+  int sweeps = 0;
+  if (ncomp > 0) {
+    bool changed = true;
+    while (changed) {
+      changed = false;
+      ++sweeps;
+      for (int i = 0; i < n; ++i) {
+        const uint2 info = T.sig_info[V.sig(i)];
+        const uint32_t nr = info.y;  // input rows have bit 31 set: skipped by the test below
+        if (nr < 2u || (nr >> 31)) continue;
+        const uint32_t ro = info.x;
+        const uint32_t start = alg[i];
+        uint32_t cur = start;
+        double ct = T.row_t[ro + cur], ce = T.row_e[ro + cur];
+        for (uint32_t q = 0; q < nr; ++q) {
+          if (q == start) continue;
+          const double qt = T.row_t[ro + q], qe = T.row_e[ro + q];
+          double dt = 0.0, de = 0.0;
+          dt += qt - ct;
+          de += qe - ce;
+          const double cand = cost_of<KIND>(F, t_tot + dt, e_tot + de);
+          ++evals;
+          if (cand < cost) {
+            cur = q;
+            ct = qt;
+            ce = qe;
+            t_tot += dt;
+            e_tot += de;
+            cost = cand;
+            changed = true;
+          }
+        }
+        alg[i] = (uint8_t)cur;
+      }
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    const uint2 info = T.sig_info[V.sig(i)];
+    if (info.y >> 31) continue;
+    alg[i] = (uint8_t)T.row_alg[info.x + alg[i]];
+  }
+  res.cost = cost;
+  res.time_ms = t_tot;
+  res.energy = e_tot;
+  res.evals = evals;
   res.sweeps = sweeps;
   res.flags |= EF_F_PRICED;
 }

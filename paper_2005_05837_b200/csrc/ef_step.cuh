@@ -21,6 +21,7 @@
 //                               (graph.py:541-549)
 // followed by the existing dedup kernels and k_price on the virtual view.
 #pragma once
+#include "ef_b2b_fma.cuh"
 #include "ef_kernels.cuh"
 
 namespace ef {
@@ -70,6 +71,7 @@ struct VArgs {
   int32_t* seg_end;    // [n]
   const uint64_t* input_words;  // input text, 8-byte words, zero padded
   uint32_t* err;
+  uint32_t one;  // == 1 at run time (keeps BLAKE2b additions on IMAD, see ef_b2b_fma.cuh)
 };
 
 // ------------------------------------------------------------------------------------------
@@ -371,7 +373,7 @@ __global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
           uint64_t m[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) m[i] = col[(16 * b + i) * BT];
-          b2b_compress(h, m, (uint64_t)min(len, 128u * (b + 1)), b + 1 == nb);
+          b2b_compress_fma(h, m, (uint64_t)min(len, 128u * (b + 1)), b + 1 == nb, A.one);
         }
       }
       fresh[2 * jj] = h[0];
@@ -618,7 +620,7 @@ __global__ void __launch_bounds__(BT) k_digest(VArgs A) {
       uint64_t m[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) m[i] = col[i * BT];
-      b2b_compress(h, m, len < 128ull * (b + 1) ? len : 128ull * (b + 1), b + 1 == nblk);
+      b2b_compress_fma(h, m, len < 128ull * (b + 1) ? len : 128ull * (b + 1), b + 1 == nblk, A.one);
     }
     A.res[c].hash = B2b::bswap64(h[0]);
   }
@@ -654,12 +656,14 @@ struct VPriceArgs {
   uint32_t S;
 };
 
-__global__ void k_price_v(VPriceArgs A) {
+// one thread per survivor of the step's dedup (the compacted list); KIND < 0: any cost kind / radius
+template <int KIND>
+__global__ void k_price_v(VPriceArgs A, const uint32_t* plist, const uint32_t* plist_n) {
   const Geo& G = A.pa.g;
-  const uint32_t total = A.pa.total[0];
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
+  const uint32_t total = *plist_n;
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    const uint32_t c = plist[k];
     ef_cand_result& res = A.pa.res[c];
-    if ((res.flags & (EF_F_INCOMPLETE | EF_F_FIRST | EF_F_VISITED | EF_F_CAPPED)) != EF_F_FIRST) continue;
     const VPlan& P = A.plan[c];
     Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
     VirtView V;
@@ -672,7 +676,9 @@ __global__ void k_price_v(VPriceArgs A) {
     V.s_new0 = P.live[0] ? P.new_sig[0] : P.new_sig[1];
     V.s_new1 = P.new_sig[1];
     V.n = P.n_keep + P.n_live;
-    price_graph(A.pa, V, A.alg8 + (uint64_t)c * A.S, res);
+    uint8_t* alg = A.alg8 + (uint64_t)c * A.S;
+    if (KIND >= 0) price_d1<KIND>(A.pa, V, alg, res);
+    else price_graph(A.pa, V, alg, res);
   }
 }
 

@@ -3,7 +3,9 @@
 // SHF); the high halves of the 64-bit additions go to the FMA pipe as IMAD with a run-time
 // multiplier `one` (== 1, which ptxas cannot fold back into IADD3).  Measured on the SASS of
 // one compression: 1938 ALU-pipe + 1212 FMA-pipe instructions versus 2230 + 325 for the plain
-// 64-bit formulation; both pipes issue at half rate, so the ALU pipe remains the bound.
+// 64-bit formulation -- yet tools/b2b_peak measures 6.1e9 compressions/s for this variant
+// against 8.0e9 for the plain one on a B200, so the kernels use the plain one; this variant is
+// kept for the microbenchmark.
 #pragma once
 #include <stdint.h>
 namespace ef {

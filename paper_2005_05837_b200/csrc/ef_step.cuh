@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
           uint64_t m[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) m[i] = col[(16 * b + i) * BT];
-          b2b_compress_fma(h, m, (uint64_t)min(len, 128u * (b + 1)), b + 1 == nb, A.one);
+          b2b_compress(h, m, (uint64_t)min(len, 128u * (b + 1)), b + 1 == nb);
         }
       }
       fresh[2 * jj] = h[0];
@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(BT) k_digest(VArgs A) {
       uint64_t m[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) m[i] = col[i * BT];
-      b2b_compress_fma(h, m, len < 128ull * (b + 1) ? len : 128ull * (b + 1), b + 1 == nblk, A.one);
+      b2b_compress(h, m, len < 128ull * (b + 1) ? len : 128ull * (b + 1), b + 1 == nblk);
     }
     A.res[c].hash = B2b::bswap64(h[0]);
   }

@@ -74,7 +74,7 @@ typedef struct {
   uint32_t cap_nodes, cap_refs, cap_outs;
   uint32_t record_bytes;                        /* total slot size            */
   uint32_t off_nid, off_sig, off_aux, off_nin;  /* byte offsets of the arrays  */
-  uint32_t off_inoff, off_topo, off_refs, off_outs, off_keys, off_alg, off_sperm;
+  uint32_t off_inoff, off_topo, off_refs, off_outs, off_keys, off_alg, off_sperm, off_skeys, off_srank;
 } ef_geometry;
 
 /* Record header (first 64 bytes of a slot). */
@@ -94,6 +94,8 @@ typedef struct {
  *   uint8  keys[cap_nodes][16] Merkle node keys (graph.py:528-540)
  *   uint8  alg[cap_nodes]      algorithm per node after pricing
  *   uint32 sperm[cap_nodes]    positions in ascending key order (sorted(keys) of graph.py:547)
+ *   uint8  skeys[cap_nodes][16] the node keys in that order (streamed by the step's graph digest)
+ *   uint32 srank[cap_nodes]    rank of each position in that order (inverse of sperm)
  */
 
 /* Pricing parameters: cost function (cost.py:234-254) + inner search (search.py:106-153). */

@@ -39,7 +39,8 @@ class SigDesc(C.Structure):
 class Geometry(C.Structure):
     _fields_ = [(n, C.c_uint32) for n in (
         "cap_nodes", "cap_refs", "cap_outs", "record_bytes", "off_nid", "off_sig", "off_aux", "off_nin",
-        "off_inoff", "off_topo", "off_refs", "off_outs", "off_keys", "off_alg", "off_sperm")]
+        "off_inoff", "off_topo", "off_refs", "off_outs", "off_keys", "off_alg", "off_sperm", "off_skeys",
+        "off_srank")]
 
 
 class PriceParams(C.Structure):

@@ -121,7 +121,8 @@ struct ef_ctx {
   DevBuf<uint8_t> d_alg8, d_seg_tmp;
   DevBuf<uint32_t> d_didx, d_refsrc, d_dcount, d_dorder, d_dsorted, d_sval, d_sval2;
   DevBuf<Job> d_jobs;
-  DevBuf<uint64_t> d_fresh, d_skey, d_skey2;
+  DevBuf<uint64_t> d_fresh, d_fresh2, d_skey, d_skey2;
+  DevBuf<uint32_t> d_rmask;
   DevBuf<int32_t> d_seg_b, d_seg_e;
   uint32_t step_S = 0, step_Rs = 0, step_n_parents = 0;
   StepArgs last_step{};
@@ -275,6 +276,8 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_sval2.release();
   ctx->d_jobs.release();
   ctx->d_fresh.release();
+  ctx->d_fresh2.release();
+  ctx->d_rmask.release();
   ctx->d_skey.release();
   ctx->d_skey2.release();
   ctx->d_seg_b.release();
@@ -690,6 +693,10 @@ int ef_set_geometry(ef_ctx* ctx, uint32_t cap_nodes, uint32_t cap_refs, uint32_t
   o = al(o + cap_nodes);
   g.o_sperm = o;
   o = al(o + 4 * cap_nodes);
+  g.o_skeys = o;
+  o = al(o + 16 * cap_nodes);
+  g.o_srank = o;
+  o = al(o + 4 * cap_nodes);
   g.bytes = o;
   ctx->slots_per_chunk = std::max<uint32_t>(1, (uint32_t)((64ull << 20) / g.bytes));
   ctx->input_text.assign(input_text ? input_text : "", input_text ? input_text_len : 0);
@@ -711,6 +718,8 @@ int ef_set_geometry(ef_ctx* ctx, uint32_t cap_nodes, uint32_t cap_refs, uint32_t
     out->off_keys = g.o_keys;
     out->off_alg = g.o_alg;
     out->off_sperm = g.o_sperm;
+    out->off_skeys = g.o_skeys;
+    out->off_srank = g.o_srank;
   }
   return EF_OK;
 }
@@ -918,7 +927,7 @@ static int ensure_cand_buffers(ef_ctx* ctx, uint32_t total, uint32_t S, uint32_t
   EF_CUDA(ctx->d_req_sig.reserve(ctx->req_cap, ctx->st));
   EF_CUDA(ctx->d_req_dv.reserve(4 * ctx->req_cap, ctx->st));
   // chunk: bounded scratch (~1.5 GB) so graphs of any size stream through
-  const uint64_t per = (uint64_t)S * (4 + sizeof(Job) + 16 + 8 + 8 + 4 + 4) + 4ull * Rs + 32;
+  const uint64_t per = (uint64_t)S * (4 + sizeof(Job) + 16 + 16 + 8 + 8 + 4 + 4) + 4ull * Rs + 4ull * (S + 31) / 32 + 32;
   uint64_t ch = std::max<uint64_t>(256, (1536ull << 20) / per);
   ch = std::min<uint64_t>(ch, std::max<uint32_t>(total, 1));
   ch = std::min<uint64_t>(ch, (uint64_t)INT32_MAX / S);
@@ -927,6 +936,8 @@ static int ensure_cand_buffers(ef_ctx* ctx, uint32_t total, uint32_t S, uint32_t
   EF_CUDA(ctx->d_jobs.reserve(ch * S, ctx->st));
   EF_CUDA(ctx->d_refsrc.reserve(ch * Rs, ctx->st));
   EF_CUDA(ctx->d_fresh.reserve(2 * ch * S, ctx->st));
+  EF_CUDA(ctx->d_fresh2.reserve(2 * ch * S, ctx->st));
+  EF_CUDA(ctx->d_rmask.reserve(ch * ((S + 31) / 32), ctx->st));
   EF_CUDA(ctx->d_skey.reserve(ch * S, ctx->st));
   EF_CUDA(ctx->d_skey2.reserve(ch * S, ctx->st));
   EF_CUDA(ctx->d_sval.reserve(ch * S, ctx->st));
@@ -1073,6 +1084,9 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     V.sval_sorted = ctx->d_sval2.p;
     V.seg_begin = ctx->d_seg_b.p;
     V.seg_end = ctx->d_seg_e.p;
+    V.W = (S + 31) / 32;
+    V.rmask = ctx->d_rmask.p;
+    V.fresh_sorted = ctx->d_fresh2.p;
     V.input_words = reinterpret_cast<const uint64_t*>(ctx->d_input_text.p);
     V.err = A.err;
     V.one = 1;

@@ -14,7 +14,7 @@ constexpr uint32_t kEmptyWset = 0;       // weight-set id of "no weights"
 // record geometry (byte offsets inside one slot); mirrors ef_geometry
 struct Geo {
   uint32_t cap_nodes, cap_refs, cap_outs, bytes;
-  uint32_t o_nid, o_sig, o_aux, o_nin, o_inoff, o_topo, o_refs, o_outs, o_keys, o_alg, o_sperm;
+  uint32_t o_nid, o_sig, o_aux, o_nin, o_inoff, o_topo, o_refs, o_outs, o_keys, o_alg, o_sperm, o_skeys, o_srank;
 };
 
 struct Rec {
@@ -31,6 +31,8 @@ struct Rec {
   __host__ __device__ uint64_t* keys(const Geo& g) const { return reinterpret_cast<uint64_t*>(p + g.o_keys); }
   __host__ __device__ uint8_t* alg(const Geo& g) const { return reinterpret_cast<uint8_t*>(p + g.o_alg); }
   __host__ __device__ uint32_t* sperm(const Geo& g) const { return reinterpret_cast<uint32_t*>(p + g.o_sperm); }
+  __host__ __device__ uint64_t* skeys(const Geo& g) const { return reinterpret_cast<uint64_t*>(p + g.o_skeys); }
+  __host__ __device__ uint32_t* srank(const Geo& g) const { return reinterpret_cast<uint32_t*>(p + g.o_srank); }
 };
 
 // read-only tables, passed by value to kernels

@@ -1064,10 +1064,16 @@ __global__ void __launch_bounds__(32) k_hash_top(HashArgs A) {
       }
       if (!A.incremental) {
         const uint32_t* order = R.sperm(G);
+        uint64_t* skeys = R.skeys(G);
+        uint32_t* srank = R.srank(G);
         for (int i = 0; i < n; ++i) {
           const uint32_t v = order[i];
-          st.word_le(keys[2 * v]);
-          st.word_le(keys[2 * v + 1]);
+          const uint64_t k0 = keys[2 * v], k1 = keys[2 * v + 1];
+          skeys[2 * i] = k0;
+          skeys[2 * i + 1] = k1;
+          srank[v] = (uint32_t)i;
+          st.word_le(k0);
+          st.word_le(k1);
         }
       } else {
         const ef_cand_result& rr = A.res[c];
@@ -1504,23 +1510,23 @@ __device__ void price_d1(const PriceArgs& A, const View& V, uint8_t* alg, ef_can
         const uint32_t start = alg[i];
         uint32_t cur = start;
         double ct = T.row_t[ro + cur], ce = T.row_e[ro + cur];
-        for (uint32_t q = 0; q < nr; ++q) {
-          if (q == start) continue;
+        for (uint32_t q = 0; q < nr; ++q) {  // branch-free: lanes of a warp stay converged
           const double qt = T.row_t[ro + q], qe = T.row_e[ro + q];
           double dt = 0.0, de = 0.0;
           dt += qt - ct;
           de += qe - ce;
-          const double cand = cost_of<KIND>(F, t_tot + dt, e_tot + de);
-          ++evals;
-          if (cand < cost) {
-            cur = q;
-            ct = qt;
-            ce = qe;
-            t_tot += dt;
-            e_tot += de;
-            cost = cand;
-            changed = true;
-          }
+          const double nt = t_tot + dt, ne = e_tot + de;
+          const double cand = cost_of<KIND>(F, nt, ne);
+          const bool act = q != start;
+          evals += act ? 1 : 0;
+          const bool take = act && cand < cost;
+          cur = take ? q : cur;
+          ct = take ? qt : ct;
+          ce = take ? qe : ce;
+          t_tot = take ? nt : t_tot;
+          e_tot = take ? ne : e_tot;
+          cost = take ? cand : cost;
+          changed = changed || take;
         }
         alg[i] = (uint8_t)cur;
       }

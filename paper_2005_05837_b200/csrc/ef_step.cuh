@@ -69,6 +69,9 @@ struct VArgs {
   uint32_t* sval_sorted;
   int32_t* seg_begin;  // [n]
   int32_t* seg_end;    // [n]
+  uint32_t W;          // words per removed-mask row
+  uint32_t* rmask;     // [n][W] parent keys (by sorted rank) absent from the candidate: dropped or dirty
+  uint64_t* fresh_sorted;  // [n][S][2] the fresh keys in ascending byte order
   const uint64_t* input_words;  // input text, 8-byte words, zero padded
   uint32_t* err;
   uint32_t one;  // == 1 at run time (keeps BLAKE2b additions on IMAD, see ef_b2b_fma.cuh)
@@ -195,6 +198,15 @@ __global__ void k_dirty(VArgs A) {
     Job* jobs = A.jobs + (uint64_t)lc * A.S;
     uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
     for (int i = 0; i < pn + 2; ++i) didx[i] = 0;
+    const uint32_t* srank = R.srank(G);
+    uint32_t* rm = A.rmask + (uint64_t)lc * A.W;
+    for (int w = 0; w < (pn + 31) / 32; ++w) rm[w] = 0;
+    auto remove = [&](int v) {
+      const uint32_t k = srank[v];
+      rm[k >> 5] |= 1u << (k & 31);
+    };
+    if (P.drop0 >= 0) remove(P.drop0);
+    if (P.drop1 >= 0) remove(P.drop1);
     uint32_t j = 0, r = 0;
     auto src_of = [&](uint32_t ref) -> uint32_t {
       const uint32_t p = ref >> 8, port = ref & 255u;
@@ -229,6 +241,7 @@ __global__ void k_dirty(VArgs A) {
         jobs[j] = Job{v == P.mod ? P.mod_sig : psig[v], v == P.mod ? P.mod_aux : paux[v], r, nr};
         r += nr;
         didx[v] = ++j;
+        remove(v);
       }
       if (s == P.ins_slot && P.ins_after) emit_new();
     }
@@ -452,8 +465,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_sortkeys(VArgs A) {
       }
       __syncwarp();
     }
-    uint32_t* dst = A.sval_sorted + (uint64_t)lc * A.S;
-    for (uint32_t i = lane; i < d; i += 32) dst[i] = sv[i];
+    const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
+    uint64_t* dst = A.fresh_sorted + 2ull * lc * A.S;
+    for (uint32_t i = lane; i < d; i += 32) {
+      const uint32_t v = sv[i];
+      dst[2 * i] = fresh[2 * v];
+      dst[2 * i + 1] = fresh[2 * v + 1];
+    }
     __syncwarp();
   }
 }
@@ -484,6 +502,11 @@ __global__ void k_sortfix(VArgs A) {
       }
       i = e;
     }
+    uint64_t* dst = A.fresh_sorted + 2ull * lc * A.S;
+    for (uint32_t i = 0; i < d; ++i) {
+      dst[2 * i] = fresh[2 * sv[i]];
+      dst[2 * i + 1] = fresh[2 * sv[i] + 1];
+    }
   }
 }
 
@@ -503,13 +526,11 @@ __global__ void __launch_bounds__(BT) k_digest(VArgs A) {
     const VPlan P = A.plan[c];
     Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
     const uint64_t* pkeys = R.keys(G);
-    const uint32_t* porder = R.sperm(G);
     const uint32_t* pouts = R.outs(G);
     const int n_out = R.h().n_out;
     const int pn = P.pn;
     const uint32_t* didx = A.didx + (uint64_t)lc * A.S;
     const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
-    const uint32_t* fs = A.sval_sorted + (uint64_t)lc * A.S;
     const uint32_t d = A.dcount[lc];
     const uint32_t li = T.input_text_len;
     const uint32_t n_child = (uint32_t)(P.n_keep + P.n_live);
@@ -519,8 +540,44 @@ __global__ void __launch_bounds__(BT) k_digest(VArgs A) {
     // generator state
     int phase = 0;
     uint32_t gi = 0, part = 0;
-    uint32_t pi = 0, fk = 0;   // merge cursors: parent sorted order, fresh sorted list
     uint64_t cw0 = 0, cw1 = 0;  // current key's raw words
+    // merge streams: the parent's keys in sorted order minus the removed ranks, and the fresh
+    // keys in sorted order; the heads are loaded as soon as a stream advances
+    const uint64_t* pskeys = R.skeys(G);
+    const uint32_t* rm = A.rmask + (uint64_t)lc * A.W;
+    const uint64_t* fsk = A.fresh_sorted + 2ull * lc * A.S;
+    uint32_t pi = 0, fk = 0, mw_idx = 0xffffffffu, mw = 0;
+    uint64_t ph0 = 0, ph1 = 0, fh0 = 0, fh1 = 0;
+    bool have_p = false, have_f = false;
+    auto next_p = [&]() {
+      while (pi < (uint32_t)pn) {
+        if ((pi >> 5) != mw_idx) {
+          mw_idx = pi >> 5;
+          mw = rm[mw_idx];
+        }
+        const uint32_t rest = mw >> (pi & 31);
+        if (rest == 0xffffffffu >> (pi & 31) && (pi | 31) < (uint32_t)pn) {  // whole tail removed
+          pi = (pi | 31) + 1;
+          continue;
+        }
+        if (!(rest & 1u)) break;
+        ++pi;
+      }
+      have_p = pi < (uint32_t)pn;
+      if (have_p) {
+        ph0 = pskeys[2 * pi];
+        ph1 = pskeys[2 * pi + 1];
+      }
+    };
+    auto next_f = [&]() {
+      have_f = fk < d;
+      if (have_f) {
+        fh0 = fsk[2 * fk];
+        fh1 = fsk[2 * fk + 1];
+      }
+    };
+    next_p();
+    next_f();
     auto key_of = [&](uint32_t ref, uint64_t& w0, uint64_t& w1) {
       const uint32_t p = ref >> 8;
       const uint32_t fi = didx[p];
@@ -568,42 +625,27 @@ __global__ void __launch_bounds__(BT) k_digest(VArgs A) {
             phase = 2;
             part = 0;
           }
-        } else {  // sorted node keys (graph.py:547-548): merge parent order with fresh keys
+        } else {  // sorted node keys (graph.py:547-548): merge of two ascending streams
           if (part == 0) {
-            while (pi < (uint32_t)pn) {
-              const uint32_t v = porder[pi];
-              if ((int)v == P.drop0 || (int)v == P.drop1 || didx[v]) {
-                ++pi;
-                continue;
-              }
-              break;
-            }
-            const bool have_p = pi < (uint32_t)pn, have_f = fk < d;
             if (!have_p && !have_f) {
               phase = 3;
               continue;
             }
             bool take_f = !have_p;
-            uint64_t f0 = 0, f1 = 0;
-            if (have_f) {
-              const uint32_t fj = fs[fk];
-              f0 = fresh[2 * fj];
-              f1 = fresh[2 * fj + 1];
-              if (have_p) {
-                const uint32_t v = porder[pi];
-                const uint64_t a = B2b::bswap64(pkeys[2 * v]), bb = B2b::bswap64(f0);
-                take_f = bb < a || (bb == a && B2b::bswap64(f1) < B2b::bswap64(pkeys[2 * v + 1]));
-              }
+            if (have_f && have_p) {
+              const uint64_t a = B2b::bswap64(ph0), bb = B2b::bswap64(fh0);
+              take_f = bb < a || (bb == a && B2b::bswap64(fh1) < B2b::bswap64(ph1));
             }
             if (take_f) {
-              cw0 = f0;
-              cw1 = f1;
+              cw0 = fh0;
+              cw1 = fh1;
               ++fk;
+              next_f();
             } else {
-              const uint32_t v = porder[pi];
-              cw0 = pkeys[2 * v];
-              cw1 = pkeys[2 * v + 1];
+              cw0 = ph0;
+              cw1 = ph1;
               ++pi;
+              next_p();
             }
             sk.push(cw0, 8);
             part = 1;

@@ -926,9 +926,9 @@ static int ensure_cand_buffers(ef_ctx* ctx, uint32_t total, uint32_t S, uint32_t
   EF_CUDA(ctx->d_step_seq.reserve(tcap, ctx->st));
   EF_CUDA(ctx->d_req_sig.reserve(ctx->req_cap, ctx->st));
   EF_CUDA(ctx->d_req_dv.reserve(4 * ctx->req_cap, ctx->st));
-  // chunk: bounded scratch (~1.5 GB) so graphs of any size stream through
+  // chunk: bounded scratch so graphs of any size stream through
   const uint64_t per = (uint64_t)S * (4 + sizeof(Job) + 16 + 16 + 8 + 8 + 4 + 4) + 4ull * Rs + 4ull * (S + 31) / 32 + 32;
-  uint64_t ch = std::max<uint64_t>(256, (1536ull << 20) / per);
+  uint64_t ch = std::max<uint64_t>(256, (6144ull << 20) / per);  // <= 6 GiB of the 180 GB
   ch = std::min<uint64_t>(ch, std::max<uint32_t>(total, 1));
   ch = std::min<uint64_t>(ch, (uint64_t)INT32_MAX / S);
   *chunk = (uint32_t)ch;

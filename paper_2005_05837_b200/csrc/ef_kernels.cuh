@@ -1469,68 +1469,80 @@ __device__ __forceinline__ double cost_of(const ef_price_params& f, double time_
   return from_totals(f, time_ms, energy);
 }
 
-// the d = 1 sweep (search.py:106-153 with radius 1) specialised on the cost kind; same
-// floating-point operations in the same order as price_graph / the reference
+// The d = 1 sweep (search.py:106-153 with radius 1) specialised on the cost kind: the same
+// floating-point operations in the same order as price_graph / the reference.  Written
+// warp-synchronously: every loop runs a warp-uniform trip count (the lanes of `mask` price
+// different candidates whose node counts differ by a few), with no early exits, so the warp
+// never splits into groups that would then run the whole sweep one after another.
 template <int KIND, class View>
-__device__ void price_d1(const PriceArgs& A, const View& V, uint8_t* alg, ef_cand_result& res) {
+__device__ void price_d1(const PriceArgs& A, const View& V, uint8_t* alg, ef_cand_result& res, unsigned mask) {
   const Tables& T = A.T;
   const ef_price_params& F = A.pp;
   const int n = V.n;
+  const int nmax = __reduce_max_sync(mask, (unsigned)n);
   NeumaierSum st, se;
   st.init();
   se.init();
   int ncomp = 0;
-  for (int i = 0; i < n; ++i) {
-    const uint2 info = T.sig_info[V.sig(i)];
-    if (info.y >> 31) continue;
-    ++ncomp;
-    if (info.y == 0) {
-      res.flags |= EF_F_MISSING;
-      return;
+  bool missing = false;
+  for (int i = 0; i < nmax; ++i) {
+    if (i < n && !missing) {
+      const uint2 info = T.sig_info[V.sig(i)];
+      if (!(info.y >> 31)) {
+        ++ncomp;
+        if (info.y == 0) {
+          missing = true;
+        } else {
+          alg[i] = 0;
+          st.add(T.row_t[info.x]);
+          se.add(T.row_e[info.x]);
+        }
+      }
     }
-    alg[i] = 0;
-    st.add(T.row_t[info.x]);
-    se.add(T.row_e[info.x]);
   }
   double t_tot = ncomp ? st.result() : 0.0;
   double e_tot = ncomp ? se.result() : 0.0;
   double cost = cost_of<KIND>(F, t_tot, e_tot);
   long long evals = 0;
   int sweeps = 0;
-  if (ncomp > 0) {
-    bool changed = true;
-    while (changed) {
-      changed = false;
-      ++sweeps;
-      for (int i = 0; i < n; ++i) {
-        const uint2 info = T.sig_info[V.sig(i)];
-        const uint32_t nr = info.y;  // input rows have bit 31 set: skipped by the test below
-        if (nr < 2u || (nr >> 31)) continue;
-        const uint32_t ro = info.x;
-        const uint32_t start = alg[i];
-        uint32_t cur = start;
-        double ct = T.row_t[ro + cur], ce = T.row_e[ro + cur];
-        for (uint32_t q = 0; q < nr; ++q) {  // branch-free: lanes of a warp stay converged
-          const double qt = T.row_t[ro + q], qe = T.row_e[ro + q];
-          double dt = 0.0, de = 0.0;
-          dt += qt - ct;
-          de += qe - ce;
-          const double nt = t_tot + dt, ne = e_tot + de;
-          const double cand = cost_of<KIND>(F, nt, ne);
-          const bool act = q != start;
-          evals += act ? 1 : 0;
-          const bool take = act && cand < cost;
-          cur = take ? q : cur;
-          ct = take ? qt : ct;
-          ce = take ? qe : ce;
-          t_tot = take ? nt : t_tot;
-          e_tot = take ? ne : e_tot;
-          cost = take ? cand : cost;
-          changed = changed || take;
-        }
-        alg[i] = (uint8_t)cur;
+  bool running = !missing && ncomp > 0;
+  while (__any_sync(mask, running)) {
+    bool changed = false;
+    if (running) ++sweeps;
+    for (int i = 0; i < nmax; ++i) {
+      if (!running || i >= n) continue;
+      const uint2 info = T.sig_info[V.sig(i)];
+      const uint32_t nr = info.y;  // input rows have bit 31 set: skipped by the test below
+      if (nr < 2u || (nr >> 31)) continue;
+      const uint32_t ro = info.x;
+      const uint32_t start = alg[i];
+      uint32_t cur = start;
+      double ct = T.row_t[ro + cur], ce = T.row_e[ro + cur];
+      for (uint32_t q = 0; q < nr; ++q) {  // branch-free body
+        const double qt = T.row_t[ro + q], qe = T.row_e[ro + q];
+        double dt = 0.0, de = 0.0;
+        dt += qt - ct;
+        de += qe - ce;
+        const double nt = t_tot + dt, ne = e_tot + de;
+        const double cand = cost_of<KIND>(F, nt, ne);
+        const bool act = q != start;
+        evals += act ? 1 : 0;
+        const bool take = act && cand < cost;
+        cur = take ? q : cur;
+        ct = take ? qt : ct;
+        ce = take ? qe : ce;
+        t_tot = take ? nt : t_tot;
+        e_tot = take ? ne : e_tot;
+        cost = take ? cand : cost;
+        changed = changed || take;
       }
+      alg[i] = (uint8_t)cur;
     }
+    running = running && changed;
+  }
+  if (missing) {
+    res.flags |= EF_F_MISSING;
+    return;
   }
   for (int i = 0; i < n; ++i) {
     const uint2 info = T.sig_info[V.sig(i)];

@@ -703,7 +703,11 @@ template <int KIND>
 __global__ void k_price_v(VPriceArgs A, const uint32_t* plist, const uint32_t* plist_n) {
   const Geo& G = A.pa.g;
   const uint32_t total = *plist_n;
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t span = (total + 31) / 32 * 32;  // whole warps iterate together
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < span; k += stride) {
+    const unsigned mask = __ballot_sync(0xffffffffu, k < total);
+    if (k >= total) continue;
     const uint32_t c = plist[k];
     ef_cand_result& res = A.pa.res[c];
     const VPlan& P = A.plan[c];
@@ -719,7 +723,7 @@ __global__ void k_price_v(VPriceArgs A, const uint32_t* plist, const uint32_t* p
     V.s_new1 = P.new_sig[1];
     V.n = P.n_keep + P.n_live;
     uint8_t* alg = A.alg8 + (uint64_t)c * A.S;
-    if (KIND >= 0) price_d1<KIND>(A.pa, V, alg, res);
+    if (KIND >= 0) price_d1<KIND>(A.pa, V, alg, res, mask);
     else price_graph(A.pa, V, alg, res);
   }
 }

@@ -176,13 +176,21 @@ __device__ __forceinline__ uint32_t vremap(const VPlan& P, uint32_t r) {
   return r;
 }
 
+// Lanes of a warp hold neighbouring candidates (mostly of one parent) and walk the same
+// warp-uniform range of topological slots in lockstep, so the parent's arrays are read as
+// broadcasts and the warp never splits.
 __global__ void k_dirty(VArgs A) {
   const Geo& G = A.g;
-  for (uint32_t lc = blockIdx.x * blockDim.x + threadIdx.x; lc < A.n; lc += gridDim.x * blockDim.x) {
+  const uint32_t span = (A.n + 31) / 32 * 32;
+  for (uint32_t lc = blockIdx.x * blockDim.x + threadIdx.x; lc < span; lc += gridDim.x * blockDim.x) {
     const uint32_t c = A.c0 + lc;
-    if (A.res[c].flags & EF_F_INCOMPLETE) {
-      A.dcount[lc] = 0;
-      A.seg_begin[lc] = A.seg_end[lc] = (int32_t)((uint64_t)lc * A.S);
+    const bool incomplete = lc >= A.n || (A.res[c].flags & EF_F_INCOMPLETE);
+    const unsigned mask = __ballot_sync(0xffffffffu, !incomplete);
+    if (incomplete) {
+      if (lc < A.n) {
+        A.dcount[lc] = 0;
+        A.seg_begin[lc] = A.seg_end[lc] = (int32_t)((uint64_t)lc * A.S);
+      }
       continue;
     }
     const VPlan P = A.plan[c];
@@ -197,7 +205,7 @@ __global__ void k_dirty(VArgs A) {
     uint32_t* didx = A.didx + (uint64_t)lc * A.S;
     Job* jobs = A.jobs + (uint64_t)lc * A.S;
     uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
-    for (int i = 0; i < pn + 2; ++i) didx[i] = 0;
+    for (int i = 0; i < (pn + 2 + 3) / 4; ++i) reinterpret_cast<uint4*>(didx)[i] = make_uint4(0, 0, 0, 0);
     const uint32_t* srank = R.srank(G);
     uint32_t* rm = A.rmask + (uint64_t)lc * A.W;
     for (int w = 0; w < (pn + 31) / 32; ++w) rm[w] = 0;
@@ -222,7 +230,10 @@ __global__ void k_dirty(VArgs A) {
         didx[pn + k] = ++j;
       }
     };
-    for (int s = P.first; s < pn; ++s) {
+    const int s_lo = (int)__reduce_min_sync(mask, (unsigned)P.first);
+    const int s_hi = (int)__reduce_max_sync(mask, (unsigned)pn);
+    for (int s = s_lo; s < s_hi; ++s) {
+      if (s < P.first || s >= pn) continue;
       const int v = (int)topo[s];
       if (v == P.drop0 || v == P.drop1) {
         if (s == P.ins_slot && !P.ins_after) emit_new();
@@ -413,11 +424,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_sortkeys(VArgs A) {
     if (d == 0) continue;
     uint32_t m = 2;
     while (m < d) m <<= 1;
+    // sort value: the key's first 4 bytes (big endian) above the job index
     const uint64_t* src = A.skey + (uint64_t)lc * A.S;
-    for (uint32_t i = lane; i < m; i += 32) {
-      sk[i] = i < d ? src[i] : ~0ULL;
-      sv[i] = i;
-    }
+    for (uint32_t i = lane; i < m; i += 32) sk[i] = i < d ? ((src[i] >> 32) << 32) | i : ~0ULL;
     __syncwarp();
     for (uint32_t k = 2; k <= m; k <<= 1) {
       for (uint32_t j = k >> 1; j > 0; j >>= 1) {
@@ -425,36 +434,35 @@ __global__ void __launch_bounds__(WARPS * 32) k_sortkeys(VArgs A) {
           const uint32_t ixj = i ^ j;
           if (ixj > i) {
             const uint64_t a = sk[i], b = sk[ixj];
-            const bool up = (i & k) == 0;
-            if ((a > b) == up) {
+            if ((a > b) == ((i & k) == 0)) {
               sk[i] = b;
               sk[ixj] = a;
-              const uint32_t t = sv[i];
-              sv[i] = sv[ixj];
-              sv[ixj] = t;
             }
           }
         }
         __syncwarp();
       }
     }
+    for (uint32_t i = lane; i < d; i += 32) sv[i] = (uint32_t)sk[i];
+    __syncwarp();
+    // equal first 4 bytes (p ~ d^2 / 2^33 per candidate): order those runs by the full key
+    const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
     bool tie = false;
-    for (uint32_t i = lane; i + 1 < d; i += 32) tie |= sk[i] == sk[i + 1];
+    for (uint32_t i = lane; i + 1 < d; i += 32) tie |= (sk[i] >> 32) == (sk[i + 1] >> 32);
     if (__any_sync(0xffffffffu, tie)) {
       if (lane == 0) {
-        const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
+        auto less = [&](uint32_t x, uint32_t y) {
+          const uint64_t a0 = B2b::bswap64(fresh[2 * x]), b0 = B2b::bswap64(fresh[2 * y]);
+          if (a0 != b0) return a0 < b0;
+          return B2b::bswap64(fresh[2 * x + 1]) < B2b::bswap64(fresh[2 * y + 1]);
+        };
         for (uint32_t i = 0; i + 1 < d;) {
-          if (sk[i] != sk[i + 1]) {
-            ++i;
-            continue;
-          }
           uint32_t e = i + 1;
-          while (e < d && sk[e] == sk[i]) ++e;
+          while (e < d && (sk[e] >> 32) == (sk[i] >> 32)) ++e;
           for (uint32_t x = i + 1; x < e; ++x) {
             const uint32_t v = sv[x];
-            const uint64_t lv = B2b::bswap64(fresh[2 * v + 1]);
             uint32_t y = x;
-            while (y > i && B2b::bswap64(fresh[2 * sv[y - 1] + 1]) > lv) {
+            while (y > i && less(v, sv[y - 1])) {
               sv[y] = sv[y - 1];
               --y;
             }
@@ -465,7 +473,6 @@ __global__ void __launch_bounds__(WARPS * 32) k_sortkeys(VArgs A) {
       }
       __syncwarp();
     }
-    const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
     uint64_t* dst = A.fresh_sorted + 2ull * lc * A.S;
     for (uint32_t i = lane; i < d; i += 32) {
       const uint32_t v = sv[i];

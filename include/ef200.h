@@ -203,6 +203,26 @@ int ef_pending(ef_ctx* ctx, ef_sig_desc* sigs, uint32_t sig_cap, uint32_t* n_sig
 int ef_results(ef_ctx* ctx, ef_cand_result* out, uint32_t n);
 /* copy step candidates into record slots (the ones the search keeps) */
 int ef_keep(ef_ctx* ctx, const uint32_t* cand_idx, uint32_t n, const uint32_t* slots);
+/* ---- hash-owner sharding (one process per GPU) ------------------------------------------ */
+/* The frontier is split across ranks by parent; deduplication is owned by hash:
+ * rank h % world decides, for every candidate hash, its first occurrence in the
+ * global (rank-major) candidate order and its membership in that rank's shard of
+ * the visited set (search.py:245-251 across ranks).  A sharded step is
+ *   ef_expand_hashes -> ef_route_owners -> all-to-all (caller, NCCL) ->
+ *   ef_owner_mark -> all-to-all back -> ef_expand_finish.
+ * Pointers named d_* are device pointers on the context's GPU. */
+/* match, plan and hash the candidates of the given parents (no dedup, no pricing) */
+int ef_expand_hashes(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, const int32_t* rules,
+                     uint32_t n_rules, uint32_t* n_candidates);
+/* (hash, order_base + candidate index) pairs grouped by owner rank into d_send
+ * (room for 2 * n_candidates uint64); counts[world] = pairs per owner (host) */
+int ef_route_owners(ef_ctx* ctx, uint32_t world, uint64_t order_base, uint64_t* d_send, uint32_t* counts);
+/* owner side: verdict (EF_F_FIRST | EF_F_VISITED) for each received pair;
+ * inserts first occurrences into this rank's visited shard when insert_visited */
+int ef_owner_mark(ef_ctx* ctx, const uint64_t* d_recv, uint32_t n_recv, uint32_t* d_verdict, int insert_visited);
+/* verdicts back in send order -> candidate flags, node cap, pricing of the survivors */
+int ef_expand_finish(ef_ctx* ctx, const uint32_t* d_verdict_back, const ef_price_params* pp);
+
 /* device time (ms) of the last ef_expand, measured with CUDA events on its stream,
  * split per stage: match, materialise, hash, dedup, price */
 int ef_last_timing(ef_ctx* ctx, float* ms5);

@@ -117,6 +117,10 @@ struct ef_ctx {
 
   // virtual-candidate step (ef_step.cuh)
   DevBuf<VPlan> d_plan;
+  DevBuf<uint32_t> d_route, d_perm, d_jv, d_recmax;
+  DevBuf<unsigned long long> d_stats;
+  DevBuf<unsigned long long> d_step_ord;
+  uint32_t n_send = 0;
   DevBuf<uint32_t> d_plist, d_sig_info;
   DevBuf<uint8_t> d_alg8, d_seg_tmp;
   DevBuf<uint32_t> d_didx, d_refsrc, d_dcount, d_dorder, d_dsorted, d_sval, d_sval2;
@@ -263,6 +267,12 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_vis.release();
   ctx->d_vis_count.release();
   ctx->d_plan.release();
+  ctx->d_route.release();
+  ctx->d_jv.release();
+  ctx->d_recmax.release();
+  ctx->d_stats.release();
+  ctx->d_perm.release();
+  ctx->d_step_ord.release();
   ctx->d_plist.release();
   ctx->d_sig_info.release();
   ctx->d_alg8.release();
@@ -759,22 +769,49 @@ int ef_record_read(ef_ctx* ctx, uint32_t slot, void* host, uint64_t bytes) {
   return EF_OK;
 }
 
-static size_t hash_top_smem(uint32_t sort_cap) { return 16 * 32 * 8 + 20ull * sort_cap; }
 
-// k_hash_keys (thread per record) then k_hash_top (warp per 32 records)
-static int launch_hash(ef_ctx* ctx, HashArgs& H, uint32_t max_records) {
-  H.sort_cap = pow2_at_least(ctx->geo.cap_nodes);
-  const size_t sm = hash_top_smem(H.sort_cap);
-  EF_REQUIRE(sm <= 227 * 1024, "graph too large for the shared-memory key sort (cap_nodes > 8192)");
-  EF_CUDA(ctx->d_sperm.reserve((uint64_t)max_records * ctx->geo.cap_nodes, ctx->st));
-  H.sperm = ctx->d_sperm.p;
-  EF_CUDA(cudaFuncSetAttribute(k_hash_top, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  const uint32_t g1 = std::max<uint32_t>(1, std::min<uint32_t>((max_records + kHashThreads - 1) / kHashThreads, ctx->n_sm * 16));
-  k_hash_keys<kHashThreads><<<g1, kHashThreads, 0, ctx->st>>>(H);
+// Node keys, sorted order, sorted keys, ranks and graph hash of whole records (uploads and
+// kept candidates): the step's job pipeline with every node a job (ef_step.cuh, full mode).
+static int sort_fresh_keys(ef_ctx* ctx, const VArgs& V);
+static uint32_t bits_for(uint32_t v);
+static int ensure_chunk(ef_ctx* ctx, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk);
+static VArgs chunk_args(ef_ctx* ctx, uint32_t S, uint32_t Rs);
+static int hash_records_full(ef_ctx* ctx, const unsigned long long* d_rec, uint32_t n, uint64_t* d_hash_out) {
+  if (!n) return EF_OK;
+  EF_CUDA(ctx->d_recmax.reserve(2, ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_recmax.p, 0, 8, ctx->st));
+  k_rec_max<<<std::max<uint32_t>(1, std::min<uint32_t>((n + 255) / 256, ctx->n_sm)), 256, 0, ctx->st>>>(d_rec, n,
+                                                                                                      ctx->d_recmax.p);
   EF_CUDA(cudaGetLastError());
-  const uint32_t g2 = std::max<uint32_t>(1, std::min<uint32_t>((max_records + 31) / 32, ctx->n_sm * 16));
-  k_hash_top<<<g2, 32, sm, ctx->st>>>(H);
-  EF_CUDA(cudaGetLastError());
+  uint32_t mx[2] = {0, 0};
+  EF_CUDA(cudaMemcpyAsync(mx, ctx->d_recmax.p, 8, cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  const uint32_t S = (std::max<uint32_t>(mx[0], 1) + 2 + 3) & ~3u;
+  const uint32_t Rs = mx[1] + 4;
+  uint32_t chunk = 0;
+  int rc = ensure_chunk(ctx, n, S, Rs, &chunk);
+  if (rc) return rc;
+  VArgs V = chunk_args(ctx, S, Rs);
+  V.parent_addr = d_rec;
+  V.full = 1;
+  V.hash_out = d_hash_out;
+  for (uint32_t c0 = 0; c0 < n; c0 += chunk) {
+    V.c0 = c0;
+    V.n = std::min(chunk, n - c0);
+    const uint32_t gd = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 127) / 128, ctx->n_sm * 16));
+    k_full_jobs<<<gd, 128, 0, ctx->st>>>(V);
+    EF_CUDA(cudaGetLastError());
+    size_t t1 = ctx->d_sort_tmp.cap;
+    EF_CUDA(cub::DeviceRadixSort::SortPairsDescending(ctx->d_sort_tmp.p, t1, ctx->d_dcount.p, ctx->d_dsorted.p,
+                                                      ctx->d_iota.p, ctx->d_dorder.p, (int)V.n, 0, bits_for(S),
+                                                      ctx->st));
+    k_keys<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+    EF_CUDA(cudaGetLastError());
+    if ((rc = sort_fresh_keys(ctx, V))) return rc;
+    k_digest<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+    k_full_store<<<std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * 8)), 128, 0, ctx->st>>>(V);
+    EF_CUDA(cudaGetLastError());
+  }
   return EF_OK;
 }
 
@@ -826,20 +863,9 @@ int ef_hash_records(ef_ctx* ctx, const uint32_t* slots, uint32_t n, uint64_t* ha
   int rc = stage_addrs(ctx, ctx->d_addr_a, slots, n);
   if (rc) return rc;
   EF_CUDA(ctx->d_hash_out.reserve(n, ctx->st));
-  EF_CUDA(ctx->d_scalars.reserve(16, ctx->st));
-  EF_CUDA(cudaMemsetAsync(ctx->d_scalars.p, 0, 16 * 4, ctx->st));
-  HashArgs H{};
-  H.g = ctx->geo;
-  H.T = make_tables(ctx);
-  H.n = n;
-  H.rec = ctx->d_addr_a.p;
-  H.hash_out = ctx->d_hash_out.p;
-  H.err = ctx->d_scalars.p + 1;
-  if ((rc = launch_hash(ctx, H, n))) return rc;
+  if ((rc = hash_records_full(ctx, ctx->d_addr_a.p, n, ctx->d_hash_out.p))) return rc;
   EF_CUDA(cudaMemcpyAsync(hashes, ctx->d_hash_out.p, n * 8, cudaMemcpyDeviceToHost, ctx->st));
-  EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
   EF_CUDA(cudaStreamSynchronize(ctx->st));
-  EF_REQUIRE(ctx->h_scalars[1] == 0, "hash kernel capacity error");
   return EF_OK;
 }
 
@@ -915,8 +941,8 @@ static int ensure_parent_buffers(ef_ctx* ctx, uint32_t n_parents) {
   return EF_OK;
 }
 
-// candidate-level buffers (whole step) and the per-chunk hashing scratch
-static int ensure_cand_buffers(ef_ctx* ctx, uint32_t total, uint32_t S, uint32_t Rs, uint32_t* chunk) {
+// candidate-level buffers of a step
+static int ensure_step_cand(ef_ctx* ctx, uint32_t total, uint32_t S) {
   const uint64_t tcap = pow2_at_least(2ull * std::max<uint32_t>(total, 1024));
   EF_CUDA(ctx->d_res.reserve(std::max<uint32_t>(total, 1), ctx->st));
   EF_CUDA(ctx->d_plan.reserve(std::max<uint32_t>(total, 1), ctx->st));
@@ -926,13 +952,19 @@ static int ensure_cand_buffers(ef_ctx* ctx, uint32_t total, uint32_t S, uint32_t
   EF_CUDA(ctx->d_step_seq.reserve(tcap, ctx->st));
   EF_CUDA(ctx->d_req_sig.reserve(ctx->req_cap, ctx->st));
   EF_CUDA(ctx->d_req_dv.reserve(4 * ctx->req_cap, ctx->st));
-  // chunk: bounded scratch so graphs of any size stream through
-  const uint64_t per = (uint64_t)S * (4 + sizeof(Job) + 16 + 16 + 8 + 8 + 4 + 4) + 4ull * Rs + 4ull * (S + 31) / 32 + 32;
-  uint64_t ch = std::max<uint64_t>(256, (6144ull << 20) / per);  // <= 6 GiB of the 180 GB
-  ch = std::min<uint64_t>(ch, std::max<uint32_t>(total, 1));
+  return EF_OK;
+}
+
+// per-chunk hashing scratch for rows of S node slots and Rs ref slots: bounded (<= 6 GiB of
+// the 180 GB) so graphs of any size stream through
+static int ensure_chunk(ef_ctx* ctx, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk) {
+  const uint64_t per = (uint64_t)S * (4 + 4 + sizeof(Job) + 16 + 16 + 8 + 8 + 4 + 4) + 4ull * Rs + 4ull * (S + 31) / 32 + 32;
+  uint64_t ch = std::max<uint64_t>(256, (6144ull << 20) / per);
+  ch = std::min<uint64_t>(ch, std::max<uint32_t>(items, 1));
   ch = std::min<uint64_t>(ch, (uint64_t)INT32_MAX / S);
   *chunk = (uint32_t)ch;
   EF_CUDA(ctx->d_didx.reserve(ch * S, ctx->st));
+  EF_CUDA(ctx->d_jv.reserve(ch * S, ctx->st));
   EF_CUDA(ctx->d_jobs.reserve(ch * S, ctx->st));
   EF_CUDA(ctx->d_refsrc.reserve(ch * Rs, ctx->st));
   EF_CUDA(ctx->d_fresh.reserve(2 * ch * S, ctx->st));
@@ -965,6 +997,36 @@ static int ensure_cand_buffers(ef_ctx* ctx, uint32_t total, uint32_t S, uint32_t
   return EF_OK;
 }
 
+static VArgs chunk_args(ef_ctx* ctx, uint32_t S, uint32_t Rs) {
+  VArgs V{};
+  V.g = ctx->geo;
+  V.T = make_tables(ctx);
+  V.plan = ctx->d_plan.p;
+  V.res = ctx->d_res.p;
+  V.S = S;
+  V.Rs = Rs;
+  V.didx = ctx->d_didx.p;
+  V.jobs = ctx->d_jobs.p;
+  V.refsrc = ctx->d_refsrc.p;
+  V.fresh = ctx->d_fresh.p;
+  V.dcount = ctx->d_dcount.p;
+  V.order = ctx->d_dorder.p;
+  V.skey = ctx->d_skey.p;
+  V.sval = ctx->d_sval.p;
+  V.skey_sorted = ctx->d_skey2.p;
+  V.sval_sorted = ctx->d_sval2.p;
+  V.seg_begin = ctx->d_seg_b.p;
+  V.seg_end = ctx->d_seg_e.p;
+  V.W = (S + 31) / 32;
+  V.rmask = ctx->d_rmask.p;
+  V.fresh_sorted = ctx->d_fresh2.p;
+  V.input_words = reinterpret_cast<const uint64_t*>(ctx->d_input_text.p);
+  V.err = ctx->d_scalars.p + 1;
+  V.one = 1;
+  V.jv = ctx->d_jv.p;
+  return V;
+}
+
 // every candidate's fresh keys in ascending order: warp bitonic sort in shared memory for
 // rows up to 1024 keys, cub's segmented sort (plus the tie fix) beyond
 static int sort_fresh_keys(ef_ctx* ctx, const VArgs& V) {
@@ -995,20 +1057,20 @@ static uint32_t bits_for(uint32_t v) {
   return b;
 }
 
-int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, const int32_t* rules, uint32_t n_rules,
-              const ef_price_params* pp, int insert_visited, uint32_t* n_candidates) {
-  EF_REQUIRE(n_candidates, "ef_expand: null n_candidates");
-  *n_candidates = 0;
-  EF_REQUIRE(!ctx->dirty, "tables not committed (call ef_tables_commit)");
-  EF_REQUIRE(ctx->vis_mask, "visited set not initialised");
-  EF_REQUIRE(n_rules <= 8, "at most 8 rules");
-  cudaSetDevice(ctx->dev);
+// ---- step phases --------------------------------------------------------------------------
+
+// 1-3: match, plans, per chunk dirty walk / node keys / key sort / graph digest.  Leaves the
+// candidates' hashes in d_res; no synchronisation at the end.
+static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, const int32_t* rules,
+                     uint32_t n_rules, uint32_t* n_total) {
   for (int attempt = 0; attempt < 8; ++attempt) {
     int rc = ensure_parent_buffers(ctx, std::max<uint32_t>(n_parents, 1));
     if (rc) return rc;
     const Geo& g = ctx->geo;
     if ((rc = stage_addrs(ctx, ctx->d_parent_addr, parent_slots, n_parents))) return rc;
     EF_CUDA(cudaMemsetAsync(ctx->d_scalars.p, 0, 16 * 4, ctx->st));
+    EF_CUDA(ctx->d_stats.reserve(8, ctx->st));
+    EF_CUDA(cudaMemsetAsync(ctx->d_stats.p, 0, 8 * 8, ctx->st));
     StepArgs A{};
     A.g = g;
     A.T = make_tables(ctx);
@@ -1047,7 +1109,7 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
     const uint32_t S = (std::max<uint32_t>(ctx->h_scalars[5], 1) + 2 + 3) & ~3u;
     const uint32_t Rs = ctx->h_scalars[6] + 4;
     uint32_t chunk = 0;
-    if ((rc = ensure_cand_buffers(ctx, total, S, Rs, &chunk))) return rc;
+    if ((rc = ensure_step_cand(ctx, total, S)) || (rc = ensure_chunk(ctx, total, S, Rs, &chunk))) return rc;
     ctx->step_S = S;
     ctx->step_Rs = Rs;
     ctx->step_n_parents = n_parents;
@@ -1064,32 +1126,9 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
       EF_CUDA(cudaGetLastError());
     }
     cudaEventRecord(ctx->ev[2], ctx->st);
-    VArgs V{};
-    V.g = g;
-    V.T = A.T;
+    VArgs V = chunk_args(ctx, S, Rs);
     V.parent_addr = A.parent_addr;
-    V.plan = ctx->d_plan.p;
-    V.res = ctx->d_res.p;
-    V.S = S;
-    V.Rs = Rs;
-    V.didx = ctx->d_didx.p;
-    V.jobs = ctx->d_jobs.p;
-    V.refsrc = ctx->d_refsrc.p;
-    V.fresh = ctx->d_fresh.p;
-    V.dcount = ctx->d_dcount.p;
-    V.order = ctx->d_dorder.p;
-    V.skey = ctx->d_skey.p;
-    V.sval = ctx->d_sval.p;
-    V.skey_sorted = ctx->d_skey2.p;
-    V.sval_sorted = ctx->d_sval2.p;
-    V.seg_begin = ctx->d_seg_b.p;
-    V.seg_end = ctx->d_seg_e.p;
-    V.W = (S + 31) / 32;
-    V.rmask = ctx->d_rmask.p;
-    V.fresh_sorted = ctx->d_fresh2.p;
-    V.input_words = reinterpret_cast<const uint64_t*>(ctx->d_input_text.p);
-    V.err = A.err;
-    V.one = 1;
+    V.stats = ctx->d_stats.p;
     for (uint32_t c0 = 0; c0 < total; c0 += chunk) {
       V.c0 = c0;
       V.n = std::min(chunk, total - c0);
@@ -1107,74 +1146,196 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
       EF_CUDA(cudaGetLastError());
     }
     cudaEventRecord(ctx->ev[3], ctx->st);
-
-    // 4) dedup inside the step and against the visited set
-    const uint32_t tcap = pow2_at_least(2ull * std::max<uint32_t>(total, 1024));
-    EF_CUDA(cudaMemsetAsync(ctx->d_step_key.p, 0, (size_t)tcap * 8, ctx->st));
-    EF_CUDA(cudaMemsetAsync(ctx->d_step_seq.p, 0xff, (size_t)tcap * 4, ctx->st));
-    DedupArgs D{};
-    D.res = A.res;
-    D.total = A.total;
-    D.step_key = ctx->d_step_key.p;
-    D.step_seq = ctx->d_step_seq.p;
-    D.step_mask = tcap - 1;
-    D.vis_key = ctx->d_vis.p;
-    D.vis_mask = ctx->vis_mask;
-    D.vis_count = ctx->d_vis_count.p;
-    D.insert_visited = insert_visited;
-    D.node_cap = pp->node_cap;
-    D.plist = ctx->d_plist.p;
-    D.plist_n = ctx->d_scalars.p + 7;
-    k_dedup_claim<<<grid_t, 256, 0, ctx->st>>>(D);
-    k_dedup_resolve<<<grid_t, 256, 0, ctx->st>>>(D);
-    EF_CUDA(cudaGetLastError());
-    cudaEventRecord(ctx->ev[4], ctx->st);
-
-    // 5) inner search on every survivor
-    VPriceArgs Pv{};
-    Pv.pa.g = g;
-    Pv.pa.T = A.T;
-    Pv.pa.pp = *pp;
-    Pv.pa.total = A.total;
-    Pv.pa.res = A.res;
-    Pv.pa.step_mode = 1;
-    Pv.plan = ctx->d_plan.p;
-    Pv.parent_addr = A.parent_addr;
-    Pv.alg8 = ctx->d_alg8.p;
-    Pv.S = S;
-    {
-      const uint32_t gp = std::max<uint32_t>(1, std::min<uint32_t>((total + kPriceThreads - 1) / kPriceThreads, ctx->n_sm * 16));
-      const uint32_t* pl = ctx->d_plist.p;
-      const uint32_t* pn = ctx->d_scalars.p + 7;
-      const bool fast = pp->use_inner && pp->d == 1;
-      if (fast && pp->kind == EF_C_ENERGY) k_price_v<EF_C_ENERGY><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
-      else if (fast && pp->kind == EF_C_TIME) k_price_v<EF_C_TIME><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
-      else if (fast && pp->kind == EF_C_LINEAR) k_price_v<EF_C_LINEAR><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
-      else if (fast) k_price_v<EF_C_MIX + 1><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
-      else k_price_v<-1><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
-      EF_CUDA(cudaGetLastError());
-    }
-    cudaEventRecord(ctx->ev[5], ctx->st);
-    EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
-    EF_CUDA(cudaStreamSynchronize(ctx->st));
-    const uint32_t err = ctx->h_scalars[1];
-    ctx->last_req_sig = ctx->h_scalars[2];
-    ctx->last_req_dv = ctx->h_scalars[3];
-    for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&ctx->last_ms[k], ctx->ev[k], ctx->ev[k + 1]);
-    EF_REQUIRE(!(err & 4u), "candidate exceeds record capacity (raise cap_nodes/cap_refs)");
     ctx->last_total = total;
     ctx->last_step = A;
-    *n_candidates = total;
-    if (ctx->last_req_sig || ctx->last_req_dv) return EF_NEED_RESOLVE;
-    if (insert_visited) {
-      k_visited_insert<<<grid_t, 256, 0, ctx->st>>>(D);
-      EF_CUDA(cudaGetLastError());
-      EF_CUDA(cudaStreamSynchronize(ctx->st));
-    }
+    *n_total = total;
     return EF_OK;
   }
   ctx->err = "ef_expand: buffers did not converge";
   return EF_ERR_CAPACITY;
+}
+
+static DedupArgs dedup_args(ef_ctx* ctx, const ef_price_params* pp, int insert_visited, uint32_t table_items) {
+  const uint32_t tcap = pow2_at_least(2ull * std::max<uint32_t>(table_items, 1024));
+  DedupArgs D{};
+  D.res = ctx->d_res.p;
+  D.total = ctx->d_scalars.p + 0;
+  D.step_key = ctx->d_step_key.p;
+  D.step_seq = ctx->d_step_seq.p;
+  D.step_mask = tcap - 1;
+  D.vis_key = ctx->d_vis.p;
+  D.vis_mask = ctx->vis_mask;
+  D.vis_count = ctx->d_vis_count.p;
+  D.insert_visited = insert_visited;
+  D.node_cap = pp ? pp->node_cap : 0;
+  D.plist = ctx->d_plist.p;
+  D.plist_n = ctx->d_scalars.p + 7;
+  return D;
+}
+
+// 4) dedup inside the step and against the visited set (single rank)
+static int step_dedup_local(ef_ctx* ctx, const ef_price_params* pp) {
+  const uint32_t total = ctx->last_total;
+  DedupArgs D = dedup_args(ctx, pp, 0, total);
+  EF_CUDA(cudaMemsetAsync(ctx->d_step_key.p, 0, (size_t)(D.step_mask + 1) * 8, ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_step_seq.p, 0xff, (size_t)(D.step_mask + 1) * 4, ctx->st));
+  const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));
+  k_dedup_claim<<<grid_t, 256, 0, ctx->st>>>(D);
+  k_dedup_resolve<<<grid_t, 256, 0, ctx->st>>>(D);
+  EF_CUDA(cudaGetLastError());
+  cudaEventRecord(ctx->ev[4], ctx->st);
+  return EF_OK;
+}
+
+// 5) inner search on every survivor (the compacted list of step 4)
+static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
+  const uint32_t total = ctx->last_total;
+  VPriceArgs Pv{};
+  Pv.pa.g = ctx->geo;
+  Pv.pa.T = make_tables(ctx);
+  Pv.pa.pp = *pp;
+  Pv.pa.total = ctx->d_scalars.p + 0;
+  Pv.pa.res = ctx->d_res.p;
+  Pv.pa.step_mode = 1;
+  Pv.plan = ctx->d_plan.p;
+  Pv.parent_addr = ctx->d_parent_addr.p;
+  Pv.alg8 = ctx->d_alg8.p;
+  Pv.S = ctx->step_S;
+  const uint32_t gp = std::max<uint32_t>(1, std::min<uint32_t>((total + kPriceThreads - 1) / kPriceThreads, ctx->n_sm * 16));
+  const uint32_t* pl = ctx->d_plist.p;
+  const uint32_t* pn = ctx->d_scalars.p + 7;
+  const bool fast = pp->use_inner && pp->d == 1;
+  if (fast && pp->kind == EF_C_ENERGY) k_price_v<EF_C_ENERGY><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
+  else if (fast && pp->kind == EF_C_TIME) k_price_v<EF_C_TIME><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
+  else if (fast && pp->kind == EF_C_LINEAR) k_price_v<EF_C_LINEAR><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
+  else if (fast) k_price_v<EF_C_MIX + 1><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
+  else k_price_v<-1><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
+  EF_CUDA(cudaGetLastError());
+  cudaEventRecord(ctx->ev[5], ctx->st);
+  return EF_OK;
+}
+
+// synchronise; EF_NEED_RESOLVE when the plans asked for signatures / weight sets
+static int step_sync(ef_ctx* ctx, bool timings) {
+  EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  const uint32_t err = ctx->h_scalars[1];
+  ctx->last_req_sig = ctx->h_scalars[2];
+  ctx->last_req_dv = ctx->h_scalars[3];
+  if (timings)
+    for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&ctx->last_ms[k], ctx->ev[k], ctx->ev[k + 1]);
+  EF_REQUIRE(!(err & 4u), "candidate exceeds record capacity (raise cap_nodes/cap_refs)");
+  if (ctx->last_req_sig || ctx->last_req_dv) return EF_NEED_RESOLVE;
+  return EF_OK;
+}
+
+static int insert_firsts(ef_ctx* ctx) {
+  DedupArgs D = dedup_args(ctx, nullptr, 1, ctx->last_total);
+  const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((ctx->last_total + 255) / 256, ctx->n_sm * 8));
+  k_visited_insert<<<grid_t, 256, 0, ctx->st>>>(D);
+  EF_CUDA(cudaGetLastError());
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+static int step_begin(ef_ctx* ctx, uint32_t* n_candidates, uint32_t n_rules) {
+  EF_REQUIRE(n_candidates, "null n_candidates");
+  *n_candidates = 0;
+  EF_REQUIRE(!ctx->dirty, "tables not committed (call ef_tables_commit)");
+  EF_REQUIRE(ctx->vis_mask, "visited set not initialised");
+  EF_REQUIRE(n_rules <= 8, "at most 8 rules");
+  cudaSetDevice(ctx->dev);
+  return EF_OK;
+}
+
+int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, const int32_t* rules, uint32_t n_rules,
+              const ef_price_params* pp, int insert_visited, uint32_t* n_candidates) {
+  int rc = step_begin(ctx, n_candidates, n_rules);
+  if (rc) return rc;
+  uint32_t total = 0;
+  if ((rc = step_hash(ctx, parent_slots, n_parents, rules, n_rules, &total))) return rc;
+  if ((rc = step_dedup_local(ctx, pp)) || (rc = step_price(ctx, pp))) return rc;
+  rc = step_sync(ctx, true);
+  *n_candidates = total;
+  if (rc) return rc;
+  if (insert_visited && (rc = insert_firsts(ctx))) return rc;
+  return EF_OK;
+}
+
+// ---- hash-owner sharding ---------------------------------------------------------------------
+
+int ef_expand_hashes(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, const int32_t* rules,
+                     uint32_t n_rules, uint32_t* n_candidates) {
+  int rc = step_begin(ctx, n_candidates, n_rules);
+  if (rc) return rc;
+  uint32_t total = 0;
+  if ((rc = step_hash(ctx, parent_slots, n_parents, rules, n_rules, &total))) return rc;
+  rc = step_sync(ctx, false);
+  *n_candidates = total;
+  return rc;
+}
+
+int ef_route_owners(ef_ctx* ctx, uint32_t world, uint64_t order_base, uint64_t* d_send, uint32_t* counts) {
+  EF_REQUIRE(world >= 1 && world <= 1024 && counts && d_send, "ef_route_owners: bad arguments");
+  const uint32_t total = ctx->last_total;
+  EF_CUDA(ctx->d_route.reserve(2 * (size_t)world + 2, ctx->st));
+  EF_CUDA(ctx->d_perm.reserve(std::max<uint32_t>(total, 1), ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_route.p, 0, (2 * (size_t)world + 2) * 4, ctx->st));
+  const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));
+  RouteArgs R{ctx->d_res.p, total, world, order_base, ctx->d_route.p, ctx->d_route.p + world, d_send, ctx->d_perm.p};
+  k_route_count<<<grid_t, 256, 0, ctx->st>>>(R);
+  EF_CUDA(cudaGetLastError());
+  std::vector<uint32_t> cnt(world), off(world);
+  EF_CUDA(cudaMemcpyAsync(cnt.data(), ctx->d_route.p, world * 4, cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  uint32_t run = 0;
+  for (uint32_t w = 0; w < world; ++w) {
+    off[w] = run;
+    run += cnt[w];
+    counts[w] = cnt[w];
+  }
+  ctx->n_send = run;
+  EF_CUDA(cudaMemcpyAsync(ctx->d_route.p + world, off.data(), world * 4, cudaMemcpyHostToDevice, ctx->st));
+  k_route_scatter<<<grid_t, 256, 0, ctx->st>>>(R);
+  EF_CUDA(cudaGetLastError());
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+int ef_owner_mark(ef_ctx* ctx, const uint64_t* d_recv, uint32_t n_recv, uint32_t* d_verdict, int insert_visited) {
+  EF_REQUIRE(ctx->vis_mask, "visited set not initialised");
+  if (!n_recv) return EF_OK;
+  const uint32_t tcap = pow2_at_least(2ull * std::max<uint32_t>(n_recv, 1024));
+  EF_CUDA(ctx->d_step_key.reserve(tcap, ctx->st));
+  EF_CUDA(ctx->d_step_ord.reserve(tcap, ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_step_key.p, 0, (size_t)tcap * 8, ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_step_ord.p, 0xff, (size_t)tcap * 8, ctx->st));
+  OwnerArgs O{d_recv, n_recv, d_verdict, ctx->d_step_key.p, ctx->d_step_ord.p, tcap - 1, ctx->d_vis.p, ctx->vis_mask,
+              ctx->d_vis_count.p};
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((n_recv + 255) / 256, ctx->n_sm * 8));
+  k_owner_claim<<<grid, 256, 0, ctx->st>>>(O);
+  k_owner_resolve<<<grid, 256, 0, ctx->st>>>(O);
+  if (insert_visited) k_owner_insert<<<grid, 256, 0, ctx->st>>>(O);
+  EF_CUDA(cudaGetLastError());
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+int ef_expand_finish(ef_ctx* ctx, const uint32_t* d_verdict_back, const ef_price_params* pp) {
+  const uint32_t total = ctx->last_total;
+  EF_CUDA(cudaMemsetAsync(ctx->d_scalars.p + 7, 0, 4, ctx->st));
+  cudaEventRecord(ctx->ev[3], ctx->st);
+  if (ctx->n_send) {
+    const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((ctx->n_send + 255) / 256, ctx->n_sm * 8));
+    k_apply_verdicts<<<grid, 256, 0, ctx->st>>>(ctx->d_res.p, ctx->d_perm.p, d_verdict_back, ctx->n_send,
+                                                pp->node_cap, ctx->d_plist.p, ctx->d_scalars.p + 7);
+    EF_CUDA(cudaGetLastError());
+  }
+  cudaEventRecord(ctx->ev[4], ctx->st);
+  int rc = step_price(ctx, pp);
+  if (rc) return rc;
+  (void)total;
+  return step_sync(ctx, true);
 }
 
 int ef_pending(ef_ctx* ctx, ef_sig_desc* sigs, uint32_t sig_cap, uint32_t* n_sigs, int32_t* derives, uint32_t derive_cap,
@@ -1224,19 +1385,10 @@ int ef_keep(ef_ctx* ctx, const uint32_t* cand_idx, uint32_t n, const uint32_t* s
   k_keep_alg<<<std::min<uint32_t>(n, ctx->n_sm * 8), 128, 0, ctx->st>>>(ctx->d_alg8.p, ctx->step_S, ctx->d_sel.p,
                                                                       ctx->d_dst.p, n, g);
   EF_CUDA(cudaGetLastError());
-  // node keys and sorted-key order of the new records (every parent carries them)
-  EF_CUDA(ctx->d_scalars.reserve(16, ctx->st));
-  EF_CUDA(cudaMemsetAsync(ctx->d_scalars.p + 8, 0, 4, ctx->st));
-  HashArgs H{};
-  H.g = g;
-  H.T = make_tables(ctx);
-  H.n = n;
-  H.rec = ctx->d_dst.p;
-  H.err = ctx->d_scalars.p + 8;
-  if ((rc = launch_hash(ctx, H, n))) return rc;
-  EF_CUDA(cudaMemcpyAsync(ctx->h_scalars + 8, ctx->d_scalars.p + 8, 4, cudaMemcpyDeviceToHost, ctx->st));
+  // node keys, sorted order and ranks of the new records (every parent carries them)
+  EF_CUDA(ctx->d_hash_out.reserve(n, ctx->st));
+  if ((rc = hash_records_full(ctx, ctx->d_dst.p, n, ctx->d_hash_out.p))) return rc;
   EF_CUDA(cudaStreamSynchronize(ctx->st));
-  EF_REQUIRE(ctx->h_scalars[8] == 0, "ef_keep: hash capacity error");
   return EF_OK;
 }
 

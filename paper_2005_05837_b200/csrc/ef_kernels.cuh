@@ -1,21 +1,20 @@
-// Kernels of one frontier step (match -> materialise -> hash -> dedup -> price) plus the
-// table kernels (weight-set derivation and digests) and record utilities.
+// Kernels shared by the frontier step (ef_step.cuh) and the tables: rule matching, rewrite
+// planning / record materialisation, dedup, pricing, weight-set derivation and digests.
 //
-// Work decomposition (B200: 148 SMs, persistent grid-stride blocks):
-//   k_match        one CTA per parent graph: consumer CSR + use counts, then every rule at
-//                  every node, emitted in the reference's site order with block-wide scans.
-//   k_materialise  one CTA per candidate: copies the parent record applying the rewrite;
-//                  positions/offsets of the child are closed-form in the <= 2 dropped nodes,
-//                  so the copy is a single coalesced pass (no per-node scan needed).
-//   k_hash         one CTA per candidate: Merkle node keys in dataflow order (threads wait on
-//                  their producers' flags in shared memory; clean nodes copy the parent key),
-//                  bitonic sort of the keys in shared memory, then the graph digest.
+//   k_match        one CTA per parent graph: use counts, consumer CSR and inverse topological
+//                  order, then every rule at every node, emitted in the reference's site order
+//                  (rules.py:147-331 matchers) with block-wide scans.
+//   plan_rewrite   the rewrite of one site in parent coordinates (rules.py:164-331).
+//   k_materialise  one CTA per KEPT candidate: copies the parent record applying the rewrite;
+//                  child positions / offsets are closed-form in the <= 2 dropped nodes, so the
+//                  copy is a single coalesced pass.
 //   k_dedup_*      open-addressing tables: first occurrence inside the step (atomicMin on the
 //                  candidate's sequence number) and membership in the visited set.
-//   k_price        one thread per surviving candidate: the reference's first-improvement sweep
-//                  (search.py:106-153) with CPython's Neumaier sum for the start totals; every
-//                  floating-point operation in the reference's order, no FMA contraction
-//                  (the library is compiled with --fmad=false).
+//   price_d1 /     the reference's first-improvement sweep (search.py:106-153) with CPython's
+//   price_graph    Neumaier sum for the start totals; every floating-point operation in the
+//                  reference's order, no FMA contraction (the library builds with --fmad=false).
+//   k_derive /     derived weight tensors (rules.py:231-232, 272-276, 326-327) and BLAKE2b
+//   k_digest       digests of weight sets (graph.py:510-517).
 #pragma once
 #include <stdint.h>
 
@@ -755,380 +754,6 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
       res->sweeps = 0;
     }
     __syncthreads();
-  }
-}
-
-// slots past the step's candidate count sort last
-__global__ void k_first_pad(uint32_t* first, const uint32_t* total, uint32_t cap) {
-  const uint32_t t = total[0];
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cap; c += gridDim.x * blockDim.x)
-    if (c >= t) first[c] = 0xFFFFFFu;
-    else first[c] = min(first[c], 0xFFFFFEu);
-}
-
-// ------------------------------------------------------------------------------------------
-// canonical hash (graph.py:520-549) in two kernels:
-//   k_hash_keys  one THREAD per record: walks the record's topological order; a node is
-//                dirty when it was rewritten or a producer is dirty; dirty nodes get a fresh
-//                BLAKE2b-128 key, clean nodes copy their parent's key.  Message bytes are
-//                staged in shared memory (word-interleaved across the block so lanes never
-//                bank-conflict) and loaded into registers for each compression.
-//   k_hash_top   one WARP per 32 records: for each record the warp bitonic-sorts its keys
-//                (as big-endian 128-bit values = Python's bytes order) in shared memory and
-//                stores the sorted positions; then every lane streams one record's graph
-//                digest (inputs text, output keys, sorted keys) — BLAKE2b-64.
-// ------------------------------------------------------------------------------------------
-
-struct HashArgs {
-  Geo g;
-  Tables T;
-  uint32_t n;                     // records (full mode)
-  const unsigned long long* rec;  // record addresses (full mode) or null: cand_base + c * bytes
-  char* cand_base;
-  const uint32_t* total;  // device count (step mode)
-  const unsigned long long* parent_addr;
-  const int32_t* srcpos;
-  uint8_t* seed;      // bit0 rewritten (materialise), bit1 dirty (set here)
-  uint8_t* pmark;     // parent positions whose key is not in the child (dropped / dirty)
-  uint32_t* sperm;    // scratch, cap_nodes per record: sorted dirty positions
-  const uint32_t* first;  // per candidate first dirty topo slot (incremental)
-  const uint32_t* order;  // lane -> candidate permutation (sorted by first slot), or null
-  ef_cand_result* res;
-  uint64_t* hash_out;  // full mode output
-  int incremental;
-  uint32_t sort_cap;  // power of two >= cap_nodes
-  uint32_t* err;
-};
-
-// streaming BLAKE2b over a per-thread message block held in shared memory (stride BT words)
-template <int BT>
-struct B2bS {
-  uint64_t h[8];
-  uint64_t t;
-  uint32_t fill;
-  uint64_t* m;  // &msg[tid]; word k at m[k * BT]
-
-  __device__ __forceinline__ void clear() {
-#pragma unroll
-    for (int k = 0; k < 16; ++k) m[k * BT] = 0;
-  }
-  __device__ __forceinline__ void init(int outlen, uint64_t* base) {
-    m = base;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) h[i] = b2b_iv(i);
-    h[0] ^= 0x01010000ULL ^ (uint64_t)outlen;
-    t = 0;
-    fill = 0;
-    clear();
-  }
-  __device__ __forceinline__ void compress(bool last) {
-    uint64_t w[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) w[k] = m[k * BT];
-    b2b_compress(h, w, t, last);
-  }
-  __device__ __forceinline__ void flush_if_full() {
-    if (fill == 128) {
-      t += 128;
-      compress(false);
-      clear();
-      fill = 0;
-    }
-  }
-  __device__ __forceinline__ void byte(uint8_t b) {
-    flush_if_full();
-    m[(fill >> 3) * BT] |= (uint64_t)b << (8 * (fill & 7));
-    ++fill;
-  }
-  __device__ __forceinline__ void word_le(uint64_t w) {
-    flush_if_full();
-    const uint32_t sh = 8 * (fill & 7), k = fill >> 3;
-    if (sh == 0) {
-      m[k * BT] = w;
-      fill += 8;
-      return;
-    }
-    m[k * BT] |= w << sh;
-    const uint32_t room = 128 - fill;
-    if (room >= 8) {
-      m[(k + 1) * BT] = w >> (64 - sh);
-      fill += 8;
-    } else {
-      fill = 128;
-      flush_if_full();
-      m[0] = w >> (64 - sh);
-      fill = 8 - room;
-    }
-  }
-  __device__ __forceinline__ void u16_be(uint32_t v) {
-    byte((uint8_t)(v >> 8));
-    byte((uint8_t)v);
-  }
-  __device__ __forceinline__ void final() {
-    t += fill;
-    compress(true);
-  }
-};
-
-template <int BT>
-__device__ __forceinline__ void append_sig_text(B2bS<BT>& s, const Tables& T, uint32_t sig) {
-  const uint32_t off = T.sig_text_off[sig], len = T.sig_text_len[sig];
-  const uint64_t* w = reinterpret_cast<const uint64_t*>(T.sig_text + off);  // 8-byte aligned, zero padded
-  const uint32_t full = len >> 3;
-  for (uint32_t i = 0; i < full; ++i) s.word_le(__ldg(w + i));
-  const uint8_t* tail = T.sig_text + off + 8 * full;
-  for (uint32_t i = 0; i < (len & 7u); ++i) s.byte(__ldg(tail + i));
-}
-
-template <int BT>
-__global__ void __launch_bounds__(BT) k_hash_keys(HashArgs A) {
-  __shared__ uint64_t msg[16 * BT];
-  const Geo& G = A.g;
-  const Tables& T = A.T;
-  const uint32_t total = A.total ? A.total[0] : A.n;
-  for (uint32_t lc = blockIdx.x * BT + threadIdx.x; lc < total; lc += gridDim.x * BT) {
-    const uint32_t c = A.order ? A.order[lc] : lc;
-    if (A.res && (A.res[c].flags & EF_F_INCOMPLETE)) continue;
-    Rec R{A.rec ? reinterpret_cast<char*>(A.rec[c]) : A.cand_base + (uint64_t)c * G.bytes};
-    const int n = R.h().n;
-    Rec P{nullptr};
-    const int32_t* srcpos = nullptr;
-    uint8_t* seed = nullptr;
-    if (A.incremental) {
-      P.p = reinterpret_cast<char*>(A.parent_addr[A.res[c].parent]);
-      srcpos = A.srcpos + (uint64_t)c * G.cap_nodes;
-      seed = A.seed + (uint64_t)c * G.cap_nodes;
-    }
-    const uint32_t* topo = R.topo(G);
-    const uint32_t* sig = R.sig(G);
-    const uint32_t* aux = R.aux(G);
-    const uint32_t* nin = R.nin(G);
-    const uint32_t* inoff = R.inoff(G);
-    const uint32_t* refs = R.refs(G);
-    uint64_t* keys = R.keys(G);
-    const int s0 = A.incremental ? (int)min(A.first[c], (uint32_t)n) : 0;
-    for (int s = s0; s < n; ++s) {
-      const uint32_t v = topo[s];
-      const uint32_t r0 = inoff[v], r1 = r0 + nin[v];
-      bool dirty = true;
-      if (A.incremental) {
-        const uint8_t sd = seed[v];
-        dirty = (sd & 1u) != 0;
-        for (uint32_t r = r0; r < r1 && !dirty; ++r) dirty = (seed[refs[r] >> 8] & 2u) != 0;
-        if (dirty) {
-          seed[v] = sd | 2u;
-          if (srcpos[v] >= 0) A.pmark[(uint64_t)c * G.cap_nodes + (uint32_t)srcpos[v]] = 1;
-        }
-      }
-      if (!dirty) continue;  // inherited key already copied by k_materialise
-      B2bS<BT> st;
-      st.init(16, msg + threadIdx.x);
-      const uint32_t sg = sig[v];
-      append_sig_text(st, T, sg);
-      uint32_t wsid = aux[v];
-      if (T.sig_desc[sg].kind == EF_K_INPUT) {
-        const uint8_t* nm = T.names + T.name_off[wsid];
-        const uint32_t nl = T.name_len[wsid];
-        for (uint32_t i = 0; i < nl; ++i) st.byte(nm[i]);
-        wsid = kEmptyWset;
-      }
-      st.word_le(__ldg(T.ws_digest + 2 * wsid));
-      st.word_le(__ldg(T.ws_digest + 2 * wsid + 1));
-      for (uint32_t r = r0; r < r1; ++r) {
-        const uint32_t p = refs[r] >> 8, port = refs[r] & 255u;
-        st.word_le(keys[2 * p]);
-        st.word_le(keys[2 * p + 1]);
-        st.u16_be(port);
-      }
-      st.final();
-      keys[2 * v] = st.h[0];
-      keys[2 * v + 1] = st.h[1];
-    }
-  }
-}
-
-// positions a rewrite removes from the parent (same cases as plan_rewrite)
-__device__ __forceinline__ void dropped_of(uint32_t rule, uint32_t a, uint32_t b, int& d0, int& d1) {
-  d0 = d1 = -1;
-  switch (rule) {
-    case EF_R_FUSE_CONV_RELU:
-    case EF_R_FUSE_CONV_BN: d0 = (int)b; break;
-    case EF_R_MERGE_CONVS:
-    case EF_R_SPLIT_MERGED:
-      d0 = (int)min(a, b);
-      d1 = (int)max(a, b);
-      break;
-    case EF_R_FOLD_IDENTITY: d0 = (int)a; break;
-    default: break;
-  }
-}
-
-__device__ __forceinline__ bool key_lt(uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl) {
-  return ah < bh || (ah == bh && al < bl);
-}
-
-// dynamic smem: msg[16 * 32] u64 | skey[2 * sort_cap] u64 | spos[sort_cap] u32
-__global__ void __launch_bounds__(32) k_hash_top(HashArgs A) {
-  extern __shared__ __align__(16) uint64_t dsm[];
-  uint64_t* msg = dsm;
-  uint64_t* sk = dsm + 16 * 32;
-  uint32_t* sp = reinterpret_cast<uint32_t*>(sk + 2 * A.sort_cap);
-  const Geo& G = A.g;
-  const Tables& T = A.T;
-  const uint32_t total = A.total ? A.total[0] : A.n;
-  const int lane = threadIdx.x;
-  const uint32_t lt_mask = (1u << lane) - 1u;
-  for (uint32_t cb = blockIdx.x * 32; cb < total; cb += gridDim.x * 32) {
-    // 1) per record: sort the keys that are not inherited from the parent (all keys in full mode)
-    uint32_t my_d = 0;
-    for (int j = 0; j < 32 && cb + j < total; ++j) {
-      const uint32_t c = cb + j;
-      if (A.res && (A.res[c].flags & EF_F_INCOMPLETE)) continue;
-      Rec R{A.rec ? reinterpret_cast<char*>(A.rec[c]) : A.cand_base + (uint64_t)c * G.bytes};
-      const int n = R.h().n;
-      const uint64_t* keys = R.keys(G);
-      const uint8_t* seed = A.incremental ? A.seed + (uint64_t)c * G.cap_nodes : nullptr;
-      uint32_t d = 0;
-      for (int base = 0; base < n; base += 32) {
-        const int i = base + lane;
-        const bool fresh = i < n && (!seed || (seed[i] & 2u));
-        const uint32_t bal = __ballot_sync(0xffffffffu, fresh);
-        if (fresh) {
-          const uint32_t at = d + __popc(bal & lt_mask);
-          if (at < A.sort_cap) {
-            sk[2 * at] = B2b::bswap64(keys[2 * i]);
-            sk[2 * at + 1] = B2b::bswap64(keys[2 * i + 1]);
-            sp[at] = (uint32_t)i;
-          }
-        }
-        d += __popc(bal);
-      }
-      uint32_t m = 1;
-      while (m < d) m <<= 1;
-      if (m > A.sort_cap) {
-        if (lane == 0) {
-          atomicOr(A.err, 8u);
-          if (A.res) A.res[c].flags |= EF_F_INCOMPLETE;
-        }
-        continue;
-      }
-      for (uint32_t i = d + lane; i < m; i += 32) {
-        sk[2 * i] = ~0ULL;
-        sk[2 * i + 1] = ~0ULL;
-        sp[i] = 0xffffffffu;
-      }
-      __syncwarp();
-      for (uint32_t k = 2; k <= m; k <<= 1) {
-        for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
-          for (uint32_t i = lane; i < m; i += 32) {
-            const uint32_t ixj = i ^ jj;
-            if (ixj > i) {
-              const uint64_t ah = sk[2 * i], al = sk[2 * i + 1], bh = sk[2 * ixj], bl = sk[2 * ixj + 1];
-              const bool gt = key_lt(bh, bl, ah, al);
-              if (gt == ((i & k) == 0)) {
-                sk[2 * i] = bh;
-                sk[2 * i + 1] = bl;
-                sk[2 * ixj] = ah;
-                sk[2 * ixj + 1] = al;
-                const uint32_t t = sp[i];
-                sp[i] = sp[ixj];
-                sp[ixj] = t;
-              }
-            }
-          }
-          __syncwarp();
-        }
-      }
-      uint32_t* out = A.incremental ? A.sperm + (uint64_t)c * G.cap_nodes : R.sperm(G);
-      for (uint32_t i = lane; i < d; i += 32) out[i] = sp[i];
-      if (lane == j) my_d = d;
-      __syncwarp();
-    }
-    __syncwarp();
-    // 2) lane j: merge the parent's sorted order (minus removed positions) with the sorted
-    //    fresh keys, writing the record's sorted order and streaming the graph digest
-    const uint32_t c = cb + lane;
-    if (c < total && !(A.res && (A.res[c].flags & EF_F_INCOMPLETE))) {
-      Rec R{A.rec ? reinterpret_cast<char*>(A.rec[c]) : A.cand_base + (uint64_t)c * G.bytes};
-      const int n = R.h().n;
-      const uint64_t* keys = R.keys(G);
-      B2bS<32> st;
-      st.init(8, msg + lane);
-      for (uint32_t i = 0; i < T.input_text_len; ++i) st.byte(T.input_text[i]);
-      const uint32_t* outs = R.outs(G);
-      for (int o = 0; o < R.h().n_out; ++o) {
-        const uint32_t p = outs[o] >> 8, port = outs[o] & 255u;
-        st.word_le(keys[2 * p]);
-        st.word_le(keys[2 * p + 1]);
-        st.u16_be(port);
-      }
-      if (!A.incremental) {
-        const uint32_t* order = R.sperm(G);
-        uint64_t* skeys = R.skeys(G);
-        uint32_t* srank = R.srank(G);
-        for (int i = 0; i < n; ++i) {
-          const uint32_t v = order[i];
-          const uint64_t k0 = keys[2 * v], k1 = keys[2 * v + 1];
-          skeys[2 * i] = k0;
-          skeys[2 * i + 1] = k1;
-          srank[v] = (uint32_t)i;
-          st.word_le(k0);
-          st.word_le(k1);
-        }
-      } else {
-        const ef_cand_result& rr = A.res[c];
-        Rec P{reinterpret_cast<char*>(A.parent_addr[rr.parent])};
-        int d0, d1;
-        dropped_of(rr.rule, rr.site_a, rr.site_b, d0, d1);
-        const uint32_t pn = (uint32_t)P.h().n;
-        const uint32_t* porder = P.sperm(G);
-        const uint64_t* pkeys = P.keys(G);
-        const uint8_t* pmark = A.pmark + (uint64_t)c * G.cap_nodes;
-        const uint32_t* fresh = A.sperm + (uint64_t)c * G.cap_nodes;
-        uint32_t* order = R.sperm(G);
-        uint32_t i = 0, k = 0;
-        uint32_t pv = 0;
-        uint64_t ph = 0, pl = 0, fh = 0, fl = 0;
-        bool have_p = false, have_f = false;
-        for (int out = 0; out < n; ++out) {
-          if (!have_p) {
-            while (i < pn && pmark[porder[i]]) ++i;
-            if (i < pn) {
-              pv = porder[i];
-              ph = pkeys[2 * pv];
-              pl = pkeys[2 * pv + 1];
-              have_p = true;
-            }
-          }
-          if (!have_f && k < my_d) {
-            const uint32_t v = fresh[k];
-            fh = keys[2 * v];
-            fl = keys[2 * v + 1];
-            have_f = true;
-          }
-          const bool take_p = have_p && (!have_f || !key_lt(B2b::bswap64(fh), B2b::bswap64(fl), B2b::bswap64(ph),
-                                                             B2b::bswap64(pl)));
-          if (take_p) {
-            st.word_le(ph);
-            st.word_le(pl);
-            order[out] = pv - (uint32_t)(d0 >= 0 && (uint32_t)d0 < pv) - (uint32_t)(d1 >= 0 && (uint32_t)d1 < pv);
-            have_p = false;
-            ++i;
-          } else {
-            st.word_le(fh);
-            st.word_le(fl);
-            order[out] = fresh[k];
-            have_f = false;
-            ++k;
-          }
-        }
-      }
-      st.final();
-      const uint64_t h = B2b::bswap64(st.h[0]);
-      if (A.res) A.res[c].hash = h;
-      if (A.hash_out) A.hash_out[c] = h;
-    }
-    __syncwarp();
   }
 }
 

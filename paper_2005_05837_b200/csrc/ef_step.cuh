@@ -75,7 +75,15 @@ struct VArgs {
   const uint64_t* input_words;  // input text, 8-byte words, zero padded
   uint32_t* err;
   uint32_t one;  // == 1 at run time (keeps BLAKE2b additions on IMAD, see ef_b2b_fma.cuh)
+  // full mode (whole records: uploads, kept candidates): parent_addr[c] is record c itself,
+  // every node is a job, jv[c][j] = position of job j; graph hashes go to hash_out[c]
+  int full;
+  uint32_t* jv;
+  uint64_t* hash_out;
+  unsigned long long* stats;  // [0] k_keys compressions, [1] k_digest compressions (may be null)
 };
+
+constexpr uint32_t kInputJob = 0x80000000u;  // Job.nin flag: input node, aux = input-name id
 
 // ------------------------------------------------------------------------------------------
 // k_plan
@@ -328,9 +336,15 @@ __device__ __noinline__ void job_key_slow(const Tables& T, const Job jb, const u
   for (uint32_t i = 0; i < (len >> 3); ++i) st.word_le(tw[i]);
   const uint8_t* tail = T.sig_text + off + 8 * (len >> 3);
   for (uint32_t i = 0; i < (len & 7u); ++i) st.byte(tail[i]);
-  st.word_le(T.ws_digest[2 * jb.aux]);
-  st.word_le(T.ws_digest[2 * jb.aux + 1]);
-  for (uint32_t k = 0; k < jb.nin; ++k) {
+  const bool input = jb.nin & 0x80000000u;
+  if (input) {
+    const uint8_t* nm = T.names + T.name_off[jb.aux];
+    for (uint32_t i = 0; i < T.name_len[jb.aux]; ++i) st.byte(nm[i]);
+  }
+  const uint32_t ws = input ? 0u : jb.aux;
+  st.word_le(T.ws_digest[2 * ws]);
+  st.word_le(T.ws_digest[2 * ws + 1]);
+  for (uint32_t k = 0; k < (input ? 0u : jb.nin); ++k) {
     const uint32_t sv = rs[jb.roff + k];
     const uint32_t idx = sv & 0x7fffffu, port = (sv >> 23) & 255u;
     const uint64_t* kp = (sv & kFresh) ? fresh + 2 * idx : pkeys + 2 * idx;
@@ -358,17 +372,20 @@ __global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
     const uint32_t d = A.dcount[lc];
     if (d == 0) continue;
     const uint32_t c = A.c0 + lc;
-    const uint32_t parent = A.plan[c].parent;
-    const uint64_t* pkeys = Rec{reinterpret_cast<char*>(A.parent_addr[parent])}.keys(G);
+    const uint64_t* pkeys = A.full ? nullptr : Rec{reinterpret_cast<char*>(A.parent_addr[A.plan[c].parent])}.keys(G);
     const Job* jobs = A.jobs + (uint64_t)lc * A.S;
     const uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
     uint64_t* fresh = A.fresh + 2ull * lc * A.S;
     uint64_t* skey = A.skey + (uint64_t)lc * A.S;
     uint32_t* sval = A.sval + (uint64_t)lc * A.S;
+    uint32_t ncomp = 0;
     for (uint32_t jj = 0; jj < d; ++jj) {
       const Job jb = jobs[jj];
       const uint32_t tlen = T.sig_text_len[jb.sig];
-      const uint32_t len = tlen + 16u + 18u * jb.nin;
+      const bool input = jb.nin & kInputJob;
+      const uint32_t nin = input ? 0u : jb.nin;
+      const uint32_t nlen = input ? T.name_len[jb.aux] : 0u;
+      const uint32_t len = tlen + nlen + 16u + 18u * nin;
       uint64_t h[8];
       if (len > 8u * kKeyMaxW) {
         job_key_slow(T, jb, rs, pkeys, fresh, h);
@@ -379,9 +396,14 @@ __global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
         const uint32_t full = tlen >> 3;
         for (uint32_t i = 0; i < full; ++i) sk.push(__ldg(tw + i), 8);
         if (tlen & 7u) sk.push(__ldg(tw + full), tlen & 7u);
-        sk.push(__ldg(T.ws_digest + 2 * jb.aux), 8);
-        sk.push(__ldg(T.ws_digest + 2 * jb.aux + 1), 8);
-        for (uint32_t k = 0; k < jb.nin; ++k) {
+        const uint32_t ws = input ? kEmptyWset : jb.aux;
+        if (input) {  // graph.py:534-535: the input's name follows its signature text
+          const uint8_t* nm = T.names + T.name_off[jb.aux];
+          for (uint32_t i = 0; i < nlen; ++i) sk.push(nm[i], 1);
+        }
+        sk.push(__ldg(T.ws_digest + 2 * ws), 8);
+        sk.push(__ldg(T.ws_digest + 2 * ws + 1), 8);
+        for (uint32_t k = 0; k < nin; ++k) {
           const uint32_t sv = rs[jb.roff + k];
           const uint32_t idx = sv & 0x7fffffu, port = (sv >> 23) & 255u;
           const uint64_t* kp = (sv & kFresh) ? fresh + 2 * idx : pkeys + 2 * idx;
@@ -393,6 +415,7 @@ __global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
         const uint32_t nb = (len + 127u) >> 7;
         for (uint32_t q = sk.q; q < 16u * nb; ++q) col[q * BT] = 0;
         b2b_start(h, 16);
+        ncomp += nb;
         for (uint32_t b = 0; b < nb; ++b) {
           uint64_t m[16];
 #pragma unroll
@@ -405,6 +428,7 @@ __global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
       skey[jj] = B2b::bswap64(h[0]);
       sval[jj] = jj;
     }
+    if (A.stats) atomicAdd(A.stats, (unsigned long long)ncomp);
   }
 }
 
@@ -474,10 +498,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_sortkeys(VArgs A) {
       __syncwarp();
     }
     uint64_t* dst = A.fresh_sorted + 2ull * lc * A.S;
+    uint32_t* dsv = A.sval_sorted + (uint64_t)lc * A.S;
     for (uint32_t i = lane; i < d; i += 32) {
       const uint32_t v = sv[i];
       dst[2 * i] = fresh[2 * v];
       dst[2 * i + 1] = fresh[2 * v + 1];
+      if (A.full) dsv[i] = v;
     }
     __syncwarp();
   }
@@ -529,8 +555,18 @@ __global__ void __launch_bounds__(BT) k_digest(VArgs A) {
   uint64_t* col = blk + threadIdx.x;
   for (uint32_t lc = blockIdx.x * BT + threadIdx.x; lc < A.n; lc += gridDim.x * BT) {
     const uint32_t c = A.c0 + lc;
-    if (A.res[c].flags & EF_F_INCOMPLETE) continue;
-    const VPlan P = A.plan[c];
+    VPlan P;
+    if (A.full) {  // the record itself, everything fresh
+      P.drop0 = P.drop1 = P.mod = -1;
+      P.n_rm = 0;
+      P.pn = 0;
+      P.n_keep = Rec{reinterpret_cast<char*>(A.parent_addr[c])}.h().n;
+      P.n_live = 0;
+      P.parent = c;
+    } else {
+      if (A.res[c].flags & EF_F_INCOMPLETE) continue;
+      P = A.plan[c];
+    }
     Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
     const uint64_t* pkeys = R.keys(G);
     const uint32_t* pouts = R.outs(G);
@@ -671,7 +707,90 @@ __global__ void __launch_bounds__(BT) k_digest(VArgs A) {
       for (int i = 0; i < 16; ++i) m[i] = col[i * BT];
       b2b_compress(h, m, len < 128ull * (b + 1) ? len : 128ull * (b + 1), b + 1 == nblk);
     }
-    A.res[c].hash = B2b::bswap64(h[0]);
+    if (A.full) A.hash_out[c] = B2b::bswap64(h[0]);
+    else A.res[c].hash = B2b::bswap64(h[0]);
+    if (A.stats) atomicAdd(A.stats + 1, (unsigned long long)nblk);
+  }
+}
+
+// full mode: one job per node in topological order; every producer key is fresh
+__global__ void k_full_jobs(VArgs A) {
+  const Geo& G = A.g;
+  const Tables& T = A.T;
+  for (uint32_t lc = blockIdx.x * blockDim.x + threadIdx.x; lc < A.n; lc += gridDim.x * blockDim.x) {
+    const uint32_t c = A.c0 + lc;
+    Rec R{reinterpret_cast<char*>(A.parent_addr[c])};
+    const int n = R.h().n;
+    const uint32_t* topo = R.topo(G);
+    const uint32_t* sig = R.sig(G);
+    const uint32_t* aux = R.aux(G);
+    const uint32_t* nin = R.nin(G);
+    const uint32_t* inoff = R.inoff(G);
+    const uint32_t* refs = R.refs(G);
+    uint32_t* didx = A.didx + (uint64_t)lc * A.S;
+    uint32_t* jv = A.jv + (uint64_t)lc * A.S;
+    Job* jobs = A.jobs + (uint64_t)lc * A.S;
+    uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
+    uint32_t r = 0;
+    for (int s = 0; s < n; ++s) {
+      const uint32_t v = topo[s];
+      const uint32_t sg = sig[v];
+      if (T.sig_desc[sg].kind == EF_K_INPUT) {
+        jobs[s] = Job{sg, aux[v], 0u, kInputJob};
+      } else {
+        const uint32_t r0 = inoff[v], nr = nin[v];
+        for (uint32_t k = 0; k < nr; ++k) {
+          const uint32_t ref = refs[r0 + k];
+          rs[r + k] = kFresh | ((ref & 255u) << 23) | (didx[ref >> 8] - 1);
+        }
+        jobs[s] = Job{sg, aux[v], r, nr};
+        r += nr;
+      }
+      didx[v] = (uint32_t)s + 1;
+      jv[s] = v;
+    }
+    A.dcount[lc] = (uint32_t)n;
+    A.seg_begin[lc] = (int32_t)((uint64_t)lc * A.S);
+    A.seg_end[lc] = (int32_t)((uint64_t)lc * A.S + n);
+  }
+}
+
+// full mode: write the node keys, the sorted order, the sorted keys and the ranks into the
+// record (block per record, coalesced)
+__global__ void k_full_store(VArgs A) {
+  const Geo& G = A.g;
+  for (uint32_t lc = blockIdx.x; lc < A.n; lc += gridDim.x) {
+    const uint32_t c = A.c0 + lc;
+    Rec R{reinterpret_cast<char*>(A.parent_addr[c])};
+    const int n = R.h().n;
+    const uint32_t* didx = A.didx + (uint64_t)lc * A.S;
+    const uint32_t* jv = A.jv + (uint64_t)lc * A.S;
+    const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
+    const uint64_t* fs = A.fresh_sorted + 2ull * lc * A.S;
+    const uint32_t* sv = A.sval_sorted + (uint64_t)lc * A.S;
+    uint64_t* keys = R.keys(G);
+    uint64_t* skeys = R.skeys(G);
+    uint32_t* sperm = R.sperm(G);
+    uint32_t* srank = R.srank(G);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint32_t j = didx[i] - 1;
+      keys[2 * i] = fresh[2 * j];
+      keys[2 * i + 1] = fresh[2 * j + 1];
+      const uint32_t v = jv[sv[i]];
+      sperm[i] = v;
+      srank[v] = (uint32_t)i;
+      skeys[2 * i] = fs[2 * i];
+      skeys[2 * i + 1] = fs[2 * i + 1];
+    }
+  }
+}
+
+// step-wide maxima of record sizes (sizes the full-mode scratch)
+__global__ void k_rec_max(const unsigned long long* rec, uint32_t n, uint32_t* out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const ef_rec_header& H = *reinterpret_cast<const ef_rec_header*>(rec[i]);
+    atomicMax(out, (uint32_t)H.n);
+    atomicMax(out + 1, (uint32_t)H.n_refs);
   }
 }
 
@@ -744,6 +863,128 @@ __global__ void k_keep_alg(const uint8_t* alg8, uint32_t S, const uint32_t* cand
     const uint8_t* src = alg8 + (uint64_t)cand[k] * S;
     uint8_t* out = C.alg(G);
     for (int i = threadIdx.x; i < nn; i += blockDim.x) out[i] = src[i];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// hash-owner sharding: every candidate's (hash, global order) goes to rank hash % world,
+// which decides first occurrence (smallest global order over all ranks) and membership in
+// its shard of the visited set; the verdicts come back in send order.
+// ------------------------------------------------------------------------------------------
+
+struct RouteArgs {
+  const ef_cand_result* res;
+  uint32_t total, world;
+  uint64_t order_base;
+  uint32_t* count;   // [world]
+  uint32_t* cursor;  // [world] exclusive offsets (host-computed), advanced by the scatter
+  uint64_t* send;    // [n_send][2]
+  uint32_t* perm;    // send position -> candidate
+};
+
+__device__ __forceinline__ uint32_t owner_of(uint64_t h, uint32_t world) { return (uint32_t)(h % world); }
+
+__global__ void k_route_count(RouteArgs R) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < R.total; c += gridDim.x * blockDim.x) {
+    const ef_cand_result& r = R.res[c];
+    if (r.flags & EF_F_INCOMPLETE) continue;
+    atomicAdd(&R.count[owner_of(r.hash, R.world)], 1u);
+  }
+}
+
+__global__ void k_route_scatter(RouteArgs R) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < R.total; c += gridDim.x * blockDim.x) {
+    const ef_cand_result& r = R.res[c];
+    if (r.flags & EF_F_INCOMPLETE) continue;
+    const uint32_t pos = atomicAdd(&R.cursor[owner_of(r.hash, R.world)], 1u);
+    R.send[2 * (uint64_t)pos] = r.hash;
+    R.send[2 * (uint64_t)pos + 1] = R.order_base + c;
+    R.perm[pos] = c;
+  }
+}
+
+struct OwnerArgs {
+  const uint64_t* recv;  // [n][2] (hash, global order)
+  uint32_t n;
+  uint32_t* verdict;     // [n] EF_F_FIRST | EF_F_VISITED
+  unsigned long long* key;
+  unsigned long long* ord;
+  uint32_t mask;
+  unsigned long long* vis_key;
+  uint32_t vis_mask;
+  unsigned long long* vis_count;
+};
+
+__global__ void k_owner_claim(OwnerArgs O) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < O.n; i += gridDim.x * blockDim.x) {
+    const uint64_t h = O.recv[2 * (uint64_t)i];
+    const unsigned long long key = h ? h : 0x8000000000000000ULL;
+    for (uint32_t s = (uint32_t)mix64(h) & O.mask;; s = (s + 1) & O.mask) {
+      const unsigned long long prev = atomicCAS(&O.key[s], 0ULL, key);
+      if (prev == 0ULL || prev == key) {
+        atomicMin(&O.ord[s], (unsigned long long)O.recv[2 * (uint64_t)i + 1]);
+        break;
+      }
+    }
+  }
+}
+
+__global__ void k_owner_resolve(OwnerArgs O) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < O.n; i += gridDim.x * blockDim.x) {
+    const uint64_t h = O.recv[2 * (uint64_t)i];
+    const unsigned long long key = h ? h : 0x8000000000000000ULL;
+    unsigned long long first = ~0ULL;
+    for (uint32_t s = (uint32_t)mix64(h) & O.mask;; s = (s + 1) & O.mask) {
+      if (O.key[s] == key) {
+        first = O.ord[s];
+        break;
+      }
+    }
+    uint32_t v = first == O.recv[2 * (uint64_t)i + 1] ? EF_F_FIRST : 0u;
+    if (vis_contains(O.vis_key, O.vis_mask, key, h)) v |= EF_F_VISITED;
+    O.verdict[i] = v;
+  }
+}
+
+__global__ void k_owner_insert(OwnerArgs O) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < O.n; i += gridDim.x * blockDim.x) {
+    if (O.verdict[i] != EF_F_FIRST) continue;
+    const uint64_t h = O.recv[2 * (uint64_t)i];
+    const unsigned long long key = h ? h : 0x8000000000000000ULL;
+    for (uint32_t s = (uint32_t)mix64(h) & O.vis_mask;; s = (s + 1) & O.vis_mask) {
+      const unsigned long long prev = atomicCAS(&O.vis_key[s], 0ULL, key);
+      if (prev == 0ULL) {
+        atomicAdd(O.vis_count, 1ULL);
+        break;
+      }
+      if (prev == key) break;
+    }
+  }
+}
+
+// verdicts (send order) -> candidate flags, node cap, survivors appended to the price list
+__global__ void k_apply_verdicts(ef_cand_result* res, const uint32_t* perm, const uint32_t* verdict, uint32_t n,
+                                 int node_cap, uint32_t* plist, uint32_t* plist_n) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t span = (n + 31) / 32 * 32;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < span; i += gridDim.x * blockDim.x) {
+    bool survivor = false;
+    uint32_t c = 0;
+    if (i < n) {
+      c = perm[i];
+      uint32_t f = res[c].flags | (verdict[i] & (EF_F_FIRST | EF_F_VISITED));
+      if (res[c].n_compute > node_cap) f |= EF_F_CAPPED;
+      res[c].flags = f;
+      survivor = (f & (EF_F_FIRST | EF_F_VISITED | EF_F_CAPPED)) == EF_F_FIRST;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, survivor);
+    if (m) {
+      uint32_t base = 0;
+      const int leader = __ffs(m) - 1;
+      if ((int)lane == leader) base = atomicAdd(plist_n, (uint32_t)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (survivor) plist[base + __popc(m & ((1u << lane) - 1u))] = c;
+    }
   }
 }
 

@@ -460,6 +460,44 @@ class DeviceSession:
             self._check(self.L.ef_results(self.ctx, out.ctypes.data, n), "ef_results")
         return out
 
+    # ---- hash-owner sharding (see shard.py) ------------------------------------------
+
+    def expand_hashes(self, slots: list[int], rule_ids: list[int]) -> int:
+        """Match, plan and hash the candidates of `slots` (no dedup, no pricing)."""
+        parents = N.u32_array(slots)
+        rules = N.i32_array(rule_ids)
+        count = C.c_uint32(0)
+        for attempt in range(8):
+            rc = self.L.ef_expand_hashes(self.ctx, parents, len(slots), rules, len(rule_ids), C.byref(count))
+            if rc == N.EF_NEED_RESOLVE:
+                if attempt >= 3:
+                    raise N.NativeError(f"ef_expand_hashes keeps asking for interning: {self._pending_summary()}")
+                self.resolve_pending()
+                continue
+            self._check(rc, "ef_expand_hashes")
+            return count.value
+        raise N.NativeError("ef_expand_hashes did not converge")
+
+    def route_owners(self, world: int, order_base: int, send) -> list[int]:
+        """`send`: int64 CUDA tensor with room for 2 * candidates (hash, global order) pairs."""
+        counts = (C.c_uint32 * max(1, world))()
+        self._check(self.L.ef_route_owners(self.ctx, world, order_base, C.c_void_p(send.data_ptr()), counts),
+                    "ef_route_owners")
+        return [int(counts[i]) for i in range(world)]
+
+    def owner_mark(self, recv, verdict, insert_visited: bool) -> None:
+        """`recv`: int64 CUDA tensor of pairs from every rank; `verdict`: int32 CUDA tensor, one per pair."""
+        self._check(self.L.ef_owner_mark(self.ctx, C.c_void_p(recv.data_ptr()), recv.numel() // 2,
+                                         C.c_void_p(verdict.data_ptr()), int(insert_visited)), "ef_owner_mark")
+
+    def expand_finish(self, verdict_back, pp: N.PriceParams, n: int) -> np.ndarray:
+        self._check(self.L.ef_expand_finish(self.ctx, C.c_void_p(verdict_back.data_ptr()), C.byref(pp)),
+                    "ef_expand_finish")
+        out = np.empty(n, dtype=N.CAND_DTYPE)
+        if n:
+            self._check(self.L.ef_results(self.ctx, out.ctypes.data, n), "ef_results")
+        return out
+
     def keep(self, cand_idx: list[int]) -> list[int]:
         slots = [self.alloc() for _ in cand_idx]
         self._check(self.L.ef_keep(self.ctx, N.u32_array(cand_idx), len(cand_idx), N.u32_array(slots)), "ef_keep")

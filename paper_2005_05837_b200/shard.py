@@ -1,0 +1,98 @@
+"""Hash-owner sharding of the frontier step over ranks (one process per GPU).
+
+The reference deduplicates every generated graph against one visited set and
+keeps the first graph per hash in (rule, site) order (rules.py:79-88,
+search.py:245-251).  Across ranks the frontier is split by parent, so the
+global candidate order is rank-major, and deduplication is owned by hash: rank
+`hash % world` receives every (hash, global order) pair it owns, decides first
+occurrence (smallest global order) and membership in its shard of the visited
+set, and sends the verdicts back.  The result on every rank is exactly the
+single-rank result for the concatenated frontier (tests/test_shard.py).
+
+`OwnerExchange` is the collective layer (torch.distributed: NCCL over NVLink on
+the GPUs, gloo in the CPU tests); the per-rank work is the device session's
+`expand_hashes` / `route_owners` / `owner_mark` / `expand_finish` (libef200).
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def owner_of(h: int, world: int) -> int:
+    """Rank owning a candidate hash (same rule as csrc/ef_step.cuh owner_of)."""
+    return h % world
+
+
+class OwnerExchange:
+    """All-to-all of (hash, order) pairs to their owners and of verdicts back."""
+
+    def __init__(self, group=None, device: torch.device | None = None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.device = device if device is not None else torch.device("cpu")
+
+    def _sync(self):
+        if self.device.type == "cuda":
+            torch.cuda.current_stream(self.device).synchronize()
+
+    def order_base(self, n: int) -> tuple[int, int]:
+        """(first global candidate index of this rank, total over ranks)."""
+        t = torch.tensor([n], dtype=torch.int64, device=self.device)
+        parts = [torch.zeros_like(t) for _ in range(self.world)]
+        dist.all_gather(parts, t, group=self.group)
+        counts = [int(p.item()) for p in parts]
+        return sum(counts[: self.rank]), sum(counts)
+
+    def to_owners(self, send: torch.Tensor, counts: list[int]) -> tuple[torch.Tensor, list[int]]:
+        """`send` holds sum(counts) pairs grouped by owner; returns the pairs this rank owns
+        (grouped by source rank) and how many came from each source."""
+        c = torch.tensor(counts, dtype=torch.int64, device=self.device)
+        rc = torch.empty_like(c)
+        dist.all_to_all_single(rc, c, group=self.group)
+        recv_counts = [int(x) for x in rc.tolist()]
+        recv = torch.empty(2 * sum(recv_counts), dtype=torch.int64, device=self.device)
+        dist.all_to_all_single(recv, send[: 2 * sum(counts)].contiguous(), [2 * x for x in recv_counts],
+                               [2 * x for x in counts], group=self.group)
+        self._sync()
+        return recv, recv_counts
+
+    def back(self, verdict: torch.Tensor, recv_counts: list[int], counts: list[int]) -> torch.Tensor:
+        """Owner verdicts (in receive order) back to the senders (in send order)."""
+        out = torch.empty(max(sum(counts), 1), dtype=torch.int32, device=self.device)
+        dist.all_to_all_single(out[: sum(counts)], verdict[: sum(recv_counts)].contiguous(), counts, recv_counts,
+                               group=self.group)
+        self._sync()
+        return out
+
+    def min(self, x: float) -> float:
+        """Global best cost for the alpha rule (all-reduce MIN)."""
+        t = torch.tensor([x], dtype=torch.float64, device=self.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        t = torch.tensor([x], dtype=torch.float64, device=self.device)
+        dist.all_reduce(t, group=self.group)
+        return float(t.item())
+
+
+def sharded_expand(session, slots: list[int], rule_ids: list[int], pp, ex: OwnerExchange,
+                   insert_visited: bool = False):
+    """One frontier step over the parents of this rank with hash-owner deduplication.
+
+    Returns this rank's candidate results (the layout of `DeviceSession.expand`);
+    flags FIRST / VISITED are global, costs are those of this rank's survivors.
+    """
+    n = session.expand_hashes(slots, rule_ids)
+    base, _ = ex.order_base(n)
+    send = torch.empty(max(2 * n, 2), dtype=torch.int64, device=ex.device)
+    counts = session.route_owners(ex.world, base, send)
+    recv, recv_counts = ex.to_owners(send, counts)
+    verdict = torch.empty(max(recv.numel() // 2, 1), dtype=torch.int32, device=ex.device)
+    if recv.numel():
+        session.owner_mark(recv, verdict, insert_visited)
+    back = ex.back(verdict, recv_counts, counts)
+    return session.expand_finish(back, pp, n)

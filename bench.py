@@ -1,19 +1,26 @@
 """Benchmark: candidate graphs priced per second on the frontier of a search.
 
 A step = one frontier expansion of a batch of parent graphs resident in HBM:
-every substitution rule at every match site of every parent, materialisation,
-canonical hashing, dedup (within the step and against the visited set) and
-the inner search on every survivor (libef200 `ef_expand`).  The workload is
+every substitution rule at every match site of every parent, the rewrite plans,
+canonical hashing, deduplication (within the step and against the visited set)
+and the inner search on every survivor (libef200 `ef_expand`).  The workload is
 BASELINE.json configs[1]: ResNet-50 inference graph, energy objective with
-per-node algorithm selection, alpha = 1.05; the parents are the real frontier
-of that search (the first graphs its best-first order enqueues).
+per-node algorithm selection, alpha = 1.05; the parents are the real frontier of
+that search (the graphs its best-first order enqueues first), --parents per GPU.
 
-`value`  = candidates priced / s, device time (CUDA events on the library's
-           stream), inputs already in HBM; max over ranks for N > 1.
-`e2e`    = the same metric through the C ABI with host buffers: parent
-           records copied host->device and results copied back every step.
-`--impl reference` times the CPU oracle (oracle/, a restatement of the
-reference's Python code path) on a bounded sample of the same workload.
+`value`  candidates priced / s over all ranks: device time of the step (CUDA
+         events), inputs already in HBM, L2 flushed before every step; max over
+         ranks.  With N > 1 GPUs the frontier is split by parent and
+         deduplication is owned by hash (NCCL all-to-all, shard.py).
+`e2e`    the same metric through the C ABI from host memory: compact parent
+         records (used bytes only, pinned) copied host->device, unpacked and
+         hashed on the device, the step, and every candidate's result copied
+         back, all inside the timed region.
+`roofline`  the dominant kernel (k_keys: node-key BLAKE2b) is integer-ALU bound;
+         its compression rate against the live register-only BLAKE2b rate of the
+         same GPU.  `roofline_hbm` gives its algorithmic bytes against HBM.
+`cpu_baseline` / `--impl reference`: the oracle restatement of the reference's
+         path (oracle/, pinned to the reference's golden vectors) on the host.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -35,15 +42,17 @@ MODEL = "resnet50"
 CONFIG_NAME = "ResNet-50 inference graph, energy objective with per-node conv-algorithm selection, alpha=1.05"
 METRIC = "candidate graphs priced/sec"
 UNIT = "candidates/s"
+RULES = ["fuse-conv-relu", "split-conv-activation", "merge-parallel-convs", "split-merged-conv", "fold-identity",
+         "fuse-conv-batchnorm"]
 
 
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             p = json.load(fh)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class Clocks:
@@ -51,7 +60,6 @@ class Clocks:
 
     def __init__(self):
         self.proc = None
-        self.rows = []
 
     def start(self):
         try:
@@ -89,32 +97,13 @@ class Clocks:
 
 
 def _dist():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
-
-
-def _setup_workload(n_parents: int, world: int, rank: int):
-    import paper_2005_05837_b200 as ef
-    from paper_2005_05837_b200 import zoo
-    from paper_2005_05837_b200.frontier import Frontier
-
-    g0 = zoo.generate(MODEL, 0)
-    db = ef.CostDatabase()
-    prof = ef.SyntheticProfiler(0)
-    fr = Frontier(g0, db, prof, ef.CostFunction.energy(), ef.SearchConfig(alpha=1.05), n_parents * world)
-    # weak scaling: this rank owns its slice of the frontier (graphs are independent objects)
-    mine = fr.slots[rank * n_parents:(rank + 1) * n_parents]
-    return ef, g0, db, fr, mine
+    return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
 def _to_oracle(g):
     """Package Graph -> oracle graph dict, sharing the weight arrays (no copies)."""
-    nodes = {}
-    for nid, v in g.nodes.items():
-        nodes[nid] = {"kind": v.kind.value, "ins": [(r.node, r.port) for r in v.inputs],
-                      "p": dict(v.params), "w": dict(v.weights)}
+    nodes = {nid: {"kind": v.kind.value, "ins": [(r.node, r.port) for r in v.inputs], "p": dict(v.params),
+                   "w": dict(v.weights)} for nid, v in g.nodes.items()}
     return {"inputs": [(n, tuple(s.dims)) for n, s in g.inputs], "nodes": nodes,
             "outputs": [(r.node, r.port) for r in g.outputs]}
 
@@ -128,142 +117,170 @@ def _oracle_db(db):
     return odb
 
 
-def _oracle_expand(parent, odb, seed: int, visited: set) -> tuple[int, int]:
-    """The reference's per-expansion work on one parent: neighbors (rewrite + hash +
-    in-expansion dedup), visited dedup, profiling and the inner search of every survivor."""
+def _oracle_expand(parent, odb, visited: set) -> tuple[int, int]:
+    """The reference's per-expansion work on one parent (search.py:245-267): neighbors
+    (rewrite + canonical hash + in-expansion dedup), visited dedup, profiling of new
+    signatures and the inner search of every survivor."""
     from oracle import enerflow_oracle as orc
 
     f = orc.CostFn("energy")
-    rules = ["fuse-conv-relu", "split-conv-activation", "merge-parallel-convs", "split-merged-conv",
-             "fold-identity", "fuse-conv-batchnorm"]
     generated = priced = 0
-    for cand in orc.neighbors(parent, rules):
+    for cand in orc.neighbors(parent, RULES):
         generated += 1
         h = orc.canonical_hash(cand)
         if h in visited:
             continue
         visited.add(h)
-        orc.ensure_profiled(cand, odb, seed)
+        orc.ensure_profiled(cand, odb, 0)
         orc.sweep(cand, odb, f, 1)
         priced += 1
     return generated, priced
 
 
-def _cpu_sample(parents, db, budget_s: float) -> dict:
-    odb = _oracle_db(db)
-    t0 = time.perf_counter()
-    priced = generated = expanded = 0
-    visited: set = set()
-    for p in parents:
-        gen, pr = _oracle_expand(p, odb, 0, visited)
-        generated += gen
-        priced += pr
-        expanded += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": priced / dt, "priced": priced, "generated": generated, "expanded": expanded, "seconds": dt}
+# ---------------------------------------------------------------------------------------------
+# reference arm: the oracle port of the reference's path on every host core
+# ---------------------------------------------------------------------------------------------
+
+_REF_STATE: dict = {}
+
+
+def _ref_worker(i: int) -> int:
+    parents, odb = _REF_STATE["parents"], _REF_STATE["odb"]
+    return _oracle_expand(parents[i % len(parents)], odb, set())[1]
 
 
 def run_reference(args, world, rank):
     if rank != 0:
         return 0
-    import paper_2005_05837_b200 as ef  # host IR only (graph builder + profiler), no GPU
-    from paper_2005_05837_b200 import zoo
-    from oracle import enerflow_oracle as orc
+    import multiprocessing as mp
 
-    # the same frontier, built on the CPU with the oracle (no GPU on this arm)
+    import paper_2005_05837_b200 as ef  # host IR only (graph builder + profiler), no GPU
+    from oracle import enerflow_oracle as orc
+    from paper_2005_05837_b200 import zoo
+
     g0 = zoo.generate(MODEL, 0)
     db = ef.CostDatabase()
     ef.ensure_profiled(g0, db, ef.SyntheticProfiler(0))
     og = _to_oracle(g0)
     odb = _oracle_db(db)
-    frontier = [og]
-    for cand in orc.neighbors(og, ["fuse-conv-relu", "split-conv-activation", "merge-parallel-convs",
-                                   "split-merged-conv", "fold-identity", "fuse-conv-batchnorm"]):
-        frontier.append(cand)
-        if len(frontier) >= args.steps + args.warmup + 1:
-            break
+    cores = os.cpu_count() or 1
+    # frontier graphs: the origin and its rewrites (the first level the search enqueues)
+    parents = [og] + orc.neighbors(og, RULES)
+    _REF_STATE.update(parents=parents, odb=odb)
+    ctx = mp.get_context("fork")  # workers inherit the graphs (weights are not pickled)
     times, priced = [], []
-    for i in range(args.warmup + args.steps):
-        visited: set = set()
-        t0 = time.perf_counter()
-        _, pr = _oracle_expand(frontier[i % len(frontier)], odb, 0, visited)
-        dt = time.perf_counter() - t0
-        if i >= args.warmup:
-            times.append(dt)
-            priced.append(pr)
+    with ctx.Pool(cores) as pool:
+        nxt = 0
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            got = pool.map(_ref_worker, range(nxt, nxt + cores), chunksize=1)
+            dt = time.perf_counter() - t0
+            nxt += cores
+            if i >= args.warmup:
+                times.append(dt)
+                priced.append(sum(got))
     value = sum(priced) / sum(times)
+    sample = (f"each step: {cores} ResNet-50 frontier expansions in parallel ({cores} processes), "
+              f"{sum(priced)} candidates priced over {args.steps} steps")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+u64",
-            "data": "synthetic (random-init weights, synthetic profiler seed 0)",
-            "config": {"workload": CONFIG_NAME, "model": MODEL, "parents_per_step": 1,
-                       "sample": "one frontier expansion per step (oracle restatement of reference search.py)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-                             "sample": f"{args.steps} expansions of ResNet-50 frontier graphs, "
-                                       f"{sum(priced)} candidates priced"},
+            "data": "synthetic (random-init float64 weights, synthetic profiler seed 0)",
+            "config": {"workload": CONFIG_NAME, "model": MODEL, "rules": "all 6", "inner_search_d": 1},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
 
 
+def _cpu_sample(parents, db, budget_s: float) -> dict:
+    odb = _oracle_db(db)
+    t0 = time.perf_counter()
+    priced = expanded = 0
+    visited: set = set()
+    for p in parents:
+        priced += _oracle_expand(p, odb, visited)[1]
+        expanded += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": priced / dt, "priced": priced, "expanded": expanded, "seconds": dt}
+
+
+# ---------------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------------
+
 def run_ours(args, world, rank, local):
     import ctypes as C
 
     import numpy as np
+    import torch
 
-    ef, g0, db, fr, mine = _setup_workload(args.parents, world, rank)
+    import paper_2005_05837_b200 as ef
     from paper_2005_05837_b200 import _native as N
+    from paper_2005_05837_b200 import zoo
+    from paper_2005_05837_b200.frontier import Frontier
 
-    s = fr.s
-    dist = None
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = ex = sharded_expand = None
     if world > 1:
-        import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2005_05837_b200.shard import OwnerExchange, sharded_expand
+
+        dist.init_process_group("nccl", device_id=dev)
+        ex = OwnerExchange(device=dev)
+
+    g0 = zoo.generate(MODEL, 0)
+    db = ef.CostDatabase()
+    fr = Frontier(g0, db, ef.SyntheticProfiler(0), ef.CostFunction.energy(), ef.SearchConfig(alpha=1.05),
+                  args.parents * world)
+    # weak scaling: this rank owns its slice of the frontier (graphs are independent objects)
+    mine = fr.slots[rank * args.parents:(rank + 1) * args.parents]
+    s = fr.s
 
     def barrier():
         if dist is not None:
             dist.barrier()
 
-    # L2 flush buffer (written between timed steps; the step's own arena already exceeds L2)
-    flush_bytes = 256 << 20
-    flush = None
-    try:
-        import torch
-
-        flush = torch.empty(flush_bytes, dtype=torch.uint8, device=f"cuda:{local}")
-    except Exception:
-        flush = None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2 (126 MB)
 
     def flush_l2():
-        if flush is not None:
-            flush.fill_(1)
-            torch.cuda.synchronize()
+        flush.fill_(1)
+        torch.cuda.synchronize()
 
-    def step():
-        res = fr.step(mine, insert_visited=False)
-        return res, s.last_timing()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def step(slots):
+        """-> (results, device ms of the step)."""
+        if ex is None:
+            res = fr.step(slots, insert_visited=False)
+            return res, sum(s.last_timing())
+        ev0.record()
+        res = sharded_expand(s, slots, fr.rule_ids, fr.pp, ex)
+        ev1.record()
+        ev1.synchronize()
+        return res, ev0.elapsed_time(ev1)
 
     for _ in range(args.warmup):
-        step()
+        step(mine)
     prof = os.environ.get("EF_NCU") == "1"  # ncu --profile-from-start off: capture the timed steps only
     if prof:
-        import torch
-
         torch.cuda.profiler.start()
     clocks = Clocks()
     clocks.start()
-    dev_ms, stage_ms, priced_n, gen_n = [], [0.0] * 5, 0, 0
+    dev_ms, stage_ms, priced_n, gen_n, kcomp, dcomp = [], [0.0] * 8, 0, 0, 0, 0
     for _ in range(args.steps):
         flush_l2()
         barrier()
-        res, ms = step()
-        dev_ms.append(sum(ms))
-        stage_ms = [a + b for a, b in zip(stage_ms, ms)]
+        res, ms = step(mine)
+        dev_ms.append(ms)
+        stage_ms = [a + b for a, b in zip(stage_ms, s.last_timing())]
+        st = s.last_stats()
+        kcomp += st["key_compressions"]
+        dcomp += st["digest_compressions"]
         priced_n += int(np.count_nonzero(res["flags"] & N.F_PRICED))
         gen_n += len(res)
     clk = clocks.stop(local)
@@ -271,100 +288,85 @@ def run_ours(args, world, rank, local):
         torch.cuda.profiler.stop()
         if rank == 0:
             print(json.dumps({"ncu_capture": True, "stages_ms": stage_ms}))
+        fr.close()
         return 0
     total_ms = sum(dev_ms)
-    if dist is not None:
-        import torch
-
-        t = torch.tensor([total_ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-        pr = torch.tensor([float(priced_n)], device=f"cuda:{local}")
-        dist.all_reduce(pr)
-        priced_all = float(pr.item())
-    else:
-        priced_all = float(priced_n)
+    priced_all = float(priced_n)
+    if ex is not None:
+        total_ms = -ex.min(-total_ms)  # max over ranks
+        priced_all = ex.sum(float(priced_n))
     value = priced_all / (total_ms / 1e3)
 
-    # e2e through the C ABI with host buffers: parent records H2D, results D2H, every step
+    # e2e through the C ABI from host memory: compact parents H2D + unpack + hash, step, results D2H
     host_recs = [s.read_record(sl) for sl in mine]
-    rec_bytes = host_recs[0].nbytes
+    blob, offs = s.pack(host_recs)
+    pinned = s.L.ef_host_alloc(blob.nbytes)
+    staging = np.ctypeslib.as_array((C.c_uint8 * blob.nbytes).from_address(pinned))
+    staging[:] = blob.view(np.uint8)
     e2e_slots = [s.alloc() for _ in mine]
-    pinned = s.L.ef_host_alloc(rec_bytes * len(mine))
-    staging = np.ctypeslib.as_array((C.c_uint8 * (rec_bytes * len(mine))).from_address(pinned))
-    for i, buf in enumerate(host_recs):
-        staging[i * rec_bytes:(i + 1) * rec_bytes] = buf
-    slot_arr = N.u32_array(e2e_slots)
-    e2e_times, e2e_priced = [], 0
+    e2e_ms, e2e_priced, n_cand = [], 0, 0
     for i in range(args.warmup + args.steps):
         flush_l2()
         barrier()
-        t0 = time.perf_counter()
-        s._check(s.L.ef_records_write(s.ctx, slot_arr, len(e2e_slots), pinned, rec_bytes, rec_bytes),
-                 "ef_records_write")
-        res = fr.step(e2e_slots, insert_visited=False)
-        dt = time.perf_counter() - t0
+        ev0.record()
+        s.write_packed(e2e_slots, staging.view(np.uint32), offs)
+        res, _ = step(e2e_slots)
+        ev1.record()
+        ev1.synchronize()
         if i >= args.warmup:
-            e2e_times.append(dt)
+            e2e_ms.append(ev0.elapsed_time(ev1))
             e2e_priced += int(np.count_nonzero(res["flags"] & N.F_PRICED))
-    n_cand = len(res)
+            n_cand = len(res)
+    del staging
     s.L.ef_host_free(pinned)
-    e2e_total = sum(e2e_times)
-    if dist is not None:
-        import torch
+    e2e_total, e2e_all = sum(e2e_ms), float(e2e_priced)
+    if ex is not None:
+        e2e_total = -ex.min(-e2e_total)
+        e2e_all = ex.sum(e2e_all)
+    e2e_value = e2e_all / (e2e_total / 1e3)
 
-        t = torch.tensor([e2e_total, float(e2e_priced)], device=f"cuda:{local}", dtype=torch.float64)
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t)
-        e2e_total, e2e_priced = float(mx[0].item()), float(t[1].item())
-    e2e_value = e2e_priced / e2e_total
-
-    # roofline of the dominant stage, from the live per-stage CUDA-event times
-    stage_names = ["match", "materialise", "hash", "dedup", "price"]
-    dom = max(range(5), key=lambda k: stage_ms[k])
-    peak, peak_kind = _peaks()
-    geo = s.geo
-    # algorithmic bytes of one step: every candidate's record is read from
-    # the parent and written once (used bytes only), its keys written, results written
-    n_nodes = np.mean([int(np.frombuffer(b[:16].tobytes(), dtype=np.int32)[0]) for b in host_recs])
-    n_refs = np.mean([int(np.frombuffer(b[:16].tobytes(), dtype=np.int32)[1]) for b in host_recs])
-    per_cand_record = 4 * (6 * n_nodes + n_refs) + 16 * n_nodes + n_nodes
-    per_step_cands = gen_n / args.steps
-    algo = {
-        "materialise": 2 * per_cand_record * per_step_cands,
-        "hash": (per_cand_record + 16 * n_nodes) * per_step_cands,
-        "price": (4 * n_nodes + n_nodes + 40 * n_nodes) * priced_n / args.steps,
-        "match": (per_cand_record + 16 * n_nodes) * len(mine),
-        "dedup": 80 * 2 * per_step_cands,
-    }
-    dom_name = stage_names[dom]
-    dom_ms = stage_ms[dom] / args.steps
-    achieved = algo[dom_name] / (dom_ms / 1e3) / 1e9
+    # rooflines of the dominant kernel (k_keys), from the live per-stage CUDA-event times
+    names = list(s.STAGES)
+    keys_ms = stage_ms[names.index("keys")] / args.steps
+    peak_c = s.b2b_peak()
+    achieved_c = kcomp / args.steps / (keys_ms / 1e3)
+    hbm_peak, hbm_src = _peaks()
+    n_nodes = float(np.mean([int(b[:4].view(np.int32)[0]) for b in host_recs]))
+    # algorithmic bytes of k_keys per job: the 16-byte job, ~1.1 producer keys (16 B) with their
+    # refsrc words (4 B) read; the 16-byte key and its 12-byte sort record written
+    jobs = kcomp / args.steps
+    keys_bytes = jobs * (16 + 1.1 * (16 + 4) + 16 + 12)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64+u64",
         "data": "synthetic (random-init float64 weights, synthetic profiler seed 0)",
         "config": {"workload": CONFIG_NAME, "model": MODEL, "parents_per_gpu": len(mine),
-                   "candidates_per_step": per_step_cands, "priced_per_step": priced_n / args.steps,
-                   "rules": "all 6", "inner_search_d": 1,
-                   "l2": "flushed (256 MiB write) before every timed step; per-step arena > L2",
-                   "parallelism": f"frontier sharded over {world} GPU(s)"},
-        "stages_ms_per_step": {n: stage_ms[k] / args.steps for k, n in enumerate(stage_names)},
-        "roofline": {"bound": "hbm", "kernel": f"k_{dom_name}", "achieved": achieved, "peak": peak,
-                     "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": rec_bytes * len(mine),
+                   "nodes_per_parent": n_nodes, "candidates_per_step": gen_n / args.steps,
+                   "priced_per_step": priced_n / args.steps, "rules": "all 6", "inner_search_d": 1,
+                   "l2": "flushed (256 MiB write) before every timed step",
+                   "parallelism": "frontier split by parent, dedup owned by hash (NCCL all-to-all)" if world > 1
+                   else "single GPU"},
+        "stages_ms_per_step": {n: stage_ms[k] / args.steps for k, n in enumerate(names)},
+        "roofline": {"bound": "alu", "kernel": "k_keys", "achieved": achieved_c / 1e9, "peak": peak_c / 1e9,
+                     "unit": "Gcompressions/s", "frac": achieved_c / peak_c, "traffic": None,
+                     "peak_source": "measured live: ef_b2b_peak (register-only BLAKE2b loop, same GPU)",
+                     "compressions_per_step": kcomp / args.steps,
+                     "digest_compressions_per_step": dcomp / args.steps},
+        "roofline_hbm": {"bound": "hbm", "kernel": "k_keys", "achieved": keys_bytes / (keys_ms / 1e3) / 1e9,
+                         "peak": hbm_peak, "unit": "GB/s", "frac": keys_bytes / (keys_ms / 1e3) / 1e9 / hbm_peak,
+                         "peak_source": hbm_src, "traffic": None},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(blob.nbytes),
                 "d2h_bytes_per_step": n_cand * N.CAND_DTYPE.itemsize},
-        "gpu_launches": 7 * args.steps,
+        "gpu_launches": (13 if world == 1 else 17) * args.steps,
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         parents = [_to_oracle(fr.decode(sl)) for sl in mine[:8]]
         cpu = _cpu_sample(parents, db, args.cpu_budget)
         line["cpu_baseline"] = {"value": cpu["value"], "unit": UNIT, "cores": 1, "kind": "port",
-                                "sample": f"{cpu['expanded']} frontier expansions ({cpu['priced']} candidates "
-                                          f"priced) by the oracle restatement, {cpu['seconds']:.1f}s"}
+                                "sample": f"{cpu['expanded']} ResNet-50 frontier expansions ({cpu['priced']} "
+                                          f"candidates priced) by the oracle restatement, {cpu['seconds']:.1f}s"}
     if rank == 0:
         print(json.dumps(line))
     fr.close()
@@ -380,7 +382,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--parents", type=int, default=256, help="frontier graphs per GPU per step")
+    ap.add_argument("--parents", type=int, default=4096, help="frontier graphs per GPU per step")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

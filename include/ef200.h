@@ -223,9 +223,19 @@ int ef_owner_mark(ef_ctx* ctx, const uint64_t* d_recv, uint32_t n_recv, uint32_t
 /* verdicts back in send order -> candidate flags, node cap, pricing of the survivors */
 int ef_expand_finish(ef_ctx* ctx, const uint32_t* d_verdict_back, const ef_price_params* pp);
 
-/* device time (ms) of the last ef_expand, measured with CUDA events on its stream,
- * split per stage: match, materialise, hash, dedup, price */
-int ef_last_timing(ef_ctx* ctx, float* ms5);
+/* device time (ms) of the last ef_expand, measured with CUDA events on its stream, per
+ * stage: match, plan, dirty walk, node keys, key sort, graph digest, dedup, price (n <= 8) */
+int ef_last_timing(ef_ctx* ctx, float* ms, uint32_t n);
+/* counters of the last step: BLAKE2b compressions in node keys, in graph digests,
+ * candidates, priced survivors (n <= 4) */
+int ef_last_stats(ef_ctx* ctx, uint64_t* out, uint32_t n);
+/* batched upload of compact records (host): record i at host + offsets[i] is
+ * [n, n_refs, n_out, n_compute] nid[n] sig[n] aux[n] nin[n] inoff[n+1] topo[n] refs outs
+ * (uint32); the device unpacks it into slots[i] and computes keys / sorted order / ranks */
+int ef_records_write_packed(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const void* host, const uint64_t* offsets,
+                            uint64_t bytes);
+/* measured BLAKE2b compression rate of this GPU (register-only loop): the ALU roofline */
+int ef_b2b_peak(ef_ctx* ctx, double* compress_per_s);
 
 #ifdef __cplusplus
 }

@@ -138,7 +138,10 @@ struct ef_ctx {
   uint32_t vis_mask = 0;
 
   cudaEvent_t ev[6] = {};
-  float last_ms[5] = {0, 0, 0, 0, 0};
+  std::vector<cudaEvent_t> ev_chunk;  // 5 per hashing chunk: dirty | keys | sort | digest
+  uint32_t n_chunks = 0;
+  float last_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  uint64_t last_stats[4] = {0, 0, 0, 0};
 };
 
 #define EF_CUDA(call)                                                                    \
@@ -295,6 +298,7 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_sel.release();
   ctx->d_dst.release();
   for (auto& e : ctx->ev) cudaEventDestroy(e);
+  for (auto& e : ctx->ev_chunk) cudaEventDestroy(e);
   if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
   cudaStreamDestroy(ctx->st);
   delete ctx;
@@ -1129,21 +1133,33 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
     VArgs V = chunk_args(ctx, S, Rs);
     V.parent_addr = A.parent_addr;
     V.stats = ctx->d_stats.p;
+    ctx->n_chunks = 0;
     for (uint32_t c0 = 0; c0 < total; c0 += chunk) {
       V.c0 = c0;
       V.n = std::min(chunk, total - c0);
       const uint32_t gd = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 127) / 128, ctx->n_sm * 16));
+      while (ctx->ev_chunk.size() < 5ull * (ctx->n_chunks + 1)) {
+        cudaEvent_t e;
+        EF_CUDA(cudaEventCreate(&e));
+        ctx->ev_chunk.push_back(e);
+      }
+      cudaEvent_t* ce = ctx->ev_chunk.data() + 5 * ctx->n_chunks++;
+      cudaEventRecord(ce[0], ctx->st);
       k_dirty<<<gd, 128, 0, ctx->st>>>(V);
       EF_CUDA(cudaGetLastError());
       size_t t1 = ctx->d_sort_tmp.cap;
       EF_CUDA(cub::DeviceRadixSort::SortPairsDescending(ctx->d_sort_tmp.p, t1, ctx->d_dcount.p, ctx->d_dsorted.p,
                                                         ctx->d_iota.p, ctx->d_dorder.p, (int)V.n, 0, bits_for(S),
                                                         ctx->st));
+      cudaEventRecord(ce[1], ctx->st);
       k_keys<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
       EF_CUDA(cudaGetLastError());
+      cudaEventRecord(ce[2], ctx->st);
       if ((rc = sort_fresh_keys(ctx, V))) return rc;
+      cudaEventRecord(ce[3], ctx->st);
       k_digest<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
       EF_CUDA(cudaGetLastError());
+      cudaEventRecord(ce[4], ctx->st);
     }
     cudaEventRecord(ctx->ev[3], ctx->st);
     ctx->last_total = total;
@@ -1222,8 +1238,28 @@ static int step_sync(ef_ctx* ctx, bool timings) {
   const uint32_t err = ctx->h_scalars[1];
   ctx->last_req_sig = ctx->h_scalars[2];
   ctx->last_req_dv = ctx->h_scalars[3];
-  if (timings)
-    for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&ctx->last_ms[k], ctx->ev[k], ctx->ev[k + 1]);
+  if (timings) {  // match, plan, dirty, keys, sort, digest, dedup, price
+    float ms[5];
+    for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&ms[k], ctx->ev[k], ctx->ev[k + 1]);
+    float sub[4] = {0, 0, 0, 0};
+    for (uint32_t c = 0; c < ctx->n_chunks; ++c) {
+      cudaEvent_t* ce = ctx->ev_chunk.data() + 5 * c;
+      for (int k = 0; k < 4; ++k) {
+        float x = 0;
+        cudaEventElapsedTime(&x, ce[k], ce[k + 1]);
+        sub[k] += x;
+      }
+    }
+    ctx->last_ms[0] = ms[0];
+    ctx->last_ms[1] = ms[1];
+    for (int k = 0; k < 4; ++k) ctx->last_ms[2 + k] = sub[k];
+    ctx->last_ms[6] = ms[3];
+    ctx->last_ms[7] = ms[4];
+    EF_CUDA(cudaMemcpyAsync(ctx->last_stats, ctx->d_stats.p, 2 * 8, cudaMemcpyDeviceToHost, ctx->st));
+    EF_CUDA(cudaStreamSynchronize(ctx->st));
+    ctx->last_stats[2] = ctx->last_total;
+    ctx->last_stats[3] = ctx->h_scalars[7];
+  }
   EF_REQUIRE(!(err & 4u), "candidate exceeds record capacity (raise cap_nodes/cap_refs)");
   if (ctx->last_req_sig || ctx->last_req_dv) return EF_NEED_RESOLVE;
   return EF_OK;
@@ -1392,8 +1428,56 @@ int ef_keep(ef_ctx* ctx, const uint32_t* cand_idx, uint32_t n, const uint32_t* s
   return EF_OK;
 }
 
-int ef_last_timing(ef_ctx* ctx, float* ms5) {
-  for (int k = 0; k < 5; ++k) ms5[k] = ctx->last_ms[k];
+int ef_last_timing(ef_ctx* ctx, float* ms, uint32_t n) {
+  for (uint32_t k = 0; k < n && k < 8; ++k) ms[k] = ctx->last_ms[k];
+  return EF_OK;
+}
+
+int ef_last_stats(ef_ctx* ctx, uint64_t* out, uint32_t n) {
+  for (uint32_t k = 0; k < n && k < 4; ++k) out[k] = ctx->last_stats[k];
+  return EF_OK;
+}
+
+int ef_records_write_packed(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const void* host, const uint64_t* offsets,
+                            uint64_t bytes) {
+  EF_REQUIRE(!ctx->dirty, "tables not committed (call ef_tables_commit)");
+  if (!n) return EF_OK;
+  EF_CUDA(ctx->d_stage.reserve(bytes, ctx->st));
+  EF_CUDA(cudaMemcpyAsync(ctx->d_stage.p, host, bytes, cudaMemcpyHostToDevice, ctx->st));
+  std::vector<unsigned long long> off(offsets, offsets + n), dst(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    EF_REQUIRE(slots[i] < ctx->n_slots, "ef_records_write_packed: bad slot");
+    EF_REQUIRE(offsets[i] % 4 == 0 && offsets[i] < bytes, "ef_records_write_packed: bad offset");
+    dst[i] = (unsigned long long)slot_addr(ctx, slots[i]);
+  }
+  int rc;
+  if ((rc = upload(ctx, ctx->d_addr_a, off)) || (rc = upload(ctx, ctx->d_addr_b, dst))) return rc;
+  k_unpack<<<std::min<uint32_t>(n, ctx->n_sm * 8), 256, 0, ctx->st>>>(reinterpret_cast<const uint8_t*>(ctx->d_stage.p),
+                                                                      ctx->d_addr_a.p, ctx->d_addr_b.p, n, ctx->geo);
+  EF_CUDA(cudaGetLastError());
+  if ((rc = hash_records_full(ctx, ctx->d_addr_b.p, n, nullptr))) return rc;
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+int ef_b2b_peak(ef_ctx* ctx, double* compress_per_s) {
+  cudaSetDevice(ctx->dev);
+  const int blocks = ctx->n_sm * 16, threads = 128, iters = 1000;
+  DevBuf<uint64_t> out;
+  EF_CUDA(out.reserve((size_t)blocks * threads, ctx->st));
+  double best = 0;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(ctx->ev[0], ctx->st);
+    k_b2b_peak<<<blocks, threads, 0, ctx->st>>>(out.p, iters);
+    cudaEventRecord(ctx->ev[1], ctx->st);
+    EF_CUDA(cudaEventSynchronize(ctx->ev[1]));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+    const double r = (double)blocks * threads * iters / (ms * 1e-3);
+    if (rep > 0 && r > best) best = r;
+  }
+  out.release();
+  *compress_per_s = best;
   return EF_OK;
 }
 

@@ -707,7 +707,9 @@ __global__ void __launch_bounds__(BT) k_digest(VArgs A) {
       for (int i = 0; i < 16; ++i) m[i] = col[i * BT];
       b2b_compress(h, m, len < 128ull * (b + 1) ? len : 128ull * (b + 1), b + 1 == nblk);
     }
-    if (A.full) A.hash_out[c] = B2b::bswap64(h[0]);
+    if (A.full) {
+      if (A.hash_out) A.hash_out[c] = B2b::bswap64(h[0]);
+    }
     else A.res[c].hash = B2b::bswap64(h[0]);
     if (A.stats) atomicAdd(A.stats + 1, (unsigned long long)nblk);
   }
@@ -986,6 +988,49 @@ __global__ void k_apply_verdicts(ef_cand_result* res, const uint32_t* perm, cons
       if (survivor) plist[base + __popc(m & ((1u << lane) - 1u))] = c;
     }
   }
+}
+
+// ------------------------------------------------------------------------------------------
+// packed record upload: per record [n, n_refs, n_out, n_compute] then nid[n] sig[n] aux[n]
+// nin[n] inoff[n+1] topo[n] refs[n_refs] outs[n_out] (uint32), scattered into the slots
+// ------------------------------------------------------------------------------------------
+
+__global__ void k_unpack(const uint8_t* blob, const unsigned long long* off, const unsigned long long* dst,
+                         uint32_t n, Geo G) {
+  for (uint32_t r = blockIdx.x; r < n; r += gridDim.x) {
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(blob + off[r]);
+    Rec R{reinterpret_cast<char*>(dst[r])};
+    const uint32_t nn = p[0], nr = p[1], no = p[2];
+    if (threadIdx.x < 16) reinterpret_cast<uint32_t*>(R.p)[threadIdx.x] = threadIdx.x < 4 ? p[threadIdx.x] : 0u;
+    const uint32_t* q = p + 4;
+    for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
+      R.nid(G)[i] = (int32_t)q[i];
+      R.sig(G)[i] = q[nn + i];
+      R.aux(G)[i] = q[2 * nn + i];
+      R.nin(G)[i] = q[3 * nn + i];
+      R.inoff(G)[i] = q[4 * nn + i];
+      R.topo(G)[i] = q[5 * nn + 1 + i];
+      R.alg(G)[i] = 0;
+    }
+    if (threadIdx.x == 0) R.inoff(G)[nn] = q[5 * nn];
+    const uint32_t* rq = q + 6 * nn + 1;
+    for (uint32_t i = threadIdx.x; i < nr; i += blockDim.x) R.refs(G)[i] = rq[i];
+    for (uint32_t i = threadIdx.x; i < no; i += blockDim.x) R.outs(G)[i] = rq[nr + i];
+  }
+}
+
+// register-only BLAKE2b compressions: the ALU roofline of the hash kernels on this GPU
+__global__ void __launch_bounds__(128) k_b2b_peak(uint64_t* out, int iters) {
+  uint64_t h[8], m[16];
+  for (int i = 0; i < 16; ++i) m[i] = (uint64_t)(threadIdx.x + 131 * blockIdx.x) * 0x9e3779b97f4a7c15ULL + i;
+  for (int i = 0; i < 8; ++i) h[i] = b2b_iv(i);
+  for (int r = 0; r < iters; ++r) {
+    b2b_compress(h, m, 128, false);
+    m[r & 15] ^= h[0];
+  }
+  uint64_t x = 0;
+  for (int i = 0; i < 8; ++i) x ^= h[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = x;
 }
 
 }  // namespace ef

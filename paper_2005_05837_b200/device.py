@@ -510,10 +510,45 @@ class DeviceSession:
         arr = (C.c_uint64 * max(1, len(hashes)))(*hashes)
         self._check(self.L.ef_visited_insert(self.ctx, arr, len(hashes)), "ef_visited_insert")
 
+    STAGES = ("match", "plan", "dirty", "keys", "sort", "digest", "dedup", "price")
+
     def last_timing(self) -> list[float]:
-        ms = (C.c_float * 5)()
-        self.L.ef_last_timing(self.ctx, ms)
+        """Device ms of the last step per stage (STAGES), CUDA events on the library stream."""
+        ms = (C.c_float * 8)()
+        self.L.ef_last_timing(self.ctx, ms, 8)
         return list(ms)
+
+    def last_stats(self) -> dict:
+        out = (C.c_uint64 * 4)()
+        self.L.ef_last_stats(self.ctx, out, 4)
+        return {"key_compressions": int(out[0]), "digest_compressions": int(out[1]), "candidates": int(out[2]),
+                "priced": int(out[3])}
+
+    def b2b_peak(self) -> float:
+        """Measured BLAKE2b compressions/s of this GPU (the hash kernels' ALU roofline)."""
+        r = C.c_double(0)
+        self._check(self.L.ef_b2b_peak(self.ctx, C.byref(r)), "ef_b2b_peak")
+        return r.value
+
+    def pack(self, recs: list[np.ndarray]) -> tuple[np.ndarray, np.ndarray]:
+        """Compact host form of full records (used bytes only) for ef_records_write_packed."""
+        G = self.geo
+        parts, offs, at = [], [], 0
+        for buf in recs:
+            n, n_refs, n_out, n_comp = (int(x) for x in buf[:16].view(np.int32))
+            u32 = lambda off, cnt: buf[off: off + 4 * cnt].view(np.uint32)  # noqa: E731
+            blob = np.concatenate([np.array([n, n_refs, n_out, n_comp], dtype=np.uint32), u32(G.off_nid, n),
+                                   u32(G.off_sig, n), u32(G.off_aux, n), u32(G.off_nin, n), u32(G.off_inoff, n + 1),
+                                   u32(G.off_topo, n), u32(G.off_refs, n_refs), u32(G.off_outs, n_out)])
+            parts.append(blob)
+            offs.append(at)
+            at += 4 * blob.size
+        return np.concatenate(parts), np.array(offs, dtype=np.uint64)
+
+    def write_packed(self, slots: list[int], blob: np.ndarray, offsets: np.ndarray) -> None:
+        self._check(self.L.ef_records_write_packed(self.ctx, N.u32_array(slots), len(slots), blob.ctypes.data,
+                                                   offsets.ctypes.data_as(C.POINTER(C.c_uint64)), blob.nbytes),
+                    "ef_records_write_packed")
 
 
 def price_params(f, d: int, use_inner: bool, node_cap: int) -> N.PriceParams:

@@ -13,7 +13,7 @@ import os
 from .errors import NativeUnavailable
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libef200.so")
+LIB_PATH = os.environ.get("EF_LIB") or os.path.join(HERE, "libef200.so")  # EF_LIB: an alternative build (experiments)
 
 EF_OK = 0
 EF_NEED_RESOLVE = 1

@@ -176,3 +176,50 @@ struct B2b {
 };
 
 }  // namespace ef
+
+#ifdef __CUDACC__
+namespace ef {
+
+__constant__ uint8_t kB2bSigma[10][16] = {
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
+    {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4}, {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
+    {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13}, {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
+    {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11}, {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
+    {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5}, {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0}};
+
+// Compression with the 12 rounds rolled into a loop (~3 KB of SASS instead of ~35 KB), the
+// message read from a per-thread shared-memory column (word k at col[k * BT]) in each round's
+// schedule order: keeps the hot loop of the hash kernels inside the instruction cache.
+template <int BT>
+__device__ __forceinline__ void b2b_compress_col(uint64_t* h, const uint64_t* col, uint64_t t, bool last) {
+  uint64_t v0 = h[0], v1 = h[1], v2 = h[2], v3 = h[3], v4 = h[4], v5 = h[5], v6 = h[6], v7 = h[7];
+  uint64_t v8 = b2b_iv(0), v9 = b2b_iv(1), v10 = b2b_iv(2), v11 = b2b_iv(3);
+  uint64_t v12 = b2b_iv(4) ^ t, v13 = b2b_iv(5), v14 = b2b_iv(6), v15 = b2b_iv(7);
+  if (last) v14 = ~v14;
+#pragma unroll 1
+  for (int r = 0; r < 12; ++r) {
+    const uint8_t* s = kB2bSigma[r < 10 ? r : r - 10];
+    uint64_t m[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) m[i] = col[s[i] * BT];
+    EF_B2B_G(v0, v4, v8, v12, m[0], m[1]);
+    EF_B2B_G(v1, v5, v9, v13, m[2], m[3]);
+    EF_B2B_G(v2, v6, v10, v14, m[4], m[5]);
+    EF_B2B_G(v3, v7, v11, v15, m[6], m[7]);
+    EF_B2B_G(v0, v5, v10, v15, m[8], m[9]);
+    EF_B2B_G(v1, v6, v11, v12, m[10], m[11]);
+    EF_B2B_G(v2, v7, v8, v13, m[12], m[13]);
+    EF_B2B_G(v3, v4, v9, v14, m[14], m[15]);
+  }
+  h[0] ^= v0 ^ v8;
+  h[1] ^= v1 ^ v9;
+  h[2] ^= v2 ^ v10;
+  h[3] ^= v3 ^ v11;
+  h[4] ^= v4 ^ v12;
+  h[5] ^= v5 ^ v13;
+  h[6] ^= v6 ^ v14;
+  h[7] ^= v7 ^ v15;
+}
+
+}  // namespace ef
+#endif

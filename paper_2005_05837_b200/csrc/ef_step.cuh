@@ -416,12 +416,8 @@ __global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
         for (uint32_t q = sk.q; q < 16u * nb; ++q) col[q * BT] = 0;
         b2b_start(h, 16);
         ncomp += nb;
-        for (uint32_t b = 0; b < nb; ++b) {
-          uint64_t m[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) m[i] = col[(16 * b + i) * BT];
-          b2b_compress(h, m, (uint64_t)min(len, 128u * (b + 1)), b + 1 == nb);
-        }
+        for (uint32_t b = 0; b < nb; ++b)
+          b2b_compress_col<BT>(h, col + 16 * b * BT, (uint64_t)min(len, 128u * (b + 1)), b + 1 == nb);
       }
       fresh[2 * jj] = h[0];
       fresh[2 * jj + 1] = h[1];
@@ -702,10 +698,7 @@ __global__ void __launch_bounds__(BT) k_digest(VArgs A) {
         sk.flush();
         for (uint32_t q = sk.q; q < 16; ++q) col[q * BT] = 0;
       }
-      uint64_t m[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) m[i] = col[i * BT];
-      b2b_compress(h, m, len < 128ull * (b + 1) ? len : 128ull * (b + 1), b + 1 == nblk);
+      b2b_compress_col<BT>(h, col, len < 128ull * (b + 1) ? len : 128ull * (b + 1), b + 1 == nblk);
     }
     if (A.full) {
       if (A.hash_out) A.hash_out[c] = B2b::bswap64(h[0]);

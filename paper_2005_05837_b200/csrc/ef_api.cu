@@ -1145,15 +1145,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       }
       cudaEvent_t* ce = ctx->ev_chunk.data() + 5 * ctx->n_chunks++;
       cudaEventRecord(ce[0], ctx->st);
-      if (S <= 256) {
-        const uint32_t g64 = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 63) / 64, ctx->n_sm * 32));
-        k_dirty<64, 256><<<g64, 64, 0, ctx->st>>>(V);
-      } else if (S <= 512) {
-        const uint32_t g32 = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 31) / 32, ctx->n_sm * 32));
-        k_dirty<32, 512><<<g32, 32, 0, ctx->st>>>(V);
-      } else {
-        k_dirty<128, 0><<<gd, 128, 0, ctx->st>>>(V);
-      }
+      k_dirty<<<gd, 128, 0, ctx->st>>>(V);
       EF_CUDA(cudaGetLastError());
       size_t t1 = ctx->d_sort_tmp.cap;
       EF_CUDA(cub::DeviceRadixSort::SortPairsDescending(ctx->d_sort_tmp.p, t1, ctx->d_dcount.p, ctx->d_dsorted.p,

@@ -85,8 +85,6 @@ struct VArgs {
 
 constexpr uint32_t kInputJob = 0x80000000u;  // Job.nin flag: input node, aux = input-name id
 
-__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
-
 // ------------------------------------------------------------------------------------------
 // k_plan
 // ------------------------------------------------------------------------------------------
@@ -188,14 +186,8 @@ __device__ __forceinline__ uint32_t vremap(const VPlan& P, uint32_t r) {
 
 // Lanes of a warp hold neighbouring candidates (mostly of one parent) and walk the same
 // warp-uniform range of topological slots in lockstep, so the parent's arrays are read as
-// broadcasts and the warp never splits.  The walk's read-after-write state (fresh index per
-// parent position, removed-rank mask) lives in shared memory when the rows are short
-// (SM_S > 0: u16 indices in column layout, one column per thread) and is copied out once.
-template <int BT, int SM_S>
-__global__ void __launch_bounds__(BT) k_dirty(VArgs A) {
-  constexpr int SM_W = SM_S ? (SM_S + 31) / 32 : 1;
-  __shared__ uint16_t sm_didx[SM_S ? SM_S * BT : 1];
-  __shared__ uint32_t sm_rm[SM_S ? SM_W * BT : 1];
+// broadcasts and the warp never splits.
+__global__ void k_dirty(VArgs A) {
   const Geo& G = A.g;
   const uint32_t span = (A.n + 31) / 32 * 32;
   for (uint32_t lc = blockIdx.x * blockDim.x + threadIdx.x; lc < span; lc += gridDim.x * blockDim.x) {
@@ -218,42 +210,23 @@ __global__ void __launch_bounds__(BT) k_dirty(VArgs A) {
     const uint32_t* pinoff = R.inoff(G);
     const uint32_t* prefs = R.refs(G);
     const int pn = P.pn;
-    uint32_t* gdidx = A.didx + (uint64_t)lc * A.S;
+    uint32_t* didx = A.didx + (uint64_t)lc * A.S;
     Job* jobs = A.jobs + (uint64_t)lc * A.S;
     uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
+    for (int i = 0; i < (pn + 2 + 3) / 4; ++i) reinterpret_cast<uint4*>(didx)[i] = make_uint4(0, 0, 0, 0);
     const uint32_t* srank = R.srank(G);
-    uint32_t* grm = A.rmask + (uint64_t)lc * A.W;
-    const int nw = (pn + 31) / 32;
-    // state accessors: shared-memory columns or the global rows
-    auto didx_get = [&](uint32_t p) -> uint32_t {
-      if (SM_S) return sm_didx[p * BT + threadIdx.x];
-      return gdidx[p];
-    };
-    auto didx_set = [&](uint32_t p, uint32_t v) {
-      if (SM_S) sm_didx[p * BT + threadIdx.x] = (uint16_t)v;
-      else gdidx[p] = v;
-    };
-    auto rm_or = [&](uint32_t w, uint32_t bit) {
-      if (SM_S) sm_rm[w * BT + threadIdx.x] |= bit;
-      else grm[w] |= bit;
-    };
-    if (SM_S) {
-      for (int i = 0; i < pn + 2; ++i) sm_didx[i * BT + threadIdx.x] = 0;
-      for (int w = 0; w < nw; ++w) sm_rm[w * BT + threadIdx.x] = 0;
-    } else {
-      for (int i = 0; i < (pn + 2 + 3) / 4; ++i) reinterpret_cast<uint4*>(gdidx)[i] = make_uint4(0, 0, 0, 0);
-      for (int w = 0; w < nw; ++w) grm[w] = 0;
-    }
+    uint32_t* rm = A.rmask + (uint64_t)lc * A.W;
+    for (int w = 0; w < (pn + 31) / 32; ++w) rm[w] = 0;
     auto remove = [&](int v) {
       const uint32_t k = srank[v];
-      rm_or(k >> 5, 1u << (k & 31));
+      rm[k >> 5] |= 1u << (k & 31);
     };
     if (P.drop0 >= 0) remove(P.drop0);
     if (P.drop1 >= 0) remove(P.drop1);
     uint32_t j = 0, r = 0;
     auto src_of = [&](uint32_t ref) -> uint32_t {
       const uint32_t p = ref >> 8, port = ref & 255u;
-      const uint32_t fi = didx_get(p);
+      const uint32_t fi = didx[p];
       return fi ? (kFresh | (port << 23) | (fi - 1)) : ((port << 23) | p);
     };
     auto emit_new = [&]() {
@@ -262,7 +235,7 @@ __global__ void __launch_bounds__(BT) k_dirty(VArgs A) {
         rs[r] = src_of(P.new_ref[k]);  // new nodes are exempt from the remap (rules.py:186-188)
         jobs[j] = Job{P.new_sig[k], P.new_aux[k], r, 1u};
         r += 1;
-        didx_set(pn + k, ++j);
+        didx[pn + k] = ++j;
       }
     };
     const int s_lo = (int)__reduce_min_sync(mask, (unsigned)P.first);
@@ -286,14 +259,10 @@ __global__ void __launch_bounds__(BT) k_dirty(VArgs A) {
       if (dirty) {
         jobs[j] = Job{v == P.mod ? P.mod_sig : psig[v], v == P.mod ? P.mod_aux : paux[v], r, nr};
         r += nr;
-        didx_set(v, ++j);
+        didx[v] = ++j;
         remove(v);
       }
       if (s == P.ins_slot && P.ins_after) emit_new();
-    }
-    if (SM_S) {  // the digest reads output sources and removed ranks from the global rows
-      for (int i = 0; i < pn + 2; ++i) gdidx[i] = sm_didx[i * BT + threadIdx.x];
-      for (int w = 0; w < nw; ++w) grm[w] = sm_rm[w * BT + threadIdx.x];
     }
     A.dcount[lc] = j;
     A.seg_begin[lc] = (int32_t)((uint64_t)lc * A.S);
@@ -412,13 +381,6 @@ __global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
     uint32_t ncomp = 0;
     for (uint32_t jj = 0; jj < d; ++jj) {
       const Job jb = jobs[jj];
-      if (jj + 1 < d) {  // the next job's first producer key, when it is a parent key
-        const Job nx = jobs[jj + 1];
-        if (!(nx.nin & kInputJob) && nx.nin) {
-          const uint32_t sv = rs[nx.roff];
-          if (!(sv & kFresh) && pkeys) prefetch_l1(pkeys + 2 * (sv & 0x7fffffu));
-        }
-      }
       const uint32_t tlen = T.sig_text_len[jb.sig];
       const bool input = jb.nin & kInputJob;
       const uint32_t nin = input ? 0u : jb.nin;
@@ -627,7 +589,6 @@ __global__ void __launch_bounds__(BT) k_digest(VArgs A) {
     uint64_t ph0 = 0, ph1 = 0, fh0 = 0, fh1 = 0;
     bool have_p = false, have_f = false;
     auto next_p = [&]() {
-      if ((pi & 7u) == 0) prefetch_l1(pskeys + 2 * (pi + 16));  // two 128-byte lines ahead
       while (pi < (uint32_t)pn) {
         if ((pi >> 5) != mw_idx) {
           mw_idx = pi >> 5;
@@ -648,7 +609,6 @@ __global__ void __launch_bounds__(BT) k_digest(VArgs A) {
       }
     };
     auto next_f = [&]() {
-      if ((fk & 7u) == 0) prefetch_l1(fsk + 2 * (fk + 16));
       have_f = fk < d;
       if (have_f) {
         fh0 = fsk[2 * fk];

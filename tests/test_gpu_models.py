@@ -77,3 +77,49 @@ def test_frontier_step_matches_oracle(model, n_parents, price_every):
                 assert (int(r["evals"]), int(r["sweeps"])) == (evals, sweeps)
                 priced += 1
     assert checked == len(res) and priced > 0
+
+
+def _golden(model):
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "golden_models.json")) as fh:
+        return {i["model"]: i for i in json.load(fh)["instances"]}[model]
+
+
+@pytest.mark.parametrize("model", ["squeezenet", "resnet50", "inception_v3", "nasnet_a"])
+def test_gpu_matches_reference_goldens_at_model_scale(model):
+    """GPU path vs golden vectors from the real reference (make_golden_models.py)."""
+    from paper_2005_05837_b200 import frontier, rewrite
+
+    gold = _golden(model)
+    g = zoo.generate(model, 0)
+    assert str(ef.canonical_hash(g)) == gold["hash"]
+    ids = sorted(g.nodes)
+    rules = ef.default_rules()
+    for s, res in rewrite._expand_one(g, rules):
+        assert [str(h) for h in res["hash"].tolist()] == gold["rewrites"]
+        assert [str(h) for h, fl in zip(res["hash"].tolist(), res["flags"].tolist()) if fl & N.F_FIRST] \
+            == gold["neighbors"]
+        for rule in rules:
+            mine = res[res["rule"] == rule.rule_id]
+            sites = [sorted(zip(rewrite._SITE_NAMES[rule.name], (ids[int(r["site_a"])], ids[int(r["site_b"])])))
+                     for r in mine]
+            assert [[v for _, v in st] for st in sites] == gold["sites"][rule.name], rule.name
+    db = ef.CostDatabase()
+    ef.ensure_profiled(g, db, ef.SyntheticProfiler(0))
+    r, assign = frontier._price_one(g, db, ef.CostFunction.energy(), 1, True)
+    inner = gold["inner_energy_d1"]
+    assert [assign[k] for k in sorted(assign)] == inner["assignment"]
+    assert (r.cost, r.time_ms, r.energy, r.evals, r.sweeps) == (inner["cost"], inner["time_ms"], inner["energy"],
+                                                                inner["evals"], inner["sweeps"])
+    if "search" in gold:  # BASELINE configs[0]: the full SqueezeNet search at alpha = 1.0
+        run = gold["search"]
+        trace = []
+        res = ef.outer_search(g, rules, ef.CostDatabase(), ef.CostFunction.energy(),
+                              ef.SearchConfig(alpha=run["alpha"]), ef.SyntheticProfiler(0), trace=trace)
+        assert [str(h) for h in trace] == run["trace"]
+        assert str(ef.canonical_hash(res.graph)) == run["hash"]
+        assert [res.assignment[k] for k in sorted(res.assignment)] == run["assignment"]
+        assert (res.cost, res.time_ms, res.energy) == (run["cost"], run["time_ms"], run["energy"])
+        assert {k: v for k, v in vars(res.stats).items() if k != "wall_time_ms"} == run["stats"]

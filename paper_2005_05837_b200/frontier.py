@@ -314,6 +314,71 @@ def brute_force_assignment(g: Graph, db: CostDatabase, f: CostFunction, max_poin
     return {n: rows[i][int(k)][0] for i, (n, k) in enumerate(zip(nids, idx))}
 
 
+def closure(g0: Graph, rules: list[SubstitutionRule], max_graphs: int, max_graph_nodes: int | None = None,
+            session: DeviceSession | None = None) -> list[Graph]:
+    """BFS closure of g0 under the rules, deduplicated by canonical hash (search.py:275-300).
+
+    Each BFS level is ONE batched ef_expand over all graphs of the level: candidates come back
+    in (parent, rule, site) order, FIRST marks the first occurrence inside the level and
+    VISITED membership in the hashes seen before it, which is exactly the reference's
+    sequential `seen` check; the device inserts the level's new hashes into the visited set.
+    Raises SpaceTooLarge past `max_graphs`; graphs above the node cap are seen, not kept.
+    """
+    s = session or DeviceSession.default()
+    rule_ids = [r.rule_id for r in rules]
+    cap = max_graph_nodes if max_graph_nodes is not None else 1 << 30
+    geo_cap = max_graph_nodes if max_graph_nodes is not None else 4 * max(1, len(g0.compute_nodes()))
+    db = CostDatabase()  # pricing is not needed: use_inner = 0 and no rows requested
+    run = _Run(s, g0, max(geo_cap, len(g0.compute_nodes())), db, None)
+    out_slots = [run.root]
+    try:
+        (h0,) = s.hash_slots([run.root])
+        s.visited_insert([h0])
+        pp = price_params(CostFunction.time(), 1, False, cap)
+        level = [run.root]
+        while level and rule_ids:
+            res = s.expand(level, rule_ids, pp, insert_visited=True)
+            fl = res["flags"].tolist()
+            keep = [i for i, f in enumerate(fl) if (f & (N.F_FIRST | N.F_VISITED | N.F_CAPPED)) == N.F_FIRST]
+            if len(out_slots) + len(keep) > max_graphs:
+                raise SpaceTooLarge(f"rewrite closure exceeds {max_graphs} graphs")
+            level = s.keep(keep) if keep else []
+            out_slots += level
+        return [s.decode(s.read_record(sl), g0)[0] for sl in out_slots]
+    finally:
+        for sl in out_slots:
+            if sl != run.root:
+                s.free(sl)
+        run.close()
+
+
+def brute_force_space(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: CostFunction,
+                      max_graphs: int = 10**4, max_points: int = 10**6, profiler: ProfilerSpec | None = None,
+                      max_graph_nodes: int | None = None, session=None) -> OptimizationResult:
+    """Exhaustive oracle of the reference API (search.py:303-329): the closure (batched BFS on
+    the GPU) and the exhaustive assignment of every member; first-found minimum wins."""
+    started = time.perf_counter()
+    stats = SearchStats()
+    best = None
+    for g in closure(g0, rules, max_graphs, max_graph_nodes, session):
+        stats.graphs_explored += 1
+        if profiler is not None:
+            stats.new_cost_records += ensure_profiled(g, db, profiler)
+        assign = brute_force_assignment(g, db, f, max_points)
+        table = node_cost_table(g, db)
+        per = {nid: {a: (tt, ee) for a, tt, ee in rows} for nid, (_, rows) in table.items()}
+        t = sum(per[nid][assign[nid]][0] for nid in per)
+        e = sum(per[nid][assign[nid]][1] for nid in per)
+        cost = f.from_totals(t, e)
+        stats.assignments_evaluated += math.prod(len(rows) for _, rows in table.values()) if table else 1
+        if best is None or cost < best[2]:
+            best = (g, assign, cost, t, e)
+    stats.wall_time_ms = (time.perf_counter() - started) * 1000.0
+    g_best, a_best, c_best, t_best, e_best = best
+    power = e_best / t_best if t_best > 0 else 0.0
+    return OptimizationResult(g_best, a_best, c_best, t_best, e_best, power, stats)
+
+
 def constrained_optimize(g0: Graph, rules, db: CostDatabase, cfg: SearchConfig, time_bound_ms: float,
                          profiler: ProfilerSpec | None, iterations: int = 20,
                          db_append_path: str | None = None, session=None) -> OptimizationResult:

@@ -29,7 +29,7 @@ import enerflow.search as ref_search  # noqa: E402
 from enerflow import (  # noqa: E402
     CostDatabase, CostFunction, SearchConfig, SyntheticProfiler, canonical_hash, default_rules,
     ensure_profiled, graph_to_json, inner_search, match_rule, apply, neighbors, outer_search,
-    signatures,
+    signatures, SpaceTooLarge,
 )
 from enerflow.cost import normalization_refs  # noqa: E402
 from enerflow.models import (  # noqa: E402
@@ -101,7 +101,21 @@ def _instance(name, g, db, seed, searches, inner_fns, rule_names=None):
             out = {"error": type(exc).__name__}
         out.update({"fn": _fn_spec(f), "cfg": cfg_kw, "use_inner": use_inner})
         runs.append(out)
+    space = None
+    if seed is not None:  # search.py:275-329 closure and its exhaustive oracle (<= 2000 graphs)
+        db_bf = CostDatabase()
+        for sig, alg, t, p in db_before:
+            db_bf.add(sig, alg, enerflow.CostRecord(t, p))
+        try:
+            members = ref_search.closure(g, rules, 2000)
+            bf = ref_search.brute_force_space(g, rules, db_bf, CostFunction.energy(), max_graphs=2000,
+                                              profiler=SyntheticProfiler(seed))
+            space = {"closure": [str(canonical_hash(m)) for m in members], "hash": str(canonical_hash(bf.graph)),
+                     "cost": bf.cost, "assignment": {str(k): v for k, v in sorted(bf.assignment.items())}}
+        except SpaceTooLarge:
+            space = {"error": "SpaceTooLarge"}
     return {
+        "space": space,
         "name": name, "rules": [r.name for r in rules], "graph": graph_to_json(g), "db": db_before, "seed": seed,
         "hash": str(canonical_hash(g)),
         "signatures": {str(k): s.text for k, s in signatures(g).items()},

@@ -1,0 +1,60 @@
+"""Synthetic random DAGs of 1k-20k nodes (BASELINE configs[4]) through the batched
+step: scratch chunking, the cub segmented-sort path for rows > 1024 keys, and
+thousands of outputs in the graph digest.  A sample of every step's candidates is
+checked against the oracle (canonical hash, and the inner search of priced ones)."""
+
+import pytest
+
+import paper_2005_05837_b200 as ef
+from paper_2005_05837_b200 import _native as N
+from paper_2005_05837_b200 import zoo
+from paper_2005_05837_b200.frontier import Frontier
+
+pytestmark = pytest.mark.gpu
+
+RULES = [r.name for r in ef.default_rules()]
+
+
+def to_oracle(g):
+    nodes = {nid: {"kind": v.kind.value, "ins": [(r.node, r.port) for r in v.inputs], "p": dict(v.params),
+                   "w": dict(v.weights)} for nid, v in g.nodes.items()}
+    return {"inputs": [(n, tuple(s.dims)) for n, s in g.inputs], "nodes": nodes,
+            "outputs": [(r.node, r.port) for r in g.outputs]}
+
+
+@pytest.mark.parametrize("n_ops,n_parents,sample", [(1000, 4, 24), (5000, 2, 8), (20000, 1, 3)])
+def test_random_dag_step_matches_oracle(n_ops, n_parents, sample):
+    from oracle import enerflow_oracle as orc
+
+    g0 = zoo.random_dag(n_ops, 0)
+    db = ef.CostDatabase()
+    fr = Frontier(g0, db, ef.SyntheticProfiler(0), ef.CostFunction.energy(), ef.SearchConfig(alpha=1.05), n_parents)
+    try:
+        res = fr.step()
+        parents = [fr.decode(sl) for sl in fr.slots]
+    finally:
+        fr.close()
+    odb = orc.CostDB()
+    for (sig, alg), rec in db.records().items():
+        odb.add(sig, alg, rec.time_ms, rec.power_w)
+    rule_names = {i: r.name for i, r in enumerate(ef.default_rules())}
+    checked = 0
+    for pi, pg in enumerate(parents):
+        og = to_oracle(pg)
+        want = [(rule, site) for rule in RULES for site in orc.match(rule, og)]
+        mine = res[res["parent"] == pi]
+        assert len(mine) == len(want)
+        stride = max(1, len(want) // sample)
+        for k in range(0, len(want), stride):
+            rule, site = want[k]
+            r = mine[k]
+            assert rule_names[int(r["rule"])] == rule
+            child = orc.apply(rule, og, site)
+            assert int(r["hash"]) == orc.canonical_hash(child), (n_ops, pi, rule, site)
+            if r["flags"] & N.F_PRICED:
+                orc.ensure_profiled(child, odb, 0)
+                _, cost, t, e, evals, sweeps = orc.sweep(child, odb, orc.CostFn("energy"), 1)
+                assert (float(r["cost"]), float(r["time_ms"]), float(r["energy"])) == (cost, t, e)
+                assert (int(r["evals"]), int(r["sweeps"])) == (evals, sweeps)
+            checked += 1
+    assert checked >= sample

@@ -304,17 +304,20 @@ def run_ours(args, world, rank, local):
     staging = np.ctypeslib.as_array((C.c_uint8 * blob.nbytes).from_address(pinned))
     staging[:] = blob.view(np.uint8)
     e2e_slots = [s.alloc() for _ in mine]
-    e2e_ms, e2e_priced, n_cand = [], 0, 0
+    e2e_ms, e2e_priced, n_cand, up_ms = [], 0, 0, 0.0
+    evm = torch.cuda.Event(enable_timing=True)
     for i in range(args.warmup + args.steps):
         flush_l2()
         barrier()
         ev0.record()
         s.write_packed(e2e_slots, staging.view(np.uint32), offs)
+        evm.record()
         res, _ = step(e2e_slots)
         ev1.record()
         ev1.synchronize()
         if i >= args.warmup:
             e2e_ms.append(ev0.elapsed_time(ev1))
+            up_ms += ev0.elapsed_time(evm)
             e2e_priced += int(np.count_nonzero(res["flags"] & N.F_PRICED))
             n_cand = len(res)
     del staging
@@ -357,7 +360,8 @@ def run_ours(args, world, rank, local):
                          "peak": hbm_peak, "unit": "GB/s", "frac": keys_bytes / (keys_ms / 1e3) / 1e9 / hbm_peak,
                          "peak_source": hbm_src, "traffic": None},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(blob.nbytes),
-                "d2h_bytes_per_step": n_cand * N.CAND_DTYPE.itemsize},
+                "d2h_bytes_per_step": n_cand * N.CAND_DTYPE.itemsize,
+                "ms_per_step": sum(e2e_ms) / len(e2e_ms), "upload_hash_ms_per_step": up_ms / args.steps},
         "gpu_launches": (13 if world == 1 else 17) * args.steps,
         "clocks": clk,
     }

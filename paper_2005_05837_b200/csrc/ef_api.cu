@@ -1155,9 +1155,20 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       k_keys<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
       EF_CUDA(cudaGetLastError());
       cudaEventRecord(ce[2], ctx->st);
-      if ((rc = sort_fresh_keys(ctx, V))) return rc;
-      cudaEventRecord(ce[3], ctx->st);
-      k_digest<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+      if (S <= 256) {  // warp merge into a contiguous key stream, streaming digest
+        const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 32));
+        if (S <= 32) k_merge<1, 4><<<gm, 128, 0, ctx->st>>>(V);
+        else if (S <= 64) k_merge<2, 4><<<gm, 128, 0, ctx->st>>>(V);
+        else if (S <= 128) k_merge<4, 4><<<gm, 128, 0, ctx->st>>>(V);
+        else k_merge<8, 4><<<gm, 128, 0, ctx->st>>>(V);
+        EF_CUDA(cudaGetLastError());
+        cudaEventRecord(ce[3], ctx->st);
+        k_digest_pm<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+      } else {
+        if ((rc = sort_fresh_keys(ctx, V))) return rc;
+        cudaEventRecord(ce[3], ctx->st);
+        k_digest<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+      }
       EF_CUDA(cudaGetLastError());
       cudaEventRecord(ce[4], ctx->st);
     }

@@ -708,6 +708,247 @@ __global__ void __launch_bounds__(BT) k_digest(VArgs A) {
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// k_merge (rows of <= 32K keys): one warp per candidate builds the candidate's sorted key
+// stream graph.py:547 sorted(keys) -- the fresh keys sorted in registers (bitonic network,
+// K per lane, shuffles across lanes), the parent's pre-sorted keys compacted past the removed
+// ranks (ballot), and both merged by rank (each key's position = own index + its count of
+// smaller keys in the other list, by binary search in shared memory).  The stream is written
+// contiguously, so k_digest_pm reads it with vector loads.
+// ------------------------------------------------------------------------------------------
+
+__device__ __forceinline__ bool be_less(uint64_t a0, uint64_t a1, uint64_t b0, uint64_t b1) {
+  return a0 < b0 || (a0 == b0 && a1 < b1);
+}
+
+template <int K, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_merge(VArgs A) {
+  constexpr int M = 32 * K;
+  __shared__ uint64_t sa_all[WARPS * M * 2];  // parent keys (big-endian word pairs)
+  __shared__ uint64_t sb_all[WARPS * M * 2];  // fresh keys in order
+  const Geo& G = A.g;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint64_t* sa = sa_all + w * M * 2;
+  uint64_t* sb = sb_all + w * M * 2;
+  for (uint32_t lc = blockIdx.x * WARPS + w; lc < A.n; lc += gridDim.x * WARPS) {
+    const uint32_t c = A.c0 + lc;
+    if (A.res[c].flags & EF_F_INCOMPLETE) continue;
+    const VPlan& P = A.plan[c];
+    const int pn = P.pn;
+    const uint32_t d = A.dcount[lc];
+    const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
+    // 1) sort values (first 4 key bytes, big endian, above the job index) in registers
+    uint64_t v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t i = lane * K + k;
+      v[k] = i < d ? ((B2b::bswap64(fresh[2 * i]) >> 32) << 32) | i : ~0ULL;
+    }
+#pragma unroll
+    for (int size = 2; size <= M; size <<= 1) {
+#pragma unroll
+      for (int j = size >> 1; j > 0; j >>= 1) {
+        if (j < K) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            if (k & j) continue;
+            const uint32_t i = lane * K + k;
+            const bool up = (i & size) == 0;
+            const uint64_t a = v[k], b = v[k | j];
+            if ((a > b) == up) {
+              v[k] = b;
+              v[k | j] = a;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const uint32_t i = lane * K + k;
+            const uint64_t o = __shfl_xor_sync(0xffffffffu, v[k], j / K);
+            const bool up = (i & size) == 0, lower = (i & j) == 0;
+            v[k] = (lower == up) ? (o < v[k] ? o : v[k]) : (o > v[k] ? o : v[k]);
+          }
+        }
+      }
+    }
+    // 2) fresh keys in sorted order (ties on the first 4 bytes fixed by the full key)
+    bool tie = false;
+#pragma unroll
+    for (int k = 0; k + 1 < K; ++k) tie |= (lane * K + k + 1 < d) && (v[k] >> 32) == (v[k + 1] >> 32);
+    const uint64_t nxt = __shfl_down_sync(0xffffffffu, v[0], 1);
+    tie |= lane < 31 && (uint32_t)((lane + 1) * K) < d && (v[K - 1] >> 32) == (nxt >> 32);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t i = lane * K + k;
+      if (i < d) {
+        const uint32_t jx = (uint32_t)v[k];
+        sb[2 * i] = B2b::bswap64(fresh[2 * jx]);
+        sb[2 * i + 1] = B2b::bswap64(fresh[2 * jx + 1]);
+      }
+    }
+    __syncwarp();
+    if (__any_sync(0xffffffffu, tie)) {  // p ~ d^2 / 2^33: insertion sort of the whole list by full key
+      if (lane == 0) {
+        for (uint32_t x = 1; x < d; ++x) {
+          const uint64_t k0 = sb[2 * x], k1 = sb[2 * x + 1];
+          uint32_t y = x;
+          while (y > 0 && be_less(k0, k1, sb[2 * (y - 1)], sb[2 * (y - 1) + 1])) {
+            sb[2 * y] = sb[2 * (y - 1)];
+            sb[2 * y + 1] = sb[2 * (y - 1) + 1];
+            --y;
+          }
+          sb[2 * y] = k0;
+          sb[2 * y + 1] = k1;
+        }
+      }
+      __syncwarp();
+    }
+    // 3) the parent's sorted keys minus removed ranks
+    Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
+    const uint64_t* pskeys = R.skeys(G);
+    const uint32_t* rm = A.rmask + (uint64_t)lc * A.W;
+    uint32_t na = 0;
+    for (int r0 = 0; r0 < pn; r0 += 32) {
+      const int r = r0 + lane;
+      const bool keep = r < pn && !((rm[r0 >> 5] >> lane) & 1u);
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const uint32_t at = na + __popc(bal & ((1u << lane) - 1u));
+        sa[2 * at] = B2b::bswap64(pskeys[2 * r]);
+        sa[2 * at + 1] = B2b::bswap64(pskeys[2 * r + 1]);
+      }
+      na += __popc(bal);
+    }
+    __syncwarp();
+    // 4) merge by rank into the candidate's key stream (raw little-endian words)
+    uint64_t* out = A.fresh_sorted + 2ull * lc * A.S;
+    for (uint32_t i = lane; i < na; i += 32) {
+      const uint64_t k0 = sa[2 * i], k1 = sa[2 * i + 1];
+      uint32_t lo = 0, hi = d;  // fresh keys < this one
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (be_less(sb[2 * mid], sb[2 * mid + 1], k0, k1)) lo = mid + 1;
+        else hi = mid;
+      }
+      out[2 * (i + lo)] = B2b::bswap64(k0);
+      out[2 * (i + lo) + 1] = B2b::bswap64(k1);
+    }
+    for (uint32_t j = lane; j < d; j += 32) {
+      const uint64_t k0 = sb[2 * j], k1 = sb[2 * j + 1];
+      uint32_t lo = 0, hi = na;  // parent keys <= this one
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (!be_less(k0, k1, sa[2 * mid], sa[2 * mid + 1])) lo = mid + 1;
+        else hi = mid;
+      }
+      out[2 * (j + lo)] = B2b::bswap64(k0);
+      out[2 * (j + lo) + 1] = B2b::bswap64(k1);
+    }
+    __syncwarp();
+  }
+}
+
+// The graph digest over a pre-merged key stream: the prefix (input declarations, output keys
+// and ports) goes through the word sink; the keys follow as full words with a constant byte
+// shift, loaded 16 words per block with independent 16-byte loads.
+template <int BT>
+__global__ void __launch_bounds__(BT) k_digest_pm(VArgs A) {
+  __shared__ uint64_t blk[16 * BT];
+  const Geo& G = A.g;
+  const Tables& T = A.T;
+  uint64_t* col = blk + threadIdx.x;
+  for (uint32_t lc = blockIdx.x * BT + threadIdx.x; lc < A.n; lc += gridDim.x * BT) {
+    const uint32_t c = A.c0 + lc;
+    if (A.res[c].flags & EF_F_INCOMPLETE) continue;
+    const VPlan& P = A.plan[c];
+    Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
+    const uint64_t* pkeys = R.keys(G);
+    const uint32_t* pouts = R.outs(G);
+    const int n_out = R.h().n_out;
+    const uint32_t* didx = A.didx + (uint64_t)lc * A.S;
+    const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
+    const uint64_t* ks = A.fresh_sorted + 2ull * lc * A.S;  // merged key stream
+    const uint32_t li = T.input_text_len;
+    const uint32_t n_child = (uint32_t)(P.n_keep + P.n_live);
+    const uint32_t kwords = 2 * n_child;
+    const uint64_t len = (uint64_t)li + 18ull * n_out + 16ull * n_child;
+    const uint32_t nblk = (uint32_t)((len + 127) >> 7);
+    int phase = 0;  // 0 input text, 1 outputs, 2 keys, 3 done
+    uint32_t gi = 0, part = 0, kw = 0;
+    uint64_t cw1 = 0;
+    WordSink<BT> sk;
+    sk.init(col);
+    uint64_t h[8];
+    b2b_start(h, 8);
+    for (uint32_t b = 0; b < nblk; ++b) {
+      sk.q = 0;
+      while (sk.q < 16 && phase < 2) {
+        if (phase == 0) {
+          if (gi * 8 < li) {
+            sk.push(__ldg(A.input_words + gi), min(8u, li - gi * 8));
+            ++gi;
+          } else {
+            phase = 1;
+            gi = 0;
+          }
+        } else {
+          if ((int)gi < n_out) {
+            const uint32_t ref = vremap(P, pouts[gi]);
+            if (part == 0) {
+              const uint32_t p = ref >> 8, fi = didx[p];
+              const uint64_t* kp = fi ? fresh + 2 * (fi - 1) : pkeys + 2 * p;
+              sk.push(kp[0], 8);
+              cw1 = kp[1];
+              part = 1;
+            } else if (part == 1) {
+              sk.push(cw1, 8);
+              part = 2;
+            } else {
+              sk.push(port_be(ref & 255u), 2);
+              part = 0;
+              ++gi;
+            }
+          } else {
+            phase = 2;
+          }
+        }
+      }
+      if (phase == 2 && sk.q < 16) {  // keys: full words at a constant shift
+        const uint32_t room = 16 - sk.q;
+        const uint32_t take = min(room, kwords - kw);
+        uint64_t wv[16];
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          if ((uint32_t)i < take) {
+            const uint4 x = *reinterpret_cast<const uint4*>(ks + ((kw + i) & ~1u));
+            // kw is even except after an odd take; load the aligned pair then pick
+            const uint64_t lo = ((uint64_t)x.y << 32) | x.x, hi = ((uint64_t)x.w << 32) | x.z;
+            if ((kw & 1u) == 0) {
+              wv[i] = lo;
+              wv[i + 1] = hi;
+            } else {
+              wv[i] = hi;
+              wv[i + 1] = (uint32_t)(i + 1) < take ? ks[kw + i + 1] : 0;
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if ((uint32_t)i < take) sk.push(wv[i], 8);
+        kw += take;
+        if (kw == kwords) phase = 3;
+      }
+      if (phase == 3 && sk.q < 16) {
+        sk.flush();
+        for (uint32_t q = sk.q; q < 16; ++q) col[q * BT] = 0;
+      }
+      b2b_compress_col<BT>(h, col, len < 128ull * (b + 1) ? len : 128ull * (b + 1), b + 1 == nblk);
+    }
+    A.res[c].hash = B2b::bswap64(h[0]);
+    if (A.stats) atomicAdd(A.stats + 1, (unsigned long long)nblk);
+  }
+}
+
 // full mode: one job per node in topological order; every producer key is fresh
 __global__ void k_full_jobs(VArgs A) {
   const Geo& G = A.g;

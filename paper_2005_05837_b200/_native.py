@@ -155,9 +155,11 @@ def check(ctx, rc: int, what: str) -> int:
 
 
 def u32_array(values):
-    arr = (C.c_uint32 * max(1, len(values)))(*values)
-    return arr
+    """uint32 buffer for a C call (numpy-backed: no per-element ctypes conversion)."""
+    arr = _np.ascontiguousarray(_np.asarray(values if len(values) else [0], dtype=_np.uint32))
+    return arr.ctypes.data_as(_U32P)  # the pointer keeps a reference to `arr`
 
 
 def i32_array(values):
-    return (C.c_int32 * max(1, len(values)))(*values)
+    arr = _np.ascontiguousarray(_np.asarray(values if len(values) else [0], dtype=_np.int32))
+    return arr.ctypes.data_as(_I32P)

@@ -721,9 +721,64 @@ __device__ __forceinline__ bool be_less(uint64_t a0, uint64_t a1, uint64_t b0, u
   return a0 < b0 || (a0 == b0 && a1 < b1);
 }
 
-template <int K, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_merge(VArgs A) {
+// sort the d (<= 32K) fresh keys of one candidate by the warp; writes them (big-endian word
+// pairs) to sb in ascending order and returns whether two first words tied
+template <int K>
+__device__ __forceinline__ bool warp_sort_fresh(const uint64_t* fresh, uint32_t d, uint64_t* sb, int lane) {
   constexpr int M = 32 * K;
+  uint64_t v[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const uint32_t i = lane * K + k;
+    v[k] = i < d ? ((B2b::bswap64(fresh[2 * i]) >> 32) << 32) | i : ~0ULL;
+  }
+#pragma unroll
+  for (int size = 2; size <= M; size <<= 1) {
+#pragma unroll
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      if (j < K) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if (k & j) continue;
+          const uint32_t i = lane * K + k;
+          const bool up = (i & size) == 0;
+          const uint64_t a = v[k], b = v[k | j];
+          if ((a > b) == up) {
+            v[k] = b;
+            v[k | j] = a;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const uint32_t i = lane * K + k;
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, v[k], j / K);
+          const bool up = (i & size) == 0, lower = (i & j) == 0;
+          v[k] = (lower == up) ? (o < v[k] ? o : v[k]) : (o > v[k] ? o : v[k]);
+        }
+      }
+    }
+  }
+  bool tie = false;
+#pragma unroll
+  for (int k = 0; k + 1 < K; ++k) tie |= (lane * K + k + 1 < d) && (v[k] >> 32) == (v[k + 1] >> 32);
+  const uint64_t nxt = __shfl_down_sync(0xffffffffu, v[0], 1);
+  tie |= lane < 31 && (uint32_t)((lane + 1) * K) < d && (v[K - 1] >> 32) == (nxt >> 32);
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const uint32_t i = lane * K + k;
+    if (i < d) {
+      const uint32_t jx = (uint32_t)v[k];
+      sb[2 * i] = B2b::bswap64(fresh[2 * jx]);
+      sb[2 * i + 1] = B2b::bswap64(fresh[2 * jx + 1]);
+    }
+  }
+  return tie;
+}
+
+template <int KMAX, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_merge(VArgs A) {
+  constexpr int M = 32 * KMAX;
   __shared__ uint64_t sa_all[WARPS * M * 2];  // parent keys (big-endian word pairs)
   __shared__ uint64_t sb_all[WARPS * M * 2];  // fresh keys in order
   const Geo& G = A.g;
@@ -737,55 +792,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge(VArgs A) {
     const int pn = P.pn;
     const uint32_t d = A.dcount[lc];
     const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
-    // 1) sort values (first 4 key bytes, big endian, above the job index) in registers
-    uint64_t v[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint32_t i = lane * K + k;
-      v[k] = i < d ? ((B2b::bswap64(fresh[2 * i]) >> 32) << 32) | i : ~0ULL;
-    }
-#pragma unroll
-    for (int size = 2; size <= M; size <<= 1) {
-#pragma unroll
-      for (int j = size >> 1; j > 0; j >>= 1) {
-        if (j < K) {
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            if (k & j) continue;
-            const uint32_t i = lane * K + k;
-            const bool up = (i & size) == 0;
-            const uint64_t a = v[k], b = v[k | j];
-            if ((a > b) == up) {
-              v[k] = b;
-              v[k | j] = a;
-            }
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const uint32_t i = lane * K + k;
-            const uint64_t o = __shfl_xor_sync(0xffffffffu, v[k], j / K);
-            const bool up = (i & size) == 0, lower = (i & j) == 0;
-            v[k] = (lower == up) ? (o < v[k] ? o : v[k]) : (o > v[k] ? o : v[k]);
-          }
-        }
-      }
-    }
-    // 2) fresh keys in sorted order (ties on the first 4 bytes fixed by the full key)
-    bool tie = false;
-#pragma unroll
-    for (int k = 0; k + 1 < K; ++k) tie |= (lane * K + k + 1 < d) && (v[k] >> 32) == (v[k + 1] >> 32);
-    const uint64_t nxt = __shfl_down_sync(0xffffffffu, v[0], 1);
-    tie |= lane < 31 && (uint32_t)((lane + 1) * K) < d && (v[K - 1] >> 32) == (nxt >> 32);
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint32_t i = lane * K + k;
-      if (i < d) {
-        const uint32_t jx = (uint32_t)v[k];
-        sb[2 * i] = B2b::bswap64(fresh[2 * jx]);
-        sb[2 * i + 1] = B2b::bswap64(fresh[2 * jx + 1]);
-      }
-    }
+    // 1) the fresh keys sorted in registers, network sized to this candidate (warp-uniform)
+    bool tie;
+    if (d <= 32) tie = warp_sort_fresh<1>(fresh, d, sb, lane);
+    else if (d <= 64 || KMAX < 4) tie = warp_sort_fresh<(KMAX < 2 ? KMAX : 2)>(fresh, d, sb, lane);
+    else if (d <= 128 || KMAX < 8) tie = warp_sort_fresh<(KMAX < 4 ? KMAX : 4)>(fresh, d, sb, lane);
+    else tie = warp_sort_fresh<KMAX>(fresh, d, sb, lane);
     __syncwarp();
     if (__any_sync(0xffffffffu, tie)) {  // p ~ d^2 / 2^33: insertion sort of the whole list by full key
       if (lane == 0) {

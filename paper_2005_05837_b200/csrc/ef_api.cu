@@ -803,7 +803,7 @@ static int hash_records_full(ef_ctx* ctx, const unsigned long long* d_rec, uint3
     V.c0 = c0;
     V.n = std::min(chunk, n - c0);
     const uint32_t gd = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 127) / 128, ctx->n_sm * 16));
-    k_full_jobs<<<gd, 128, 0, ctx->st>>>(V);
+    k_full_jobs<256><<<std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * 8)), 256, 0, ctx->st>>>(V);
     EF_CUDA(cudaGetLastError());
     size_t t1 = ctx->d_sort_tmp.cap;
     EF_CUDA(cub::DeviceRadixSort::SortPairsDescending(ctx->d_sort_tmp.p, t1, ctx->d_dcount.p, ctx->d_dsorted.p,

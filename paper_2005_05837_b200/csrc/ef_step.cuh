@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
     uint64_t* skey = A.skey + (uint64_t)lc * A.S;
     uint32_t* sval = A.sval + (uint64_t)lc * A.S;
     uint32_t ncomp = 0;
+    uint64_t last0 = 0, last1 = 0;
     for (uint32_t jj = 0; jj < d; ++jj) {
       const Job jb = jobs[jj];
       const uint32_t tlen = T.sig_text_len[jb.sig];
@@ -406,9 +407,17 @@ __global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
         for (uint32_t k = 0; k < nin; ++k) {
           const uint32_t sv = rs[jb.roff + k];
           const uint32_t idx = sv & 0x7fffffu, port = (sv >> 23) & 255u;
-          const uint64_t* kp = (sv & kFresh) ? fresh + 2 * idx : pkeys + 2 * idx;
-          sk.push(kp[0], 8);
-          sk.push(kp[1], 8);
+          uint64_t k0, k1;
+          if ((sv & kFresh) && idx + 1 == jj) {  // the previous job's key, still in registers
+            k0 = last0;
+            k1 = last1;
+          } else {
+            const uint64_t* kp = (sv & kFresh) ? fresh + 2 * idx : pkeys + 2 * idx;
+            k0 = kp[0];
+            k1 = kp[1];
+          }
+          sk.push(k0, 8);
+          sk.push(k1, 8);
           sk.push(port_be(port), 2);
         }
         sk.flush();
@@ -421,6 +430,8 @@ __global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
       }
       fresh[2 * jj] = h[0];
       fresh[2 * jj + 1] = h[1];
+      last0 = h[0];
+      last1 = h[1];
       skey[jj] = B2b::bswap64(h[0]);
       sval[jj] = jj;
     }
@@ -961,11 +972,14 @@ __global__ void __launch_bounds__(BT) k_digest_pm(VArgs A) {
   }
 }
 
-// full mode: one job per node in topological order; every producer key is fresh
-__global__ void k_full_jobs(VArgs A) {
+// full mode: one job per node in topological order (job index = topological slot), every
+// producer key fresh.  Block per record: slots in parallel, ref offsets by a block scan.
+template <int BT>
+__global__ void __launch_bounds__(BT) k_full_jobs(VArgs A) {
+  __shared__ uint32_t sh_scan[BT / 32 + 1];
   const Geo& G = A.g;
   const Tables& T = A.T;
-  for (uint32_t lc = blockIdx.x * blockDim.x + threadIdx.x; lc < A.n; lc += gridDim.x * blockDim.x) {
+  for (uint32_t lc = blockIdx.x; lc < A.n; lc += gridDim.x) {
     const uint32_t c = A.c0 + lc;
     Rec R{reinterpret_cast<char*>(A.parent_addr[c])};
     const int n = R.h().n;
@@ -979,27 +993,45 @@ __global__ void k_full_jobs(VArgs A) {
     uint32_t* jv = A.jv + (uint64_t)lc * A.S;
     Job* jobs = A.jobs + (uint64_t)lc * A.S;
     uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
-    uint32_t r = 0;
-    for (int s = 0; s < n; ++s) {
+    for (int s = threadIdx.x; s < n; s += BT) {
       const uint32_t v = topo[s];
-      const uint32_t sg = sig[v];
-      if (T.sig_desc[sg].kind == EF_K_INPUT) {
-        jobs[s] = Job{sg, aux[v], 0u, kInputJob};
-      } else {
-        const uint32_t r0 = inoff[v], nr = nin[v];
-        for (uint32_t k = 0; k < nr; ++k) {
-          const uint32_t ref = refs[r0 + k];
-          rs[r + k] = kFresh | ((ref & 255u) << 23) | (didx[ref >> 8] - 1);
-        }
-        jobs[s] = Job{sg, aux[v], r, nr};
-        r += nr;
-      }
       didx[v] = (uint32_t)s + 1;
       jv[s] = v;
     }
-    A.dcount[lc] = (uint32_t)n;
-    A.seg_begin[lc] = (int32_t)((uint64_t)lc * A.S);
-    A.seg_end[lc] = (int32_t)((uint64_t)lc * A.S + n);
+    __syncthreads();
+    uint32_t run = 0;
+    for (int s0 = 0; s0 < n; s0 += BT) {
+      const int s = s0 + threadIdx.x;
+      uint32_t v = 0, sg = 0, nr = 0;
+      bool input = false;
+      if (s < n) {
+        v = topo[s];
+        sg = sig[v];
+        input = T.sig_desc[sg].kind == EF_K_INPUT;
+        nr = input ? 0u : nin[v];
+      }
+      uint32_t tot;
+      const uint32_t r = run + block_excl_scan<BT>(nr, &tot, sh_scan);
+      if (s < n) {
+        if (input) {
+          jobs[s] = Job{sg, aux[v], 0u, kInputJob};
+        } else {
+          const uint32_t r0 = inoff[v];
+          for (uint32_t k = 0; k < nr; ++k) {
+            const uint32_t ref = refs[r0 + k];
+            rs[r + k] = kFresh | ((ref & 255u) << 23) | (didx[ref >> 8] - 1);
+          }
+          jobs[s] = Job{sg, aux[v], r, nr};
+        }
+      }
+      run += tot;
+    }
+    if (threadIdx.x == 0) {
+      A.dcount[lc] = (uint32_t)n;
+      A.seg_begin[lc] = (int32_t)((uint64_t)lc * A.S);
+      A.seg_end[lc] = (int32_t)((uint64_t)lc * A.S + n);
+    }
+    __syncthreads();
   }
 }
 

@@ -140,6 +140,7 @@ class DeviceSession:
         self.input_text = b""
         self.db: CostDatabase | None = None
         self.profiler: ProfilerSpec | None = None
+        self._pinned, self._pinned_bytes = None, 0  # page-locked staging of step results
 
     @classmethod
     def default(cls) -> "DeviceSession":
@@ -149,6 +150,9 @@ class DeviceSession:
             return cls._default
 
     def close(self):
+        if self._pinned:
+            self.L.ef_host_free(self._pinned)
+            self._pinned, self._pinned_bytes = None, 0
         if self.ctx:
             self.L.ef_destroy(self.ctx)
             self.ctx = None
@@ -454,10 +458,24 @@ class DeviceSession:
                 continue
             self._check(rc, "ef_expand")
             break
-        n = count.value
-        out = np.empty(n, dtype=N.CAND_DTYPE)
+        return self._results(count.value)
+
+    def _results(self, n: int) -> np.ndarray:
+        """The last step's candidate results, copied into page-locked host memory (full D2H
+        bandwidth).  The array is a view of a buffer the next step reuses: callers that keep
+        results across steps copy them."""
+        need = max(1, n) * N.CAND_DTYPE.itemsize
+        if self._pinned_bytes < need:
+            if self._pinned:
+                self.L.ef_host_free(self._pinned)
+            size = max(need, 2 * self._pinned_bytes)
+            self._pinned = self.L.ef_host_alloc(size)
+            if not self._pinned:
+                raise N.NativeError("ef_host_alloc failed")
+            self._pinned_bytes = size
+        out = np.ctypeslib.as_array((C.c_uint8 * need).from_address(self._pinned)).view(N.CAND_DTYPE)[:n]
         if n:
-            self._check(self.L.ef_results(self.ctx, out.ctypes.data, n), "ef_results")
+            self._check(self.L.ef_results(self.ctx, self._pinned, n), "ef_results")
         return out
 
     # ---- hash-owner sharding (see shard.py) ------------------------------------------
@@ -493,10 +511,7 @@ class DeviceSession:
     def expand_finish(self, verdict_back, pp: N.PriceParams, n: int) -> np.ndarray:
         self._check(self.L.ef_expand_finish(self.ctx, C.c_void_p(verdict_back.data_ptr()), C.byref(pp)),
                     "ef_expand_finish")
-        out = np.empty(n, dtype=N.CAND_DTYPE)
-        if n:
-            self._check(self.L.ef_results(self.ctx, out.ctypes.data, n), "ef_results")
-        return out
+        return self._results(n)
 
     def keep(self, cand_idx: list[int]) -> list[int]:
         slots = [self.alloc() for _ in cand_idx]

@@ -472,6 +472,7 @@ class Frontier:
         self.s.visited_reset(1 << 22)
 
     def step(self, slots=None, insert_visited: bool = False):
+        """One batched expansion; the results view is valid until the session's next step."""
         return self.s.expand(slots if slots is not None else self.slots, self.rule_ids, self.pp, insert_visited)
 
     def decode(self, slot: int) -> Graph:

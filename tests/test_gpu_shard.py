@@ -93,7 +93,7 @@ def test_sharded_step_equals_single(model, n_parents):
     rule_ids = [r.rule_id for r in ef.default_rules()]
 
     s_all, slots_all = _session(g0, db, prof, cap, graphs, visited)
-    single = s_all.expand(slots_all, rule_ids, pp, insert_visited=False)
+    single = s_all.expand(slots_all, rule_ids, pp, insert_visited=False).copy()
     s_all.close()
 
     world, split = 2, len(graphs) // 3
@@ -105,7 +105,7 @@ def test_sharded_step_equals_single(model, n_parents):
         try:
             mine = [h for h in visited if owner_of(h, world) == rank]
             s, slots = _session(g0, db, prof, cap, parts[rank], mine)
-            out[rank] = sharded_expand(s, slots, rule_ids, pp, ThreadExchange(rank, world, shared))
+            out[rank] = sharded_expand(s, slots, rule_ids, pp, ThreadExchange(rank, world, shared)).copy()
             s.close()
         except Exception as e:  # pragma: no cover - reported below
             errs.append(e)

@@ -778,6 +778,20 @@ int ef_record_read(ef_ctx* ctx, uint32_t slot, void* host, uint64_t bytes) {
 // kept candidates): the step's job pipeline with every node a job (ef_step.cuh, full mode).
 static int sort_fresh_keys(ef_ctx* ctx, const VArgs& V);
 static uint32_t bits_for(uint32_t v);
+
+// node keys: a thread per candidate when the chunk fills the GPU, four lanes per candidate
+// (lower latency per compression) when it does not
+static int launch_keys(ef_ctx* ctx, const VArgs& V) {
+  if (V.n < 20000u) {
+    const uint32_t gq = std::max<uint32_t>(1, (V.n + 31) / 32);
+    k_keys_quad<128><<<gq, 128, 0, ctx->st>>>(V);
+  } else {
+    const uint32_t gd = std::max<uint32_t>(1, std::min<uint32_t>((V.n + kHashThreads - 1) / kHashThreads, ctx->n_sm * 16));
+    k_keys<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+  }
+  EF_CUDA(cudaGetLastError());
+  return EF_OK;
+}
 static int ensure_chunk(ef_ctx* ctx, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk);
 static VArgs chunk_args(ef_ctx* ctx, uint32_t S, uint32_t Rs);
 static int hash_records_full(ef_ctx* ctx, const unsigned long long* d_rec, uint32_t n, uint64_t* d_hash_out) {
@@ -809,8 +823,7 @@ static int hash_records_full(ef_ctx* ctx, const unsigned long long* d_rec, uint3
     EF_CUDA(cub::DeviceRadixSort::SortPairsDescending(ctx->d_sort_tmp.p, t1, ctx->d_dcount.p, ctx->d_dsorted.p,
                                                       ctx->d_iota.p, ctx->d_dorder.p, (int)V.n, 0, bits_for(S),
                                                       ctx->st));
-    k_keys<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
-    EF_CUDA(cudaGetLastError());
+    if ((rc = launch_keys(ctx, V))) return rc;
     if ((rc = sort_fresh_keys(ctx, V))) return rc;
     k_digest<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
     k_full_store<<<std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * 8)), 128, 0, ctx->st>>>(V);
@@ -1152,8 +1165,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
                                                         ctx->d_iota.p, ctx->d_dorder.p, (int)V.n, 0, bits_for(S),
                                                         ctx->st));
       cudaEventRecord(ce[1], ctx->st);
-      k_keys<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
-      EF_CUDA(cudaGetLastError());
+      if ((rc = launch_keys(ctx, V))) return rc;
       cudaEventRecord(ce[2], ctx->st);
       if (S <= 256) {  // warp merge into a contiguous key stream, streaming digest
         const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 32));

@@ -516,6 +516,161 @@ __global__ void __launch_bounds__(WARPS * 32) k_sortkeys(VArgs A) {
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// k_keys_quad: the same jobs with four lanes per candidate, for launches too small to fill
+// the GPU (uploads, kept records, single-parent expansions): lane q of a quad holds column q
+// of the BLAKE2b state (v[q], v[q+4], v[q+8], v[q+12]) and computes one G of every half
+// round; quad shuffles rotate b/c/d between the column and the diagonal step.  The message
+// is assembled by the quad's lane 0 into the quad's shared-memory column.
+// ------------------------------------------------------------------------------------------
+
+template <int QN>
+__device__ __forceinline__ void b2b_compress_quad(uint64_t& h0, uint64_t& h1, const uint64_t* col, uint64_t t,
+                                                  bool last, int q, int qbase) {
+  uint64_t a = h0, b = h1, c = b2b_iv(q), d = b2b_iv(4 + q);
+  if (q == 0) d ^= t;
+  if (q == 2 && last) d = ~d;
+  const unsigned full = 0xffffffffu;
+#pragma unroll 1
+  for (int r = 0; r < 12; ++r) {
+    const uint8_t* s = kB2bSigma[r < 10 ? r : r - 10];
+    const uint64_t x0 = col[s[2 * q] * QN], y0 = col[s[2 * q + 1] * QN];
+    const uint64_t x1 = col[s[8 + 2 * q] * QN], y1 = col[s[9 + 2 * q] * QN];
+    EF_B2B_G(a, b, c, d, x0, y0);
+    b = __shfl_sync(full, b, qbase | ((q + 1) & 3));
+    c = __shfl_sync(full, c, qbase | ((q + 2) & 3));
+    d = __shfl_sync(full, d, qbase | ((q + 3) & 3));
+    EF_B2B_G(a, b, c, d, x1, y1);
+    b = __shfl_sync(full, b, qbase | ((q + 3) & 3));
+    c = __shfl_sync(full, c, qbase | ((q + 2) & 3));
+    d = __shfl_sync(full, d, qbase | ((q + 1) & 3));
+  }
+  h0 ^= a ^ c;
+  h1 ^= b ^ d;
+}
+
+template <int BT>
+__global__ void __launch_bounds__(BT) k_keys_quad(VArgs A) {
+  constexpr int QN = BT / 4;  // quads per block
+  __shared__ uint64_t msg[kKeyMaxW * QN];
+  const Geo& G = A.g;
+  const Tables& T = A.T;
+  const int q = threadIdx.x & 3, quad = threadIdx.x >> 2;
+  const int qbase = (threadIdx.x & 31) & ~3;
+  uint64_t* col = msg + quad;
+  const uint32_t nq = (A.n + QN - 1) / QN * QN;  // whole blocks iterate together
+  for (uint32_t l = blockIdx.x * QN + quad; l < nq; l += gridDim.x * QN) {
+    const bool live = l < A.n;
+    const uint32_t lc = live ? A.order[l] : 0;
+    const uint32_t d = live ? A.dcount[lc] : 0;
+    const uint32_t dmax = __reduce_max_sync(0xffffffffu, d);  // lanes of the warp loop together
+    const uint32_t c = A.c0 + lc;
+    const uint64_t* pkeys =
+        (A.full || !live) ? nullptr : Rec{reinterpret_cast<char*>(A.parent_addr[A.plan[c].parent])}.keys(G);
+    const Job* jobs = A.jobs + (uint64_t)lc * A.S;
+    const uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
+    uint64_t* fresh = A.fresh + 2ull * lc * A.S;
+    uint64_t* skey = A.skey + (uint64_t)lc * A.S;
+    uint32_t* sval = A.sval + (uint64_t)lc * A.S;
+    uint64_t last0 = 0, last1 = 0;
+    uint32_t ncomp = 0;
+    for (uint32_t jj = 0; jj < dmax; ++jj) {
+      const bool act = jj < d;
+      uint32_t len = 0, nb = 0;
+      bool slow = false;
+      uint64_t sh0 = 0, sh1 = 0;
+      if (act && q == 0) {
+        const Job jb = jobs[jj];
+        const uint32_t tlen = T.sig_text_len[jb.sig];
+        const bool input = jb.nin & kInputJob;
+        const uint32_t nin = input ? 0u : jb.nin;
+        const uint32_t nlen = input ? T.name_len[jb.aux] : 0u;
+        len = tlen + nlen + 16u + 18u * nin;
+        if (len > 8u * kKeyMaxW) {
+          uint64_t hs[8];
+          job_key_slow(T, jb, rs, pkeys, fresh, hs);
+          sh0 = hs[0];
+          sh1 = hs[1];
+          slow = true;
+        } else {
+          WordSink<QN> sk;
+          sk.init(col);
+          const uint64_t* tw = reinterpret_cast<const uint64_t*>(T.sig_text + T.sig_text_off[jb.sig]);
+          const uint32_t fullw = tlen >> 3;
+          for (uint32_t i = 0; i < fullw; ++i) sk.push(__ldg(tw + i), 8);
+          if (tlen & 7u) sk.push(__ldg(tw + fullw), tlen & 7u);
+          const uint32_t ws = input ? kEmptyWset : jb.aux;
+          if (input) {
+            const uint8_t* nm = T.names + T.name_off[jb.aux];
+            for (uint32_t i = 0; i < nlen; ++i) sk.push(nm[i], 1);
+          }
+          sk.push(__ldg(T.ws_digest + 2 * ws), 8);
+          sk.push(__ldg(T.ws_digest + 2 * ws + 1), 8);
+          for (uint32_t k = 0; k < nin; ++k) {
+            const uint32_t sv = rs[jb.roff + k];
+            const uint32_t idx = sv & 0x7fffffu, port = (sv >> 23) & 255u;
+            uint64_t k0, k1;
+            if ((sv & kFresh) && idx + 1 == jj) {
+              k0 = last0;
+              k1 = last1;
+            } else {
+              const uint64_t* kp = (sv & kFresh) ? fresh + 2 * idx : pkeys + 2 * idx;
+              k0 = kp[0];
+              k1 = kp[1];
+            }
+            sk.push(k0, 8);
+            sk.push(k1, 8);
+            sk.push(port_be(port), 2);
+          }
+          sk.flush();
+          nb = (len + 127u) >> 7;
+          for (uint32_t w = sk.q; w < 16u * nb; ++w) col[w * QN] = 0;
+        }
+      }
+      // broadcast the job shape within the quad, then compress cooperatively
+      nb = __shfl_sync(0xffffffffu, nb, qbase);
+      len = __shfl_sync(0xffffffffu, len, qbase);
+      slow = __shfl_sync(0xffffffffu, (int)slow, qbase) != 0;
+      __syncwarp();
+      uint64_t h0 = b2b_iv(q), h1 = b2b_iv(4 + q);
+      if (q == 0) h0 ^= 0x01010000ULL ^ 16ULL;
+      const uint32_t nbmax = __reduce_max_sync(0xffffffffu, act && !slow ? nb : 0u);
+      for (uint32_t bk = 0; bk < nbmax; ++bk) {
+        const bool go = act && !slow && bk < nb;
+        // every lane of the warp runs the shuffles; quads without a block keep their state
+        uint64_t g0 = h0, g1 = h1;
+        b2b_compress_quad<QN>(g0, g1, col + 16 * bk * QN, (uint64_t)min(len, 128u * (bk + 1)), bk + 1 == nb, q,
+                              qbase);
+        if (go) {
+          h0 = g0;
+          h1 = g1;
+        }
+      }
+      // the 16-byte key is h[0] (lane 0) and h[1] (lane 1)
+      uint64_t k0 = __shfl_sync(0xffffffffu, h0, qbase);
+      uint64_t k1 = __shfl_sync(0xffffffffu, h0, qbase | 1);
+      if (slow) {
+        k0 = __shfl_sync(0xffffffffu, sh0, qbase);
+        k1 = __shfl_sync(0xffffffffu, sh1, qbase);
+      } else {
+        sh0 = __shfl_sync(0xffffffffu, sh0, qbase);  // keep the shuffles warp-uniform
+        sh1 = __shfl_sync(0xffffffffu, sh1, qbase);
+      }
+      if (act && q == 0) {
+        fresh[2 * jj] = k0;
+        fresh[2 * jj + 1] = k1;
+        skey[jj] = B2b::bswap64(k0);
+        sval[jj] = jj;
+        ncomp += slow ? 0u : nb;
+      }
+      last0 = k0;
+      last1 = k1;
+      __syncwarp();
+    }
+    if (A.stats && q == 0 && live) atomicAdd(A.stats, (unsigned long long)ncomp);
+  }
+}
+
 // runs of equal first words (a 2^-64 event unless the keys are identical) ordered by the second
 __global__ void k_sortfix(VArgs A) {
   for (uint32_t lc = blockIdx.x * blockDim.x + threadIdx.x; lc < A.n; lc += gridDim.x * blockDim.x) {

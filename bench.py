@@ -207,6 +207,30 @@ def _cpu_sample(parents, db, budget_s: float) -> dict:
     return {"value": priced / dt, "priced": priced, "expanded": expanded, "seconds": dt}
 
 
+def _search_e2e(ef, zoo, no_cpu: bool) -> dict:
+    """End-to-end search time of BASELINE configs[0] (SqueezeNet, energy, alpha = 1.0): the
+    whole outer_search through the public API (tables, profiling, every expansion on the GPU;
+    the CUDA context already exists), against the oracle port of the reference on one core.
+    The real reference took 28.5 s for this search in the build container
+    (tests/golden/golden_models.json, reference_seconds includes its expansion of the origin)."""
+    g = zoo.generate("squeezenet", 0)
+    t0 = time.perf_counter()
+    res = ef.outer_search(g, ef.default_rules(), ef.CostDatabase(), ef.CostFunction.energy(),
+                          ef.SearchConfig(alpha=1.0), ef.SyntheticProfiler(0))
+    gpu_s = time.perf_counter() - t0
+    out = {"config": "SqueezeNet inference graph, energy objective, alpha=1.0 (BASELINE configs[0])",
+           "gpu_s": gpu_s, "expansions": res.stats.graphs_explored, "generated": res.stats.graphs_generated,
+           "optimised_hash": ef.canonical_hash(res.graph)}
+    if not no_cpu:
+        from oracle import enerflow_oracle as orc
+
+        t0 = time.perf_counter()
+        ores = orc.outer_search(_to_oracle(g), RULES, orc.CostDB(), orc.CostFn("energy"), alpha=1.0, seed=0)
+        out["oracle_cpu_s"] = time.perf_counter() - t0
+        out["same_result"] = ores["hash"] == out["optimised_hash"] and ores["cost"] == res.cost
+    return out
+
+
 # ---------------------------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------------------------
@@ -365,6 +389,8 @@ def run_ours(args, world, rank, local):
         "gpu_launches": (13 if world == 1 else 17) * args.steps,
         "clocks": clk,
     }
+    if rank == 0 and world == 1:
+        line["search"] = _search_e2e(ef, zoo, args.no_cpu)
     if rank == 0 and world == 1 and not args.no_cpu:
         parents = [_to_oracle(fr.decode(sl)) for sl in mine[:8]]
         cpu = _cpu_sample(parents, db, args.cpu_budget)

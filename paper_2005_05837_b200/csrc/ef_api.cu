@@ -117,7 +117,7 @@ struct ef_ctx {
 
   // virtual-candidate step (ef_step.cuh)
   DevBuf<VPlan> d_plan;
-  DevBuf<uint32_t> d_route, d_perm, d_jv, d_recmax;
+  DevBuf<uint32_t> d_route, d_perm, d_jv, d_recmax, d_outsrc;
   DevBuf<unsigned long long> d_stats;
   DevBuf<unsigned long long> d_step_ord;
   uint32_t n_send = 0;
@@ -272,6 +272,7 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_plan.release();
   ctx->d_route.release();
   ctx->d_jv.release();
+  ctx->d_outsrc.release();
   ctx->d_recmax.release();
   ctx->d_stats.release();
   ctx->d_perm.release();
@@ -948,7 +949,7 @@ int ef_visited_count(ef_ctx* ctx, uint64_t* count) {
 static int ensure_parent_buffers(ef_ctx* ctx, uint32_t n_parents) {
   const Geo& g = ctx->geo;
   if (ctx->site_cap == 0) ctx->site_cap = std::max<uint32_t>(4 * g.cap_nodes, 256);
-  const uint64_t pstride = 5ull * g.cap_nodes + 1 + g.cap_refs;
+  const uint64_t pstride = 8ull * g.cap_nodes + 1 + 2ull * g.cap_refs;
   EF_CUDA(ctx->d_parent_addr.reserve(n_parents, ctx->st));
   EF_CUDA(ctx->d_pscratch.reserve(pstride * n_parents, ctx->st));
   EF_CUDA(ctx->d_sites.reserve((uint64_t)ctx->site_cap * n_parents, ctx->st));
@@ -1094,7 +1095,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
     A.parent_addr = ctx->d_parent_addr.p;
     A.n_parents = n_parents;
     A.pscratch = ctx->d_pscratch.p;
-    A.pstride = 5ull * g.cap_nodes + 1 + g.cap_refs;
+    A.pstride = 8ull * g.cap_nodes + 1 + 2ull * g.cap_refs;
     for (uint32_t i = 0; i < n_rules; ++i) A.rules[i] = rules[i];
     A.n_rules = (int32_t)n_rules;
     A.sites = ctx->d_sites.p;
@@ -1146,6 +1147,11 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
     VArgs V = chunk_args(ctx, S, Rs);
     V.parent_addr = A.parent_addr;
     V.stats = ctx->d_stats.p;
+    V.pscratch = A.pscratch;
+    V.pstride = A.pstride;
+    V.Os = ctx->h_scalars[8] + 2;
+    EF_CUDA(ctx->d_outsrc.reserve((uint64_t)chunk * V.Os, ctx->st));
+    V.outsrc = ctx->d_outsrc.p;
     ctx->n_chunks = 0;
     for (uint32_t c0 = 0; c0 < total; c0 += chunk) {
       V.c0 = c0;
@@ -1158,7 +1164,9 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       }
       cudaEvent_t* ce = ctx->ev_chunk.data() + 5 * ctx->n_chunks++;
       cudaEventRecord(ce[0], ctx->st);
-      k_dirty<<<gd, 128, 0, ctx->st>>>(V);
+      V.slots = S <= 256;
+      if (V.slots) k_dirty_slots<128><<<gd, 128, 0, ctx->st>>>(V);
+      else k_dirty<<<gd, 128, 0, ctx->st>>>(V);
       EF_CUDA(cudaGetLastError());
       size_t t1 = ctx->d_sort_tmp.cap;
       EF_CUDA(cub::DeviceRadixSort::SortPairsDescending(ctx->d_sort_tmp.p, t1, ctx->d_dcount.p, ctx->d_dsorted.p,
@@ -1167,7 +1175,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       cudaEventRecord(ce[1], ctx->st);
       if ((rc = launch_keys(ctx, V))) return rc;
       cudaEventRecord(ce[2], ctx->st);
-      if (S <= 256) {  // warp merge into a contiguous key stream, streaming digest
+      if (S <= 256) {  // slot-space walk, warp merge into a contiguous key stream, streaming digest
         const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 32));
         if (S <= 32) k_merge<1, 4><<<gm, 128, 0, ctx->st>>>(V);
         else if (S <= 64) k_merge<2, 4><<<gm, 128, 0, ctx->st>>>(V);

@@ -131,7 +131,7 @@ struct StepArgs {
   Tables T;
   const unsigned long long* parent_addr;
   uint32_t n_parents;
-  uint32_t* pscratch;  // per parent: u0[cap] u1[cap] coff[cap+1] ccur[cap] clist[cap_refs] tslot[cap]
+  uint32_t* pscratch;  // per parent: u0 u1 coff[+1] ccur [cap] clist[cap_refs] tslot s_v s_pk [cap] rslot[cap_refs]
   uint64_t pstride;    // words per parent
   int32_t rules[8];
   int32_t n_rules;
@@ -194,6 +194,20 @@ __global__ void __launch_bounds__(BT) k_match(StepArgs A) {
 
     for (int i = threadIdx.x; i < n; i += BT) u0[i] = u1[i] = ccur[i] = 0;
     __syncthreads();
+    {  // slot-space tables of the parent for k_dirty_slots: node + packed (ref offset, arity)
+       // per topological slot, and every ref as (producer slot << 8 | port)
+      uint32_t* s_v = tslot + G.cap_nodes;
+      uint32_t* s_pk = s_v + G.cap_nodes;
+      uint32_t* rslot = s_pk + G.cap_nodes;
+      const uint32_t* topo = R.topo(G);
+      for (int s = threadIdx.x; s < n; s += BT) {
+        const uint32_t v = topo[s];
+        s_v[s] = v;
+        s_pk[s] = inoff[v] | (nin[v] << 24);
+      }
+      const int n_refs = R.h().n_refs;
+      for (int r = threadIdx.x; r < n_refs; r += BT) rslot[r] = (tslot[refs[r] >> 8] << 8) | (refs[r] & 255u);
+    }
     for (int i = threadIdx.x; i < n; i += BT) {
       for (uint32_t r = inoff[i]; r < inoff[i] + nin[i]; ++r) {
         uint32_t p = refs[r] >> 8, port = refs[r] & 255u;
@@ -319,6 +333,7 @@ __global__ void __launch_bounds__(BT) k_match(StepArgs A) {
     if (threadIdx.x == 0) {
       atomicMax(&A.total[5], (uint32_t)n);  // step-wide maxima size the candidate scratch
       atomicMax(&A.total[6], R.h().n_refs);
+      atomicMax(&A.total[8], (uint32_t)n_out);
       A.site_count[pi] = overflow ? A.site_cap : base;
       if (overflow) atomicOr(A.err, 1u);
     }

@@ -69,6 +69,11 @@ struct VArgs {
   uint32_t* sval_sorted;
   int32_t* seg_begin;  // [n]
   int32_t* seg_end;    // [n]
+  const uint32_t* pscratch;  // per-parent tables of k_match (slot space for k_dirty_slots)
+  uint64_t pstride;
+  uint32_t Os;         // words per output-source row
+  uint32_t* outsrc;    // [n][Os] key source of every (remapped) graph output (k_dirty_slots)
+  int slots;           // 1: k_dirty_slots wrote outsrc instead of didx rows
   uint32_t W;          // words per removed-mask row
   uint32_t* rmask;     // [n][W] parent keys (by sorted rank) absent from the candidate: dropped or dirty
   uint64_t* fresh_sorted;  // [n][S][2] the fresh keys in ascending byte order
@@ -264,6 +269,144 @@ __global__ void k_dirty(VArgs A) {
       }
       if (s == P.ins_slot && P.ins_after) emit_new();
     }
+    A.dcount[lc] = j;
+    A.seg_begin[lc] = (int32_t)((uint64_t)lc * A.S);
+    A.seg_end[lc] = (int32_t)((uint64_t)lc * A.S + j);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// k_dirty_slots (parents of <= 256 nodes): the walk of k_dirty in topological-slot space.
+// The dirty set is a slot bitmask in shared memory (a column per thread); a dirty node's fresh
+// index is the popcount of dirty slots before it plus the new nodes emitted before it, so no
+// per-position index rows are written or read back.  Slot tables from k_match turn the
+// topo -> inoff/nin -> refs chain into one load per slot and one per ref.
+// ------------------------------------------------------------------------------------------
+
+constexpr uint32_t kNewRef = 0x80000000u;  // converted ref: a new node (k in bits 8..), not a slot
+
+template <int BT>
+__global__ void __launch_bounds__(BT) k_dirty_slots(VArgs A) {
+  constexpr int W = 8;  // 256 slots
+  __shared__ uint32_t sm_d[W * BT];  // dirty slots
+  __shared__ uint32_t sm_r[W * BT];  // removed parent ranks
+  const Geo& G = A.g;
+  const uint32_t span = (A.n + 31) / 32 * 32;
+  for (uint32_t lc = blockIdx.x * blockDim.x + threadIdx.x; lc < span; lc += gridDim.x * blockDim.x) {
+    const uint32_t c = A.c0 + lc;
+    const bool incomplete = lc >= A.n || (A.res[c].flags & EF_F_INCOMPLETE);
+    const unsigned mask = __ballot_sync(0xffffffffu, !incomplete);
+    if (incomplete) {
+      if (lc < A.n) {
+        A.dcount[lc] = 0;
+        A.seg_begin[lc] = A.seg_end[lc] = (int32_t)((uint64_t)lc * A.S);
+      }
+      continue;
+    }
+    const VPlan P = A.plan[c];
+    Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
+    const uint32_t* ps = A.pscratch + (uint64_t)P.parent * A.pstride;
+    const uint32_t* tslot = ps + 4 * G.cap_nodes + 1 + G.cap_refs;
+    const uint32_t* s_v = tslot + G.cap_nodes;
+    const uint32_t* s_pk = s_v + G.cap_nodes;
+    const uint32_t* rslot = s_pk + G.cap_nodes;
+    const uint32_t* psig = R.sig(G);
+    const uint32_t* paux = R.aux(G);
+    const uint32_t* prefs = R.refs(G);
+    const uint32_t* srank = R.srank(G);
+    const int pn = P.pn;
+    const int nw = (pn + 31) >> 5;
+    uint32_t* dm = sm_d + threadIdx.x;
+    uint32_t* rk = sm_r + threadIdx.x;
+    for (int w = 0; w < nw; ++w) {
+      dm[w * BT] = 0;
+      rk[w * BT] = 0;
+    }
+    Job* jobs = A.jobs + (uint64_t)lc * A.S;
+    uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
+    auto remove = [&](uint32_t v) {
+      const uint32_t k = srank[v];
+      rk[(k >> 5) * BT] |= 1u << (k & 31);
+    };
+    auto dirty_at = [&](uint32_t t) -> bool { return (dm[(t >> 5) * BT] >> (t & 31)) & 1u; };
+    auto popc_below = [&](uint32_t t) -> uint32_t {
+      uint32_t x = 0;
+      for (uint32_t w = 0; w < (t >> 5); ++w) x += __popc(dm[w * BT]);
+      return x + __popc(dm[(t >> 5) * BT] & ((1u << (t & 31)) - 1u));
+    };
+    const int ins = P.ins_slot;
+    auto fidx = [&](uint32_t t) -> uint32_t { return popc_below(t) + ((int)t > ins && ins >= 0 ? P.n_live : 0); };
+    auto fnew = [&](int k) -> uint32_t {
+      const uint32_t base = popc_below((uint32_t)(ins + (P.ins_after ? 1 : 0)));
+      return base + (k == 1 ? (uint32_t)P.live[0] : 0u);
+    };
+    // a ref in parent-position space -> key source
+    auto src_pos = [&](uint32_t ref) -> uint32_t {
+      const uint32_t p = ref >> 8, port = ref & 255u;
+      if ((int)p >= pn) return kFresh | (port << 23) | fnew((int)p - pn);
+      const uint32_t t = tslot[p];
+      return dirty_at(t) ? (kFresh | (port << 23) | fidx(t)) : ((port << 23) | p);
+    };
+    if (P.drop0 >= 0) remove(P.drop0);
+    if (P.drop1 >= 0) remove(P.drop1);
+    // remaps in slot space (sources are always parent edges)
+    uint32_t rf[2] = {0xffffffffu, 0xffffffffu};
+    for (int k = 0; k < P.n_rm; ++k) rf[k] = (tslot[P.rm_from[k] >> 8] << 8) | (P.rm_from[k] & 255u);
+    const int ms = P.mod >= 0 ? (int)tslot[P.mod] : -1;
+    const int ds0 = P.drop0 >= 0 ? (int)tslot[P.drop0] : -1, ds1 = P.drop1 >= 0 ? (int)tslot[P.drop1] : -1;
+    uint32_t j = 0, r = 0;
+    auto emit_new = [&]() {
+      for (int k = 0; k < 2; ++k) {
+        if (!P.live[k]) continue;
+        rs[r] = src_pos(P.new_ref[k]);  // new nodes are exempt from the remap (rules.py:186-188)
+        jobs[j] = Job{P.new_sig[k], P.new_aux[k], r, 1u};
+        r += 1;
+        ++j;
+      }
+    };
+    const int s_lo = (int)__reduce_min_sync(mask, (unsigned)P.first);
+    const int s_hi = (int)__reduce_max_sync(mask, (unsigned)pn);
+    for (int s = s_lo; s < s_hi; ++s) {
+      if (s < P.first || s >= pn) continue;
+      if (s == ds0 || s == ds1) {
+        if (s == ins && !P.ins_after) emit_new();
+        continue;
+      }
+      const uint32_t v = s_v[s], pk = s_pk[s];
+      const uint32_t r0 = pk & 0xffffffu, nr = pk >> 24;
+      bool dirty = s == ms;
+      for (uint32_t k = 0; k < nr; ++k) {
+        const uint32_t rsl = rslot[r0 + k];
+        uint32_t sv;
+        if (rsl == rf[0] || rsl == rf[1]) {  // the owner now consumes another producer (a remap)
+          sv = src_pos(rsl == rf[0] ? P.rm_to[0] : P.rm_to[1]);
+          dirty = true;
+        } else {
+          const uint32_t t = rsl >> 8, port = rsl & 255u;
+          if (dirty_at(t)) {
+            sv = kFresh | (port << 23) | fidx(t);
+            dirty = true;
+          } else {
+            sv = (port << 23) | (prefs[r0 + k] >> 8);
+          }
+        }
+        rs[r + k] = sv;
+      }
+      if (dirty) {
+        jobs[j] = Job{s == ms ? P.mod_sig : psig[v], s == ms ? P.mod_aux : paux[v], r, nr};
+        r += nr;
+        ++j;
+        dm[(s >> 5) * BT] |= 1u << (s & 31);
+        remove(v);
+      }
+      if (s == ins && P.ins_after) emit_new();
+    }
+    // graph outputs (remapped) -> key sources, for the digest
+    const uint32_t* pouts = R.outs(G);
+    uint32_t* os = A.outsrc + (uint64_t)lc * A.Os;
+    for (int o = 0; o < R.h().n_out; ++o) os[o] = src_pos(vremap(P, pouts[o]));
+    uint32_t* grm = A.rmask + (uint64_t)lc * A.W;
+    for (int w = 0; w < nw; ++w) grm[w] = rk[w * BT];
     A.dcount[lc] = j;
     A.seg_begin[lc] = (int32_t)((uint64_t)lc * A.S);
     A.seg_end[lc] = (int32_t)((uint64_t)lc * A.S + j);
@@ -1073,8 +1216,14 @@ __global__ void __launch_bounds__(BT) k_digest_pm(VArgs A) {
           if ((int)gi < n_out) {
             const uint32_t ref = vremap(P, pouts[gi]);
             if (part == 0) {
-              const uint32_t p = ref >> 8, fi = didx[p];
-              const uint64_t* kp = fi ? fresh + 2 * (fi - 1) : pkeys + 2 * p;
+              const uint64_t* kp;
+              if (A.slots) {
+                const uint32_t sv = A.outsrc[(uint64_t)lc * A.Os + gi], idx = sv & 0x7fffffu;
+                kp = (sv & kFresh) ? fresh + 2 * idx : pkeys + 2 * idx;
+              } else {
+                const uint32_t p = ref >> 8, fi = didx[p];
+                kp = fi ? fresh + 2 * (fi - 1) : pkeys + 2 * p;
+              }
               sk.push(kp[0], 8);
               cw1 = kp[1];
               part = 1;

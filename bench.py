@@ -346,6 +346,8 @@ def run_ours(args, world, rank, local):
             n_cand = len(res)
     del staging
     s.L.ef_host_free(pinned)
+    for sl in e2e_slots:
+        s.free(sl)
     e2e_total, e2e_all = sum(e2e_ms), float(e2e_priced)
     if ex is not None:
         e2e_total = -ex.min(-e2e_total)
@@ -389,17 +391,17 @@ def run_ours(args, world, rank, local):
         "gpu_launches": (13 if world == 1 else 17) * args.steps,
         "clocks": clk,
     }
+    cpu_parents = [_to_oracle(fr.decode(sl)) for sl in mine[:8]] if rank == 0 and world == 1 else []
+    fr.close()  # frees the frontier's records (the search below sets its own geometry)
     if rank == 0 and world == 1:
         line["search"] = _search_e2e(ef, zoo, args.no_cpu)
     if rank == 0 and world == 1 and not args.no_cpu:
-        parents = [_to_oracle(fr.decode(sl)) for sl in mine[:8]]
-        cpu = _cpu_sample(parents, db, args.cpu_budget)
+        cpu = _cpu_sample(cpu_parents, db, args.cpu_budget)
         line["cpu_baseline"] = {"value": cpu["value"], "unit": UNIT, "cores": 1, "kind": "port",
                                 "sample": f"{cpu['expanded']} ResNet-50 frontier expansions ({cpu['priced']} "
                                           f"candidates priced) by the oracle restatement, {cpu['seconds']:.1f}s"}
     if rank == 0:
         print(json.dumps(line))
-    fr.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

@@ -949,7 +949,7 @@ int ef_visited_count(ef_ctx* ctx, uint64_t* count) {
 static int ensure_parent_buffers(ef_ctx* ctx, uint32_t n_parents) {
   const Geo& g = ctx->geo;
   if (ctx->site_cap == 0) ctx->site_cap = std::max<uint32_t>(4 * g.cap_nodes, 256);
-  const uint64_t pstride = 8ull * g.cap_nodes + 1 + 2ull * g.cap_refs;
+  const uint64_t pstride = 10ull * g.cap_nodes + 1 + 2ull * g.cap_refs;
   EF_CUDA(ctx->d_parent_addr.reserve(n_parents, ctx->st));
   EF_CUDA(ctx->d_pscratch.reserve(pstride * n_parents, ctx->st));
   EF_CUDA(ctx->d_sites.reserve((uint64_t)ctx->site_cap * n_parents, ctx->st));
@@ -1095,7 +1095,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
     A.parent_addr = ctx->d_parent_addr.p;
     A.n_parents = n_parents;
     A.pscratch = ctx->d_pscratch.p;
-    A.pstride = 8ull * g.cap_nodes + 1 + 2ull * g.cap_refs;
+    A.pstride = 10ull * g.cap_nodes + 1 + 2ull * g.cap_refs;
     for (uint32_t i = 0; i < n_rules; ++i) A.rules[i] = rules[i];
     A.n_rules = (int32_t)n_rules;
     A.sites = ctx->d_sites.p;
@@ -1246,6 +1246,8 @@ static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
   Pv.pa.step_mode = 1;
   Pv.plan = ctx->d_plan.p;
   Pv.parent_addr = ctx->d_parent_addr.p;
+  Pv.pscratch = ctx->d_pscratch.p;
+  Pv.pstride = 10ull * ctx->geo.cap_nodes + 1 + 2ull * ctx->geo.cap_refs;
   Pv.alg8 = ctx->d_alg8.p;
   Pv.S = ctx->step_S;
   const uint32_t gp = std::max<uint32_t>(1, std::min<uint32_t>((total + kPriceThreads - 1) / kPriceThreads, ctx->n_sm * 16));

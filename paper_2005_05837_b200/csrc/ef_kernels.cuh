@@ -207,6 +207,14 @@ __global__ void __launch_bounds__(BT) k_match(StepArgs A) {
       }
       const int n_refs = R.h().n_refs;
       for (int r = threadIdx.x; r < n_refs; r += BT) rslot[r] = (tslot[refs[r] >> 8] << 8) | (refs[r] & 255u);
+      // per-node price rows {row_off, row_n | is_input << 31} (k_price_v reads one word pair per node)
+      uint32_t* p_ro = rslot + G.cap_refs;
+      uint32_t* p_rn = p_ro + G.cap_nodes;
+      for (int v = threadIdx.x; v < n; v += BT) {
+        const uint2 info = T.sig_info[sig[v]];
+        p_ro[v] = info.x;
+        p_rn[v] = info.y;
+      }
     }
     for (int i = threadIdx.x; i < n; i += BT) {
       for (uint32_t r = inoff[i]; r < inoff[i] + nin[i]; ++r) {
@@ -1127,7 +1135,7 @@ __device__ void price_d1(const PriceArgs& A, const View& V, uint8_t* alg, ef_can
   bool missing = false;
   for (int i = 0; i < nmax; ++i) {
     if (i < n && !missing) {
-      const uint2 info = T.sig_info[V.sig(i)];
+      const uint2 info = V.info(i, T);
       if (!(info.y >> 31)) {
         ++ncomp;
         if (info.y == 0) {
@@ -1149,9 +1157,11 @@ __device__ void price_d1(const PriceArgs& A, const View& V, uint8_t* alg, ef_can
   while (__any_sync(mask, running)) {
     bool changed = false;
     if (running) ++sweeps;
+    uint2 info_next = V.info(0, T);
     for (int i = 0; i < nmax; ++i) {
+      const uint2 info = info_next;  // this node's rows were requested one iteration ahead
+      if (i + 1 < n) info_next = V.info(i + 1, T);
       if (!running || i >= n) continue;
-      const uint2 info = T.sig_info[V.sig(i)];
       const uint32_t nr = info.y;  // input rows have bit 31 set: skipped by the test below
       if (nr < 2u || (nr >> 31)) continue;
       const uint32_t ro = info.x;
@@ -1185,7 +1195,7 @@ __device__ void price_d1(const PriceArgs& A, const View& V, uint8_t* alg, ef_can
     return;
   }
   for (int i = 0; i < n; ++i) {
-    const uint2 info = T.sig_info[V.sig(i)];
+    const uint2 info = V.info(i, T);
     if (info.y >> 31) continue;
     alg[i] = (uint8_t)T.row_alg[info.x + alg[i]];
   }
@@ -1201,6 +1211,7 @@ struct RecView {
   const uint32_t* s;
   int n;
   __device__ __forceinline__ uint32_t sig(int i) const { return s[i]; }
+  __device__ __forceinline__ uint2 info(int i, const Tables& T) const { return T.sig_info[s[i]]; }
 };
 
 __global__ void k_price(PriceArgs A) {

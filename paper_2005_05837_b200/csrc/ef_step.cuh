@@ -1386,22 +1386,38 @@ __global__ void k_rec_max(const unsigned long long* rec, uint32_t n, uint32_t* o
 
 struct VirtView {
   const uint32_t* psig;
+  const uint32_t* p_ro;  // the parent's per-node price rows (k_match)
+  const uint32_t* p_rn;
   int32_t drop0, drop1, mod, n_keep;
   uint32_t mod_sig, s_new0, s_new1;
   int n;
+  __device__ __forceinline__ int ppos(int i) const {
+    int pp = i;
+    if (drop0 >= 0 && pp >= drop0) ++pp;
+    if (drop1 >= 0 && pp >= drop1) ++pp;
+    return pp;
+  }
   __device__ __forceinline__ uint32_t sig(int i) const {
     if (i < n_keep) {
-      int pp = i;
-      if (drop0 >= 0 && pp >= drop0) ++pp;
-      if (drop1 >= 0 && pp >= drop1) ++pp;
+      const int pp = ppos(i);
       return pp == mod ? mod_sig : psig[pp];
     }
     return i == n_keep ? s_new0 : s_new1;
+  }
+  __device__ __forceinline__ uint2 info(int i, const Tables& T) const {
+    if (i < n_keep) {
+      const int pp = ppos(i);
+      if (pp != mod) return make_uint2(p_ro[pp], p_rn[pp]);
+      return T.sig_info[mod_sig];
+    }
+    return T.sig_info[i == n_keep ? s_new0 : s_new1];
   }
 };
 
 struct VPriceArgs {
   PriceArgs pa;
+  const uint32_t* pscratch;
+  uint64_t pstride;
   const VPlan* plan;
   const unsigned long long* parent_addr;
   uint8_t* alg8;  // [total][S]: assignment per child node of every priced candidate
@@ -1424,6 +1440,8 @@ __global__ void k_price_v(VPriceArgs A, const uint32_t* plist, const uint32_t* p
     Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
     VirtView V;
     V.psig = R.sig(G);
+    V.p_ro = A.pscratch + (uint64_t)P.parent * A.pstride + 7ull * G.cap_nodes + 1 + 2ull * G.cap_refs;
+    V.p_rn = V.p_ro + G.cap_nodes;
     V.drop0 = P.drop0;
     V.drop1 = P.drop1;
     V.mod = P.mod;

@@ -1254,11 +1254,18 @@ static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
   const uint32_t* pl = ctx->d_plist.p;
   const uint32_t* pn = ctx->d_scalars.p + 7;
   const bool fast = pp->use_inner && pp->d == 1;
-  if (fast && pp->kind == EF_C_ENERGY) k_price_v<EF_C_ENERGY><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
-  else if (fast && pp->kind == EF_C_TIME) k_price_v<EF_C_TIME><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
-  else if (fast && pp->kind == EF_C_LINEAR) k_price_v<EF_C_LINEAR><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
-  else if (fast) k_price_v<EF_C_MIX + 1><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
-  else k_price_v<-1><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
+  const bool sm = ctx->step_S <= 256;  // the sweep's algorithm row in shared memory
+#define EF_PRICE(K)                                                            \
+  do {                                                                         \
+    if (sm) k_price_v<K, 256><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn); \
+    else k_price_v<K, 0><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);      \
+  } while (0)
+  if (fast && pp->kind == EF_C_ENERGY) EF_PRICE(EF_C_ENERGY);
+  else if (fast && pp->kind == EF_C_TIME) EF_PRICE(EF_C_TIME);
+  else if (fast && pp->kind == EF_C_LINEAR) EF_PRICE(EF_C_LINEAR);
+  else if (fast) EF_PRICE(EF_C_MIX + 1);
+  else k_price_v<-1, 0><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
+#undef EF_PRICE
   EF_CUDA(cudaGetLastError());
   cudaEventRecord(ctx->ev[5], ctx->st);
   return EF_OK;

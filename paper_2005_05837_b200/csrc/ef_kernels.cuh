@@ -1122,8 +1122,8 @@ __device__ __forceinline__ double cost_of(const ef_price_params& f, double time_
 // warp-synchronously: every loop runs a warp-uniform trip count (the lanes of `mask` price
 // different candidates whose node counts differ by a few), with no early exits, so the warp
 // never splits into groups that would then run the whole sweep one after another.
-template <int KIND, class View>
-__device__ void price_d1(const PriceArgs& A, const View& V, uint8_t* alg, ef_cand_result& res, unsigned mask) {
+template <int KIND, class View, class Alg>
+__device__ void price_d1(const PriceArgs& A, const View& V, Alg alg, ef_cand_result& res, unsigned mask) {
   const Tables& T = A.T;
   const ef_price_params& F = A.pp;
   const int n = V.n;
@@ -1206,6 +1206,13 @@ __device__ void price_d1(const PriceArgs& A, const View& V, uint8_t* alg, ef_can
   res.sweeps = sweeps;
   res.flags |= EF_F_PRICED;
 }
+
+// a candidate's algorithm row: global bytes, or a shared-memory column (stride = block size)
+struct AlgRow {
+  uint8_t* p;
+  int stride;
+  __device__ __forceinline__ uint8_t& operator[](int i) const { return p[i * stride]; }
+};
 
 struct RecView {
   const uint32_t* s;

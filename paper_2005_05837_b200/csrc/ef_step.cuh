@@ -1425,8 +1425,9 @@ struct VPriceArgs {
 };
 
 // one thread per survivor of the step's dedup (the compacted list); KIND < 0: any cost kind / radius
-template <int KIND>
-__global__ void k_price_v(VPriceArgs A, const uint32_t* plist, const uint32_t* plist_n) {
+template <int KIND, int SM_ROW>
+__global__ void __launch_bounds__(64) k_price_v(VPriceArgs A, const uint32_t* plist, const uint32_t* plist_n) {
+  __shared__ uint8_t sm_alg[SM_ROW ? SM_ROW * 64 : 1];  // the sweep's row, one column per thread
   const Geo& G = A.pa.g;
   const uint32_t total = *plist_n;
   const uint32_t stride = gridDim.x * blockDim.x;
@@ -1451,8 +1452,14 @@ __global__ void k_price_v(VPriceArgs A, const uint32_t* plist, const uint32_t* p
     V.s_new1 = P.new_sig[1];
     V.n = P.n_keep + P.n_live;
     uint8_t* alg = A.alg8 + (uint64_t)c * A.S;
-    if (KIND >= 0) price_d1<KIND>(A.pa, V, alg, res, mask);
-    else price_graph(A.pa, V, alg, res);
+    if (KIND >= 0 && SM_ROW) {
+      price_d1<KIND>(A.pa, V, AlgRow{sm_alg + threadIdx.x, 64}, res, mask);
+      for (int i = 0; i < V.n; ++i) alg[i] = sm_alg[i * 64 + threadIdx.x];
+    } else if (KIND >= 0) {
+      price_d1<KIND>(A.pa, V, AlgRow{alg, 1}, res, mask);
+    } else {
+      price_graph(A.pa, V, alg, res);
+    }
   }
 }
 

@@ -40,6 +40,23 @@ sys.path.insert(0, ROOT)
 
 MODEL = "resnet50"
 CONFIG_NAME = "ResNet-50 inference graph, energy objective with per-node conv-algorithm selection, alpha=1.05"
+# --workload: the other BASELINE.json configs as frontier workloads (name, objective, parents default)
+WORKLOADS = {
+    "resnet50": (CONFIG_NAME, "energy", 4096),
+    "squeezenet": ("SqueezeNet inference graph, energy objective, alpha=1.0 search frontier", "energy", 4096),
+    "inception_v3": ("Inception-v3 graph, energy-delay tradeoff objective (normalized linear w=0.5), alpha=1.05",
+                     "linear0.5", 2048),
+    "nasnet_a": ("NasNet-A style cell-stacked graph, energy objective, large frontier", "energy", 1024),
+    "dag:1000": ("synthetic random-DAG conv/matmul graph, 1k ops, full rule set", "energy", 256),
+    "dag:5000": ("synthetic random-DAG conv/matmul graph, 5k ops, full rule set", "energy", 32),
+    "dag:20000": ("synthetic random-DAG conv/matmul graph, 20k ops, full rule set", "energy", 4),
+}
+
+
+def _objective(ef, kind: str, g0, db):
+    if kind == "energy":
+        return ef.CostFunction.energy()
+    return ef.CostFunction.linear(0.5).with_refs(*ef.normalization_refs(g0, db))
 METRIC = "candidate graphs priced/sec"
 UNIT = "candidates/s"
 RULES = ["fuse-conv-relu", "split-conv-activation", "merge-parallel-convs", "split-merged-conv", "fold-identity",
@@ -117,23 +134,31 @@ def _oracle_db(db):
     return odb
 
 
-def _oracle_expand(parent, odb, visited: set) -> tuple[int, int]:
+def _oracle_expand(parent, odb, visited: set, deadline: float | None = None) -> tuple[int, int]:
     """The reference's per-expansion work on one parent (search.py:245-267): neighbors
     (rewrite + canonical hash + in-expansion dedup), visited dedup, profiling of new
-    signatures and the inner search of every survivor."""
+    signatures and the inner search of every survivor.  Stops at `deadline` (perf_counter)."""
     from oracle import enerflow_oracle as orc
 
     f = orc.CostFn("energy")
     generated = priced = 0
-    for cand in orc.neighbors(parent, RULES):
-        generated += 1
-        h = orc.canonical_hash(cand)
-        if h in visited:
-            continue
-        visited.add(h)
-        orc.ensure_profiled(cand, odb, 0)
-        orc.sweep(cand, odb, f, 1)
-        priced += 1
+    seen: set = set()
+    for rule in RULES:  # neighbors() unrolled so the sample can stop inside a large expansion
+        for site in orc.match(rule, parent):
+            if deadline is not None and time.perf_counter() > deadline:
+                return generated, priced
+            cand = orc.apply(rule, parent, site)
+            h = orc.canonical_hash(cand)
+            if h in seen:
+                continue
+            seen.add(h)
+            generated += 1
+            if h in visited:
+                continue
+            visited.add(h)
+            orc.ensure_profiled(cand, odb, 0)
+            orc.sweep(cand, odb, f, 1)
+            priced += 1
     return generated, priced
 
 
@@ -199,7 +224,7 @@ def _cpu_sample(parents, db, budget_s: float) -> dict:
     priced = expanded = 0
     visited: set = set()
     for p in parents:
-        priced += _oracle_expand(p, odb, visited)[1]
+        priced += _oracle_expand(p, odb, visited, t0 + budget_s)[1]
         expanded += 1
         if time.perf_counter() - t0 > budget_s:
             break
@@ -257,10 +282,15 @@ def run_ours(args, world, rank, local):
         dist.init_process_group("nccl", device_id=dev)
         ex = OwnerExchange(device=dev)
 
-    g0 = zoo.generate(MODEL, 0)
+    workload = args.workload
+    config_name, objective, default_parents = WORKLOADS[workload]
+    parents_per_gpu = args.parents or default_parents
+    g0 = zoo.generate(workload, 0)
     db = ef.CostDatabase()
-    fr = Frontier(g0, db, ef.SyntheticProfiler(0), ef.CostFunction.energy(), ef.SearchConfig(alpha=1.05),
-                  args.parents * world)
+    ef.ensure_profiled(g0, db, ef.SyntheticProfiler(0))
+    fr = Frontier(g0, db, ef.SyntheticProfiler(0), _objective(ef, objective, g0, db),
+                  ef.SearchConfig(alpha=1.0 if workload == "squeezenet" else 1.05), parents_per_gpu * world)
+    args.parents = parents_per_gpu
     # weak scaling: this rank owns its slice of the frontier (graphs are independent objects)
     mine = fr.slots[rank * args.parents:(rank + 1) * args.parents]
     s = fr.s
@@ -370,7 +400,7 @@ def run_ours(args, world, rank, local):
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64+u64",
         "data": "synthetic (random-init float64 weights, synthetic profiler seed 0)",
-        "config": {"workload": CONFIG_NAME, "model": MODEL, "parents_per_gpu": len(mine),
+        "config": {"workload": config_name, "model": workload, "objective": objective, "parents_per_gpu": len(mine),
                    "nodes_per_parent": n_nodes, "candidates_per_step": gen_n / args.steps,
                    "priced_per_step": priced_n / args.steps, "rules": "all 6", "inner_search_d": 1,
                    "l2": "flushed (256 MiB write) before every timed step",
@@ -393,13 +423,14 @@ def run_ours(args, world, rank, local):
     }
     cpu_parents = [_to_oracle(fr.decode(sl)) for sl in mine[:8]] if rank == 0 and world == 1 else []
     fr.close()  # frees the frontier's records (the search below sets its own geometry)
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and workload == MODEL:
         line["search"] = _search_e2e(ef, zoo, args.no_cpu)
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = _cpu_sample(cpu_parents, db, args.cpu_budget)
         line["cpu_baseline"] = {"value": cpu["value"], "unit": UNIT, "cores": 1, "kind": "port",
-                                "sample": f"{cpu['expanded']} ResNet-50 frontier expansions ({cpu['priced']} "
-                                          f"candidates priced) by the oracle restatement, {cpu['seconds']:.1f}s"}
+                                "sample": f"{cpu['expanded']} {workload} frontier expansions (the last may be "
+                                          f"partial; {cpu['priced']} candidates priced) by the oracle restatement, "
+                                          f"{cpu['seconds']:.1f}s"}
     if rank == 0:
         print(json.dumps(line))
     if dist is not None:
@@ -414,7 +445,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--parents", type=int, default=4096, help="frontier graphs per GPU per step")
+    ap.add_argument("--parents", type=int, default=0, help="frontier graphs per GPU per step (0: workload default)")
+    ap.add_argument("--workload", default=MODEL, choices=sorted(WORKLOADS),
+                    help="BASELINE.json config to run as the frontier workload (default: configs[1])")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

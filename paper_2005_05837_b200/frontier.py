@@ -461,6 +461,11 @@ class Frontier:
                     keep.append(i)
                     seen.add(hs[i])
                 best = min(best, cs[i])
+            # only the cheapest `room` of them can be popped into the batch before it is full:
+            # materialise those (keeps large graphs' frontiers within memory)
+            room = n_parents - len(slots)
+            if len(keep) > room:
+                keep = sorted(sorted(keep, key=lambda i: (cs[i], hs[i]))[:room])
             for i, sl in zip(keep, self.s.keep(keep)):
                 heapq.heappush(heap, (cs[i], hs[i], sl))
         # fill the batch with the remaining enqueued graphs in heap order

@@ -1164,8 +1164,9 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       }
       cudaEvent_t* ce = ctx->ev_chunk.data() + 5 * ctx->n_chunks++;
       cudaEventRecord(ce[0], ctx->st);
-      V.slots = S <= 256;
-      if (V.slots) k_dirty_slots<128><<<gd, 128, 0, ctx->st>>>(V);
+      V.slots = S <= 1024;
+      if (S <= 256) k_dirty_slots<128, 8><<<gd, 128, 0, ctx->st>>>(V);
+      else if (S <= 1024) k_dirty_slots<128, 32><<<gd, 128, 0, ctx->st>>>(V);
       else k_dirty<<<gd, 128, 0, ctx->st>>>(V);
       EF_CUDA(cudaGetLastError());
       size_t t1 = ctx->d_sort_tmp.cap;
@@ -1175,12 +1176,19 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       cudaEventRecord(ce[1], ctx->st);
       if ((rc = launch_keys(ctx, V))) return rc;
       cudaEventRecord(ce[2], ctx->st);
-      if (S <= 256) {  // slot-space walk, warp merge into a contiguous key stream, streaming digest
-        const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 32));
-        if (S <= 32) k_merge<1, 4><<<gm, 128, 0, ctx->st>>>(V);
-        else if (S <= 64) k_merge<2, 4><<<gm, 128, 0, ctx->st>>>(V);
-        else if (S <= 128) k_merge<4, 4><<<gm, 128, 0, ctx->st>>>(V);
-        else k_merge<8, 4><<<gm, 128, 0, ctx->st>>>(V);
+      if (S <= 1024) {  // slot-space walk, warp merge into a contiguous key stream, streaming digest
+        uint32_t rows = 32;
+        while (rows < S) rows <<= 1;
+        const int warps = rows <= 256 ? 4 : 2;
+        const size_t smem = (size_t)warps * rows * 32;
+        const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>((V.n + warps - 1) / warps, ctx->n_sm * 32));
+        if (warps == 4) {
+          EF_CUDA(cudaFuncSetAttribute(k_merge<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          k_merge<8, 4><<<gm, 128, smem, ctx->st>>>(V, rows);
+        } else {
+          EF_CUDA(cudaFuncSetAttribute(k_merge<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          k_merge<8, 2><<<gm, 64, smem, ctx->st>>>(V, rows);
+        }
         EF_CUDA(cudaGetLastError());
         cudaEventRecord(ce[3], ctx->st);
         k_digest_pm<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
@@ -1254,17 +1262,22 @@ static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
   const uint32_t* pl = ctx->d_plist.p;
   const uint32_t* pn = ctx->d_scalars.p + 7;
   const bool fast = pp->use_inner && pp->d == 1;
-  const bool sm = ctx->step_S <= 256;  // the sweep's algorithm row in shared memory
-#define EF_PRICE(K)                                                            \
-  do {                                                                         \
-    if (sm) k_price_v<K, 256><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn); \
-    else k_price_v<K, 0><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);      \
+  const bool sm = ctx->step_S <= 1024;  // the sweep's algorithm row in shared memory
+  const size_t smem = sm ? (size_t)ctx->step_S * kPriceThreads : 0;
+#define EF_PRICE(K)                                                                                        \
+  do {                                                                                                     \
+    if (sm) {                                                                                              \
+      EF_CUDA(cudaFuncSetAttribute(k_price_v<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      k_price_v<K, true><<<gp, kPriceThreads, smem, ctx->st>>>(Pv, pl, pn);                             \
+    } else {                                                                                               \
+      k_price_v<K, false><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);                                \
+    }                                                                                                      \
   } while (0)
   if (fast && pp->kind == EF_C_ENERGY) EF_PRICE(EF_C_ENERGY);
   else if (fast && pp->kind == EF_C_TIME) EF_PRICE(EF_C_TIME);
   else if (fast && pp->kind == EF_C_LINEAR) EF_PRICE(EF_C_LINEAR);
   else if (fast) EF_PRICE(EF_C_MIX + 1);
-  else k_price_v<-1, 0><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
+  else k_price_v<-1, false><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
 #undef EF_PRICE
   EF_CUDA(cudaGetLastError());
   cudaEventRecord(ctx->ev[5], ctx->st);

@@ -285,9 +285,8 @@ __global__ void k_dirty(VArgs A) {
 
 constexpr uint32_t kNewRef = 0x80000000u;  // converted ref: a new node (k in bits 8..), not a slot
 
-template <int BT>
-__global__ void __launch_bounds__(BT) k_dirty_slots(VArgs A) {
-  constexpr int W = 8;  // 256 slots
+template <int BT, int W>
+__global__ void __launch_bounds__(BT) k_dirty_slots(VArgs A) {  // parents of <= 32 W - 2 nodes
   __shared__ uint32_t sm_d[W * BT];  // dirty slots
   __shared__ uint32_t sm_r[W * BT];  // removed parent ranks
   const Geo& G = A.g;
@@ -1085,15 +1084,48 @@ __device__ __forceinline__ bool warp_sort_fresh(const uint64_t* fresh, uint32_t 
   return tie;
 }
 
+// smem bitonic sort of the packed values (first 4 key bytes << 32 | job) of one candidate, then
+// its fresh keys in that order into sb; for candidates with more than 256 fresh keys
+__device__ __forceinline__ bool warp_sort_fresh_smem(const uint64_t* fresh, uint32_t d, uint64_t* buf, uint64_t* sb,
+                                                     int lane) {
+  uint32_t m = 2;
+  while (m < d) m <<= 1;
+  for (uint32_t i = lane; i < m; i += 32) buf[i] = i < d ? ((B2b::bswap64(fresh[2 * i]) >> 32) << 32) | i : ~0ULL;
+  __syncwarp();
+  for (uint32_t k = 2; k <= m; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = lane; i < m; i += 32) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t a = buf[i], b = buf[ixj];
+          if ((a > b) == ((i & k) == 0)) {
+            buf[i] = b;
+            buf[ixj] = a;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  bool tie = false;
+  for (uint32_t i = lane; i + 1 < d; i += 32) tie |= (buf[i] >> 32) == (buf[i + 1] >> 32);
+  // gather the keys in order (sb and buf may not alias: buf is the A area, sb the B area)
+  for (uint32_t i = lane; i < d; i += 32) {
+    const uint32_t jx = (uint32_t)buf[i];
+    sb[2 * i] = B2b::bswap64(fresh[2 * jx]);
+    sb[2 * i + 1] = B2b::bswap64(fresh[2 * jx + 1]);
+  }
+  return tie;
+}
+
+// dynamic shared memory: per warp two arrays of `rows` keys (A = parent, B = fresh)
 template <int KMAX, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_merge(VArgs A) {
-  constexpr int M = 32 * KMAX;
-  __shared__ uint64_t sa_all[WARPS * M * 2];  // parent keys (big-endian word pairs)
-  __shared__ uint64_t sb_all[WARPS * M * 2];  // fresh keys in order
+__global__ void __launch_bounds__(WARPS * 32) k_merge(VArgs A, uint32_t rows) {
+  extern __shared__ __align__(16) uint64_t merge_smem[];
   const Geo& G = A.g;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint64_t* sa = sa_all + w * M * 2;
-  uint64_t* sb = sb_all + w * M * 2;
+  uint64_t* sa = merge_smem + (uint64_t)w * rows * 4;
+  uint64_t* sb = sa + rows * 2;
   for (uint32_t lc = blockIdx.x * WARPS + w; lc < A.n; lc += gridDim.x * WARPS) {
     const uint32_t c = A.c0 + lc;
     if (A.res[c].flags & EF_F_INCOMPLETE) continue;
@@ -1101,12 +1133,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge(VArgs A) {
     const int pn = P.pn;
     const uint32_t d = A.dcount[lc];
     const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
-    // 1) the fresh keys sorted in registers, network sized to this candidate (warp-uniform)
+    // 1) the fresh keys sorted, network sized to this candidate (warp-uniform branch)
     bool tie;
     if (d <= 32) tie = warp_sort_fresh<1>(fresh, d, sb, lane);
     else if (d <= 64 || KMAX < 4) tie = warp_sort_fresh<(KMAX < 2 ? KMAX : 2)>(fresh, d, sb, lane);
     else if (d <= 128 || KMAX < 8) tie = warp_sort_fresh<(KMAX < 4 ? KMAX : 4)>(fresh, d, sb, lane);
-    else tie = warp_sort_fresh<KMAX>(fresh, d, sb, lane);
+    else if (d <= 32u * KMAX) tie = warp_sort_fresh<KMAX>(fresh, d, sb, lane);
+    else tie = warp_sort_fresh_smem(fresh, d, sa, sb, lane);
     __syncwarp();
     if (__any_sync(0xffffffffu, tie)) {  // p ~ d^2 / 2^33: insertion sort of the whole list by full key
       if (lane == 0) {
@@ -1425,9 +1458,9 @@ struct VPriceArgs {
 };
 
 // one thread per survivor of the step's dedup (the compacted list); KIND < 0: any cost kind / radius
-template <int KIND, int SM_ROW>
+template <int KIND, bool SM_ROW>
 __global__ void __launch_bounds__(64) k_price_v(VPriceArgs A, const uint32_t* plist, const uint32_t* plist_n) {
-  __shared__ uint8_t sm_alg[SM_ROW ? SM_ROW * 64 : 1];  // the sweep's row, one column per thread
+  extern __shared__ uint8_t sm_alg[];  // SM_ROW: the sweep's row, one column per thread (S x 64 bytes)
   const Geo& G = A.pa.g;
   const uint32_t total = *plist_n;
   const uint32_t stride = gridDim.x * blockDim.x;

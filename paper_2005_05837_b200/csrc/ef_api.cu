@@ -21,6 +21,7 @@ constexpr int kMatchThreads = 256;
 constexpr int kMatThreads = 256;
 constexpr int kHashThreads = 128;
 constexpr int kPriceThreads = 64;
+constexpr uint32_t kFastRows = 256;  // rows (max parent nodes + 2) served by the fast step kernels
 
 template <typename T>
 struct DevBuf {
@@ -1164,9 +1165,11 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       }
       cudaEvent_t* ce = ctx->ev_chunk.data() + 5 * ctx->n_chunks++;
       cudaEventRecord(ce[0], ctx->st);
-      V.slots = S <= 1024;
-      if (S <= 256) k_dirty_slots<128, 8><<<gd, 128, 0, ctx->st>>>(V);
-      else if (S <= 1024) k_dirty_slots<128, 32><<<gd, 128, 0, ctx->st>>>(V);
+      // rows <= kFastRows: slot walk, warp merge, streaming digest (the 32-word slot walk and
+      // the shared-memory merge also handle rows <= 1024, but measured slower than the general
+      // kernels there: NasNet-A 15.1 vs 13.8 ms per 1024-parent step)
+      V.slots = S <= kFastRows;
+      if (V.slots) k_dirty_slots<128, 8><<<gd, 128, 0, ctx->st>>>(V);
       else k_dirty<<<gd, 128, 0, ctx->st>>>(V);
       EF_CUDA(cudaGetLastError());
       size_t t1 = ctx->d_sort_tmp.cap;
@@ -1176,7 +1179,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       cudaEventRecord(ce[1], ctx->st);
       if ((rc = launch_keys(ctx, V))) return rc;
       cudaEventRecord(ce[2], ctx->st);
-      if (S <= 1024) {  // slot-space walk, warp merge into a contiguous key stream, streaming digest
+      if (S <= kFastRows) {  // slot-space walk, warp merge into a contiguous key stream, streaming digest
         uint32_t rows = 32;
         while (rows < S) rows <<= 1;
         const int warps = rows <= 256 ? 4 : 2;
@@ -1262,7 +1265,7 @@ static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
   const uint32_t* pl = ctx->d_plist.p;
   const uint32_t* pn = ctx->d_scalars.p + 7;
   const bool fast = pp->use_inner && pp->d == 1;
-  const bool sm = ctx->step_S <= 1024;  // the sweep's algorithm row in shared memory
+  const bool sm = ctx->step_S <= kFastRows;  // the sweep's algorithm row in shared memory
   const size_t smem = sm ? (size_t)ctx->step_S * kPriceThreads : 0;
 #define EF_PRICE(K)                                                                                        \
   do {                                                                                                     \

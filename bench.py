@@ -357,8 +357,9 @@ def run_ours(args, world, rank, local):
     pinned = s.L.ef_host_alloc(blob.nbytes)
     staging = np.ctypeslib.as_array((C.c_uint8 * blob.nbytes).from_address(pinned))
     staging[:] = blob.view(np.uint8)
+    # (a) serial: upload + hash, then the step, then the results, one step at a time
     e2e_slots = [s.alloc() for _ in mine]
-    e2e_ms, e2e_priced, n_cand, up_ms = [], 0, 0, 0.0
+    ser_ms, up_ms = [], 0.0
     evm = torch.cuda.Event(enable_timing=True)
     for i in range(args.warmup + args.steps):
         flush_l2()
@@ -370,18 +371,41 @@ def run_ours(args, world, rank, local):
         ev1.record()
         ev1.synchronize()
         if i >= args.warmup:
-            e2e_ms.append(ev0.elapsed_time(ev1))
+            ser_ms.append(ev0.elapsed_time(ev1))
             up_ms += ev0.elapsed_time(evm)
-            e2e_priced += int(np.count_nonzero(res["flags"] & N.F_PRICED))
+    # (b) pipelined (the headline): the next batch's upload + hash run on the upload stream
+    # while this batch's step runs; every batch's H2D and results D2H are inside the region
+    sets = [e2e_slots, [s.alloc() for _ in mine]]
+    e2e_total = 0.0
+    e2e_priced = n_cand = 0
+    for rep in range(2):  # rep 0 warms up
+        barrier()
+        ev0.record()
+        s.write_packed(sets[0], staging.view(np.uint32), offs, asynchronous=True)
+        s.upload_fence()
+        priced_rep = 0
+        for i in range(args.steps):
+            if i + 1 < args.steps:
+                s.write_packed(sets[(i + 1) % 2], staging.view(np.uint32), offs, asynchronous=True)
+            res, _ = step(sets[i % 2])
+            s.upload_fence()
+            priced_rep += int(np.count_nonzero(res["flags"] & N.F_PRICED))
             n_cand = len(res)
+        ev1.record()
+        ev1.synchronize()
+        if rep == 1:
+            e2e_total, e2e_priced = ev0.elapsed_time(ev1), priced_rep
     del staging
     s.L.ef_host_free(pinned)
-    for sl in e2e_slots:
+    for sl in sets[0] + sets[1]:
         s.free(sl)
-    e2e_total, e2e_all = sum(e2e_ms), float(e2e_priced)
+    e2e_all = float(e2e_priced)
+    ser_total, ser_priced = sum(ser_ms), float(priced_n)
     if ex is not None:
         e2e_total = -ex.min(-e2e_total)
         e2e_all = ex.sum(e2e_all)
+        ser_total = -ex.min(-ser_total)
+        ser_priced = ex.sum(ser_priced)
     e2e_value = e2e_all / (e2e_total / 1e3)
 
     # rooflines of the dominant kernel (k_keys), from the live per-stage CUDA-event times
@@ -416,8 +440,10 @@ def run_ours(args, world, rank, local):
                          "peak": hbm_peak, "unit": "GB/s", "frac": keys_bytes / (keys_ms / 1e3) / 1e9 / hbm_peak,
                          "peak_source": hbm_src, "traffic": None},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(blob.nbytes),
-                "d2h_bytes_per_step": n_cand * N.CAND_DTYPE.itemsize,
-                "ms_per_step": sum(e2e_ms) / len(e2e_ms), "upload_hash_ms_per_step": up_ms / args.steps},
+                "d2h_bytes_per_step": n_cand * N.CAND_DTYPE.itemsize, "ms_per_step": e2e_total / args.steps,
+                "mode": "pipelined: batch i+1 uploaded and hashed on the upload stream during step i",
+                "serial_value": ser_priced / (ser_total / 1e3), "serial_ms_per_step": ser_total / args.steps,
+                "serial_upload_hash_ms_per_step": up_ms / args.steps},
         "gpu_launches": (13 if world == 1 else 17) * args.steps,
         "clocks": clk,
     }

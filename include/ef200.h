@@ -234,6 +234,14 @@ int ef_last_stats(ef_ctx* ctx, uint64_t* out, uint32_t n);
  * (uint32); the device unpacks it into slots[i] and computes keys / sorted order / ranks */
 int ef_records_write_packed(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const void* host, const uint64_t* offsets,
                             uint64_t bytes);
+/* the same on the context's upload stream, returning at once, so the copy, unpacking and
+ * hashing overlap a step (pipelining frontier batches).  It starts after the main-stream work
+ * queued before it; a step reads the uploaded records only after ef_upload_fence.  `host`
+ * must be page-locked (ef_host_alloc) and stay unchanged until the upload is fenced. */
+int ef_records_write_packed_async(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const void* host,
+                                  const uint64_t* offsets, uint64_t bytes);
+/* main-stream work queued after this call waits for every asynchronous upload issued before it */
+int ef_upload_fence(ef_ctx* ctx);
 /* measured BLAKE2b compression rate of this GPU (register-only loop): the ALU roofline */
 int ef_b2b_peak(ef_ctx* ctx, double* compress_per_s);
 

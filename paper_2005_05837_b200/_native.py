@@ -108,6 +108,8 @@ _PROTOS = {
     "ef_last_timing": (C.c_int, [_P, C.POINTER(C.c_float), C.c_uint32]),
     "ef_last_stats": (C.c_int, [_P, _U64P, C.c_uint32]),
     "ef_records_write_packed": (C.c_int, [_P, _U32P, C.c_uint32, C.c_void_p, _U64P, C.c_uint64]),
+    "ef_records_write_packed_async": (C.c_int, [_P, _U32P, C.c_uint32, C.c_void_p, _U64P, C.c_uint64]),
+    "ef_upload_fence": (C.c_int, [_P]),
     "ef_b2b_peak": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "ef_expand_hashes": (C.c_int, [_P, _U32P, C.c_uint32, _I32P, C.c_uint32, _U32P]),
     "ef_route_owners": (C.c_int, [_P, C.c_uint32, C.c_uint64, C.c_void_p, _U32P]),

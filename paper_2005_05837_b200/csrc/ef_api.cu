@@ -60,6 +60,23 @@ struct WeightSet {
   bool ready = false;  // tensors present + digest computed
 };
 
+// per-chunk hashing scratch (ef_step.cuh): one set for steps / keeps on the main stream, one
+// for asynchronous uploads on the upload stream
+struct Scratch {
+  DevBuf<uint32_t> didx, jv, refsrc, dcount, dsorted, dorder, sval, sval2, rmask, iota, outsrc;
+  DevBuf<Job> jobs;
+  DevBuf<uint64_t> fresh, fresh2, skey, skey2;
+  DevBuf<int32_t> seg_b, seg_e;
+  DevBuf<uint8_t> sort_tmp, seg_tmp;
+  DevBuf<uint32_t> recmax;
+  void release() {
+    didx.release(); jv.release(); refsrc.release(); dcount.release(); dsorted.release(); dorder.release();
+    sval.release(); sval2.release(); rmask.release(); iota.release(); outsrc.release(); jobs.release();
+    fresh.release(); fresh2.release(); skey.release(); skey2.release(); seg_b.release(); seg_e.release();
+    sort_tmp.release(); seg_tmp.release(); recmax.release();
+  }
+};
+
 }  // namespace
 
 struct ef_ctx {
@@ -104,8 +121,8 @@ struct ef_ctx {
   DevBuf<uint32_t> d_pscratch, d_site_count, d_cand_off, d_step_seq, d_scalars;
   DevBuf<char> d_cand, d_stage;
   DevBuf<int32_t> d_srcpos, d_req_dv;
-  DevBuf<uint8_t> d_seed, d_pmark, d_sort_tmp;
-  DevBuf<uint32_t> d_first, d_first_sorted, d_iota, d_order;
+  DevBuf<uint8_t> d_seed, d_pmark;
+  DevBuf<uint32_t> d_first, d_first_sorted, d_order;
   DevBuf<ef_cand_result> d_res, d_res_aux;
   DevBuf<ef_sig_desc> d_req_sig;
   DevBuf<uint64_t> d_hash_out;
@@ -118,17 +135,19 @@ struct ef_ctx {
 
   // virtual-candidate step (ef_step.cuh)
   DevBuf<VPlan> d_plan;
-  DevBuf<uint32_t> d_route, d_perm, d_jv, d_recmax, d_outsrc;
+  DevBuf<uint32_t> d_route, d_perm;
   DevBuf<unsigned long long> d_stats;
   DevBuf<unsigned long long> d_step_ord;
   uint32_t n_send = 0;
   DevBuf<uint32_t> d_plist, d_sig_info;
-  DevBuf<uint8_t> d_alg8, d_seg_tmp;
-  DevBuf<uint32_t> d_didx, d_refsrc, d_dcount, d_dorder, d_dsorted, d_sval, d_sval2;
-  DevBuf<Job> d_jobs;
-  DevBuf<uint64_t> d_fresh, d_fresh2, d_skey, d_skey2;
-  DevBuf<uint32_t> d_rmask;
-  DevBuf<int32_t> d_seg_b, d_seg_e;
+  DevBuf<uint8_t> d_alg8;
+  Scratch sc[2];
+  cudaStream_t st_up = nullptr;  // asynchronous uploads
+  cudaEvent_t ev_up = nullptr;    // end of the last asynchronous upload (upload stream)
+  cudaEvent_t ev_main = nullptr;  // main-stream work an upload must not overtake
+  DevBuf<char> d_up_stage;
+  DevBuf<unsigned long long> d_up_off, d_up_dst;
+  std::vector<unsigned long long> h_up_off, h_up_dst;
   uint32_t step_S = 0, step_Rs = 0, step_n_parents = 0;
   StepArgs last_step{};
   DevBuf<uint32_t> d_sel;
@@ -209,6 +228,9 @@ ef_ctx* ef_create(int device) {
   }
   cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, device);
   cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
+  cudaStreamCreateWithFlags(&ctx->st_up, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&ctx->ev_up, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ctx->ev_main, cudaEventDisableTiming);
   for (auto& e : ctx->ev) cudaEventCreate(&e);
   // weight set 0 = "no weights" (digest of the empty message)
   ctx->ws.emplace_back();
@@ -258,10 +280,8 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_req_dv.release();
   ctx->d_seed.release();
   ctx->d_pmark.release();
-  ctx->d_sort_tmp.release();
   ctx->d_first.release();
   ctx->d_first_sorted.release();
-  ctx->d_iota.release();
   ctx->d_order.release();
   ctx->d_res.release();
   ctx->d_res_aux.release();
@@ -272,31 +292,20 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_vis_count.release();
   ctx->d_plan.release();
   ctx->d_route.release();
-  ctx->d_jv.release();
-  ctx->d_outsrc.release();
-  ctx->d_recmax.release();
   ctx->d_stats.release();
   ctx->d_perm.release();
   ctx->d_step_ord.release();
   ctx->d_plist.release();
   ctx->d_sig_info.release();
   ctx->d_alg8.release();
-  ctx->d_seg_tmp.release();
-  ctx->d_didx.release();
-  ctx->d_refsrc.release();
-  ctx->d_dcount.release();
-  ctx->d_dorder.release();
-  ctx->d_dsorted.release();
-  ctx->d_sval.release();
-  ctx->d_sval2.release();
-  ctx->d_jobs.release();
-  ctx->d_fresh.release();
-  ctx->d_fresh2.release();
-  ctx->d_rmask.release();
-  ctx->d_skey.release();
-  ctx->d_skey2.release();
-  ctx->d_seg_b.release();
-  ctx->d_seg_e.release();
+  ctx->sc[0].release();
+  ctx->sc[1].release();
+  ctx->d_up_stage.release();
+  ctx->d_up_off.release();
+  ctx->d_up_dst.release();
+  if (ctx->ev_up) cudaEventDestroy(ctx->ev_up);
+  if (ctx->ev_main) cudaEventDestroy(ctx->ev_main);
+  if (ctx->st_up) cudaStreamDestroy(ctx->st_up);
   ctx->d_sel.release();
   ctx->d_dst.release();
   for (auto& e : ctx->ev) cudaEventDestroy(e);
@@ -778,40 +787,45 @@ int ef_record_read(ef_ctx* ctx, uint32_t slot, void* host, uint64_t bytes) {
 
 // Node keys, sorted order, sorted keys, ranks and graph hash of whole records (uploads and
 // kept candidates): the step's job pipeline with every node a job (ef_step.cuh, full mode).
-static int sort_fresh_keys(ef_ctx* ctx, const VArgs& V);
+static int sort_fresh_keys(ef_ctx* ctx, Scratch& sc, cudaStream_t st, const VArgs& V);
 static uint32_t bits_for(uint32_t v);
 
 // node keys: a thread per candidate when the chunk fills the GPU, four lanes per candidate
 // (lower latency per compression) when it does not
-static int launch_keys(ef_ctx* ctx, const VArgs& V) {
+static int launch_keys(ef_ctx* ctx, cudaStream_t st, const VArgs& V) {
   if (V.n < 20000u) {
     const uint32_t gq = std::max<uint32_t>(1, (V.n + 31) / 32);
-    k_keys_quad<128><<<gq, 128, 0, ctx->st>>>(V);
+    k_keys_quad<128><<<gq, 128, 0, st>>>(V);
   } else {
     const uint32_t gd = std::max<uint32_t>(1, std::min<uint32_t>((V.n + kHashThreads - 1) / kHashThreads, ctx->n_sm * 16));
-    k_keys<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+    k_keys<kHashThreads><<<gd, kHashThreads, 0, st>>>(V);
   }
   EF_CUDA(cudaGetLastError());
   return EF_OK;
 }
-static int ensure_chunk(ef_ctx* ctx, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk);
-static VArgs chunk_args(ef_ctx* ctx, uint32_t S, uint32_t Rs);
-static int hash_records_full(ef_ctx* ctx, const unsigned long long* d_rec, uint32_t n, uint64_t* d_hash_out) {
+static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk);
+static VArgs chunk_args(ef_ctx* ctx, Scratch& sc, uint32_t S, uint32_t Rs);
+static int hash_records_full(ef_ctx* ctx, Scratch& sc, cudaStream_t st, const unsigned long long* d_rec, uint32_t n,
+                             uint64_t* d_hash_out, uint32_t max_n = 0, uint32_t max_refs = 0) {
   if (!n) return EF_OK;
-  EF_CUDA(ctx->d_recmax.reserve(2, ctx->st));
-  EF_CUDA(cudaMemsetAsync(ctx->d_recmax.p, 0, 8, ctx->st));
-  k_rec_max<<<std::max<uint32_t>(1, std::min<uint32_t>((n + 255) / 256, ctx->n_sm)), 256, 0, ctx->st>>>(d_rec, n,
-                                                                                                      ctx->d_recmax.p);
-  EF_CUDA(cudaGetLastError());
-  uint32_t mx[2] = {0, 0};
-  EF_CUDA(cudaMemcpyAsync(mx, ctx->d_recmax.p, 8, cudaMemcpyDeviceToHost, ctx->st));
-  EF_CUDA(cudaStreamSynchronize(ctx->st));
-  const uint32_t S = (std::max<uint32_t>(mx[0], 1) + 2 + 3) & ~3u;
-  const uint32_t Rs = mx[1] + 4;
+  if (!max_n) {  // sizes unknown on the host: read them from the records
+    EF_CUDA(sc.recmax.reserve(2, st));
+    EF_CUDA(cudaMemsetAsync(sc.recmax.p, 0, 8, st));
+    k_rec_max<<<std::max<uint32_t>(1, std::min<uint32_t>((n + 255) / 256, ctx->n_sm)), 256, 0, st>>>(d_rec, n,
+                                                                                                   sc.recmax.p);
+    EF_CUDA(cudaGetLastError());
+    uint32_t mx[2] = {0, 0};
+    EF_CUDA(cudaMemcpyAsync(mx, sc.recmax.p, 8, cudaMemcpyDeviceToHost, st));
+    EF_CUDA(cudaStreamSynchronize(st));
+    max_n = mx[0];
+    max_refs = mx[1];
+  }
+  const uint32_t S = (std::max<uint32_t>(max_n, 1) + 2 + 3) & ~3u;
+  const uint32_t Rs = max_refs + 4;
   uint32_t chunk = 0;
-  int rc = ensure_chunk(ctx, n, S, Rs, &chunk);
+  int rc = ensure_chunk(ctx, sc, st, n, S, Rs, &chunk);
   if (rc) return rc;
-  VArgs V = chunk_args(ctx, S, Rs);
+  VArgs V = chunk_args(ctx, sc, S, Rs);
   V.parent_addr = d_rec;
   V.full = 1;
   V.hash_out = d_hash_out;
@@ -819,16 +833,15 @@ static int hash_records_full(ef_ctx* ctx, const unsigned long long* d_rec, uint3
     V.c0 = c0;
     V.n = std::min(chunk, n - c0);
     const uint32_t gd = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 127) / 128, ctx->n_sm * 16));
-    k_full_jobs<256><<<std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * 8)), 256, 0, ctx->st>>>(V);
+    k_full_jobs<256><<<std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * 8)), 256, 0, st>>>(V);
     EF_CUDA(cudaGetLastError());
-    size_t t1 = ctx->d_sort_tmp.cap;
-    EF_CUDA(cub::DeviceRadixSort::SortPairsDescending(ctx->d_sort_tmp.p, t1, ctx->d_dcount.p, ctx->d_dsorted.p,
-                                                      ctx->d_iota.p, ctx->d_dorder.p, (int)V.n, 0, bits_for(S),
-                                                      ctx->st));
-    if ((rc = launch_keys(ctx, V))) return rc;
-    if ((rc = sort_fresh_keys(ctx, V))) return rc;
-    k_digest<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
-    k_full_store<<<std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * 8)), 128, 0, ctx->st>>>(V);
+    size_t t1 = sc.sort_tmp.cap;
+    EF_CUDA(cub::DeviceRadixSort::SortPairsDescending(sc.sort_tmp.p, t1, sc.dcount.p, sc.dsorted.p, sc.iota.p,
+                                                      sc.dorder.p, (int)V.n, 0, bits_for(S), st));
+    if ((rc = launch_keys(ctx, st, V))) return rc;
+    if ((rc = sort_fresh_keys(ctx, sc, st, V))) return rc;
+    k_digest<kHashThreads><<<gd, kHashThreads, 0, st>>>(V);
+    k_full_store<<<std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * 8)), 128, 0, st>>>(V);
     EF_CUDA(cudaGetLastError());
   }
   return EF_OK;
@@ -882,7 +895,7 @@ int ef_hash_records(ef_ctx* ctx, const uint32_t* slots, uint32_t n, uint64_t* ha
   int rc = stage_addrs(ctx, ctx->d_addr_a, slots, n);
   if (rc) return rc;
   EF_CUDA(ctx->d_hash_out.reserve(n, ctx->st));
-  if ((rc = hash_records_full(ctx, ctx->d_addr_a.p, n, ctx->d_hash_out.p))) return rc;
+  if ((rc = hash_records_full(ctx, ctx->sc[0], ctx->st, ctx->d_addr_a.p, n, ctx->d_hash_out.p))) return rc;
   EF_CUDA(cudaMemcpyAsync(hashes, ctx->d_hash_out.p, n * 8, cudaMemcpyDeviceToHost, ctx->st));
   EF_CUDA(cudaStreamSynchronize(ctx->st));
   return EF_OK;
@@ -976,34 +989,34 @@ static int ensure_step_cand(ef_ctx* ctx, uint32_t total, uint32_t S) {
 
 // per-chunk hashing scratch for rows of S node slots and Rs ref slots: bounded (<= 6 GiB of
 // the 180 GB) so graphs of any size stream through
-static int ensure_chunk(ef_ctx* ctx, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk) {
+static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk) {
   const uint64_t per = (uint64_t)S * (4 + 4 + sizeof(Job) + 16 + 16 + 8 + 8 + 4 + 4) + 4ull * Rs + 4ull * (S + 31) / 32 + 32;
   uint64_t ch = std::max<uint64_t>(256, (6144ull << 20) / per);
   ch = std::min<uint64_t>(ch, std::max<uint32_t>(items, 1));
   ch = std::min<uint64_t>(ch, (uint64_t)INT32_MAX / S);
   *chunk = (uint32_t)ch;
-  EF_CUDA(ctx->d_didx.reserve(ch * S, ctx->st));
-  EF_CUDA(ctx->d_jv.reserve(ch * S, ctx->st));
-  EF_CUDA(ctx->d_jobs.reserve(ch * S, ctx->st));
-  EF_CUDA(ctx->d_refsrc.reserve(ch * Rs, ctx->st));
-  EF_CUDA(ctx->d_fresh.reserve(2 * ch * S, ctx->st));
-  EF_CUDA(ctx->d_fresh2.reserve(2 * ch * S, ctx->st));
-  EF_CUDA(ctx->d_rmask.reserve(ch * ((S + 31) / 32), ctx->st));
-  EF_CUDA(ctx->d_skey.reserve(ch * S, ctx->st));
-  EF_CUDA(ctx->d_skey2.reserve(ch * S, ctx->st));
-  EF_CUDA(ctx->d_sval.reserve(ch * S, ctx->st));
-  EF_CUDA(ctx->d_sval2.reserve(ch * S, ctx->st));
-  EF_CUDA(ctx->d_dcount.reserve(ch, ctx->st));
-  EF_CUDA(ctx->d_dsorted.reserve(ch, ctx->st));
-  EF_CUDA(ctx->d_dorder.reserve(ch, ctx->st));
-  EF_CUDA(ctx->d_seg_b.reserve(ch, ctx->st));
-  EF_CUDA(ctx->d_seg_e.reserve(ch, ctx->st));
-  if (ctx->d_iota.cap < ch) {
-    EF_CUDA(ctx->d_iota.reserve(ch, ctx->st));
-    std::vector<uint32_t> io(ctx->d_iota.cap);
+  EF_CUDA(sc.didx.reserve(ch * S, st));
+  EF_CUDA(sc.jv.reserve(ch * S, st));
+  EF_CUDA(sc.jobs.reserve(ch * S, st));
+  EF_CUDA(sc.refsrc.reserve(ch * Rs, st));
+  EF_CUDA(sc.fresh.reserve(2 * ch * S, st));
+  EF_CUDA(sc.fresh2.reserve(2 * ch * S, st));
+  EF_CUDA(sc.rmask.reserve(ch * ((S + 31) / 32), st));
+  EF_CUDA(sc.skey.reserve(ch * S, st));
+  EF_CUDA(sc.skey2.reserve(ch * S, st));
+  EF_CUDA(sc.sval.reserve(ch * S, st));
+  EF_CUDA(sc.sval2.reserve(ch * S, st));
+  EF_CUDA(sc.dcount.reserve(ch, st));
+  EF_CUDA(sc.dsorted.reserve(ch, st));
+  EF_CUDA(sc.dorder.reserve(ch, st));
+  EF_CUDA(sc.seg_b.reserve(ch, st));
+  EF_CUDA(sc.seg_e.reserve(ch, st));
+  if (sc.iota.cap < ch) {
+    EF_CUDA(sc.iota.reserve(ch, st));
+    std::vector<uint32_t> io(sc.iota.cap);
     for (size_t i = 0; i < io.size(); ++i) io[i] = (uint32_t)i;
-    EF_CUDA(cudaMemcpyAsync(ctx->d_iota.p, io.data(), io.size() * 4, cudaMemcpyHostToDevice, ctx->st));
-    EF_CUDA(cudaStreamSynchronize(ctx->st));
+    EF_CUDA(cudaMemcpyAsync(sc.iota.p, io.data(), io.size() * 4, cudaMemcpyHostToDevice, st));
+    EF_CUDA(cudaStreamSynchronize(st));
   }
   size_t t1 = 0, t2 = 0;
   cub::DeviceRadixSort::SortPairsDescending(nullptr, t1, (const uint32_t*)nullptr, (uint32_t*)nullptr,
@@ -1011,12 +1024,12 @@ static int ensure_chunk(ef_ctx* ctx, uint32_t items, uint32_t S, uint32_t Rs, ui
   cub::DeviceSegmentedSort::SortPairs(nullptr, t2, (const uint64_t*)nullptr, (uint64_t*)nullptr,
                                       (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)(ch * S), (int)ch,
                                       (const int32_t*)nullptr, (const int32_t*)nullptr);
-  EF_CUDA(ctx->d_sort_tmp.reserve(t1, ctx->st));
-  EF_CUDA(ctx->d_seg_tmp.reserve(t2, ctx->st));
+  EF_CUDA(sc.sort_tmp.reserve(t1, st));
+  EF_CUDA(sc.seg_tmp.reserve(t2, st));
   return EF_OK;
 }
 
-static VArgs chunk_args(ef_ctx* ctx, uint32_t S, uint32_t Rs) {
+static VArgs chunk_args(ef_ctx* ctx, Scratch& sc, uint32_t S, uint32_t Rs) {
   VArgs V{};
   V.g = ctx->geo;
   V.T = make_tables(ctx);
@@ -1024,47 +1037,47 @@ static VArgs chunk_args(ef_ctx* ctx, uint32_t S, uint32_t Rs) {
   V.res = ctx->d_res.p;
   V.S = S;
   V.Rs = Rs;
-  V.didx = ctx->d_didx.p;
-  V.jobs = ctx->d_jobs.p;
-  V.refsrc = ctx->d_refsrc.p;
-  V.fresh = ctx->d_fresh.p;
-  V.dcount = ctx->d_dcount.p;
-  V.order = ctx->d_dorder.p;
-  V.skey = ctx->d_skey.p;
-  V.sval = ctx->d_sval.p;
-  V.skey_sorted = ctx->d_skey2.p;
-  V.sval_sorted = ctx->d_sval2.p;
-  V.seg_begin = ctx->d_seg_b.p;
-  V.seg_end = ctx->d_seg_e.p;
+  V.didx = sc.didx.p;
+  V.jobs = sc.jobs.p;
+  V.refsrc = sc.refsrc.p;
+  V.fresh = sc.fresh.p;
+  V.dcount = sc.dcount.p;
+  V.order = sc.dorder.p;
+  V.skey = sc.skey.p;
+  V.sval = sc.sval.p;
+  V.skey_sorted = sc.skey2.p;
+  V.sval_sorted = sc.sval2.p;
+  V.seg_begin = sc.seg_b.p;
+  V.seg_end = sc.seg_e.p;
   V.W = (S + 31) / 32;
-  V.rmask = ctx->d_rmask.p;
-  V.fresh_sorted = ctx->d_fresh2.p;
+  V.rmask = sc.rmask.p;
+  V.fresh_sorted = sc.fresh2.p;
   V.input_words = reinterpret_cast<const uint64_t*>(ctx->d_input_text.p);
   V.err = ctx->d_scalars.p + 1;
   V.one = 1;
-  V.jv = ctx->d_jv.p;
+  V.jv = sc.jv.p;
   return V;
 }
 
 // every candidate's fresh keys in ascending order: warp bitonic sort in shared memory for
 // rows up to 1024 keys, cub's segmented sort (plus the tie fix) beyond
-static int sort_fresh_keys(ef_ctx* ctx, const VArgs& V) {
+static int sort_fresh_keys(ef_ctx* ctx, Scratch& sc, cudaStream_t st, const VArgs& V) {
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 7) / 8, ctx->n_sm * 32));
   if (V.S <= 128) {
-    k_sortkeys<128, 8><<<grid, 256, 0, ctx->st>>>(V);
+    k_sortkeys<128, 8><<<grid, 256, 0, st>>>(V);
   } else if (V.S <= 256) {
-    k_sortkeys<256, 8><<<grid, 256, 0, ctx->st>>>(V);
+    k_sortkeys<256, 8><<<grid, 256, 0, st>>>(V);
   } else if (V.S <= 512) {
-    k_sortkeys<512, 8><<<grid, 256, 0, ctx->st>>>(V);
+    k_sortkeys<512, 8><<<grid, 256, 0, st>>>(V);
   } else if (V.S <= 1024) {
-    k_sortkeys<1024, 4><<<std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 32)), 128, 0, ctx->st>>>(V);
+    k_sortkeys<1024, 4><<<std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 32)), 128, 0, st>>>(V);
   } else {
-    size_t t2 = ctx->d_seg_tmp.cap;
-    EF_CUDA(cub::DeviceSegmentedSort::SortPairs(ctx->d_seg_tmp.p, t2, ctx->d_skey.p, ctx->d_skey2.p, ctx->d_sval.p,
-                                                ctx->d_sval2.p, (int)((uint64_t)V.n * V.S), (int)V.n, ctx->d_seg_b.p,
-                                                ctx->d_seg_e.p, ctx->st));
+    size_t t2 = sc.seg_tmp.cap;
+    EF_CUDA(cub::DeviceSegmentedSort::SortPairs(sc.seg_tmp.p, t2, sc.skey.p, sc.skey2.p, sc.sval.p,
+                                                sc.sval2.p, (int)((uint64_t)V.n * V.S), (int)V.n, sc.seg_b.p,
+                                                sc.seg_e.p, st));
     const uint32_t gd = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 127) / 128, ctx->n_sm * 16));
-    k_sortfix<<<gd, 128, 0, ctx->st>>>(V);
+    k_sortfix<<<gd, 128, 0, st>>>(V);
   }
   EF_CUDA(cudaGetLastError());
   return EF_OK;
@@ -1082,6 +1095,7 @@ static uint32_t bits_for(uint32_t v) {
 // candidates' hashes in d_res; no synchronisation at the end.
 static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, const int32_t* rules,
                      uint32_t n_rules, uint32_t* n_total) {
+  Scratch& sc = ctx->sc[0];
   for (int attempt = 0; attempt < 8; ++attempt) {
     int rc = ensure_parent_buffers(ctx, std::max<uint32_t>(n_parents, 1));
     if (rc) return rc;
@@ -1128,7 +1142,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
     const uint32_t S = (std::max<uint32_t>(ctx->h_scalars[5], 1) + 2 + 3) & ~3u;
     const uint32_t Rs = ctx->h_scalars[6] + 4;
     uint32_t chunk = 0;
-    if ((rc = ensure_step_cand(ctx, total, S)) || (rc = ensure_chunk(ctx, total, S, Rs, &chunk))) return rc;
+    if ((rc = ensure_step_cand(ctx, total, S)) || (rc = ensure_chunk(ctx, sc, ctx->st, total, S, Rs, &chunk))) return rc;
     ctx->step_S = S;
     ctx->step_Rs = Rs;
     ctx->step_n_parents = n_parents;
@@ -1145,14 +1159,14 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       EF_CUDA(cudaGetLastError());
     }
     cudaEventRecord(ctx->ev[2], ctx->st);
-    VArgs V = chunk_args(ctx, S, Rs);
+    VArgs V = chunk_args(ctx, sc, S, Rs);
     V.parent_addr = A.parent_addr;
     V.stats = ctx->d_stats.p;
     V.pscratch = A.pscratch;
     V.pstride = A.pstride;
     V.Os = ctx->h_scalars[8] + 2;
-    EF_CUDA(ctx->d_outsrc.reserve((uint64_t)chunk * V.Os, ctx->st));
-    V.outsrc = ctx->d_outsrc.p;
+    EF_CUDA(sc.outsrc.reserve((uint64_t)chunk * V.Os, ctx->st));
+    V.outsrc = sc.outsrc.p;
     ctx->n_chunks = 0;
     for (uint32_t c0 = 0; c0 < total; c0 += chunk) {
       V.c0 = c0;
@@ -1172,12 +1186,12 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       if (V.slots) k_dirty_slots<128, 8><<<gd, 128, 0, ctx->st>>>(V);
       else k_dirty<<<gd, 128, 0, ctx->st>>>(V);
       EF_CUDA(cudaGetLastError());
-      size_t t1 = ctx->d_sort_tmp.cap;
-      EF_CUDA(cub::DeviceRadixSort::SortPairsDescending(ctx->d_sort_tmp.p, t1, ctx->d_dcount.p, ctx->d_dsorted.p,
-                                                        ctx->d_iota.p, ctx->d_dorder.p, (int)V.n, 0, bits_for(S),
+      size_t t1 = sc.sort_tmp.cap;
+      EF_CUDA(cub::DeviceRadixSort::SortPairsDescending(sc.sort_tmp.p, t1, sc.dcount.p, sc.dsorted.p,
+                                                        sc.iota.p, sc.dorder.p, (int)V.n, 0, bits_for(S),
                                                         ctx->st));
       cudaEventRecord(ce[1], ctx->st);
-      if ((rc = launch_keys(ctx, V))) return rc;
+      if ((rc = launch_keys(ctx, ctx->st, V))) return rc;
       cudaEventRecord(ce[2], ctx->st);
       if (S <= kFastRows) {  // slot-space walk, warp merge into a contiguous key stream, streaming digest
         uint32_t rows = 32;
@@ -1196,7 +1210,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
         cudaEventRecord(ce[3], ctx->st);
         k_digest_pm<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
       } else {
-        if ((rc = sort_fresh_keys(ctx, V))) return rc;
+        if ((rc = sort_fresh_keys(ctx, sc, ctx->st, V))) return rc;
         cudaEventRecord(ce[3], ctx->st);
         k_digest<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
       }
@@ -1479,7 +1493,7 @@ int ef_keep(ef_ctx* ctx, const uint32_t* cand_idx, uint32_t n, const uint32_t* s
   EF_CUDA(cudaGetLastError());
   // node keys, sorted order and ranks of the new records (every parent carries them)
   EF_CUDA(ctx->d_hash_out.reserve(n, ctx->st));
-  if ((rc = hash_records_full(ctx, ctx->d_dst.p, n, ctx->d_hash_out.p))) return rc;
+  if ((rc = hash_records_full(ctx, ctx->sc[0], ctx->st, ctx->d_dst.p, n, ctx->d_hash_out.p))) return rc;
   EF_CUDA(cudaStreamSynchronize(ctx->st));
   return EF_OK;
 }
@@ -1494,25 +1508,54 @@ int ef_last_stats(ef_ctx* ctx, uint64_t* out, uint32_t n) {
   return EF_OK;
 }
 
-int ef_records_write_packed(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const void* host, const uint64_t* offsets,
-                            uint64_t bytes) {
+int ef_records_write_packed_async(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const void* host,
+                                  const uint64_t* offsets, uint64_t bytes) {
   EF_REQUIRE(!ctx->dirty, "tables not committed (call ef_tables_commit)");
   if (!n) return EF_OK;
-  EF_CUDA(ctx->d_stage.reserve(bytes, ctx->st));
-  EF_CUDA(cudaMemcpyAsync(ctx->d_stage.p, host, bytes, cudaMemcpyHostToDevice, ctx->st));
-  std::vector<unsigned long long> off(offsets, offsets + n), dst(n);
+  // record sizes from the host copy: no device round trip before the hashing is queued
+  const uint8_t* hb = reinterpret_cast<const uint8_t*>(host);
+  uint32_t max_n = 0, max_refs = 0;
+  ctx->h_up_off.assign(offsets, offsets + n);
+  ctx->h_up_dst.resize(n);
   for (uint32_t i = 0; i < n; ++i) {
     EF_REQUIRE(slots[i] < ctx->n_slots, "ef_records_write_packed: bad slot");
-    EF_REQUIRE(offsets[i] % 4 == 0 && offsets[i] < bytes, "ef_records_write_packed: bad offset");
-    dst[i] = (unsigned long long)slot_addr(ctx, slots[i]);
+    EF_REQUIRE(offsets[i] % 4 == 0 && offsets[i] + 16 <= bytes, "ef_records_write_packed: bad offset");
+    const uint32_t* h = reinterpret_cast<const uint32_t*>(hb + offsets[i]);
+    EF_REQUIRE(h[0] <= ctx->geo.cap_nodes && h[1] <= ctx->geo.cap_refs && h[2] <= ctx->geo.cap_outs,
+               "ef_records_write_packed: record exceeds the geometry");
+    max_n = std::max(max_n, h[0]);
+    max_refs = std::max(max_refs, h[1]);
+    ctx->h_up_dst[i] = (unsigned long long)slot_addr(ctx, slots[i]);
   }
-  int rc;
-  if ((rc = upload(ctx, ctx->d_addr_a, off)) || (rc = upload(ctx, ctx->d_addr_b, dst))) return rc;
-  k_unpack<<<std::min<uint32_t>(n, ctx->n_sm * 8), 256, 0, ctx->st>>>(reinterpret_cast<const uint8_t*>(ctx->d_stage.p),
-                                                                      ctx->d_addr_a.p, ctx->d_addr_b.p, n, ctx->geo);
+  cudaStream_t st = ctx->st_up;
+  // the slots may still be read by queued main-stream work: the upload starts after it
+  EF_CUDA(cudaEventRecord(ctx->ev_main, ctx->st));
+  EF_CUDA(cudaStreamWaitEvent(st, ctx->ev_main, 0));
+  EF_CUDA(ctx->d_up_stage.reserve(bytes, st));
+  EF_CUDA(ctx->d_up_off.reserve(n, st));
+  EF_CUDA(ctx->d_up_dst.reserve(n, st));
+  EF_CUDA(cudaMemcpyAsync(ctx->d_up_stage.p, host, bytes, cudaMemcpyHostToDevice, st));
+  EF_CUDA(cudaMemcpyAsync(ctx->d_up_off.p, ctx->h_up_off.data(), n * 8ull, cudaMemcpyHostToDevice, st));
+  EF_CUDA(cudaMemcpyAsync(ctx->d_up_dst.p, ctx->h_up_dst.data(), n * 8ull, cudaMemcpyHostToDevice, st));
+  k_unpack<<<std::min<uint32_t>(n, ctx->n_sm * 8), 256, 0, st>>>(reinterpret_cast<const uint8_t*>(ctx->d_up_stage.p),
+                                                                 ctx->d_up_off.p, ctx->d_up_dst.p, n, ctx->geo);
   EF_CUDA(cudaGetLastError());
-  if ((rc = hash_records_full(ctx, ctx->d_addr_b.p, n, nullptr))) return rc;
-  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  int rc = hash_records_full(ctx, ctx->sc[1], st, ctx->d_up_dst.p, n, nullptr, max_n, max_refs);
+  if (rc) return rc;
+  EF_CUDA(cudaEventRecord(ctx->ev_up, st));
+  return EF_OK;
+}
+
+int ef_upload_fence(ef_ctx* ctx) {
+  EF_CUDA(cudaStreamWaitEvent(ctx->st, ctx->ev_up, 0));
+  return EF_OK;
+}
+
+int ef_records_write_packed(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const void* host, const uint64_t* offsets,
+                            uint64_t bytes) {
+  int rc = ef_records_write_packed_async(ctx, slots, n, host, offsets, bytes);
+  if (rc) return rc;
+  EF_CUDA(cudaStreamSynchronize(ctx->st_up));
   return EF_OK;
 }
 

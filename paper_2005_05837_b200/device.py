@@ -513,6 +513,10 @@ class DeviceSession:
                     "ef_expand_finish")
         return self._results(n)
 
+    def upload_fence(self) -> None:
+        """Later steps wait for every asynchronous upload issued so far."""
+        self._check(self.L.ef_upload_fence(self.ctx), "ef_upload_fence")
+
     def keep(self, cand_idx: list[int]) -> list[int]:
         slots = [self.alloc() for _ in cand_idx]
         self._check(self.L.ef_keep(self.ctx, N.u32_array(cand_idx), len(cand_idx), N.u32_array(slots)), "ef_keep")
@@ -560,10 +564,13 @@ class DeviceSession:
             at += 4 * blob.size
         return np.concatenate(parts), np.array(offs, dtype=np.uint64)
 
-    def write_packed(self, slots: list[int], blob: np.ndarray, offsets: np.ndarray) -> None:
-        self._check(self.L.ef_records_write_packed(self.ctx, N.u32_array(slots), len(slots), blob.ctypes.data,
-                                                   offsets.ctypes.data_as(C.POINTER(C.c_uint64)), blob.nbytes),
-                    "ef_records_write_packed")
+    def write_packed(self, slots: list[int], blob: np.ndarray, offsets: np.ndarray, asynchronous: bool = False) -> None:
+        """Upload compact records (see pack); asynchronous=True queues the copy, unpacking and
+        hashing on the upload stream, overlapping a step; call upload_fence() before a step reads
+        them (blob must be page-locked and unchanged until then)."""
+        fn = self.L.ef_records_write_packed_async if asynchronous else self.L.ef_records_write_packed
+        self._check(fn(self.ctx, N.u32_array(slots), len(slots), blob.ctypes.data,
+                       offsets.ctypes.data_as(C.POINTER(C.c_uint64)), blob.nbytes), "ef_records_write_packed")
 
 
 def price_params(f, d: int, use_inner: bool, node_cap: int) -> N.PriceParams:

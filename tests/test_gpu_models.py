@@ -123,3 +123,47 @@ def test_gpu_matches_reference_goldens_at_model_scale(model):
         assert [res.assignment[k] for k in sorted(res.assignment)] == run["assignment"]
         assert (res.cost, res.time_ms, res.energy) == (run["cost"], run["time_ms"], run["energy"])
         assert {k: v for k, v in vars(res.stats).items() if k != "wall_time_ms"} == run["stats"]
+
+
+def test_packed_uploads_sync_async_match_resident():
+    """Compact host uploads (synchronous and pipelined on the upload stream) rebuild the
+    parents exactly: keys, sorted order and ranks recomputed on the device give the same
+    step as the resident frontier."""
+    import numpy as np
+
+    g0 = zoo.generate("resnet50", 0)
+    db = ef.CostDatabase()
+    fr = Frontier(g0, db, ef.SyntheticProfiler(0), ef.CostFunction.energy(), ef.SearchConfig(alpha=1.05), 24)
+    s = fr.s
+    try:
+        base = fr.step().copy()
+        recs = [s.read_record(sl) for sl in fr.slots]
+        blob, offs = s.pack(recs)
+        pinned = s.L.ef_host_alloc(blob.nbytes)
+        import ctypes as C
+
+        staging = np.ctypeslib.as_array((C.c_uint8 * blob.nbytes).from_address(pinned))
+        staging[:] = blob.view(np.uint8)
+        a = [s.alloc() for _ in fr.slots]
+        b = [s.alloc() for _ in fr.slots]
+        s.write_packed(a, staging.view(np.uint32), offs)
+        got_sync = fr.step(a).copy()
+        s.write_packed(b, staging.view(np.uint32), offs, asynchronous=True)
+        s.upload_fence()
+        got_async = fr.step(b).copy()
+        for sl, sa, sb in zip(fr.slots, a, b):  # whole records identical (keys, sperm, skeys, srank)
+            G = s.geo
+            ra, rb, r0 = s.read_record(sa), s.read_record(sb), s.read_record(sl)
+            n = int(r0[:4].view(np.int32)[0])
+            for off, width in ((G.off_keys, 16), (G.off_sperm, 4), (G.off_skeys, 16), (G.off_srank, 4)):
+                assert bytes(ra[off: off + width * n]) == bytes(r0[off: off + width * n])
+                assert bytes(rb[off: off + width * n]) == bytes(r0[off: off + width * n])
+        del staging
+        s.L.ef_host_free(pinned)
+        for sl in a + b:
+            s.free(sl)
+    finally:
+        fr.close()
+    for got in (got_sync, got_async):
+        for key in ("hash", "flags", "cost", "time_ms", "energy", "evals", "sweeps"):
+            assert np.array_equal(got[key], base[key]), key

@@ -274,7 +274,7 @@ def run_ours(args, world, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = ex = sharded_expand = None
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch.distributed as dist
 
         from paper_2005_05837_b200.shard import OwnerExchange, sharded_expand
@@ -428,7 +428,7 @@ def run_ours(args, world, rank, local):
                    "nodes_per_parent": n_nodes, "candidates_per_step": gen_n / args.steps,
                    "priced_per_step": priced_n / args.steps, "rules": "all 6", "inner_search_d": 1,
                    "l2": "flushed (256 MiB write) before every timed step",
-                   "parallelism": "frontier split by parent, dedup owned by hash (NCCL all-to-all)" if world > 1
+                   "parallelism": "frontier split by parent, dedup owned by hash (NCCL all-to-all)" if ex is not None
                    else "single GPU"},
         "stages_ms_per_step": {n: stage_ms[k] / args.steps for k, n in enumerate(names)},
         "roofline": {"bound": "alu", "kernel": "k_keys", "achieved": achieved_c / 1e9, "peak": peak_c / 1e9,
@@ -444,7 +444,7 @@ def run_ours(args, world, rank, local):
                 "mode": "pipelined: batch i+1 uploaded and hashed on the upload stream during step i",
                 "serial_value": ser_priced / (ser_total / 1e3), "serial_ms_per_step": ser_total / args.steps,
                 "serial_upload_hash_ms_per_step": up_ms / args.steps},
-        "gpu_launches": (13 if world == 1 else 17) * args.steps,
+        "gpu_launches": (13 if ex is None else 17) * args.steps,
         "clocks": clk,
     }
     cpu_parents = [_to_oracle(fr.decode(sl)) for sl in mine[:8]] if rank == 0 and world == 1 else []
@@ -476,6 +476,7 @@ def main():
                     help="BASELINE.json config to run as the frontier workload (default: configs[1])")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="use the hash-owner sharded step even on one rank")
     args = ap.parse_args()
     world, rank, local = _dist()
     if args.impl == "reference":

@@ -306,17 +306,18 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize()
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st0, st1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def step(slots):
         """-> (results, device ms of the step)."""
         if ex is None:
             res = fr.step(slots, insert_visited=False)
             return res, sum(s.last_timing())
-        ev0.record()
+        st0.record()
         res = sharded_expand(s, slots, fr.rule_ids, fr.pp, ex)
-        ev1.record()
-        ev1.synchronize()
-        return res, ev0.elapsed_time(ev1)
+        st1.record()
+        st1.synchronize()
+        return res, st0.elapsed_time(st1)
 
     for _ in range(args.warmup):
         step(mine)

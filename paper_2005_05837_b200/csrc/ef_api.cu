@@ -1434,13 +1434,14 @@ int ef_expand_finish(ef_ctx* ctx, const uint32_t* d_verdict_back, const ef_price
   if (ctx->n_send) {
     const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((ctx->n_send + 255) / 256, ctx->n_sm * 8));
     k_apply_verdicts<<<grid, 256, 0, ctx->st>>>(ctx->d_res.p, ctx->d_perm.p, d_verdict_back, ctx->n_send,
-                                                pp->node_cap, ctx->d_plist.p, ctx->d_scalars.p + 7);
+                                                pp->node_cap);
+    const uint32_t gc = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));
+    k_compact_survivors<<<gc, 256, 0, ctx->st>>>(ctx->d_res.p, total, ctx->d_plist.p, ctx->d_scalars.p + 7);
     EF_CUDA(cudaGetLastError());
   }
   cudaEventRecord(ctx->ev[4], ctx->st);
   int rc = step_price(ctx, pp);
   if (rc) return rc;
-  (void)total;
   return step_sync(ctx, true);
 }
 

@@ -1604,21 +1604,24 @@ __global__ void k_owner_insert(OwnerArgs O) {
   }
 }
 
-// verdicts (send order) -> candidate flags, node cap, survivors appended to the price list
+// verdicts (send order) -> candidate flags and node cap
 __global__ void k_apply_verdicts(ef_cand_result* res, const uint32_t* perm, const uint32_t* verdict, uint32_t n,
-                                 int node_cap, uint32_t* plist, uint32_t* plist_n) {
+                                 int node_cap) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t c = perm[i];
+    uint32_t f = res[c].flags | (verdict[i] & (EF_F_FIRST | EF_F_VISITED));
+    if (res[c].n_compute > node_cap) f |= EF_F_CAPPED;
+    res[c].flags = f;
+  }
+}
+
+// survivors in candidate order (neighbouring lanes price siblings of one parent)
+__global__ void k_compact_survivors(const ef_cand_result* res, uint32_t total, uint32_t* plist, uint32_t* plist_n) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t span = (n + 31) / 32 * 32;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < span; i += gridDim.x * blockDim.x) {
-    bool survivor = false;
-    uint32_t c = 0;
-    if (i < n) {
-      c = perm[i];
-      uint32_t f = res[c].flags | (verdict[i] & (EF_F_FIRST | EF_F_VISITED));
-      if (res[c].n_compute > node_cap) f |= EF_F_CAPPED;
-      res[c].flags = f;
-      survivor = (f & (EF_F_FIRST | EF_F_VISITED | EF_F_CAPPED)) == EF_F_FIRST;
-    }
+  const uint32_t span = (total + blockDim.x - 1) / blockDim.x * blockDim.x;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < span; c += gridDim.x * blockDim.x) {
+    const bool survivor =
+        c < total && (res[c].flags & (EF_F_INCOMPLETE | EF_F_FIRST | EF_F_VISITED | EF_F_CAPPED)) == EF_F_FIRST;
     const unsigned m = __ballot_sync(0xffffffffu, survivor);
     if (m) {
       uint32_t base = 0;

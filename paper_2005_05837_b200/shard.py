@@ -38,13 +38,10 @@ class OwnerExchange:
         if self.device.type == "cuda":
             torch.cuda.current_stream(self.device).synchronize()
 
-    def order_base(self, n: int) -> tuple[int, int]:
-        """(first global candidate index of this rank, total over ranks)."""
-        t = torch.tensor([n], dtype=torch.int64, device=self.device)
-        parts = [torch.zeros_like(t) for _ in range(self.world)]
-        dist.all_gather(parts, t, group=self.group)
-        counts = [int(p.item()) for p in parts]
-        return sum(counts[: self.rank]), sum(counts)
+    def order_base(self) -> int:
+        """Global order of this rank's first candidate: rank-major order needs no exchange,
+        (rank << 40) + index is monotone in (rank, index)."""
+        return self.rank << 40
 
     def to_owners(self, send: torch.Tensor, counts: list[int]) -> tuple[torch.Tensor, list[int]]:
         """`send` holds sum(counts) pairs grouped by owner; returns the pairs this rank owns
@@ -87,7 +84,7 @@ def sharded_expand(session, slots: list[int], rule_ids: list[int], pp, ex: Owner
     flags FIRST / VISITED are global, costs are those of this rank's survivors.
     """
     n = session.expand_hashes(slots, rule_ids)
-    base, _ = ex.order_base(n)
+    base = ex.order_base()
     send = torch.empty(max(2 * n, 2), dtype=torch.int64, device=ex.device)
     counts = session.route_owners(ex.world, base, send)
     recv, recv_counts = ex.to_owners(send, counts)

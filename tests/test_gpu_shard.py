@@ -35,9 +35,8 @@ class ThreadExchange:
         self.sh["barrier"].wait()
         return out
 
-    def order_base(self, n):
-        counts = self._gather(n)
-        return sum(counts[: self.rank]), sum(counts)
+    def order_base(self):
+        return self.rank << 40
 
     def to_owners(self, send, counts):
         data = self._gather((send, counts))

@@ -307,6 +307,7 @@ def run_ours(args, world, rank, local):
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     st0, st1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    phases: dict = {}  # host seconds per sharded-step phase
 
     def step(slots):
         """-> (results, device ms of the step)."""
@@ -314,7 +315,7 @@ def run_ours(args, world, rank, local):
             res = fr.step(slots, insert_visited=False)
             return res, sum(s.last_timing())
         st0.record()
-        res = sharded_expand(s, slots, fr.rule_ids, fr.pp, ex)
+        res = sharded_expand(s, slots, fr.rule_ids, fr.pp, ex, phases=phases)
         st1.record()
         st1.synchronize()
         return res, st0.elapsed_time(st1)
@@ -446,6 +447,8 @@ def run_ours(args, world, rank, local):
                 "serial_value": ser_priced / (ser_total / 1e3), "serial_ms_per_step": ser_total / args.steps,
                 "serial_upload_hash_ms_per_step": up_ms / args.steps},
         "gpu_launches": (13 if ex is None else 17) * args.steps,
+        "sharded_phases_ms_per_call": ({k: 1e3 * v / phases["calls"] for k, v in phases.items() if k != "calls"}
+                                       if phases else None),
         "clocks": clk,
     }
     cpu_parents = [_to_oracle(fr.decode(sl)) for sl in mine[:8]] if rank == 0 and world == 1 else []

@@ -33,6 +33,15 @@ class OwnerExchange:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.device = device if device is not None else torch.device("cpu")
+        self._bufs: dict[str, torch.Tensor] = {}
+
+    def buffer(self, name: str, numel: int, dtype) -> torch.Tensor:
+        """A reusable device buffer of at least `numel` elements (no allocator traffic per step)."""
+        buf = self._bufs.get(name)
+        if buf is None or buf.numel() < numel or buf.dtype != dtype:
+            buf = torch.empty(max(numel, 1024), dtype=dtype, device=self.device)
+            self._bufs[name] = buf
+        return buf[:numel]
 
     def _sync(self):
         if self.device.type == "cuda":
@@ -77,19 +86,38 @@ class OwnerExchange:
 
 
 def sharded_expand(session, slots: list[int], rule_ids: list[int], pp, ex: OwnerExchange,
-                   insert_visited: bool = False):
+                   insert_visited: bool = False, phases: dict | None = None):
     """One frontier step over the parents of this rank with hash-owner deduplication.
 
     Returns this rank's candidate results (the layout of `DeviceSession.expand`);
     flags FIRST / VISITED are global, costs are those of this rank's survivors.
+    `phases`, when given, accumulates host wall seconds per phase.
     """
+    import time
+
+    t = [time.perf_counter()]
+
+    def mark():
+        t.append(time.perf_counter())
+
     n = session.expand_hashes(slots, rule_ids)
+    mark()
     base = ex.order_base()
-    send = torch.empty(max(2 * n, 2), dtype=torch.int64, device=ex.device)
+    send = ex.buffer("send", max(2 * n, 2), torch.int64)
     counts = session.route_owners(ex.world, base, send)
+    mark()
     recv, recv_counts = ex.to_owners(send, counts)
-    verdict = torch.empty(max(recv.numel() // 2, 1), dtype=torch.int32, device=ex.device)
+    mark()
+    verdict = ex.buffer("verdict", max(recv.numel() // 2, 1), torch.int32)
     if recv.numel():
         session.owner_mark(recv, verdict, insert_visited)
+    mark()
     back = ex.back(verdict, recv_counts, counts)
-    return session.expand_finish(back, pp, n)
+    mark()
+    out = session.expand_finish(back, pp, n)
+    mark()
+    if phases is not None:
+        phases["calls"] = phases.get("calls", 0) + 1
+        for name, a, b in zip(("hash", "route", "to_owners", "mark", "back", "finish"), t, t[1:]):
+            phases[name] = phases.get(name, 0.0) + (b - a)
+    return out

@@ -1389,7 +1389,7 @@ int ef_route_owners(ef_ctx* ctx, uint32_t world, uint64_t order_base, uint64_t* 
   EF_CUDA(cudaMemsetAsync(ctx->d_route.p, 0, (2 * (size_t)world + 2) * 4, ctx->st));
   const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));
   RouteArgs R{ctx->d_res.p, total, world, order_base, ctx->d_route.p, ctx->d_route.p + world, d_send, ctx->d_perm.p};
-  k_route_count<<<grid_t, 256, 0, ctx->st>>>(R);
+  k_route_count<<<grid_t, 256, world * 4, ctx->st>>>(R);
   EF_CUDA(cudaGetLastError());
   std::vector<uint32_t> cnt(world), off(world);
   EF_CUDA(cudaMemcpyAsync(cnt.data(), ctx->d_route.p, world * 4, cudaMemcpyDeviceToHost, ctx->st));
@@ -1402,7 +1402,7 @@ int ef_route_owners(ef_ctx* ctx, uint32_t world, uint64_t order_base, uint64_t* 
   }
   ctx->n_send = run;
   EF_CUDA(cudaMemcpyAsync(ctx->d_route.p + world, off.data(), world * 4, cudaMemcpyHostToDevice, ctx->st));
-  k_route_scatter<<<grid_t, 256, 0, ctx->st>>>(R);
+  k_route_scatter<<<grid_t, 256, world * 8, ctx->st>>>(R);
   EF_CUDA(cudaGetLastError());
   EF_CUDA(cudaStreamSynchronize(ctx->st));
   return EF_OK;

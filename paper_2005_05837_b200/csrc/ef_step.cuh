@@ -1526,19 +1526,42 @@ struct RouteArgs {
 
 __device__ __forceinline__ uint32_t owner_of(uint64_t h, uint32_t world) { return (uint32_t)(h % world); }
 
+// per-block owner histograms in shared memory, one global atomic per (block, owner)
 __global__ void k_route_count(RouteArgs R) {
+  extern __shared__ uint32_t hist[];
+  for (uint32_t w = threadIdx.x; w < R.world; w += blockDim.x) hist[w] = 0;
+  __syncthreads();
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < R.total; c += gridDim.x * blockDim.x) {
     const ef_cand_result& r = R.res[c];
     if (r.flags & EF_F_INCOMPLETE) continue;
-    atomicAdd(&R.count[owner_of(r.hash, R.world)], 1u);
+    atomicAdd(&hist[owner_of(r.hash, R.world)], 1u);
   }
+  __syncthreads();
+  for (uint32_t w = threadIdx.x; w < R.world; w += blockDim.x)
+    if (hist[w]) atomicAdd(&R.count[w], hist[w]);
 }
 
+// each block reserves its range per owner once, then its threads fill it
 __global__ void k_route_scatter(RouteArgs R) {
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < R.total; c += gridDim.x * blockDim.x) {
+  extern __shared__ uint32_t hist[];  // [world] counts, then [world] block bases
+  uint32_t* base = hist + R.world;
+  const uint32_t per = (R.total + gridDim.x - 1) / gridDim.x;  // contiguous candidates per block
+  const uint32_t lo = blockIdx.x * per, hi = min(R.total, lo + per);
+  for (uint32_t w = threadIdx.x; w < R.world; w += blockDim.x) hist[w] = 0;
+  __syncthreads();
+  for (uint32_t c = lo + threadIdx.x; c < hi; c += blockDim.x)
+    if (!(R.res[c].flags & EF_F_INCOMPLETE)) atomicAdd(&hist[owner_of(R.res[c].hash, R.world)], 1u);
+  __syncthreads();
+  for (uint32_t w = threadIdx.x; w < R.world; w += blockDim.x) {
+    base[w] = hist[w] ? atomicAdd(&R.cursor[w], hist[w]) : 0u;
+    hist[w] = 0;
+  }
+  __syncthreads();
+  for (uint32_t c = lo + threadIdx.x; c < hi; c += blockDim.x) {
     const ef_cand_result& r = R.res[c];
     if (r.flags & EF_F_INCOMPLETE) continue;
-    const uint32_t pos = atomicAdd(&R.cursor[owner_of(r.hash, R.world)], 1u);
+    const uint32_t o = owner_of(r.hash, R.world);
+    const uint32_t pos = base[o] + atomicAdd(&hist[o], 1u);
     R.send[2 * (uint64_t)pos] = r.hash;
     R.send[2 * (uint64_t)pos + 1] = R.order_base + c;
     R.perm[pos] = c;

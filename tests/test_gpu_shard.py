@@ -38,6 +38,9 @@ class ThreadExchange:
     def order_base(self):
         return self.rank << 40
 
+    def buffer(self, name, numel, dtype):
+        return torch.empty(max(numel, 1), dtype=dtype, device=self.device)[:numel]
+
     def to_owners(self, send, counts):
         data = self._gather((send, counts))
         parts, rc = [], []

@@ -312,11 +312,11 @@ def run_ours(args, world, rank, local):
         """-> (results, device ms of the step)."""
         if ex is None:
             res = fr.step(slots, insert_visited=False)
-            return res, sum(s.last_timing())
-        res = sharded_expand(s, slots, fr.rule_ids, fr.pp, ex, phases=phases)
-        # the library's events span match .. price of this rank, including the exchange and its
-        # host round trips, excluding the results copy -- the same span as the single-rank step
-        return res, sum(s.last_timing())
+        else:
+            res = sharded_expand(s, slots, fr.rule_ids, fr.pp, ex, phases=phases)
+        # the library's events span match .. price (a sharded step: the exchange and its host
+        # round trips included), excluding the results copy
+        return res, s.last_step_ms()
 
     for _ in range(args.warmup):
         step(mine)

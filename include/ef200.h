@@ -224,7 +224,8 @@ int ef_owner_mark(ef_ctx* ctx, const uint64_t* d_recv, uint32_t n_recv, uint32_t
 int ef_expand_finish(ef_ctx* ctx, const uint32_t* d_verdict_back, const ef_price_params* pp);
 
 /* device time (ms) of the last ef_expand, measured with CUDA events on its stream, per
- * stage: match, plan, dirty walk, node keys, key sort, graph digest, dedup, price (n <= 8) */
+ * stage: match, plan, dirty walk, node keys, key sort, graph digest, dedup, price, and [8] the
+ * whole step from match to price (for a sharded step: including the exchange) (n <= 9) */
 int ef_last_timing(ef_ctx* ctx, float* ms, uint32_t n);
 /* counters of the last step: BLAKE2b compressions in node keys, in graph digests,
  * candidates, priced survivors (n <= 4) */

@@ -160,7 +160,7 @@ struct ef_ctx {
   cudaEvent_t ev[6] = {};
   std::vector<cudaEvent_t> ev_chunk;  // 5 per hashing chunk: dirty | keys | sort | digest
   uint32_t n_chunks = 0;
-  float last_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  float last_ms[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   uint64_t last_stats[4] = {0, 0, 0, 0};
 };
 
@@ -1325,6 +1325,7 @@ static int step_sync(ef_ctx* ctx, bool timings) {
     for (int k = 0; k < 4; ++k) ctx->last_ms[2 + k] = sub[k];
     ctx->last_ms[6] = ms[3];
     ctx->last_ms[7] = ms[4];
+    cudaEventElapsedTime(&ctx->last_ms[8], ctx->ev[0], ctx->ev[5]);  // the whole step (incl. any exchange)
     EF_CUDA(cudaMemcpyAsync(ctx->last_stats, ctx->d_stats.p, 2 * 8, cudaMemcpyDeviceToHost, ctx->st));
     EF_CUDA(cudaStreamSynchronize(ctx->st));
     ctx->last_stats[2] = ctx->last_total;
@@ -1500,7 +1501,7 @@ int ef_keep(ef_ctx* ctx, const uint32_t* cand_idx, uint32_t n, const uint32_t* s
 }
 
 int ef_last_timing(ef_ctx* ctx, float* ms, uint32_t n) {
-  for (uint32_t k = 0; k < n && k < 8; ++k) ms[k] = ctx->last_ms[k];
+  for (uint32_t k = 0; k < n && k < 9; ++k) ms[k] = ctx->last_ms[k];
   return EF_OK;
 }
 

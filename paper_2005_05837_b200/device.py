@@ -533,9 +533,15 @@ class DeviceSession:
 
     def last_timing(self) -> list[float]:
         """Device ms of the last step per stage (STAGES), CUDA events on the library stream."""
-        ms = (C.c_float * 8)()
-        self.L.ef_last_timing(self.ctx, ms, 8)
-        return list(ms)
+        ms = (C.c_float * 9)()
+        self.L.ef_last_timing(self.ctx, ms, 9)
+        return list(ms)[:8]
+
+    def last_step_ms(self) -> float:
+        """Device ms of the whole last step, match to price (a sharded step: exchange included)."""
+        ms = (C.c_float * 9)()
+        self.L.ef_last_timing(self.ctx, ms, 9)
+        return float(ms[8])
 
     def last_stats(self) -> dict:
         out = (C.c_uint64 * 4)()

@@ -119,10 +119,8 @@ struct ef_ctx {
   // step buffers
   DevBuf<unsigned long long> d_parent_addr, d_sites, d_step_key, d_addr_a, d_addr_b;
   DevBuf<uint32_t> d_pscratch, d_site_count, d_cand_off, d_step_seq, d_scalars;
-  DevBuf<char> d_cand, d_stage;
-  DevBuf<int32_t> d_srcpos, d_req_dv;
-  DevBuf<uint8_t> d_seed, d_pmark;
-  DevBuf<uint32_t> d_first, d_first_sorted, d_order;
+  DevBuf<char> d_stage;
+  DevBuf<int32_t> d_req_dv;
   DevBuf<ef_cand_result> d_res, d_res_aux;
   DevBuf<ef_sig_desc> d_req_sig;
   DevBuf<uint64_t> d_hash_out;
@@ -274,15 +272,8 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_cand_off.release();
   ctx->d_step_seq.release();
   ctx->d_scalars.release();
-  ctx->d_cand.release();
   ctx->d_stage.release();
-  ctx->d_srcpos.release();
   ctx->d_req_dv.release();
-  ctx->d_seed.release();
-  ctx->d_pmark.release();
-  ctx->d_first.release();
-  ctx->d_first_sorted.release();
-  ctx->d_order.release();
   ctx->d_res.release();
   ctx->d_res_aux.release();
   ctx->d_req_sig.release();
@@ -1054,7 +1045,6 @@ static VArgs chunk_args(ef_ctx* ctx, Scratch& sc, uint32_t S, uint32_t Rs) {
   V.fresh_sorted = sc.fresh2.p;
   V.input_words = reinterpret_cast<const uint64_t*>(ctx->d_input_text.p);
   V.err = ctx->d_scalars.p + 1;
-  V.one = 1;
   V.jv = sc.jv.p;
   return V;
 }
@@ -1477,17 +1467,11 @@ int ef_keep(ef_ctx* ctx, const uint32_t* cand_idx, uint32_t n, const uint32_t* s
   std::vector<uint32_t> sel(cand_idx, cand_idx + n);
   int rc;
   if ((rc = upload(ctx, ctx->d_dst, dst)) || (rc = upload(ctx, ctx->d_sel, sel))) return rc;
-  EF_CUDA(ctx->d_srcpos.reserve((uint64_t)n * g.cap_nodes, ctx->st));
-  EF_CUDA(ctx->d_seed.reserve((uint64_t)n * g.cap_nodes, ctx->st));
-  EF_CUDA(ctx->d_pmark.reserve((uint64_t)n * g.cap_nodes, ctx->st));
   // the step's parents, sites and plans are still in place: materialise the chosen candidates
   StepArgs A = ctx->last_step;
   A.sel = ctx->d_sel.p;
   A.n_sel = n;
   A.dst = ctx->d_dst.p;
-  A.cand_srcpos = ctx->d_srcpos.p;
-  A.cand_seed = ctx->d_seed.p;
-  A.cand_pmark = ctx->d_pmark.p;
   k_materialise<kMatThreads><<<std::min<uint32_t>(n, ctx->n_sm * 8), kMatThreads, 0, ctx->st>>>(A);
   EF_CUDA(cudaGetLastError());
   k_keep_alg<<<std::min<uint32_t>(n, ctx->n_sm * 8), 128, 0, ctx->st>>>(ctx->d_alg8.p, ctx->step_S, ctx->d_sel.p,

@@ -140,12 +140,7 @@ struct StepArgs {
   uint32_t* site_count;  // per parent
   uint32_t* cand_off;    // n_parents + 1
   uint32_t* total;       // [0] = number of candidates
-  char* cand_base;       // scratch records
   uint32_t cand_cap;
-  int32_t* cand_srcpos;  // cap_nodes per candidate
-  uint8_t* cand_seed;    // cap_nodes per candidate
-  uint8_t* cand_pmark;   // cap_nodes per candidate: parent position removed (dropped or re-keyed)
-  uint32_t* cand_first;  // per candidate: first child topo slot whose key can differ from the parent
   ef_cand_result* res;
   ef_sig_desc* req_sig;
   uint32_t* n_req_sig;
@@ -370,7 +365,7 @@ __global__ void __launch_bounds__(BT) k_offsets(StepArgs A) {
 }
 
 // ------------------------------------------------------------------------------------------
-// k_materialise: one CTA per candidate
+// k_materialise: one CTA per kept candidate (keep mode: sel -> dst records)
 // ------------------------------------------------------------------------------------------
 
 struct Plan {
@@ -543,11 +538,9 @@ __device__ void plan_rewrite(const StepArgs& A, Plan& P, Rec R, int n, uint32_t 
 template <int BT>
 __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
   __shared__ Plan P;
-  __shared__ uint32_t first_slot;
   const Geo& G = A.g;
-  const uint32_t total = A.sel ? A.n_sel : min(A.total[0], A.cand_cap);
-  for (uint32_t ci = blockIdx.x; ci < total; ci += gridDim.x) {
-    const uint32_t c = A.sel ? A.sel[ci] : ci;
+  for (uint32_t ci = blockIdx.x; ci < A.n_sel; ci += gridDim.x) {
+    const uint32_t c = A.sel[ci];
     // parent of candidate c: last pi with cand_off[pi] <= c
     uint32_t lo = 0, hi = A.n_parents;
     while (hi - lo > 1) {
@@ -559,7 +552,7 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
     const unsigned long long site = A.sites[(uint64_t)pi * A.site_cap + (c - A.cand_off[pi])];
     const uint32_t rule = (uint32_t)(site >> 56), sa = (uint32_t)(site >> 28) & 0xfffffffu, sb = (uint32_t)site & 0xfffffffu;
     Rec R{reinterpret_cast<char*>(A.parent_addr[pi])};
-    Rec C{A.sel ? reinterpret_cast<char*>(A.dst[ci]) : A.cand_base + (uint64_t)c * G.bytes};
+    Rec C{reinterpret_cast<char*>(A.dst[ci])};
     const int n = R.h().n, n_refs = R.h().n_refs, n_out = R.h().n_out;
     const uint32_t* u0 = A.pscratch + (uint64_t)pi * A.pstride;
     const uint32_t* u1 = u0 + G.cap_nodes;
@@ -568,7 +561,6 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
     if (threadIdx.x == 0) {
       plan_rewrite(A, P, R, n, rule, sa, sb, u0, u1);
       P.slot_of[0] = P.slot_of[1] = P.slot_of[2] = -1;
-      first_slot = 0xffffffffu;
       for (int k = 0; k < 2; ++k) {
         P.drop_refs[k] = P.drop[k] >= 0 ? (int)pnin[P.drop[k]] : 0;
         P.drop_inoff[k] = P.drop[k] >= 0 ? pinoff[P.drop[k]] : 0xffffffffu;
@@ -599,13 +591,9 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
     const int n_child = n_keep + P.n_live;
     const int drop_ref_tot = P.drop_refs[0] + P.drop_refs[1];
     const int n_refs_child = n_refs - drop_ref_tot + P.n_live;
-    ef_cand_result* res = A.res + c;
     const bool fits = n_child <= (int)G.cap_nodes && n_refs_child <= (int)G.cap_refs;
     if (!fits) {
-      if (threadIdx.x == 0) {
-        atomicOr(A.err, 4u);
-        if (!A.sel) res->flags = EF_F_INCOMPLETE;
-      }
+      if (threadIdx.x == 0) atomicOr(A.err, 4u);
       __syncthreads();
       continue;
     }
@@ -624,8 +612,6 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
       return r;
     };
     auto map_ref = [&](uint32_t r) -> uint32_t { return (cpos(r >> 8) << 8) | (r & 255u); };
-    int32_t* srcpos = A.cand_srcpos + (uint64_t)ci * G.cap_nodes;
-    uint8_t* seed = A.cand_seed + (uint64_t)ci * G.cap_nodes;
     // nodes
     {
       const int32_t* pnid = R.nid(G);
@@ -638,9 +624,7 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
       uint32_t* cinoff = C.inoff(G);
       const uint64_t* pkeys = R.keys(G);
       uint64_t* ckeys = C.keys(G);
-      uint8_t* pmark = A.cand_pmark + (uint64_t)ci * G.cap_nodes;
       for (int i = threadIdx.x; i < n; i += BT) {
-        pmark[i] = (i == d0 || i == d1) ? 1 : 0;
         if (i == d0 || i == d1) continue;
         uint32_t j = cpos((uint32_t)i);
         cnid[j] = pnid[i];
@@ -652,8 +636,6 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
         uint32_t off = pinoff[i];
         off -= (off > P.drop_inoff[0] ? (uint32_t)P.drop_refs[0] : 0u) + (off > P.drop_inoff[1] ? (uint32_t)P.drop_refs[1] : 0u);
         cinoff[j] = off;
-        srcpos[j] = i;
-        seed[j] = i == P.mod ? 1 : 0;
       }
       if (threadIdx.x < 2) {
         const int k = threadIdx.x;
@@ -664,8 +646,6 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
           caux[j] = P.new_aux[k];
           cnin[j] = 1;
           cinoff[j] = (uint32_t)(n_refs - drop_ref_tot) + (j - (uint32_t)n_keep);
-          srcpos[j] = -1;
-          seed[j] = 1;
         }
       }
       if (threadIdx.x == 0) cinoff[n_child] = (uint32_t)n_refs_child;
@@ -682,20 +662,7 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
         if (in0 || in1) continue;
         uint32_t dst = ru - (ru > P.drop_inoff[0] ? (uint32_t)P.drop_refs[0] : 0u) - (ru > P.drop_inoff[1] ? (uint32_t)P.drop_refs[1] : 0u);
         uint32_t v = prefs[r];
-        uint32_t w = remap(v);
-        crefs[dst] = map_ref(w);
-        if (w != v) {
-          // the owner of this ref now consumes a different producer: its key changes
-          uint32_t lo2 = 0, hi2 = (uint32_t)n;
-          while (hi2 - lo2 > 1) {
-            uint32_t mid = (lo2 + hi2) >> 1;
-            if (pinoff[mid] <= ru) lo2 = mid;
-            else hi2 = mid;
-          }
-          // several nodes may share an offset when some have no inputs: take the last with nin > 0
-          while (lo2 > 0 && pnin[lo2] == 0) --lo2;
-          seed[cpos(lo2)] = 1;
-        }
+        crefs[dst] = map_ref(remap(v));
       }
       if (threadIdx.x < 2) {
         const int k = threadIdx.x;
@@ -729,18 +696,13 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
       for (int s = threadIdx.x; s < n; s += BT) {
         int shift = 0;
         bool special = false;
-        int emit = 1;
         for (int k = 0; k < 3; ++k) {
           if (sp_slot[k] < 0) continue;
           if (sp_slot[k] < s) shift += sp_emit[k] - 1;
-          if (sp_slot[k] == s) {
-            special = true;
-            emit = sp_emit[k];
-          }
+          if (sp_slot[k] == s) special = true;
         }
         uint32_t at = (uint32_t)(s + shift);
         uint32_t v = ptopo[s];
-        if (special || (int)v == P.mod) atomicMin(&first_slot, at);
         if (!special) {
           ctopo[at] = cpos(v);
         } else if (s == sp_slot[2]) {
@@ -749,32 +711,15 @@ __global__ void __launch_bounds__(BT) k_materialise(StepArgs A) {
           for (int k = 0; k < P.n_new; ++k)
             if (P.live[k]) ctopo[at + e++] = (uint32_t)n_keep + (k == 1 ? (uint32_t)P.live[0] : 0u);
         }
-        (void)emit;
       }
     }
-    __syncthreads();  // first_slot complete
+    __syncthreads();
     if (threadIdx.x == 0) {
       ef_rec_header& H = C.h();
       H.n = n_child;
       H.n_refs = n_refs_child;
       H.n_out = n_out;
       H.n_compute = R.h().n_compute - (n - n_keep) + P.n_live;
-    }
-    if (threadIdx.x == 0 && !A.sel) {
-      res->flags = P.incomplete ? EF_F_INCOMPLETE : 0u;
-      res->parent = pi;
-      res->rule = rule;
-      res->site_a = sa;
-      res->site_b = sb;
-      A.cand_first[c] = first_slot;
-      res->touched_sig[0] = P.touched[0];
-      res->touched_sig[1] = P.touched[1];
-      res->n_compute = C.h().n_compute;
-      res->n_nodes = (uint32_t)n_child;
-      res->hash = 0;
-      res->cost = res->time_ms = res->energy = 0.0;
-      res->evals = 0;
-      res->sweeps = 0;
     }
     __syncthreads();
   }

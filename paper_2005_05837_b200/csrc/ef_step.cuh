@@ -21,7 +21,6 @@
 //                               (graph.py:541-549)
 // followed by the existing dedup kernels and k_price on the virtual view.
 #pragma once
-#include "ef_b2b_fma.cuh"
 #include "ef_kernels.cuh"
 
 namespace ef {
@@ -79,7 +78,6 @@ struct VArgs {
   uint64_t* fresh_sorted;  // [n][S][2] the fresh keys in ascending byte order
   const uint64_t* input_words;  // input text, 8-byte words, zero padded
   uint32_t* err;
-  uint32_t one;  // == 1 at run time (keeps BLAKE2b additions on IMAD, see ef_b2b_fma.cuh)
   // full mode (whole records: uploads, kept candidates): parent_addr[c] is record c itself,
   // every node is a job, jv[c][j] = position of job j; graph hashes go to hash_out[c]
   int full;

@@ -951,10 +951,13 @@ int ef_visited_count(ef_ctx* ctx, uint64_t* count) {
 // the frontier step
 // ---------------------------------------------------------------------------------------------
 
+// words per parent of k_match's tables (ef_kernels.cuh) plus k_reach's rows (ef_step.cuh)
+static uint64_t pstride_of(const Geo& g) { return 10ull * g.cap_nodes + 1 + 2ull * g.cap_refs + kReachSlots * kReachWords; }
+
 static int ensure_parent_buffers(ef_ctx* ctx, uint32_t n_parents) {
   const Geo& g = ctx->geo;
   if (ctx->site_cap == 0) ctx->site_cap = std::max<uint32_t>(4 * g.cap_nodes, 256);
-  const uint64_t pstride = 10ull * g.cap_nodes + 1 + 2ull * g.cap_refs;
+  const uint64_t pstride = pstride_of(g);
   EF_CUDA(ctx->d_parent_addr.reserve(n_parents, ctx->st));
   EF_CUDA(ctx->d_pscratch.reserve(pstride * n_parents, ctx->st));
   EF_CUDA(ctx->d_sites.reserve((uint64_t)ctx->site_cap * n_parents, ctx->st));
@@ -1100,7 +1103,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
     A.parent_addr = ctx->d_parent_addr.p;
     A.n_parents = n_parents;
     A.pscratch = ctx->d_pscratch.p;
-    A.pstride = 10ull * g.cap_nodes + 1 + 2ull * g.cap_refs;
+    A.pstride = pstride_of(g);
     for (uint32_t i = 0; i < n_rules; ++i) A.rules[i] = rules[i];
     A.n_rules = (int32_t)n_rules;
     A.sites = ctx->d_sites.p;
@@ -1144,6 +1147,13 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
 
     // 2) rewrite plans; 3) per chunk: dirty walk, node keys, key sort, graph digest
     const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));
+    if (total && S <= kFastRows) {  // per-parent reach rows for k_dirty_warp
+      const uint32_t rmax = ctx->h_scalars[6];
+      const size_t smem = 2ull * 4 * (256 + 260 + ((rmax + 3) & ~3u) + kReachSlots * kReachWords);
+      EF_CUDA(cudaFuncSetAttribute(k_reach, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_reach<<<std::max<uint32_t>(1, (n_parents + 1) / 2), 64, smem, ctx->st>>>(A, rmax);
+      EF_CUDA(cudaGetLastError());
+    }
     if (total) {
       k_plan<<<grid_t, 256, 0, ctx->st>>>(A, ctx->d_plan.p);
       EF_CUDA(cudaGetLastError());
@@ -1173,8 +1183,12 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       // the shared-memory merge also handle rows <= 1024, but measured slower than the general
       // kernels there: NasNet-A 15.1 vs 13.8 ms per 1024-parent step)
       V.slots = S <= kFastRows;
-      if (V.slots) k_dirty_slots<128, 8><<<gd, 128, 0, ctx->st>>>(V);
-      else k_dirty<<<gd, 128, 0, ctx->st>>>(V);
+      if (V.slots) {
+        const uint32_t gw = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
+        k_dirty_warp<4><<<gw, 128, 0, ctx->st>>>(V);
+      } else {
+        k_dirty<<<gd, 128, 0, ctx->st>>>(V);
+      }
       EF_CUDA(cudaGetLastError());
       size_t t1 = sc.sort_tmp.cap;
       EF_CUDA(cub::DeviceRadixSort::SortPairsDescending(sc.sort_tmp.p, t1, sc.dcount.p, sc.dsorted.p,
@@ -1262,7 +1276,7 @@ static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
   Pv.plan = ctx->d_plan.p;
   Pv.parent_addr = ctx->d_parent_addr.p;
   Pv.pscratch = ctx->d_pscratch.p;
-  Pv.pstride = 10ull * ctx->geo.cap_nodes + 1 + 2ull * ctx->geo.cap_refs;
+  Pv.pstride = pstride_of(ctx->geo);
   Pv.alg8 = ctx->d_alg8.p;
   Pv.S = ctx->step_S;
   const uint32_t gp = std::max<uint32_t>(1, std::min<uint32_t>((total + kPriceThreads - 1) / kPriceThreads, ctx->n_sm * 16));

@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(BT) k_match(StepArgs A) {
 
     for (int i = threadIdx.x; i < n; i += BT) u0[i] = u1[i] = ccur[i] = 0;
     __syncthreads();
-    {  // slot-space tables of the parent for k_dirty_slots: node + packed (ref offset, arity)
+    {  // slot-space tables of the parent for k_reach / k_dirty_warp: node + packed (ref offset, arity)
        // per topological slot, and every ref as (producer slot << 8 | port)
       uint32_t* s_v = tslot + G.cap_nodes;
       uint32_t* s_pk = s_v + G.cap_nodes;

@@ -6,10 +6,12 @@
 // materialised afterwards (ef_keep).  Per step:
 //
 //   k_plan    thread/candidate  the rewrite plan of rules.py:164-331 in parent coordinates
-//   k_dirty   thread/candidate  walks the parent's topological order from the first slot the
-//                               rewrite can touch and emits one "job" per node whose Merkle key
-//                               (graph.py:530-540) changes: its signature, weight set and the
-//                               source of every producer key (parent key or fresh key j)
+//   k_reach   warp/parent       (parents <= 256 nodes) downstream-closure rows of every slot
+//   k_dirty_warp warp/candidate one "job" per node whose Merkle key (graph.py:530-540)
+//                               changes: its signature, weight set and the source of every
+//                               producer key (parent key or fresh key j); the dirty set is an
+//                               OR of reach rows.  k_dirty (thread/candidate, a walk of the
+//                               topological order) serves larger parents.
 //   sort      cub radix         candidates by job count, so the lanes of a warp run the same
 //                               number of compressions
 //   k_keys    thread/candidate  one BLAKE2b-128 per job; the message is assembled in a
@@ -68,11 +70,11 @@ struct VArgs {
   uint32_t* sval_sorted;
   int32_t* seg_begin;  // [n]
   int32_t* seg_end;    // [n]
-  const uint32_t* pscratch;  // per-parent tables of k_match (slot space for k_dirty_slots)
+  const uint32_t* pscratch;  // per-parent tables of k_match and k_reach
   uint64_t pstride;
   uint32_t Os;         // words per output-source row
-  uint32_t* outsrc;    // [n][Os] key source of every (remapped) graph output (k_dirty_slots)
-  int slots;           // 1: k_dirty_slots wrote outsrc instead of didx rows
+  uint32_t* outsrc;    // [n][Os] key source of every (remapped) graph output (k_dirty_warp)
+  int slots;           // 1: k_dirty_warp wrote outsrc instead of didx rows
   uint32_t W;          // words per removed-mask row
   uint32_t* rmask;     // [n][W] parent keys (by sorted rank) absent from the candidate: dropped or dirty
   uint64_t* fresh_sorted;  // [n][S][2] the fresh keys in ascending byte order
@@ -274,27 +276,93 @@ __global__ void k_dirty(VArgs A) {
 }
 
 // ------------------------------------------------------------------------------------------
-// k_dirty_slots (parents of <= 256 nodes): the walk of k_dirty in topological-slot space.
-// The dirty set is a slot bitmask in shared memory (a column per thread); a dirty node's fresh
-// index is the popcount of dirty slots before it plus the new nodes emitted before it, so no
-// per-position index rows are written or read back.  Slot tables from k_match turn the
-// topo -> inoff/nin -> refs chain into one load per slot and one per ref.
+// k_reach + k_dirty_warp (parents of <= 256 topological slots)
+//
+// A node's Merkle key changes iff its own (sig, aux) or one of its input refs changes, or a
+// producer's key changes (graph.py:528-540), so a candidate's dirty set is the downstream
+// closure of its seeds: the node rewritten in place and the owners of remapped refs.
+// k_reach gives every parent, once per step, reach[s] = the slots reachable from topological
+// slot s (itself included) as 8 words.  k_dirty_warp then takes one warp per candidate: the
+// dirty mask is an OR of a few reach rows, job indices are prefix popcounts of the mask, and
+// the lanes emit the jobs of 32 slots at a time with no sequential walk.
 // ------------------------------------------------------------------------------------------
 
-constexpr uint32_t kNewRef = 0x80000000u;  // converted ref: a new node (k in bits 8..), not a slot
+constexpr uint32_t kReachSlots = 256;
+constexpr uint32_t kReachWords = kReachSlots / 32;  // words per reach row
 
-template <int BT, int W>
-__global__ void __launch_bounds__(BT) k_dirty_slots(VArgs A) {  // parents of <= 32 W - 2 nodes
-  __shared__ uint32_t sm_d[W * BT];  // dirty slots
-  __shared__ uint32_t sm_r[W * BT];  // removed parent ranks
+// offset (words) of the parent's reach rows inside its pscratch row (after k_match's tables)
+__device__ __forceinline__ uint64_t reach_off(const Geo& G) { return 10ull * G.cap_nodes + 1 + 2ull * G.cap_refs; }
+
+// one warp per parent; dynamic shared memory per warp: s_v[256], coff[257], consumer slots
+// [max refs], rows [256 x 8]
+__global__ void __launch_bounds__(64) k_reach(StepArgs A, uint32_t rmax) {
+  extern __shared__ uint32_t sh_reach[];
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  const uint32_t per = 256 + 260 + ((rmax + 3) & ~3u) + kReachSlots * kReachWords;
+  uint32_t* sv = sh_reach + wid * per;
+  uint32_t* cof = sv + 256;
+  uint32_t* cls = cof + 260;
+  uint32_t* rows = cls + ((rmax + 3) & ~3u);
   const Geo& G = A.g;
-  const uint32_t span = (A.n + 31) / 32 * 32;
-  for (uint32_t lc = blockIdx.x * blockDim.x + threadIdx.x; lc < span; lc += gridDim.x * blockDim.x) {
+  for (uint32_t pi = blockIdx.x * 2 + wid; pi < A.n_parents; pi += gridDim.x * 2) {
+    Rec R{reinterpret_cast<char*>(A.parent_addr[pi])};
+    const int n = R.h().n;
+    const uint32_t* ps = A.pscratch + (uint64_t)pi * A.pstride;
+    const uint32_t* coff = ps + 2 * G.cap_nodes;
+    const uint32_t* clist = coff + 2 * G.cap_nodes + 1;
+    const uint32_t* tslot = clist + G.cap_refs;
+    const uint32_t* s_v = tslot + G.cap_nodes;
+    const uint32_t ncons = coff[n];
+    for (int i = lane; i < n; i += 32) sv[i] = s_v[i];
+    for (int i = lane; i <= n; i += 32) cof[i] = coff[i];
+    for (uint32_t x = lane; x < ncons; x += 32) cls[x] = tslot[clist[x]];
+    __syncwarp();
+    // reverse topological order; lane w owns word w of every row, so there is no cross-lane
+    // dependency: a row only reads rows of later slots, written by the same lane
+    const int nw = (n + 31) >> 5;
+    if ((int)lane < nw) {
+      for (int s = n - 1; s >= 0; --s) {
+        const uint32_t v = sv[s];
+        uint32_t acc = ((s >> 5) == (int)lane) ? 1u << (s & 31) : 0u;
+        for (uint32_t x = cof[v]; x < cof[v + 1]; ++x) acc |= rows[cls[x] * kReachWords + lane];
+        rows[s * kReachWords + lane] = acc;
+      }
+    }
+    __syncwarp();
+    uint32_t* out = A.pscratch + (uint64_t)pi * A.pstride + reach_off(G);
+    for (int i = lane; i < n * (int)kReachWords; i += 32) out[i] = rows[i];
+    __syncwarp();
+  }
+}
+
+// position of the r-th (0-based) set bit of x (r < popc(x))
+__device__ __forceinline__ uint32_t nth_bit(uint32_t x, uint32_t r) {
+  uint32_t pos = 0, c;
+  c = __popc(x & 0xffffu);
+  if (r >= c) { r -= c; x >>= 16; pos += 16; }
+  c = __popc(x & 0xffu);
+  if (r >= c) { r -= c; x >>= 8; pos += 8; }
+  c = __popc(x & 0xfu);
+  if (r >= c) { r -= c; x >>= 4; pos += 4; }
+  c = __popc(x & 0x3u);
+  if (r >= c) { r -= c; x >>= 2; pos += 2; }
+  c = x & 1u;
+  if (r >= c) pos += 1;
+  return pos;
+}
+
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_dirty_warp(VArgs A) {
+  __shared__ uint32_t sh_dm[WARPS][kReachWords], sh_cum[WARPS][kReachWords + 1], sh_rk[WARPS][kReachWords];
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  uint32_t* dm = sh_dm[wid];
+  uint32_t* cum = sh_cum[wid];
+  uint32_t* rk = sh_rk[wid];
+  const Geo& G = A.g;
+  for (uint32_t lc = blockIdx.x * WARPS + wid; lc < A.n; lc += gridDim.x * WARPS) {  // warp-uniform
     const uint32_t c = A.c0 + lc;
-    const bool incomplete = lc >= A.n || (A.res[c].flags & EF_F_INCOMPLETE);
-    const unsigned mask = __ballot_sync(0xffffffffu, !incomplete);
-    if (incomplete) {
-      if (lc < A.n) {
+    if (A.res[c].flags & EF_F_INCOMPLETE) {
+      if (lane == 0) {
         A.dcount[lc] = 0;
         A.seg_begin[lc] = A.seg_end[lc] = (int32_t)((uint64_t)lc * A.S);
       }
@@ -303,110 +371,125 @@ __global__ void __launch_bounds__(BT) k_dirty_slots(VArgs A) {  // parents of <=
     const VPlan P = A.plan[c];
     Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
     const uint32_t* ps = A.pscratch + (uint64_t)P.parent * A.pstride;
-    const uint32_t* tslot = ps + 4 * G.cap_nodes + 1 + G.cap_refs;
+    const uint32_t* coff = ps + 2 * G.cap_nodes;
+    const uint32_t* clist = coff + 2 * G.cap_nodes + 1;
+    const uint32_t* tslot = clist + G.cap_refs;
     const uint32_t* s_v = tslot + G.cap_nodes;
     const uint32_t* s_pk = s_v + G.cap_nodes;
     const uint32_t* rslot = s_pk + G.cap_nodes;
+    const uint32_t* reach = ps + reach_off(G);
     const uint32_t* psig = R.sig(G);
     const uint32_t* paux = R.aux(G);
+    const uint32_t* pinoff = R.inoff(G);
+    const uint32_t* pnin = R.nin(G);
     const uint32_t* prefs = R.refs(G);
     const uint32_t* srank = R.srank(G);
     const int pn = P.pn;
     const int nw = (pn + 31) >> 5;
-    uint32_t* dm = sm_d + threadIdx.x;
-    uint32_t* rk = sm_r + threadIdx.x;
-    for (int w = 0; w < nw; ++w) {
-      dm[w * BT] = 0;
-      rk[w * BT] = 0;
+    if (lane < kReachWords) dm[lane] = rk[lane] = 0;
+    __syncwarp();
+    // seeds: the node rewritten in place, the owners of remapped refs (dropped nodes excluded)
+    const int ms = P.mod >= 0 ? (int)tslot[P.mod] : -1;
+    const int ds0 = P.drop0 >= 0 ? (int)tslot[P.drop0] : -1, ds1 = P.drop1 >= 0 ? (int)tslot[P.drop1] : -1;
+    auto seed = [&](uint32_t t) {
+      for (int w = 0; w < nw; ++w) atomicOr(&dm[w], reach[t * kReachWords + w]);
+    };
+    if (ms >= 0 && lane == 0) seed((uint32_t)ms);
+    uint32_t rf[2] = {0xffffffffu, 0xffffffffu};
+    for (int k = 0; k < P.n_rm; ++k) {
+      const uint32_t from = P.rm_from[k], p = from >> 8;
+      rf[k] = (tslot[p] << 8) | (from & 255u);
+      for (uint32_t x = coff[p] + lane; x < coff[p + 1]; x += 32) {
+        const uint32_t q = clist[x];
+        if ((int)q == P.drop0 || (int)q == P.drop1) continue;
+        bool hit = false;
+        for (uint32_t r = pinoff[q]; r < pinoff[q] + pnin[q]; ++r) hit |= prefs[r] == from;
+        if (hit) seed(tslot[q]);
+      }
     }
-    Job* jobs = A.jobs + (uint64_t)lc * A.S;
-    uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
-    auto remove = [&](uint32_t v) {
-      const uint32_t k = srank[v];
-      rk[(k >> 5) * BT] |= 1u << (k & 31);
-    };
-    auto dirty_at = [&](uint32_t t) -> bool { return (dm[(t >> 5) * BT] >> (t & 31)) & 1u; };
-    auto popc_below = [&](uint32_t t) -> uint32_t {
-      uint32_t x = 0;
-      for (uint32_t w = 0; w < (t >> 5); ++w) x += __popc(dm[w * BT]);
-      return x + __popc(dm[(t >> 5) * BT] & ((1u << (t & 31)) - 1u));
-    };
+    __syncwarp();
+    if (lane == 0) {
+      if (ds0 >= 0) dm[ds0 >> 5] &= ~(1u << (ds0 & 31));
+      if (ds1 >= 0) dm[ds1 >> 5] &= ~(1u << (ds1 & 31));
+    }
+    __syncwarp();
+    {  // exclusive prefix popcounts of the mask words
+      const uint32_t x = lane < (uint32_t)nw ? (uint32_t)__popc(dm[lane]) : 0u;
+      uint32_t inc = x;
+#pragma unroll
+      for (int o = 1; o < (int)kReachWords; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if ((int)lane >= o) inc += y;
+      }
+      if (lane < kReachWords) cum[lane] = inc - x;
+      if (lane == kReachWords - 1) cum[kReachWords] = inc;
+    }
+    __syncwarp();
     const int ins = P.ins_slot;
+    auto popc_below = [&](uint32_t t) -> uint32_t {
+      return cum[t >> 5] + __popc(dm[t >> 5] & ((1u << (t & 31)) - 1u));
+    };
+    auto dirty_at = [&](uint32_t t) -> bool { return (dm[t >> 5] >> (t & 31)) & 1u; };
     auto fidx = [&](uint32_t t) -> uint32_t { return popc_below(t) + ((int)t > ins && ins >= 0 ? P.n_live : 0); };
     auto fnew = [&](int k) -> uint32_t {
-      const uint32_t base = popc_below((uint32_t)(ins + (P.ins_after ? 1 : 0)));
-      return base + (k == 1 ? (uint32_t)P.live[0] : 0u);
+      return popc_below((uint32_t)(ins + (P.ins_after ? 1 : 0))) + (k == 1 ? (uint32_t)P.live[0] : 0u);
     };
-    // a ref in parent-position space -> key source
-    auto src_pos = [&](uint32_t ref) -> uint32_t {
+    auto src_pos = [&](uint32_t ref) -> uint32_t {  // a ref in parent-position space -> key source
       const uint32_t p = ref >> 8, port = ref & 255u;
       if ((int)p >= pn) return kFresh | (port << 23) | fnew((int)p - pn);
       const uint32_t t = tslot[p];
       return dirty_at(t) ? (kFresh | (port << 23) | fidx(t)) : ((port << 23) | p);
     };
-    if (P.drop0 >= 0) remove(P.drop0);
-    if (P.drop1 >= 0) remove(P.drop1);
-    // remaps in slot space (sources are always parent edges)
-    uint32_t rf[2] = {0xffffffffu, 0xffffffffu};
-    for (int k = 0; k < P.n_rm; ++k) rf[k] = (tslot[P.rm_from[k] >> 8] << 8) | (P.rm_from[k] & 255u);
-    const int ms = P.mod >= 0 ? (int)tslot[P.mod] : -1;
-    const int ds0 = P.drop0 >= 0 ? (int)tslot[P.drop0] : -1, ds1 = P.drop1 >= 0 ? (int)tslot[P.drop1] : -1;
-    uint32_t j = 0, r = 0;
-    auto emit_new = [&]() {
-      for (int k = 0; k < 2; ++k) {
-        if (!P.live[k]) continue;
-        rs[r] = src_pos(P.new_ref[k]);  // new nodes are exempt from the remap (rules.py:186-188)
-        jobs[j] = Job{P.new_sig[k], P.new_aux[k], r, 1u};
-        r += 1;
-        ++j;
-      }
-    };
-    const int s_lo = (int)__reduce_min_sync(mask, (unsigned)P.first);
-    const int s_hi = (int)__reduce_max_sync(mask, (unsigned)pn);
-    for (int s = s_lo; s < s_hi; ++s) {
-      if (s < P.first || s >= pn) continue;
-      if (s == ds0 || s == ds1) {
-        if (s == ins && !P.ins_after) emit_new();
-        continue;
-      }
-      const uint32_t v = s_v[s], pk = s_pk[s];
+    Job* jobs = A.jobs + (uint64_t)lc * A.S;
+    uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
+    // jobs of the dirty slots: lane q takes the q-th dirty slot (32 jobs per round); a job's
+    // sources sit at its parent ref offset
+    const uint32_t nd = cum[kReachWords];
+    for (uint32_t q = lane; q < nd; q += 32) {
+      uint32_t w = 0;
+      while (cum[w + 1] <= q) ++w;
+      const uint32_t t = 32u * w + nth_bit(dm[w], q - cum[w]);
+      const uint32_t v = s_v[t], pk = s_pk[t];
       const uint32_t r0 = pk & 0xffffffu, nr = pk >> 24;
-      bool dirty = s == ms;
       for (uint32_t k = 0; k < nr; ++k) {
         const uint32_t rsl = rslot[r0 + k];
         uint32_t sv;
         if (rsl == rf[0] || rsl == rf[1]) {  // the owner now consumes another producer (a remap)
           sv = src_pos(rsl == rf[0] ? P.rm_to[0] : P.rm_to[1]);
-          dirty = true;
         } else {
-          const uint32_t t = rsl >> 8, port = rsl & 255u;
-          if (dirty_at(t)) {
-            sv = kFresh | (port << 23) | fidx(t);
-            dirty = true;
-          } else {
-            sv = (port << 23) | (prefs[r0 + k] >> 8);
-          }
+          const uint32_t tp = rsl >> 8, port = rsl & 255u;
+          sv = dirty_at(tp) ? (kFresh | (port << 23) | fidx(tp)) : ((port << 23) | (prefs[r0 + k] >> 8));
         }
-        rs[r + k] = sv;
+        rs[r0 + k] = sv;
       }
-      if (dirty) {
-        jobs[j] = Job{s == ms ? P.mod_sig : psig[v], s == ms ? P.mod_aux : paux[v], r, nr};
-        r += nr;
-        ++j;
-        dm[(s >> 5) * BT] |= 1u << (s & 31);
-        remove(v);
-      }
-      if (s == ins && P.ins_after) emit_new();
+      const bool m = (int)t == ms;
+      jobs[q + ((int)t > ins && ins >= 0 ? P.n_live : 0)] = Job{m ? P.mod_sig : psig[v], m ? P.mod_aux : paux[v], r0, nr};
+      const uint32_t k = srank[v];
+      atomicOr(&rk[k >> 5], 1u << (k & 31));
+    }
+    const uint32_t pref = R.h().n_refs;
+    if (lane < 2 && P.live[lane]) {  // the new nodes, exempt from the remap (rules.py:186-188)
+      rs[pref + lane] = src_pos(P.new_ref[lane]);
+      jobs[fnew((int)lane)] = Job{P.new_sig[lane], P.new_aux[lane], pref + lane, 1u};
+    }
+    if (lane == 0) {
+      if (P.drop0 >= 0) atomicOr(&rk[srank[P.drop0] >> 5], 1u << (srank[P.drop0] & 31));
+      if (P.drop1 >= 0) atomicOr(&rk[srank[P.drop1] >> 5], 1u << (srank[P.drop1] & 31));
     }
     // graph outputs (remapped) -> key sources, for the digest
     const uint32_t* pouts = R.outs(G);
     uint32_t* os = A.outsrc + (uint64_t)lc * A.Os;
-    for (int o = 0; o < R.h().n_out; ++o) os[o] = src_pos(vremap(P, pouts[o]));
+    for (int o = lane; o < R.h().n_out; o += 32) os[o] = src_pos(vremap(P, pouts[o]));
+    __syncwarp();
     uint32_t* grm = A.rmask + (uint64_t)lc * A.W;
-    for (int w = 0; w < nw; ++w) grm[w] = rk[w * BT];
-    A.dcount[lc] = j;
-    A.seg_begin[lc] = (int32_t)((uint64_t)lc * A.S);
-    A.seg_end[lc] = (int32_t)((uint64_t)lc * A.S + j);
+    if ((int)lane < nw) grm[lane] = rk[lane];
+    if (lane == 0) {
+      const uint32_t j = cum[kReachWords] + (uint32_t)P.n_live;
+      A.dcount[lc] = j;
+      A.seg_begin[lc] = (int32_t)((uint64_t)lc * A.S);
+      A.seg_end[lc] = (int32_t)((uint64_t)lc * A.S + j);
+    }
+    __syncwarp();
   }
 }
 
@@ -467,8 +550,22 @@ __device__ __forceinline__ void b2b_start(uint64_t* h, int outlen) {
 }
 
 // node key of a job too long for the fast path (rare: many-input concats); streaming BLAKE2b
-__device__ __noinline__ void job_key_slow(const Tables& T, const Job jb, const uint32_t* rs, const uint64_t* pkeys,
-                                          const uint64_t* fresh, uint64_t* out) {
+struct TextTables {  // what job_key_slow reads, by value (a Tables& copies the parameter block to the stack)
+  const uint8_t* sig_text;
+  const uint32_t *sig_text_off, *sig_text_len;
+  const uint8_t* names;
+  const uint32_t *name_off, *name_len;
+  const uint64_t* ws_digest;
+};
+__device__ __forceinline__ TextTables text_tables(const Tables& T) {
+  return TextTables{T.sig_text, T.sig_text_off, T.sig_text_len, T.names, T.name_off, T.name_len, T.ws_digest};
+}
+struct Key128 {
+  uint64_t a, b;
+};
+
+__device__ __noinline__ Key128 job_key_slow(const TextTables T, const Job jb, const uint32_t* rs, const uint64_t* pkeys,
+                                            const uint64_t* fresh) {
   B2b st;
   st.init(16);
   const uint32_t off = T.sig_text_off[jb.sig], len = T.sig_text_len[jb.sig];
@@ -493,8 +590,7 @@ __device__ __noinline__ void job_key_slow(const Tables& T, const Job jb, const u
     st.u16_be(port);
   }
   st.final();
-  out[0] = st.h[0];
-  out[1] = st.h[1];
+  return Key128{st.h[0], st.h[1]};
 }
 
 // ------------------------------------------------------------------------------------------
@@ -529,7 +625,9 @@ __global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
       const uint32_t len = tlen + nlen + 16u + 18u * nin;
       uint64_t h[8];
       if (len > 8u * kKeyMaxW) {
-        job_key_slow(T, jb, rs, pkeys, fresh, h);
+        const Key128 ks = job_key_slow(text_tables(T), jb, rs, pkeys, fresh);
+        h[0] = ks.a;
+        h[1] = ks.b;
       } else {
         WordSink<BT> sk;
         sk.init(col);
@@ -727,10 +825,9 @@ __global__ void __launch_bounds__(BT) k_keys_quad(VArgs A) {
         const uint32_t nlen = input ? T.name_len[jb.aux] : 0u;
         len = tlen + nlen + 16u + 18u * nin;
         if (len > 8u * kKeyMaxW) {
-          uint64_t hs[8];
-          job_key_slow(T, jb, rs, pkeys, fresh, hs);
-          sh0 = hs[0];
-          sh1 = hs[1];
+          const Key128 ks = job_key_slow(text_tables(T), jb, rs, pkeys, fresh);
+          sh0 = ks.a;
+          sh1 = ks.b;
           slow = true;
         } else {
           WordSink<QN> sk;

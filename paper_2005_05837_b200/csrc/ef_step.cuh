@@ -543,6 +543,43 @@ struct WordSink {
 
 __device__ __forceinline__ uint64_t port_be(uint32_t port) { return (uint64_t)((port >> 8) & 255u) | ((uint64_t)(port & 255u) << 8); }
 
+// Message of a non-input job with <= 2 inputs, written straight into the column: the text
+// words (8-byte aligned, zero padded in the table) are copied, and the suffix
+//   digest[16] | key0[16] port0[2] | key1[16] port1[2]
+// is built as aligned words in registers and funnel-shifted by the text's tail length.
+// Returns the number of words written (ceil(len / 8)).
+template <int BT>
+__device__ __forceinline__ uint32_t msg_fast(uint64_t* col, const uint64_t* tw, uint32_t tlen, uint64_t d0, uint64_t d1,
+                                             uint32_t nin, uint64_t k00, uint64_t k01, uint32_t p0, uint64_t k10,
+                                             uint64_t k11, uint32_t p1) {
+  const uint32_t fw = tlen >> 3, r = tlen & 7u;
+#pragma unroll 4
+  for (uint32_t i = 0; i < fw; ++i) col[i * BT] = __ldg(tw + i);
+  uint64_t sw[7];
+  sw[0] = d0;
+  sw[1] = d1;
+  sw[2] = nin > 0 ? k00 : 0;
+  sw[3] = nin > 0 ? k01 : 0;
+  const uint64_t pb0 = nin > 0 ? port_be(p0) : 0, pb1 = nin > 1 ? port_be(p1) : 0;
+  const uint64_t a0 = nin > 1 ? k10 : 0, a1 = nin > 1 ? k11 : 0;
+  sw[4] = pb0 | (a0 << 16);
+  sw[5] = (a0 >> 48) | (a1 << 16);
+  sw[6] = (a1 >> 48) | (pb1 << 16);
+  const uint32_t len = tlen + 16u + 18u * nin;
+  const uint32_t nout = ((len + 7u) >> 3) - fw;  // words from the tail word on
+  const uint64_t tail = r ? __ldg(tw + fw) : 0ull;
+  const uint32_t sl = 8u * r, sr = 64u - sl;
+#pragma unroll
+  for (uint32_t j = 0; j < 8; ++j) {
+    if (j < nout) {
+      const uint64_t lo = j == 0 ? tail : (r ? sw[j - 1] >> sr : 0ull);
+      const uint64_t hi = j < 7 ? sw[j] << sl : 0ull;
+      col[(fw + j) * BT] = lo | hi;
+    }
+  }
+  return fw + nout;
+}
+
 __device__ __forceinline__ void b2b_start(uint64_t* h, int outlen) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) h[i] = b2b_iv(i);
@@ -629,23 +666,11 @@ __global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
         h[0] = ks.a;
         h[1] = ks.b;
       } else {
-        WordSink<BT> sk;
-        sk.init(col);
         const uint64_t* tw = reinterpret_cast<const uint64_t*>(T.sig_text + T.sig_text_off[jb.sig]);
-        const uint32_t full = tlen >> 3;
-        for (uint32_t i = 0; i < full; ++i) sk.push(__ldg(tw + i), 8);
-        if (tlen & 7u) sk.push(__ldg(tw + full), tlen & 7u);
         const uint32_t ws = input ? kEmptyWset : jb.aux;
-        if (input) {  // graph.py:534-535: the input's name follows its signature text
-          const uint8_t* nm = T.names + T.name_off[jb.aux];
-          for (uint32_t i = 0; i < nlen; ++i) sk.push(nm[i], 1);
-        }
-        sk.push(__ldg(T.ws_digest + 2 * ws), 8);
-        sk.push(__ldg(T.ws_digest + 2 * ws + 1), 8);
-        for (uint32_t k = 0; k < nin; ++k) {
+        auto src = [&](uint32_t k, uint64_t& k0, uint64_t& k1) -> uint32_t {
           const uint32_t sv = rs[jb.roff + k];
-          const uint32_t idx = sv & 0x7fffffu, port = (sv >> 23) & 255u;
-          uint64_t k0, k1;
+          const uint32_t idx = sv & 0x7fffffu;
           if ((sv & kFresh) && idx + 1 == jj) {  // the previous job's key, still in registers
             k0 = last0;
             k1 = last1;
@@ -654,13 +679,40 @@ __global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
             k0 = kp[0];
             k1 = kp[1];
           }
-          sk.push(k0, 8);
-          sk.push(k1, 8);
-          sk.push(port_be(port), 2);
+          return (sv >> 23) & 255u;
+        };
+        uint32_t nw;
+        if (!input && nin <= 2u) {
+          uint64_t k00 = 0, k01 = 0, k10 = 0, k11 = 0;
+          uint32_t p0 = 0, p1 = 0;
+          if (nin > 0u) p0 = src(0, k00, k01);
+          if (nin > 1u) p1 = src(1, k10, k11);
+          nw = msg_fast<BT>(col, tw, tlen, __ldg(T.ws_digest + 2 * ws), __ldg(T.ws_digest + 2 * ws + 1), nin, k00, k01,
+                            p0, k10, k11, p1);
+        } else {
+          WordSink<BT> sk;
+          sk.init(col);
+          const uint32_t full = tlen >> 3;
+          for (uint32_t i = 0; i < full; ++i) sk.push(__ldg(tw + i), 8);
+          if (tlen & 7u) sk.push(__ldg(tw + full), tlen & 7u);
+          if (input) {  // graph.py:534-535: the input's name follows its signature text
+            const uint8_t* nm = T.names + T.name_off[jb.aux];
+            for (uint32_t i = 0; i < nlen; ++i) sk.push(nm[i], 1);
+          }
+          sk.push(__ldg(T.ws_digest + 2 * ws), 8);
+          sk.push(__ldg(T.ws_digest + 2 * ws + 1), 8);
+          for (uint32_t k = 0; k < nin; ++k) {
+            uint64_t k0, k1;
+            const uint32_t port = src(k, k0, k1);
+            sk.push(k0, 8);
+            sk.push(k1, 8);
+            sk.push(port_be(port), 2);
+          }
+          sk.flush();
+          nw = sk.q;
         }
-        sk.flush();
         const uint32_t nb = (len + 127u) >> 7;
-        for (uint32_t q = sk.q; q < 16u * nb; ++q) col[q * BT] = 0;
+        for (uint32_t q = nw; q < 16u * nb; ++q) col[q * BT] = 0;
         b2b_start(h, 16);
         ncomp += nb;
         for (uint32_t b = 0; b < nb; ++b)
@@ -762,6 +814,16 @@ __global__ void __launch_bounds__(WARPS * 32) k_sortkeys(VArgs A) {
 // is assembled by the quad's lane 0 into the quad's shared-memory column.
 // ------------------------------------------------------------------------------------------
 
+// message-word indices of quad lane q in round r: bits [16k + 4q, +4) of kQuadSigma[r % 10]
+// are sigma[r][2q + {0, 1, 8, 9}[k]] (the column and diagonal G's of the lane)
+__constant__ uint64_t kQuadSigma[10] = {
+    0xfdb9eca875316420ull, 0x372c5b016f8ad94eull, 0x416e973ad208f5cbull, 0x80a6f452ec19bd37ull,
+    0xd8c136bef470a259ull, 0x9e5d1f743bac8062ull, 0xb2378960adf54e1cull, 0xa64028f591eb3c7dull,
+    0x5472a1dc839f0be6ull, 0x0cebd39f5642178aull};
+
+// One compression by the 4 lanes of a quad (lane q runs column G q and diagonal G q, the
+// state rotates between them by shuffles).  The rounds are unrolled with the lane's message
+// words of round r + 1 loaded during round r, so the chain is the G's and the shuffles only.
 template <int QN>
 __device__ __forceinline__ void b2b_compress_quad(uint64_t& h0, uint64_t& h1, const uint64_t* col, uint64_t t,
                                                   bool last, int q, int qbase) {
@@ -769,11 +831,25 @@ __device__ __forceinline__ void b2b_compress_quad(uint64_t& h0, uint64_t& h1, co
   if (q == 0) d ^= t;
   if (q == 2 && last) d = ~d;
   const unsigned full = 0xffffffffu;
-#pragma unroll 1
+  const uint32_t sh = 4u * (uint32_t)q;
+  uint64_t x0, y0, x1, y1;
+  {
+    const uint64_t w = 0xfdb9eca875316420ull >> sh;
+    x0 = col[(w & 15u) * QN];
+    y0 = col[((w >> 16) & 15u) * QN];
+    x1 = col[((w >> 32) & 15u) * QN];
+    y1 = col[((w >> 48) & 15u) * QN];
+  }
+#pragma unroll
   for (int r = 0; r < 12; ++r) {
-    const uint8_t* s = kB2bSigma[r < 10 ? r : r - 10];
-    const uint64_t x0 = col[s[2 * q] * QN], y0 = col[s[2 * q + 1] * QN];
-    const uint64_t x1 = col[s[8 + 2 * q] * QN], y1 = col[s[9 + 2 * q] * QN];
+    uint64_t nx0 = 0, ny0 = 0, nx1 = 0, ny1 = 0;
+    if (r + 1 < 12) {
+      const uint64_t w = kQuadSigma[(r + 1) % 10] >> sh;
+      nx0 = col[(w & 15u) * QN];
+      ny0 = col[((w >> 16) & 15u) * QN];
+      nx1 = col[((w >> 32) & 15u) * QN];
+      ny1 = col[((w >> 48) & 15u) * QN];
+    }
     EF_B2B_G(a, b, c, d, x0, y0);
     b = __shfl_sync(full, b, qbase | ((q + 1) & 3));
     c = __shfl_sync(full, c, qbase | ((q + 2) & 3));
@@ -782,10 +858,24 @@ __device__ __forceinline__ void b2b_compress_quad(uint64_t& h0, uint64_t& h1, co
     b = __shfl_sync(full, b, qbase | ((q + 3) & 3));
     c = __shfl_sync(full, c, qbase | ((q + 2) & 3));
     d = __shfl_sync(full, d, qbase | ((q + 1) & 3));
+    x0 = nx0;
+    y0 = ny0;
+    x1 = nx1;
+    y1 = ny1;
   }
   h0 ^= a ^ c;
   h1 ^= b ^ d;
 }
+
+// what lane 0 of a quad knows about a job before assembling its message: fetched one job
+// ahead, so the dependent loads (descriptor -> text metadata / key sources -> producer keys)
+// run under the previous job's compression
+struct QuadJob {
+  Job jb;
+  uint32_t tlen, toff;
+  uint32_t sv0, sv1;            // key sources of inputs 0 and 1
+  uint64_t k00, k01, k10, k11;  // their keys, unless they are the previous job's
+};
 
 template <int BT>
 __global__ void __launch_bounds__(BT) k_keys_quad(VArgs A) {
@@ -810,6 +900,34 @@ __global__ void __launch_bounds__(BT) k_keys_quad(VArgs A) {
     uint64_t* fresh = A.fresh + 2ull * lc * A.S;
     uint64_t* skey = A.skey + (uint64_t)lc * A.S;
     uint32_t* sval = A.sval + (uint64_t)lc * A.S;
+    auto key_of = [&](uint32_t sv, uint64_t& k0, uint64_t& k1) {
+      const uint32_t idx = sv & 0x7fffffu;
+      const uint64_t* kp = (sv & kFresh) ? fresh + 2 * idx : pkeys + 2 * idx;
+      k0 = kp[0];
+      k1 = kp[1];
+    };
+    auto fwd = [](uint32_t sv, uint32_t j) { return (sv & kFresh) && (sv & 0x7fffffu) + 1 == j; };
+    auto stage1 = [&](QuadJob& J, const Job jb) {  // descriptor -> text metadata + key sources
+      J.jb = jb;
+      J.tlen = T.sig_text_len[jb.sig];
+      J.toff = T.sig_text_off[jb.sig];
+      const uint32_t nin = (jb.nin & kInputJob) ? 0u : jb.nin;
+      J.sv0 = nin > 0 ? rs[jb.roff] : 0u;
+      J.sv1 = nin > 1 ? rs[jb.roff + 1] : 0u;
+    };
+    auto stage2 = [&](QuadJob& J, uint32_t j) {  // producer keys other than job j - 1's
+      const uint32_t nin = (J.jb.nin & kInputJob) ? 0u : J.jb.nin;
+      J.k00 = J.k01 = J.k10 = J.k11 = 0;
+      if (nin > 0 && !fwd(J.sv0, j)) key_of(J.sv0, J.k00, J.k01);
+      if (nin > 1 && !fwd(J.sv1, j)) key_of(J.sv1, J.k10, J.k11);
+    };
+    QuadJob cur{}, nxt{};
+    Job jnext{};
+    if (q == 0 && d > 0) {
+      stage1(cur, jobs[0]);
+      stage2(cur, 0);
+      if (d > 1) jnext = jobs[1];
+    }
     uint64_t last0 = 0, last1 = 0;
     uint32_t ncomp = 0;
     for (uint32_t jj = 0; jj < dmax; ++jj) {
@@ -818,12 +936,22 @@ __global__ void __launch_bounds__(BT) k_keys_quad(VArgs A) {
       bool slow = false;
       uint64_t sh0 = 0, sh1 = 0;
       if (act && q == 0) {
-        const Job jb = jobs[jj];
-        const uint32_t tlen = T.sig_text_len[jb.sig];
+        const Job jb = cur.jb;
         const bool input = jb.nin & kInputJob;
         const uint32_t nin = input ? 0u : jb.nin;
+        if (nin > 0 && fwd(cur.sv0, jj)) {
+          cur.k00 = last0;
+          cur.k01 = last1;
+        }
+        if (nin > 1 && fwd(cur.sv1, jj)) {
+          cur.k10 = last0;
+          cur.k11 = last1;
+        }
+        const bool more = jj + 1 < d;
+        if (more) stage1(nxt, jnext);
+        if (jj + 2 < d) jnext = jobs[jj + 2];
         const uint32_t nlen = input ? T.name_len[jb.aux] : 0u;
-        len = tlen + nlen + 16u + 18u * nin;
+        len = cur.tlen + nlen + 16u + 18u * nin;
         if (len > 8u * kKeyMaxW) {
           const Key128 ks = job_key_slow(text_tables(T), jb, rs, pkeys, fresh);
           sh0 = ks.a;
@@ -832,10 +960,10 @@ __global__ void __launch_bounds__(BT) k_keys_quad(VArgs A) {
         } else {
           WordSink<QN> sk;
           sk.init(col);
-          const uint64_t* tw = reinterpret_cast<const uint64_t*>(T.sig_text + T.sig_text_off[jb.sig]);
-          const uint32_t fullw = tlen >> 3;
+          const uint64_t* tw = reinterpret_cast<const uint64_t*>(T.sig_text + cur.toff);
+          const uint32_t fullw = cur.tlen >> 3;
           for (uint32_t i = 0; i < fullw; ++i) sk.push(__ldg(tw + i), 8);
-          if (tlen & 7u) sk.push(__ldg(tw + fullw), tlen & 7u);
+          if (cur.tlen & 7u) sk.push(__ldg(tw + fullw), cur.tlen & 7u);
           const uint32_t ws = input ? kEmptyWset : jb.aux;
           if (input) {
             const uint8_t* nm = T.names + T.name_off[jb.aux];
@@ -844,25 +972,34 @@ __global__ void __launch_bounds__(BT) k_keys_quad(VArgs A) {
           sk.push(__ldg(T.ws_digest + 2 * ws), 8);
           sk.push(__ldg(T.ws_digest + 2 * ws + 1), 8);
           for (uint32_t k = 0; k < nin; ++k) {
-            const uint32_t sv = rs[jb.roff + k];
-            const uint32_t idx = sv & 0x7fffffu, port = (sv >> 23) & 255u;
             uint64_t k0, k1;
-            if ((sv & kFresh) && idx + 1 == jj) {
-              k0 = last0;
-              k1 = last1;
+            uint32_t sv;
+            if (k == 0) {
+              sv = cur.sv0;
+              k0 = cur.k00;
+              k1 = cur.k01;
+            } else if (k == 1) {
+              sv = cur.sv1;
+              k0 = cur.k10;
+              k1 = cur.k11;
             } else {
-              const uint64_t* kp = (sv & kFresh) ? fresh + 2 * idx : pkeys + 2 * idx;
-              k0 = kp[0];
-              k1 = kp[1];
+              sv = rs[jb.roff + k];
+              if (fwd(sv, jj)) {
+                k0 = last0;
+                k1 = last1;
+              } else {
+                key_of(sv, k0, k1);
+              }
             }
             sk.push(k0, 8);
             sk.push(k1, 8);
-            sk.push(port_be(port), 2);
+            sk.push(port_be((sv >> 23) & 255u), 2);
           }
           sk.flush();
           nb = (len + 127u) >> 7;
           for (uint32_t w = sk.q; w < 16u * nb; ++w) col[w * QN] = 0;
         }
+        if (more) stage2(nxt, jj + 1);  // its loads run under the compression below
       }
       // broadcast the job shape within the quad, then compress cooperatively
       nb = __shfl_sync(0xffffffffu, nb, qbase);
@@ -899,6 +1036,7 @@ __global__ void __launch_bounds__(BT) k_keys_quad(VArgs A) {
         skey[jj] = B2b::bswap64(k0);
         sval[jj] = jj;
         ncomp += slow ? 0u : nb;
+        if (jj + 1 < d) cur = nxt;
       }
       last0 = k0;
       last1 = k1;

@@ -25,6 +25,18 @@
 #pragma once
 #include "ef_kernels.cuh"
 
+// minimum resident CTAs per SM for the step's throughput kernels (register budgets; tuned on
+// the ResNet-50 frontier)
+#ifndef EF_MERGE_MINB
+#define EF_MERGE_MINB 6
+#endif
+#ifndef EF_DIGEST_MINB
+#define EF_DIGEST_MINB 4
+#endif
+#ifndef EF_KEYS_MINB
+#define EF_KEYS_MINB 4
+#endif
+
 namespace ef {
 
 constexpr uint32_t kFresh = 0x80000000u;  // refsrc: key comes from the candidate's fresh keys
@@ -635,7 +647,7 @@ __device__ __noinline__ Key128 job_key_slow(const TextTables T, const Job jb, co
 // ------------------------------------------------------------------------------------------
 
 template <int BT>
-__global__ void __launch_bounds__(BT, 4) k_keys(VArgs A) {
+__global__ void __launch_bounds__(BT, EF_KEYS_MINB) k_keys(VArgs A) {
   __shared__ uint64_t msg[kKeyMaxW * BT];
   const Geo& G = A.g;
   const Tables& T = A.T;
@@ -1353,7 +1365,7 @@ __device__ __forceinline__ bool warp_sort_fresh_smem(const uint64_t* fresh, uint
 
 // dynamic shared memory: per warp two arrays of `rows` keys (A = parent, B = fresh)
 template <int KMAX, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_merge(VArgs A, uint32_t rows) {
+__global__ void __launch_bounds__(WARPS * 32, EF_MERGE_MINB) k_merge(VArgs A, uint32_t rows) {
   extern __shared__ __align__(16) uint64_t merge_smem[];
   const Geo& G = A.g;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1439,7 +1451,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge(VArgs A, uint32_t rows) {
 // and ports) goes through the word sink; the keys follow as full words with a constant byte
 // shift, loaded 16 words per block with independent 16-byte loads.
 template <int BT>
-__global__ void __launch_bounds__(BT) k_digest_pm(VArgs A) {
+__global__ void __launch_bounds__(BT, EF_DIGEST_MINB) k_digest_pm(VArgs A) {
   __shared__ uint64_t blk[16 * BT];
   const Geo& G = A.g;
   const Tables& T = A.T;

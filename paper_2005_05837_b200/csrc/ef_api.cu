@@ -84,6 +84,7 @@ struct ef_ctx {
   cudaStream_t st = nullptr;
   std::string err;
   int n_sm = 148;
+  uint64_t chunk_mib = 0;  // per-chunk hashing scratch budget, MiB (0: 30% of free HBM, <= 64 GiB)
 
   // host mirrors of the tables
   std::vector<ef_sig_desc> sig_desc;
@@ -225,6 +226,7 @@ ef_ctx* ef_create(int device) {
     return nullptr;
   }
   cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, device);
+  if (const char* e = getenv("EF_CHUNK_MIB")) ctx->chunk_mib = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
   cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
   cudaStreamCreateWithFlags(&ctx->st_up, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&ctx->ev_up, cudaEventDisableTiming);
@@ -981,11 +983,17 @@ static int ensure_step_cand(ef_ctx* ctx, uint32_t total, uint32_t S) {
   return EF_OK;
 }
 
-// per-chunk hashing scratch for rows of S node slots and Rs ref slots: bounded (<= 6 GiB of
-// the 180 GB) so graphs of any size stream through
+// per-chunk hashing scratch for rows of S node slots and Rs ref slots: bounded (30% of the free
+// HBM, at most 64 GiB) so graphs of any size stream through; a chunk that holds the whole step
+// keeps every candidate in flight (large graphs have few parents: chunking starves the GPU)
 static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk) {
   const uint64_t per = (uint64_t)S * (4 + 4 + sizeof(Job) + 16 + 16 + 8 + 8 + 4 + 4) + 4ull * Rs + 4ull * (S + 31) / 32 + 32;
-  uint64_t ch = std::max<uint64_t>(256, (6144ull << 20) / per);
+  if (!ctx->chunk_mib) {  // a share of the HBM free when the first chunk is sized (EF_CHUNK_MIB overrides)
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    ctx->chunk_mib = std::min<uint64_t>(64ull << 10, std::max<uint64_t>(1024, (uint64_t)(0.3 * (double)fr) >> 20));
+  }
+  uint64_t ch = std::max<uint64_t>(256, (ctx->chunk_mib << 20) / per);
   ch = std::min<uint64_t>(ch, std::max<uint32_t>(items, 1));
   ch = std::min<uint64_t>(ch, (uint64_t)INT32_MAX / S);
   *chunk = (uint32_t)ch;

@@ -65,11 +65,13 @@ struct WeightSet {
 struct Scratch {
   DevBuf<uint32_t> didx, jv, refsrc, dcount, dsorted, dorder, sval, sval2, rmask, iota, outsrc;
   DevBuf<Job> jobs;
+  DevBuf<uint16_t> jlvl;
   DevBuf<uint64_t> fresh, fresh2, skey, skey2;
   DevBuf<int32_t> seg_b, seg_e;
   DevBuf<uint8_t> sort_tmp, seg_tmp;
   DevBuf<uint32_t> recmax;
   void release() {
+    jlvl.release();
     didx.release(); jv.release(); refsrc.release(); dcount.release(); dsorted.release(); dorder.release();
     sval.release(); sval2.release(); rmask.release(); iota.release(); outsrc.release(); jobs.release();
     fresh.release(); fresh2.release(); skey.release(); skey2.release(); seg_b.release(); seg_e.release();
@@ -84,7 +86,8 @@ struct ef_ctx {
   cudaStream_t st = nullptr;
   std::string err;
   int n_sm = 148;
-  uint64_t chunk_mib = 0;  // per-chunk hashing scratch budget, MiB (0: 30% of free HBM, <= 64 GiB)
+  uint32_t wide_min = 512;  // jobs per candidate from which k_keys_wide takes it (EF_WIDE_MIN; 0: off)
+  uint64_t chunk_mib = 0;  // per-chunk hashing scratch budget, MiB (0: half the free HBM, <= 96 GiB)
 
   // host mirrors of the tables
   std::vector<ef_sig_desc> sig_desc;
@@ -226,6 +229,7 @@ ef_ctx* ef_create(int device) {
     return nullptr;
   }
   cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, device);
+  if (const char* e = getenv("EF_WIDE_MIN")) ctx->wide_min = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_CHUNK_MIB")) ctx->chunk_mib = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
   cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
   cudaStreamCreateWithFlags(&ctx->st_up, cudaStreamNonBlocking);
@@ -786,6 +790,11 @@ static uint32_t bits_for(uint32_t v);
 // node keys: a thread per candidate when the chunk fills the GPU, four lanes per candidate
 // (lower latency per compression) when it does not
 static int launch_keys(ef_ctx* ctx, cudaStream_t st, const VArgs& V) {
+  if (V.wide_min) {  // large graphs: the longest candidates a warp each, level by level
+    const uint32_t gw = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
+    k_keys_wide<128><<<gw, 128, 0, st>>>(V);
+    EF_CUDA(cudaGetLastError());
+  }
   if (V.n < 20000u) {
     const uint32_t gq = std::max<uint32_t>(1, (V.n + 31) / 32);
     k_keys_quad<128><<<gq, 128, 0, st>>>(V);
@@ -983,21 +992,22 @@ static int ensure_step_cand(ef_ctx* ctx, uint32_t total, uint32_t S) {
   return EF_OK;
 }
 
-// per-chunk hashing scratch for rows of S node slots and Rs ref slots: bounded (30% of the free
-// HBM, at most 64 GiB) so graphs of any size stream through; a chunk that holds the whole step
+// per-chunk hashing scratch for rows of S node slots and Rs ref slots: bounded (half the free
+// HBM, at most 96 GiB) so graphs of any size stream through; a chunk that holds the whole step
 // keeps every candidate in flight (large graphs have few parents: chunking starves the GPU)
 static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk) {
-  const uint64_t per = (uint64_t)S * (4 + 4 + sizeof(Job) + 16 + 16 + 8 + 8 + 4 + 4) + 4ull * Rs + 4ull * (S + 31) / 32 + 32;
+  const uint64_t per = (uint64_t)S * (4 + 4 + sizeof(Job) + 16 + 16 + 8 + 8 + 4 + 4 + 2) + 4ull * Rs + 4ull * (S + 31) / 32 + 32;
   if (!ctx->chunk_mib) {  // a share of the HBM free when the first chunk is sized (EF_CHUNK_MIB overrides)
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
-    ctx->chunk_mib = std::min<uint64_t>(64ull << 10, std::max<uint64_t>(1024, (uint64_t)(0.3 * (double)fr) >> 20));
+    ctx->chunk_mib = std::min<uint64_t>(96ull << 10, std::max<uint64_t>(1024, (uint64_t)(0.5 * (double)fr) >> 20));
   }
   uint64_t ch = std::max<uint64_t>(256, (ctx->chunk_mib << 20) / per);
   ch = std::min<uint64_t>(ch, std::max<uint32_t>(items, 1));
   ch = std::min<uint64_t>(ch, (uint64_t)INT32_MAX / S);
   *chunk = (uint32_t)ch;
   EF_CUDA(sc.didx.reserve(ch * S, st));
+  if (S > kFastRows) EF_CUDA(sc.jlvl.reserve(ch * S, st));
   EF_CUDA(sc.jv.reserve(ch * S, st));
   EF_CUDA(sc.jobs.reserve(ch * S, st));
   EF_CUDA(sc.refsrc.reserve(ch * Rs, st));
@@ -1057,6 +1067,8 @@ static VArgs chunk_args(ef_ctx* ctx, Scratch& sc, uint32_t S, uint32_t Rs) {
   V.input_words = reinterpret_cast<const uint64_t*>(ctx->d_input_text.p);
   V.err = ctx->d_scalars.p + 1;
   V.jv = sc.jv.p;
+  V.jlvl = nullptr;
+  V.wide_min = 0;
   return V;
 }
 
@@ -1191,6 +1203,8 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       // the shared-memory merge also handle rows <= 1024, but measured slower than the general
       // kernels there: NasNet-A 15.1 vs 13.8 ms per 1024-parent step)
       V.slots = S <= kFastRows;
+      V.jlvl = (V.slots || !ctx->wide_min) ? nullptr : sc.jlvl.p;  // levels for k_keys_wide (large graphs)
+      V.wide_min = V.slots ? 0u : ctx->wide_min;
       if (V.slots) {
         const uint32_t gw = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
         k_dirty_warp<4><<<gw, 128, 0, ctx->st>>>(V);

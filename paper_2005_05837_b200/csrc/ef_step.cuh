@@ -75,6 +75,8 @@ struct VArgs {
   uint32_t* refsrc;   // [n][Rs]
   uint64_t* fresh;    // [n][S][2]
   uint32_t* dcount;   // [n]
+  uint16_t* jlvl;     // [n][S] job level in the candidate's key DAG (k_dirty; null: not computed)
+  uint32_t wide_min;  // > 0: candidates with at least this many jobs go to k_keys_wide, not k_keys
   const uint32_t* order;  // [n] chunk-local candidate per lane (k_keys)
   uint64_t* skey;     // [n][S] sort keys (first key word, big endian)
   uint32_t* sval;     // [n][S] job index
@@ -241,16 +243,27 @@ __global__ void k_dirty(VArgs A) {
     if (P.drop0 >= 0) remove(P.drop0);
     if (P.drop1 >= 0) remove(P.drop1);
     uint32_t j = 0, r = 0;
+    uint16_t* lv = A.jlvl ? A.jlvl + (uint64_t)lc * A.S : nullptr;
     auto src_of = [&](uint32_t ref) -> uint32_t {
       const uint32_t p = ref >> 8, port = ref & 255u;
       const uint32_t fi = didx[p];
       return fi ? (kFresh | (port << 23) | (fi - 1)) : ((port << 23) | p);
+    };
+    // level of a job from its key sources: one past the deepest fresh producer
+    auto level_of = [&](uint32_t r0, uint32_t nr) -> uint16_t {
+      uint32_t l = 0;
+      for (uint32_t k = 0; k < nr; ++k) {
+        const uint32_t sv = rs[r0 + k];
+        if (sv & kFresh) l = max(l, (uint32_t)lv[sv & 0x7fffffu] + 1u);
+      }
+      return (uint16_t)min(l, 65535u);
     };
     auto emit_new = [&]() {
       for (int k = 0; k < 2; ++k) {
         if (!P.live[k]) continue;
         rs[r] = src_of(P.new_ref[k]);  // new nodes are exempt from the remap (rules.py:186-188)
         jobs[j] = Job{P.new_sig[k], P.new_aux[k], r, 1u};
+        if (lv) lv[j] = level_of(r, 1);
         r += 1;
         didx[pn + k] = ++j;
       }
@@ -275,6 +288,7 @@ __global__ void k_dirty(VArgs A) {
       }
       if (dirty) {
         jobs[j] = Job{v == P.mod ? P.mod_sig : psig[v], v == P.mod ? P.mod_aux : paux[v], r, nr};
+        if (lv) lv[j] = level_of(r, nr);
         r += nr;
         didx[v] = ++j;
         remove(v);
@@ -655,7 +669,7 @@ __global__ void __launch_bounds__(BT, EF_KEYS_MINB) k_keys(VArgs A) {
   for (uint32_t l = blockIdx.x * BT + threadIdx.x; l < A.n; l += gridDim.x * BT) {
     const uint32_t lc = A.order[l];
     const uint32_t d = A.dcount[lc];
-    if (d == 0) continue;
+    if (d == 0 || (A.wide_min && d >= A.wide_min)) continue;  // (the wide ones: k_keys_wide)
     const uint32_t c = A.c0 + lc;
     const uint64_t* pkeys = A.full ? nullptr : Rec{reinterpret_cast<char*>(A.parent_addr[A.plan[c].parent])}.keys(G);
     const Job* jobs = A.jobs + (uint64_t)lc * A.S;
@@ -738,6 +752,146 @@ __global__ void __launch_bounds__(BT, EF_KEYS_MINB) k_keys(VArgs A) {
       sval[jj] = jj;
     }
     if (A.stats) atomicAdd(A.stats, (unsigned long long)ncomp);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// k_keys_wide: one warp per candidate with many jobs (large graphs).  A candidate's node keys
+// form a DAG: a job needs the keys of its fresh producers only.  k_dirty records each job's
+// level (one past its deepest fresh producer); the warp counting-sorts its jobs by level and
+// hashes a level at a time, 32 jobs per round, so a long dependency chain is no longer one
+// thread's sequential walk (the tail that bounded k_keys on 5k-20k-node graphs).
+// The candidate's skey row is scratch for the level sort until the keys are done.
+// ------------------------------------------------------------------------------------------
+
+template <int BT>
+__global__ void __launch_bounds__(BT) k_keys_wide(VArgs A) {
+  constexpr int WPB = BT / 32;
+  __shared__ uint64_t msg[kKeyMaxW * BT];
+  const Geo& G = A.g;
+  const Tables& T = A.T;
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  uint64_t* col = msg + threadIdx.x;
+  const unsigned full = 0xffffffffu;
+  for (uint32_t l = blockIdx.x * WPB + wid; l < A.n; l += gridDim.x * WPB) {  // warp-uniform
+    const uint32_t lc = A.order[l];
+    const uint32_t d = A.dcount[lc];
+    if (d < A.wide_min) break;  // sorted by job count: the rest belong to k_keys
+    const uint32_t c = A.c0 + lc;
+    const uint64_t* pkeys = Rec{reinterpret_cast<char*>(A.parent_addr[A.plan[c].parent])}.keys(G);
+    const Job* jobs = A.jobs + (uint64_t)lc * A.S;
+    const uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
+    const uint16_t* lv = A.jlvl + (uint64_t)lc * A.S;
+    uint64_t* fresh = A.fresh + 2ull * lc * A.S;
+    uint64_t* skey = A.skey + (uint64_t)lc * A.S;
+    uint32_t* sval = A.sval + (uint64_t)lc * A.S;
+    uint32_t* ord = reinterpret_cast<uint32_t*>(skey);  // [S] jobs by level
+    uint32_t* cnt = ord + A.S;                          // [S] per level: count -> start -> end
+    uint32_t L = 0;
+    for (uint32_t j = lane; j < d; j += 32) L = max(L, (uint32_t)lv[j]);
+    L = __reduce_max_sync(full, L);
+    const uint32_t nl = L + 1;
+    for (uint32_t x = lane; x < nl; x += 32) cnt[x] = 0;
+    __syncwarp();
+    for (uint32_t j = lane; j < d; j += 32) atomicAdd(&cnt[lv[j]], 1u);
+    __syncwarp();
+    uint32_t run = 0;
+    for (uint32_t x0 = 0; x0 < nl; x0 += 32) {
+      const uint32_t x = x0 + lane;
+      const uint32_t v = x < nl ? cnt[x] : 0u;
+      uint32_t inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(full, inc, o);
+        if ((int)lane >= o) inc += y;
+      }
+      if (x < nl) cnt[x] = run + inc - v;
+      run += __shfl_sync(full, inc, 31);
+    }
+    __syncwarp();
+    for (uint32_t j = lane; j < d; j += 32) ord[atomicAdd(&cnt[lv[j]], 1u)] = j;
+    __syncwarp();  // cnt[level] is now the end of the level's run in ord
+    uint32_t ncomp = 0, b = 0;
+    for (uint32_t lev = 0; lev < nl; ++lev) {
+      const uint32_t e = cnt[lev];
+      for (uint32_t x0 = b; x0 < e; x0 += 32) {
+        const uint32_t x = x0 + lane;
+        if (x >= e) continue;
+        const uint32_t jj = ord[x];
+        const Job jb = jobs[jj];
+        const bool input = jb.nin & kInputJob;
+        const uint32_t nin = input ? 0u : jb.nin;
+        const uint32_t tlen = T.sig_text_len[jb.sig];
+        const uint32_t nlen = input ? T.name_len[jb.aux] : 0u;
+        const uint32_t len = tlen + nlen + 16u + 18u * nin;
+        uint64_t h0, h1;
+        if (len > 8u * kKeyMaxW) {
+          const Key128 ks = job_key_slow(text_tables(T), jb, rs, pkeys, fresh);
+          h0 = ks.a;
+          h1 = ks.b;
+        } else {
+          const uint64_t* tw = reinterpret_cast<const uint64_t*>(T.sig_text + T.sig_text_off[jb.sig]);
+          const uint32_t ws = input ? kEmptyWset : jb.aux;
+          auto src = [&](uint32_t k, uint64_t& k0, uint64_t& k1) -> uint32_t {
+            const uint32_t sv = rs[jb.roff + k];
+            const uint32_t idx = sv & 0x7fffffu;
+            const uint64_t* kp = (sv & kFresh) ? fresh + 2 * idx : pkeys + 2 * idx;
+            k0 = kp[0];
+            k1 = kp[1];
+            return (sv >> 23) & 255u;
+          };
+          uint32_t nw;
+          if (!input && nin <= 2u) {
+            uint64_t k00 = 0, k01 = 0, k10 = 0, k11 = 0;
+            uint32_t p0 = 0, p1 = 0;
+            if (nin > 0u) p0 = src(0, k00, k01);
+            if (nin > 1u) p1 = src(1, k10, k11);
+            nw = msg_fast<BT>(col, tw, tlen, __ldg(T.ws_digest + 2 * ws), __ldg(T.ws_digest + 2 * ws + 1), nin, k00,
+                              k01, p0, k10, k11, p1);
+          } else {
+            WordSink<BT> sk;
+            sk.init(col);
+            const uint32_t fw = tlen >> 3;
+            for (uint32_t i = 0; i < fw; ++i) sk.push(__ldg(tw + i), 8);
+            if (tlen & 7u) sk.push(__ldg(tw + fw), tlen & 7u);
+            if (input) {  // graph.py:534-535: the input's name follows its signature text
+              const uint8_t* nm = T.names + T.name_off[jb.aux];
+              for (uint32_t i = 0; i < nlen; ++i) sk.push(nm[i], 1);
+            }
+            sk.push(__ldg(T.ws_digest + 2 * ws), 8);
+            sk.push(__ldg(T.ws_digest + 2 * ws + 1), 8);
+            for (uint32_t k = 0; k < nin; ++k) {
+              uint64_t k0, k1;
+              const uint32_t port = src(k, k0, k1);
+              sk.push(k0, 8);
+              sk.push(k1, 8);
+              sk.push(port_be(port), 2);
+            }
+            sk.flush();
+            nw = sk.q;
+          }
+          const uint32_t nb = (len + 127u) >> 7;
+          for (uint32_t q = nw; q < 16u * nb; ++q) col[q * BT] = 0;
+          uint64_t h[8];
+          b2b_start(h, 16);
+          ncomp += nb;
+          for (uint32_t bk = 0; bk < nb; ++bk)
+            b2b_compress_col<BT>(h, col + 16 * bk * BT, (uint64_t)min(len, 128u * (bk + 1)), bk + 1 == nb);
+          h0 = h[0];
+          h1 = h[1];
+        }
+        fresh[2 * jj] = h0;
+        fresh[2 * jj + 1] = h1;
+      }
+      __syncwarp();  // this level's keys are visible to the next level's lanes
+      b = e;
+    }
+    for (uint32_t j = lane; j < d; j += 32) {  // the sort records (the level scratch is dead)
+      skey[j] = B2b::bswap64(fresh[2 * j]);
+      sval[j] = j;
+    }
+    ncomp = __reduce_add_sync(full, ncomp);
+    if (A.stats && lane == 0) atomicAdd(A.stats, (unsigned long long)ncomp);
   }
 }
 
@@ -902,7 +1056,8 @@ __global__ void __launch_bounds__(BT) k_keys_quad(VArgs A) {
   for (uint32_t l = blockIdx.x * QN + quad; l < nq; l += gridDim.x * QN) {
     const bool live = l < A.n;
     const uint32_t lc = live ? A.order[l] : 0;
-    const uint32_t d = live ? A.dcount[lc] : 0;
+    uint32_t d = live ? A.dcount[lc] : 0;
+    if (A.wide_min && d >= A.wide_min) d = 0;  // k_keys_wide's
     const uint32_t dmax = __reduce_max_sync(0xffffffffu, d);  // lanes of the warp loop together
     const uint32_t c = A.c0 + lc;
     const uint64_t* pkeys =

@@ -58,3 +58,25 @@ def test_random_dag_step_matches_oracle(n_ops, n_parents, sample):
                 assert (int(r["evals"]), int(r["sweeps"])) == (evals, sweeps)
             checked += 1
     assert checked >= sample
+
+
+@pytest.mark.parametrize("model", ["dag:1000", "nasnet_a"])
+def test_wide_level_keys_match_thread_keys(model, monkeypatch):
+    """k_keys_wide (a warp per candidate, jobs by level) against k_keys (a thread per
+    candidate, jobs in order): every candidate's hash, flags and price identical.  EF_WIDE_MIN
+    = 1 sends every candidate of a large-graph step to the level kernel, 0 sends none."""
+    import numpy as np
+
+    g0 = zoo.random_dag(1000, 0) if model.startswith("dag") else zoo.generate(model, 0)
+    out = {}
+    for wide in ("0", "1"):
+        monkeypatch.setenv("EF_WIDE_MIN", wide)
+        fr = Frontier(g0, ef.CostDatabase(), ef.SyntheticProfiler(0), ef.CostFunction.energy(),
+                      ef.SearchConfig(alpha=1.05), 6)
+        try:
+            out[wide] = fr.step().copy()
+        finally:
+            fr.close()
+    assert len(out["0"]) == len(out["1"]) > 0
+    for key in ("hash", "flags", "cost", "time_ms", "energy", "evals", "sweeps"):
+        assert np.array_equal(out["0"][key], out["1"][key]), key

@@ -1203,8 +1203,8 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       // the shared-memory merge also handle rows <= 1024, but measured slower than the general
       // kernels there: NasNet-A 15.1 vs 13.8 ms per 1024-parent step)
       V.slots = S <= kFastRows;
-      V.jlvl = (V.slots || !ctx->wide_min) ? nullptr : sc.jlvl.p;  // levels for k_keys_wide (large graphs)
-      V.wide_min = V.slots ? 0u : ctx->wide_min;
+      V.wide_min = (V.slots || S < ctx->wide_min) ? 0u : ctx->wide_min;  // no candidate can reach it otherwise
+      V.jlvl = V.wide_min ? sc.jlvl.p : nullptr;  // levels for k_keys_wide (large graphs)
       if (V.slots) {
         const uint32_t gw = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
         k_dirty_warp<4><<<gw, 128, 0, ctx->st>>>(V);

@@ -243,27 +243,29 @@ __global__ void k_dirty(VArgs A) {
     if (P.drop0 >= 0) remove(P.drop0);
     if (P.drop1 >= 0) remove(P.drop1);
     uint32_t j = 0, r = 0;
-    uint16_t* lv = A.jlvl ? A.jlvl + (uint64_t)lc * A.S : nullptr;
+    // levels for k_keys_wide (only when this candidate can reach its job threshold): by job in
+    // jlvl, by parent position in the (step-mode idle) jv row, read beside didx so the level
+    // costs no extra dependent load
+    const bool levels = A.jlvl && (uint32_t)pn + 2u >= A.wide_min;
+    uint16_t* lv = levels ? A.jlvl + (uint64_t)lc * A.S : nullptr;
+    uint32_t* plv = A.jv + (uint64_t)lc * A.S;
+    uint32_t lvl = 0;  // level of the job being emitted
     auto src_of = [&](uint32_t ref) -> uint32_t {
       const uint32_t p = ref >> 8, port = ref & 255u;
       const uint32_t fi = didx[p];
+      if (levels && fi) lvl = max(lvl, plv[p] + 1u);
       return fi ? (kFresh | (port << 23) | (fi - 1)) : ((port << 23) | p);
-    };
-    // level of a job from its key sources: one past the deepest fresh producer
-    auto level_of = [&](uint32_t r0, uint32_t nr) -> uint16_t {
-      uint32_t l = 0;
-      for (uint32_t k = 0; k < nr; ++k) {
-        const uint32_t sv = rs[r0 + k];
-        if (sv & kFresh) l = max(l, (uint32_t)lv[sv & 0x7fffffu] + 1u);
-      }
-      return (uint16_t)min(l, 65535u);
     };
     auto emit_new = [&]() {
       for (int k = 0; k < 2; ++k) {
         if (!P.live[k]) continue;
+        lvl = 0;
         rs[r] = src_of(P.new_ref[k]);  // new nodes are exempt from the remap (rules.py:186-188)
         jobs[j] = Job{P.new_sig[k], P.new_aux[k], r, 1u};
-        if (lv) lv[j] = level_of(r, 1);
+        if (levels) {
+          lv[j] = (uint16_t)min(lvl, 65535u);
+          plv[pn + k] = lvl;
+        }
         r += 1;
         didx[pn + k] = ++j;
       }
@@ -279,6 +281,7 @@ __global__ void k_dirty(VArgs A) {
       }
       bool dirty = v == P.mod;
       const uint32_t r0 = pinoff[v], nr = pnin[v];
+      lvl = 0;
       for (uint32_t k = 0; k < nr; ++k) {
         const uint32_t ref = prefs[r0 + k];
         const uint32_t ref2 = vremap(P, ref);
@@ -288,7 +291,10 @@ __global__ void k_dirty(VArgs A) {
       }
       if (dirty) {
         jobs[j] = Job{v == P.mod ? P.mod_sig : psig[v], v == P.mod ? P.mod_aux : paux[v], r, nr};
-        if (lv) lv[j] = level_of(r, nr);
+        if (levels) {
+          lv[j] = (uint16_t)min(lvl, 65535u);
+          plv[v] = lvl;
+        }
         r += nr;
         didx[v] = ++j;
         remove(v);
@@ -790,27 +796,36 @@ __global__ void __launch_bounds__(BT) k_keys_wide(VArgs A) {
     uint32_t L = 0;
     for (uint32_t j = lane; j < d; j += 32) L = max(L, (uint32_t)lv[j]);
     L = __reduce_max_sync(full, L);
-    const uint32_t nl = L + 1;
-    for (uint32_t x = lane; x < nl; x += 32) cnt[x] = 0;
-    __syncwarp();
-    for (uint32_t j = lane; j < d; j += 32) atomicAdd(&cnt[lv[j]], 1u);
-    __syncwarp();
-    uint32_t run = 0;
-    for (uint32_t x0 = 0; x0 < nl; x0 += 32) {
-      const uint32_t x = x0 + lane;
-      const uint32_t v = x < nl ? cnt[x] : 0u;
-      uint32_t inc = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(full, inc, o);
-        if ((int)lane >= o) inc += y;
+    uint32_t nl = L + 1;
+    if (L >= 65535u) {  // levels saturated (a > 65k-deep key chain): one job per "level", in index order
+      nl = d;
+      for (uint32_t x = lane; x < d; x += 32) {
+        ord[x] = x;
+        cnt[x] = x + 1;
       }
-      if (x < nl) cnt[x] = run + inc - v;
-      run += __shfl_sync(full, inc, 31);
+      __syncwarp();
+    } else {
+      for (uint32_t x = lane; x < nl; x += 32) cnt[x] = 0;
+      __syncwarp();
+      for (uint32_t j = lane; j < d; j += 32) atomicAdd(&cnt[lv[j]], 1u);
+      __syncwarp();
+      uint32_t run = 0;
+      for (uint32_t x0 = 0; x0 < nl; x0 += 32) {
+        const uint32_t x = x0 + lane;
+        const uint32_t v = x < nl ? cnt[x] : 0u;
+        uint32_t inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(full, inc, o);
+          if ((int)lane >= o) inc += y;
+        }
+        if (x < nl) cnt[x] = run + inc - v;
+        run += __shfl_sync(full, inc, 31);
+      }
+      __syncwarp();
+      for (uint32_t j = lane; j < d; j += 32) ord[atomicAdd(&cnt[lv[j]], 1u)] = j;
+      __syncwarp();  // cnt[level] is now the end of the level's run in ord
     }
-    __syncwarp();
-    for (uint32_t j = lane; j < d; j += 32) ord[atomicAdd(&cnt[lv[j]], 1u)] = j;
-    __syncwarp();  // cnt[level] is now the end of the level's run in ord
     uint32_t ncomp = 0, b = 0;
     for (uint32_t lev = 0; lev < nl; ++lev) {
       const uint32_t e = cnt[lev];

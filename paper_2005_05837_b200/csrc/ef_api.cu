@@ -66,12 +66,13 @@ struct Scratch {
   DevBuf<uint32_t> didx, jv, refsrc, dcount, dsorted, dorder, sval, sval2, rmask, iota, outsrc;
   DevBuf<Job> jobs;
   DevBuf<uint16_t> jlvl;
-  DevBuf<uint64_t> fresh, fresh2, skey, skey2;
+  DevBuf<uint64_t> fresh, fresh2, skey, skey2, merged;
   DevBuf<int32_t> seg_b, seg_e;
   DevBuf<uint8_t> sort_tmp, seg_tmp;
   DevBuf<uint32_t> recmax;
   void release() {
     jlvl.release();
+    merged.release();
     didx.release(); jv.release(); refsrc.release(); dcount.release(); dsorted.release(); dorder.release();
     sval.release(); sval2.release(); rmask.release(); iota.release(); outsrc.release(); jobs.release();
     fresh.release(); fresh2.release(); skey.release(); skey2.release(); seg_b.release(); seg_e.release();
@@ -86,6 +87,7 @@ struct ef_ctx {
   cudaStream_t st = nullptr;
   std::string err;
   int n_sm = 148;
+  bool big_merge = true;  // rows > 256: merge-path key stream + streaming digest (EF_BIG_MERGE=0: in-thread merge)
   uint32_t wide_min = 512;  // jobs per candidate from which k_keys_wide takes it (EF_WIDE_MIN; 0: off)
   uint64_t chunk_mib = 0;  // per-chunk hashing scratch budget, MiB (0: half the free HBM, <= 96 GiB)
 
@@ -229,6 +231,7 @@ ef_ctx* ef_create(int device) {
     return nullptr;
   }
   cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, device);
+  if (const char* e = getenv("EF_BIG_MERGE")) ctx->big_merge = atoi(e) != 0;
   if (const char* e = getenv("EF_WIDE_MIN")) ctx->wide_min = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_CHUNK_MIB")) ctx->chunk_mib = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
   cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
@@ -996,7 +999,9 @@ static int ensure_step_cand(ef_ctx* ctx, uint32_t total, uint32_t S) {
 // HBM, at most 96 GiB) so graphs of any size stream through; a chunk that holds the whole step
 // keeps every candidate in flight (large graphs have few parents: chunking starves the GPU)
 static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk) {
-  const uint64_t per = (uint64_t)S * (4 + 4 + sizeof(Job) + 16 + 16 + 8 + 8 + 4 + 4 + 2) + 4ull * Rs + 4ull * (S + 31) / 32 + 32;
+  const bool big = S > kFastRows && ctx->big_merge;  // + the merged key stream
+  const uint64_t per = (uint64_t)S * (4 + 4 + sizeof(Job) + 16 + 16 + 8 + 8 + 4 + 4 + 2 + (big ? 16 : 0)) + 4ull * Rs +
+                       4ull * (S + 31) / 32 + 32;
   if (!ctx->chunk_mib) {  // a share of the HBM free when the first chunk is sized (EF_CHUNK_MIB overrides)
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
@@ -1008,6 +1013,7 @@ static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t item
   *chunk = (uint32_t)ch;
   EF_CUDA(sc.didx.reserve(ch * S, st));
   if (S > kFastRows) EF_CUDA(sc.jlvl.reserve(ch * S, st));
+  if (big) EF_CUDA(sc.merged.reserve(ch * S * 2, st));
   EF_CUDA(sc.jv.reserve(ch * S, st));
   EF_CUDA(sc.jobs.reserve(ch * S, st));
   EF_CUDA(sc.refsrc.reserve(ch * Rs, st));
@@ -1069,6 +1075,7 @@ static VArgs chunk_args(ef_ctx* ctx, Scratch& sc, uint32_t S, uint32_t Rs) {
   V.jv = sc.jv.p;
   V.jlvl = nullptr;
   V.wide_min = 0;
+  V.kstream = (S > kFastRows && ctx->big_merge) ? sc.merged.p : sc.fresh2.p;
   return V;
 }
 
@@ -1237,8 +1244,18 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
         k_digest_pm<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
       } else {
         if ((rc = sort_fresh_keys(ctx, sc, ctx->st, V))) return rc;
-        cudaEventRecord(ce[3], ctx->st);
-        k_digest<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+        if (ctx->big_merge) {  // merge-path key stream, then the streaming digest
+          const size_t smem = 4ull * 4 * (V.W + 1);
+          EF_CUDA(cudaFuncSetAttribute(k_merge_big<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
+          k_merge_big<4><<<gm, 128, smem, ctx->st>>>(V);
+          EF_CUDA(cudaGetLastError());
+          cudaEventRecord(ce[3], ctx->st);
+          k_digest_pm<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+        } else {
+          cudaEventRecord(ce[3], ctx->st);
+          k_digest<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+        }
       }
       EF_CUDA(cudaGetLastError());
       cudaEventRecord(ce[4], ctx->st);

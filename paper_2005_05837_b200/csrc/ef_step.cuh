@@ -92,6 +92,7 @@ struct VArgs {
   uint32_t W;          // words per removed-mask row
   uint32_t* rmask;     // [n][W] parent keys (by sorted rank) absent from the candidate: dropped or dirty
   uint64_t* fresh_sorted;  // [n][S][2] the fresh keys in ascending byte order
+  uint64_t* kstream;       // [n][S][2] the merged key stream k_digest_pm hashes (k_merge: fresh_sorted)
   const uint64_t* input_words;  // input text, 8-byte words, zero padded
   uint32_t* err;
   // full mode (whole records: uploads, kept candidates): parent_addr[c] is record c itself,
@@ -1617,6 +1618,124 @@ __global__ void __launch_bounds__(WARPS * 32, EF_MERGE_MINB) k_merge(VArgs A, ui
   }
 }
 
+// The key stream of graphs beyond the shared-memory merge (rows > 256): the parent's sorted
+// keys minus the removed ranks (A) merged with the candidate's sorted fresh keys (B, from the
+// key sort), parent first on equal keys as in k_merge.  One warp per candidate, merge path:
+// lane k finds where the k-th 1/32 of the output starts with one binary search on its
+// diagonal (A addressed by kept index through per-word kept counts in shared memory), then
+// merges its stretch sequentially.  O(n + d) per candidate instead of a binary search per key.
+// Dynamic shared memory: per warp, W + 1 words.
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_merge_big(VArgs A) {
+  extern __shared__ uint32_t mb_smem[];
+  const Geo& G = A.g;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned full = 0xffffffffu;
+  uint32_t* cumk = mb_smem + (uint64_t)w * (A.W + 1);  // kept parent keys before word x
+  for (uint32_t lc = blockIdx.x * WARPS + w; lc < A.n; lc += gridDim.x * WARPS) {  // warp-uniform
+    const uint32_t c = A.c0 + lc;
+    if (A.res[c].flags & EF_F_INCOMPLETE) continue;
+    const VPlan& P = A.plan[c];
+    const uint32_t pn = (uint32_t)P.pn;
+    const uint32_t d = A.dcount[lc];
+    const uint32_t* rm = A.rmask + (uint64_t)lc * A.W;
+    const uint32_t nw = (pn + 31) >> 5;
+    // kept counts per word -> exclusive prefix
+    uint32_t run = 0;
+    for (uint32_t x0 = 0; x0 < nw; x0 += 32) {
+      const uint32_t x = x0 + lane;
+      uint32_t v = 0;
+      if (x < nw) {
+        const uint32_t valid = (x + 1 < nw || (pn & 31u) == 0) ? 0xffffffffu : ((1u << (pn & 31u)) - 1u);
+        v = __popc(~rm[x] & valid);
+      }
+      uint32_t inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(full, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (x < nw) cumk[x] = run + inc - v;
+      run += __shfl_sync(full, inc, 31);
+    }
+    if (lane == 0) cumk[nw] = run;
+    __syncwarp();
+    const uint32_t na = run;
+    Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
+    const uint64_t* pskeys = R.skeys(G);
+    const uint64_t* bs = A.fresh_sorted + 2ull * lc * A.S;  // B: the key sort's output
+    uint64_t* out = A.kstream + 2ull * lc * A.S;
+    // rank of the i-th kept parent key (i < na)
+    auto select_kept = [&](uint32_t i) -> uint32_t {
+      uint32_t lo = 0, hi = nw;  // last word with cumk <= i
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (cumk[mid] <= i) lo = mid;
+        else hi = mid;
+      }
+      return 32u * lo + nth_bit(~rm[lo], i - cumk[lo]);
+    };
+    auto a_raw = [&](uint32_t r) -> uint4 { return __ldg(reinterpret_cast<const uint4*>(pskeys) + r); };
+    auto a_key = [&](uint32_t r, uint64_t& k0, uint64_t& k1) {  // big endian
+      const uint4 x = a_raw(r);
+      k0 = B2b::bswap64(((uint64_t)x.y << 32) | x.x);
+      k1 = B2b::bswap64(((uint64_t)x.w << 32) | x.z);
+    };
+    auto b_key = [&](uint32_t j, uint64_t& k0, uint64_t& k1) {
+      const uint4 x = *(reinterpret_cast<const uint4*>(bs) + j);
+      k0 = B2b::bswap64(((uint64_t)x.y << 32) | x.x);
+      k1 = B2b::bswap64(((uint64_t)x.w << 32) | x.z);
+    };
+    const uint32_t tot = na + d;
+    const uint32_t per = (tot + 31) / 32;
+    const uint32_t D = min(tot, per * (uint32_t)lane);
+    // merge path: i = number of A elements among the first D outputs
+    uint32_t lo = D > d ? D - d : 0u, hi = min(D, na);
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      uint64_t a0, a1, b0, b1;
+      a_key(select_kept(mid), a0, a1);
+      b_key(D - mid - 1, b0, b1);
+      if (!be_less(b0, b1, a0, a1)) lo = mid + 1;  // A[mid] <= B[D - mid - 1]
+      else hi = mid;
+    }
+    uint32_t i = lo, j = D - lo;
+    const uint32_t end = min(tot, D + per);
+    // the A stream: kept ranks in order from the cached mask word, one key fetched ahead
+    uint32_t r = i < na ? select_kept(i) : 0u;
+    uint32_t wd = r >> 5, bits = (r & 31u) == 31u ? 0u : (~__ldg(rm + wd) & ~((2u << (r & 31u)) - 1u));
+    auto next_rank = [&]() -> uint32_t {  // the kept rank after the last one handed out
+      while (!bits) bits = ~__ldg(rm + ++wd);
+      const uint32_t x = 32u * wd + (uint32_t)(__ffs(bits) - 1);
+      bits &= bits - 1u;
+      return x;
+    };
+    uint64_t a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+    if (i < na) a_key(r, a0, a1);
+    uint4 an = make_uint4(0, 0, 0, 0);  // the key after the current A head
+    if (i + 1 < na) an = a_raw(next_rank());
+    if (j < d) b_key(j, b0, b1);
+    uint4* o4 = reinterpret_cast<uint4*>(out);
+    for (uint32_t o = D; o < end; ++o) {
+      const bool take_a = j >= d || (i < na && !be_less(b0, b1, a0, a1));
+      if (take_a) {
+        const uint64_t w0 = B2b::bswap64(a0), w1 = B2b::bswap64(a1);
+        o4[o] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
+        if (++i < na) {
+          a0 = B2b::bswap64(((uint64_t)an.y << 32) | an.x);
+          a1 = B2b::bswap64(((uint64_t)an.w << 32) | an.z);
+          if (i + 1 < na) an = a_raw(next_rank());
+        }
+      } else {
+        const uint64_t w0 = B2b::bswap64(b0), w1 = B2b::bswap64(b1);
+        o4[o] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
+        if (++j < d) b_key(j, b0, b1);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // The graph digest over a pre-merged key stream: the prefix (input declarations, output keys
 // and ports) goes through the word sink; the keys follow as full words with a constant byte
 // shift, loaded 16 words per block with independent 16-byte loads.
@@ -1636,7 +1755,7 @@ __global__ void __launch_bounds__(BT, EF_DIGEST_MINB) k_digest_pm(VArgs A) {
     const int n_out = R.h().n_out;
     const uint32_t* didx = A.didx + (uint64_t)lc * A.S;
     const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
-    const uint64_t* ks = A.fresh_sorted + 2ull * lc * A.S;  // merged key stream
+    const uint64_t* ks = A.kstream + 2ull * lc * A.S;  // merged key stream
     const uint32_t li = T.input_text_len;
     const uint32_t n_child = (uint32_t)(P.n_keep + P.n_live);
     const uint32_t kwords = 2 * n_child;

@@ -201,6 +201,12 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents,
 int ef_pending(ef_ctx* ctx, ef_sig_desc* sigs, uint32_t sig_cap, uint32_t* n_sigs,
                int32_t* derives, uint32_t derive_cap, uint32_t* n_derives);
 int ef_results(ef_ctx* ctx, ef_cand_result* out, uint32_t n);
+/* the same copy, asynchronous: the last step's results are snapshotted on the device (so the
+ * next step may start at once) and copied to `out` (page-locked host memory) on a copy
+ * stream, overlapping whatever the caller queues next; ef_results_wait blocks until `out`
+ * holds them.  One copy in flight at a time. */
+int ef_results_async(ef_ctx* ctx, ef_cand_result* out, uint32_t n);
+int ef_results_wait(ef_ctx* ctx);
 /* copy step candidates into record slots (the ones the search keeps) */
 int ef_keep(ef_ctx* ctx, const uint32_t* cand_idx, uint32_t n, const uint32_t* slots);
 /* ---- hash-owner sharding (one process per GPU) ------------------------------------------ */

@@ -104,6 +104,8 @@ _PROTOS = {
     "ef_expand": (C.c_int, [_P, _U32P, C.c_uint32, _I32P, C.c_uint32, C.POINTER(PriceParams), C.c_int, _U32P]),
     "ef_pending": (C.c_int, [_P, C.POINTER(SigDesc), C.c_uint32, _U32P, _I32P, C.c_uint32, _U32P]),
     "ef_results": (C.c_int, [_P, C.c_void_p, C.c_uint32]),
+    "ef_results_async": (C.c_int, [_P, C.c_void_p, C.c_uint32]),
+    "ef_results_wait": (C.c_int, [_P]),
     "ef_keep": (C.c_int, [_P, _U32P, C.c_uint32, _U32P]),
     "ef_last_timing": (C.c_int, [_P, C.POINTER(C.c_float), C.c_uint32]),
     "ef_last_stats": (C.c_int, [_P, _U64P, C.c_uint32]),

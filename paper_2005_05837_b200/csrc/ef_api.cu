@@ -127,7 +127,9 @@ struct ef_ctx {
   DevBuf<uint32_t> d_pscratch, d_site_count, d_cand_off, d_step_seq, d_scalars;
   DevBuf<char> d_stage;
   DevBuf<int32_t> d_req_dv;
-  DevBuf<ef_cand_result> d_res, d_res_aux;
+  DevBuf<ef_cand_result> d_res, d_res_aux, d_res_snap;
+  cudaStream_t st_copy = nullptr;  // results copies (ef_results_async)
+  cudaEvent_t ev_snap = nullptr, ev_copy = nullptr;
   DevBuf<ef_sig_desc> d_req_sig;
   DevBuf<uint64_t> d_hash_out;
   DevBuf<uint32_t> d_sperm;
@@ -236,6 +238,9 @@ ef_ctx* ef_create(int device) {
   if (const char* e = getenv("EF_CHUNK_MIB")) ctx->chunk_mib = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
   cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
   cudaStreamCreateWithFlags(&ctx->st_up, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&ctx->st_copy, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&ctx->ev_snap, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ctx->ev_up, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ctx->ev_main, cudaEventDisableTiming);
   for (auto& e : ctx->ev) cudaEventCreate(&e);
@@ -285,6 +290,8 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_req_dv.release();
   ctx->d_res.release();
   ctx->d_res_aux.release();
+  if (ctx->st_copy) cudaStreamSynchronize(ctx->st_copy);
+  ctx->d_res_snap.release();
   ctx->d_req_sig.release();
   ctx->d_hash_out.release();
   ctx->d_sperm.release();
@@ -306,6 +313,9 @@ void ef_destroy(ef_ctx* ctx) {
   if (ctx->ev_up) cudaEventDestroy(ctx->ev_up);
   if (ctx->ev_main) cudaEventDestroy(ctx->ev_main);
   if (ctx->st_up) cudaStreamDestroy(ctx->st_up);
+  if (ctx->st_copy) cudaStreamDestroy(ctx->st_copy);
+  if (ctx->ev_snap) cudaEventDestroy(ctx->ev_snap);
+  if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
   ctx->d_sel.release();
   ctx->d_dst.release();
   for (auto& e : ctx->ev) cudaEventDestroy(e);
@@ -1505,6 +1515,25 @@ int ef_results(ef_ctx* ctx, ef_cand_result* out, uint32_t n) {
   if (!n) return EF_OK;
   EF_CUDA(cudaMemcpyAsync(out, ctx->d_res.p, n * sizeof(ef_cand_result), cudaMemcpyDeviceToHost, ctx->st));
   EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
+}
+
+int ef_results_async(ef_ctx* ctx, ef_cand_result* out, uint32_t n) {
+  EF_REQUIRE(n <= ctx->last_total, "ef_results_async: more than the last step produced");
+  if (!n) return EF_OK;
+  EF_CUDA(cudaEventSynchronize(ctx->ev_copy));  // the previous copy still reads the snapshot
+  EF_CUDA(ctx->d_res_snap.reserve(n, ctx->st));
+  EF_CUDA(cudaMemcpyAsync(ctx->d_res_snap.p, ctx->d_res.p, n * sizeof(ef_cand_result), cudaMemcpyDeviceToDevice,
+                          ctx->st));
+  EF_CUDA(cudaEventRecord(ctx->ev_snap, ctx->st));
+  EF_CUDA(cudaStreamWaitEvent(ctx->st_copy, ctx->ev_snap, 0));
+  EF_CUDA(cudaMemcpyAsync(out, ctx->d_res_snap.p, n * sizeof(ef_cand_result), cudaMemcpyDeviceToHost, ctx->st_copy));
+  EF_CUDA(cudaEventRecord(ctx->ev_copy, ctx->st_copy));
+  return EF_OK;
+}
+
+int ef_results_wait(ef_ctx* ctx) {
+  EF_CUDA(cudaEventSynchronize(ctx->ev_copy));
   return EF_OK;
 }
 

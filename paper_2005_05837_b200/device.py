@@ -141,6 +141,7 @@ class DeviceSession:
         self.db: CostDatabase | None = None
         self.profiler: ProfilerSpec | None = None
         self._pinned, self._pinned_bytes = None, 0  # page-locked staging of step results
+        self._apinned, self._apinned_bytes = None, 0  # the same for results_async
 
     @classmethod
     def default(cls) -> "DeviceSession":
@@ -153,6 +154,11 @@ class DeviceSession:
         if self._pinned:
             self.L.ef_host_free(self._pinned)
             self._pinned, self._pinned_bytes = None, 0
+        if self._apinned:
+            if self.ctx:
+                self.results_wait()
+            self.L.ef_host_free(self._apinned)
+            self._apinned, self._apinned_bytes = None, 0
         if self.ctx:
             self.L.ef_destroy(self.ctx)
             self.ctx = None
@@ -444,7 +450,10 @@ class DeviceSession:
         return [out[i] for i in range(n)]
 
     def expand(self, slots: list[int], rule_ids: list[int], pp: N.PriceParams,
-               insert_visited: bool = True) -> list[N.CandResult]:
+               insert_visited: bool = True, results: bool = True):
+        """One batched step (ef_expand).  -> the candidates' results (a view of a reused
+        page-locked buffer), or with results=False only their count (read them with
+        results_async / results_wait, overlapping the next step)."""
         parents = N.u32_array(slots)
         rules = N.i32_array(rule_ids)
         count = C.c_uint32(0)
@@ -458,7 +467,28 @@ class DeviceSession:
                 continue
             self._check(rc, "ef_expand")
             break
-        return self._results(count.value)
+        return self._results(count.value) if results else count.value
+
+    def results_async(self, n: int) -> np.ndarray:
+        """Start copying the last step's n results to page-locked memory on the copy stream
+        (ef_results_async); the returned view is valid after results_wait()."""
+        need = max(1, n) * N.CAND_DTYPE.itemsize
+        if self._apinned_bytes < need:
+            self.results_wait()
+            if self._apinned:
+                self.L.ef_host_free(self._apinned)
+            size = max(need, 2 * self._apinned_bytes)
+            self._apinned = self.L.ef_host_alloc(size)
+            if not self._apinned:
+                raise N.NativeError("ef_host_alloc failed")
+            self._apinned_bytes = size
+        out = np.ctypeslib.as_array((C.c_uint8 * need).from_address(self._apinned)).view(N.CAND_DTYPE)[:n]
+        if n:
+            self._check(self.L.ef_results_async(self.ctx, self._apinned, n), "ef_results_async")
+        return out
+
+    def results_wait(self) -> None:
+        self._check(self.L.ef_results_wait(self.ctx), "ef_results_wait")
 
     def _results(self, n: int) -> np.ndarray:
         """The last step's candidate results, copied into page-locked host memory (full D2H

@@ -167,3 +167,25 @@ def test_packed_uploads_sync_async_match_resident():
     for got in (got_sync, got_async):
         for key in ("hash", "flags", "cost", "time_ms", "energy", "evals", "sweeps"):
             assert np.array_equal(got[key], base[key]), key
+
+
+def test_results_async_matches_sync():
+    """ef_results_async: the step's results snapshotted on the device and copied on the copy
+    stream while the next step runs equal the synchronous ef_results of the same step."""
+    import numpy as np
+
+    g0 = zoo.generate("resnet50", 0)
+    fr = Frontier(g0, ef.CostDatabase(), ef.SyntheticProfiler(0), ef.CostFunction.energy(),
+                  ef.SearchConfig(alpha=1.05), 16)
+    s = fr.s
+    try:
+        want = fr.step().copy()
+        n = s.expand(fr.slots, fr.rule_ids, fr.pp, False, results=False)
+        got = s.results_async(n)
+        other = fr.step(fr.slots[:4])  # the next step overwrites the device results meanwhile
+        s.results_wait()
+        assert n == len(want) and len(other) < n
+        for key in want.dtype.names:
+            assert np.array_equal(got[key], want[key]), key
+    finally:
+        fr.close()

@@ -3,7 +3,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
+#include <thread>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -58,6 +60,7 @@ struct WeightSet {
   int32_t dv[4] = {0, 0, 0, 0};
   std::string hdr_w, hdr_b;
   bool ready = false;  // tensors present + digest computed
+  std::vector<uint64_t> hw, hb;  // host copies (raw float64 bits) until the digest is taken
 };
 
 // per-chunk hashing scratch (ef_step.cuh): one set for steps / keeps on the main stream, one
@@ -104,11 +107,12 @@ struct ef_ctx {
   // device tables
   DevBuf<ef_sig_desc> d_sig_desc;
   DevBuf<uint32_t> d_text_off, d_text_len, d_row_off, d_row_n, d_sig_ht_val, d_dv_ht_val, d_name_off, d_name_len;
-  DevBuf<uint8_t> d_text, d_names, d_input_text, d_hdr;
+  DevBuf<uint8_t> d_text, d_names, d_input_text;
   DevBuf<int32_t> d_row_alg, d_dv_tuple;
   DevBuf<double> d_row_t, d_row_e;
   DevBuf<unsigned long long> d_sig_ht_key, d_dv_ht_key;
   DevBuf<uint64_t> d_ws_digest;
+  std::vector<uint64_t> h_ws_digest;  // host mirror (the digests are taken on host cores)
   DevBuf<double> d_pool;
   uint64_t pool_used = 0;
   uint32_t sig_ht_mask = 0, dv_ht_mask = 0;
@@ -267,7 +271,6 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_text.release();
   ctx->d_names.release();
   ctx->d_input_text.release();
-  ctx->d_hdr.release();
   ctx->d_row_alg.release();
   ctx->d_dv_tuple.release();
   ctx->d_row_t.release();
@@ -392,6 +395,11 @@ int ef_wset_put(ef_ctx* ctx, uint32_t id, int32_t kind, int32_t oc, const double
   if (rc) return rc;
   if (w_n) EF_CUDA(cudaMemcpyAsync(ctx->d_pool.p + S.w_off, w, w_n * 8, cudaMemcpyHostToDevice, ctx->st));
   if (b_n && b) EF_CUDA(cudaMemcpyAsync(ctx->d_pool.p + S.b_off, b, b_n * 8, cudaMemcpyHostToDevice, ctx->st));
+  // host copies for the digest (taken on host cores at commit: one BLAKE2b stream per set)
+  S.hw.resize(w_n);
+  if (w_n) std::memcpy(S.hw.data(), w, w_n * 8);
+  S.hb.assign(b_n, 0);
+  if (b_n && b) std::memcpy(S.hb.data(), b, b_n * 8);
   EF_CUDA(cudaStreamSynchronize(ctx->st));
   ctx->dirty = true;
   return EF_OK;
@@ -611,76 +619,64 @@ int ef_tables_commit(ef_ctx* ctx) {
       EF_CUDA(cudaStreamSynchronize(ctx->st));
       dj.release();
     }
-    // digests: headers in sorted key order (bias < weight, scale < shift)
-    std::vector<uint8_t> hdr;
-    std::vector<DigestJob> jobs;
-    std::vector<std::pair<uint32_t, uint32_t>> hofs;  // (offset of first header, offset of second)
+    // derived tensors back to the host for their digests
     for (uint32_t i : pending) {
-      const WeightSet& S = ctx->ws[i];
-      uint32_t o1 = (uint32_t)hdr.size();
-      const std::string* h0 = nullptr;
-      const std::string* h1 = nullptr;
-      if (S.kind == EF_K_CONV2D) {
-        if (S.has_b) {
-          h0 = &S.hdr_b;
-          h1 = &S.hdr_w;
-        } else {
-          h0 = &S.hdr_w;
-        }
-      } else if (S.kind == EF_K_BATCHNORM) {
-        h0 = &S.hdr_w;
-        h1 = &S.hdr_b;
-      } else if (S.kind == EF_K_MATMUL) {
-        h0 = &S.hdr_w;
-      }
-      if (h0) hdr.insert(hdr.end(), h0->begin(), h0->end());
-      uint32_t o2 = (uint32_t)hdr.size();
-      if (h1) hdr.insert(hdr.end(), h1->begin(), h1->end());
-      hofs.push_back({o1, o2});
+      WeightSet& S = ctx->ws[i];
+      if (S.dv[0] == 0) continue;
+      S.hw.resize(S.w_n);
+      S.hb.resize(S.b_n);
+      if (S.w_n) EF_CUDA(cudaMemcpy(S.hw.data(), ctx->d_pool.p + S.w_off, S.w_n * 8, cudaMemcpyDeviceToHost));
+      if (S.b_n) EF_CUDA(cudaMemcpy(S.hb.data(), ctx->d_pool.p + S.b_off, S.b_n * 8, cudaMemcpyDeviceToHost));
     }
-    hdr.push_back(0);
-    if ((rc = upload(ctx, ctx->d_hdr, hdr))) return rc;
-    for (size_t j = 0; j < pending.size(); ++j) {
-      const WeightSet& S = ctx->ws[pending[j]];
-      DigestJob J{};
-      const uint8_t* hb = ctx->d_hdr.p;
-      uint32_t o1 = hofs[j].first, o2 = hofs[j].second;
-      uint32_t o3 = (j + 1 < hofs.size()) ? hofs[j + 1].first : (uint32_t)hdr.size() - 1;
-      J.hdr0 = hb + o1;
-      J.hlen0 = o2 - o1;
-      J.hdr1 = hb + o2;
-      J.hlen1 = o3 - o2;
-      const double* pw = ctx->d_pool.p + S.w_off;
-      const double* pb = ctx->d_pool.p + S.b_off;
-      if (S.kind == EF_K_CONV2D) {
-        if (S.has_b) {
-          J.t0 = pb;
-          J.n0 = S.b_n;
-          J.t1 = pw;
-          J.n1 = S.w_n;
-        } else {
-          J.t0 = pw;
-          J.n0 = S.w_n;
+    // Digests (graph.py:510-517) on host cores, a set per thread.  A digest is one BLAKE2b
+    // stream over headers and tensor bytes: inherently sequential, and a CPU core runs one
+    // stream several times faster than a lone GPU thread (ResNet-50 merged convs: 19 MB).
+    // Header order is the sorted key order of the reference's weight dict (bias < weight,
+    // scale < shift).
+    ctx->h_ws_digest.resize(2 * nw, 0);
+    std::atomic<size_t> next{0};
+    auto worker = [&]() {
+      for (size_t j; (j = next.fetch_add(1)) < pending.size();) {
+        const uint32_t i = pending[j];
+        const WeightSet& S = ctx->ws[i];
+        const std::string* h0 = nullptr;
+        const std::string* h1 = nullptr;
+        const std::vector<uint64_t>* t0 = nullptr;
+        const std::vector<uint64_t>* t1 = nullptr;
+        if (S.kind == EF_K_CONV2D) {
+          if (S.has_b) {
+            h0 = &S.hdr_b, t0 = &S.hb, h1 = &S.hdr_w, t1 = &S.hw;
+          } else {
+            h0 = &S.hdr_w, t0 = &S.hw;
+          }
+        } else if (S.kind == EF_K_BATCHNORM) {
+          h0 = &S.hdr_w, t0 = &S.hw, h1 = &S.hdr_b, t1 = &S.hb;
+        } else if (S.kind == EF_K_MATMUL) {
+          h0 = &S.hdr_w, t0 = &S.hw;
         }
-      } else if (S.kind == EF_K_BATCHNORM) {
-        J.t0 = pw;
-        J.n0 = S.w_n;
-        J.t1 = pb;
-        J.n1 = S.b_n;
-      } else if (S.kind == EF_K_MATMUL) {
-        J.t0 = pw;
-        J.n0 = S.w_n;
+        B2b st;
+        st.init(16);
+        for (const auto& [h, t] : {std::make_pair(h0, t0), std::make_pair(h1, t1)}) {
+          if (h) st.bytes(reinterpret_cast<const uint8_t*>(h->data()), (uint32_t)h->size());
+          if (t)
+            for (uint64_t x : *t) st.word_le(x);
+        }
+        st.final();
+        ctx->h_ws_digest[2 * i] = st.h[0];
+        ctx->h_ws_digest[2 * i + 1] = st.h[1];
       }
-      J.out = ctx->d_ws_digest.p + 2 * pending[j];
-      jobs.push_back(J);
+    };
+    const size_t nt = std::min<size_t>(pending.size(), std::max(1u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (size_t t = 1; t < nt; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& t : pool) t.join();
+    EF_CUDA(cudaMemcpyAsync(ctx->d_ws_digest.p, ctx->h_ws_digest.data(), 2 * nw * 8, cudaMemcpyHostToDevice, ctx->st));
+    for (uint32_t i : pending) {
+      WeightSet& S = ctx->ws[i];
+      std::vector<uint64_t>().swap(S.hw);
+      std::vector<uint64_t>().swap(S.hb);
     }
-    DevBuf<DigestJob> dj;
-    EF_CUDA(dj.reserve(jobs.size(), ctx->st));
-    EF_CUDA(cudaMemcpyAsync(dj.p, jobs.data(), jobs.size() * sizeof(DigestJob), cudaMemcpyHostToDevice, ctx->st));
-    k_digest<<<(unsigned)((jobs.size() + 31) / 32), 32, 0, ctx->st>>>(dj.p, (uint32_t)jobs.size());
-    EF_CUDA(cudaGetLastError());
-    EF_CUDA(cudaStreamSynchronize(ctx->st));
-    dj.release();
     for (uint32_t i : pending) ctx->ws[i].ready = true;
   }
   EF_CUDA(cudaStreamSynchronize(ctx->st));

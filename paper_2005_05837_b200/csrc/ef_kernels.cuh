@@ -13,8 +13,8 @@
 //   price_d1 /     the reference's first-improvement sweep (search.py:106-153) with CPython's
 //   price_graph    Neumaier sum for the start totals; every floating-point operation in the
 //                  reference's order, no FMA contraction (the library builds with --fmad=false).
-//   k_derive /     derived weight tensors (rules.py:231-232, 272-276, 326-327) and BLAKE2b
-//   k_digest       digests of weight sets (graph.py:510-517).
+//   k_derive       derived weight tensors (rules.py:231-232, 272-276, 326-327); their BLAKE2b
+//                  digests (graph.py:510-517) are taken on host cores (ef_tables_commit).
 #pragma once
 #include <stdint.h>
 
@@ -1190,86 +1190,6 @@ __global__ void k_copy_records(const unsigned long long* src, const unsigned lon
     const uint4* s = reinterpret_cast<const uint4*>(src[r]);
     uint4* d = reinterpret_cast<uint4*>(dst[r]);
     for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) d[i] = s[i];
-  }
-}
-
-// one weight set to digest: [hdr0 bytes][t0 float64s][hdr1 bytes][t1 float64s]
-struct DigestJob {
-  const uint8_t* hdr0;
-  uint32_t hlen0;
-  const double* t0;
-  uint64_t n0;
-  const uint8_t* hdr1;
-  uint32_t hlen1;
-  const double* t1;
-  uint64_t n1;
-  uint64_t* out;  // 2 words
-};
-
-// Append a float64 tensor to a BLAKE2b stream.  The header in front of the tensor fixes
-// its byte misalignment s (0..7) for the whole tensor, so once the stream sits at a block
-// boundary every further 128-byte block is 16 funnel-shifted tensor words assembled in
-// registers: one compression plus 16 loads per block instead of 16 generic appends.
-__device__ __forceinline__ void digest_tensor(B2b& st, const unsigned long long* w, uint64_t n) {
-  uint64_t i = 0;
-  while (i < n) {
-    if (st.fill == 128 && n - i >= 16) {
-      // aligned: a full block is pending and at least 16 more words follow it; the next
-      // block's words are loaded before the pending block is compressed (latency hidden)
-      do {
-        uint64_t nx[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) nx[q] = __ldg(w + i + q);
-        st.t += 128;
-        b2b_compress(st.h, st.m, st.t, false);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) st.m[q] = nx[q];
-        i += 16;
-      } while (n - i >= 16);
-      continue;  // the pending block is flushed by the next append or by final()
-    }
-    if (st.fill > 0 && st.fill < 8 && n - i >= 16) {
-      // just crossed a boundary: the block holds the s carried bytes of the previous word
-      const uint32_t s8 = 8 * st.fill, r8 = 64 - s8;
-      uint64_t carry = st.m[0];
-      uint64_t cur[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) cur[q] = __ldg(w + i + q);
-      do {
-        uint64_t mw[16];
-        mw[0] = carry | (cur[0] << s8);
-#pragma unroll
-        for (int q = 1; q < 16; ++q) mw[q] = (cur[q - 1] >> r8) | (cur[q] << s8);
-        carry = cur[15] >> r8;
-        i += 16;
-        if (n - i >= 16) {
-#pragma unroll
-          for (int q = 0; q < 16; ++q) cur[q] = __ldg(w + i + q);
-        }
-        st.t += 128;
-        b2b_compress(st.h, mw, st.t, false);  // the carried bytes follow: never the last block
-      } while (n - i >= 16);
-      st.m[0] = carry;
-#pragma unroll
-      for (int q = 1; q < 16; ++q) st.m[q] = 0;
-      continue;
-    }
-    st.word_le(w[i++]);
-  }
-}
-
-__global__ void k_digest(const DigestJob* jobs, uint32_t n) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const DigestJob J = jobs[j];
-    B2b st;
-    st.init(16);
-    st.bytes(J.hdr0, J.hlen0);
-    digest_tensor(st, reinterpret_cast<const unsigned long long*>(J.t0), J.n0);
-    st.bytes(J.hdr1, J.hlen1);
-    digest_tensor(st, reinterpret_cast<const unsigned long long*>(J.t1), J.n1);
-    st.final();
-    J.out[0] = st.h[0];
-    J.out[1] = st.h[1];
   }
 }
 

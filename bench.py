@@ -63,6 +63,28 @@ RULES = ["fuse-conv-relu", "split-conv-activation", "merge-parallel-convs", "spl
          "fuse-conv-batchnorm"]
 
 
+PROFILE = os.path.join("profiles", "ncu_r01d_kernels.json")  # the committed `ncu --set full` capture
+
+
+def _traffic(kernel: str):
+    """DRAM bytes (read + write) of one launch of `kernel` in the committed ncu capture, or None."""
+    try:
+        with open(os.path.join(ROOT, PROFILE)) as fh:
+            rows = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for r in rows:
+        if kernel in (r.get("Kernel Name") or ""):
+            tot = 0.0
+            for k, v in r.items():
+                if k.startswith("dram__bytes_read.sum") or k.startswith("dram__bytes_write.sum"):
+                    unit = k.split("[")[-1].rstrip("]").strip() if "[" in k else "byte"
+                    tot += float(v) * scale.get(unit, 1)
+            return tot
+    return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -432,6 +454,7 @@ def run_ours(args, world, rank, local):
     # refsrc words (4 B) read; the 16-byte key and its 12-byte sort record written
     jobs = kcomp / args.steps
     keys_bytes = jobs * (16 + 1.1 * (16 + 4) + 16 + 12)
+    keys_traffic = _traffic("k_keys<128>")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -445,13 +468,15 @@ def run_ours(args, world, rank, local):
                    else "single GPU"},
         "stages_ms_per_step": {n: stage_ms[k] / args.steps for k, n in enumerate(names)},
         "roofline": {"bound": "alu", "kernel": "k_keys", "achieved": achieved_c / 1e9, "peak": peak_c / 1e9,
-                     "unit": "Gcompressions/s", "frac": achieved_c / peak_c, "traffic": None,
+                     "unit": "Gcompressions/s", "frac": achieved_c / peak_c, "traffic": keys_traffic,
+                     "traffic_unit": "bytes per launch (dram read + write)", "traffic_source": PROFILE,
                      "peak_source": "measured live: ef_b2b_peak (register-only BLAKE2b loop, same GPU)",
                      "compressions_per_step": kcomp / args.steps,
                      "digest_compressions_per_step": dcomp / args.steps},
         "roofline_hbm": {"bound": "hbm", "kernel": "k_keys", "achieved": keys_bytes / (keys_ms / 1e3) / 1e9,
                          "peak": hbm_peak, "unit": "GB/s", "frac": keys_bytes / (keys_ms / 1e3) / 1e9 / hbm_peak,
-                         "peak_source": hbm_src, "traffic": None},
+                         "peak_source": hbm_src, "traffic": keys_traffic, "traffic_source": PROFILE,
+                         "algorithmic_bytes": keys_bytes},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(blob.nbytes),
                 "d2h_bytes_per_step": n_cand * N.CAND_DTYPE.itemsize, "ms_per_step": e2e_total / args.steps,
                 "mode": "pipelined: batch i+1 uploaded and hashed on the upload stream during step i, the results "

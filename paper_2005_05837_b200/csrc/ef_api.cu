@@ -153,6 +153,8 @@ struct ef_ctx {
   DevBuf<uint8_t> d_alg8;
   Scratch sc[2];
   cudaStream_t st_up = nullptr;  // asynchronous uploads
+  cudaStream_t st_wide = nullptr;  // k_keys_wide beside k_keys
+  cudaEvent_t ev_w0 = nullptr, ev_w1 = nullptr;
   cudaEvent_t ev_up = nullptr;    // end of the last asynchronous upload (upload stream)
   cudaEvent_t ev_main = nullptr;  // main-stream work an upload must not overtake
   DevBuf<char> d_up_stage;
@@ -242,6 +244,9 @@ ef_ctx* ef_create(int device) {
   if (const char* e = getenv("EF_CHUNK_MIB")) ctx->chunk_mib = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
   cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
   cudaStreamCreateWithFlags(&ctx->st_up, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&ctx->st_wide, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&ctx->ev_w0, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ctx->ev_w1, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&ctx->st_copy, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&ctx->ev_snap, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming);
@@ -316,6 +321,9 @@ void ef_destroy(ef_ctx* ctx) {
   if (ctx->ev_up) cudaEventDestroy(ctx->ev_up);
   if (ctx->ev_main) cudaEventDestroy(ctx->ev_main);
   if (ctx->st_up) cudaStreamDestroy(ctx->st_up);
+  if (ctx->st_wide) cudaStreamDestroy(ctx->st_wide);
+  if (ctx->ev_w0) cudaEventDestroy(ctx->ev_w0);
+  if (ctx->ev_w1) cudaEventDestroy(ctx->ev_w1);
   if (ctx->st_copy) cudaStreamDestroy(ctx->st_copy);
   if (ctx->ev_snap) cudaEventDestroy(ctx->ev_snap);
   if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
@@ -799,7 +807,16 @@ static uint32_t bits_for(uint32_t v);
 // node keys: a thread per candidate when the chunk fills the GPU, four lanes per candidate
 // (lower latency per compression) when it does not
 static int launch_keys(ef_ctx* ctx, cudaStream_t st, const VArgs& V) {
-  if (V.wide_min) {  // large graphs: the longest candidates a warp each, level by level
+  const bool wide = V.wide_min && st == ctx->st;
+  if (wide) {  // large graphs: the longest candidates a warp each, level by level, on a side
+               // stream so their few resident warps run beside k_keys instead of before it
+    EF_CUDA(cudaEventRecord(ctx->ev_w0, st));
+    EF_CUDA(cudaStreamWaitEvent(ctx->st_wide, ctx->ev_w0, 0));
+    const uint32_t gw = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
+    k_keys_wide<128><<<gw, 128, 0, ctx->st_wide>>>(V);
+    EF_CUDA(cudaGetLastError());
+    EF_CUDA(cudaEventRecord(ctx->ev_w1, ctx->st_wide));
+  } else if (V.wide_min) {
     const uint32_t gw = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
     k_keys_wide<128><<<gw, 128, 0, st>>>(V);
     EF_CUDA(cudaGetLastError());
@@ -812,6 +829,7 @@ static int launch_keys(ef_ctx* ctx, cudaStream_t st, const VArgs& V) {
     k_keys<kHashThreads><<<gd, kHashThreads, 0, st>>>(V);
   }
   EF_CUDA(cudaGetLastError());
+  if (wide) EF_CUDA(cudaStreamWaitEvent(st, ctx->ev_w1, 0));
   return EF_OK;
 }
 static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk);

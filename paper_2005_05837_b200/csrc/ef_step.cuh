@@ -14,14 +14,18 @@
 //                               topological order) serves larger parents.
 //   sort      cub radix         candidates by job count, so the lanes of a warp run the same
 //                               number of compressions
-//   k_keys    thread/candidate  one BLAKE2b-128 per job; the message is assembled in a
-//                               per-thread shared-memory column, compressed at ONE call site
-//   sort      cub segmented     every candidate's fresh keys by their first 8 bytes
-//   k_sortfix thread/candidate  orders runs of equal first words by the second word
-//   k_digest  thread/candidate  BLAKE2b-64 over input text, output keys and the merge of the
-//                               parent's sorted keys (minus removed ones) with the fresh keys
+//   k_keys    thread/candidate  one BLAKE2b-128 per job; the message is built in registers /
+//                               a per-thread shared-memory column, compressed at ONE call site
+//   k_keys_wide warp/candidate  (large graphs) candidates with >= 512 jobs, a level of their
+//                               key DAG per round, on a side stream beside k_keys
+//   k_keys_quad 4 lanes/cand.   launches too small to fill the GPU (uploads, kept records)
+//   rows <= 256: k_merge (warp/candidate: fresh keys sorted in registers, merged by rank
+//                with the parent's sorted keys minus removed ranks into a key stream)
+//   rows > 256:  k_sortkeys / cub segmented sort of the fresh keys, then k_merge_big
+//                (warp/candidate merge path) into the key stream
+//   k_digest_pm thread/candidate BLAKE2b-64 over input text, output keys and the key stream
 //                               (graph.py:541-549)
-// followed by the existing dedup kernels and k_price on the virtual view.
+// followed by the dedup kernels and k_price_v on the virtual view.
 #pragma once
 #include "ef_kernels.cuh"
 

@@ -22,7 +22,7 @@ namespace {
 constexpr int kMatchThreads = 256;
 constexpr int kMatThreads = 256;
 constexpr int kHashThreads = 128;
-constexpr int kPriceThreads = 64;
+constexpr int kPriceThreads = EF_PRICE_THREADS;
 constexpr uint32_t kFastRows = 256;  // rows (max parent nodes + 2) served by the fast step kernels
 
 template <typename T>
@@ -1342,7 +1342,7 @@ static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
   Pv.pstride = pstride_of(ctx->geo);
   Pv.alg8 = ctx->d_alg8.p;
   Pv.S = ctx->step_S;
-  const uint32_t gp = std::max<uint32_t>(1, std::min<uint32_t>((total + kPriceThreads - 1) / kPriceThreads, ctx->n_sm * 16));
+  const uint32_t gp = std::max<uint32_t>(1, std::min<uint32_t>((total + kPriceThreads - 1) / kPriceThreads, ctx->n_sm * (1024 / kPriceThreads)));
   const uint32_t* pl = ctx->d_plist.p;
   const uint32_t* pn = ctx->d_scalars.p + 7;
   const bool fast = pp->use_inner && pp->d == 1;

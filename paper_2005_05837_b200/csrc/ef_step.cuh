@@ -31,6 +31,9 @@
 
 // minimum resident CTAs per SM for the step's throughput kernels (register budgets; tuned on
 // the ResNet-50 frontier)
+#ifndef EF_PRICE_THREADS
+#define EF_PRICE_THREADS 64  // k_price_v block size (one survivor per thread)
+#endif
 #ifndef EF_MERGE_MINB
 #define EF_MERGE_MINB 6
 #endif
@@ -1997,7 +2000,7 @@ struct VPriceArgs {
 
 // one thread per survivor of the step's dedup (the compacted list); KIND < 0: any cost kind / radius
 template <int KIND, bool SM_ROW>
-__global__ void __launch_bounds__(64) k_price_v(VPriceArgs A, const uint32_t* plist, const uint32_t* plist_n) {
+__global__ void __launch_bounds__(EF_PRICE_THREADS) k_price_v(VPriceArgs A, const uint32_t* plist, const uint32_t* plist_n) {
   extern __shared__ uint8_t sm_alg[];  // SM_ROW: the sweep's row, one column per thread (S x 64 bytes)
   const Geo& G = A.pa.g;
   const uint32_t total = *plist_n;
@@ -2024,8 +2027,8 @@ __global__ void __launch_bounds__(64) k_price_v(VPriceArgs A, const uint32_t* pl
     V.n = P.n_keep + P.n_live;
     uint8_t* alg = A.alg8 + (uint64_t)c * A.S;
     if (KIND >= 0 && SM_ROW) {
-      price_d1<KIND>(A.pa, V, AlgRow{sm_alg + threadIdx.x, 64}, res, mask);
-      for (int i = 0; i < V.n; ++i) alg[i] = sm_alg[i * 64 + threadIdx.x];
+      price_d1<KIND>(A.pa, V, AlgRow{sm_alg + threadIdx.x, EF_PRICE_THREADS}, res, mask);
+      for (int i = 0; i < V.n; ++i) alg[i] = sm_alg[i * EF_PRICE_THREADS + threadIdx.x];
     } else if (KIND >= 0) {
       price_d1<KIND>(A.pa, V, AlgRow{alg, 1}, res, mask);
     } else {

@@ -265,9 +265,16 @@ def _search_e2e(ef, zoo, no_cpu: bool) -> dict:
     res = ef.outer_search(g, ef.default_rules(), ef.CostDatabase(), ef.CostFunction.energy(),
                           ef.SearchConfig(alpha=1.0), ef.SyntheticProfiler(0))
     gpu_s = time.perf_counter() - t0
+    # the same search again in this process: signatures, weight sets and their digests are
+    # already interned on the device (a search service's steady state); fresh cost database
+    t0 = time.perf_counter()
+    ef.outer_search(g, ef.default_rules(), ef.CostDatabase(), ef.CostFunction.energy(), ef.SearchConfig(alpha=1.0),
+                    ef.SyntheticProfiler(0))
+    warm_s = time.perf_counter() - t0
     out = {"config": "SqueezeNet inference graph, energy objective, alpha=1.0 (BASELINE configs[0])",
-           "gpu_s": gpu_s, "expansions": res.stats.graphs_explored, "generated": res.stats.graphs_generated,
-           "optimised_hash": ef.canonical_hash(res.graph)}
+           "gpu_s": gpu_s, "gpu_warm_s": warm_s, "expansions": res.stats.graphs_explored,
+           "generated": res.stats.graphs_generated, "optimised_hash": ef.canonical_hash(res.graph),
+           "reference_s_build_container": 28.5}
     if not no_cpu:
         from oracle import enerflow_oracle as orc
 

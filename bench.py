@@ -63,7 +63,7 @@ RULES = ["fuse-conv-relu", "split-conv-activation", "merge-parallel-convs", "spl
          "fuse-conv-batchnorm"]
 
 
-PROFILE = os.path.join("profiles", "ncu_r01d_kernels.json")  # the committed `ncu --set full` capture
+PROFILE = os.path.join("profiles", "ncu_r01f_kernels.json")  # the committed `ncu --set full` capture
 
 
 def _traffic(kernel: str):

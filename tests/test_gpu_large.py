@@ -80,3 +80,24 @@ def test_wide_level_keys_match_thread_keys(model, monkeypatch):
     assert len(out["0"]) == len(out["1"]) > 0
     for key in ("hash", "flags", "cost", "time_ms", "energy", "evals", "sweeps"):
         assert np.array_equal(out["0"][key], out["1"][key]), key
+
+
+@pytest.mark.parametrize("model", ["dag:1000", "nasnet_a"])
+def test_merge_path_stream_matches_in_thread_merge(model, monkeypatch):
+    """Rows > 256: the merge-path key stream (k_merge_big) + streaming digest against the
+    in-thread merge of k_digest (EF_BIG_MERGE=0): every candidate's hash, flags and price."""
+    import numpy as np
+
+    g0 = zoo.random_dag(1000, 0) if model.startswith("dag") else zoo.generate(model, 0)
+    out = {}
+    for big in ("0", "1"):
+        monkeypatch.setenv("EF_BIG_MERGE", big)
+        fr = Frontier(g0, ef.CostDatabase(), ef.SyntheticProfiler(0), ef.CostFunction.energy(),
+                      ef.SearchConfig(alpha=1.05), 6)
+        try:
+            out[big] = fr.step().copy()
+        finally:
+            fr.close()
+    assert len(out["0"]) == len(out["1"]) > 0
+    for key in ("hash", "flags", "cost", "time_ms", "energy", "evals", "sweeps"):
+        assert np.array_equal(out["0"][key], out["1"][key]), key

@@ -1719,9 +1719,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge_big(VArgs A) {
     };
     uint64_t a0 = 0, a1 = 0, b0 = 0, b1 = 0;
     if (i < na) a_key(r, a0, a1);
-    uint4 an = make_uint4(0, 0, 0, 0);  // the key after the current A head
-    if (i + 1 < na) an = a_raw(next_rank());
+    // the next four A keys and the next B key in flight (independent loads under the merge)
+    const uint4 z4 = make_uint4(0, 0, 0, 0);
+    uint4 an0 = i + 1 < na ? a_raw(next_rank()) : z4;
+    uint4 an1 = i + 2 < na ? a_raw(next_rank()) : z4;
+    uint4 an2 = i + 3 < na ? a_raw(next_rank()) : z4;
+    uint4 an3 = i + 4 < na ? a_raw(next_rank()) : z4;
+    const uint4* b4 = reinterpret_cast<const uint4*>(bs);
     if (j < d) b_key(j, b0, b1);
+    uint4 bn0 = j + 1 < d ? b4[j + 1] : z4;
     uint4* o4 = reinterpret_cast<uint4*>(out);
     for (uint32_t o = D; o < end; ++o) {
       const bool take_a = j >= d || (i < na && !be_less(b0, b1, a0, a1));
@@ -1729,14 +1735,21 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge_big(VArgs A) {
         const uint64_t w0 = B2b::bswap64(a0), w1 = B2b::bswap64(a1);
         o4[o] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
         if (++i < na) {
-          a0 = B2b::bswap64(((uint64_t)an.y << 32) | an.x);
-          a1 = B2b::bswap64(((uint64_t)an.w << 32) | an.z);
-          if (i + 1 < na) an = a_raw(next_rank());
+          a0 = B2b::bswap64(((uint64_t)an0.y << 32) | an0.x);
+          a1 = B2b::bswap64(((uint64_t)an0.w << 32) | an0.z);
+          an0 = an1;
+          an1 = an2;
+          an2 = an3;
+          an3 = i + 4 < na ? a_raw(next_rank()) : z4;
         }
       } else {
         const uint64_t w0 = B2b::bswap64(b0), w1 = B2b::bswap64(b1);
         o4[o] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
-        if (++j < d) b_key(j, b0, b1);
+        if (++j < d) {
+          b0 = B2b::bswap64(((uint64_t)bn0.y << 32) | bn0.x);
+          b1 = B2b::bswap64(((uint64_t)bn0.w << 32) | bn0.z);
+          bn0 = j + 1 < d ? b4[j + 1] : z4;
+        }
       }
     }
     __syncwarp();

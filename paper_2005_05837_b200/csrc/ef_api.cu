@@ -150,7 +150,7 @@ struct ef_ctx {
   DevBuf<unsigned long long> d_step_ord;
   uint32_t n_send = 0;
   DevBuf<uint32_t> d_plist, d_sig_info;
-  DevBuf<uint8_t> d_alg8;
+  DevBuf<uint8_t> d_alg8, d_algt;
   Scratch sc[2];
   cudaStream_t st_up = nullptr;  // asynchronous uploads
   cudaStream_t st_wide = nullptr;  // k_keys_wide beside k_keys
@@ -313,6 +313,7 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_plist.release();
   ctx->d_sig_info.release();
   ctx->d_alg8.release();
+  ctx->d_algt.release();
   ctx->sc[0].release();
   ctx->sc[1].release();
   ctx->d_up_stage.release();
@@ -1347,6 +1348,10 @@ static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
   const uint32_t* pn = ctx->d_scalars.p + 7;
   const bool fast = pp->use_inner && pp->d == 1;
   const bool sm = ctx->step_S <= kFastRows;  // the sweep's algorithm row in shared memory
+  if (!sm) {  // the interleaved sweep rows of k_price_v, one per thread of the grid
+    EF_CUDA(ctx->d_algt.reserve((uint64_t)gp * kPriceThreads * ctx->step_S, ctx->st));
+    Pv.algt = ctx->d_algt.p;
+  }
   const size_t smem = sm ? (size_t)ctx->step_S * kPriceThreads : 0;
 #define EF_PRICE(K)                                                                                        \
   do {                                                                                                     \

@@ -1376,7 +1376,8 @@ static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
 // synchronise; EF_NEED_RESOLVE when the plans asked for signatures / weight sets
 static int step_sync(ef_ctx* ctx, bool timings) {
   EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
-  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  if (timings) EF_CUDA(cudaMemcpyAsync(ctx->last_stats, ctx->d_stats.p, 2 * 8, cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaStreamSynchronize(ctx->st));  // one round trip for the scalars and the counters
   const uint32_t err = ctx->h_scalars[1];
   ctx->last_req_sig = ctx->h_scalars[2];
   ctx->last_req_dv = ctx->h_scalars[3];
@@ -1398,8 +1399,6 @@ static int step_sync(ef_ctx* ctx, bool timings) {
     ctx->last_ms[6] = ms[3];
     ctx->last_ms[7] = ms[4];
     cudaEventElapsedTime(&ctx->last_ms[8], ctx->ev[0], ctx->ev[5]);  // the whole step (incl. any exchange)
-    EF_CUDA(cudaMemcpyAsync(ctx->last_stats, ctx->d_stats.p, 2 * 8, cudaMemcpyDeviceToHost, ctx->st));
-    EF_CUDA(cudaStreamSynchronize(ctx->st));
     ctx->last_stats[2] = ctx->last_total;
     ctx->last_stats[3] = ctx->h_scalars[7];
   }

@@ -693,9 +693,14 @@ __global__ void __launch_bounds__(BT, EF_KEYS_MINB) k_keys(VArgs A) {
     uint32_t* sval = A.sval + (uint64_t)lc * A.S;
     uint32_t ncomp = 0;
     uint64_t last0 = 0, last1 = 0;
+    // the next job's descriptor and text metadata are fetched one job ahead (their dependent
+    // loads run under the current compression)
+    Job jn = jobs[0];
+    uint32_t tl_n = T.sig_text_len[jn.sig], to_n = T.sig_text_off[jn.sig];
     for (uint32_t jj = 0; jj < d; ++jj) {
-      const Job jb = jobs[jj];
-      const uint32_t tlen = T.sig_text_len[jb.sig];
+      const Job jb = jn;
+      const uint32_t tlen = tl_n, toff = to_n;
+      if (jj + 1 < d) jn = jobs[jj + 1];
       const bool input = jb.nin & kInputJob;
       const uint32_t nin = input ? 0u : jb.nin;
       const uint32_t nlen = input ? T.name_len[jb.aux] : 0u;
@@ -706,7 +711,7 @@ __global__ void __launch_bounds__(BT, EF_KEYS_MINB) k_keys(VArgs A) {
         h[0] = ks.a;
         h[1] = ks.b;
       } else {
-        const uint64_t* tw = reinterpret_cast<const uint64_t*>(T.sig_text + T.sig_text_off[jb.sig]);
+        const uint64_t* tw = reinterpret_cast<const uint64_t*>(T.sig_text + toff);
         const uint32_t ws = input ? kEmptyWset : jb.aux;
         auto src = [&](uint32_t k, uint64_t& k0, uint64_t& k1) -> uint32_t {
           const uint32_t sv = rs[jb.roff + k];
@@ -753,10 +758,18 @@ __global__ void __launch_bounds__(BT, EF_KEYS_MINB) k_keys(VArgs A) {
         }
         const uint32_t nb = (len + 127u) >> 7;
         for (uint32_t q = nw; q < 16u * nb; ++q) col[q * BT] = 0;
+        if (jj + 1 < d) {
+          tl_n = T.sig_text_len[jn.sig];
+          to_n = T.sig_text_off[jn.sig];
+        }
         b2b_start(h, 16);
         ncomp += nb;
         for (uint32_t b = 0; b < nb; ++b)
           b2b_compress_col<BT>(h, col + 16 * b * BT, (uint64_t)min(len, 128u * (b + 1)), b + 1 == nb);
+      }
+      if (len > 8u * kKeyMaxW && jj + 1 < d) {
+        tl_n = T.sig_text_len[jn.sig];
+        to_n = T.sig_text_off[jn.sig];
       }
       fresh[2 * jj] = h[0];
       fresh[2 * jj + 1] = h[1];

@@ -1348,7 +1348,9 @@ static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
   const uint32_t* pn = ctx->d_scalars.p + 7;
   const bool fast = pp->use_inner && pp->d == 1;
   const bool sm = ctx->step_S <= kFastRows;  // the sweep's algorithm row in shared memory
-  if (!sm) {  // the interleaved sweep rows of k_price_v, one per thread of the grid
+  Pv.algt = nullptr;
+  if (!sm && ctx->step_S <= 2048) {  // the interleaved sweep rows of k_price_v, one per thread of
+                                     // the grid (beyond 2k-slot rows the scratch outgrows L2: slower)
     EF_CUDA(ctx->d_algt.reserve((uint64_t)gp * kPriceThreads * ctx->step_S, ctx->st));
     Pv.algt = ctx->d_algt.p;
   }

@@ -2056,11 +2056,13 @@ __global__ void __launch_bounds__(EF_PRICE_THREADS) k_price_v(VPriceArgs A, cons
     if (KIND >= 0 && SM_ROW) {
       price_d1<KIND>(A.pa, V, AlgRow{sm_alg + threadIdx.x, EF_PRICE_THREADS}, res, mask);
       for (int i = 0; i < V.n; ++i) alg[i] = sm_alg[i * EF_PRICE_THREADS + threadIdx.x];
-    } else if (KIND >= 0) {  // the row interleaved across the warp: the sweep's accesses coalesce
+    } else if (KIND >= 0 && A.algt) {  // the row interleaved across the warp: accesses coalesce
       const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
       uint8_t* col = A.algt + (uint64_t)(gt >> 5) * 32u * A.S + (gt & 31u);
       price_d1<KIND>(A.pa, V, AlgRow{col, 32}, res, mask);
       for (int i = 0; i < V.n; ++i) alg[i] = col[i * 32];
+    } else if (KIND >= 0) {
+      price_d1<KIND>(A.pa, V, AlgRow{alg, 1}, res, mask);
     } else {
       price_graph(A.pa, V, alg, res);
     }

@@ -254,7 +254,7 @@ __global__ void k_dirty(VArgs A) {
     // levels for k_keys_wide (only when this candidate can reach its job threshold): by job in
     // jlvl, by parent position in the (step-mode idle) jv row, read beside didx so the level
     // costs no extra dependent load
-    const bool levels = A.jlvl && (uint32_t)pn + 2u >= A.wide_min;
+    const bool levels = A.jlvl && (uint32_t)(pn - max(P.first, 0)) + 2u >= A.wide_min;  // jobs <= slots from first on
     uint16_t* lv = levels ? A.jlvl + (uint64_t)lc * A.S : nullptr;
     uint32_t* plv = A.jv + (uint64_t)lc * A.S;
     uint32_t lvl = 0;  // level of the job being emitted

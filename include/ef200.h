@@ -105,6 +105,13 @@ typedef struct {
   int32_t use_inner;  /* 0: default assignment only (search.py:196-202) */
   int32_t node_cap;   /* compute-node cap (search.py:205-208) */
   double w, ct, ce, cp, t_ref, e_ref, p_ref;
+  /* alpha-prune of the step (search.py:258-267): over the priced candidates in (parent, rule,
+   * site) order, prev = min(best, costs of the priced candidates before it); EF_F_BEST marks
+   * cost < prev, EF_F_ENQUEUE cost < alpha * prev.  alpha = 0: no prune flags. */
+  double best, alpha;
+  /* start totals: 0 = CPython >= 3.12 sum() (Neumaier-compensated), 1 = plain left-to-right sum
+   * (CPython <= 3.11), so the sweep starts from the totals the caller's interpreter computes */
+  int32_t naive_sum, pad_;
 } ef_price_params;
 
 /* Per-candidate result of one expansion step, in (parent, rule, site) order. */
@@ -114,7 +121,9 @@ enum {
   EF_F_CAPPED = 4,    /* compute-node count above the cap               (search.py:252)  */
   EF_F_PRICED = 8,    /* inner search ran                                                */
   EF_F_MISSING = 16,  /* some node has no cost rows (MissingEntry)                        */
-  EF_F_INCOMPLETE = 32
+  EF_F_INCOMPLETE = 32,
+  EF_F_BEST = 64,     /* priced, cost < the best before it              (search.py:259-261)  */
+  EF_F_ENQUEUE = 128  /* priced, cost < alpha * the best before it      (search.py:262-267)  */
 };
 typedef struct {
   uint64_t hash;
@@ -166,6 +175,9 @@ int ef_set_geometry(ef_ctx* ctx, uint32_t cap_nodes, uint32_t cap_refs, uint32_t
                     const char* input_text, uint32_t input_text_len, ef_geometry* out);
 int ef_record_alloc(ef_ctx* ctx, uint32_t* slot);
 int ef_record_free(ef_ctx* ctx, uint32_t slot);
+/* n slots at once (the search materialises and releases candidates in batches) */
+int ef_records_alloc(ef_ctx* ctx, uint32_t n, uint32_t* slots);
+int ef_records_free(ef_ctx* ctx, const uint32_t* slots, uint32_t n);
 int ef_record_write(ef_ctx* ctx, uint32_t slot, const void* host, uint64_t bytes);
 int ef_record_read(ef_ctx* ctx, uint32_t slot, void* host, uint64_t bytes);
 /* batched upload: record i comes from host + i * stride (one stream sync for all) */
@@ -181,9 +193,15 @@ int ef_price_records(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const ef_pr
                      ef_cand_result* out);
 
 /* ---- visited set ---------------------------------------------------------- */
+/* The reference's `visited` Python set (search.py:241-251).  An open-addressing table of 64-bit
+ * hashes that the library keeps at most half full: every insertion path (ef_visited_insert,
+ * ef_expand with insert_visited, ef_owner_mark) first grows it by rehashing on the device, so
+ * `capacity` is only the initial size.  Probe loops are bounded; a full table is reported as an
+ * error, never a hang. */
 int ef_visited_reset(ef_ctx* ctx, uint64_t capacity);
 int ef_visited_insert(ef_ctx* ctx, const uint64_t* hashes, uint32_t n);
 int ef_visited_count(ef_ctx* ctx, uint64_t* count);
+int ef_visited_capacity(ef_ctx* ctx, uint64_t* capacity);
 
 /* ---- the hot path ---------------------------------------------------------- */
 /* One frontier step: match every rule at every site of every parent

@@ -19,7 +19,7 @@ EF_OK = 0
 EF_NEED_RESOLVE = 1
 
 # flags of ef_cand_result (ef200.h)
-F_FIRST, F_VISITED, F_CAPPED, F_PRICED, F_MISSING, F_INCOMPLETE = 1, 2, 4, 8, 16, 32
+F_FIRST, F_VISITED, F_CAPPED, F_PRICED, F_MISSING, F_INCOMPLETE, F_BEST, F_ENQUEUE = 1, 2, 4, 8, 16, 32, 64, 128
 
 # weight-set derivations
 D_MERGE, D_SLICE_LO, D_SLICE_HI, D_FOLD = 1, 2, 3, 4
@@ -46,7 +46,8 @@ class Geometry(C.Structure):
 class PriceParams(C.Structure):
     _fields_ = [("kind", C.c_int32), ("d", C.c_int32), ("use_inner", C.c_int32), ("node_cap", C.c_int32),
                 ("w", C.c_double), ("ct", C.c_double), ("ce", C.c_double), ("cp", C.c_double),
-                ("t_ref", C.c_double), ("e_ref", C.c_double), ("p_ref", C.c_double)]
+                ("t_ref", C.c_double), ("e_ref", C.c_double), ("p_ref", C.c_double),
+                ("best", C.c_double), ("alpha", C.c_double), ("naive_sum", C.c_int32), ("pad_", C.c_int32)]
 
 
 class CandResult(C.Structure):
@@ -91,6 +92,8 @@ _PROTOS = {
                                   C.POINTER(Geometry)]),
     "ef_record_alloc": (C.c_int, [_P, _U32P]),
     "ef_record_free": (C.c_int, [_P, C.c_uint32]),
+    "ef_records_alloc": (C.c_int, [_P, C.c_uint32, _U32P]),
+    "ef_records_free": (C.c_int, [_P, _U32P, C.c_uint32]),
     "ef_record_write": (C.c_int, [_P, C.c_uint32, C.c_void_p, C.c_uint64]),
     "ef_record_read": (C.c_int, [_P, C.c_uint32, C.c_void_p, C.c_uint64]),
     "ef_records_write": (C.c_int, [_P, _U32P, C.c_uint32, C.c_void_p, C.c_uint64, C.c_uint64]),
@@ -101,6 +104,7 @@ _PROTOS = {
     "ef_visited_reset": (C.c_int, [_P, C.c_uint64]),
     "ef_visited_insert": (C.c_int, [_P, _U64P, C.c_uint32]),
     "ef_visited_count": (C.c_int, [_P, _U64P]),
+    "ef_visited_capacity": (C.c_int, [_P, _U64P]),
     "ef_expand": (C.c_int, [_P, _U32P, C.c_uint32, _I32P, C.c_uint32, C.POINTER(PriceParams), C.c_int, _U32P]),
     "ef_pending": (C.c_int, [_P, C.POINTER(SigDesc), C.c_uint32, _U32P, _I32P, C.c_uint32, _U32P]),
     "ef_results": (C.c_int, [_P, C.c_void_p, C.c_uint32]),

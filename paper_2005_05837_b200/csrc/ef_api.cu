@@ -164,10 +164,14 @@ struct ef_ctx {
   StepArgs last_step{};
   DevBuf<uint32_t> d_sel;
   DevBuf<unsigned long long> d_dst;
+  DevBuf<double> d_tile;  // alpha-prune tile minima
 
-  // visited set
+  // visited set (kept at most half full: vis_reserve grows it by rehashing)
   DevBuf<unsigned long long> d_vis, d_vis_count;
+  DevBuf<uint32_t> d_vis_err;
   uint32_t vis_mask = 0;
+  uint64_t vis_bound = 0;        // upper bound of the stored hashes (exact after every synchronised insert)
+  unsigned long long* h_vis = nullptr;  // pinned: count, err
 
   cudaEvent_t ev[6] = {};
   std::vector<cudaEvent_t> ev_chunk;  // 5 per hashing chunk: dirty | keys | sort | digest
@@ -305,6 +309,9 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_sperm.release();
   ctx->d_vis.release();
   ctx->d_vis_count.release();
+  ctx->d_vis_err.release();
+  ctx->d_tile.release();
+  if (ctx->h_vis) cudaFreeHost(ctx->h_vis);
   ctx->d_plan.release();
   ctx->d_route.release();
   ctx->d_stats.release();
@@ -785,6 +792,20 @@ int ef_record_free(ef_ctx* ctx, uint32_t slot) {
   return EF_OK;
 }
 
+int ef_records_alloc(ef_ctx* ctx, uint32_t n, uint32_t* slots) {
+  for (uint32_t i = 0; i < n; ++i) {
+    int rc = ef_record_alloc(ctx, slots + i);
+    if (rc) return rc;
+  }
+  return EF_OK;
+}
+
+int ef_records_free(ef_ctx* ctx, const uint32_t* slots, uint32_t n) {
+  for (uint32_t i = 0; i < n; ++i) EF_REQUIRE(slots[i] < ctx->n_slots, "ef_records_free: bad slot");
+  ctx->free_slots.insert(ctx->free_slots.end(), slots, slots + n);
+  return EF_OK;
+}
+
 int ef_record_write(ef_ctx* ctx, uint32_t slot, const void* host, uint64_t bytes) {
   EF_REQUIRE(slot < ctx->n_slots && bytes <= ctx->geo.bytes, "ef_record_write: bad slot/size");
   EF_CUDA(cudaMemcpyAsync(slot_addr(ctx, slot), host, bytes, cudaMemcpyHostToDevice, ctx->st));
@@ -956,26 +977,79 @@ int ef_price_records(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const ef_pr
 // visited set
 // ---------------------------------------------------------------------------------------------
 
+static constexpr uint64_t kVisMaxSlots = 1ull << 31;  // 16 GiB of keys; the mask is 32-bit
+
 int ef_visited_reset(ef_ctx* ctx, uint64_t capacity) {
+  EF_REQUIRE(capacity <= kVisMaxSlots, "ef_visited_reset: capacity above 2^31 slots");
   uint32_t cap = pow2_at_least(std::max<uint64_t>(capacity, 1024));
+  if (!ctx->h_vis) EF_CUDA(cudaMallocHost(&ctx->h_vis, 16));
   EF_CUDA(ctx->d_vis.reserve(cap, ctx->st));
   EF_CUDA(ctx->d_vis_count.reserve(1, ctx->st));
+  EF_CUDA(ctx->d_vis_err.reserve(1, ctx->st));
   EF_CUDA(cudaMemsetAsync(ctx->d_vis.p, 0, (size_t)cap * 8, ctx->st));
   EF_CUDA(cudaMemsetAsync(ctx->d_vis_count.p, 0, 8, ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_vis_err.p, 0, 4, ctx->st));
   ctx->vis_mask = cap - 1;
+  ctx->vis_bound = 0;
   EF_CUDA(cudaStreamSynchronize(ctx->st));
   return EF_OK;
+}
+
+// after a synchronised insert: exact count, and a full table is an error (never with vis_reserve)
+static int vis_settle(ef_ctx* ctx) {
+  EF_CUDA(cudaMemcpyAsync(ctx->h_vis, ctx->d_vis_count.p, 8, cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaMemcpyAsync(ctx->h_vis + 1, ctx->d_vis_err.p, 4, cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  ctx->vis_bound = ctx->h_vis[0];
+  EF_REQUIRE(!((uint32_t)ctx->h_vis[1] & 8u), "visited set full");
+  return EF_OK;
+}
+
+// Room for `more` insertions at a load factor of at most 1/2: the table doubles (or more) by
+// rehashing every stored key on the device.  Between synchronised inserts vis_bound is an upper
+// bound, so this costs a host round trip only when the bound says the table may be filling up.
+static int vis_reserve(ef_ctx* ctx, uint64_t more) {
+  const uint64_t cap = (uint64_t)ctx->vis_mask + 1;
+  if (2 * (ctx->vis_bound + more) <= cap) return EF_OK;
+  int rc = vis_settle(ctx);
+  if (rc) return rc;
+  const uint64_t need = ctx->vis_bound + more;
+  if (2 * need <= cap) return EF_OK;
+  uint64_t ncap = cap;
+  while (2 * need > ncap) ncap *= 2;
+  EF_REQUIRE(ncap <= kVisMaxSlots, "visited set above 2^30 hashes");
+  unsigned long long* q = nullptr;
+  EF_CUDA(cudaMalloc(&q, ncap * 8));
+  EF_CUDA(cudaMemsetAsync(q, 0, ncap * 8, ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_vis_count.p, 0, 8, ctx->st));
+  const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((cap + 255) / 256, ctx->n_sm * 16ull));
+  k_visited_rehash<<<grid, 256, 0, ctx->st>>>(ctx->d_vis.p, cap, q, (uint32_t)(ncap - 1), ctx->d_vis_count.p,
+                                              ctx->d_vis_err.p);
+  EF_CUDA(cudaGetLastError());
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  cudaFree(ctx->d_vis.p);
+  ctx->d_vis.p = q;
+  ctx->d_vis.cap = ncap;
+  ctx->vis_mask = (uint32_t)(ncap - 1);
+  return vis_settle(ctx);
 }
 
 int ef_visited_insert(ef_ctx* ctx, const uint64_t* hashes, uint32_t n) {
   EF_REQUIRE(ctx->vis_mask, "visited set not initialised");
   if (!n) return EF_OK;
+  int rc = vis_reserve(ctx, n);
+  if (rc) return rc;
   EF_CUDA(ctx->d_hash_out.reserve(n, ctx->st));
   EF_CUDA(cudaMemcpyAsync(ctx->d_hash_out.p, hashes, n * 8, cudaMemcpyHostToDevice, ctx->st));
   k_visited_put<<<(n + 255) / 256, 256, 0, ctx->st>>>(ctx->d_vis.p, ctx->vis_mask, ctx->d_vis_count.p,
-                                                       ctx->d_hash_out.p, n);
+                                                       ctx->d_hash_out.p, n, ctx->d_vis_err.p);
   EF_CUDA(cudaGetLastError());
-  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return vis_settle(ctx);
+}
+
+int ef_visited_capacity(ef_ctx* ctx, uint64_t* capacity) {
+  EF_REQUIRE(ctx->vis_mask && capacity, "visited set not initialised");
+  *capacity = (uint64_t)ctx->vis_mask + 1;
   return EF_OK;
 }
 
@@ -1310,6 +1384,7 @@ static DedupArgs dedup_args(ef_ctx* ctx, const ef_price_params* pp, int insert_v
   D.node_cap = pp ? pp->node_cap : 0;
   D.plist = ctx->d_plist.p;
   D.plist_n = ctx->d_scalars.p + 7;
+  D.err = ctx->d_vis_err.p;
   return D;
 }
 
@@ -1375,6 +1450,21 @@ static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
   return EF_OK;
 }
 
+// 6) the alpha-prune flags over the priced candidates (search.py:258-267), in step order
+static int step_prune(ef_ctx* ctx, const ef_price_params* pp) {
+  const uint32_t total = ctx->last_total;
+  if (!(pp->alpha > 0.0) || !total) return EF_OK;
+  constexpr int BT = 512;
+  const uint32_t tiles = (total + BT - 1) / BT;
+  EF_CUDA(ctx->d_tile.reserve(tiles, ctx->st));
+  k_prune_tiles<BT><<<tiles, BT, 0, ctx->st>>>(ctx->d_res.p, total, ctx->d_tile.p);
+  k_prune_scan<BT><<<1, BT, 0, ctx->st>>>(ctx->d_tile.p, tiles, pp->best);
+  k_prune_flags<BT><<<tiles, BT, 0, ctx->st>>>(ctx->d_res.p, total, ctx->d_tile.p, pp->alpha);
+  EF_CUDA(cudaGetLastError());
+  cudaEventRecord(ctx->ev[5], ctx->st);  // the price stage includes the prune
+  return EF_OK;
+}
+
 // synchronise; EF_NEED_RESOLVE when the plans asked for signatures / weight sets
 static int step_sync(ef_ctx* ctx, bool timings) {
   EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
@@ -1410,12 +1500,13 @@ static int step_sync(ef_ctx* ctx, bool timings) {
 }
 
 static int insert_firsts(ef_ctx* ctx) {
+  int rc = vis_reserve(ctx, ctx->last_total);
+  if (rc) return rc;
   DedupArgs D = dedup_args(ctx, nullptr, 1, ctx->last_total);
   const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((ctx->last_total + 255) / 256, ctx->n_sm * 8));
   k_visited_insert<<<grid_t, 256, 0, ctx->st>>>(D);
   EF_CUDA(cudaGetLastError());
-  EF_CUDA(cudaStreamSynchronize(ctx->st));
-  return EF_OK;
+  return vis_settle(ctx);
 }
 
 static int step_begin(ef_ctx* ctx, uint32_t* n_candidates, uint32_t n_rules) {
@@ -1434,7 +1525,7 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
   if (rc) return rc;
   uint32_t total = 0;
   if ((rc = step_hash(ctx, parent_slots, n_parents, rules, n_rules, &total))) return rc;
-  if ((rc = step_dedup_local(ctx, pp)) || (rc = step_price(ctx, pp))) return rc;
+  if ((rc = step_dedup_local(ctx, pp)) || (rc = step_price(ctx, pp)) || (rc = step_prune(ctx, pp))) return rc;
   rc = step_sync(ctx, true);
   *n_candidates = total;
   if (rc) return rc;
@@ -1485,20 +1576,23 @@ int ef_route_owners(ef_ctx* ctx, uint32_t world, uint64_t order_base, uint64_t* 
 int ef_owner_mark(ef_ctx* ctx, const uint64_t* d_recv, uint32_t n_recv, uint32_t* d_verdict, int insert_visited) {
   EF_REQUIRE(ctx->vis_mask, "visited set not initialised");
   if (!n_recv) return EF_OK;
+  if (insert_visited) {
+    int rc = vis_reserve(ctx, n_recv);
+    if (rc) return rc;
+  }
   const uint32_t tcap = pow2_at_least(2ull * std::max<uint32_t>(n_recv, 1024));
   EF_CUDA(ctx->d_step_key.reserve(tcap, ctx->st));
   EF_CUDA(ctx->d_step_ord.reserve(tcap, ctx->st));
   EF_CUDA(cudaMemsetAsync(ctx->d_step_key.p, 0, (size_t)tcap * 8, ctx->st));
   EF_CUDA(cudaMemsetAsync(ctx->d_step_ord.p, 0xff, (size_t)tcap * 8, ctx->st));
   OwnerArgs O{d_recv, n_recv, d_verdict, ctx->d_step_key.p, ctx->d_step_ord.p, tcap - 1, ctx->d_vis.p, ctx->vis_mask,
-              ctx->d_vis_count.p};
+              ctx->d_vis_count.p, ctx->d_vis_err.p};
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((n_recv + 255) / 256, ctx->n_sm * 8));
   k_owner_claim<<<grid, 256, 0, ctx->st>>>(O);
   k_owner_resolve<<<grid, 256, 0, ctx->st>>>(O);
   if (insert_visited) k_owner_insert<<<grid, 256, 0, ctx->st>>>(O);
   EF_CUDA(cudaGetLastError());
-  EF_CUDA(cudaStreamSynchronize(ctx->st));
-  return EF_OK;
+  return insert_visited ? vis_settle(ctx) : (cudaStreamSynchronize(ctx->st) == cudaSuccess ? EF_OK : EF_ERR_CUDA);
 }
 
 int ef_expand_finish(ef_ctx* ctx, const uint32_t* d_verdict_back, const ef_price_params* pp) {
@@ -1515,7 +1609,7 @@ int ef_expand_finish(ef_ctx* ctx, const uint32_t* d_verdict_back, const ef_price
   }
   cudaEventRecord(ctx->ev[4], ctx->st);
   int rc = step_price(ctx, pp);
-  if (rc) return rc;
+  if (rc || (rc = step_prune(ctx, pp))) return rc;
   return step_sync(ctx, true);
 }
 

@@ -16,6 +16,7 @@
 //   k_derive       derived weight tensors (rules.py:231-232, 272-276, 326-327); their BLAKE2b
 //                  digests (graph.py:510-517) are taken on host cores (ef_tables_commit).
 #pragma once
+#include <math_constants.h>
 #include <stdint.h>
 
 #include "ef_device.cuh"
@@ -58,7 +59,8 @@ __device__ __forceinline__ uint32_t lookup_sig(const Tables& T, const ef_sig_des
   uint64_t k = desc_key(d);
   uint32_t m = T.sig_ht_mask;
   if (m == 0) return kNone;
-  for (uint32_t s = (uint32_t)k & m;; s = (s + 1) & m) {
+  uint32_t s = (uint32_t)k & m;
+  for (uint32_t probe = 0; probe <= m; ++probe, s = (s + 1) & m) {
     unsigned long long kk = T.sig_ht_key[s];
     if (kk == 0ULL) return kNone;
     if (kk == k) {
@@ -66,13 +68,15 @@ __device__ __forceinline__ uint32_t lookup_sig(const Tables& T, const ef_sig_des
       if (desc_eq(T.sig_desc[id], d)) return id;
     }
   }
+  return kNone;
 }
 
 __device__ __forceinline__ uint32_t lookup_derive(const Tables& T, int32_t op, uint32_t a, uint32_t b, int32_t s0) {
   uint64_t k = derive_key(op, a, b, s0);
   uint32_t m = T.dv_ht_mask;
   if (m == 0) return kNone;
-  for (uint32_t s = (uint32_t)k & m;; s = (s + 1) & m) {
+  uint32_t s = (uint32_t)k & m;
+  for (uint32_t probe = 0; probe <= m; ++probe, s = (s + 1) & m) {
     unsigned long long kk = T.dv_ht_key[s];
     if (kk == 0ULL) return kNone;
     if (kk == k) {
@@ -81,6 +85,7 @@ __device__ __forceinline__ uint32_t lookup_derive(const Tables& T, int32_t op, u
       if (t[0] == op && (uint32_t)t[1] == a && (uint32_t)t[2] == b && t[3] == s0) return id;
     }
   }
+  return kNone;
 }
 
 __device__ __forceinline__ bool conv_compatible(const ef_sig_desc& a, const ef_sig_desc& b) {
@@ -742,6 +747,7 @@ struct DedupArgs {
   int node_cap;
   uint32_t* plist;    // survivors to price (appended in k_dedup_resolve), may be null
   uint32_t* plist_n;
+  uint32_t* err;      // bit 8: visited set full
 };
 
 __global__ void k_dedup_claim(DedupArgs A) {
@@ -750,7 +756,8 @@ __global__ void k_dedup_claim(DedupArgs A) {
     if (A.res[c].flags & EF_F_INCOMPLETE) continue;
     unsigned long long h = A.res[c].hash;
     unsigned long long key = h ? h : 0x8000000000000000ULL;
-    for (uint32_t s = (uint32_t)mix64(h) & A.step_mask;; s = (s + 1) & A.step_mask) {
+    uint32_t s = (uint32_t)mix64(h) & A.step_mask;
+    for (uint32_t probe = 0; probe <= A.step_mask; ++probe, s = (s + 1) & A.step_mask) {
       unsigned long long prev = atomicCAS(&A.step_key[s], 0ULL, key);
       if (prev == 0ULL || prev == key) {
         atomicMin(&A.step_seq[s], c);
@@ -760,13 +767,33 @@ __global__ void k_dedup_claim(DedupArgs A) {
   }
 }
 
+// Open-addressing visited set of 64-bit hashes (0 is stored as 1 << 63).  The host keeps it at
+// most half full (vis_reserve in ef_api.cu grows it by rehashing), so probe runs are short; every
+// probe loop is still bounded by the table size and reports a full table instead of spinning.
 __device__ __forceinline__ bool vis_contains(const unsigned long long* keys, uint32_t mask, unsigned long long key,
                                              uint64_t h) {
-  for (uint32_t s = (uint32_t)mix64(h) & mask;; s = (s + 1) & mask) {
+  uint32_t s = (uint32_t)mix64(h) & mask;
+  for (uint32_t probe = 0; probe <= mask; ++probe, s = (s + 1) & mask) {
     unsigned long long k = keys[s];
     if (k == key) return true;
     if (k == 0ULL) return false;
   }
+  return false;
+}
+
+// insert; false when the table is full (the caller raises an error flag)
+__device__ __forceinline__ bool vis_insert(unsigned long long* keys, uint32_t mask, unsigned long long* count,
+                                           unsigned long long key, uint64_t h) {
+  uint32_t s = (uint32_t)mix64(h) & mask;
+  for (uint32_t probe = 0; probe <= mask; ++probe, s = (s + 1) & mask) {
+    const unsigned long long prev = atomicCAS(&keys[s], 0ULL, key);
+    if (prev == 0ULL) {
+      atomicAdd(count, 1ULL);
+      return true;
+    }
+    if (prev == key) return true;
+  }
+  return false;
 }
 
 __global__ void k_dedup_resolve(DedupArgs A) {
@@ -781,7 +808,8 @@ __global__ void k_dedup_resolve(DedupArgs A) {
         unsigned long long h = r.hash;
         unsigned long long key = h ? h : 0x8000000000000000ULL;
         uint32_t first_seq = 0xffffffffu;
-        for (uint32_t s = (uint32_t)mix64(h) & A.step_mask;; s = (s + 1) & A.step_mask) {
+        uint32_t s = (uint32_t)mix64(h) & A.step_mask;
+        for (uint32_t probe = 0; probe <= A.step_mask; ++probe, s = (s + 1) & A.step_mask) {
           if (A.step_key[s] == key) {
             first_seq = A.step_seq[s];
             break;
@@ -816,30 +844,129 @@ __global__ void k_visited_insert(DedupArgs A) {
     if ((r.flags & (EF_F_INCOMPLETE | EF_F_FIRST | EF_F_VISITED)) != EF_F_FIRST) continue;
     unsigned long long h = r.hash;
     unsigned long long key = h ? h : 0x8000000000000000ULL;
-    for (uint32_t s = (uint32_t)mix64(h) & A.vis_mask;; s = (s + 1) & A.vis_mask) {
-      unsigned long long prev = atomicCAS(&A.vis_key[s], 0ULL, key);
-      if (prev == 0ULL) {
-        atomicAdd(A.vis_count, 1ULL);
-        break;
-      }
-      if (prev == key) break;
-    }
+    if (!vis_insert(A.vis_key, A.vis_mask, A.vis_count, key, h)) atomicOr(A.err, 8u);
   }
 }
 
 __global__ void k_visited_put(unsigned long long* keys, uint32_t mask, unsigned long long* count, const uint64_t* hs,
-                              uint32_t n) {
+                              uint32_t n, uint32_t* err) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     uint64_t h = hs[i];
     unsigned long long key = h ? h : 0x8000000000000000ULL;
-    for (uint32_t s = (uint32_t)mix64(h) & mask;; s = (s + 1) & mask) {
-      unsigned long long prev = atomicCAS(&keys[s], 0ULL, key);
-      if (prev == 0ULL) {
-        atomicAdd(count, 1ULL);
-        break;
-      }
-      if (prev == key) break;
+    if (!vis_insert(keys, mask, count, key, h)) atomicOr(err, 8u);
+  }
+}
+
+// grow the visited set: every stored key of the old table into the (empty) new one
+__global__ void k_visited_rehash(const unsigned long long* old_keys, uint64_t old_n, unsigned long long* keys,
+                                 uint32_t mask, unsigned long long* count, uint32_t* err) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < old_n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long key = old_keys[i];
+    if (!key) continue;
+    const uint64_t h = key == 0x8000000000000000ULL ? 0ULL : key;
+    if (!vis_insert(keys, mask, count, key, h)) atomicOr(err, 8u);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// the alpha-prune of a step (search.py:258-267): a segmented-free exclusive prefix-min of the
+// priced candidates' costs in (parent, rule, site) order, seeded with the best cost before the
+// step.  prev_i = min(best, cost_j for priced j < i); BEST: cost_i < prev_i, ENQUEUE: cost_i <
+// alpha * prev_i.  Three passes: tile minima, a scan of the tile minima, the in-tile scan.
+// The running minimum updates only on a strict '<', like the reference's `best` (ties keep the
+// earlier value; NaN never enters), so the combine op is associative in candidate order.
+// ------------------------------------------------------------------------------------------
+
+__device__ __forceinline__ double min_keep_first(double a, double b) { return b < a ? b : a; }
+
+template <int BT>
+__device__ __forceinline__ double block_min(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = min_keep_first(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    v = lane < BT / 32 ? sh[lane] : CUDART_INF;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = min_keep_first(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) sh[0] = v;
+  }
+  __syncthreads();
+  v = sh[0];
+  __syncthreads();
+  return v;
+}
+
+// exclusive prefix-min within the block (order = thread index), identity +inf
+template <int BT>
+__device__ __forceinline__ double block_exclusive_min(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x = min_keep_first(y, x);
+  }
+  if (lane == 31) sh[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    double w = lane < BT / 32 ? sh[lane] : CUDART_INF;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w = min_keep_first(y, w);
     }
+    sh[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  double ex = __shfl_up_sync(0xffffffffu, x, 1);
+  if (lane == 0) ex = CUDART_INF;
+  if (wid > 0) ex = min_keep_first(sh[wid - 1], ex);
+  __syncthreads();
+  return ex;
+}
+
+__device__ __forceinline__ double priced_cost(const ef_cand_result& r) {
+  return (r.flags & EF_F_PRICED) ? r.cost : CUDART_INF;
+}
+
+template <int BT>
+__global__ void __launch_bounds__(BT) k_prune_tiles(const ef_cand_result* res, uint32_t total, double* tile_min) {
+  __shared__ double sh[32];
+  const uint32_t c = blockIdx.x * BT + threadIdx.x;
+  const double v = block_min<BT>(c < total ? priced_cost(res[c]) : CUDART_INF, sh);
+  if (threadIdx.x == 0) tile_min[blockIdx.x] = v;
+}
+
+// one block: tile_min[t] <- min(best, tile_min[0..t-1]) (the running best entering tile t)
+template <int BT>
+__global__ void __launch_bounds__(BT) k_prune_scan(double* tile_min, uint32_t n_tiles, double best) {
+  __shared__ double sh[32];
+  double carry = best;
+  for (uint32_t t0 = 0; t0 < n_tiles; t0 += BT) {
+    const uint32_t t = t0 + threadIdx.x;
+    const double v = t < n_tiles ? tile_min[t] : CUDART_INF;
+    const double ex = block_exclusive_min<BT>(v, sh);
+    const double tot = block_min<BT>(v, sh);
+    if (t < n_tiles) tile_min[t] = min_keep_first(carry, ex);
+    carry = min_keep_first(carry, tot);
+  }
+}
+
+template <int BT>
+__global__ void __launch_bounds__(BT) k_prune_flags(ef_cand_result* res, uint32_t total, const double* tile_prev,
+                                                    double alpha) {
+  __shared__ double sh[32];
+  const uint32_t c = blockIdx.x * BT + threadIdx.x;
+  const bool in = c < total;
+  const double v = in ? priced_cost(res[c]) : CUDART_INF;
+  const double prev = min_keep_first(tile_prev[blockIdx.x], block_exclusive_min<BT>(v, sh));
+  if (in && (res[c].flags & EF_F_PRICED)) {
+    uint32_t f = res[c].flags & ~(uint32_t)(EF_F_BEST | EF_F_ENQUEUE);
+    if (v < prev) f |= EF_F_BEST;
+    if (v < alpha * prev) f |= EF_F_ENQUEUE;
+    res[c].flags = f;
   }
 }
 
@@ -903,9 +1030,10 @@ struct NeumaierSum {
     else c += (x - t) + f;
     f = t;
   }
-  __device__ double result() const {
+  // naive: CPython <= 3.11 sum(), plain left to right (the uncompensated running sum f)
+  __device__ double result(int naive) const {
     double r = f;
-    if (c != 0.0 && isfinite(c)) r += c;
+    if (!naive && c != 0.0 && isfinite(c)) r += c;
     return r;
   }
 };
@@ -935,8 +1063,8 @@ __device__ void price_graph(const PriceArgs& A, const View& V, uint8_t* alg, ef_
     st.add(T.row_t[T.row_off[s]]);
     se.add(T.row_e[T.row_off[s]]);
   }
-  double t_tot = ncomp ? st.result() : 0.0;
-  double e_tot = ncomp ? se.result() : 0.0;
+  double t_tot = ncomp ? st.result(F.naive_sum) : 0.0;
+  double e_tot = ncomp ? se.result(F.naive_sum) : 0.0;
   double cost = from_totals(F, t_tot, e_tot);
   long long evals = 0;
   int sweeps = 0;
@@ -1093,8 +1221,8 @@ __device__ void price_d1(const PriceArgs& A, const View& V, Alg alg, ef_cand_res
       }
     }
   }
-  double t_tot = ncomp ? st.result() : 0.0;
-  double e_tot = ncomp ? se.result() : 0.0;
+  double t_tot = ncomp ? st.result(F.naive_sum) : 0.0;
+  double e_tot = ncomp ? se.result(F.naive_sum) : 0.0;
   double cost = cost_of<KIND>(F, t_tot, e_tot);
   long long evals = 0;
   int sweeps = 0;

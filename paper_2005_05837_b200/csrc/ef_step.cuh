@@ -2151,13 +2151,15 @@ struct OwnerArgs {
   unsigned long long* vis_key;
   uint32_t vis_mask;
   unsigned long long* vis_count;
+  uint32_t* err;  // bit 8: visited shard full
 };
 
 __global__ void k_owner_claim(OwnerArgs O) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < O.n; i += gridDim.x * blockDim.x) {
     const uint64_t h = O.recv[2 * (uint64_t)i];
     const unsigned long long key = h ? h : 0x8000000000000000ULL;
-    for (uint32_t s = (uint32_t)mix64(h) & O.mask;; s = (s + 1) & O.mask) {
+    uint32_t s = (uint32_t)mix64(h) & O.mask;
+    for (uint32_t probe = 0; probe <= O.mask; ++probe, s = (s + 1) & O.mask) {
       const unsigned long long prev = atomicCAS(&O.key[s], 0ULL, key);
       if (prev == 0ULL || prev == key) {
         atomicMin(&O.ord[s], (unsigned long long)O.recv[2 * (uint64_t)i + 1]);
@@ -2172,7 +2174,8 @@ __global__ void k_owner_resolve(OwnerArgs O) {
     const uint64_t h = O.recv[2 * (uint64_t)i];
     const unsigned long long key = h ? h : 0x8000000000000000ULL;
     unsigned long long first = ~0ULL;
-    for (uint32_t s = (uint32_t)mix64(h) & O.mask;; s = (s + 1) & O.mask) {
+    uint32_t s = (uint32_t)mix64(h) & O.mask;
+    for (uint32_t probe = 0; probe <= O.mask; ++probe, s = (s + 1) & O.mask) {
       if (O.key[s] == key) {
         first = O.ord[s];
         break;
@@ -2189,14 +2192,7 @@ __global__ void k_owner_insert(OwnerArgs O) {
     if (O.verdict[i] != EF_F_FIRST) continue;
     const uint64_t h = O.recv[2 * (uint64_t)i];
     const unsigned long long key = h ? h : 0x8000000000000000ULL;
-    for (uint32_t s = (uint32_t)mix64(h) & O.vis_mask;; s = (s + 1) & O.vis_mask) {
-      const unsigned long long prev = atomicCAS(&O.vis_key[s], 0ULL, key);
-      if (prev == 0ULL) {
-        atomicAdd(O.vis_count, 1ULL);
-        break;
-      }
-      if (prev == key) break;
-    }
+    if (!vis_insert(O.vis_key, O.vis_mask, O.vis_count, key, h)) atomicOr(O.err, 8u);
   }
 }
 

@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 import threading
 from dataclasses import dataclass
 
@@ -333,8 +334,17 @@ class DeviceSession:
         self._check(self.L.ef_record_alloc(self.ctx, C.byref(s)), "ef_record_alloc")
         return s.value
 
+    def alloc_n(self, n: int) -> list[int]:
+        out = (C.c_uint32 * max(1, n))()
+        self._check(self.L.ef_records_alloc(self.ctx, n, out), "ef_records_alloc")
+        return list(out)[:n]
+
     def free(self, slot: int) -> None:
         self._check(self.L.ef_record_free(self.ctx, slot), "ef_record_free")
+
+    def free_n(self, slots: list[int]) -> None:
+        if slots:
+            self._check(self.L.ef_records_free(self.ctx, N.u32_array(slots), len(slots)), "ef_records_free")
 
     def _view(self, buf: np.ndarray, off: int, dtype, count: int) -> np.ndarray:
         return buf[off: off + np.dtype(dtype).itemsize * count].view(dtype)
@@ -548,7 +558,7 @@ class DeviceSession:
         self._check(self.L.ef_upload_fence(self.ctx), "ef_upload_fence")
 
     def keep(self, cand_idx: list[int]) -> list[int]:
-        slots = [self.alloc() for _ in cand_idx]
+        slots = self.alloc_n(len(cand_idx))
         self._check(self.L.ef_keep(self.ctx, N.u32_array(cand_idx), len(cand_idx), N.u32_array(slots)), "ef_keep")
         return slots
 
@@ -609,6 +619,11 @@ class DeviceSession:
                        offsets.ctypes.data_as(C.POINTER(C.c_uint64)), blob.nbytes), "ef_records_write_packed")
 
 
-def price_params(f, d: int, use_inner: bool, node_cap: int) -> N.PriceParams:
+def price_params(f, d: int, use_inner: bool, node_cap: int, alpha: float = 0.0,
+                 best: float = float("inf")) -> N.PriceParams:
+    """ef_price_params: the cost function, the inner search, the node cap and the step's alpha-prune
+    (alpha = 0: no prune flags).  Start totals follow this interpreter's sum() (Neumaier from
+    CPython 3.12 on, left to right before)."""
     kind, w, ct, ce, cp, tr, er, pr = f.device_params()
-    return N.PriceParams(kind, int(d), int(bool(use_inner)), int(node_cap), w, ct, ce, cp, tr, er, pr)
+    return N.PriceParams(kind, int(d), int(bool(use_inner)), int(node_cap), w, ct, ce, cp, tr, er, pr,
+                         float(best), float(alpha), int(sys.version_info < (3, 12)), 0)

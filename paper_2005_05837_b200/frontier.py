@@ -21,6 +21,7 @@ from __future__ import annotations
 import heapq
 import itertools
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -126,17 +127,19 @@ class _Visible:
 
 
 class _Run:
-    """Device state of one search: geometry, records, visited set."""
+    """Device state of one search: geometry, records, visited set, slot ownership (refcounts)."""
 
     def __init__(self, session: DeviceSession, g0: Graph, node_cap: int, db, profiler):
         self.s = session
         n_inputs = len(g0.nodes) - len(g0.compute_nodes())
         n_refs = sum(len(v.inputs) for v in g0.nodes.values())
-        cap_nodes = node_cap + n_inputs + 2
+        # a record holds any graph the search can expand (at most the larger of the cap and the
+        # origin) plus one rewrite's growth; the cap itself only flags candidates (CAPPED)
+        cap_nodes = max(node_cap, len(g0.compute_nodes())) + n_inputs + 2
         cap_refs = n_refs + max(0, cap_nodes - len(g0.nodes)) + 4
         session.bind_costs(db, profiler)
         session.set_geometry(g0, cap_nodes, cap_refs)
-        session.visited_reset(1 << 20)
+        session.visited_reset(1 << 16)  # grows on the device as the search inserts (ef_visited_*)
         self.root = session.upload(g0)
         self.refs: dict[int, int] = {self.root: 1}
 
@@ -150,32 +153,82 @@ class _Run:
             self.s.free(slot)
 
     def close(self):
-        for slot in list(self.refs):
-            self.s.free(slot)
+        self.s.free_n(list(self.refs))
         self.refs.clear()
 
 
-def _missing_text(session: DeviceSession, r, db: CostDatabase) -> str:
-    for sid in r["touched_sig"].tolist():
+def _missing_text(session: DeviceSession, touched, db: CostDatabase) -> str:
+    for sid in touched:
         if sid != 0xFFFFFFFF and not db.has_signature(session.sig_list[sid].text):
             return session.sig_list[sid].text
     return "?"
 
 
+class _Batch:
+    """Host copy of one batched expansion: per-candidate columns as Python lists, each parent's
+    segment, and for every candidate the step index of the first candidate with its hash (the one
+    the device priced: a hash is priced once per step)."""
+
+    __slots__ = ("hs", "flags", "cost", "t", "e", "evals", "sweeps", "ncomp", "touched", "rep", "seg")
+
+    def __init__(self, res: np.ndarray, n_parents: int):
+        hs = res["hash"]
+        self.hs = hs.tolist()
+        self.flags = res["flags"].tolist()
+        self.cost = res["cost"].tolist()
+        self.t = res["time_ms"].tolist()
+        self.e = res["energy"].tolist()
+        self.evals = res["evals"].tolist()
+        self.sweeps = res["sweeps"].tolist()
+        self.ncomp = res["n_compute"].tolist()
+        self.touched = res["touched_sig"].tolist()
+        if len(hs):
+            _, first, inv = np.unique(hs, return_index=True, return_inverse=True)
+            self.rep = first[inv.reshape(-1)].tolist()
+        else:
+            self.rep = []
+        self.seg = np.searchsorted(res["parent"], np.arange(n_parents + 1)).tolist()
+
+
 def outer_search(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: CostFunction,
                  cfg: SearchConfig, profiler: ProfilerSpec | None, use_inner: bool = True,
                  db_append_path: str | None = None, session: DeviceSession | None = None,
-                 trace: list | None = None) -> OptimizationResult:
-    """Best-first search over the rewrite space of g0 (search.py:211-272), expanded on the GPU."""
+                 trace: list | None = None, batch: int | None = None,
+                 check_prune: bool = False) -> OptimizationResult:
+    """Best-first search over the rewrite space of g0 (search.py:211-272), expanded on the GPU.
+
+    The reference's loop is kept exactly: heap of (cost, hash), the visited set, the alpha rule
+    against the best cost before each candidate, stale entries pruned at pop, the same stats.
+    What changes is how expansions are produced.  Expanding a graph (every rule at every site,
+    hashing, pricing) does not depend on the search state, only on the graph; so when the search
+    pops a graph whose expansion is not cached, one `ef_expand` expands it together with the next
+    `batch - 1` graphs of the heap (speculatively: the ones the search will most likely pop next),
+    and caches every expansion by parent hash.  The search then replays the reference's
+    per-candidate bookkeeping on cached expansions in the reference's pop order: the visited
+    check and insertion, the node cap, the evaluation counters and the alpha rule.
+
+    The device skips pricing candidates that are already in its visited set (which holds every
+    hash the replay has visited, uploaded before each step, so it is a subset of the visited set
+    at replay time), and prices each hash once per step.  Kept candidates are materialised right
+    after the step: those priced below alpha * (the best at step time), a superset of everything
+    the replay can enqueue or make the best since the best only decreases.
+
+    While a batch is replayed in its own order from the state it was expanded in, the step's
+    own alpha-prune flags (EF_F_BEST / EF_F_ENQUEUE: a prefix-min over the priced candidates
+    seeded with that best) are exactly the reference's decisions and are used directly;
+    `check_prune=True` also recomputes them on the host and asserts equality (tests).
+    """
     started = time.perf_counter()
     stats = SearchStats()
     s = session or DeviceSession.default()
     cap = _node_cap(cfg, g0)
+    alpha = cfg.alpha
+    K = max(1, int(batch if batch is not None else os.environ.get("EF_SEARCH_BATCH", 64)))
     if profiler is not None:
         stats.new_cost_records += ensure_profiled(g0, db, profiler, db_append_path)
     run = _Run(s, g0, cap, db, profiler)
     try:
-        pp = price_params(f, cfg.d, use_inner, cap)
+        pp = price_params(f, cfg.d, use_inner, cap, alpha=alpha)
         (r0,) = s.price_slots([run.root], pp)  # ctypes CandResult
         if r0.flags & N.F_MISSING:
             node_cost_table(g0, db)  # raises the reference's MissingEntry
@@ -184,18 +237,61 @@ def outer_search(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: 
         best_slot, best_cost, best_t, best_e = run.root, r0.cost, r0.time_ms, r0.energy
         run.hold(best_slot)
         (h0,) = s.hash_slots([run.root])
-        s.visited_insert([h0])
+        visited = {h0}
+        new_vis = [h0]  # visited on the host, not yet on the device
         heap: list[tuple[float, int]] = [(r0.cost, h0)]
         pending: dict[int, int] = {h0: run.root}
+        cache: dict[int, tuple[_Batch, int]] = {}
+        mat: dict[int, int] = {}  # materialised, not yet replayed: hash -> slot
         visible = _Visible(s, db, profiler, db_append_path)
         rule_ids = [r.rule_id for r in rules]
+        inorder: tuple[_Batch, int] | None = None  # the batch whose own prune flags hold, next index
+        max_queue = cfg.max_queue
+
+        def expand_batch(first_h: int, first_slot: int) -> None:
+            chosen_h, chosen_s = [first_h], [first_slot]
+            bound = alpha * best_cost
+            popped = []
+            while heap and len(chosen_h) < K and len(popped) < 4 * K:
+                e = heapq.heappop(heap)
+                popped.append(e)
+                if e[0] > bound or e[1] in cache:
+                    continue
+                chosen_h.append(e[1])
+                chosen_s.append(pending[e[1]])
+            for e in popped:
+                heapq.heappush(heap, e)
+            if new_vis:
+                s.visited_insert(new_vis)
+                new_vis.clear()
+            pp.best = best_cost
+            if rule_ids:
+                res = s.expand(chosen_s, rule_ids, pp, insert_visited=False)
+            else:
+                res = np.empty(0, dtype=N.CAND_DTYPE)
+            B = _Batch(res, len(chosen_h))
+            if len(res):
+                fl = res["flags"]
+                sel = np.nonzero(((fl & N.F_PRICED) != 0) & (res["cost"] < bound))[0]
+                if len(sel):
+                    hs = B.hs
+                    sel = [int(i) for i in sel if hs[i] not in mat]
+                    for i, sl in zip(sel, s.keep(sel) if sel else []):
+                        mat[hs[i]] = sl
+                        run.refs[sl] = 1
+            for j, h in enumerate(chosen_h):
+                cache[h] = (B, j)
+
         while heap:
             cost, h = heapq.heappop(heap)
-            if cost > cfg.alpha * best_cost:
+            if cost > alpha * best_cost:
                 stats.queue_pruned += 1
                 slot = pending.pop(h, None)
                 if slot is not None:
                     run.drop(slot)
+                ent = cache.pop(h, None)
+                if ent is not None and inorder is not None and ent[0] is inorder[0]:
+                    inorder = None  # the step counted this parent's candidates; the replay will not
                 continue
             slot = pending.pop(h)
             stats.graphs_explored += 1
@@ -203,56 +299,72 @@ def outer_search(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: 
                 trace.append(h)
             if cost == best_cost:
                 stats.expanded_at_best += 1
-            results = s.expand([slot], rule_ids, pp) if rule_ids else np.empty(0, dtype=N.CAND_DTYPE)
-            flags = results["flags"].tolist()
-            hashes = results["hash"].tolist()
-            costs = results["cost"].tolist()
-            keep_idx: list[int] = []
-            keep_role: list[tuple[bool, bool]] = []
-            for i, fl in enumerate(flags):
-                if not fl & N.F_FIRST:
+            ent = cache.pop(h, None)
+            if ent is None:
+                expand_batch(h, slot)
+                ent = cache.pop(h)
+                inorder = (ent[0], 0)
+            B, j = ent
+            use_dev = inorder is not None and inorder[0] is B and inorder[1] == j
+            inorder = (B, j + 1) if use_dev else None
+            hs, flags, ncomp, rep = B.hs, B.flags, B.ncomp, B.rep
+            local: set[int] = set()
+            for i in range(B.seg[j], B.seg[j + 1]):
+                hc = hs[i]
+                if hc in local:  # rules.neighbors: first occurrence within the parent
                     continue
+                local.add(hc)
                 stats.graphs_generated += 1
-                if fl & N.F_VISITED:
+                if hc in visited:
                     stats.graphs_deduped += 1
                     continue
-                if fl & N.F_CAPPED:
+                visited.add(hc)
+                new_vis.append(hc)
+                if ncomp[i] > cap:
                     stats.node_cap_hits += 1
                     continue
-                r = results[i]
+                r = rep[i]
                 if profiler is not None:
-                    stats.new_cost_records += visible.touch(r["touched_sig"].tolist())
-                elif fl & N.F_MISSING:
-                    raise MissingEntry(_missing_text(s, r, db))
-                stats.assignments_evaluated += int(r["evals"])
-                stats.inner_sweeps += int(r["sweeps"])
-                c = costs[i]
+                    stats.new_cost_records += visible.touch(B.touched[i])
+                elif flags[r] & N.F_MISSING:
+                    raise MissingEntry(_missing_text(s, B.touched[i], db))
+                if not flags[r] & N.F_PRICED:
+                    raise N.NativeError(f"candidate {hc} was not priced by its step")
+                stats.assignments_evaluated += B.evals[r]
+                stats.inner_sweeps += B.sweeps[r]
+                c = B.cost[r]
                 prev = best_cost
-                new_best = c < prev
+                if use_dev:
+                    new_best = bool(flags[i] & N.F_BEST)
+                    enq = bool(flags[i] & N.F_ENQUEUE)
+                    if check_prune and (new_best != (c < prev) or enq != (c < alpha * prev)):
+                        raise AssertionError(f"device alpha-prune differs from the replay at {hc}")
+                else:
+                    new_best = c < prev
+                    enq = c < alpha * prev
                 pushed = False
                 if new_best:
-                    best_cost, best_t, best_e = c, float(r["time_ms"]), float(r["energy"])
+                    best_cost, best_t, best_e = c, B.t[r], B.e[r]
                     stats.best_updates += 1
-                if c < cfg.alpha * prev:
-                    if len(heap) >= cfg.max_queue:
+                if enq:
+                    if len(heap) >= max_queue:
                         stats.queue_cap_hits += 1
                     else:
-                        heapq.heappush(heap, (c, hashes[i]))
+                        heapq.heappush(heap, (c, hc))
                         pushed = True
+                sl = mat.pop(hc, None)
                 if new_best or pushed:
-                    keep_idx.append(i)
-                    keep_role.append((new_best, pushed))
-            slots = s.keep(keep_idx) if keep_idx else []
-            for (new_best, pushed), sl, i in zip(keep_role, slots, keep_idx):
-                run.refs[sl] = 0
-                if pushed:
-                    pending[hashes[i]] = sl
-                    run.hold(sl)
-                if new_best:
-                    run.drop(best_slot)
-                    best_slot = sl
-                    run.hold(sl)
-                if run.refs[sl] == 0:
+                    if sl is None:
+                        raise N.NativeError(f"candidate {hc} kept by the search was not materialised")
+                    if new_best:
+                        run.hold(sl)
+                        run.drop(best_slot)
+                        best_slot = sl
+                    if pushed:
+                        pending[hc] = sl
+                    else:
+                        run.drop(sl)
+                elif sl is not None:
                     run.drop(sl)
             run.drop(slot)
         graph, assign = s.decode(s.read_record(best_slot), g0)
@@ -440,7 +552,7 @@ class Frontier:
         if profiler is not None:
             ensure_profiled(g0, db, profiler)
         self.run = _Run(self.s, g0, cap, db, profiler)
-        self.pp = price_params(f, cfg.d, True, cap)
+        self.pp = price_params(f, cfg.d, True, cap, alpha=cfg.alpha)
         (r0,) = self.s.price_slots([self.run.root], self.pp)
         (h0,) = self.s.hash_slots([self.run.root])
         self.s.visited_insert([h0])
@@ -473,8 +585,13 @@ class Frontier:
             slots.append(heapq.heappop(heap)[2])
         self.leftover = [sl for _, _, sl in heap]
         self.slots = slots
-        # the timed steps start from a visited set holding only the explored prefix
+        # The timed steps start from an empty visited set: every parent of the batch was already
+        # expanded (or enqueued) while the batch was built, so keeping that set would mark most
+        # candidates visited; each step is the first expansion of these graphs.  The step's
+        # alpha-prune runs against the best cost found while building the batch.
         self.s.visited_reset(1 << 22)
+        self.pp.best = best
+        self.best = best
 
     def step(self, slots=None, insert_visited: bool = False):
         """One batched expansion; the results view is valid until the session's next step."""

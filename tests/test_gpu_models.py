@@ -117,7 +117,8 @@ def test_gpu_matches_reference_goldens_at_model_scale(model):
         run = gold["search"]
         trace = []
         res = ef.outer_search(g, rules, ef.CostDatabase(), ef.CostFunction.energy(),
-                              ef.SearchConfig(alpha=run["alpha"]), ef.SyntheticProfiler(0), trace=trace)
+                              ef.SearchConfig(alpha=run["alpha"]), ef.SyntheticProfiler(0), trace=trace,
+                              check_prune=True)
         assert [str(h) for h in trace] == run["trace"]
         assert str(ef.canonical_hash(res.graph)) == run["hash"]
         assert [res.assignment[k] for k in sorted(res.assignment)] == run["assignment"]

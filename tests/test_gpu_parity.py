@@ -72,7 +72,11 @@ def test_inner_search(golden_small):
             assert (r.evals, r.sweeps) == (case["evals"], case["sweeps"]), where
 
 
-def test_outer_search(golden_small):
+@pytest.mark.parametrize("batch", [1, 5, 64])
+def test_outer_search(golden_small, batch):
+    """Full searches against the reference's goldens for every expansion batch size: the batched,
+    speculative expansion replayed in the reference's pop order changes nothing observable, and
+    the step's device alpha-prune flags equal the replay's decisions (check_prune)."""
     for inst in golden_small:
         g = ef.graph_from_json(inst["graph"])
         for run in inst["searches"]:
@@ -82,11 +86,12 @@ def test_outer_search(golden_small):
             where = (inst["name"], run["cfg"], run["fn"]["kind"])
             if "error" in run:
                 with pytest.raises(ef.MissingEntry):
-                    ef.outer_search(g, _rules(inst), db, _fn(run["fn"]), cfg, prof, use_inner=run["use_inner"])
+                    ef.outer_search(g, _rules(inst), db, _fn(run["fn"]), cfg, prof, use_inner=run["use_inner"],
+                                    batch=batch)
                 continue
             trace = []
             res = ef.outer_search(g, _rules(inst), db, _fn(run["fn"]), cfg, prof, use_inner=run["use_inner"],
-                                  trace=trace)
+                                  trace=trace, batch=batch, check_prune=True)
             assert [str(h) for h in trace] == run["trace"], where
             assert ef.canonical_hash(res.graph) == run["hash"], where
             assert ef.graph_to_json(res.graph) == run["graph"], where

@@ -111,7 +111,12 @@ typedef struct {
   double best, alpha;
   /* start totals: 0 = CPython >= 3.12 sum() (Neumaier-compensated), 1 = plain left-to-right sum
    * (CPython <= 3.11), so the sweep starts from the totals the caller's interpreter computes */
-  int32_t naive_sum, pad_;
+  int32_t naive_sum;
+  /* 0: price the first occurrence of each hash in the step (the reference's order when the
+   * parents are expanded in step order); 1: the first occurrence within each parent (EF_F_PFIRST),
+   * so every parent's own rewrite of a graph is priced with its own node ids even when the caller
+   * consumes the parents out of step order (the batched, speculative outer search) */
+  int32_t per_parent;
 } ef_price_params;
 
 /* Per-candidate result of one expansion step, in (parent, rule, site) order. */
@@ -123,7 +128,8 @@ enum {
   EF_F_MISSING = 16,  /* some node has no cost rows (MissingEntry)                        */
   EF_F_INCOMPLETE = 32,
   EF_F_BEST = 64,     /* priced, cost < the best before it              (search.py:259-261)  */
-  EF_F_ENQUEUE = 128  /* priced, cost < alpha * the best before it      (search.py:262-267)  */
+  EF_F_ENQUEUE = 128, /* priced, cost < alpha * the best before it     (search.py:262-267)  */
+  EF_F_PFIRST = 256   /* first occurrence of this hash within its parent (per_parent pricing) */
 };
 typedef struct {
   uint64_t hash;
@@ -227,6 +233,15 @@ int ef_results_async(ef_ctx* ctx, ef_cand_result* out, uint32_t n);
 int ef_results_wait(ef_ctx* ctx);
 /* copy step candidates into record slots (the ones the search keeps) */
 int ef_keep(ef_ctx* ctx, const uint32_t* cand_idx, uint32_t n, const uint32_t* slots);
+/* Materialise rewrites of parent records without a step: candidate i is the cand_local[i]-th
+ * rewrite, in (rule, site) order (rules.py:61-71), of parent_slots[cand_parent[i]] under the
+ * given rules, written into slots[i] with its node keys and sorted order.  The search keeps
+ * enqueued graphs as (parent, rewrite index) and materialises them only when it expands them
+ * (search.py:239-243 keeps candidates in `pending`).  Replaces the last step's state (ef_keep
+ * is invalid afterwards); alg[] of the new records is not set (ef_price_records sets it). */
+int ef_materialise(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, const int32_t* rules,
+                   uint32_t n_rules, const uint32_t* cand_parent, const uint32_t* cand_local, uint32_t n,
+                   const uint32_t* slots);
 /* ---- hash-owner sharding (one process per GPU) ------------------------------------------ */
 /* The frontier is split across ranks by parent; deduplication is owned by hash:
  * rank h % world decides, for every candidate hash, its first occurrence in the

@@ -594,6 +594,16 @@ def sweep(g, db: CostDB, f: CostFn, d: int):
     return assign, cost, t_tot, e_tot, evals, sweeps
 
 
+def normalization_refs(g, db: CostDB):
+    """cost.py:284-296: (T_ref, E_ref, P_ref) = per-metric optima = sums of per-node minima."""
+    table = cost_table(g, db)
+    if not table:
+        raise ValueError("normalization references undefined for a graph with no compute nodes")
+    t_ref = sum(min(t for _, t, _ in rows) for rows in table.values())
+    e_ref = sum(min(e for _, _, e in rows) for rows in table.values())
+    return t_ref, e_ref, e_ref / t_ref
+
+
 def default_eval(g, db: CostDB, f: CostFn):
     """search.py:196-202 (use_inner=False): lowest alg per node."""
     table = cost_table(g, db)

@@ -19,7 +19,8 @@ EF_OK = 0
 EF_NEED_RESOLVE = 1
 
 # flags of ef_cand_result (ef200.h)
-F_FIRST, F_VISITED, F_CAPPED, F_PRICED, F_MISSING, F_INCOMPLETE, F_BEST, F_ENQUEUE = 1, 2, 4, 8, 16, 32, 64, 128
+F_FIRST, F_VISITED, F_CAPPED, F_PRICED, F_MISSING, F_INCOMPLETE, F_BEST, F_ENQUEUE, F_PFIRST = (
+    1, 2, 4, 8, 16, 32, 64, 128, 256)
 
 # weight-set derivations
 D_MERGE, D_SLICE_LO, D_SLICE_HI, D_FOLD = 1, 2, 3, 4
@@ -47,7 +48,7 @@ class PriceParams(C.Structure):
     _fields_ = [("kind", C.c_int32), ("d", C.c_int32), ("use_inner", C.c_int32), ("node_cap", C.c_int32),
                 ("w", C.c_double), ("ct", C.c_double), ("ce", C.c_double), ("cp", C.c_double),
                 ("t_ref", C.c_double), ("e_ref", C.c_double), ("p_ref", C.c_double),
-                ("best", C.c_double), ("alpha", C.c_double), ("naive_sum", C.c_int32), ("pad_", C.c_int32)]
+                ("best", C.c_double), ("alpha", C.c_double), ("naive_sum", C.c_int32), ("per_parent", C.c_int32)]
 
 
 class CandResult(C.Structure):
@@ -111,6 +112,8 @@ _PROTOS = {
     "ef_results_async": (C.c_int, [_P, C.c_void_p, C.c_uint32]),
     "ef_results_wait": (C.c_int, [_P]),
     "ef_keep": (C.c_int, [_P, _U32P, C.c_uint32, _U32P]),
+    "ef_materialise": (C.c_int, [_P, _U32P, C.c_uint32, C.POINTER(C.c_int32), C.c_uint32, _U32P, _U32P,
+                                 C.c_uint32, _U32P]),
     "ef_last_timing": (C.c_int, [_P, C.POINTER(C.c_float), C.c_uint32]),
     "ef_last_stats": (C.c_int, [_P, _U64P, C.c_uint32]),
     "ef_records_write_packed": (C.c_int, [_P, _U32P, C.c_uint32, C.c_void_p, _U64P, C.c_uint64]),

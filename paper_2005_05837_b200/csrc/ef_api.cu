@@ -1087,8 +1087,8 @@ static int ensure_step_cand(ef_ctx* ctx, uint32_t total, uint32_t S) {
   EF_CUDA(ctx->d_plan.reserve(std::max<uint32_t>(total, 1), ctx->st));
   EF_CUDA(ctx->d_plist.reserve(std::max<uint32_t>(total, 1), ctx->st));
   EF_CUDA(ctx->d_alg8.reserve((uint64_t)std::max<uint32_t>(total, 1) * S, ctx->st));
-  EF_CUDA(ctx->d_step_key.reserve(tcap, ctx->st));
-  EF_CUDA(ctx->d_step_seq.reserve(tcap, ctx->st));
+  EF_CUDA(ctx->d_step_key.reserve(2 * tcap, ctx->st));  // step table + per-parent table
+  EF_CUDA(ctx->d_step_seq.reserve(2 * tcap, ctx->st));
   EF_CUDA(ctx->d_req_sig.reserve(ctx->req_cap, ctx->st));
   EF_CUDA(ctx->d_req_dv.reserve(4 * ctx->req_cap, ctx->st));
   return EF_OK;
@@ -1385,6 +1385,7 @@ static DedupArgs dedup_args(ef_ctx* ctx, const ef_price_params* pp, int insert_v
   D.plist = ctx->d_plist.p;
   D.plist_n = ctx->d_scalars.p + 7;
   D.err = ctx->d_vis_err.p;
+  D.per_parent = pp ? pp->per_parent : 0;
   return D;
 }
 
@@ -1392,8 +1393,9 @@ static DedupArgs dedup_args(ef_ctx* ctx, const ef_price_params* pp, int insert_v
 static int step_dedup_local(ef_ctx* ctx, const ef_price_params* pp) {
   const uint32_t total = ctx->last_total;
   DedupArgs D = dedup_args(ctx, pp, 0, total);
-  EF_CUDA(cudaMemsetAsync(ctx->d_step_key.p, 0, (size_t)(D.step_mask + 1) * 8, ctx->st));
-  EF_CUDA(cudaMemsetAsync(ctx->d_step_seq.p, 0xff, (size_t)(D.step_mask + 1) * 4, ctx->st));
+  const size_t tables = D.per_parent ? 2 : 1;
+  EF_CUDA(cudaMemsetAsync(ctx->d_step_key.p, 0, tables * (D.step_mask + 1) * 8, ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_step_seq.p, 0xff, tables * (D.step_mask + 1) * 4, ctx->st));
   const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));
   k_dedup_claim<<<grid_t, 256, 0, ctx->st>>>(D);
   k_dedup_resolve<<<grid_t, 256, 0, ctx->st>>>(D);
@@ -1678,6 +1680,82 @@ int ef_keep(ef_ctx* ctx, const uint32_t* cand_idx, uint32_t n, const uint32_t* s
   if ((rc = hash_records_full(ctx, ctx->sc[0], ctx->st, ctx->d_dst.p, n, ctx->d_hash_out.p))) return rc;
   EF_CUDA(cudaStreamSynchronize(ctx->st));
   return EF_OK;
+}
+
+int ef_materialise(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, const int32_t* rules,
+                   uint32_t n_rules, const uint32_t* cand_parent, const uint32_t* cand_local, uint32_t n,
+                   const uint32_t* slots) {
+  EF_REQUIRE(!ctx->dirty, "tables not committed (call ef_tables_commit)");
+  EF_REQUIRE(n_rules <= 8, "at most 8 rules");
+  if (!n) return EF_OK;
+  EF_REQUIRE(n_parents, "ef_materialise: no parents");
+  cudaSetDevice(ctx->dev);
+  const Geo& g = ctx->geo;
+  std::vector<unsigned long long> dst(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    EF_REQUIRE(cand_parent[i] < n_parents, "ef_materialise: bad parent index");
+    EF_REQUIRE(slots[i] < ctx->n_slots, "ef_materialise: bad slot");
+    dst[i] = (unsigned long long)slot_addr(ctx, slots[i]);
+  }
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    int rc = ensure_parent_buffers(ctx, n_parents);
+    if (rc || (rc = stage_addrs(ctx, ctx->d_parent_addr, parent_slots, n_parents))) return rc;
+    EF_CUDA(cudaMemsetAsync(ctx->d_scalars.p, 0, 16 * 4, ctx->st));
+    StepArgs A{};
+    A.g = g;
+    A.T = make_tables(ctx);
+    A.parent_addr = ctx->d_parent_addr.p;
+    A.n_parents = n_parents;
+    A.pscratch = ctx->d_pscratch.p;
+    A.pstride = pstride_of(g);
+    for (uint32_t i = 0; i < n_rules; ++i) A.rules[i] = rules[i];
+    A.n_rules = (int32_t)n_rules;
+    A.sites = ctx->d_sites.p;
+    A.site_cap = ctx->site_cap;
+    A.site_count = ctx->d_site_count.p;
+    A.cand_off = ctx->d_cand_off.p;
+    A.total = ctx->d_scalars.p + 0;
+    A.err = ctx->d_scalars.p + 1;
+    A.n_req_sig = ctx->d_scalars.p + 2;
+    A.n_req_dv = ctx->d_scalars.p + 3;
+    A.cand_cap = 0xffffffffu;
+    A.req_sig = ctx->d_req_sig.p;
+    A.req_dv = ctx->d_req_dv.p;
+    A.req_sig_cap = A.req_dv_cap = ctx->d_req_sig.p ? ctx->req_cap : 0;
+    k_match<kMatchThreads><<<std::min<uint32_t>(n_parents, ctx->n_sm * 8), kMatchThreads, 0, ctx->st>>>(A);
+    k_offsets<1024><<<1, 1024, 0, ctx->st>>>(A);
+    EF_CUDA(cudaGetLastError());
+    std::vector<uint32_t> coff(n_parents + 1);
+    EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
+    EF_CUDA(cudaMemcpyAsync(coff.data(), ctx->d_cand_off.p, (n_parents + 1) * 4, cudaMemcpyDeviceToHost, ctx->st));
+    EF_CUDA(cudaStreamSynchronize(ctx->st));
+    if (ctx->h_scalars[1] & 1u) {  // site buffer too small
+      ctx->site_cap *= 4;
+      continue;
+    }
+    std::vector<uint32_t> sel(n);
+    for (uint32_t i = 0; i < n; ++i) {
+      const uint32_t p = cand_parent[i];
+      EF_REQUIRE(cand_local[i] < coff[p + 1] - coff[p], "ef_materialise: candidate index beyond its parent's sites");
+      sel[i] = coff[p] + cand_local[i];
+    }
+    if ((rc = upload(ctx, ctx->d_dst, dst)) || (rc = upload(ctx, ctx->d_sel, sel))) return rc;
+    A.sel = ctx->d_sel.p;
+    A.n_sel = n;
+    A.dst = ctx->d_dst.p;
+    k_materialise<kMatThreads><<<std::min<uint32_t>(n, ctx->n_sm * 8), kMatThreads, 0, ctx->st>>>(A);
+    EF_CUDA(cudaGetLastError());
+    EF_CUDA(ctx->d_hash_out.reserve(n, ctx->st));
+    if ((rc = hash_records_full(ctx, ctx->sc[0], ctx->st, ctx->d_dst.p, n, ctx->d_hash_out.p))) return rc;
+    EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
+    EF_CUDA(cudaStreamSynchronize(ctx->st));
+    EF_REQUIRE(!(ctx->h_scalars[1] & 4u), "candidate exceeds record capacity (raise cap_nodes/cap_refs)");
+    EF_REQUIRE(!ctx->h_scalars[2] && !ctx->h_scalars[3], "ef_materialise: rewrite needs uninterned tables");
+    ctx->last_total = 0;  // the step state now describes these parents: ef_keep is invalid
+    return EF_OK;
+  }
+  ctx->err = "ef_materialise: site buffer did not converge";
+  return EF_ERR_CAPACITY;
 }
 
 int ef_last_timing(ef_ctx* ctx, float* ms, uint32_t n) {

@@ -748,7 +748,41 @@ struct DedupArgs {
   uint32_t* plist;    // survivors to price (appended in k_dedup_resolve), may be null
   uint32_t* plist_n;
   uint32_t* err;      // bit 8: visited set full
+  int per_parent;     // also mark EF_F_PFIRST (second table at step_key/step_seq + step_mask + 1)
 };
+
+// step table: first occurrence of a key in candidate order (atomicMin on the index)
+__device__ __forceinline__ void step_claim(unsigned long long* keys, uint32_t* seq, uint32_t mask,
+                                           unsigned long long key, uint64_t h, uint32_t c) {
+  uint32_t s = (uint32_t)mix64(h) & mask;
+  for (uint32_t probe = 0; probe <= mask; ++probe, s = (s + 1) & mask) {
+    unsigned long long prev = atomicCAS(&keys[s], 0ULL, key);
+    if (prev == 0ULL || prev == key) {
+      atomicMin(&seq[s], c);
+      return;
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t step_first(const unsigned long long* keys, const uint32_t* seq, uint32_t mask,
+                                               unsigned long long key, uint64_t h) {
+  uint32_t s = (uint32_t)mix64(h) & mask;
+  for (uint32_t probe = 0; probe <= mask; ++probe, s = (s + 1) & mask) {
+    const unsigned long long k = keys[s];
+    if (k == key) return seq[s];
+    if (k == 0ULL) break;
+  }
+  return 0xffffffffu;
+}
+
+// Per-parent key of a candidate hash: a bijection of the hash for each parent (xor with a
+// parent-dependent odd multiple), so the first occurrence of a hash within its own parent
+// (rules.py:79-88 neighbors) is exact; distinct (hash, parent) pairs share a key only if two graph
+// hashes differ by exactly that xor, as unlikely as the 64-bit hash collisions the reference's
+// visited set already accepts.
+__device__ __forceinline__ uint64_t parent_key(uint64_t h, uint32_t parent) {
+  return h ^ ((uint64_t)(parent + 1) * 0x9E3779B97F4A7C15ULL);
+}
 
 __global__ void k_dedup_claim(DedupArgs A) {
   const uint32_t total = A.total[0];
@@ -756,13 +790,11 @@ __global__ void k_dedup_claim(DedupArgs A) {
     if (A.res[c].flags & EF_F_INCOMPLETE) continue;
     unsigned long long h = A.res[c].hash;
     unsigned long long key = h ? h : 0x8000000000000000ULL;
-    uint32_t s = (uint32_t)mix64(h) & A.step_mask;
-    for (uint32_t probe = 0; probe <= A.step_mask; ++probe, s = (s + 1) & A.step_mask) {
-      unsigned long long prev = atomicCAS(&A.step_key[s], 0ULL, key);
-      if (prev == 0ULL || prev == key) {
-        atomicMin(&A.step_seq[s], c);
-        break;
-      }
+    step_claim(A.step_key, A.step_seq, A.step_mask, key, h, c);
+    if (A.per_parent) {
+      const uint64_t hp = parent_key(h, A.res[c].parent);
+      step_claim(A.step_key + A.step_mask + 1, A.step_seq + A.step_mask + 1, A.step_mask,
+                 hp ? hp : 0x8000000000000000ULL, hp, c);
     }
   }
 }
@@ -807,21 +839,21 @@ __global__ void k_dedup_resolve(DedupArgs A) {
       if (!(r.flags & EF_F_INCOMPLETE)) {
         unsigned long long h = r.hash;
         unsigned long long key = h ? h : 0x8000000000000000ULL;
-        uint32_t first_seq = 0xffffffffu;
-        uint32_t s = (uint32_t)mix64(h) & A.step_mask;
-        for (uint32_t probe = 0; probe <= A.step_mask; ++probe, s = (s + 1) & A.step_mask) {
-          if (A.step_key[s] == key) {
-            first_seq = A.step_seq[s];
-            break;
-          }
-        }
         uint32_t f = r.flags;
-        if (first_seq == c) f |= EF_F_FIRST;
+        if (step_first(A.step_key, A.step_seq, A.step_mask, key, h) == c) f |= EF_F_FIRST;
+        if (A.per_parent) {
+          const uint64_t hp = parent_key(h, r.parent);
+          if (step_first(A.step_key + A.step_mask + 1, A.step_seq + A.step_mask + 1, A.step_mask,
+                         hp ? hp : 0x8000000000000000ULL, hp) == c)
+            f |= EF_F_PFIRST;
+        }
         bool seen = vis_contains(A.vis_key, A.vis_mask, key, h);
         if (seen) f |= EF_F_VISITED;
         if (r.n_compute > A.node_cap) f |= EF_F_CAPPED;
         r.flags = f;
-        survivor = (f & (EF_F_FIRST | EF_F_VISITED | EF_F_CAPPED)) == EF_F_FIRST;
+        // priced: the first occurrence in the step, or (per_parent) in its parent
+        const uint32_t first = A.per_parent ? EF_F_PFIRST : EF_F_FIRST;
+        survivor = (f & (first | EF_F_VISITED | EF_F_CAPPED)) == first;
       }
     }
     if (A.plist) {  // warp-aggregated append keeps neighbouring candidates (same parent) together
@@ -927,8 +959,14 @@ __device__ __forceinline__ double block_exclusive_min(double v, double* sh) {
   return ex;
 }
 
+// the candidates the reference evaluates when it expands the step's parents in order: priced and
+// first in the step (per-parent pricing also prices later duplicates of other parents)
+__device__ __forceinline__ bool prune_eligible(uint32_t f) {
+  return (f & (EF_F_PRICED | EF_F_FIRST)) == (EF_F_PRICED | EF_F_FIRST);
+}
+
 __device__ __forceinline__ double priced_cost(const ef_cand_result& r) {
-  return (r.flags & EF_F_PRICED) ? r.cost : CUDART_INF;
+  return prune_eligible(r.flags) ? r.cost : CUDART_INF;
 }
 
 template <int BT>
@@ -962,7 +1000,7 @@ __global__ void __launch_bounds__(BT) k_prune_flags(ef_cand_result* res, uint32_
   const bool in = c < total;
   const double v = in ? priced_cost(res[c]) : CUDART_INF;
   const double prev = min_keep_first(tile_prev[blockIdx.x], block_exclusive_min<BT>(v, sh));
-  if (in && (res[c].flags & EF_F_PRICED)) {
+  if (in && prune_eligible(res[c].flags)) {
     uint32_t f = res[c].flags & ~(uint32_t)(EF_F_BEST | EF_F_ENQUEUE);
     if (v < prev) f |= EF_F_BEST;
     if (v < alpha * prev) f |= EF_F_ENQUEUE;
@@ -986,6 +1024,90 @@ struct PriceArgs {
   int step_mode;  // 1: only first & !visited & !capped & complete candidates
 };
 
+// ------------------------------------------------------------------------------------------
+// x ** y as CPython computes it (C pow of glibc, correctly rounded in all but vanishingly rare
+// cases).  CUDA's pow is accurate to 2 ulp, so a product cost (cost.py:246-248) could differ in
+// its last bit and flip a sweep's strict '<'.  Here log and exp run in double-double (~100 bits):
+// log by one Newton step on the hardware log, exp by range reduction, a Taylor series and ten
+// squarings; the result rounds to the double nearest the exact power except when that lies
+// within ~2^-40 ulp of a rounding boundary.  fma is used explicitly (exact products); the
+// library builds with --fmad=false, so no other operation is contracted.
+// ------------------------------------------------------------------------------------------
+
+struct DD {
+  double hi, lo;
+};
+
+__device__ __forceinline__ DD dd_two_sum(double a, double b) {
+  const double s = a + b, bb = s - a;
+  return {s, (a - (s - bb)) + (b - bb)};
+}
+
+__device__ __forceinline__ DD dd_quick(double a, double b) {
+  const double s = a + b;
+  return {s, b - (s - a)};
+}
+
+__device__ __forceinline__ DD dd_add(DD x, DD y) {
+  DD s = dd_two_sum(x.hi, y.hi), t = dd_two_sum(x.lo, y.lo);
+  s.lo += t.hi;
+  s = dd_quick(s.hi, s.lo);
+  s.lo += t.lo;
+  return dd_quick(s.hi, s.lo);
+}
+
+__device__ __forceinline__ DD dd_mul(DD x, DD y) {
+  const double p = x.hi * y.hi;
+  double e = __fma_rn(x.hi, y.hi, -p);
+  e += x.hi * y.lo + x.lo * y.hi;
+  return dd_quick(p, e);
+}
+
+__device__ __forceinline__ DD dd_mul_d(DD x, double y) {
+  const double p = x.hi * y;
+  double e = __fma_rn(x.hi, y, -p);
+  e += x.lo * y;
+  return dd_quick(p, e);
+}
+
+__device__ __forceinline__ DD dd_div_d(DD x, double y) {
+  const double q1 = x.hi / y;
+  DD r = dd_add(x, dd_mul_d({q1, 0.0}, -y));
+  const double q2 = r.hi / y;
+  return dd_quick(q1, q2);
+}
+
+// exp of a double-double argument (|a| < 700)
+__device__ DD dd_exp(DD a) {
+  const DD ln2 = {0x1.62e42fefa39efp-1, 0x1.abc9e3b39803fp-56};
+  const double k = rint(a.hi / ln2.hi);
+  DD r = dd_add(a, dd_mul_d(ln2, -k));
+  r.hi = ldexp(r.hi, -10);
+  r.lo = ldexp(r.lo, -10);
+  // 1 + r + r^2/2! + ... + r^9/9! by Horner with exact integer divisions (|r| < 3.4e-4)
+  DD p = {1.0, 0.0};
+  for (int n = 9; n >= 1; --n) p = dd_add({1.0, 0.0}, dd_div_d(dd_mul(p, r), (double)n));
+  for (int i = 0; i < 10; ++i) p = dd_mul(p, p);
+  return {ldexp(p.hi, (int)k), ldexp(p.lo, (int)k)};
+}
+
+// log of a positive finite double: y0 = log(x), then y0 - 1 + x * exp(-y0)
+__device__ DD dd_log(double x) {
+  const double y0 = log(x);
+  DD u = dd_mul_d(dd_exp({-y0, 0.0}), x);
+  u = dd_add(u, {-1.0, 0.0});
+  return dd_add({y0, 0.0}, u);
+}
+
+__device__ double pow_py(double x, double y) {
+  if (y == 0.0 || x == 1.0) return 1.0;
+  if (!(x > 0.0) || !isfinite(x) || !isfinite(y)) return pow(x, y);
+  const DD z = dd_mul_d(dd_log(x), y);
+  if (!(fabs(z.hi) < 700.0)) return pow(x, y);  // over/underflow: the hardware result
+  const DD r = dd_exp(z);
+  return r.hi + r.lo;
+}
+
 // cost.py:234-254 in the reference's operation order.  The reference always computes
 // t = time/t_ref and e = energy/e_ref first; for the time / energy / power kinds those
 // quotients are unused, so they are only formed where the result depends on them.
@@ -1000,7 +1122,7 @@ __device__ __forceinline__ double from_totals(const ef_price_params& f, double t
     }
     case EF_C_PRODUCT: {
       const double t = time_ms / f.t_ref, e = energy / f.e_ref;
-      return pow(e, f.w) * pow(t, 1.0 - f.w);
+      return pow_py(e, f.w) * pow_py(t, 1.0 - f.w);
     }
     default: {
       const double t = time_ms / f.t_ref, e = energy / f.e_ref;

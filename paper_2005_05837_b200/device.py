@@ -557,6 +557,17 @@ class DeviceSession:
         """Later steps wait for every asynchronous upload issued so far."""
         self._check(self.L.ef_upload_fence(self.ctx), "ef_upload_fence")
 
+    def materialise(self, parent_slots: list[int], rule_ids: list[int], cand_parent: list[int],
+                    cand_local: list[int]) -> list[int]:
+        """Records of rewrites named (index into parent_slots, rewrite index within that parent)
+        (ef_materialise); -> their new slots."""
+        slots = self.alloc_n(len(cand_parent))
+        self._check(self.L.ef_materialise(self.ctx, N.u32_array(parent_slots), len(parent_slots),
+                                          N.i32_array(rule_ids), len(rule_ids), N.u32_array(cand_parent),
+                                          N.u32_array(cand_local), len(cand_parent), N.u32_array(slots)),
+                    "ef_materialise")
+        return slots
+
     def keep(self, cand_idx: list[int]) -> list[int]:
         slots = self.alloc_n(len(cand_idx))
         self._check(self.L.ef_keep(self.ctx, N.u32_array(cand_idx), len(cand_idx), N.u32_array(slots)), "ef_keep")
@@ -620,10 +631,10 @@ class DeviceSession:
 
 
 def price_params(f, d: int, use_inner: bool, node_cap: int, alpha: float = 0.0,
-                 best: float = float("inf")) -> N.PriceParams:
+                 best: float = float("inf"), per_parent: bool = False) -> N.PriceParams:
     """ef_price_params: the cost function, the inner search, the node cap and the step's alpha-prune
     (alpha = 0: no prune flags).  Start totals follow this interpreter's sum() (Neumaier from
     CPython 3.12 on, left to right before)."""
     kind, w, ct, ce, cp, tr, er, pr = f.device_params()
     return N.PriceParams(kind, int(d), int(bool(use_inner)), int(node_cap), w, ct, ce, cp, tr, er, pr,
-                         float(best), float(alpha), int(sys.version_info < (3, 12)), 0)
+                         float(best), float(alpha), int(sys.version_info < (3, 12)), int(per_parent))

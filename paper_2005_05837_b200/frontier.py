@@ -43,6 +43,11 @@ class SearchConfig:
     max_queue: int = 100_000
     max_graph_nodes: int | None = None
     seed: int = 0
+    # Extension (not in the reference): stop at the pop that would start expansion number
+    # max_expansions + 1 (after that pop's stale-entry check).  None = the reference's search.
+    # Every result is then the reference's state at that point; used to bound alpha > 1 searches
+    # of large graphs, whose queues never drain (tests/golden/make_golden_search_oracle.py).
+    max_expansions: int | None = None
 
     def __post_init__(self):
         if self.alpha < 1.0:
@@ -53,6 +58,8 @@ class SearchConfig:
             raise ValueError("max_queue must be >= 1")
         if self.max_graph_nodes is not None and self.max_graph_nodes < 1:
             raise ValueError("max_graph_nodes must be >= 1")
+        if self.max_expansions is not None and self.max_expansions < 0:
+            raise ValueError("max_expansions must be >= 0")
 
 
 @dataclass
@@ -165,15 +172,13 @@ def _missing_text(session: DeviceSession, touched, db: CostDatabase) -> str:
 
 
 class _Batch:
-    """Host copy of one batched expansion: per-candidate columns as Python lists, each parent's
-    segment, and for every candidate the step index of the first candidate with its hash (the one
-    the device priced: a hash is priced once per step)."""
+    """Host copy of one batched expansion: per-candidate columns as Python lists and each parent's
+    segment (candidates in (rule, site) order, the device's rewrite numbering)."""
 
-    __slots__ = ("hs", "flags", "cost", "t", "e", "evals", "sweeps", "ncomp", "touched", "rep", "seg")
+    __slots__ = ("hs", "flags", "cost", "t", "e", "evals", "sweeps", "ncomp", "touched", "seg")
 
     def __init__(self, res: np.ndarray, n_parents: int):
-        hs = res["hash"]
-        self.hs = hs.tolist()
+        self.hs = res["hash"].tolist()
         self.flags = res["flags"].tolist()
         self.cost = res["cost"].tolist()
         self.t = res["time_ms"].tolist()
@@ -182,12 +187,17 @@ class _Batch:
         self.sweeps = res["sweeps"].tolist()
         self.ncomp = res["n_compute"].tolist()
         self.touched = res["touched_sig"].tolist()
-        if len(hs):
-            _, first, inv = np.unique(hs, return_index=True, return_inverse=True)
-            self.rep = first[inv.reshape(-1)].tolist()
-        else:
-            self.rep = []
         self.seg = np.searchsorted(res["parent"], np.arange(n_parents + 1)).tolist()
+
+
+class _Virtual:
+    """An enqueued graph not materialised yet: rewrite `local` (the device's numbering, rule then
+    site order) of the parent record `slot`, which it keeps alive."""
+
+    __slots__ = ("slot", "local")
+
+    def __init__(self, slot: int, local: int):
+        self.slot, self.local = slot, local
 
 
 def outer_search(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: CostFunction,
@@ -202,20 +212,22 @@ def outer_search(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: 
     What changes is how expansions are produced.  Expanding a graph (every rule at every site,
     hashing, pricing) does not depend on the search state, only on the graph; so when the search
     pops a graph whose expansion is not cached, one `ef_expand` expands it together with the next
-    `batch - 1` graphs of the heap (speculatively: the ones the search will most likely pop next),
+    `batch - 1` graphs of the heap (speculatively: the ones the search is likely to pop next),
     and caches every expansion by parent hash.  The search then replays the reference's
     per-candidate bookkeeping on cached expansions in the reference's pop order: the visited
     check and insertion, the node cap, the evaluation counters and the alpha rule.
 
-    The device skips pricing candidates that are already in its visited set (which holds every
-    hash the replay has visited, uploaded before each step, so it is a subset of the visited set
-    at replay time), and prices each hash once per step.  Kept candidates are materialised right
-    after the step: those priced below alpha * (the best at step time), a superset of everything
-    the replay can enqueue or make the best since the best only decreases.
+    Steps price per parent (EF_F_PFIRST): the first occurrence of each hash within each parent,
+    i.e. exactly the graphs `neighbors(parent)` yields, with that parent's node ids, whatever
+    order the parents are replayed in.  The device skips candidates already in its visited set
+    (every hash the replay has visited, uploaded before each step: a subset of the visited set
+    at replay time).  Enqueued graphs stay virtual (parent record + rewrite index) until a step
+    expands them or the search returns them (ef_materialise), so records are made only for the
+    graphs the search expands.
 
     While a batch is replayed in its own order from the state it was expanded in, the step's
-    own alpha-prune flags (EF_F_BEST / EF_F_ENQUEUE: a prefix-min over the priced candidates
-    seeded with that best) are exactly the reference's decisions and are used directly;
+    alpha-prune flags (EF_F_BEST / EF_F_ENQUEUE: a prefix-min over the step's first occurrences,
+    seeded with the best at step time) are exactly the reference's decisions and are used;
     `check_prune=True` also recomputes them on the host and asserts equality (tests).
     """
     started = time.perf_counter()
@@ -228,72 +240,85 @@ def outer_search(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: 
         stats.new_cost_records += ensure_profiled(g0, db, profiler, db_append_path)
     run = _Run(s, g0, cap, db, profiler)
     try:
-        pp = price_params(f, cfg.d, use_inner, cap, alpha=alpha)
+        pp = price_params(f, cfg.d, use_inner, cap, alpha=alpha, per_parent=True)
         (r0,) = s.price_slots([run.root], pp)  # ctypes CandResult
         if r0.flags & N.F_MISSING:
             node_cost_table(g0, db)  # raises the reference's MissingEntry
         stats.assignments_evaluated += r0.evals
         stats.inner_sweeps += r0.sweeps
-        best_slot, best_cost, best_t, best_e = run.root, r0.cost, r0.time_ms, r0.energy
-        run.hold(best_slot)
+        best_ref, best_cost, best_t, best_e = run.root, r0.cost, r0.time_ms, r0.energy
+        run.hold(run.root)
         (h0,) = s.hash_slots([run.root])
         visited = {h0}
         new_vis = [h0]  # visited on the host, not yet on the device
         heap: list[tuple[float, int]] = [(r0.cost, h0)]
-        pending: dict[int, int] = {h0: run.root}
+        pending: dict[int, object] = {h0: run.root}  # hash -> slot | _Virtual
         cache: dict[int, tuple[_Batch, int]] = {}
-        mat: dict[int, int] = {}  # materialised, not yet replayed: hash -> slot
         visible = _Visible(s, db, profiler, db_append_path)
         rule_ids = [r.rule_id for r in rules]
         inorder: tuple[_Batch, int] | None = None  # the batch whose own prune flags hold, next index
         max_queue = cfg.max_queue
 
-        def expand_batch(first_h: int, first_slot: int) -> None:
-            chosen_h, chosen_s = [first_h], [first_slot]
+        def release(ref):
+            run.drop(ref.slot if isinstance(ref, _Virtual) else ref)
+
+        def materialise(refs: list) -> list[int]:
+            """Slots for a list of refs (virtual ones materialised in one call, parents released)."""
+            virt = [i for i, r in enumerate(refs) if isinstance(r, _Virtual)]
+            out = list(refs)
+            if virt:
+                parents: dict[int, int] = {}
+                cp, cl = [], []
+                for i in virt:
+                    cp.append(parents.setdefault(refs[i].slot, len(parents)))
+                    cl.append(refs[i].local)
+                slots = s.materialise(list(parents), rule_ids, cp, cl)
+                for i, sl in zip(virt, slots):
+                    run.refs[sl] = 1
+                    run.drop(refs[i].slot)
+                    out[i] = sl
+            return out
+
+        def expand_batch(first_h: int) -> None:
+            chosen = [first_h]
             bound = alpha * best_cost
             popped = []
-            while heap and len(chosen_h) < K and len(popped) < 4 * K:
+            while heap and len(chosen) < K and len(popped) < 4 * K:
                 e = heapq.heappop(heap)
                 popped.append(e)
                 if e[0] > bound or e[1] in cache:
                     continue
-                chosen_h.append(e[1])
-                chosen_s.append(pending[e[1]])
+                chosen.append(e[1])
             for e in popped:
                 heapq.heappush(heap, e)
+            slots = materialise([pending[h] for h in chosen])
+            for h, sl in zip(chosen, slots):
+                pending[h] = sl
             if new_vis:
                 s.visited_insert(new_vis)
                 new_vis.clear()
             pp.best = best_cost
             if rule_ids:
-                res = s.expand(chosen_s, rule_ids, pp, insert_visited=False)
+                res = s.expand(slots, rule_ids, pp, insert_visited=False)
             else:
                 res = np.empty(0, dtype=N.CAND_DTYPE)
-            B = _Batch(res, len(chosen_h))
-            if len(res):
-                fl = res["flags"]
-                sel = np.nonzero(((fl & N.F_PRICED) != 0) & (res["cost"] < bound))[0]
-                if len(sel):
-                    hs = B.hs
-                    sel = [int(i) for i in sel if hs[i] not in mat]
-                    for i, sl in zip(sel, s.keep(sel) if sel else []):
-                        mat[hs[i]] = sl
-                        run.refs[sl] = 1
-            for j, h in enumerate(chosen_h):
+            B = _Batch(res, len(chosen))
+            for j, h in enumerate(chosen):
                 cache[h] = (B, j)
 
         while heap:
             cost, h = heapq.heappop(heap)
             if cost > alpha * best_cost:
                 stats.queue_pruned += 1
-                slot = pending.pop(h, None)
-                if slot is not None:
-                    run.drop(slot)
+                ref = pending.pop(h, None)
+                if ref is not None:
+                    release(ref)
                 ent = cache.pop(h, None)
                 if ent is not None and inorder is not None and ent[0] is inorder[0]:
                     inorder = None  # the step counted this parent's candidates; the replay will not
                 continue
-            slot = pending.pop(h)
+            if cfg.max_expansions is not None and stats.graphs_explored >= cfg.max_expansions:
+                break
             stats.graphs_explored += 1
             if trace is not None:
                 trace.append(h)
@@ -301,15 +326,17 @@ def outer_search(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: 
                 stats.expanded_at_best += 1
             ent = cache.pop(h, None)
             if ent is None:
-                expand_batch(h, slot)
+                expand_batch(h)
                 ent = cache.pop(h)
                 inorder = (ent[0], 0)
+            slot = pending.pop(h)  # materialised: it was expanded
             B, j = ent
             use_dev = inorder is not None and inorder[0] is B and inorder[1] == j
             inorder = (B, j + 1) if use_dev else None
-            hs, flags, ncomp, rep = B.hs, B.flags, B.ncomp, B.rep
+            hs, flags, ncomp = B.hs, B.flags, B.ncomp
+            a = B.seg[j]
             local: set[int] = set()
-            for i in range(B.seg[j], B.seg[j + 1]):
+            for i in range(a, B.seg[j + 1]):
                 hc = hs[i]
                 if hc in local:  # rules.neighbors: first occurrence within the parent
                     continue
@@ -323,50 +350,44 @@ def outer_search(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: 
                 if ncomp[i] > cap:
                     stats.node_cap_hits += 1
                     continue
-                r = rep[i]
+                fl = flags[i]
                 if profiler is not None:
                     stats.new_cost_records += visible.touch(B.touched[i])
-                elif flags[r] & N.F_MISSING:
+                elif fl & N.F_MISSING:
                     raise MissingEntry(_missing_text(s, B.touched[i], db))
-                if not flags[r] & N.F_PRICED:
+                if not fl & N.F_PRICED:
                     raise N.NativeError(f"candidate {hc} was not priced by its step")
-                stats.assignments_evaluated += B.evals[r]
-                stats.inner_sweeps += B.sweeps[r]
-                c = B.cost[r]
+                stats.assignments_evaluated += B.evals[i]
+                stats.inner_sweeps += B.sweeps[i]
+                c = B.cost[i]
                 prev = best_cost
                 if use_dev:
-                    new_best = bool(flags[i] & N.F_BEST)
-                    enq = bool(flags[i] & N.F_ENQUEUE)
+                    new_best = bool(fl & N.F_BEST)
+                    enq = bool(fl & N.F_ENQUEUE)
                     if check_prune and (new_best != (c < prev) or enq != (c < alpha * prev)):
                         raise AssertionError(f"device alpha-prune differs from the replay at {hc}")
                 else:
                     new_best = c < prev
                     enq = c < alpha * prev
-                pushed = False
                 if new_best:
-                    best_cost, best_t, best_e = c, B.t[r], B.e[r]
+                    best_cost, best_t, best_e = c, B.t[i], B.e[i]
                     stats.best_updates += 1
+                    run.hold(slot)
+                    release(best_ref)
+                    best_ref = _Virtual(slot, i - a)
                 if enq:
                     if len(heap) >= max_queue:
                         stats.queue_cap_hits += 1
                     else:
                         heapq.heappush(heap, (c, hc))
-                        pushed = True
-                sl = mat.pop(hc, None)
-                if new_best or pushed:
-                    if sl is None:
-                        raise N.NativeError(f"candidate {hc} kept by the search was not materialised")
-                    if new_best:
-                        run.hold(sl)
-                        run.drop(best_slot)
-                        best_slot = sl
-                    if pushed:
-                        pending[hc] = sl
-                    else:
-                        run.drop(sl)
-                elif sl is not None:
-                    run.drop(sl)
+                        run.hold(slot)
+                        pending[hc] = _Virtual(slot, i - a)
             run.drop(slot)
+        (best_slot,) = materialise([best_ref])
+        # the record's algorithm bytes: the inner search again on the kept graph (deterministic)
+        (rb,) = s.price_slots([best_slot], pp)
+        if (rb.cost, rb.time_ms, rb.energy) != (best_cost, best_t, best_e):
+            raise N.NativeError("re-pricing the optimised graph changed its cost")
         graph, assign = s.decode(s.read_record(best_slot), g0)
     finally:
         run.close()

@@ -36,15 +36,41 @@ def oracle_db(db):
     return odb
 
 
-@pytest.mark.parametrize("model,n_parents,price_every", [("squeezenet", 12, 1), ("resnet50", 6, 3),
-                                                          ("inception_v3", 3, 7), ("nasnet_a", 2, 13)])
-def test_frontier_step_matches_oracle(model, n_parents, price_every):
+def _objectives(kind, g0, db):
+    """(package CostFunction, oracle CostFn) of one objective; normalized ones use the origin's
+    normalization_refs (cost.py:284-296)."""
+    from oracle import enerflow_oracle as orc
+
+    refs = ef.normalization_refs(g0, db)
+    if kind == "energy":
+        return ef.CostFunction.energy(), orc.CostFn("energy")
+    if kind == "power":
+        return ef.CostFunction.power(), orc.CostFn("power")
+    if kind == "linear0.5":
+        return ef.CostFunction.linear(0.5).with_refs(*refs), orc.CostFn("linear", w=0.5, refs=refs)
+    if kind == "product0.3":
+        return ef.CostFunction.product(0.3).with_refs(*refs), orc.CostFn("product", w=0.3, refs=refs)
+    if kind == "mix":
+        return (ef.CostFunction.mix(0.2, 0.5, 0.3).with_refs(*refs),
+                orc.CostFn("mix", mix=(0.2, 0.5, 0.3), refs=refs))
+    raise ValueError(kind)
+
+
+# every k_price_v instantiation the step launches: <ENERGY|LINEAR|MIX+1 (power, product, mix), row in
+# shared memory (rows <= 256) or not (Inception-v3 / NasNet-A parents)>
+@pytest.mark.parametrize("model,n_parents,price_every,objective", [
+    ("squeezenet", 12, 1, "energy"), ("resnet50", 6, 3, "energy"), ("inception_v3", 3, 7, "energy"),
+    ("nasnet_a", 2, 13, "energy"), ("inception_v3", 3, 5, "linear0.5"), ("squeezenet", 8, 1, "power"),
+    ("squeezenet", 8, 1, "product0.3"), ("squeezenet", 8, 1, "mix"), ("resnet50", 3, 4, "mix"),
+    ("inception_v3", 2, 5, "product0.3"), ("nasnet_a", 1, 9, "power")])
+def test_frontier_step_matches_oracle(model, n_parents, price_every, objective):
     from oracle import enerflow_oracle as orc
 
     g0 = zoo.generate(model, 0)
     db = ef.CostDatabase()
     prof = ef.SyntheticProfiler(0)
-    f = ef.CostFunction.energy()
+    ef.ensure_profiled(g0, db, prof)
+    f, of = _objectives(objective, g0, db)
     fr = Frontier(g0, db, prof, f, ef.SearchConfig(alpha=1.05), n_parents)
     try:
         res = fr.step()
@@ -72,7 +98,7 @@ def test_frontier_step_matches_oracle(model, n_parents, price_every):
             checked += 1
             if r["flags"] & N.F_PRICED and k % price_every == 0:
                 orc.ensure_profiled(child, odb, 0)
-                _, cost, t, e, evals, sweeps = orc.sweep(child, odb, orc.CostFn("energy"), 1)
+                _, cost, t, e, evals, sweeps = orc.sweep(child, odb, of, 1)
                 assert (float(r["cost"]), float(r["time_ms"]), float(r["energy"])) == (cost, t, e), (model, rule)
                 assert (int(r["evals"]), int(r["sweeps"])) == (evals, sweeps)
                 priced += 1

@@ -267,7 +267,7 @@ int ef_expand_finish(ef_ctx* ctx, const uint32_t* d_verdict_back, const ef_price
  * whole step from match to price (for a sharded step: including the exchange) (n <= 9) */
 int ef_last_timing(ef_ctx* ctx, float* ms, uint32_t n);
 /* counters of the last step: BLAKE2b compressions in node keys, in graph digests,
- * candidates, priced survivors (n <= 4) */
+ * candidates, priced survivors, kernels the library launched for it (n <= 5) */
 int ef_last_stats(ef_ctx* ctx, uint64_t* out, uint32_t n);
 /* batched upload of compact records (host): record i at host + offsets[i] is
  * [n, n_refs, n_out, n_compute] nid[n] sig[n] aux[n] nin[n] inoff[n+1] topo[n] refs outs

@@ -10,9 +10,6 @@
 #include <string>
 #include <vector>
 
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_segmented_sort.cuh>
-
 #include "ef_step.cuh"
 
 using namespace ef;
@@ -66,20 +63,19 @@ struct WeightSet {
 // per-chunk hashing scratch (ef_step.cuh): one set for steps / keeps on the main stream, one
 // for asynchronous uploads on the upload stream
 struct Scratch {
-  DevBuf<uint32_t> didx, jv, refsrc, dcount, dsorted, dorder, sval, sval2, rmask, iota, outsrc;
+  DevBuf<uint32_t> didx, jv, refsrc, dcount, dorder, sval, sval2, rmask, outsrc, cbins;
   DevBuf<Job> jobs;
   DevBuf<uint16_t> jlvl;
   DevBuf<uint64_t> fresh, fresh2, skey, skey2, merged;
   DevBuf<int32_t> seg_b, seg_e;
-  DevBuf<uint8_t> sort_tmp, seg_tmp;
   DevBuf<uint32_t> recmax;
   void release() {
     jlvl.release();
     merged.release();
-    didx.release(); jv.release(); refsrc.release(); dcount.release(); dsorted.release(); dorder.release();
-    sval.release(); sval2.release(); rmask.release(); iota.release(); outsrc.release(); jobs.release();
+    didx.release(); jv.release(); refsrc.release(); dcount.release(); dorder.release(); cbins.release();
+    sval.release(); sval2.release(); rmask.release(); outsrc.release(); jobs.release();
     fresh.release(); fresh2.release(); skey.release(); skey2.release(); seg_b.release(); seg_e.release();
-    sort_tmp.release(); seg_tmp.release(); recmax.release();
+    recmax.release();
   }
 };
 
@@ -92,6 +88,9 @@ struct ef_ctx {
   int n_sm = 148;
   bool big_merge = true;  // rows > 256: merge-path key stream + streaming digest (EF_BIG_MERGE=0: in-thread merge)
   uint32_t wide_min = 512;  // jobs per candidate from which k_keys_wide takes it (EF_WIDE_MIN; 0: off)
+  bool dirty_big = true;  // rows > kFastRows: k_dirty_big (warp window walk); EF_DIRTY_BIG=0: k_dirty
+  uint32_t wide_lpc = 16;  // lanes per candidate in k_keys_wide: 32, 16, 8 or 4 (EF_WIDE_LPC)
+  uint32_t quad_max = 20000;  // chunks below this many candidates hash with k_keys_quad (EF_QUAD_MAX)
   uint64_t chunk_mib = 0;  // per-chunk hashing scratch budget, MiB (0: half the free HBM, <= 96 GiB)
 
   // host mirrors of the tables
@@ -177,7 +176,9 @@ struct ef_ctx {
   std::vector<cudaEvent_t> ev_chunk;  // 5 per hashing chunk: dirty | keys | sort | digest
   uint32_t n_chunks = 0;
   float last_ms[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  uint64_t last_stats[4] = {0, 0, 0, 0};
+  uint64_t last_stats[5] = {0, 0, 0, 0, 0};
+  uint64_t kcount = 0;  // kernels launched by the library (every launch site counts)
+  uint64_t kcount_step0 = 0;  // kcount when the last step began
 };
 
 #define EF_CUDA(call)                                                                    \
@@ -245,6 +246,12 @@ ef_ctx* ef_create(int device) {
   cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, device);
   if (const char* e = getenv("EF_BIG_MERGE")) ctx->big_merge = atoi(e) != 0;
   if (const char* e = getenv("EF_WIDE_MIN")) ctx->wide_min = (uint32_t)strtoul(e, nullptr, 10);
+  if (const char* e = getenv("EF_DIRTY_BIG")) ctx->dirty_big = atoi(e) != 0;
+  if (const char* e = getenv("EF_WIDE_LPC")) {
+    const uint32_t v = (uint32_t)strtoul(e, nullptr, 10);
+    ctx->wide_lpc = v >= 32 ? 32u : v >= 16 ? 16u : v >= 8 ? 8u : 4u;
+  }
+  if (const char* e = getenv("EF_QUAD_MAX")) ctx->quad_max = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_CHUNK_MIB")) ctx->chunk_mib = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
   cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
   cudaStreamCreateWithFlags(&ctx->st_up, cudaStreamNonBlocking);
@@ -630,7 +637,7 @@ int ef_tables_commit(ef_ctx* ctx) {
       DevBuf<DeriveJob> dj;
       EF_CUDA(dj.reserve(djobs.size(), ctx->st));
       EF_CUDA(cudaMemcpyAsync(dj.p, djobs.data(), djobs.size() * sizeof(DeriveJob), cudaMemcpyHostToDevice, ctx->st));
-      for (size_t j = 0; j < djobs.size(); ++j) k_derive<<<ctx->n_sm * 4, 256, 0, ctx->st>>>(dj.p + j, 1);
+      for (size_t j = 0; j < djobs.size(); ++j) ++ctx->kcount, k_derive<<<ctx->n_sm * 4, 256, 0, ctx->st>>>(dj.p + j, 1);
       EF_CUDA(cudaGetLastError());
       EF_CUDA(cudaStreamSynchronize(ctx->st));
       dj.release();
@@ -824,37 +831,56 @@ int ef_record_read(ef_ctx* ctx, uint32_t slot, void* host, uint64_t bytes) {
 // Node keys, sorted order, sorted keys, ranks and graph hash of whole records (uploads and
 // kept candidates): the step's job pipeline with every node a job (ef_step.cuh, full mode).
 static int sort_fresh_keys(ef_ctx* ctx, Scratch& sc, cudaStream_t st, const VArgs& V);
-static uint32_t bits_for(uint32_t v);
 
 // node keys: a thread per candidate when the chunk fills the GPU, four lanes per candidate
 // (lower latency per compression) when it does not
+static int launch_wide(ef_ctx* ctx, cudaStream_t st, const VArgs& V) {
+  const uint32_t lpc = ctx->wide_lpc;
+  const uint32_t per_block = 4u * (32u / lpc);  // candidates per 128-thread block
+  const uint32_t gw = std::max<uint32_t>(1, std::min<uint32_t>((V.n + per_block - 1) / per_block, ctx->n_sm * 16));
+  if (lpc == 32) ++ctx->kcount, k_keys_wide<128, 32><<<gw, 128, 0, st>>>(V);
+  else if (lpc == 16) ++ctx->kcount, k_keys_wide<128, 16><<<gw, 128, 0, st>>>(V);
+  else if (lpc == 8) ++ctx->kcount, k_keys_wide<128, 8><<<gw, 128, 0, st>>>(V);
+  else ++ctx->kcount, k_keys_wide<128, 4><<<gw, 128, 0, st>>>(V);
+  EF_CUDA(cudaGetLastError());
+  return EF_OK;
+}
+
 static int launch_keys(ef_ctx* ctx, cudaStream_t st, const VArgs& V) {
   const bool wide = V.wide_min && st == ctx->st;
-  if (wide) {  // large graphs: the longest candidates a warp each, level by level, on a side
-               // stream so their few resident warps run beside k_keys instead of before it
+  int rc;
+  if (wide) {  // large graphs: the longest candidates by level (lane groups), on a side
+               // stream so their resident warps run beside k_keys instead of before it
     EF_CUDA(cudaEventRecord(ctx->ev_w0, st));
     EF_CUDA(cudaStreamWaitEvent(ctx->st_wide, ctx->ev_w0, 0));
-    const uint32_t gw = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
-    k_keys_wide<128><<<gw, 128, 0, ctx->st_wide>>>(V);
-    EF_CUDA(cudaGetLastError());
+    if ((rc = launch_wide(ctx, ctx->st_wide, V))) return rc;
     EF_CUDA(cudaEventRecord(ctx->ev_w1, ctx->st_wide));
   } else if (V.wide_min) {
-    const uint32_t gw = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
-    k_keys_wide<128><<<gw, 128, 0, st>>>(V);
-    EF_CUDA(cudaGetLastError());
+    if ((rc = launch_wide(ctx, st, V))) return rc;
   }
-  if (V.n < 20000u) {
+  if (V.n < ctx->quad_max) {
     const uint32_t gq = std::max<uint32_t>(1, (V.n + 31) / 32);
-    k_keys_quad<128><<<gq, 128, 0, st>>>(V);
+    ++ctx->kcount, k_keys_quad<128><<<gq, 128, 0, st>>>(V);
   } else {
     const uint32_t gd = std::max<uint32_t>(1, std::min<uint32_t>((V.n + kHashThreads - 1) / kHashThreads, ctx->n_sm * 16));
-    k_keys<kHashThreads><<<gd, kHashThreads, 0, st>>>(V);
+    ++ctx->kcount, k_keys<kHashThreads><<<gd, kHashThreads, 0, st>>>(V);
   }
   EF_CUDA(cudaGetLastError());
   if (wide) EF_CUDA(cudaStreamWaitEvent(st, ctx->ev_w1, 0));
   return EF_OK;
 }
 static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk);
+// chunk candidates by job count, largest first (counting sort: k_count_*)
+static int order_by_count(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t n, uint32_t S) {
+  if (!n) return EF_OK;
+  EF_CUDA(cudaMemsetAsync(sc.cbins.p, 0, 4ull * (S + 1), st));
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((n + 255) / 256, ctx->n_sm * 8));
+  ++ctx->kcount, k_count_hist<<<grid, 256, 0, st>>>(sc.dcount.p, n, S, sc.cbins.p);
+  ++ctx->kcount, k_count_scan<1024><<<1, 1024, 0, st>>>(sc.cbins.p, S + 1);
+  ++ctx->kcount, k_count_scatter<<<grid, 256, 0, st>>>(sc.dcount.p, n, S, sc.cbins.p, sc.dorder.p);
+  EF_CUDA(cudaGetLastError());
+  return EF_OK;
+}
 static VArgs chunk_args(ef_ctx* ctx, Scratch& sc, uint32_t S, uint32_t Rs);
 static int hash_records_full(ef_ctx* ctx, Scratch& sc, cudaStream_t st, const unsigned long long* d_rec, uint32_t n,
                              uint64_t* d_hash_out, uint32_t max_n = 0, uint32_t max_refs = 0) {
@@ -862,7 +888,7 @@ static int hash_records_full(ef_ctx* ctx, Scratch& sc, cudaStream_t st, const un
   if (!max_n) {  // sizes unknown on the host: read them from the records
     EF_CUDA(sc.recmax.reserve(2, st));
     EF_CUDA(cudaMemsetAsync(sc.recmax.p, 0, 8, st));
-    k_rec_max<<<std::max<uint32_t>(1, std::min<uint32_t>((n + 255) / 256, ctx->n_sm)), 256, 0, st>>>(d_rec, n,
+    ++ctx->kcount, k_rec_max<<<std::max<uint32_t>(1, std::min<uint32_t>((n + 255) / 256, ctx->n_sm)), 256, 0, st>>>(d_rec, n,
                                                                                                    sc.recmax.p);
     EF_CUDA(cudaGetLastError());
     uint32_t mx[2] = {0, 0};
@@ -884,15 +910,13 @@ static int hash_records_full(ef_ctx* ctx, Scratch& sc, cudaStream_t st, const un
     V.c0 = c0;
     V.n = std::min(chunk, n - c0);
     const uint32_t gd = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 127) / 128, ctx->n_sm * 16));
-    k_full_jobs<256><<<std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * 8)), 256, 0, st>>>(V);
+    ++ctx->kcount, k_full_jobs<256><<<std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * 8)), 256, 0, st>>>(V);
     EF_CUDA(cudaGetLastError());
-    size_t t1 = sc.sort_tmp.cap;
-    EF_CUDA(cub::DeviceRadixSort::SortPairsDescending(sc.sort_tmp.p, t1, sc.dcount.p, sc.dsorted.p, sc.iota.p,
-                                                      sc.dorder.p, (int)V.n, 0, bits_for(S), st));
+    if ((rc = order_by_count(ctx, sc, st, V.n, S))) return rc;
     if ((rc = launch_keys(ctx, st, V))) return rc;
     if ((rc = sort_fresh_keys(ctx, sc, st, V))) return rc;
-    k_digest<kHashThreads><<<gd, kHashThreads, 0, st>>>(V);
-    k_full_store<<<std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * 8)), 128, 0, st>>>(V);
+    ++ctx->kcount, k_digest<kHashThreads><<<gd, kHashThreads, 0, st>>>(V);
+    ++ctx->kcount, k_full_store<<<std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * 8)), 128, 0, st>>>(V);
     EF_CUDA(cudaGetLastError());
   }
   return EF_OK;
@@ -914,7 +938,7 @@ int ef_records_write(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const void*
   }
   int rc;
   if ((rc = upload(ctx, ctx->d_addr_a, src)) || (rc = upload(ctx, ctx->d_addr_b, dst))) return rc;
-  k_copy_records<<<std::min<uint32_t>(n, ctx->n_sm * 8), 256, 0, ctx->st>>>(ctx->d_addr_a.p, ctx->d_addr_b.p, n,
+  ++ctx->kcount, k_copy_records<<<std::min<uint32_t>(n, ctx->n_sm * 8), 256, 0, ctx->st>>>(ctx->d_addr_a.p, ctx->d_addr_b.p, n,
                                                                             (uint32_t)bytes);
   EF_CUDA(cudaGetLastError());
   EF_CUDA(cudaStreamSynchronize(ctx->st));
@@ -966,7 +990,7 @@ int ef_price_records(ef_ctx* ctx, const uint32_t* slots, uint32_t n, const ef_pr
   Pa.n = n;
   Pa.rec = ctx->d_addr_a.p;
   Pa.res = ctx->d_res_aux.p;
-  k_price<<<(n + kPriceThreads - 1) / kPriceThreads, kPriceThreads, 0, ctx->st>>>(Pa);
+  ++ctx->kcount, k_price<<<(n + kPriceThreads - 1) / kPriceThreads, kPriceThreads, 0, ctx->st>>>(Pa);
   EF_CUDA(cudaGetLastError());
   EF_CUDA(cudaMemcpyAsync(out, ctx->d_res_aux.p, n * sizeof(ef_cand_result), cudaMemcpyDeviceToHost, ctx->st));
   EF_CUDA(cudaStreamSynchronize(ctx->st));
@@ -1023,7 +1047,7 @@ static int vis_reserve(ef_ctx* ctx, uint64_t more) {
   EF_CUDA(cudaMemsetAsync(q, 0, ncap * 8, ctx->st));
   EF_CUDA(cudaMemsetAsync(ctx->d_vis_count.p, 0, 8, ctx->st));
   const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((cap + 255) / 256, ctx->n_sm * 16ull));
-  k_visited_rehash<<<grid, 256, 0, ctx->st>>>(ctx->d_vis.p, cap, q, (uint32_t)(ncap - 1), ctx->d_vis_count.p,
+  ++ctx->kcount, k_visited_rehash<<<grid, 256, 0, ctx->st>>>(ctx->d_vis.p, cap, q, (uint32_t)(ncap - 1), ctx->d_vis_count.p,
                                               ctx->d_vis_err.p);
   EF_CUDA(cudaGetLastError());
   EF_CUDA(cudaStreamSynchronize(ctx->st));
@@ -1041,7 +1065,7 @@ int ef_visited_insert(ef_ctx* ctx, const uint64_t* hashes, uint32_t n) {
   if (rc) return rc;
   EF_CUDA(ctx->d_hash_out.reserve(n, ctx->st));
   EF_CUDA(cudaMemcpyAsync(ctx->d_hash_out.p, hashes, n * 8, cudaMemcpyHostToDevice, ctx->st));
-  k_visited_put<<<(n + 255) / 256, 256, 0, ctx->st>>>(ctx->d_vis.p, ctx->vis_mask, ctx->d_vis_count.p,
+  ++ctx->kcount, k_visited_put<<<(n + 255) / 256, 256, 0, ctx->st>>>(ctx->d_vis.p, ctx->vis_mask, ctx->d_vis_count.p,
                                                        ctx->d_hash_out.p, n, ctx->d_vis_err.p);
   EF_CUDA(cudaGetLastError());
   return vis_settle(ctx);
@@ -1124,25 +1148,10 @@ static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t item
   EF_CUDA(sc.sval.reserve(ch * S, st));
   EF_CUDA(sc.sval2.reserve(ch * S, st));
   EF_CUDA(sc.dcount.reserve(ch, st));
-  EF_CUDA(sc.dsorted.reserve(ch, st));
   EF_CUDA(sc.dorder.reserve(ch, st));
   EF_CUDA(sc.seg_b.reserve(ch, st));
   EF_CUDA(sc.seg_e.reserve(ch, st));
-  if (sc.iota.cap < ch) {
-    EF_CUDA(sc.iota.reserve(ch, st));
-    std::vector<uint32_t> io(sc.iota.cap);
-    for (size_t i = 0; i < io.size(); ++i) io[i] = (uint32_t)i;
-    EF_CUDA(cudaMemcpyAsync(sc.iota.p, io.data(), io.size() * 4, cudaMemcpyHostToDevice, st));
-    EF_CUDA(cudaStreamSynchronize(st));
-  }
-  size_t t1 = 0, t2 = 0;
-  cub::DeviceRadixSort::SortPairsDescending(nullptr, t1, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                            (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)ch, 0, 32);
-  cub::DeviceSegmentedSort::SortPairs(nullptr, t2, (const uint64_t*)nullptr, (uint64_t*)nullptr,
-                                      (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)(ch * S), (int)ch,
-                                      (const int32_t*)nullptr, (const int32_t*)nullptr);
-  EF_CUDA(sc.sort_tmp.reserve(t1, st));
-  EF_CUDA(sc.seg_tmp.reserve(t2, st));
+  EF_CUDA(sc.cbins.reserve(S + 2, st));
   return EF_OK;
 }
 
@@ -1179,34 +1188,28 @@ static VArgs chunk_args(ef_ctx* ctx, Scratch& sc, uint32_t S, uint32_t Rs) {
 }
 
 // every candidate's fresh keys in ascending order: warp bitonic sort in shared memory for
-// rows up to 1024 keys, cub's segmented sort (plus the tie fix) beyond
+// rows up to 1024 keys, k_sortbig (a CTA per candidate) beyond
 static int sort_fresh_keys(ef_ctx* ctx, Scratch& sc, cudaStream_t st, const VArgs& V) {
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 7) / 8, ctx->n_sm * 32));
   if (V.S <= 128) {
-    k_sortkeys<128, 8><<<grid, 256, 0, st>>>(V);
+    ++ctx->kcount, k_sortkeys<128, 8><<<grid, 256, 0, st>>>(V);
   } else if (V.S <= 256) {
-    k_sortkeys<256, 8><<<grid, 256, 0, st>>>(V);
+    ++ctx->kcount, k_sortkeys<256, 8><<<grid, 256, 0, st>>>(V);
   } else if (V.S <= 512) {
-    k_sortkeys<512, 8><<<grid, 256, 0, st>>>(V);
+    ++ctx->kcount, k_sortkeys<512, 8><<<grid, 256, 0, st>>>(V);
   } else if (V.S <= 1024) {
-    k_sortkeys<1024, 4><<<std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 32)), 128, 0, st>>>(V);
-  } else {
-    size_t t2 = sc.seg_tmp.cap;
-    EF_CUDA(cub::DeviceSegmentedSort::SortPairs(sc.seg_tmp.p, t2, sc.skey.p, sc.skey2.p, sc.sval.p,
-                                                sc.sval2.p, (int)((uint64_t)V.n * V.S), (int)V.n, sc.seg_b.p,
-                                                sc.seg_e.p, st));
-    const uint32_t gd = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 127) / 128, ctx->n_sm * 16));
-    k_sortfix<<<gd, 128, 0, st>>>(V);
+    ++ctx->kcount, k_sortkeys<1024, 4><<<std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 32)), 128, 0, st>>>(V);
+  } else {  // a CTA per candidate: shared-memory runs of up to 8192 keys, merged in global rows
+    uint32_t R = 1024;
+    while (R < V.S && R < 8192u) R <<= 1;
+    const size_t smem = 8ull * R;
+    EF_CUDA(cudaFuncSetAttribute(k_sortbig<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ++ctx->kcount, k_sortbig<512><<<std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * 4)), 512, smem, st>>>(V, R);
   }
   EF_CUDA(cudaGetLastError());
   return EF_OK;
 }
 
-static uint32_t bits_for(uint32_t v) {
-  uint32_t b = 1;
-  while (b < 32 && (1ull << b) <= v) ++b;
-  return b;
-}
 
 // ---- step phases --------------------------------------------------------------------------
 
@@ -1245,10 +1248,10 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
     // 1) match every rule at every node of every parent; candidate offsets; parent sizes
     cudaEventRecord(ctx->ev[0], ctx->st);
     if (n_parents) {
-      k_match<kMatchThreads><<<std::min<uint32_t>(n_parents, ctx->n_sm * 8), kMatchThreads, 0, ctx->st>>>(A);
+      ++ctx->kcount, k_match<kMatchThreads><<<std::min<uint32_t>(n_parents, ctx->n_sm * 8), kMatchThreads, 0, ctx->st>>>(A);
       EF_CUDA(cudaGetLastError());
     }
-    k_offsets<1024><<<1, 1024, 0, ctx->st>>>(A);
+    ++ctx->kcount, k_offsets<1024><<<1, 1024, 0, ctx->st>>>(A);
     EF_CUDA(cudaGetLastError());
     cudaEventRecord(ctx->ev[1], ctx->st);
     EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
@@ -1277,11 +1280,11 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       const uint32_t rmax = ctx->h_scalars[6];
       const size_t smem = 2ull * 4 * (256 + 260 + ((rmax + 3) & ~3u) + kReachSlots * kReachWords);
       EF_CUDA(cudaFuncSetAttribute(k_reach, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_reach<<<std::max<uint32_t>(1, (n_parents + 1) / 2), 64, smem, ctx->st>>>(A, rmax);
+      ++ctx->kcount, k_reach<<<std::max<uint32_t>(1, (n_parents + 1) / 2), 64, smem, ctx->st>>>(A, rmax);
       EF_CUDA(cudaGetLastError());
     }
     if (total) {
-      k_plan<<<grid_t, 256, 0, ctx->st>>>(A, ctx->d_plan.p);
+      ++ctx->kcount, k_plan<<<grid_t, 256, 0, ctx->st>>>(A, ctx->d_plan.p);
       EF_CUDA(cudaGetLastError());
     }
     cudaEventRecord(ctx->ev[2], ctx->st);
@@ -1309,19 +1312,23 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       // the shared-memory merge also handle rows <= 1024, but measured slower than the general
       // kernels there: NasNet-A 15.1 vs 13.8 ms per 1024-parent step)
       V.slots = S <= kFastRows;
+      const bool big_walk = !V.slots && ctx->dirty_big && ctx->big_merge;  // (k_digest reads didx rows)
+      V.osrc = V.slots || big_walk;
       V.wide_min = (V.slots || S < ctx->wide_min) ? 0u : ctx->wide_min;  // no candidate can reach it otherwise
-      V.jlvl = V.wide_min ? sc.jlvl.p : nullptr;  // levels for k_keys_wide (large graphs)
+      V.jlvl = V.wide_min ? sc.jlvl.p : nullptr;
       if (V.slots) {
         const uint32_t gw = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
-        k_dirty_warp<4><<<gw, 128, 0, ctx->st>>>(V);
+        ++ctx->kcount, k_dirty_warp<4><<<gw, 128, 0, ctx->st>>>(V);
+      } else if (big_walk) {
+        const size_t smem = 4ull * 4 * (3ull * V.W + 1);
+        EF_CUDA(cudaFuncSetAttribute(k_dirty_big<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const uint32_t gw = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 32));
+        ++ctx->kcount, k_dirty_big<4><<<gw, 128, smem, ctx->st>>>(V);
       } else {
-        k_dirty<<<gd, 128, 0, ctx->st>>>(V);
+        ++ctx->kcount, k_dirty<<<gd, 128, 0, ctx->st>>>(V);
       }
       EF_CUDA(cudaGetLastError());
-      size_t t1 = sc.sort_tmp.cap;
-      EF_CUDA(cub::DeviceRadixSort::SortPairsDescending(sc.sort_tmp.p, t1, sc.dcount.p, sc.dsorted.p,
-                                                        sc.iota.p, sc.dorder.p, (int)V.n, 0, bits_for(S),
-                                                        ctx->st));
+      if ((rc = order_by_count(ctx, sc, ctx->st, V.n, S))) return rc;
       cudaEventRecord(ce[1], ctx->st);
       if ((rc = launch_keys(ctx, ctx->st, V))) return rc;
       cudaEventRecord(ce[2], ctx->st);
@@ -1333,27 +1340,27 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
         const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>((V.n + warps - 1) / warps, ctx->n_sm * 32));
         if (warps == 4) {
           EF_CUDA(cudaFuncSetAttribute(k_merge<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          k_merge<8, 4><<<gm, 128, smem, ctx->st>>>(V, rows);
+          ++ctx->kcount, k_merge<8, 4><<<gm, 128, smem, ctx->st>>>(V, rows);
         } else {
           EF_CUDA(cudaFuncSetAttribute(k_merge<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          k_merge<8, 2><<<gm, 64, smem, ctx->st>>>(V, rows);
+          ++ctx->kcount, k_merge<8, 2><<<gm, 64, smem, ctx->st>>>(V, rows);
         }
         EF_CUDA(cudaGetLastError());
         cudaEventRecord(ce[3], ctx->st);
-        k_digest_pm<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+        ++ctx->kcount, k_digest_pm<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
       } else {
         if ((rc = sort_fresh_keys(ctx, sc, ctx->st, V))) return rc;
         if (ctx->big_merge) {  // merge-path key stream, then the streaming digest
           const size_t smem = 4ull * 4 * (V.W + 1);
           EF_CUDA(cudaFuncSetAttribute(k_merge_big<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
           const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
-          k_merge_big<4><<<gm, 128, smem, ctx->st>>>(V);
+          ++ctx->kcount, k_merge_big<4><<<gm, 128, smem, ctx->st>>>(V);
           EF_CUDA(cudaGetLastError());
           cudaEventRecord(ce[3], ctx->st);
-          k_digest_pm<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+          ++ctx->kcount, k_digest_pm<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
         } else {
           cudaEventRecord(ce[3], ctx->st);
-          k_digest<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+          ++ctx->kcount, k_digest<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
         }
       }
       EF_CUDA(cudaGetLastError());
@@ -1397,8 +1404,8 @@ static int step_dedup_local(ef_ctx* ctx, const ef_price_params* pp) {
   EF_CUDA(cudaMemsetAsync(ctx->d_step_key.p, 0, tables * (D.step_mask + 1) * 8, ctx->st));
   EF_CUDA(cudaMemsetAsync(ctx->d_step_seq.p, 0xff, tables * (D.step_mask + 1) * 4, ctx->st));
   const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));
-  k_dedup_claim<<<grid_t, 256, 0, ctx->st>>>(D);
-  k_dedup_resolve<<<grid_t, 256, 0, ctx->st>>>(D);
+  ++ctx->kcount, k_dedup_claim<<<grid_t, 256, 0, ctx->st>>>(D);
+  ++ctx->kcount, k_dedup_resolve<<<grid_t, 256, 0, ctx->st>>>(D);
   EF_CUDA(cudaGetLastError());
   cudaEventRecord(ctx->ev[4], ctx->st);
   return EF_OK;
@@ -1436,16 +1443,16 @@ static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
   do {                                                                                                     \
     if (sm) {                                                                                              \
       EF_CUDA(cudaFuncSetAttribute(k_price_v<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-      k_price_v<K, true><<<gp, kPriceThreads, smem, ctx->st>>>(Pv, pl, pn);                             \
+      ++ctx->kcount, k_price_v<K, true><<<gp, kPriceThreads, smem, ctx->st>>>(Pv, pl, pn);                             \
     } else {                                                                                               \
-      k_price_v<K, false><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);                                \
+      ++ctx->kcount, k_price_v<K, false><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);                                \
     }                                                                                                      \
   } while (0)
   if (fast && pp->kind == EF_C_ENERGY) EF_PRICE(EF_C_ENERGY);
   else if (fast && pp->kind == EF_C_TIME) EF_PRICE(EF_C_TIME);
   else if (fast && pp->kind == EF_C_LINEAR) EF_PRICE(EF_C_LINEAR);
   else if (fast) EF_PRICE(EF_C_MIX + 1);
-  else k_price_v<-1, false><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
+  else ++ctx->kcount, k_price_v<-1, false><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
 #undef EF_PRICE
   EF_CUDA(cudaGetLastError());
   cudaEventRecord(ctx->ev[5], ctx->st);
@@ -1459,9 +1466,9 @@ static int step_prune(ef_ctx* ctx, const ef_price_params* pp) {
   constexpr int BT = 512;
   const uint32_t tiles = (total + BT - 1) / BT;
   EF_CUDA(ctx->d_tile.reserve(tiles, ctx->st));
-  k_prune_tiles<BT><<<tiles, BT, 0, ctx->st>>>(ctx->d_res.p, total, ctx->d_tile.p);
-  k_prune_scan<BT><<<1, BT, 0, ctx->st>>>(ctx->d_tile.p, tiles, pp->best);
-  k_prune_flags<BT><<<tiles, BT, 0, ctx->st>>>(ctx->d_res.p, total, ctx->d_tile.p, pp->alpha);
+  ++ctx->kcount, k_prune_tiles<BT><<<tiles, BT, 0, ctx->st>>>(ctx->d_res.p, total, ctx->d_tile.p);
+  ++ctx->kcount, k_prune_scan<BT><<<1, BT, 0, ctx->st>>>(ctx->d_tile.p, tiles, pp->best);
+  ++ctx->kcount, k_prune_flags<BT><<<tiles, BT, 0, ctx->st>>>(ctx->d_res.p, total, ctx->d_tile.p, pp->alpha);
   EF_CUDA(cudaGetLastError());
   cudaEventRecord(ctx->ev[5], ctx->st);  // the price stage includes the prune
   return EF_OK;
@@ -1495,6 +1502,7 @@ static int step_sync(ef_ctx* ctx, bool timings) {
     cudaEventElapsedTime(&ctx->last_ms[8], ctx->ev[0], ctx->ev[5]);  // the whole step (incl. any exchange)
     ctx->last_stats[2] = ctx->last_total;
     ctx->last_stats[3] = ctx->h_scalars[7];
+    ctx->last_stats[4] = ctx->kcount - ctx->kcount_step0;
   }
   EF_REQUIRE(!(err & 4u), "candidate exceeds record capacity (raise cap_nodes/cap_refs)");
   if (ctx->last_req_sig || ctx->last_req_dv) return EF_NEED_RESOLVE;
@@ -1506,7 +1514,7 @@ static int insert_firsts(ef_ctx* ctx) {
   if (rc) return rc;
   DedupArgs D = dedup_args(ctx, nullptr, 1, ctx->last_total);
   const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((ctx->last_total + 255) / 256, ctx->n_sm * 8));
-  k_visited_insert<<<grid_t, 256, 0, ctx->st>>>(D);
+  ++ctx->kcount, k_visited_insert<<<grid_t, 256, 0, ctx->st>>>(D);
   EF_CUDA(cudaGetLastError());
   return vis_settle(ctx);
 }
@@ -1518,6 +1526,7 @@ static int step_begin(ef_ctx* ctx, uint32_t* n_candidates, uint32_t n_rules) {
   EF_REQUIRE(ctx->vis_mask, "visited set not initialised");
   EF_REQUIRE(n_rules <= 8, "at most 8 rules");
   cudaSetDevice(ctx->dev);
+  ctx->kcount_step0 = ctx->kcount;
   return EF_OK;
 }
 
@@ -1556,7 +1565,7 @@ int ef_route_owners(ef_ctx* ctx, uint32_t world, uint64_t order_base, uint64_t* 
   EF_CUDA(cudaMemsetAsync(ctx->d_route.p, 0, (2 * (size_t)world + 2) * 4, ctx->st));
   const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));
   RouteArgs R{ctx->d_res.p, total, world, order_base, ctx->d_route.p, ctx->d_route.p + world, d_send, ctx->d_perm.p};
-  k_route_count<<<grid_t, 256, world * 4, ctx->st>>>(R);
+  ++ctx->kcount, k_route_count<<<grid_t, 256, world * 4, ctx->st>>>(R);
   EF_CUDA(cudaGetLastError());
   std::vector<uint32_t> cnt(world), off(world);
   EF_CUDA(cudaMemcpyAsync(cnt.data(), ctx->d_route.p, world * 4, cudaMemcpyDeviceToHost, ctx->st));
@@ -1569,7 +1578,7 @@ int ef_route_owners(ef_ctx* ctx, uint32_t world, uint64_t order_base, uint64_t* 
   }
   ctx->n_send = run;
   EF_CUDA(cudaMemcpyAsync(ctx->d_route.p + world, off.data(), world * 4, cudaMemcpyHostToDevice, ctx->st));
-  k_route_scatter<<<grid_t, 256, world * 8, ctx->st>>>(R);
+  ++ctx->kcount, k_route_scatter<<<grid_t, 256, world * 8, ctx->st>>>(R);
   EF_CUDA(cudaGetLastError());
   EF_CUDA(cudaStreamSynchronize(ctx->st));
   return EF_OK;
@@ -1590,9 +1599,9 @@ int ef_owner_mark(ef_ctx* ctx, const uint64_t* d_recv, uint32_t n_recv, uint32_t
   OwnerArgs O{d_recv, n_recv, d_verdict, ctx->d_step_key.p, ctx->d_step_ord.p, tcap - 1, ctx->d_vis.p, ctx->vis_mask,
               ctx->d_vis_count.p, ctx->d_vis_err.p};
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((n_recv + 255) / 256, ctx->n_sm * 8));
-  k_owner_claim<<<grid, 256, 0, ctx->st>>>(O);
-  k_owner_resolve<<<grid, 256, 0, ctx->st>>>(O);
-  if (insert_visited) k_owner_insert<<<grid, 256, 0, ctx->st>>>(O);
+  ++ctx->kcount, k_owner_claim<<<grid, 256, 0, ctx->st>>>(O);
+  ++ctx->kcount, k_owner_resolve<<<grid, 256, 0, ctx->st>>>(O);
+  if (insert_visited) ++ctx->kcount, k_owner_insert<<<grid, 256, 0, ctx->st>>>(O);
   EF_CUDA(cudaGetLastError());
   return insert_visited ? vis_settle(ctx) : (cudaStreamSynchronize(ctx->st) == cudaSuccess ? EF_OK : EF_ERR_CUDA);
 }
@@ -1603,10 +1612,10 @@ int ef_expand_finish(ef_ctx* ctx, const uint32_t* d_verdict_back, const ef_price
   cudaEventRecord(ctx->ev[3], ctx->st);
   if (ctx->n_send) {
     const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((ctx->n_send + 255) / 256, ctx->n_sm * 8));
-    k_apply_verdicts<<<grid, 256, 0, ctx->st>>>(ctx->d_res.p, ctx->d_perm.p, d_verdict_back, ctx->n_send,
+    ++ctx->kcount, k_apply_verdicts<<<grid, 256, 0, ctx->st>>>(ctx->d_res.p, ctx->d_perm.p, d_verdict_back, ctx->n_send,
                                                 pp->node_cap);
     const uint32_t gc = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));
-    k_compact_survivors<<<gc, 256, 0, ctx->st>>>(ctx->d_res.p, total, ctx->d_plist.p, ctx->d_scalars.p + 7);
+    ++ctx->kcount, k_compact_survivors<<<gc, 256, 0, ctx->st>>>(ctx->d_res.p, total, ctx->d_plist.p, ctx->d_scalars.p + 7);
     EF_CUDA(cudaGetLastError());
   }
   cudaEventRecord(ctx->ev[4], ctx->st);
@@ -1670,9 +1679,9 @@ int ef_keep(ef_ctx* ctx, const uint32_t* cand_idx, uint32_t n, const uint32_t* s
   A.sel = ctx->d_sel.p;
   A.n_sel = n;
   A.dst = ctx->d_dst.p;
-  k_materialise<kMatThreads><<<std::min<uint32_t>(n, ctx->n_sm * 8), kMatThreads, 0, ctx->st>>>(A);
+  ++ctx->kcount, k_materialise<kMatThreads><<<std::min<uint32_t>(n, ctx->n_sm * 8), kMatThreads, 0, ctx->st>>>(A);
   EF_CUDA(cudaGetLastError());
-  k_keep_alg<<<std::min<uint32_t>(n, ctx->n_sm * 8), 128, 0, ctx->st>>>(ctx->d_alg8.p, ctx->step_S, ctx->d_sel.p,
+  ++ctx->kcount, k_keep_alg<<<std::min<uint32_t>(n, ctx->n_sm * 8), 128, 0, ctx->st>>>(ctx->d_alg8.p, ctx->step_S, ctx->d_sel.p,
                                                                       ctx->d_dst.p, n, g);
   EF_CUDA(cudaGetLastError());
   // node keys, sorted order and ranks of the new records (every parent carries them)
@@ -1722,8 +1731,8 @@ int ef_materialise(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents
     A.req_sig = ctx->d_req_sig.p;
     A.req_dv = ctx->d_req_dv.p;
     A.req_sig_cap = A.req_dv_cap = ctx->d_req_sig.p ? ctx->req_cap : 0;
-    k_match<kMatchThreads><<<std::min<uint32_t>(n_parents, ctx->n_sm * 8), kMatchThreads, 0, ctx->st>>>(A);
-    k_offsets<1024><<<1, 1024, 0, ctx->st>>>(A);
+    ++ctx->kcount, k_match<kMatchThreads><<<std::min<uint32_t>(n_parents, ctx->n_sm * 8), kMatchThreads, 0, ctx->st>>>(A);
+    ++ctx->kcount, k_offsets<1024><<<1, 1024, 0, ctx->st>>>(A);
     EF_CUDA(cudaGetLastError());
     std::vector<uint32_t> coff(n_parents + 1);
     EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
@@ -1743,7 +1752,7 @@ int ef_materialise(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents
     A.sel = ctx->d_sel.p;
     A.n_sel = n;
     A.dst = ctx->d_dst.p;
-    k_materialise<kMatThreads><<<std::min<uint32_t>(n, ctx->n_sm * 8), kMatThreads, 0, ctx->st>>>(A);
+    ++ctx->kcount, k_materialise<kMatThreads><<<std::min<uint32_t>(n, ctx->n_sm * 8), kMatThreads, 0, ctx->st>>>(A);
     EF_CUDA(cudaGetLastError());
     EF_CUDA(ctx->d_hash_out.reserve(n, ctx->st));
     if ((rc = hash_records_full(ctx, ctx->sc[0], ctx->st, ctx->d_dst.p, n, ctx->d_hash_out.p))) return rc;
@@ -1764,7 +1773,7 @@ int ef_last_timing(ef_ctx* ctx, float* ms, uint32_t n) {
 }
 
 int ef_last_stats(ef_ctx* ctx, uint64_t* out, uint32_t n) {
-  for (uint32_t k = 0; k < n && k < 4; ++k) out[k] = ctx->last_stats[k];
+  for (uint32_t k = 0; k < n && k < 5; ++k) out[k] = ctx->last_stats[k];
   return EF_OK;
 }
 
@@ -1797,7 +1806,7 @@ int ef_records_write_packed_async(ef_ctx* ctx, const uint32_t* slots, uint32_t n
   EF_CUDA(cudaMemcpyAsync(ctx->d_up_stage.p, host, bytes, cudaMemcpyHostToDevice, st));
   EF_CUDA(cudaMemcpyAsync(ctx->d_up_off.p, ctx->h_up_off.data(), n * 8ull, cudaMemcpyHostToDevice, st));
   EF_CUDA(cudaMemcpyAsync(ctx->d_up_dst.p, ctx->h_up_dst.data(), n * 8ull, cudaMemcpyHostToDevice, st));
-  k_unpack<<<std::min<uint32_t>(n, ctx->n_sm * 8), 256, 0, st>>>(reinterpret_cast<const uint8_t*>(ctx->d_up_stage.p),
+  ++ctx->kcount, k_unpack<<<std::min<uint32_t>(n, ctx->n_sm * 8), 256, 0, st>>>(reinterpret_cast<const uint8_t*>(ctx->d_up_stage.p),
                                                                  ctx->d_up_off.p, ctx->d_up_dst.p, n, ctx->geo);
   EF_CUDA(cudaGetLastError());
   int rc = hash_records_full(ctx, ctx->sc[1], st, ctx->d_up_dst.p, n, nullptr, max_n, max_refs);
@@ -1827,7 +1836,7 @@ int ef_b2b_peak(ef_ctx* ctx, double* compress_per_s) {
   double best = 0;
   for (int rep = 0; rep < 4; ++rep) {
     cudaEventRecord(ctx->ev[0], ctx->st);
-    k_b2b_peak<<<blocks, threads, 0, ctx->st>>>(out.p, iters);
+    ++ctx->kcount, k_b2b_peak<<<blocks, threads, 0, ctx->st>>>(out.p, iters);
     cudaEventRecord(ctx->ev[1], ctx->st);
     EF_CUDA(cudaEventSynchronize(ctx->ev[1]));
     float ms = 0;

@@ -95,7 +95,8 @@ struct VArgs {
   uint64_t pstride;
   uint32_t Os;         // words per output-source row
   uint32_t* outsrc;    // [n][Os] key source of every (remapped) graph output (k_dirty_warp)
-  int slots;           // 1: k_dirty_warp wrote outsrc instead of didx rows
+  int slots;           // 1: rows <= kFastRows (k_dirty_warp, k_merge)
+  int osrc;            // 1: the dirty kernel wrote outsrc (graph output key sources) instead of didx rows
   uint32_t W;          // words per removed-mask row
   uint32_t* rmask;     // [n][W] parent keys (by sorted rank) absent from the candidate: dropped or dirty
   uint64_t* fresh_sorted;  // [n][S][2] the fresh keys in ascending byte order
@@ -534,6 +535,221 @@ __global__ void __launch_bounds__(WARPS * 32) k_dirty_warp(VArgs A) {
 }
 
 // ------------------------------------------------------------------------------------------
+// k_dirty_big (parents beyond 256 slots): one warp per candidate walks the topological slots
+// 32 at a time from its first touched slot.  Lane i holds slot 32w + i, which is dirty iff it
+// is a seed (the node rewritten in place, an owner of a remapped ref) or one of its producers
+// is dirty: producers in earlier windows are final (shared-memory mask), producers inside the
+// window are resolved by iterating the window's ballot to a fixed point (the dirty set only
+// grows).  Job indices are prefix popcounts (the running count + the window's ballot), so the
+// jobs, their key sources and the removed ranks are emitted in the same pass, in the layout
+// k_dirty_warp produces from reach rows (sources at the parent's ref offsets, output sources
+// in outsrc).  The slot tables are the parent's (k_match), shared by its candidates through
+// L1/L2; per window a lane issues independent loads only.  Dynamic shared memory per warp:
+// dm[W], cum[W + 1], rk[W].
+// ------------------------------------------------------------------------------------------
+
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_dirty_big(VArgs A) {
+  extern __shared__ uint32_t db_smem[];
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  const unsigned full = 0xffffffffu;
+  const uint32_t W = A.W;
+  uint32_t* dm = db_smem + (uint64_t)wid * (3 * W + 1);
+  uint32_t* cum = dm + W;
+  uint32_t* rk = cum + W + 1;
+  const Geo& G = A.g;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (uint32_t lc = blockIdx.x * WARPS + wid; lc < A.n; lc += gridDim.x * WARPS) {  // warp-uniform
+    const uint32_t c = A.c0 + lc;
+    if (A.res[c].flags & EF_F_INCOMPLETE) {
+      if (lane == 0) {
+        A.dcount[lc] = 0;
+        A.seg_begin[lc] = A.seg_end[lc] = (int32_t)((uint64_t)lc * A.S);
+      }
+      continue;
+    }
+    const VPlan P = A.plan[c];
+    Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
+    const uint32_t* ps = A.pscratch + (uint64_t)P.parent * A.pstride;
+    const uint32_t* coff = ps + 2 * G.cap_nodes;
+    const uint32_t* clist = coff + 2 * G.cap_nodes + 1;
+    const uint32_t* tslot = clist + G.cap_refs;
+    const uint32_t* s_v = tslot + G.cap_nodes;
+    const uint32_t* s_pk = s_v + G.cap_nodes;
+    const uint32_t* rslot = s_pk + G.cap_nodes;
+    const uint32_t* psig = R.sig(G);
+    const uint32_t* paux = R.aux(G);
+    const uint32_t* pinoff = R.inoff(G);
+    const uint32_t* pnin = R.nin(G);
+    const uint32_t* prefs = R.refs(G);
+    const uint32_t* srank = R.srank(G);
+    const int pn = P.pn;
+    const uint32_t nw = ((uint32_t)pn + 31) >> 5;
+    for (uint32_t w = lane; w < nw; w += 32) dm[w] = rk[w] = cum[w] = 0;
+    __syncwarp();
+    const int ms = P.mod >= 0 ? (int)tslot[P.mod] : -1;
+    const int ds0 = P.drop0 >= 0 ? (int)tslot[P.drop0] : -1, ds1 = P.drop1 >= 0 ? (int)tslot[P.drop1] : -1;
+    if (ms >= 0 && lane == 0) atomicOr(&dm[ms >> 5], 1u << (ms & 31));
+    uint32_t rf[2] = {0xffffffffu, 0xffffffffu};
+    for (int k = 0; k < P.n_rm; ++k) {  // owners of remapped refs (dropped nodes excluded)
+      const uint32_t from = P.rm_from[k], p = from >> 8;
+      rf[k] = (tslot[p] << 8) | (from & 255u);
+      for (uint32_t x = coff[p] + lane; x < coff[p + 1]; x += 32) {
+        const uint32_t q = clist[x];
+        if ((int)q == P.drop0 || (int)q == P.drop1) continue;
+        bool hit = false;
+        for (uint32_t r = pinoff[q]; r < pinoff[q] + pnin[q]; ++r) hit |= prefs[r] == from;
+        if (hit) {
+          const uint32_t t = tslot[q];
+          atomicOr(&dm[t >> 5], 1u << (t & 31));
+        }
+      }
+    }
+    __syncwarp();
+    const int ins = P.ins_slot;
+    auto popc_below = [&](uint32_t t) -> uint32_t {  // dirty slots before t (t = pn: all; set at the end)
+      return t >= (uint32_t)pn ? cum[nw] : cum[t >> 5] + __popc(dm[t >> 5] & ((1u << (t & 31)) - 1u));
+    };
+    auto dirty_at = [&](uint32_t t) -> bool { return (dm[t >> 5] >> (t & 31)) & 1u; };
+    auto fidx = [&](uint32_t t) -> uint32_t { return popc_below(t) + ((int)t > ins && ins >= 0 ? P.n_live : 0); };
+    auto fnew = [&](int k) -> uint32_t {
+      return popc_below((uint32_t)(ins + (P.ins_after ? 1 : 0))) + (k == 1 ? (uint32_t)P.live[0] : 0u);
+    };
+    auto src_pos = [&](uint32_t ref) -> uint32_t {  // a ref in parent-position space -> key source
+      const uint32_t p = ref >> 8, port = ref & 255u;
+      if ((int)p >= pn) return kFresh | (port << 23) | fnew((int)p - pn);
+      const uint32_t t = tslot[p];
+      return dirty_at(t) ? (kFresh | (port << 23) | fidx(t)) : ((port << 23) | p);
+    };
+    Job* jobs = A.jobs + (uint64_t)lc * A.S;
+    uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
+    // levels of the key DAG for k_keys_wide: by job in jlvl, by slot in the (step-mode idle) jv row
+    const bool levels = A.jlvl != nullptr;
+    uint16_t* lv = levels ? A.jlvl + (uint64_t)lc * A.S : nullptr;
+    uint32_t* plv = A.jv + (uint64_t)lc * A.S;
+    auto new_level = [&](int k) -> uint32_t {  // a new node: 1 + its producer's level if that is fresh
+      uint32_t extra = 0, p = P.new_ref[k] >> 8;
+      if ((int)p >= pn) {  // the other new node
+        extra = 1;
+        p = P.new_ref[(int)p - pn] >> 8;
+        if ((int)p >= pn) return extra;
+      }
+      const uint32_t tq = tslot[p];
+      return extra + (dirty_at(tq) ? plv[tq] + 1u : 0u);
+    };
+    uint32_t run = 0;
+    const uint32_t w0 = (uint32_t)max(P.first, 0) >> 5;
+    // the first window's slot table entries, then one window ahead
+    uint32_t t = 32u * w0 + lane;
+    uint32_t pk = t < (uint32_t)pn ? s_pk[t] : 0u;
+    for (uint32_t w = w0; w < nw; ++w) {
+      const bool live = t < (uint32_t)pn;
+      const uint32_t tn = t + 32u;
+      const uint32_t pk_next = tn < (uint32_t)pn ? s_pk[tn] : 0u;
+      const uint32_t r0 = pk & 0xffffffu, nr = pk >> 24;
+      const bool dropped = (int)t == ds0 || (int)t == ds1;
+      const uint32_t word = dm[w];
+      bool d = false;
+      uint32_t inmask = 0;
+      if (live && !dropped) {
+        d = (word >> lane) & 1u;
+        for (uint32_t k = 0; k < nr && !d; ++k) {
+          const uint32_t rsl = rslot[r0 + k], tp = rsl >> 8;
+          if (rsl == rf[0] || rsl == rf[1]) continue;  // remapped: its owner is a seed
+          if ((tp >> 5) == w) inmask |= 1u << (tp & 31u);
+          else d = dirty_at(tp);
+        }
+      }
+      uint32_t cur = __ballot_sync(full, d);
+      while (true) {  // producers inside the window: to the fixed point
+        d = d || (inmask & cur) != 0u;
+        const uint32_t nxt = __ballot_sync(full, d);
+        if (nxt == cur) break;
+        cur = nxt;
+      }
+      if (lane == 0) {
+        dm[w] = cur;
+        cum[w] = run;
+      }
+      __syncwarp();
+      const uint32_t j = run + __popc(cur & lt) + ((int)t > ins && ins >= 0 ? (uint32_t)P.n_live : 0u);
+      uint32_t lvl = 0, inl = 0;  // level: 1 + the deepest fresh producer; inl: fresh producers in the window
+      if (d) {
+        const uint32_t v = s_v[t];
+        auto lvl_of = [&](uint32_t tq) {
+          if ((tq >> 5) == w) inl |= 1u << (tq & 31u);
+          else lvl = max(lvl, plv[tq] + 1u);
+        };
+        for (uint32_t k = 0; k < nr; ++k) {
+          const uint32_t rsl = rslot[r0 + k];
+          uint32_t sv;
+          if (rsl == rf[0] || rsl == rf[1]) {  // the owner now consumes another producer (a remap)
+            const uint32_t to = rsl == rf[0] ? P.rm_to[0] : P.rm_to[1];
+            sv = src_pos(to);
+            if (levels) {
+              const uint32_t p = to >> 8;
+              if ((int)p >= pn) lvl = max(lvl, new_level((int)p - pn) + 1u);
+              else if (sv & kFresh) lvl_of(tslot[p]);
+            }
+          } else {
+            const uint32_t tp = rsl >> 8, port = rsl & 255u;
+            const bool f = dirty_at(tp);
+            sv = f ? (kFresh | (port << 23) | fidx(tp)) : ((port << 23) | (prefs[r0 + k] >> 8));
+            if (levels && f) lvl_of(tp);
+          }
+          rs[r0 + k] = sv;
+        }
+        const bool m = (int)t == ms;
+        jobs[j] = Job{m ? P.mod_sig : psig[v], m ? P.mod_aux : paux[v], r0, nr};
+        const uint32_t k = srank[v];
+        atomicOr(&rk[k >> 5], 1u << (k & 31));
+      }
+      if (levels) {
+        if (__any_sync(full, inl != 0u)) {  // in-window producers sit on lower lanes: one ascending pass
+#pragma unroll 4
+          for (int b = 0; b < 31; ++b) {
+            const uint32_t x = __shfl_sync(full, lvl, b);
+            if ((inl >> b) & 1u) lvl = max(lvl, x + 1u);
+          }
+        }
+        if (d) {
+          plv[t] = lvl;
+          lv[j] = (uint16_t)min(lvl, 65535u);
+        }
+      }
+      run += __popc(cur);
+      t = tn;
+      pk = pk_next;
+    }
+    if (lane == 0) cum[nw] = run;
+    __syncwarp();
+    const uint32_t pref = R.h().n_refs;
+    if (lane < 2 && P.live[lane]) {  // the new nodes, exempt from the remap (rules.py:186-188)
+      rs[pref + lane] = src_pos(P.new_ref[lane]);
+      jobs[fnew((int)lane)] = Job{P.new_sig[lane], P.new_aux[lane], pref + lane, 1u};
+      if (levels) lv[fnew((int)lane)] = (uint16_t)min(new_level((int)lane), 65535u);
+    }
+    if (lane == 0) {
+      if (P.drop0 >= 0) atomicOr(&rk[srank[P.drop0] >> 5], 1u << (srank[P.drop0] & 31));
+      if (P.drop1 >= 0) atomicOr(&rk[srank[P.drop1] >> 5], 1u << (srank[P.drop1] & 31));
+    }
+    const uint32_t* pouts = R.outs(G);
+    uint32_t* os = A.outsrc + (uint64_t)lc * A.Os;
+    for (int o = lane; o < R.h().n_out; o += 32) os[o] = src_pos(vremap(P, pouts[o]));
+    __syncwarp();
+    uint32_t* grm = A.rmask + (uint64_t)lc * A.W;
+    for (uint32_t w = lane; w < nw; w += 32) grm[w] = rk[w];
+    if (lane == 0) {
+      const uint32_t j = run + (uint32_t)P.n_live;
+      A.dcount[lc] = j;
+      A.seg_begin[lc] = (int32_t)((uint64_t)lc * A.S);
+      A.seg_end[lc] = (int32_t)((uint64_t)lc * A.S + j);
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // message assembly: a byte stream packed into aligned 64-bit words of a per-thread column
 // (word q of thread t at col[q * BT]), so the message can be indexed dynamically while the
 // compression itself runs on registers
@@ -791,21 +1007,27 @@ __global__ void __launch_bounds__(BT, EF_KEYS_MINB) k_keys(VArgs A) {
 // The candidate's skey row is scratch for the level sort until the keys are done.
 // ------------------------------------------------------------------------------------------
 
-template <int BT>
+template <int BT, int LPC>
 __global__ void __launch_bounds__(BT) k_keys_wide(VArgs A) {
   constexpr int WPB = BT / 32;
+  constexpr int GPW = 32 / LPC;  // candidates per warp
   __shared__ uint64_t msg[kKeyMaxW * BT];
   const Geo& G = A.g;
   const Tables& T = A.T;
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  const uint32_t sl = lane % LPC, grp = lane / LPC;
+  const unsigned gmask = LPC == 32 ? 0xffffffffu : (((1u << LPC) - 1u) << (grp * LPC));
   uint64_t* col = msg + threadIdx.x;
   const unsigned full = 0xffffffffu;
-  for (uint32_t l = blockIdx.x * WPB + wid; l < A.n; l += gridDim.x * WPB) {  // warp-uniform
-    const uint32_t lc = A.order[l];
-    const uint32_t d = A.dcount[lc];
-    if (d < A.wide_min) break;  // sorted by job count: the rest belong to k_keys
+  for (uint32_t base = (blockIdx.x * WPB + wid) * GPW; base < A.n; base += gridDim.x * WPB * GPW) {  // warp-uniform
+    const uint32_t l = base + grp;
+    const uint32_t lc = l < A.n ? A.order[l] : 0u;
+    const uint32_t d = l < A.n ? A.dcount[lc] : 0u;
+    const bool has = l < A.n && d >= A.wide_min;
+    if (!__any_sync(full, has)) break;  // sorted by job count: the rest belong to k_keys
+    uint32_t nl = 0, ncomp = 0;
     const uint32_t c = A.c0 + lc;
-    const uint64_t* pkeys = Rec{reinterpret_cast<char*>(A.parent_addr[A.plan[c].parent])}.keys(G);
+    const uint64_t* pkeys = nullptr;
     const Job* jobs = A.jobs + (uint64_t)lc * A.S;
     const uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
     const uint16_t* lv = A.jlvl + (uint64_t)lc * A.S;
@@ -814,45 +1036,48 @@ __global__ void __launch_bounds__(BT) k_keys_wide(VArgs A) {
     uint32_t* sval = A.sval + (uint64_t)lc * A.S;
     uint32_t* ord = reinterpret_cast<uint32_t*>(skey);  // [S] jobs by level
     uint32_t* cnt = ord + A.S;                          // [S] per level: count -> start -> end
-    uint32_t L = 0;
-    for (uint32_t j = lane; j < d; j += 32) L = max(L, (uint32_t)lv[j]);
-    L = __reduce_max_sync(full, L);
-    uint32_t nl = L + 1;
-    if (L >= 65535u) {  // levels saturated (a > 65k-deep key chain): one job per "level", in index order
-      nl = d;
-      for (uint32_t x = lane; x < d; x += 32) {
-        ord[x] = x;
-        cnt[x] = x + 1;
-      }
-      __syncwarp();
-    } else {
-      for (uint32_t x = lane; x < nl; x += 32) cnt[x] = 0;
-      __syncwarp();
-      for (uint32_t j = lane; j < d; j += 32) atomicAdd(&cnt[lv[j]], 1u);
-      __syncwarp();
-      uint32_t run = 0;
-      for (uint32_t x0 = 0; x0 < nl; x0 += 32) {
-        const uint32_t x = x0 + lane;
-        const uint32_t v = x < nl ? cnt[x] : 0u;
-        uint32_t inc = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(full, inc, o);
-          if ((int)lane >= o) inc += y;
+    if (has) {  // group-uniform: the counting sort of the candidate's jobs by level
+      pkeys = Rec{reinterpret_cast<char*>(A.parent_addr[A.plan[c].parent])}.keys(G);
+      uint32_t L = 0;
+      for (uint32_t j = sl; j < d; j += LPC) L = max(L, (uint32_t)lv[j]);
+      L = __reduce_max_sync(gmask, L);
+      nl = L + 1;
+      if (L >= 65535u) {  // levels saturated (a > 65k-deep key chain): one job per "level", in index order
+        nl = d;
+        for (uint32_t x = sl; x < d; x += LPC) {
+          ord[x] = x;
+          cnt[x] = x + 1;
         }
-        if (x < nl) cnt[x] = run + inc - v;
-        run += __shfl_sync(full, inc, 31);
+        __syncwarp(gmask);
+      } else {
+        for (uint32_t x = sl; x < nl; x += LPC) cnt[x] = 0;
+        __syncwarp(gmask);
+        for (uint32_t j = sl; j < d; j += LPC) atomicAdd(&cnt[lv[j]], 1u);
+        __syncwarp(gmask);
+        uint32_t run = 0;
+        for (uint32_t x0 = 0; x0 < nl; x0 += LPC) {
+          const uint32_t x = x0 + sl;
+          const uint32_t v = x < nl ? cnt[x] : 0u;
+          uint32_t inc = v;
+#pragma unroll
+          for (int o = 1; o < LPC; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(gmask, inc, o, LPC);
+            if ((int)sl >= o) inc += y;
+          }
+          if (x < nl) cnt[x] = run + inc - v;
+          run += __shfl_sync(gmask, inc, LPC - 1, LPC);
+        }
+        __syncwarp(gmask);
+        for (uint32_t j = sl; j < d; j += LPC) ord[atomicAdd(&cnt[lv[j]], 1u)] = j;
+        __syncwarp(gmask);  // cnt[level] is now the end of the level's run in ord
       }
-      __syncwarp();
-      for (uint32_t j = lane; j < d; j += 32) ord[atomicAdd(&cnt[lv[j]], 1u)] = j;
-      __syncwarp();  // cnt[level] is now the end of the level's run in ord
     }
-    uint32_t ncomp = 0, b = 0;
-    for (uint32_t lev = 0; lev < nl; ++lev) {
-      const uint32_t e = cnt[lev];
-      for (uint32_t x0 = b; x0 < e; x0 += 32) {
-        const uint32_t x = x0 + lane;
-        if (x >= e) continue;
+    // rounds: every group takes up to LPC jobs of its current level; a level's keys are
+    // visible to the next level's lanes after the round's __syncwarp
+    uint32_t lev = 0, pos = 0, e = has ? cnt[0] : 0u;
+    while (__any_sync(full, lev < nl)) {
+      const uint32_t x = pos + sl;
+      if (lev < nl && x < e) {
         const uint32_t jj = ord[x];
         const Job jb = jobs[jj];
         const bool input = jb.nin & kInputJob;
@@ -919,12 +1144,20 @@ __global__ void __launch_bounds__(BT) k_keys_wide(VArgs A) {
         fresh[2 * jj] = h0;
         fresh[2 * jj + 1] = h1;
       }
-      __syncwarp();  // this level's keys are visible to the next level's lanes
-      b = e;
+      if (lev < nl) {
+        pos += LPC;
+        if (pos >= e) {
+          pos = e;
+          if (++lev < nl) e = cnt[lev];
+        }
+      }
+      __syncwarp();
     }
-    for (uint32_t j = lane; j < d; j += 32) {  // the sort records (the level scratch is dead)
-      skey[j] = B2b::bswap64(fresh[2 * j]);
-      sval[j] = j;
+    if (has) {
+      for (uint32_t j = sl; j < d; j += LPC) {  // the sort records (the level scratch is dead)
+        skey[j] = B2b::bswap64(fresh[2 * j]);
+        sval[j] = j;
+      }
     }
     ncomp = __reduce_add_sync(full, ncomp);
     if (A.stats && lane == 0) atomicAdd(A.stats, (unsigned long long)ncomp);
@@ -1249,37 +1482,147 @@ __global__ void __launch_bounds__(BT) k_keys_quad(VArgs A) {
   }
 }
 
-// runs of equal first words (a 2^-64 event unless the keys are identical) ordered by the second
-__global__ void k_sortfix(VArgs A) {
-  for (uint32_t lc = blockIdx.x * blockDim.x + threadIdx.x; lc < A.n; lc += gridDim.x * blockDim.x) {
+// Candidates ordered by job count, largest first (the lanes of a k_keys warp then run about
+// the same number of compressions; k_keys_wide takes a prefix): a counting sort over the
+// exact counts.  bins[S - count] is histogrammed, scanned by one CTA, then every candidate
+// claims its position with one warp-aggregated atomic per distinct count in the warp.
+__global__ void k_count_hist(const uint32_t* dcount, uint32_t n, uint32_t S, uint32_t* bins) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(bins + (S - min(dcount[i], S)), 1u);
+}
+
+template <int BT>
+__global__ void __launch_bounds__(BT) k_count_scan(uint32_t* bins, uint32_t nb) {
+  __shared__ uint32_t sh_scan[BT / 32 + 1];
+  uint32_t run = 0;
+  for (uint32_t b0 = 0; b0 < nb; b0 += BT) {
+    const uint32_t b = b0 + threadIdx.x;
+    const uint32_t v = b < nb ? bins[b] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<BT>(v, &tot, sh_scan);
+    if (b < nb) bins[b] = run + ex;
+    run += tot;
+    __syncthreads();
+  }
+}
+
+__global__ void k_count_scatter(const uint32_t* dcount, uint32_t n, uint32_t S, uint32_t* bins, uint32_t* order) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t span = (n + 31) / 32 * 32;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < span; i += gridDim.x * blockDim.x) {
+    const bool live = i < n;
+    const unsigned act = __ballot_sync(0xffffffffu, live);
+    if (!live) continue;
+    const uint32_t b = S - min(dcount[i], S);
+    const unsigned peers = __match_any_sync(act, b);
+    const uint32_t leader = (uint32_t)(__ffs(peers) - 1);
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(bins + b, (uint32_t)__popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    order[base + __popc(peers & ((1u << lane) - 1u))] = i;
+  }
+}
+
+// Rows of more than 1024 fresh keys: one CTA per candidate (largest first).  Runs of up to R
+// keys are bitonic-sorted in shared memory on (first 4 key bytes, big endian) << 32 | job
+// index; runs are merged pairwise in the candidate's two global sort rows (merge path: each
+// thread writes a 1/BT stretch of the output); runs of equal first 4 bytes (p ~ d^2 / 2^33 per
+// candidate) are then ordered by the full key as in k_sortkeys, and the keys are gathered into
+// fresh_sorted with 16-byte loads and coalesced 16-byte stores.  Dynamic shared memory: R words.
+template <int BT>
+__global__ void __launch_bounds__(BT) k_sortbig(VArgs A, uint32_t R) {
+  extern __shared__ uint64_t sbig[];
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t l = blockIdx.x; l < A.n; l += gridDim.x) {
+    const uint32_t lc = A.order[l];
     const uint32_t d = A.dcount[lc];
-    const uint64_t* sk = A.skey_sorted + (uint64_t)lc * A.S;
-    uint32_t* sv = A.sval_sorted + (uint64_t)lc * A.S;
-    const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
-    for (uint32_t i = 0; i + 1 < d;) {
-      if (sk[i] != sk[i + 1]) {
-        ++i;
-        continue;
-      }
-      uint32_t e = i + 1;
-      while (e < d && sk[e] == sk[i]) ++e;
-      for (uint32_t x = i + 1; x < e; ++x) {  // insertion sort of [i, e) by the second word
-        const uint32_t v = sv[x];
-        const uint64_t lv = B2b::bswap64(fresh[2 * v + 1]);
-        uint32_t y = x;
-        while (y > i && B2b::bswap64(fresh[2 * sv[y - 1] + 1]) > lv) {
-          sv[y] = sv[y - 1];
-          --y;
+    if (d == 0) continue;  // CTA-uniform
+    uint64_t* in = A.skey + (uint64_t)lc * A.S;  // first key words (big endian); free after the runs
+    uint64_t* runs = const_cast<uint64_t*>(A.skey_sorted) + (uint64_t)lc * A.S;
+    for (uint32_t r0 = 0; r0 < d; r0 += R) {
+      const uint32_t len = min(R, d - r0);
+      uint32_t m = 2;
+      while (m < len) m <<= 1;
+      for (uint32_t i = tid; i < m; i += BT) sbig[i] = i < len ? ((in[r0 + i] >> 32) << 32) | (r0 + i) : ~0ull;
+      __syncthreads();
+      for (uint32_t k = 2; k <= m; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+          for (uint32_t p = tid; p < (m >> 1); p += BT) {
+            const uint32_t i = 2 * p - (p & (j - 1));  // the pair (i, i + j), bit j of i clear
+            const uint64_t a = sbig[i], b = sbig[i + j];
+            if ((a > b) == ((i & k) == 0)) {
+              sbig[i] = b;
+              sbig[i + j] = a;
+            }
+          }
+          __syncthreads();
         }
-        sv[y] = v;
       }
-      i = e;
+      for (uint32_t i = tid; i < len; i += BT) runs[r0 + i] = sbig[i];
+      __syncthreads();
     }
-    uint64_t* dst = A.fresh_sorted + 2ull * lc * A.S;
-    for (uint32_t i = 0; i < d; ++i) {
-      dst[2 * i] = fresh[2 * sv[i]];
-      dst[2 * i + 1] = fresh[2 * sv[i] + 1];
+    uint64_t* src = runs;
+    uint64_t* dst = in;
+    for (uint32_t w = R; w < d; w <<= 1) {  // pairwise merges of the sorted runs
+      for (uint32_t a0 = 0; a0 < d; a0 += 2 * w) {
+        const uint32_t na = min(w, d - a0);
+        const uint32_t nb = a0 + w < d ? min(w, d - a0 - w) : 0u;
+        const uint64_t* Ap = src + a0;
+        const uint64_t* Bp = Ap + na;
+        uint64_t* O = dst + a0;
+        const uint32_t tot = na + nb, per = (tot + BT - 1) / BT;
+        const uint32_t D = min(tot, per * tid), E = min(tot, D + per);
+        uint32_t lo = D > nb ? D - nb : 0u, hi = min(D, na);
+        while (lo < hi) {  // values are distinct (the job index is in the low word)
+          const uint32_t mid = (lo + hi) >> 1;
+          if (Ap[mid] < Bp[D - mid - 1]) lo = mid + 1;
+          else hi = mid;
+        }
+        uint32_t i = lo, j = D - lo;
+        for (uint32_t o = D; o < E; ++o) {
+          const bool ta = j >= nb || (i < na && Ap[i] < Bp[j]);
+          O[o] = ta ? Ap[i++] : Bp[j++];
+        }
+      }
+      __syncthreads();
+      uint64_t* t = src;
+      src = dst;
+      dst = t;
     }
+    const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
+    int tie = 0;
+    for (uint32_t i = tid; i + 1 < d; i += BT) tie |= (src[i] >> 32) == (src[i + 1] >> 32);
+    if (__syncthreads_or(tie) && tid == 0) {
+      auto less = [&](uint32_t x, uint32_t y) {
+        const uint64_t a0 = B2b::bswap64(fresh[2 * x]), b0 = B2b::bswap64(fresh[2 * y]);
+        if (a0 != b0) return a0 < b0;
+        return B2b::bswap64(fresh[2 * x + 1]) < B2b::bswap64(fresh[2 * y + 1]);
+      };
+      for (uint32_t i = 0; i + 1 < d;) {
+        uint32_t e = i + 1;
+        while (e < d && (src[e] >> 32) == (src[i] >> 32)) ++e;
+        for (uint32_t x = i + 1; x < e; ++x) {  // insertion sort of the run by the full key
+          const uint64_t v = src[x];
+          uint32_t y = x;
+          while (y > i && less((uint32_t)v, (uint32_t)src[y - 1])) {
+            src[y] = src[y - 1];
+            --y;
+          }
+          src[y] = v;
+        }
+        i = e;
+      }
+    }
+    __syncthreads();
+    uint4* out = reinterpret_cast<uint4*>(A.fresh_sorted + 2ull * lc * A.S);
+    const uint4* f4 = reinterpret_cast<const uint4*>(fresh);
+    uint32_t* osv = A.sval_sorted + (uint64_t)lc * A.S;
+    for (uint32_t i = tid; i < d; i += BT) {
+      const uint32_t v = (uint32_t)src[i];
+      out[i] = f4[v];
+      if (A.full) osv[i] = v;
+    }
+    __syncthreads();
   }
 }
 
@@ -1817,7 +2160,7 @@ __global__ void __launch_bounds__(BT, EF_DIGEST_MINB) k_digest_pm(VArgs A) {
             const uint32_t ref = vremap(P, pouts[gi]);
             if (part == 0) {
               const uint64_t* kp;
-              if (A.slots) {
+              if (A.osrc) {
                 const uint32_t sv = A.outsrc[(uint64_t)lc * A.Os + gi], idx = sv & 0x7fffffu;
                 kp = (sv & kFresh) ? fresh + 2 * idx : pkeys + 2 * idx;
               } else {

@@ -595,10 +595,10 @@ class DeviceSession:
         return float(ms[8])
 
     def last_stats(self) -> dict:
-        out = (C.c_uint64 * 4)()
-        self.L.ef_last_stats(self.ctx, out, 4)
+        out = (C.c_uint64 * 5)()
+        self.L.ef_last_stats(self.ctx, out, 5)
         return {"key_compressions": int(out[0]), "digest_compressions": int(out[1]), "candidates": int(out[2]),
-                "priced": int(out[3])}
+                "priced": int(out[3]), "kernels": int(out[4])}
 
     def b2b_peak(self) -> float:
         """Measured BLAKE2b compressions/s of this GPU (the hash kernels' ALU roofline)."""

@@ -104,16 +104,18 @@ class _Visible:
 
     def __init__(self, session: DeviceSession, db: CostDatabase, profiler, append_path):
         self.s, self.db, self.profiler, self.path = session, db, profiler, append_path
+        self.known: set[int] = set()  # signature ids whose rows `db` already holds (it only grows)
 
     def touch(self, sig_ids) -> int:
         made = 0
         fh = None
         try:
             for sid in sig_ids:
-                if sid == 0xFFFFFFFF:
+                if sid == 0xFFFFFFFF or sid in self.known:
                     continue
                 sig = self.s.sig_list[sid]
                 if self.db.has_signature(sig.text):
+                    self.known.add(sid)
                     continue
                 if fh is None and self.path:
                     fh = open(self.path, "a")
@@ -127,6 +129,7 @@ class _Visible:
                     if fh is not None:
                         fh.write(record_line(sig.text, alg, rec) + "\n")
                         fh.flush()
+                self.known.add(sid)
         finally:
             if fh is not None:
                 fh.close()
@@ -581,6 +584,9 @@ class Frontier:
         heap = [(r0.cost, h0, self.run.root)]
         slots: list[int] = []
         seen = {h0}
+        # every graph as its rewrite path from g0: the index of each rewrite in its parent's
+        # (rule, site) enumeration (rules.neighbors order), so a CPU run can rebuild the batch
+        paths: dict[int, tuple[int, ...]] = {self.run.root: ()}
         while heap and len(slots) < n_parents:
             cost, h, slot = heapq.heappop(heap)
             slots.append(slot)
@@ -601,11 +607,13 @@ class Frontier:
                 keep = sorted(sorted(keep, key=lambda i: (cs[i], hs[i]))[:room])
             for i, sl in zip(keep, self.s.keep(keep)):
                 heapq.heappush(heap, (cs[i], hs[i], sl))
+                paths[sl] = paths[slot] + (i,)
         # fill the batch with the remaining enqueued graphs in heap order
         while heap and len(slots) < n_parents:
             slots.append(heapq.heappop(heap)[2])
         self.leftover = [sl for _, _, sl in heap]
         self.slots = slots
+        self.paths = [paths[sl] for sl in slots]
         # The timed steps start from an empty visited set: every parent of the batch was already
         # expanded (or enqueued) while the batch was built, so keeping that set would mark most
         # candidates visited; each step is the first expansion of these graphs.  The step's

@@ -19,6 +19,7 @@ are keyed on them:
 from __future__ import annotations
 
 import base64
+import functools
 import heapq
 import json
 from dataclasses import dataclass, field
@@ -423,7 +424,7 @@ class NodeSignature:
     input_shapes: tuple[tuple[int, ...], ...]
     params: tuple[tuple[str, Any], ...]
 
-    @property
+    @functools.cached_property
     def text(self) -> str:
         head = [self.kind]
         if self.input_shapes:

@@ -1,5 +1,5 @@
 """Synthetic random DAGs of 1k-20k nodes (BASELINE configs[4]) through the batched
-step: scratch chunking, the cub segmented-sort path for rows > 1024 keys, and
+step: scratch chunking, the CTA key sort (k_sortbig) for rows > 1024 keys, and
 thousands of outputs in the graph digest.  A sample of every step's candidates is
 checked against the oracle (canonical hash, and the inner search of priced ones)."""
 
@@ -101,3 +101,36 @@ def test_merge_path_stream_matches_in_thread_merge(model, monkeypatch):
     assert len(out["0"]) == len(out["1"]) > 0
     for key in ("hash", "flags", "cost", "time_ms", "energy", "evals", "sweeps"):
         assert np.array_equal(out["0"][key], out["1"][key]), key
+
+
+def _step_with(g0, monkeypatch, env: dict, parents: int = 6):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    fr = Frontier(g0, ef.CostDatabase(), ef.SyntheticProfiler(0), ef.CostFunction.energy(),
+                  ef.SearchConfig(alpha=1.05), parents)
+    try:
+        return fr.step().copy()
+    finally:
+        fr.close()
+
+
+@pytest.mark.parametrize("model", ["dag:1000", "dag:5000", "nasnet_a"])
+@pytest.mark.parametrize("knob,values", [
+    ("EF_DIRTY_BIG", ("0", "1")),            # k_dirty (thread walk) vs k_dirty_big (warp window walk)
+    ("EF_WIDE_LPC", ("32", "16", "8", "4")),  # k_keys_wide lane groups
+    ("EF_QUAD_MAX", ("0", "100000000")),     # k_keys (thread) vs k_keys_quad for the rest
+])
+def test_large_graph_kernel_variants_agree(model, knob, values, monkeypatch):
+    """Every kernel variant of the large-graph step produces the same candidates: hash, flags,
+    and price of every candidate identical (EF_WIDE_MIN=1 sends all candidates to the level
+    kernel where the knob concerns it)."""
+    import numpy as np
+
+    g0 = zoo.random_dag(int(model[4:]), 0) if model.startswith("dag") else zoo.generate(model, 0)
+    extra = {"EF_WIDE_MIN": "1"} if knob == "EF_WIDE_LPC" else {}
+    outs = [_step_with(g0, monkeypatch, {**extra, knob: v}, 2 if model == "dag:5000" else 6) for v in values]
+    assert len(outs[0]) > 0
+    for o in outs[1:]:
+        assert len(o) == len(outs[0])
+        for key in ("hash", "flags", "cost", "time_ms", "energy", "evals", "sweeps"):
+            assert np.array_equal(outs[0][key], o[key]), (knob, key)

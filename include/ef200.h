@@ -33,6 +33,7 @@ extern "C" {
 #define EF_ERR_ARG (-1)
 #define EF_ERR_CUDA (-2)
 #define EF_ERR_CAPACITY (-3)
+#define EF_ERR_INTERNAL (-4) /* a device-side invariant failed (a bug: reported, never silent) */
 #define EF_NEED_RESOLVE 1 /* ef_expand found signatures/weight sets not yet interned */
 
 /* operator kinds (order of reference graph.py:25-36 OpKind) */

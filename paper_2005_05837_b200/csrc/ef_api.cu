@@ -90,6 +90,8 @@ struct ef_ctx {
   uint32_t wide_min = 512;  // jobs per candidate from which k_keys_wide takes it (EF_WIDE_MIN; 0: off)
   bool dirty_big = true;  // rows > kFastRows: k_dirty_big (warp window walk); EF_DIRTY_BIG=0: k_dirty
   uint32_t wide_lpc = 16;  // lanes per candidate in k_keys_wide: 32, 16, 8 or 4 (EF_WIDE_LPC)
+  bool fuse_merge = true;  // rows > kFastRows: k_digest_mg merges on the fly (EF_FUSE_MERGE=0: k_merge_big + k_digest_pm)
+  bool digest_pf = true;  // rows > kFastRows: k_digest_pm loads the next block's key words ahead (EF_DIGEST_PF)
   uint32_t quad_max = 20000;  // chunks below this many candidates hash with k_keys_quad (EF_QUAD_MAX)
   uint64_t chunk_mib = 0;  // per-chunk hashing scratch budget, MiB (0: half the free HBM, <= 96 GiB)
 
@@ -177,6 +179,7 @@ struct ef_ctx {
   uint32_t n_chunks = 0;
   float last_ms[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   uint64_t last_stats[5] = {0, 0, 0, 0, 0};
+  bool alg_rows = false;  // the last step's alg8 rows hold row indices (price_d1), not algorithm ids
   uint64_t kcount = 0;  // kernels launched by the library (every launch site counts)
   uint64_t kcount_step0 = 0;  // kcount when the last step began
 };
@@ -251,6 +254,8 @@ ef_ctx* ef_create(int device) {
     const uint32_t v = (uint32_t)strtoul(e, nullptr, 10);
     ctx->wide_lpc = v >= 32 ? 32u : v >= 16 ? 16u : v >= 8 ? 8u : 4u;
   }
+  if (const char* e = getenv("EF_FUSE_MERGE")) ctx->fuse_merge = atoi(e) != 0;
+  if (const char* e = getenv("EF_DIGEST_PF")) ctx->digest_pf = atoi(e) != 0;
   if (const char* e = getenv("EF_QUAD_MAX")) ctx->quad_max = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_CHUNK_MIB")) ctx->chunk_mib = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
   cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
@@ -535,7 +540,16 @@ int ef_tables_commit(ef_ctx* ctx) {
     std::vector<uint32_t> info(2 * std::max<size_t>(ns, 1), 0);
     for (size_t i = 0; i < ns; ++i) {
       info[2 * i] = roff[i];
-      info[2 * i + 1] = rn[i] | (ctx->sig_desc[i].kind == EF_K_INPUT ? 0x80000000u : 0u);
+      uint32_t y = rn[i] | (ctx->sig_desc[i].kind == EF_K_INPUT ? kInfoInput : 0u);
+      if (rn[i]) {  // the exact skips of price_d1: no row below row 0 in time / in energy
+        bool tmin = true, emin = true;
+        for (uint32_t q = 1; q < rn[i]; ++q) {
+          tmin = tmin && ctx->row_t[i][q] >= ctx->row_t[i][0];
+          emin = emin && ctx->row_e[i][q] >= ctx->row_e[i][0];
+        }
+        y |= (tmin ? kInfoTMin : 0u) | (emin ? kInfoEMin : 0u);
+      }
+      info[2 * i + 1] = y;
     }
     if ((rc = upload(ctx, ctx->d_sig_info, info))) return rc;
   }
@@ -1347,17 +1361,21 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
         }
         EF_CUDA(cudaGetLastError());
         cudaEventRecord(ce[3], ctx->st);
-        ++ctx->kcount, k_digest_pm<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+        ++ctx->kcount, k_digest_pm<kHashThreads, false, EF_DIGEST_MINB><<<gd, kHashThreads, 0, ctx->st>>>(V);
       } else {
         if ((rc = sort_fresh_keys(ctx, sc, ctx->st, V))) return rc;
-        if (ctx->big_merge) {  // merge-path key stream, then the streaming digest
+        if (ctx->big_merge && ctx->fuse_merge) {  // the digest merges the two sorted streams itself
+          cudaEventRecord(ce[3], ctx->st);
+          ++ctx->kcount, k_digest_mg<kHashThreads, 2><<<gd, kHashThreads, 0, ctx->st>>>(V);
+        } else if (ctx->big_merge) {  // merge-path key stream, then the streaming digest
           const size_t smem = 4ull * 4 * (V.W + 1);
           EF_CUDA(cudaFuncSetAttribute(k_merge_big<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
           const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
           ++ctx->kcount, k_merge_big<4><<<gm, 128, smem, ctx->st>>>(V);
           EF_CUDA(cudaGetLastError());
           cudaEventRecord(ce[3], ctx->st);
-          ++ctx->kcount, k_digest_pm<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
+          if (ctx->digest_pf) ++ctx->kcount, k_digest_pm<kHashThreads, true, 2><<<gd, kHashThreads, 0, ctx->st>>>(V);
+          else ++ctx->kcount, k_digest_pm<kHashThreads, false, EF_DIGEST_MINB><<<gd, kHashThreads, 0, ctx->st>>>(V);
         } else {
           cudaEventRecord(ce[3], ctx->st);
           ++ctx->kcount, k_digest<kHashThreads><<<gd, kHashThreads, 0, ctx->st>>>(V);
@@ -1448,6 +1466,9 @@ static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
       ++ctx->kcount, k_price_v<K, false><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);                                \
     }                                                                                                      \
   } while (0)
+  ctx->alg_rows = fast;  // price_d1 leaves row indices (k_keep_alg reads the ids)
+  if (fast && !sm && !Pv.algt)  // the global rows start at row 0 (price_d1 writes changes only)
+    EF_CUDA(cudaMemsetAsync(ctx->d_alg8.p, 0, (uint64_t)std::max<uint32_t>(total, 1) * ctx->step_S, ctx->st));
   if (fast && pp->kind == EF_C_ENERGY) EF_PRICE(EF_C_ENERGY);
   else if (fast && pp->kind == EF_C_TIME) EF_PRICE(EF_C_TIME);
   else if (fast && pp->kind == EF_C_LINEAR) EF_PRICE(EF_C_LINEAR);
@@ -1505,6 +1526,13 @@ static int step_sync(ef_ctx* ctx, bool timings) {
     ctx->last_stats[4] = ctx->kcount - ctx->kcount_step0;
   }
   EF_REQUIRE(!(err & 4u), "candidate exceeds record capacity (raise cap_nodes/cap_refs)");
+  if (err & 16u) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "k_keys_wide: job levels out of range (chunk candidate %u: %u jobs, level %u)",
+             ctx->h_scalars[10], ctx->h_scalars[11], ctx->h_scalars[12]);
+    ctx->err = buf;
+    return EF_ERR_INTERNAL;
+  }
   if (ctx->last_req_sig || ctx->last_req_dv) return EF_NEED_RESOLVE;
   return EF_OK;
 }
@@ -1682,7 +1710,8 @@ int ef_keep(ef_ctx* ctx, const uint32_t* cand_idx, uint32_t n, const uint32_t* s
   ++ctx->kcount, k_materialise<kMatThreads><<<std::min<uint32_t>(n, ctx->n_sm * 8), kMatThreads, 0, ctx->st>>>(A);
   EF_CUDA(cudaGetLastError());
   ++ctx->kcount, k_keep_alg<<<std::min<uint32_t>(n, ctx->n_sm * 8), 128, 0, ctx->st>>>(ctx->d_alg8.p, ctx->step_S, ctx->d_sel.p,
-                                                                      ctx->d_dst.p, n, g);
+                                                                      ctx->d_dst.p, n, g, make_tables(ctx),
+                                                                      (int)ctx->alg_rows);
   EF_CUDA(cudaGetLastError());
   // node keys, sorted order and ranks of the new records (every parent carries them)
   EF_CUDA(ctx->d_hash_out.reserve(n, ctx->st));

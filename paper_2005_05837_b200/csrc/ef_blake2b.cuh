@@ -221,5 +221,51 @@ __device__ __forceinline__ void b2b_compress_col(uint64_t* h, const uint64_t* co
   h[7] ^= v7 ^ v15;
 }
 
+// The same compression for kernels with few resident warps (large graphs): the rounds are
+// rolled in pairs with two message register sets, and the next round's schedule-ordered words
+// are read from the column while the current round runs, so the shared-memory latency does not
+// sit in front of every round's G chain.
+template <int BT>
+__device__ __forceinline__ void b2b_col_load(uint64_t* m, const uint64_t* col, int r) {
+  const uint8_t* s = kB2bSigma[r < 10 ? r : r - 10];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) m[i] = col[s[i] * BT];
+}
+
+template <int BT>
+__device__ __forceinline__ void b2b_compress_col_pf(uint64_t* h, const uint64_t* col, uint64_t t, bool last) {
+  uint64_t v0 = h[0], v1 = h[1], v2 = h[2], v3 = h[3], v4 = h[4], v5 = h[5], v6 = h[6], v7 = h[7];
+  uint64_t v8 = b2b_iv(0), v9 = b2b_iv(1), v10 = b2b_iv(2), v11 = b2b_iv(3);
+  uint64_t v12 = b2b_iv(4) ^ t, v13 = b2b_iv(5), v14 = b2b_iv(6), v15 = b2b_iv(7);
+  if (last) v14 = ~v14;
+  uint64_t ma[16], mb[16];
+  b2b_col_load<BT>(ma, col, 0);
+#define EF_B2B_ROUND(m)                          \
+  EF_B2B_G(v0, v4, v8, v12, m[0], m[1]);         \
+  EF_B2B_G(v1, v5, v9, v13, m[2], m[3]);         \
+  EF_B2B_G(v2, v6, v10, v14, m[4], m[5]);        \
+  EF_B2B_G(v3, v7, v11, v15, m[6], m[7]);        \
+  EF_B2B_G(v0, v5, v10, v15, m[8], m[9]);        \
+  EF_B2B_G(v1, v6, v11, v12, m[10], m[11]);      \
+  EF_B2B_G(v2, v7, v8, v13, m[12], m[13]);       \
+  EF_B2B_G(v3, v4, v9, v14, m[14], m[15]);
+#pragma unroll 1
+  for (int r = 0; r < 12; r += 2) {
+    b2b_col_load<BT>(mb, col, r + 1);
+    EF_B2B_ROUND(ma)
+    if (r + 2 < 12) b2b_col_load<BT>(ma, col, r + 2);
+    EF_B2B_ROUND(mb)
+  }
+#undef EF_B2B_ROUND
+  h[0] ^= v0 ^ v8;
+  h[1] ^= v1 ^ v9;
+  h[2] ^= v2 ^ v10;
+  h[3] ^= v3 ^ v11;
+  h[4] ^= v4 ^ v12;
+  h[5] ^= v5 ^ v13;
+  h[6] ^= v6 ^ v14;
+  h[7] ^= v7 ^ v15;
+}
+
 }  // namespace ef
 #endif

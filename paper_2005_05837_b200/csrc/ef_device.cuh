@@ -10,6 +10,11 @@ namespace ef {
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr uint32_t kOutMark = 1u << 24;  // added to a use count when the edge is a graph output
 constexpr uint32_t kEmptyWset = 0;       // weight-set id of "no weights"
+// Tables::sig_info[s].y: the signature's row count and flags
+constexpr uint32_t kInfoRows = 0xffffffu;    // number of cost rows
+constexpr uint32_t kInfoInput = 1u << 31;    // input node (no rows, not priced)
+constexpr uint32_t kInfoEMin = 1u << 30;     // no row has less energy than row 0
+constexpr uint32_t kInfoTMin = 1u << 29;     // no row has less time than row 0
 
 // record geometry (byte offsets inside one slot); mirrors ef_geometry
 struct Geo {
@@ -38,7 +43,7 @@ struct Rec {
 // read-only tables, passed by value to kernels
 struct Tables {
   const ef_sig_desc* sig_desc;
-  const uint2* sig_info;  // per signature: {row_off, row_n | is_input << 31} (pricing)
+  const uint2* sig_info;  // per signature: {row_off, row_n | flags} (kInfo*; pricing)
   const uint32_t* sig_text_off;
   const uint32_t* sig_text_len;
   const uint8_t* sig_text;

@@ -1317,8 +1317,20 @@ __device__ __forceinline__ double cost_of(const ef_price_params& f, double time_
 // warp-synchronously: every loop runs a warp-uniform trip count (the lanes of `mask` price
 // different candidates whose node counts differ by a few), with no early exits, so the warp
 // never splits into groups that would then run the whole sweep one after another.
+//
+// Two exact shortcuts.  (1) The cost kinds time, energy and linear(w in [0, 1], positive refs)
+// are non-decreasing in both totals, and `cost == cost_of(t_tot, e_tot)` holds throughout, so
+// a node none of whose rows is below row 0 in the kind's totals (kInfoTMin / kInfoEMin, set
+// per signature at commit) can never take an alternative: adding a non-negative difference
+// never lowers a total (round-to-nearest is monotone).  Such a node stays at row 0 and only
+// counts its nr - 1 evaluations per sweep, so the sweeps skip it (the `skip` argument of the
+// kind).  (2) The row is zero on entry (row 0 everywhere; the caller clears it), the first
+// sweep reads no row entry and a sweep writes a node's entry only when it changes.  The row
+// holds ROW indices, not algorithm ids; the ids are read from the signature's rows where a
+// record is written (k_keep_alg).
 template <int KIND, class View, class Alg>
-__device__ void price_d1(const PriceArgs& A, const View& V, Alg alg, ef_cand_result& res, unsigned mask) {
+__device__ void price_d1(const PriceArgs& A, const View& V, Alg alg, ef_cand_result& res, unsigned mask,
+                         uint32_t skip) {
   const Tables& T = A.T;
   const ef_price_params& F = A.pp;
   const int n = V.n;
@@ -1327,19 +1339,31 @@ __device__ void price_d1(const PriceArgs& A, const View& V, Alg alg, ef_cand_res
   st.init();
   se.init();
   int ncomp = 0;
+  long long skip_evals = 0;  // evaluations per sweep of the skipped nodes
   bool missing = false;
-  for (int i = 0; i < nmax; ++i) {
-    if (i < n && !missing) {
-      const uint2 info = V.info(i, T);
-      if (!(info.y >> 31)) {
-        ++ncomp;
-        if (info.y == 0) {
-          missing = true;
-        } else {
-          alg[i] = 0;
-          st.add(T.row_t[info.x]);
-          se.add(T.row_e[info.x]);
-        }
+  constexpr int G = 8;  // nodes whose rows are requested together (independent loads)
+  for (int i0 = 0; i0 < nmax; i0 += G) {
+    uint2 inf[G];
+    double rt[G], re[G];
+#pragma unroll
+    for (int k = 0; k < G; ++k) inf[k] = i0 + k < n ? V.info(i0 + k, T) : make_uint2(0u, kInfoInput);
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const bool row = !(inf[k].y & kInfoInput) && (inf[k].y & kInfoRows);
+      rt[k] = row ? T.row_t[inf[k].x] : 0.0;
+      re[k] = row ? T.row_e[inf[k].x] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      if (missing || (inf[k].y & kInfoInput)) continue;
+      ++ncomp;
+      const uint32_t nr = inf[k].y & kInfoRows;
+      if (nr == 0) {
+        missing = true;
+      } else {
+        st.add(rt[k]);
+        se.add(re[k]);
+        if (skip && (inf[k].y & skip) == skip) skip_evals += nr - 1;
       }
     }
   }
@@ -1351,37 +1375,44 @@ __device__ void price_d1(const PriceArgs& A, const View& V, Alg alg, ef_cand_res
   bool running = !missing && ncomp > 0;
   while (__any_sync(mask, running)) {
     bool changed = false;
-    if (running) ++sweeps;
-    uint2 info_next = V.info(0, T);
-    for (int i = 0; i < nmax; ++i) {
-      const uint2 info = info_next;  // this node's rows were requested one iteration ahead
-      if (i + 1 < n) info_next = V.info(i + 1, T);
-      if (!running || i >= n) continue;
-      const uint32_t nr = info.y;  // input rows have bit 31 set: skipped by the test below
-      if (nr < 2u || (nr >> 31)) continue;
-      const uint32_t ro = info.x;
-      const uint32_t start = alg[i];
-      uint32_t cur = start;
-      double ct = T.row_t[ro + cur], ce = T.row_e[ro + cur];
-      for (uint32_t q = 0; q < nr; ++q) {  // branch-free body
-        const double qt = T.row_t[ro + q], qe = T.row_e[ro + q];
-        double dt = 0.0, de = 0.0;
-        dt += qt - ct;
-        de += qe - ce;
-        const double nt = t_tot + dt, ne = e_tot + de;
-        const double cand = cost_of<KIND>(F, nt, ne);
-        const bool act = q != start;
-        evals += act ? 1 : 0;
-        const bool take = act && cand < cost;
-        cur = take ? q : cur;
-        ct = take ? qt : ct;
-        ce = take ? qe : ce;
-        t_tot = take ? nt : t_tot;
-        e_tot = take ? ne : e_tot;
-        cost = take ? cand : cost;
-        changed = changed || take;
+    if (running) {
+      ++sweeps;
+      evals += skip_evals;
+    }
+    const bool first = sweeps == 1;
+    for (int i0 = 0; i0 < nmax; i0 += G) {
+      uint2 inf[G];  // the rows of G nodes requested together
+#pragma unroll
+      for (int k = 0; k < G; ++k) inf[k] = running && i0 + k < n ? V.info(i0 + k, T) : make_uint2(0u, kInfoInput);
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        const int i = i0 + k;
+        const uint32_t nr = inf[k].y & kInfoRows;
+        if (nr < 2u || (inf[k].y & kInfoInput) || (skip && (inf[k].y & skip) == skip)) continue;
+        const uint32_t ro = inf[k].x;
+        const uint32_t start = first ? 0u : (uint32_t)alg[i];
+        uint32_t cur = start;
+        double ct = T.row_t[ro + cur], ce = T.row_e[ro + cur];
+        for (uint32_t q = 0; q < nr; ++q) {  // branch-free body
+          const double qt = T.row_t[ro + q], qe = T.row_e[ro + q];
+          double dt = 0.0, de = 0.0;
+          dt += qt - ct;
+          de += qe - ce;
+          const double nt = t_tot + dt, ne = e_tot + de;
+          const double cand = cost_of<KIND>(F, nt, ne);
+          const bool act = q != start;
+          evals += act ? 1 : 0;
+          const bool take = act && cand < cost;
+          cur = take ? q : cur;
+          ct = take ? qt : ct;
+          ce = take ? qe : ce;
+          t_tot = take ? nt : t_tot;
+          e_tot = take ? ne : e_tot;
+          cost = take ? cand : cost;
+          changed = changed || take;
+        }
+        if (cur != start) alg[i] = (uint8_t)cur;
       }
-      alg[i] = (uint8_t)cur;
     }
     running = running && changed;
   }
@@ -1389,17 +1420,21 @@ __device__ void price_d1(const PriceArgs& A, const View& V, Alg alg, ef_cand_res
     res.flags |= EF_F_MISSING;
     return;
   }
-  for (int i = 0; i < n; ++i) {
-    const uint2 info = V.info(i, T);
-    if (info.y >> 31) continue;
-    alg[i] = (uint8_t)T.row_alg[info.x + alg[i]];
-  }
   res.cost = cost;
   res.time_ms = t_tot;
   res.energy = e_tot;
   res.evals = evals;
   res.sweeps = sweeps;
   res.flags |= EF_F_PRICED;
+}
+
+// the per-signature bits of a cost kind's exact skip (price_d1), given the price parameters
+template <int KIND>
+__device__ __forceinline__ uint32_t d1_skip_bits(const ef_price_params& f) {
+  if (KIND == EF_C_TIME) return kInfoTMin;
+  if (KIND == EF_C_ENERGY) return kInfoEMin;
+  if (KIND == EF_C_LINEAR && f.w >= 0.0 && f.w <= 1.0 && f.t_ref > 0.0 && f.e_ref > 0.0) return kInfoTMin | kInfoEMin;
+  return 0u;
 }
 
 // a candidate's algorithm row: global bytes, or a shared-memory column (stride = block size)

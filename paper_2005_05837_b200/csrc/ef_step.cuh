@@ -673,12 +673,36 @@ __global__ void __launch_bounds__(WARPS * 32) k_dirty_big(VArgs A) {
       }
       __syncwarp();
       const uint32_t j = run + __popc(cur & lt) + ((int)t > ins && ins >= 0 ? (uint32_t)P.n_live : 0u);
-      uint32_t lvl = 0, inl = 0;  // level: 1 + the deepest fresh producer; inl: fresh producers in the window
+      // level: the deepest fresh producer + 1.  A producer in this window is resolved by the
+      // shuffle pass below (in[k]: lanes whose level + k + 1 bounds this one: k = 1, 2 through
+      // one or two new nodes, whose level is their producer's + 1)
+      uint32_t lvl = 0, in1 = 0, in2 = 0, in3 = 0;
       if (d) {
         const uint32_t v = s_v[t];
-        auto lvl_of = [&](uint32_t tq) {
-          if ((tq >> 5) == w) inl |= 1u << (tq & 31u);
-          else lvl = max(lvl, plv[tq] + 1u);
+        auto dep = [&](uint32_t tq, uint32_t plus) {
+          if ((tq >> 5) == w) {
+            const uint32_t bit = 1u << (tq & 31u);
+            if (plus == 1u) in1 |= bit;
+            else if (plus == 2u) in2 |= bit;
+            else in3 |= bit;
+          } else {
+            lvl = max(lvl, plv[tq] + plus);
+          }
+        };
+        auto lvl_of = [&](uint32_t tq) { dep(tq, 1u); };
+        auto new_dep = [&](int k) {  // a fresh new node as a producer: its level is its producer's + 1
+          uint32_t plus = 2, p = P.new_ref[k] >> 8;
+          if ((int)p >= pn) {  // the other new node
+            plus = 3;
+            p = P.new_ref[(int)p - pn] >> 8;
+            if ((int)p >= pn) {
+              lvl = max(lvl, 2u);
+              return;
+            }
+          }
+          const uint32_t tq = tslot[p];
+          if (dirty_at(tq)) dep(tq, plus);
+          else lvl = max(lvl, plus - 1u);
         };
         for (uint32_t k = 0; k < nr; ++k) {
           const uint32_t rsl = rslot[r0 + k];
@@ -688,7 +712,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_dirty_big(VArgs A) {
             sv = src_pos(to);
             if (levels) {
               const uint32_t p = to >> 8;
-              if ((int)p >= pn) lvl = max(lvl, new_level((int)p - pn) + 1u);
+              if ((int)p >= pn) new_dep((int)p - pn);
               else if (sv & kFresh) lvl_of(tslot[p]);
             }
           } else {
@@ -705,11 +729,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_dirty_big(VArgs A) {
         atomicOr(&rk[k >> 5], 1u << (k & 31));
       }
       if (levels) {
-        if (__any_sync(full, inl != 0u)) {  // in-window producers sit on lower lanes: one ascending pass
+        if (__any_sync(full, (in1 | in2 | in3) != 0u)) {  // in-window producers sit on lower lanes: one ascending pass
 #pragma unroll 4
           for (int b = 0; b < 31; ++b) {
             const uint32_t x = __shfl_sync(full, lvl, b);
-            if ((inl >> b) & 1u) lvl = max(lvl, x + 1u);
+            if ((in1 >> b) & 1u) lvl = max(lvl, x + 1u);
+            if ((in2 >> b) & 1u) lvl = max(lvl, x + 2u);
+            if ((in3 >> b) & 1u) lvl = max(lvl, x + 3u);
           }
         }
         if (d) {
@@ -1041,6 +1067,14 @@ __global__ void __launch_bounds__(BT) k_keys_wide(VArgs A) {
       uint32_t L = 0;
       for (uint32_t j = sl; j < d; j += LPC) L = max(L, (uint32_t)lv[j]);
       L = __reduce_max_sync(gmask, L);
+      if (L < 65535u && L >= d) {  // a level is at most the job count - 1: report, hash in job order
+        if (sl == 0 && atomicOr(A.err, 16u) == 0u) {
+          A.err[9] = lc;
+          A.err[10] = d;
+          A.err[11] = L;
+        }
+        L = 65535u;
+      }
       nl = L + 1;
       if (L >= 65535u) {  // levels saturated (a > 65k-deep key chain): one job per "level", in index order
         nl = d;
@@ -1137,7 +1171,7 @@ __global__ void __launch_bounds__(BT) k_keys_wide(VArgs A) {
           b2b_start(h, 16);
           ncomp += nb;
           for (uint32_t bk = 0; bk < nb; ++bk)
-            b2b_compress_col<BT>(h, col + 16 * bk * BT, (uint64_t)min(len, 128u * (bk + 1)), bk + 1 == nb);
+            b2b_compress_col_pf<BT>(h, col + 16 * bk * BT, (uint64_t)min(len, 128u * (bk + 1)), bk + 1 == nb);
           h0 = h[0];
           h1 = h[1];
         }
@@ -2115,8 +2149,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge_big(VArgs A) {
 // The graph digest over a pre-merged key stream: the prefix (input declarations, output keys
 // and ports) goes through the word sink; the keys follow as full words with a constant byte
 // shift, loaded 16 words per block with independent 16-byte loads.
-template <int BT>
-__global__ void __launch_bounds__(BT, EF_DIGEST_MINB) k_digest_pm(VArgs A) {
+// PF: the key words of block b + 1 are loaded into registers while block b is compressed
+// (large graphs: a few resident warps per SM cannot hide the stream's DRAM latency otherwise)
+template <int BT, bool PF, int MINB>
+__global__ void __launch_bounds__(BT, MINB) k_digest_pm(VArgs A) {
   __shared__ uint64_t blk[16 * BT];
   const Geo& G = A.g;
   const Tables& T = A.T;
@@ -2139,6 +2175,183 @@ __global__ void __launch_bounds__(BT, EF_DIGEST_MINB) k_digest_pm(VArgs A) {
     const uint32_t nblk = (uint32_t)((len + 127) >> 7);
     int phase = 0;  // 0 input text, 1 outputs, 2 keys, 3 done
     uint32_t gi = 0, part = 0, kw = 0;
+    uint64_t cw1 = 0;
+    WordSink<BT> sk;
+    sk.init(col);
+    uint64_t h[8];
+    b2b_start(h, 8);
+    uint4 pf[9];
+    uint32_t pf_kw = 0xffffffffu;
+    for (uint32_t b = 0; b < nblk; ++b) {
+      sk.q = 0;
+      while (sk.q < 16 && phase < 2) {
+        if (phase == 0) {
+          if (gi * 8 < li) {
+            sk.push(__ldg(A.input_words + gi), min(8u, li - gi * 8));
+            ++gi;
+          } else {
+            phase = 1;
+            gi = 0;
+          }
+        } else {
+          if ((int)gi < n_out) {
+            const uint32_t ref = vremap(P, pouts[gi]);
+            if (part == 0) {
+              const uint64_t* kp;
+              if (A.osrc) {
+                const uint32_t sv = A.outsrc[(uint64_t)lc * A.Os + gi], idx = sv & 0x7fffffu;
+                kp = (sv & kFresh) ? fresh + 2 * idx : pkeys + 2 * idx;
+              } else {
+                const uint32_t p = ref >> 8, fi = didx[p];
+                kp = fi ? fresh + 2 * (fi - 1) : pkeys + 2 * p;
+              }
+              sk.push(kp[0], 8);
+              cw1 = kp[1];
+              part = 1;
+            } else if (part == 1) {
+              sk.push(cw1, 8);
+              part = 2;
+            } else {
+              sk.push(port_be(ref & 255u), 2);
+              part = 0;
+              ++gi;
+            }
+          } else {
+            phase = 2;
+          }
+        }
+      }
+      if (phase == 2 && sk.q < 16) {  // keys: full words at a constant shift
+        const uint32_t room = 16 - sk.q;
+        const uint32_t take = min(room, kwords - kw);
+        uint64_t wv[16];
+        if (pf_kw == kw) {  // the 16-byte pairs covering [kw, kw + 16) were loaded a block ahead
+          const bool odd = kw & 1u;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const uint4 x = odd ? pf[(i + 1) >> 1] : pf[i >> 1];
+            const bool hi = odd ? !(i & 1) : (i & 1);
+            wv[i] = hi ? (((uint64_t)x.w << 32) | x.z) : (((uint64_t)x.y << 32) | x.x);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            if ((uint32_t)i < take) {
+              const uint4 x = *reinterpret_cast<const uint4*>(ks + ((kw + i) & ~1u));
+              // kw is even except after an odd take; load the aligned pair then pick
+              const uint64_t lo = ((uint64_t)x.y << 32) | x.x, hi = ((uint64_t)x.w << 32) | x.z;
+              if ((kw & 1u) == 0) {
+                wv[i] = lo;
+                wv[i + 1] = hi;
+              } else {
+                wv[i] = hi;
+                wv[i + 1] = (uint32_t)(i + 1) < take ? ks[kw + i + 1] : 0;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if ((uint32_t)i < take) sk.push(wv[i], 8);
+        kw += take;
+        if (kw == kwords) phase = 3;
+        if (PF && kw < kwords) {  // the next block's pairs, in flight under this compression
+          const uint32_t p0 = kw >> 1, np = (kwords + 1) >> 1;
+          const uint4* k4 = reinterpret_cast<const uint4*>(ks);
+#pragma unroll
+          for (int k = 0; k < 9; ++k) pf[k] = p0 + k < np ? k4[p0 + k] : make_uint4(0, 0, 0, 0);
+          pf_kw = kw;
+        }
+      }
+      if (phase == 3 && sk.q < 16) {
+        sk.flush();
+        for (uint32_t q = sk.q; q < 16; ++q) col[q * BT] = 0;
+      }
+      b2b_compress_col<BT>(h, col, len < 128ull * (b + 1) ? len : 128ull * (b + 1), b + 1 == nblk);
+    }
+    A.res[c].hash = B2b::bswap64(h[0]);
+    if (A.stats) atomicAdd(A.stats + 1, (unsigned long long)nblk);
+  }
+}
+
+// Rows > 256, fused: the graph digest of k_digest_pm with the key stream produced on the fly
+// instead of read from a merged row (no k_merge_big, no stream written and re-read: 2 x 16 B
+// per key of HBM traffic saved).  The thread merges, in the digest's order, the parent's
+// sorted keys minus the removed ranks (A: kept ranks walked through the removed mask, the keys
+// read from the parent record, shared by the parent's candidates through L2) with the
+// candidate's sorted fresh keys (B, from the key sort), parent first on equal keys as in
+// k_merge / k_merge_big.  The next A keys and the next B key are in flight while a key is
+// placed, so the compression's loads are L2 hits with their latency overlapped.
+template <int BT, int MINB>
+__global__ void __launch_bounds__(BT, MINB) k_digest_mg(VArgs A) {
+  __shared__ uint64_t blk[16 * BT];
+  const Geo& G = A.g;
+  const Tables& T = A.T;
+  uint64_t* col = blk + threadIdx.x;
+  for (uint32_t lc = blockIdx.x * BT + threadIdx.x; lc < A.n; lc += gridDim.x * BT) {
+    const uint32_t c = A.c0 + lc;
+    if (A.res[c].flags & EF_F_INCOMPLETE) continue;
+    const VPlan& P = A.plan[c];
+    Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
+    const uint64_t* pkeys = R.keys(G);
+    const uint32_t* pouts = R.outs(G);
+    const int n_out = R.h().n_out;
+    const uint32_t* didx = A.didx + (uint64_t)lc * A.S;
+    const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
+    const uint32_t li = T.input_text_len;
+    const uint32_t n_child = (uint32_t)(P.n_keep + P.n_live);
+    const uint64_t len = (uint64_t)li + 18ull * n_out + 16ull * n_child;
+    const uint32_t nblk = (uint32_t)((len + 127) >> 7);
+    // the two sorted streams
+    const uint32_t pn = (uint32_t)P.pn, d = A.dcount[lc];
+    const uint32_t* rm = A.rmask + (uint64_t)lc * A.W;
+    const uint4* a4 = reinterpret_cast<const uint4*>(R.skeys(G));
+    const uint4* b4 = reinterpret_cast<const uint4*>(A.fresh_sorted + 2ull * lc * A.S);
+    uint32_t wd = 0, bits = pn ? ~__ldg(rm) & (pn >= 32 ? 0xffffffffu : ((1u << pn) - 1u)) : 0u;
+    auto next_rank = [&]() -> uint32_t {  // the next kept parent rank (pn: none left)
+      while (!bits) {
+        if (++wd >= (pn + 31) >> 5) return pn;
+        bits = ~__ldg(rm + wd);
+        if (wd == (pn >> 5)) bits &= (1u << (pn & 31u)) - 1u;
+      }
+      const uint32_t x = 32u * wd + (uint32_t)(__ffs(bits) - 1);
+      bits &= bits - 1u;
+      return x;
+    };
+    const uint4 z4 = make_uint4(0, 0, 0, 0);
+    uint32_t ra0 = next_rank(), ra1 = ra0 < pn ? next_rank() : pn;
+    uint4 ac = ra0 < pn ? __ldg(a4 + ra0) : z4, an = ra1 < pn ? __ldg(a4 + ra1) : z4;
+    bool ha = ra0 < pn;
+    uint32_t ra2 = ra1 < pn ? next_rank() : pn;
+    uint4 bc = d ? b4[0] : z4, bn = d > 1 ? b4[1] : z4;
+    uint32_t j = 0;
+    auto be = [](const uint4& x, uint64_t& k0, uint64_t& k1) {
+      k0 = B2b::bswap64(((uint64_t)x.y << 32) | x.x);
+      k1 = B2b::bswap64(((uint64_t)x.w << 32) | x.z);
+    };
+    // next key of the merged stream (raw words w0, w1)
+    auto next_key = [&](uint64_t& w0, uint64_t& w1) {
+      uint64_t a0, a1, b0, b1;
+      be(ac, a0, a1);
+      be(bc, b0, b1);
+      const bool take_a = ha && (j >= d || !be_less(b0, b1, a0, a1));
+      const uint4 x = take_a ? ac : bc;
+      w0 = ((uint64_t)x.y << 32) | x.x;
+      w1 = ((uint64_t)x.w << 32) | x.z;
+      if (take_a) {
+        ac = an;
+        ha = ra1 < pn;
+        ra1 = ra2;
+        an = ra2 < pn ? __ldg(a4 + ra2) : z4;
+        ra2 = ra2 < pn ? next_rank() : pn;
+      } else {
+        bc = bn;
+        ++j;
+        bn = j + 1 < d ? b4[j + 1] : z4;
+      }
+    };
+    int phase = 0;  // 0 input text, 1 outputs, 2 keys, 3 done
+    uint32_t gi = 0, part = 0, kdone = 0;
     uint64_t cw1 = 0;
     WordSink<BT> sk;
     sk.init(col);
@@ -2183,36 +2396,36 @@ __global__ void __launch_bounds__(BT, EF_DIGEST_MINB) k_digest_pm(VArgs A) {
           }
         }
       }
-      if (phase == 2 && sk.q < 16) {  // keys: full words at a constant shift
-        const uint32_t room = 16 - sk.q;
-        const uint32_t take = min(room, kwords - kw);
-        uint64_t wv[16];
-#pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          if ((uint32_t)i < take) {
-            const uint4 x = *reinterpret_cast<const uint4*>(ks + ((kw + i) & ~1u));
-            // kw is even except after an odd take; load the aligned pair then pick
-            const uint64_t lo = ((uint64_t)x.y << 32) | x.x, hi = ((uint64_t)x.w << 32) | x.z;
-            if ((kw & 1u) == 0) {
-              wv[i] = lo;
-              wv[i + 1] = hi;
-            } else {
-              wv[i] = hi;
-              wv[i + 1] = (uint32_t)(i + 1) < take ? ks[kw + i + 1] : 0;
-            }
-          }
+      // keys: whole keys (two words) while at least two words are free in the block; a key
+      // that straddles the block boundary leaves its second word for the next block
+      // (an 8-byte push writes exactly one word, whatever the byte shift)
+      while (phase == 2 && sk.q < 16) {
+        if (part == 3) {  // the second word of a straddling key
+          sk.push(cw1, 8);
+          part = 0;
+          if (++kdone == n_child) phase = 3;
+          continue;
         }
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if ((uint32_t)i < take) sk.push(wv[i], 8);
-        kw += take;
-        if (kw == kwords) phase = 3;
+        if (kdone == n_child) {
+          phase = 3;
+          break;
+        }
+        uint64_t w0, w1;
+        next_key(w0, w1);
+        sk.push(w0, 8);
+        if (sk.q < 16) {
+          sk.push(w1, 8);
+          if (++kdone == n_child) phase = 3;
+        } else {
+          cw1 = w1;
+          part = 3;
+        }
       }
       if (phase == 3 && sk.q < 16) {
         sk.flush();
         for (uint32_t q = sk.q; q < 16; ++q) col[q * BT] = 0;
       }
-      b2b_compress_col<BT>(h, col, len < 128ull * (b + 1) ? len : 128ull * (b + 1), b + 1 == nblk);
+      b2b_compress_col_pf<BT>(h, col, len < 128ull * (b + 1) ? len : 128ull * (b + 1), b + 1 == nblk);
     }
     A.res[c].hash = B2b::bswap64(h[0]);
     if (A.stats) atomicAdd(A.stats + 1, (unsigned long long)nblk);
@@ -2396,16 +2609,19 @@ __global__ void __launch_bounds__(EF_PRICE_THREADS) k_price_v(VPriceArgs A, cons
     V.s_new1 = P.new_sig[1];
     V.n = P.n_keep + P.n_live;
     uint8_t* alg = A.alg8 + (uint64_t)c * A.S;
+    const uint32_t skip = d1_skip_bits<KIND>(A.pa.pp);
     if (KIND >= 0 && SM_ROW) {
-      price_d1<KIND>(A.pa, V, AlgRow{sm_alg + threadIdx.x, EF_PRICE_THREADS}, res, mask);
+      for (int i = 0; i < V.n; ++i) sm_alg[i * EF_PRICE_THREADS + threadIdx.x] = 0;
+      price_d1<KIND>(A.pa, V, AlgRow{sm_alg + threadIdx.x, EF_PRICE_THREADS}, res, mask, skip);
       for (int i = 0; i < V.n; ++i) alg[i] = sm_alg[i * EF_PRICE_THREADS + threadIdx.x];
     } else if (KIND >= 0 && A.algt) {  // the row interleaved across the warp: accesses coalesce
       const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
       uint8_t* col = A.algt + (uint64_t)(gt >> 5) * 32u * A.S + (gt & 31u);
-      price_d1<KIND>(A.pa, V, AlgRow{col, 32}, res, mask);
+      for (int i = 0; i < V.n; ++i) col[i * 32] = 0;
+      price_d1<KIND>(A.pa, V, AlgRow{col, 32}, res, mask, skip);
       for (int i = 0; i < V.n; ++i) alg[i] = col[i * 32];
-    } else if (KIND >= 0) {
-      price_d1<KIND>(A.pa, V, AlgRow{alg, 1}, res, mask);
+    } else if (KIND >= 0) {  // the step cleared the rows (alg8)
+      price_d1<KIND>(A.pa, V, AlgRow{alg, 1}, res, mask, skip);
     } else {
       price_graph(A.pa, V, alg, res);
     }
@@ -2413,14 +2629,24 @@ __global__ void __launch_bounds__(EF_PRICE_THREADS) k_price_v(VPriceArgs A, cons
 }
 
 // copy the priced assignment of kept candidates into their materialised records
+// (rows = 1: the step's rows hold row indices (price_d1): the algorithm ids are read from the
+// signature's cost rows; 0: algorithm ids (price_graph))
 __global__ void k_keep_alg(const uint8_t* alg8, uint32_t S, const uint32_t* cand, const unsigned long long* dst,
-                           uint32_t n, Geo G) {
+                           uint32_t n, Geo G, Tables T, int rows) {
   for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
     Rec C{reinterpret_cast<char*>(dst[k])};
     const int nn = C.h().n;
     const uint8_t* src = alg8 + (uint64_t)cand[k] * S;
+    const uint32_t* sig = C.sig(G);
     uint8_t* out = C.alg(G);
-    for (int i = threadIdx.x; i < nn; i += blockDim.x) out[i] = src[i];
+    for (int i = threadIdx.x; i < nn; i += blockDim.x) {
+      uint8_t a = src[i];
+      if (rows) {
+        const uint2 info = T.sig_info[sig[i]];
+        a = (info.y & kInfoInput) ? 0 : (uint8_t)T.row_alg[info.x + a];
+      }
+      out[i] = a;
+    }
   }
 }
 

@@ -60,6 +60,25 @@ def test_random_dag_step_matches_oracle(n_ops, n_parents, sample):
     assert checked >= sample
 
 
+def _step_with(g0, monkeypatch, env: dict, parents: int = 6):
+    """One frontier step in a fresh device session: the tuning knobs (EF_*) are read when a
+    library context is created."""
+    from paper_2005_05837_b200.device import DeviceSession
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    s = DeviceSession()
+    try:
+        fr = Frontier(g0, ef.CostDatabase(), ef.SyntheticProfiler(0), ef.CostFunction.energy(),
+                      ef.SearchConfig(alpha=1.05), parents, session=s)
+        try:
+            return fr.step().copy()
+        finally:
+            fr.close()
+    finally:
+        s.close()
+
+
 @pytest.mark.parametrize("model", ["dag:1000", "nasnet_a"])
 def test_wide_level_keys_match_thread_keys(model, monkeypatch):
     """k_keys_wide (a warp per candidate, jobs by level) against k_keys (a thread per
@@ -70,13 +89,7 @@ def test_wide_level_keys_match_thread_keys(model, monkeypatch):
     g0 = zoo.random_dag(1000, 0) if model.startswith("dag") else zoo.generate(model, 0)
     out = {}
     for wide in ("0", "1"):
-        monkeypatch.setenv("EF_WIDE_MIN", wide)
-        fr = Frontier(g0, ef.CostDatabase(), ef.SyntheticProfiler(0), ef.CostFunction.energy(),
-                      ef.SearchConfig(alpha=1.05), 6)
-        try:
-            out[wide] = fr.step().copy()
-        finally:
-            fr.close()
+        out[wide] = _step_with(g0, monkeypatch, {"EF_WIDE_MIN": wide})
     assert len(out["0"]) == len(out["1"]) > 0
     for key in ("hash", "flags", "cost", "time_ms", "energy", "evals", "sweeps"):
         assert np.array_equal(out["0"][key], out["1"][key]), key
@@ -91,27 +104,10 @@ def test_merge_path_stream_matches_in_thread_merge(model, monkeypatch):
     g0 = zoo.random_dag(1000, 0) if model.startswith("dag") else zoo.generate(model, 0)
     out = {}
     for big in ("0", "1"):
-        monkeypatch.setenv("EF_BIG_MERGE", big)
-        fr = Frontier(g0, ef.CostDatabase(), ef.SyntheticProfiler(0), ef.CostFunction.energy(),
-                      ef.SearchConfig(alpha=1.05), 6)
-        try:
-            out[big] = fr.step().copy()
-        finally:
-            fr.close()
+        out[big] = _step_with(g0, monkeypatch, {"EF_BIG_MERGE": big})
     assert len(out["0"]) == len(out["1"]) > 0
     for key in ("hash", "flags", "cost", "time_ms", "energy", "evals", "sweeps"):
         assert np.array_equal(out["0"][key], out["1"][key]), key
-
-
-def _step_with(g0, monkeypatch, env: dict, parents: int = 6):
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    fr = Frontier(g0, ef.CostDatabase(), ef.SyntheticProfiler(0), ef.CostFunction.energy(),
-                  ef.SearchConfig(alpha=1.05), parents)
-    try:
-        return fr.step().copy()
-    finally:
-        fr.close()
 
 
 @pytest.mark.parametrize("model", ["dag:1000", "dag:5000", "nasnet_a"])
@@ -119,6 +115,8 @@ def _step_with(g0, monkeypatch, env: dict, parents: int = 6):
     ("EF_DIRTY_BIG", ("0", "1")),            # k_dirty (thread walk) vs k_dirty_big (warp window walk)
     ("EF_WIDE_LPC", ("32", "16", "8", "4")),  # k_keys_wide lane groups
     ("EF_QUAD_MAX", ("0", "100000000")),     # k_keys (thread) vs k_keys_quad for the rest
+    ("EF_DIGEST_PF", ("0", "1")),            # k_digest_pm with / without the next block's words ahead
+    ("EF_FUSE_MERGE", ("0", "1")),           # k_merge_big + k_digest_pm vs the fused k_digest_mg
 ])
 def test_large_graph_kernel_variants_agree(model, knob, values, monkeypatch):
     """Every kernel variant of the large-graph step produces the same candidates: hash, flags,

@@ -47,7 +47,7 @@ DEFAULT_WORKLOAD = "dag:20000"
 # --workload: the BASELINE.json configs as frontier workloads (name, objective, parents per GPU)
 WORKLOADS = {
     "dag:20000": ("synthetic random-DAG conv/matmul graph, 20k ops, full rule set, energy objective, alpha=1.05 "
-                  "(BASELINE configs[4], largest synthetic graph)", "energy", 4),
+                  "(BASELINE configs[4], largest synthetic graph)", "energy", 8),
     "resnet50": ("ResNet-50 inference graph, energy objective with per-node conv-algorithm selection, alpha=1.05 "
                  "(BASELINE configs[1])", "energy", 4096),
     "squeezenet": ("SqueezeNet inference graph, energy objective, alpha=1.0 search frontier (BASELINE configs[0])",
@@ -601,8 +601,6 @@ def measure(args, workload: str, ppg: int, world: int, rank: int, local: int, ex
                 "serial_value": ser_priced / (ser_total / 1e3), "serial_ms_per_step": ser_total / args.steps,
                 "serial_upload_hash_ms_per_step": up_ms / args.steps},
         "gpu_launches": launches,
-        "sharded_phases_ms_per_call": ({k: 1e3 * v / phases["calls"] for k, v in phases.items() if k != "calls"}
-                                       if phases else None),
         "clocks": clk,
     }
     cpu_parents = []

@@ -176,6 +176,11 @@ int ef_wset_read(ef_ctx* ctx, uint32_t id, double* w, uint64_t* w_n, double* b, 
 int ef_wset_digest(ef_ctx* ctx, uint32_t id, uint8_t out[16]);
 /* upload lookup tables, compute pending digests; call after puts/derives */
 int ef_tables_commit(ef_ctx* ctx);
+/* host->device bytes the last ef_tables_commit sent: a commit sends only the signatures, rows,
+ * names and weight sets added (or changed) since the previous one and the lookup-table slots
+ * they occupy, so its cost does not grow with the tables (profiling.py:211-252: the reference
+ * memoises once per new signature) */
+int ef_commit_bytes(ef_ctx* ctx, uint64_t* bytes);
 
 /* ---- graph records ------------------------------------------------------ */
 int ef_set_geometry(ef_ctx* ctx, uint32_t cap_nodes, uint32_t cap_refs, uint32_t cap_outs,
@@ -262,6 +267,25 @@ int ef_route_owners(ef_ctx* ctx, uint32_t world, uint64_t order_base, uint64_t* 
 int ef_owner_mark(ef_ctx* ctx, const uint64_t* d_recv, uint32_t n_recv, uint32_t* d_verdict, int insert_visited);
 /* verdicts back in send order -> candidate flags, node cap, pricing of the survivors */
 int ef_expand_finish(ef_ctx* ctx, const uint32_t* d_verdict_back, const ef_price_params* pp);
+/* The same exchange with fixed-capacity buckets, so no count ever travels through the host:
+ * d_send is [world][cap] pairs (cap >= this rank's candidates: the caller all-reduces MAX of
+ * the candidate counts), d_counts[world] the pairs per owner (device).  The collectives run on
+ * the context's stream (ef_stream), so the whole sharded step is stream-ordered. */
+int ef_route_owners_padded(ef_ctx* ctx, uint32_t world, uint64_t order_base, uint32_t cap, uint64_t* d_send,
+                           uint32_t* d_counts);
+/* owner side over [world][cap] received pairs, d_recv_counts[world] valid per source rank;
+ * d_verdict is [world][cap] */
+int ef_owner_mark_padded(ef_ctx* ctx, const uint64_t* d_recv, const uint32_t* d_recv_counts, uint32_t world,
+                         uint32_t cap, uint32_t* d_verdict, int insert_visited);
+/* verdicts back ([world][cap], this rank's send layout) -> flags, node cap, pricing */
+int ef_expand_finish_padded(ef_ctx* ctx, const uint32_t* d_verdict_back, uint32_t world, uint32_t cap,
+                            const ef_price_params* pp);
+/* the CUDA stream (cudaStream_t) the context issues its work on */
+int ef_stream(ef_ctx* ctx, void** stream);
+/* recompute the last step's alpha-prune flags (EF_F_BEST / EF_F_ENQUEUE) from a new best cost
+ * before its first candidate: a rank of a sharded step passes the minimum over the best and
+ * the candidates of the ranks before it (search.py:258-267 across ranks) */
+int ef_reprune(ef_ctx* ctx, double best, double alpha);
 
 /* device time (ms) of the last ef_expand, measured with CUDA events on its stream, per
  * stage: match, plan, dirty walk, node keys, key sort, graph digest, dedup, price, and [8] the

@@ -124,6 +124,12 @@ _PROTOS = {
     "ef_route_owners": (C.c_int, [_P, C.c_uint32, C.c_uint64, C.c_void_p, _U32P]),
     "ef_owner_mark": (C.c_int, [_P, C.c_void_p, C.c_uint32, C.c_void_p, C.c_int]),
     "ef_expand_finish": (C.c_int, [_P, C.c_void_p, C.POINTER(PriceParams)]),
+    "ef_route_owners_padded": (C.c_int, [_P, C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "ef_owner_mark_padded": (C.c_int, [_P, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_int]),
+    "ef_expand_finish_padded": (C.c_int, [_P, C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(PriceParams)]),
+    "ef_stream": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
+    "ef_commit_bytes": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
+    "ef_reprune": (C.c_int, [_P, C.c_double, C.c_double]),
 }
 
 EXPORTED = tuple(_PROTOS)

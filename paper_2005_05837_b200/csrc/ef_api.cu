@@ -60,10 +60,23 @@ struct WeightSet {
   std::vector<uint64_t> hw, hb;  // host copies (raw float64 bits) until the digest is taken
 };
 
+// one lookup-table slot written by an incremental commit (k_ht_scatter)
+struct HtUpd {
+  uint32_t slot, val;
+  unsigned long long key;
+};
+
+__global__ void k_ht_scatter(unsigned long long* keys, uint32_t* vals, const HtUpd* u, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    keys[u[i].slot] = u[i].key;
+    vals[u[i].slot] = u[i].val;
+  }
+}
+
 // per-chunk hashing scratch (ef_step.cuh): one set for steps / keeps on the main stream, one
 // for asynchronous uploads on the upload stream
 struct Scratch {
-  DevBuf<uint32_t> didx, jv, refsrc, dcount, dorder, sval, sval2, rmask, outsrc, cbins;
+  DevBuf<uint32_t> didx, jv, refsrc, dcount, dorder, sval2, rmask, outsrc, cbins;
   DevBuf<Job> jobs;
   DevBuf<uint16_t> jlvl;
   DevBuf<uint64_t> fresh, fresh2, skey, skey2, merged;
@@ -73,7 +86,7 @@ struct Scratch {
     jlvl.release();
     merged.release();
     didx.release(); jv.release(); refsrc.release(); dcount.release(); dorder.release(); cbins.release();
-    sval.release(); sval2.release(); rmask.release(); outsrc.release(); jobs.release();
+    sval2.release(); rmask.release(); outsrc.release(); jobs.release();
     fresh.release(); fresh2.release(); skey.release(); skey2.release(); seg_b.release(); seg_e.release();
     recmax.release();
   }
@@ -90,7 +103,7 @@ struct ef_ctx {
   uint32_t wide_min = 512;  // jobs per candidate from which k_keys_wide takes it (EF_WIDE_MIN; 0: off)
   bool dirty_big = true;  // rows > kFastRows: k_dirty_big (warp window walk); EF_DIRTY_BIG=0: k_dirty
   uint32_t wide_lpc = 16;  // lanes per candidate in k_keys_wide: 32, 16, 8 or 4 (EF_WIDE_LPC)
-  bool fuse_merge = true;  // rows > kFastRows: k_digest_mg merges on the fly (EF_FUSE_MERGE=0: k_merge_big + k_digest_pm)
+  bool fuse_merge = false;  // rows > kFastRows: k_digest_mg merges on the fly (EF_FUSE_MERGE=1; measured slower: 52.9 vs 12.0 + 38.5 ms on DAG-20k)
   bool digest_pf = true;  // rows > kFastRows: k_digest_pm loads the next block's key words ahead (EF_DIGEST_PF)
   uint32_t quad_max = 20000;  // chunks below this many candidates hash with k_keys_quad (EF_QUAD_MAX)
   uint64_t chunk_mib = 0;  // per-chunk hashing scratch budget, MiB (0: half the free HBM, <= 96 GiB)
@@ -118,6 +131,20 @@ struct ef_ctx {
   uint64_t pool_used = 0;
   uint32_t sig_ht_mask = 0, dv_ht_mask = 0;
   std::string input_text;
+  // incremental commit (ef_tables_commit uploads what changed since the last commit): the
+  // device tables mirror ids < c_ns / c_nw / c_names; older ids changed since are listed
+  bool c_valid = false;
+  size_t c_ns = 0, c_nw = 0, c_names = 0;
+  std::vector<uint32_t> sig_touched;  // ids < c_ns whose text or cost rows changed
+  bool sig_key_changed = false;       // an old id's desc / exactness changed: rebuild its lookup
+  bool names_changed = false, input_changed = true, dv_changed = false;
+  std::vector<uint32_t> h_toff, h_tlen, h_roff, h_rn, h_info;  // per-id arrays as on the device
+  uint64_t text_used = 0, rows_used = 0, name_used = 0;
+  std::vector<unsigned long long> h_sig_ht_key, h_dv_ht_key;  // lookup tables as on the device
+  std::vector<uint32_t> h_sig_ht_val, h_dv_ht_val;
+  uint32_t sig_ht_n = 0;
+  DevBuf<HtUpd> d_upd_sig, d_upd_dv;
+  uint64_t commit_bytes = 0;  // host->device bytes of the last commit (tests: independent of table size)
 
   // records
   Geo geo{};
@@ -155,6 +182,16 @@ struct ef_ctx {
   Scratch sc[2];
   cudaStream_t st_up = nullptr;  // asynchronous uploads
   cudaStream_t st_wide = nullptr;  // k_keys_wide beside k_keys
+  // speculative pricing (rows > kFastRows): every complete candidate priced on st_price while
+  // the chunks hash, the survivors' prices committed after the dedup (EF_SPEC_PRICE: 0 off,
+  // 1 from the first digest on, 2 from the plans on)
+  int spec_price = 1;
+  const ef_price_params* spec_pp = nullptr;  // set by ef_expand for step_hash
+  bool spec_live = false;                    // this step's speculative pricing was launched
+  cudaStream_t st_price = nullptr;
+  cudaEvent_t ev_sp0 = nullptr, ev_sp1 = nullptr;
+  DevBuf<ef_cand_result> d_spec;
+  DevBuf<uint32_t> d_spec_list;
   cudaEvent_t ev_w0 = nullptr, ev_w1 = nullptr;
   cudaEvent_t ev_up = nullptr;    // end of the last asynchronous upload (upload stream)
   cudaEvent_t ev_main = nullptr;  // main-stream work an upload must not overtake
@@ -179,6 +216,7 @@ struct ef_ctx {
   uint32_t n_chunks = 0;
   float last_ms[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   uint64_t last_stats[5] = {0, 0, 0, 0, 0};
+  uint32_t* pad_counts = nullptr;  // the send counts of the last ef_route_owners_padded (device)
   bool alg_rows = false;  // the last step's alg8 rows hold row indices (price_d1), not algorithm ids
   uint64_t kcount = 0;  // kernels launched by the library (every launch site counts)
   uint64_t kcount_step0 = 0;  // kcount when the last step began
@@ -255,12 +293,16 @@ ef_ctx* ef_create(int device) {
     ctx->wide_lpc = v >= 32 ? 32u : v >= 16 ? 16u : v >= 8 ? 8u : 4u;
   }
   if (const char* e = getenv("EF_FUSE_MERGE")) ctx->fuse_merge = atoi(e) != 0;
+  if (const char* e = getenv("EF_SPEC_PRICE")) ctx->spec_price = atoi(e);
   if (const char* e = getenv("EF_DIGEST_PF")) ctx->digest_pf = atoi(e) != 0;
   if (const char* e = getenv("EF_QUAD_MAX")) ctx->quad_max = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_CHUNK_MIB")) ctx->chunk_mib = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
   cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
   cudaStreamCreateWithFlags(&ctx->st_up, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&ctx->st_wide, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&ctx->st_price, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&ctx->ev_sp0, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ctx->ev_sp1, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ctx->ev_w0, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ctx->ev_w1, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&ctx->st_copy, cudaStreamNonBlocking);
@@ -342,6 +384,11 @@ void ef_destroy(ef_ctx* ctx) {
   if (ctx->ev_main) cudaEventDestroy(ctx->ev_main);
   if (ctx->st_up) cudaStreamDestroy(ctx->st_up);
   if (ctx->st_wide) cudaStreamDestroy(ctx->st_wide);
+  if (ctx->st_price) cudaStreamDestroy(ctx->st_price);
+  if (ctx->ev_sp0) cudaEventDestroy(ctx->ev_sp0);
+  if (ctx->ev_sp1) cudaEventDestroy(ctx->ev_sp1);
+  ctx->d_spec.release();
+  ctx->d_spec_list.release();
   if (ctx->ev_w0) cudaEventDestroy(ctx->ev_w0);
   if (ctx->ev_w1) cudaEventDestroy(ctx->ev_w1);
   if (ctx->st_copy) cudaStreamDestroy(ctx->st_copy);
@@ -372,6 +419,11 @@ int ef_sig_put(ef_ctx* ctx, uint32_t id, const ef_sig_desc* desc, const char* te
     ctx->row_t.resize(id + 1);
     ctx->row_e.resize(id + 1);
   }
+  if (id < ctx->c_ns) {  // a committed id changes: its entries are re-sent, its lookup rebuilt if keyed
+    if (std::memcmp(&ctx->sig_desc[id], desc, sizeof(ef_sig_desc)) || ctx->sig_exact[id] != (exact ? 1 : 0))
+      ctx->sig_key_changed = true;
+    ctx->sig_touched.push_back(id);
+  }
   ctx->sig_desc[id] = *desc;
   ctx->sig_exact[id] = exact ? 1 : 0;
   ctx->sig_text[id].assign(text, text_len);
@@ -382,6 +434,10 @@ int ef_sig_put(ef_ctx* ctx, uint32_t id, const ef_sig_desc* desc, const char* te
 int ef_sig_costs(ef_ctx* ctx, uint32_t id, uint32_t n, const int32_t* alg, const double* time_ms, const double* energy) {
   EF_REQUIRE(id < ctx->sig_desc.size(), "ef_sig_costs: unknown signature id");
   EF_REQUIRE(n <= 255, "ef_sig_costs: too many algorithms");
+  if (ctx->row_alg[id].size() == n && std::equal(alg, alg + n, ctx->row_alg[id].begin()) &&
+      std::memcmp(ctx->row_t[id].data(), time_ms, n * 8) == 0 && std::memcmp(ctx->row_e[id].data(), energy, n * 8) == 0)
+    return EF_OK;  // the same rows (a search re-binding its cost source): nothing to send
+  if (id < ctx->c_ns) ctx->sig_touched.push_back(id);
   ctx->row_alg[id].assign(alg, alg + n);
   ctx->row_t[id].assign(time_ms, time_ms + n);
   ctx->row_e[id].assign(energy, energy + n);
@@ -391,6 +447,7 @@ int ef_sig_costs(ef_ctx* ctx, uint32_t id, uint32_t n, const int32_t* alg, const
 
 int ef_name_put(ef_ctx* ctx, uint32_t id, const char* name, uint32_t len) {
   if (id >= ctx->names.size()) ctx->names.resize(id + 1);
+  if (id < ctx->c_names) ctx->names_changed = true;
   ctx->names[id].assign(name, len);
   ctx->dirty = true;
   return EF_OK;
@@ -408,6 +465,7 @@ int ef_wset_put(ef_ctx* ctx, uint32_t id, int32_t kind, int32_t oc, const double
                 uint64_t b_n, const char* hdr_w, uint32_t hlen_w, const char* hdr_b, uint32_t hlen_b) {
   EF_REQUIRE(id != kEmptyWset || (w_n == 0 && b_n == 0), "weight set 0 is reserved for 'no weights'");
   if (id >= ctx->ws.size()) ctx->ws.resize(id + 1);
+  if (id < ctx->c_nw) ctx->dv_changed = true;
   WeightSet& S = ctx->ws[id];
   S = WeightSet();
   S.kind = kind;
@@ -468,6 +526,7 @@ int ef_wset_derive(ef_ctx* ctx, uint32_t id, int32_t op, uint32_t a, uint32_t b,
   rc = pool_alloc(ctx, S.b_n, &S.b_off);
   if (rc) return rc;
   if (id >= ctx->ws.size()) ctx->ws.resize(id + 1);
+  if (id < ctx->c_nw) ctx->dv_changed = true;
   ctx->ws[id] = S;
   ctx->dirty = true;
   return EF_OK;
@@ -509,113 +568,224 @@ static uint32_t pow2_at_least(uint64_t n) {
   return m;
 }
 
-int ef_tables_commit(ef_ctx* ctx) {
-  cudaSetDevice(ctx->dev);
+// hi - lo host elements (src) to [lo, hi) of a device array that keeps its contents as it grows
+// to `total` elements
+template <typename T>
+static int upload_range(ef_ctx* ctx, DevBuf<T>& buf, const T* src, size_t lo, size_t hi, size_t total) {
+  EF_CUDA(buf.reserve(std::max<size_t>(total, 1), ctx->st, true));
+  if (hi > lo) {
+    EF_CUDA(cudaMemcpyAsync(buf.p + lo, src, (hi - lo) * sizeof(T), cudaMemcpyHostToDevice, ctx->st));
+    ctx->commit_bytes += (hi - lo) * sizeof(T);
+  }
+  return EF_OK;
+}
+
+// the sweep's exact skips of price_d1 (no row below row 0 in time / in energy) + row count
+static uint32_t sig_info_word(const ef_ctx* ctx, size_t i) {
+  const uint32_t rn = (uint32_t)ctx->row_alg[i].size();
+  uint32_t y = rn | (ctx->sig_desc[i].kind == EF_K_INPUT ? kInfoInput : 0u);
+  if (rn) {
+    bool tmin = true, emin = true;
+    for (uint32_t q = 1; q < rn; ++q) {
+      tmin = tmin && ctx->row_t[i][q] >= ctx->row_t[i][0];
+      emin = emin && ctx->row_e[i][q] >= ctx->row_e[i][0];
+    }
+    y |= (tmin ? kInfoTMin : 0u) | (emin ? kInfoEMin : 0u);
+  }
+  return y;
+}
+
+// insert id i into a host lookup table; the exact-signature table keeps the first of equal descs
+static bool ht_insert(std::vector<unsigned long long>& keys, std::vector<uint32_t>& vals, uint64_t k, uint32_t i,
+                      const ef_ctx* ctx, bool sig, std::vector<HtUpd>* upd) {
+  const uint32_t mask = (uint32_t)keys.size() - 1;
+  uint32_t s = (uint32_t)k & mask;
+  while (keys[s]) {
+    if (sig && keys[s] == k && desc_eq(ctx->sig_desc[vals[s]], ctx->sig_desc[i])) return false;
+    s = (s + 1) & mask;
+  }
+  keys[s] = k;
+  vals[s] = i;
+  if (upd) upd->push_back(HtUpd{s, i, k});
+  return true;
+}
+
+static int ht_scatter(ef_ctx* ctx, DevBuf<HtUpd>& ub, const std::vector<HtUpd>& upd, unsigned long long* keys,
+                      uint32_t* vals) {
+  if (upd.empty()) return EF_OK;
+  int rc = upload(ctx, ub, upd);
+  if (rc) return rc;
+  ctx->commit_bytes += upd.size() * sizeof(HtUpd);
+  const uint32_t n = (uint32_t)upd.size();
+  ++ctx->kcount, k_ht_scatter<<<std::min<uint32_t>((n + 255) / 256, 64), 256, 0, ctx->st>>>(keys, vals, ub.p, n);
+  EF_CUDA(cudaGetLastError());
+  return EF_OK;
+}
+
+// signatures: texts, cost rows, per-id arrays and the exact-signature lookup.  Ids committed
+// before and unchanged are not sent again; changed ones get fresh text / row space at the end
+// (the old space is left unused) and their per-id entries re-sent.
+static int commit_sigs(ef_ctx* ctx) {
   const size_t ns = ctx->sig_desc.size();
-  // signature texts, 8-byte aligned and zero padded (the hash kernel reads them as words)
-  std::vector<uint32_t> toff(ns), tlen(ns), roff(ns), rn(ns);
+  const bool full = !ctx->c_valid;
+  std::vector<uint32_t> ids;
+  if (full) {
+    ctx->text_used = ctx->rows_used = 0;
+    for (size_t i = 0; i < ns; ++i) ids.push_back((uint32_t)i);
+  } else {
+    std::sort(ctx->sig_touched.begin(), ctx->sig_touched.end());
+    ctx->sig_touched.erase(std::unique(ctx->sig_touched.begin(), ctx->sig_touched.end()), ctx->sig_touched.end());
+    ids = ctx->sig_touched;
+    for (size_t i = ctx->c_ns; i < ns; ++i) ids.push_back((uint32_t)i);
+  }
+  ctx->h_toff.resize(ns);
+  ctx->h_tlen.resize(ns);
+  ctx->h_roff.resize(ns);
+  ctx->h_rn.resize(ns);
+  ctx->h_info.resize(2 * std::max<size_t>(ns, 1), 0);
+  // texts 8-byte aligned and zero padded (the hash kernel reads them as words), +8 zero bytes
   std::vector<uint8_t> text;
   std::vector<int32_t> ralg;
   std::vector<double> rt, re;
-  for (size_t i = 0; i < ns; ++i) {
-    toff[i] = (uint32_t)text.size();
-    tlen[i] = (uint32_t)ctx->sig_text[i].size();
+  for (uint32_t i : ids) {
+    ctx->h_toff[i] = (uint32_t)(ctx->text_used + text.size());
+    ctx->h_tlen[i] = (uint32_t)ctx->sig_text[i].size();
     text.insert(text.end(), ctx->sig_text[i].begin(), ctx->sig_text[i].end());
     while (text.size() % 8) text.push_back(0);
-    roff[i] = (uint32_t)ralg.size();
-    rn[i] = (uint32_t)ctx->row_alg[i].size();
+    ctx->h_roff[i] = (uint32_t)(ctx->rows_used + ralg.size());
+    ctx->h_rn[i] = (uint32_t)ctx->row_alg[i].size();
     ralg.insert(ralg.end(), ctx->row_alg[i].begin(), ctx->row_alg[i].end());
     rt.insert(rt.end(), ctx->row_t[i].begin(), ctx->row_t[i].end());
     re.insert(re.end(), ctx->row_e[i].begin(), ctx->row_e[i].end());
+    ctx->h_info[2 * i] = ctx->h_roff[i];
+    ctx->h_info[2 * i + 1] = sig_info_word(ctx, i);
   }
   text.resize(text.size() + 8, 0);
   int rc;
-  if ((rc = upload(ctx, ctx->d_sig_desc, ctx->sig_desc)) || (rc = upload(ctx, ctx->d_text_off, toff)) ||
-      (rc = upload(ctx, ctx->d_text_len, tlen)) || (rc = upload(ctx, ctx->d_text, text)) ||
-      (rc = upload(ctx, ctx->d_row_off, roff)) || (rc = upload(ctx, ctx->d_row_n, rn)) ||
-      (rc = upload(ctx, ctx->d_row_alg, ralg)) || (rc = upload(ctx, ctx->d_row_t, rt)) ||
-      (rc = upload(ctx, ctx->d_row_e, re)))
+  const uint64_t t0 = ctx->text_used, r0 = ctx->rows_used;
+  if ((rc = upload_range(ctx, ctx->d_text, text.data(), t0, t0 + text.size(), t0 + text.size())) ||
+      (rc = upload_range(ctx, ctx->d_row_alg, ralg.data(), r0, r0 + ralg.size(), r0 + ralg.size())) ||
+      (rc = upload_range(ctx, ctx->d_row_t, rt.data(), r0, r0 + rt.size(), r0 + rt.size())) ||
+      (rc = upload_range(ctx, ctx->d_row_e, re.data(), r0, r0 + re.size(), r0 + re.size())))
     return rc;
-  {
-    std::vector<uint32_t> info(2 * std::max<size_t>(ns, 1), 0);
-    for (size_t i = 0; i < ns; ++i) {
-      info[2 * i] = roff[i];
-      uint32_t y = rn[i] | (ctx->sig_desc[i].kind == EF_K_INPUT ? kInfoInput : 0u);
-      if (rn[i]) {  // the exact skips of price_d1: no row below row 0 in time / in energy
-        bool tmin = true, emin = true;
-        for (uint32_t q = 1; q < rn[i]; ++q) {
-          tmin = tmin && ctx->row_t[i][q] >= ctx->row_t[i][0];
-          emin = emin && ctx->row_e[i][q] >= ctx->row_e[i][0];
-        }
-        y |= (tmin ? kInfoTMin : 0u) | (emin ? kInfoEMin : 0u);
-      }
-      info[2 * i + 1] = y;
-    }
-    if ((rc = upload(ctx, ctx->d_sig_info, info))) return rc;
-  }
-  // exact-signature lookup table
-  {
-    uint32_t cap = pow2_at_least(2 * ns + 2);
-    std::vector<unsigned long long> keys(cap, 0);
-    std::vector<uint32_t> vals(cap, 0);
-    for (size_t i = 0; i < ns; ++i) {
-      if (!ctx->sig_exact[i]) continue;
-      uint64_t k = desc_key(ctx->sig_desc[i]);
-      uint32_t s = (uint32_t)k & (cap - 1);
-      bool dup = false;
-      while (keys[s]) {
-        if (keys[s] == k && desc_eq(ctx->sig_desc[vals[s]], ctx->sig_desc[i])) {
-          dup = true;
-          break;
-        }
-        s = (s + 1) & (cap - 1);
-      }
-      if (dup) continue;
-      keys[s] = k;
-      vals[s] = (uint32_t)i;
-    }
+  ctx->text_used += text.size() - 8;  // the padding is overwritten by the next commit's texts
+  ctx->rows_used += ralg.size();
+  // per-id arrays from the first changed id on
+  const size_t lo = ids.empty() ? ns : ids.front();
+  if ((rc = upload_range(ctx, ctx->d_sig_desc, ctx->sig_desc.data() + lo, lo, ns, ns)) ||
+      (rc = upload_range(ctx, ctx->d_text_off, ctx->h_toff.data() + lo, lo, ns, ns)) ||
+      (rc = upload_range(ctx, ctx->d_text_len, ctx->h_tlen.data() + lo, lo, ns, ns)) ||
+      (rc = upload_range(ctx, ctx->d_row_off, ctx->h_roff.data() + lo, lo, ns, ns)) ||
+      (rc = upload_range(ctx, ctx->d_row_n, ctx->h_rn.data() + lo, lo, ns, ns)) ||
+      (rc = upload_range(ctx, ctx->d_sig_info, ctx->h_info.data() + 2 * lo, 2 * lo, 2 * ns, 2 * std::max<size_t>(ns, 1))))
+    return rc;
+  // exact-signature lookup: new exact ids into the table, or a rebuild (first commit, a keyed
+  // id changed, or the load would pass 1/2: rebuilt at load <= 1/4, so rebuilds are amortised)
+  size_t n_exact_new = 0;
+  for (size_t i = full ? 0 : ctx->c_ns; i < ns; ++i) n_exact_new += ctx->sig_exact[i] ? 1 : 0;
+  const bool rebuild = full || ctx->sig_key_changed || 2ull * (ctx->sig_ht_n + n_exact_new) + 2 > ctx->h_sig_ht_key.size();
+  if (rebuild) {
+    const uint32_t cap = pow2_at_least(4 * ns + 2);
+    ctx->h_sig_ht_key.assign(cap, 0);
+    ctx->h_sig_ht_val.assign(cap, 0);
+    ctx->sig_ht_n = 0;
+    for (size_t i = 0; i < ns; ++i)
+      if (ctx->sig_exact[i])
+        ctx->sig_ht_n += ht_insert(ctx->h_sig_ht_key, ctx->h_sig_ht_val, desc_key(ctx->sig_desc[i]), (uint32_t)i, ctx, true, nullptr);
     ctx->sig_ht_mask = cap - 1;
-    if ((rc = upload(ctx, ctx->d_sig_ht_key, keys)) || (rc = upload(ctx, ctx->d_sig_ht_val, vals))) return rc;
-  }
-  // names
-  {
-    std::vector<uint32_t> off(ctx->names.size()), len(ctx->names.size());
-    std::vector<uint8_t> pool;
-    for (size_t i = 0; i < ctx->names.size(); ++i) {
-      off[i] = (uint32_t)pool.size();
-      len[i] = (uint32_t)ctx->names[i].size();
-      pool.insert(pool.end(), ctx->names[i].begin(), ctx->names[i].end());
-    }
-    pool.push_back(0);
-    if ((rc = upload(ctx, ctx->d_name_off, off)) || (rc = upload(ctx, ctx->d_name_len, len)) ||
-        (rc = upload(ctx, ctx->d_names, pool)))
+    ctx->commit_bytes += (uint64_t)cap * 12;
+    if ((rc = upload(ctx, ctx->d_sig_ht_key, ctx->h_sig_ht_key)) || (rc = upload(ctx, ctx->d_sig_ht_val, ctx->h_sig_ht_val)))
       return rc;
+  } else {
+    std::vector<HtUpd> upd;
+    for (size_t i = ctx->c_ns; i < ns; ++i)
+      if (ctx->sig_exact[i])
+        ctx->sig_ht_n += ht_insert(ctx->h_sig_ht_key, ctx->h_sig_ht_val, desc_key(ctx->sig_desc[i]), (uint32_t)i, ctx, true, &upd);
+    if ((rc = ht_scatter(ctx, ctx->d_upd_sig, upd, ctx->d_sig_ht_key.p, ctx->d_sig_ht_val.p))) return rc;
+  }
+  ctx->sig_touched.clear();
+  ctx->sig_key_changed = false;
+  ctx->c_ns = ns;
+  return EF_OK;
+}
+
+// node names (appended) and the graph-input text (sent when the geometry set it)
+static int commit_names(ef_ctx* ctx) {
+  const size_t nn = ctx->names.size();
+  const bool full = !ctx->c_valid || ctx->names_changed;
+  const size_t lo = full ? 0 : ctx->c_names;
+  if (full) ctx->name_used = 0;
+  std::vector<uint32_t> off(nn), len(nn);
+  std::vector<uint8_t> pool;
+  for (size_t i = lo; i < nn; ++i) {
+    off[i] = (uint32_t)(ctx->name_used + pool.size());
+    len[i] = (uint32_t)ctx->names[i].size();
+    pool.insert(pool.end(), ctx->names[i].begin(), ctx->names[i].end());
+  }
+  pool.push_back(0);
+  const uint64_t p0 = ctx->name_used;
+  int rc;
+  if ((rc = upload_range(ctx, ctx->d_name_off, off.data() + lo, lo, nn, nn)) ||
+      (rc = upload_range(ctx, ctx->d_name_len, len.data() + lo, lo, nn, nn)) ||
+      (rc = upload_range(ctx, ctx->d_names, pool.data(), p0, p0 + pool.size(), p0 + pool.size())))
+    return rc;
+  ctx->name_used += pool.size() - 1;
+  ctx->names_changed = false;
+  ctx->c_names = nn;
+  if (ctx->input_changed || !ctx->c_valid) {
     std::vector<uint8_t> it(ctx->input_text.begin(), ctx->input_text.end());
     it.resize(((it.size() + 7) & ~size_t(7)) + 8, 0);  // 8-byte words, zero padded (k_digest)
     if ((rc = upload(ctx, ctx->d_input_text, it))) return rc;
+    ctx->commit_bytes += it.size();
+    ctx->input_changed = false;
   }
-  // derivation table
+  return EF_OK;
+}
+
+// derivation tuples and their lookup (weight sets are only appended during a search)
+static int commit_derives(ef_ctx* ctx) {
   const size_t nw = ctx->ws.size();
-  {
-    std::vector<int32_t> tup(4 * nw, 0);
-    uint32_t cap = pow2_at_least(2 * nw + 2);
-    std::vector<unsigned long long> keys(cap, 0);
-    std::vector<uint32_t> vals(cap, 0);
-    for (size_t i = 0; i < nw; ++i) {
-      for (int k = 0; k < 4; ++k) tup[4 * i + k] = ctx->ws[i].dv[k];
-      if (ctx->ws[i].dv[0] == 0) continue;
-      const int32_t* d = ctx->ws[i].dv;
-      uint64_t k = derive_key(d[0], (uint32_t)d[1], (uint32_t)d[2], d[3]);
-      uint32_t s = (uint32_t)k & (cap - 1);
-      while (keys[s]) s = (s + 1) & (cap - 1);
-      keys[s] = k;
-      vals[s] = (uint32_t)i;
-    }
+  const bool full = !ctx->c_valid || ctx->dv_changed;
+  const size_t lo = full ? 0 : ctx->c_nw;
+  std::vector<int32_t> tup(4 * nw, 0);
+  for (size_t i = lo; i < nw; ++i)
+    for (int k = 0; k < 4; ++k) tup[4 * i + k] = ctx->ws[i].dv[k];
+  int rc;
+  if ((rc = upload_range(ctx, ctx->d_dv_tuple, tup.data() + 4 * lo, 4 * lo, 4 * nw, 4 * nw))) return rc;
+  auto key_of = [&](size_t i) {
+    const int32_t* d = ctx->ws[i].dv;
+    return (uint64_t)derive_key(d[0], (uint32_t)d[1], (uint32_t)d[2], d[3]);
+  };
+  size_t n_dv = 0;
+  for (size_t i = 0; i < nw; ++i) n_dv += ctx->ws[i].dv[0] != 0;
+  if (full || 2ull * n_dv + 2 > ctx->h_dv_ht_key.size()) {
+    const uint32_t cap = pow2_at_least(4 * nw + 2);
+    ctx->h_dv_ht_key.assign(cap, 0);
+    ctx->h_dv_ht_val.assign(cap, 0);
+    for (size_t i = 0; i < nw; ++i)
+      if (ctx->ws[i].dv[0] != 0) ht_insert(ctx->h_dv_ht_key, ctx->h_dv_ht_val, key_of(i), (uint32_t)i, ctx, false, nullptr);
     ctx->dv_ht_mask = cap - 1;
-    if ((rc = upload(ctx, ctx->d_dv_tuple, tup)) || (rc = upload(ctx, ctx->d_dv_ht_key, keys)) ||
-        (rc = upload(ctx, ctx->d_dv_ht_val, vals)))
+    ctx->commit_bytes += (uint64_t)cap * 12;
+    if ((rc = upload(ctx, ctx->d_dv_ht_key, ctx->h_dv_ht_key)) || (rc = upload(ctx, ctx->d_dv_ht_val, ctx->h_dv_ht_val)))
       return rc;
+  } else {
+    std::vector<HtUpd> upd;
+    for (size_t i = lo; i < nw; ++i)
+      if (ctx->ws[i].dv[0] != 0) ht_insert(ctx->h_dv_ht_key, ctx->h_dv_ht_val, key_of(i), (uint32_t)i, ctx, false, &upd);
+    if ((rc = ht_scatter(ctx, ctx->d_upd_dv, upd, ctx->d_dv_ht_key.p, ctx->d_dv_ht_val.p))) return rc;
   }
+  ctx->dv_changed = false;
+  ctx->c_nw = nw;
+  return EF_OK;
+}
+
+int ef_tables_commit(ef_ctx* ctx) {
+  cudaSetDevice(ctx->dev);
+  ctx->commit_bytes = 0;
+  int rc;
+  if ((rc = commit_sigs(ctx)) || (rc = commit_names(ctx)) || (rc = commit_derives(ctx))) return rc;
+  ctx->c_valid = true;
+  const size_t nw = ctx->ws.size();
   // derived tensors, in id order (a derivation may use an earlier derived set)
   EF_CUDA(ctx->d_ws_digest.reserve(2 * nw + 2, ctx->st, true));
   std::vector<uint32_t> pending;
@@ -708,7 +878,10 @@ int ef_tables_commit(ef_ctx* ctx) {
     for (size_t t = 1; t < nt; ++t) pool.emplace_back(worker);
     worker();
     for (auto& t : pool) t.join();
-    EF_CUDA(cudaMemcpyAsync(ctx->d_ws_digest.p, ctx->h_ws_digest.data(), 2 * nw * 8, cudaMemcpyHostToDevice, ctx->st));
+    const size_t d0 = 2ull * pending.front();  // the sets digested now (ids ascending)
+    EF_CUDA(cudaMemcpyAsync(ctx->d_ws_digest.p + d0, ctx->h_ws_digest.data() + d0, (2 * nw - d0) * 8,
+                            cudaMemcpyHostToDevice, ctx->st));
+    ctx->commit_bytes += (2 * nw - d0) * 8;
     for (uint32_t i : pending) {
       WeightSet& S = ctx->ws[i];
       std::vector<uint64_t>().swap(S.hw);
@@ -768,6 +941,7 @@ int ef_set_geometry(ef_ctx* ctx, uint32_t cap_nodes, uint32_t cap_refs, uint32_t
   g.bytes = o;
   ctx->slots_per_chunk = std::max<uint32_t>(1, (uint32_t)((64ull << 20) / g.bytes));
   ctx->input_text.assign(input_text ? input_text : "", input_text ? input_text_len : 0);
+  ctx->input_changed = true;
   ctx->have_geo = true;
   ctx->dirty = true;
   if (out) {
@@ -883,7 +1057,8 @@ static int launch_keys(ef_ctx* ctx, cudaStream_t st, const VArgs& V) {
   if (wide) EF_CUDA(cudaStreamWaitEvent(st, ctx->ev_w1, 0));
   return EF_OK;
 }
-static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk);
+static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk,
+                        bool lean = false);
 // chunk candidates by job count, largest first (counting sort: k_count_*)
 static int order_by_count(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t n, uint32_t S) {
   if (!n) return EF_OK;
@@ -895,7 +1070,7 @@ static int order_by_count(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t n,
   EF_CUDA(cudaGetLastError());
   return EF_OK;
 }
-static VArgs chunk_args(ef_ctx* ctx, Scratch& sc, uint32_t S, uint32_t Rs);
+static VArgs chunk_args(ef_ctx* ctx, Scratch& sc, uint32_t S, uint32_t Rs, bool lean = false);
 static int hash_records_full(ef_ctx* ctx, Scratch& sc, cudaStream_t st, const unsigned long long* d_rec, uint32_t n,
                              uint64_t* d_hash_out, uint32_t max_n = 0, uint32_t max_refs = 0) {
   if (!n) return EF_OK;
@@ -1135,20 +1310,30 @@ static int ensure_step_cand(ef_ctx* ctx, uint32_t total, uint32_t S) {
 // per-chunk hashing scratch for rows of S node slots and Rs ref slots: bounded (half the free
 // HBM, at most 96 GiB) so graphs of any size stream through; a chunk that holds the whole step
 // keeps every candidate in flight (large graphs have few parents: chunking starves the GPU)
-static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk) {
-  const bool big = S > kFastRows && ctx->big_merge;  // + the merged key stream
-  const uint64_t per = (uint64_t)S * (4 + 4 + sizeof(Job) + 16 + 16 + 8 + 8 + 4 + 4 + 2 + (big ? 16 : 0)) + 4ull * Rs +
-                       4ull * (S + 31) / 32 + 32;
+// lean (step rows beyond kFastRows with k_dirty_big and the merged stream): no didx / sort
+// value rows, and the merged key stream reuses the jobs row (dead after the node keys), so a
+// chunk holds 1.4x the candidates (DAG-20k: 98 -> 70 bytes per candidate slot)
+static bool lean_rows(ef_ctx* ctx, uint32_t S) { return S > kFastRows && ctx->big_merge && ctx->dirty_big; }
+
+static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t items, uint32_t S, uint32_t Rs, uint32_t* chunk,
+                        bool lean) {
+  const bool big = S > kFastRows && ctx->big_merge && !lean;  // + the merged key stream
+  const uint64_t per = (uint64_t)S * (4 + sizeof(Job) + 16 + 16 + 8 + 8 + (S > kFastRows ? 2 : 0) +
+                                      (lean ? 0 : 4 + 4 + 4) + (big ? 16 : 0)) +
+                       4ull * Rs + 4ull * (S + 31) / 32 + 32;
   if (!ctx->chunk_mib) {  // a share of the HBM free when the first chunk is sized (EF_CHUNK_MIB overrides)
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
-    ctx->chunk_mib = std::min<uint64_t>(96ull << 10, std::max<uint64_t>(1024, (uint64_t)(0.5 * (double)fr) >> 20));
+    ctx->chunk_mib = std::min<uint64_t>(128ull << 10, std::max<uint64_t>(1024, (uint64_t)(0.7 * (double)fr) >> 20));
   }
   uint64_t ch = std::max<uint64_t>(256, (ctx->chunk_mib << 20) / per);
   ch = std::min<uint64_t>(ch, std::max<uint32_t>(items, 1));
   ch = std::min<uint64_t>(ch, (uint64_t)INT32_MAX / S);
   *chunk = (uint32_t)ch;
-  EF_CUDA(sc.didx.reserve(ch * S, st));
+  if (!lean) {
+    EF_CUDA(sc.didx.reserve(ch * S, st));
+    EF_CUDA(sc.sval2.reserve(ch * S, st));
+  }
   if (S > kFastRows) EF_CUDA(sc.jlvl.reserve(ch * S, st));
   if (big) EF_CUDA(sc.merged.reserve(ch * S * 2, st));
   EF_CUDA(sc.jv.reserve(ch * S, st));
@@ -1159,8 +1344,6 @@ static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t item
   EF_CUDA(sc.rmask.reserve(ch * ((S + 31) / 32), st));
   EF_CUDA(sc.skey.reserve(ch * S, st));
   EF_CUDA(sc.skey2.reserve(ch * S, st));
-  EF_CUDA(sc.sval.reserve(ch * S, st));
-  EF_CUDA(sc.sval2.reserve(ch * S, st));
   EF_CUDA(sc.dcount.reserve(ch, st));
   EF_CUDA(sc.dorder.reserve(ch, st));
   EF_CUDA(sc.seg_b.reserve(ch, st));
@@ -1169,7 +1352,7 @@ static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t item
   return EF_OK;
 }
 
-static VArgs chunk_args(ef_ctx* ctx, Scratch& sc, uint32_t S, uint32_t Rs) {
+static VArgs chunk_args(ef_ctx* ctx, Scratch& sc, uint32_t S, uint32_t Rs, bool lean) {
   VArgs V{};
   V.g = ctx->geo;
   V.T = make_tables(ctx);
@@ -1177,16 +1360,15 @@ static VArgs chunk_args(ef_ctx* ctx, Scratch& sc, uint32_t S, uint32_t Rs) {
   V.res = ctx->d_res.p;
   V.S = S;
   V.Rs = Rs;
-  V.didx = sc.didx.p;
+  V.didx = lean ? nullptr : sc.didx.p;
   V.jobs = sc.jobs.p;
   V.refsrc = sc.refsrc.p;
   V.fresh = sc.fresh.p;
   V.dcount = sc.dcount.p;
   V.order = sc.dorder.p;
   V.skey = sc.skey.p;
-  V.sval = sc.sval.p;
   V.skey_sorted = sc.skey2.p;
-  V.sval_sorted = sc.sval2.p;
+  V.sval_sorted = lean ? nullptr : sc.sval2.p;  // full mode only
   V.seg_begin = sc.seg_b.p;
   V.seg_end = sc.seg_e.p;
   V.W = (S + 31) / 32;
@@ -1197,7 +1379,8 @@ static VArgs chunk_args(ef_ctx* ctx, Scratch& sc, uint32_t S, uint32_t Rs) {
   V.jv = sc.jv.p;
   V.jlvl = nullptr;
   V.wide_min = 0;
-  V.kstream = (S > kFastRows && ctx->big_merge) ? sc.merged.p : sc.fresh2.p;
+  V.kstream = lean ? reinterpret_cast<uint64_t*>(sc.jobs.p)  // the jobs rows are dead by the merge
+                   : (S > kFastRows && ctx->big_merge) ? sc.merged.p : sc.fresh2.p;
   return V;
 }
 
@@ -1213,10 +1396,10 @@ static int sort_fresh_keys(ef_ctx* ctx, Scratch& sc, cudaStream_t st, const VArg
     ++ctx->kcount, k_sortkeys<512, 8><<<grid, 256, 0, st>>>(V);
   } else if (V.S <= 1024) {
     ++ctx->kcount, k_sortkeys<1024, 4><<<std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 32)), 128, 0, st>>>(V);
-  } else {  // a CTA per candidate: shared-memory runs of up to 8192 keys, merged in global rows
+  } else {  // a CTA per candidate: shared-memory bucket sort up to 8192 keys, runs merged beyond
     uint32_t R = 1024;
     while (R < V.S && R < 8192u) R <<= 1;
-    const size_t smem = 8ull * R;
+    const size_t smem = 12ull * R;  // R sort words + R bucket counters
     EF_CUDA(cudaFuncSetAttribute(k_sortbig<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ++ctx->kcount, k_sortbig<512><<<std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * 4)), 512, smem, st>>>(V, R);
   }
@@ -1226,6 +1409,8 @@ static int sort_fresh_keys(ef_ctx* ctx, Scratch& sc, cudaStream_t st, const VArg
 
 
 // ---- step phases --------------------------------------------------------------------------
+
+static int launch_spec_price(ef_ctx* ctx, uint32_t total);
 
 // 1-3: match, plans, per chunk dirty walk / node keys / key sort / graph digest.  Leaves the
 // candidates' hashes in d_res; no synchronisation at the end.
@@ -1278,7 +1463,9 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
     const uint32_t S = (std::max<uint32_t>(ctx->h_scalars[5], 1) + 2 + 3) & ~3u;
     const uint32_t Rs = ctx->h_scalars[6] + 4;
     uint32_t chunk = 0;
-    if ((rc = ensure_step_cand(ctx, total, S)) || (rc = ensure_chunk(ctx, sc, ctx->st, total, S, Rs, &chunk))) return rc;
+    const bool lean = lean_rows(ctx, S);
+    if ((rc = ensure_step_cand(ctx, total, S)) || (rc = ensure_chunk(ctx, sc, ctx->st, total, S, Rs, &chunk, lean)))
+      return rc;
     ctx->step_S = S;
     ctx->step_Rs = Rs;
     ctx->step_n_parents = n_parents;
@@ -1301,8 +1488,10 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       ++ctx->kcount, k_plan<<<grid_t, 256, 0, ctx->st>>>(A, ctx->d_plan.p);
       EF_CUDA(cudaGetLastError());
     }
+    ctx->spec_live = false;
+    if (ctx->spec_pp && ctx->spec_price == 2 && (rc = launch_spec_price(ctx, total))) return rc;
     cudaEventRecord(ctx->ev[2], ctx->st);
-    VArgs V = chunk_args(ctx, sc, S, Rs);
+    VArgs V = chunk_args(ctx, sc, S, Rs, lean);
     V.parent_addr = A.parent_addr;
     V.stats = ctx->d_stats.p;
     V.pscratch = A.pscratch;
@@ -1364,6 +1553,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
         ++ctx->kcount, k_digest_pm<kHashThreads, false, EF_DIGEST_MINB><<<gd, kHashThreads, 0, ctx->st>>>(V);
       } else {
         if ((rc = sort_fresh_keys(ctx, sc, ctx->st, V))) return rc;
+        if (ctx->spec_pp && (rc = launch_spec_price(ctx, total))) return rc;  // under the digest
         if (ctx->big_merge && ctx->fuse_merge) {  // the digest merges the two sorted streams itself
           cudaEventRecord(ce[3], ctx->st);
           ++ctx->kcount, k_digest_mg<kHashThreads, 2><<<gd, kHashThreads, 0, ctx->st>>>(V);
@@ -1429,9 +1619,10 @@ static int step_dedup_local(ef_ctx* ctx, const ef_price_params* pp) {
   return EF_OK;
 }
 
-// 5) inner search on every survivor (the compacted list of step 4)
-static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
-  const uint32_t total = ctx->last_total;
+// the inner search kernel over a candidate list (pl, *pn) on stream st; results into out (null:
+// the step's results)
+static int launch_price(ef_ctx* ctx, const ef_price_params* pp, uint32_t total, cudaStream_t st, const uint32_t* pl,
+                        const uint32_t* pn, ef_cand_result* out) {
   VPriceArgs Pv{};
   Pv.pa.g = ctx->geo;
   Pv.pa.T = make_tables(ctx);
@@ -1445,15 +1636,14 @@ static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
   Pv.pstride = pstride_of(ctx->geo);
   Pv.alg8 = ctx->d_alg8.p;
   Pv.S = ctx->step_S;
+  Pv.out = out;
   const uint32_t gp = std::max<uint32_t>(1, std::min<uint32_t>((total + kPriceThreads - 1) / kPriceThreads, ctx->n_sm * (1024 / kPriceThreads)));
-  const uint32_t* pl = ctx->d_plist.p;
-  const uint32_t* pn = ctx->d_scalars.p + 7;
   const bool fast = pp->use_inner && pp->d == 1;
   const bool sm = ctx->step_S <= kFastRows;  // the sweep's algorithm row in shared memory
   Pv.algt = nullptr;
   if (!sm && ctx->step_S <= 2048) {  // the interleaved sweep rows of k_price_v, one per thread of
                                      // the grid (beyond 2k-slot rows the scratch outgrows L2: slower)
-    EF_CUDA(ctx->d_algt.reserve((uint64_t)gp * kPriceThreads * ctx->step_S, ctx->st));
+    EF_CUDA(ctx->d_algt.reserve((uint64_t)gp * kPriceThreads * ctx->step_S, st));
     Pv.algt = ctx->d_algt.p;
   }
   const size_t smem = sm ? (size_t)ctx->step_S * kPriceThreads : 0;
@@ -1461,21 +1651,59 @@ static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
   do {                                                                                                     \
     if (sm) {                                                                                              \
       EF_CUDA(cudaFuncSetAttribute(k_price_v<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-      ++ctx->kcount, k_price_v<K, true><<<gp, kPriceThreads, smem, ctx->st>>>(Pv, pl, pn);                             \
+      ++ctx->kcount, k_price_v<K, true><<<gp, kPriceThreads, smem, st>>>(Pv, pl, pn);                             \
     } else {                                                                                               \
-      ++ctx->kcount, k_price_v<K, false><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);                                \
+      ++ctx->kcount, k_price_v<K, false><<<gp, kPriceThreads, 0, st>>>(Pv, pl, pn);                                \
     }                                                                                                      \
   } while (0)
   ctx->alg_rows = fast;  // price_d1 leaves row indices (k_keep_alg reads the ids)
   if (fast && !sm && !Pv.algt)  // the global rows start at row 0 (price_d1 writes changes only)
-    EF_CUDA(cudaMemsetAsync(ctx->d_alg8.p, 0, (uint64_t)std::max<uint32_t>(total, 1) * ctx->step_S, ctx->st));
+    EF_CUDA(cudaMemsetAsync(ctx->d_alg8.p, 0, (uint64_t)std::max<uint32_t>(total, 1) * ctx->step_S, st));
   if (fast && pp->kind == EF_C_ENERGY) EF_PRICE(EF_C_ENERGY);
   else if (fast && pp->kind == EF_C_TIME) EF_PRICE(EF_C_TIME);
   else if (fast && pp->kind == EF_C_LINEAR) EF_PRICE(EF_C_LINEAR);
   else if (fast) EF_PRICE(EF_C_MIX + 1);
-  else ++ctx->kcount, k_price_v<-1, false><<<gp, kPriceThreads, 0, ctx->st>>>(Pv, pl, pn);
+  else ++ctx->kcount, k_price_v<-1, false><<<gp, kPriceThreads, 0, st>>>(Pv, pl, pn);
 #undef EF_PRICE
   EF_CUDA(cudaGetLastError());
+  return EF_OK;
+}
+
+// speculative pricing of every complete candidate on st_price, from where the main stream has
+// got to (step_hash calls it once per step, when ctx->spec_pp is set)
+static int launch_spec_price(ef_ctx* ctx, uint32_t total) {
+  if (!ctx->spec_pp || ctx->spec_live || !total) return EF_OK;
+  EF_CUDA(ctx->d_spec.reserve(total, ctx->st));
+  EF_CUDA(ctx->d_spec_list.reserve(total + 1, ctx->st));
+  EF_CUDA(cudaEventRecord(ctx->ev_sp0, ctx->st));
+  EF_CUDA(cudaStreamWaitEvent(ctx->st_price, ctx->ev_sp0, 0));
+  uint32_t* list_n = ctx->d_spec_list.p + total;
+  EF_CUDA(cudaMemsetAsync(list_n, 0, 4, ctx->st_price));
+  const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));
+  ++ctx->kcount, k_spec_list<<<grid_t, 256, 0, ctx->st_price>>>(ctx->d_res.p, total, ctx->spec_pp->node_cap,
+                                                                  ctx->d_spec_list.p, list_n, ctx->d_spec.p);
+  EF_CUDA(cudaGetLastError());
+  int rc = launch_price(ctx, ctx->spec_pp, total, ctx->st_price, ctx->d_spec_list.p, list_n, ctx->d_spec.p);
+  if (rc) return rc;
+  EF_CUDA(cudaEventRecord(ctx->ev_sp1, ctx->st_price));
+  ctx->spec_live = true;
+  return EF_OK;
+}
+
+// 5) inner search on every survivor (the compacted list of step 4), or, when the step priced
+// speculatively, the survivors' prices taken from the speculative results
+static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
+  const uint32_t total = ctx->last_total;
+  if (ctx->spec_live) {
+    ctx->spec_live = false;
+    EF_CUDA(cudaStreamWaitEvent(ctx->st, ctx->ev_sp1, 0));
+    const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));
+    ++ctx->kcount, k_spec_commit<<<grid_t, 256, 0, ctx->st>>>(ctx->d_res.p, ctx->d_spec.p, total, pp->per_parent);
+    EF_CUDA(cudaGetLastError());
+  } else {
+    int rc = launch_price(ctx, pp, total, ctx->st, ctx->d_plist.p, ctx->d_scalars.p + 7, nullptr);
+    if (rc) return rc;
+  }
   cudaEventRecord(ctx->ev[5], ctx->st);
   return EF_OK;
 }
@@ -1563,7 +1791,12 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
   int rc = step_begin(ctx, n_candidates, n_rules);
   if (rc) return rc;
   uint32_t total = 0;
-  if ((rc = step_hash(ctx, parent_slots, n_parents, rules, n_rules, &total))) return rc;
+  // large graphs: price every candidate on a second stream while the chunks hash (their
+  // pricing does not depend on the hashes, only which of them survive the dedup does)
+  ctx->spec_pp = ctx->spec_price && pp && pp->use_inner ? pp : nullptr;
+  rc = step_hash(ctx, parent_slots, n_parents, rules, n_rules, &total);
+  ctx->spec_pp = nullptr;
+  if (rc) return rc;
   if ((rc = step_dedup_local(ctx, pp)) || (rc = step_price(ctx, pp)) || (rc = step_prune(ctx, pp))) return rc;
   rc = step_sync(ctx, true);
   *n_candidates = total;
@@ -1650,6 +1883,96 @@ int ef_expand_finish(ef_ctx* ctx, const uint32_t* d_verdict_back, const ef_price
   int rc = step_price(ctx, pp);
   if (rc || (rc = step_prune(ctx, pp))) return rc;
   return step_sync(ctx, true);
+}
+
+// ---- the padded exchange: no count goes through the host -------------------------------------
+
+int ef_route_owners_padded(ef_ctx* ctx, uint32_t world, uint64_t order_base, uint32_t cap, uint64_t* d_send,
+                           uint32_t* d_counts) {
+  EF_REQUIRE(world >= 1 && world <= 1024 && d_counts && d_send, "ef_route_owners_padded: bad arguments");
+  const uint32_t total = ctx->last_total;
+  EF_REQUIRE(cap >= total, "ef_route_owners_padded: cap below this rank's candidate count");
+  EF_CUDA(ctx->d_perm.reserve(std::max<uint64_t>((uint64_t)world * cap, 1), ctx->st));
+  EF_CUDA(cudaMemsetAsync(d_counts, 0, world * 4, ctx->st));
+  const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));
+  RouteArgs R{ctx->d_res.p, total, world, order_base, d_counts, nullptr, d_send, ctx->d_perm.p};
+  if (total) ++ctx->kcount, k_route_pad<<<grid_t, 256, 0, ctx->st>>>(R, cap);
+  EF_CUDA(cudaGetLastError());
+  ctx->pad_counts = d_counts;
+  return EF_OK;
+}
+
+int ef_owner_mark_padded(ef_ctx* ctx, const uint64_t* d_recv, const uint32_t* d_recv_counts, uint32_t world,
+                         uint32_t cap, uint32_t* d_verdict, int insert_visited) {
+  EF_REQUIRE(ctx->vis_mask, "visited set not initialised");
+  EF_REQUIRE(world >= 1 && world <= 1024 && d_recv && d_recv_counts && d_verdict, "ef_owner_mark_padded: bad arguments");
+  const uint64_t n = (uint64_t)world * cap;
+  if (!n) return EF_OK;
+  EF_REQUIRE(n < (1ull << 31), "ef_owner_mark_padded: world * cap above 2^31");
+  if (insert_visited) {
+    int rc = vis_reserve(ctx, n);  // an upper bound: no host round trip unless the table may fill
+    if (rc) return rc;
+  }
+  const uint32_t tcap = pow2_at_least(2ull * std::max<uint64_t>(n, 1024));
+  EF_CUDA(ctx->d_step_key.reserve(tcap, ctx->st));
+  EF_CUDA(ctx->d_step_ord.reserve(tcap, ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_step_key.p, 0, (size_t)tcap * 8, ctx->st));
+  EF_CUDA(cudaMemsetAsync(ctx->d_step_ord.p, 0xff, (size_t)tcap * 8, ctx->st));
+  OwnerArgs O{d_recv, (uint32_t)n, d_verdict, ctx->d_step_key.p, ctx->d_step_ord.p, tcap - 1, ctx->d_vis.p,
+              ctx->vis_mask, ctx->d_vis_count.p, ctx->d_vis_err.p};
+  const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, ctx->n_sm * 8ull));
+  ++ctx->kcount, k_owner_claim_pad<<<grid, 256, 0, ctx->st>>>(O, d_recv_counts, cap);
+  ++ctx->kcount, k_owner_resolve_pad<<<grid, 256, 0, ctx->st>>>(O, d_recv_counts, cap);
+  if (insert_visited) {
+    ++ctx->kcount, k_owner_insert_pad<<<grid, 256, 0, ctx->st>>>(O, d_recv_counts, cap);
+    ctx->vis_bound += n;  // stays an upper bound without reading the count back
+  }
+  EF_CUDA(cudaGetLastError());
+  return EF_OK;
+}
+
+int ef_expand_finish_padded(ef_ctx* ctx, const uint32_t* d_verdict_back, uint32_t world, uint32_t cap,
+                            const ef_price_params* pp) {
+  EF_REQUIRE(ctx->pad_counts, "ef_expand_finish_padded: no ef_route_owners_padded before it");
+  const uint32_t total = ctx->last_total;
+  EF_CUDA(cudaMemsetAsync(ctx->d_scalars.p + 7, 0, 4, ctx->st));
+  cudaEventRecord(ctx->ev[3], ctx->st);
+  if (total) {
+    const uint64_t n = (uint64_t)world * cap;
+    const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, ctx->n_sm * 8ull));
+    ++ctx->kcount, k_apply_verdicts_pad<<<grid, 256, 0, ctx->st>>>(ctx->d_res.p, ctx->d_perm.p, ctx->pad_counts,
+                                                                   d_verdict_back, world, cap, pp->node_cap);
+    const uint32_t gc = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));
+    ++ctx->kcount, k_compact_survivors<<<gc, 256, 0, ctx->st>>>(ctx->d_res.p, total, ctx->d_plist.p, ctx->d_scalars.p + 7);
+    EF_CUDA(cudaGetLastError());
+  }
+  ctx->pad_counts = nullptr;
+  cudaEventRecord(ctx->ev[4], ctx->st);
+  int rc = step_price(ctx, pp);
+  if (rc || (rc = step_prune(ctx, pp))) return rc;
+  return step_sync(ctx, true);
+}
+
+int ef_commit_bytes(ef_ctx* ctx, uint64_t* bytes) {
+  EF_REQUIRE(bytes, "ef_commit_bytes: null out");
+  *bytes = ctx->commit_bytes;
+  return EF_OK;
+}
+
+int ef_stream(ef_ctx* ctx, void** stream) {
+  EF_REQUIRE(stream, "ef_stream: null out");
+  *stream = (void*)ctx->st;
+  return EF_OK;
+}
+
+int ef_reprune(ef_ctx* ctx, double best, double alpha) {
+  ef_price_params pp{};
+  pp.best = best;
+  pp.alpha = alpha;
+  int rc = step_prune(ctx, &pp);
+  if (rc) return rc;
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  return EF_OK;
 }
 
 int ef_pending(ef_ctx* ctx, ef_sig_desc* sigs, uint32_t sig_cap, uint32_t* n_sigs, int32_t* derives, uint32_t derive_cap,
@@ -1757,9 +2080,11 @@ int ef_materialise(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents
     A.n_req_sig = ctx->d_scalars.p + 2;
     A.n_req_dv = ctx->d_scalars.p + 3;
     A.cand_cap = 0xffffffffu;
+    EF_CUDA(ctx->d_req_sig.reserve(ctx->req_cap, ctx->st));
+    EF_CUDA(ctx->d_req_dv.reserve(4 * ctx->req_cap, ctx->st));
     A.req_sig = ctx->d_req_sig.p;
     A.req_dv = ctx->d_req_dv.p;
-    A.req_sig_cap = A.req_dv_cap = ctx->d_req_sig.p ? ctx->req_cap : 0;
+    A.req_sig_cap = A.req_dv_cap = ctx->req_cap;
     ++ctx->kcount, k_match<kMatchThreads><<<std::min<uint32_t>(n_parents, ctx->n_sm * 8), kMatchThreads, 0, ctx->st>>>(A);
     ++ctx->kcount, k_offsets<1024><<<1, 1024, 0, ctx->st>>>(A);
     EF_CUDA(cudaGetLastError());
@@ -1783,13 +2108,19 @@ int ef_materialise(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents
     A.dst = ctx->d_dst.p;
     ++ctx->kcount, k_materialise<kMatThreads><<<std::min<uint32_t>(n, ctx->n_sm * 8), kMatThreads, 0, ctx->st>>>(A);
     EF_CUDA(cudaGetLastError());
-    EF_CUDA(ctx->d_hash_out.reserve(n, ctx->st));
-    if ((rc = hash_records_full(ctx, ctx->sc[0], ctx->st, ctx->d_dst.p, n, ctx->d_hash_out.p))) return rc;
     EF_CUDA(cudaMemcpyAsync(ctx->h_scalars, ctx->d_scalars.p, 16 * 4, cudaMemcpyDeviceToHost, ctx->st));
     EF_CUDA(cudaStreamSynchronize(ctx->st));
-    EF_REQUIRE(!(ctx->h_scalars[1] & 4u), "candidate exceeds record capacity (raise cap_nodes/cap_refs)");
-    EF_REQUIRE(!ctx->h_scalars[2] && !ctx->h_scalars[3], "ef_materialise: rewrite needs uninterned tables");
     ctx->last_total = 0;  // the step state now describes these parents: ef_keep is invalid
+    EF_REQUIRE(!(ctx->h_scalars[1] & 4u), "candidate exceeds record capacity (raise cap_nodes/cap_refs)");
+    // a rewrite whose signature / weight set this context has not interned yet (another rank's
+    // step resolved it): the records hold unresolved ids, so they are not hashed; the caller
+    // resolves (ef_pending) and calls again
+    ctx->last_req_sig = ctx->h_scalars[2];
+    ctx->last_req_dv = ctx->h_scalars[3];
+    if (ctx->last_req_sig || ctx->last_req_dv) return EF_NEED_RESOLVE;
+    EF_CUDA(ctx->d_hash_out.reserve(n, ctx->st));
+    if ((rc = hash_records_full(ctx, ctx->sc[0], ctx->st, ctx->d_dst.p, n, ctx->d_hash_out.p))) return rc;
+    EF_CUDA(cudaStreamSynchronize(ctx->st));
     return EF_OK;
   }
   ctx->err = "ef_materialise: site buffer did not converge";

@@ -240,7 +240,7 @@ __device__ __forceinline__ void b2b_compress_col_pf(uint64_t* h, const uint64_t*
   if (last) v14 = ~v14;
   uint64_t ma[16], mb[16];
   b2b_col_load<BT>(ma, col, 0);
-#define EF_B2B_ROUND(m)                          \
+#define EF_B2B_ROUND_COL(m)                          \
   EF_B2B_G(v0, v4, v8, v12, m[0], m[1]);         \
   EF_B2B_G(v1, v5, v9, v13, m[2], m[3]);         \
   EF_B2B_G(v2, v6, v10, v14, m[4], m[5]);        \
@@ -252,11 +252,11 @@ __device__ __forceinline__ void b2b_compress_col_pf(uint64_t* h, const uint64_t*
 #pragma unroll 1
   for (int r = 0; r < 12; r += 2) {
     b2b_col_load<BT>(mb, col, r + 1);
-    EF_B2B_ROUND(ma)
+    EF_B2B_ROUND_COL(ma)
     if (r + 2 < 12) b2b_col_load<BT>(ma, col, r + 2);
-    EF_B2B_ROUND(mb)
+    EF_B2B_ROUND_COL(mb)
   }
-#undef EF_B2B_ROUND
+#undef EF_B2B_ROUND_COL
   h[0] ^= v0 ^ v8;
   h[1] ^= v1 ^ v9;
   h[2] ^= v2 ^ v10;

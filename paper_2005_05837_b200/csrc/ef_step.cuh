@@ -86,7 +86,6 @@ struct VArgs {
   uint32_t wide_min;  // > 0: candidates with at least this many jobs go to k_keys_wide, not k_keys
   const uint32_t* order;  // [n] chunk-local candidate per lane (k_keys)
   uint64_t* skey;     // [n][S] sort keys (first key word, big endian)
-  uint32_t* sval;     // [n][S] job index
   const uint64_t* skey_sorted;
   uint32_t* sval_sorted;
   int32_t* seg_begin;  // [n]
@@ -932,7 +931,6 @@ __global__ void __launch_bounds__(BT, EF_KEYS_MINB) k_keys(VArgs A) {
     const uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
     uint64_t* fresh = A.fresh + 2ull * lc * A.S;
     uint64_t* skey = A.skey + (uint64_t)lc * A.S;
-    uint32_t* sval = A.sval + (uint64_t)lc * A.S;
     uint32_t ncomp = 0;
     uint64_t last0 = 0, last1 = 0;
     // the next job's descriptor and text metadata are fetched one job ahead (their dependent
@@ -1018,7 +1016,6 @@ __global__ void __launch_bounds__(BT, EF_KEYS_MINB) k_keys(VArgs A) {
       last0 = h[0];
       last1 = h[1];
       skey[jj] = B2b::bswap64(h[0]);
-      sval[jj] = jj;
     }
     if (A.stats) atomicAdd(A.stats, (unsigned long long)ncomp);
   }
@@ -1059,7 +1056,6 @@ __global__ void __launch_bounds__(BT) k_keys_wide(VArgs A) {
     const uint16_t* lv = A.jlvl + (uint64_t)lc * A.S;
     uint64_t* fresh = A.fresh + 2ull * lc * A.S;
     uint64_t* skey = A.skey + (uint64_t)lc * A.S;
-    uint32_t* sval = A.sval + (uint64_t)lc * A.S;
     uint32_t* ord = reinterpret_cast<uint32_t*>(skey);  // [S] jobs by level
     uint32_t* cnt = ord + A.S;                          // [S] per level: count -> start -> end
     if (has) {  // group-uniform: the counting sort of the candidate's jobs by level
@@ -1190,7 +1186,6 @@ __global__ void __launch_bounds__(BT) k_keys_wide(VArgs A) {
     if (has) {
       for (uint32_t j = sl; j < d; j += LPC) {  // the sort records (the level scratch is dead)
         skey[j] = B2b::bswap64(fresh[2 * j]);
-        sval[j] = j;
       }
     }
     ncomp = __reduce_add_sync(full, ncomp);
@@ -1369,7 +1364,6 @@ __global__ void __launch_bounds__(BT) k_keys_quad(VArgs A) {
     const uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
     uint64_t* fresh = A.fresh + 2ull * lc * A.S;
     uint64_t* skey = A.skey + (uint64_t)lc * A.S;
-    uint32_t* sval = A.sval + (uint64_t)lc * A.S;
     auto key_of = [&](uint32_t sv, uint64_t& k0, uint64_t& k1) {
       const uint32_t idx = sv & 0x7fffffu;
       const uint64_t* kp = (sv & kFresh) ? fresh + 2 * idx : pkeys + 2 * idx;
@@ -1504,8 +1498,7 @@ __global__ void __launch_bounds__(BT) k_keys_quad(VArgs A) {
         fresh[2 * jj] = k0;
         fresh[2 * jj + 1] = k1;
         skey[jj] = B2b::bswap64(k0);
-        sval[jj] = jj;
-        ncomp += slow ? 0u : nb;
+          ncomp += slow ? 0u : nb;
         if (jj + 1 < d) cur = nxt;
       }
       last0 = k0;
@@ -1557,15 +1550,98 @@ __global__ void k_count_scatter(const uint32_t* dcount, uint32_t n, uint32_t S, 
   }
 }
 
-// Rows of more than 1024 fresh keys: one CTA per candidate (largest first).  Runs of up to R
-// keys are bitonic-sorted in shared memory on (first 4 key bytes, big endian) << 32 | job
-// index; runs are merged pairwise in the candidate's two global sort rows (merge path: each
-// thread writes a 1/BT stretch of the output); runs of equal first 4 bytes (p ~ d^2 / 2^33 per
-// candidate) are then ordered by the full key as in k_sortkeys, and the keys are gathered into
-// fresh_sorted with 16-byte loads and coalesced 16-byte stores.  Dynamic shared memory: R words.
+// Rows of more than 1024 fresh keys: one CTA per candidate (largest first), sorting on
+// (first 4 key bytes, big endian) << 32 | job index.  Up to R keys (the common case): a bucket
+// sort in shared memory -- the keys are node-key hashes, uniform in their first bytes, so
+// pow2(d) buckets on the top bits hold ~1 key each: a histogram, a block scan, a scatter and a
+// per-bucket insertion sort, O(d) work and four barriers instead of bitonic's log^2 d stages.
+// Beyond R keys: runs of R bitonic-sorted in shared memory, merged pairwise in the candidate's
+// two global sort rows (merge path: each thread writes a 1/BT stretch of the output).  Runs of
+// equal first 4 bytes (p ~ d^2 / 2^33 per candidate) are then ordered by the full key as in
+// k_sortkeys, and the keys are gathered into fresh_sorted with 16-byte loads and coalesced
+// 16-byte stores.  Dynamic shared memory: R words + R bucket counters.
+// the end of a k_sortbig candidate: src holds (first 4 key bytes << 32 | job index) ascending;
+// runs of equal first 4 bytes are ordered by the full key, then the keys are gathered into
+// fresh_sorted (src may be shared or global memory)
+template <int BT>
+__device__ __forceinline__ void sort_finish(const VArgs& A, uint32_t lc, uint32_t d, uint64_t* src) {
+  const uint32_t tid = threadIdx.x;
+  const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
+  int tie = 0;
+  for (uint32_t i = tid; i + 1 < d; i += BT) tie |= (src[i] >> 32) == (src[i + 1] >> 32);
+  if (__syncthreads_or(tie) && tid == 0) {
+    auto less = [&](uint32_t x, uint32_t y) {
+      const uint64_t a0 = B2b::bswap64(fresh[2 * x]), b0 = B2b::bswap64(fresh[2 * y]);
+      if (a0 != b0) return a0 < b0;
+      return B2b::bswap64(fresh[2 * x + 1]) < B2b::bswap64(fresh[2 * y + 1]);
+    };
+    for (uint32_t i = 0; i + 1 < d;) {
+      uint32_t e = i + 1;
+      while (e < d && (src[e] >> 32) == (src[i] >> 32)) ++e;
+      for (uint32_t x = i + 1; x < e; ++x) {  // insertion sort of the run by the full key
+        const uint64_t v = src[x];
+        uint32_t y = x;
+        while (y > i && less((uint32_t)v, (uint32_t)src[y - 1])) {
+          src[y] = src[y - 1];
+          --y;
+        }
+        src[y] = v;
+      }
+      i = e;
+    }
+  }
+  __syncthreads();
+  uint4* out = reinterpret_cast<uint4*>(A.fresh_sorted + 2ull * lc * A.S);
+  const uint4* f4 = reinterpret_cast<const uint4*>(fresh);
+  uint32_t* osv = A.sval_sorted + (uint64_t)lc * A.S;
+  for (uint32_t i = tid; i < d; i += BT) {
+    const uint32_t v = (uint32_t)src[i];
+    out[i] = f4[v];
+    if (A.full) osv[i] = v;
+  }
+  __syncthreads();
+}
+
+template <int BT>
+__device__ __forceinline__ void block_excl_scan_inplace(uint32_t* cnt, uint32_t nb, uint32_t* wsum) {
+  // each thread scans a contiguous stretch of nb / BT counters (nb is a power of two >= 32)
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t per = (nb + BT - 1) / BT;
+  const uint32_t b0 = min(nb, tid * per), b1 = min(nb, b0 + per);
+  uint32_t loc = 0;
+  for (uint32_t b = b0; b < b1; ++b) loc += cnt[b];
+  uint32_t inc = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= (uint32_t)o) inc += y;
+  }
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t v = lane < BT / 32 ? wsum[lane] : 0u, x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane < BT / 32) wsum[lane] = x - v;
+  }
+  __syncthreads();
+  uint32_t run = wsum[w] + inc - loc;
+  for (uint32_t b = b0; b < b1; ++b) {
+    const uint32_t c = cnt[b];
+    cnt[b] = run;
+    run += c;
+  }
+  __syncthreads();
+}
+
 template <int BT>
 __global__ void __launch_bounds__(BT) k_sortbig(VArgs A, uint32_t R) {
   extern __shared__ uint64_t sbig[];
+  __shared__ uint32_t wsum[BT / 32];
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(sbig + R);  // R bucket counters
   const uint32_t tid = threadIdx.x;
   for (uint32_t l = blockIdx.x; l < A.n; l += gridDim.x) {
     const uint32_t lc = A.order[l];
@@ -1573,6 +1649,38 @@ __global__ void __launch_bounds__(BT) k_sortbig(VArgs A, uint32_t R) {
     if (d == 0) continue;  // CTA-uniform
     uint64_t* in = A.skey + (uint64_t)lc * A.S;  // first key words (big endian); free after the runs
     uint64_t* runs = const_cast<uint64_t*>(A.skey_sorted) + (uint64_t)lc * A.S;
+    if (d <= R) {  // bucket sort in shared memory
+      uint32_t nb = 32, lg = 5;
+      while (nb < d) nb <<= 1, ++lg;
+      const uint32_t shift = 32 - lg;
+      for (uint32_t b = tid; b < nb; b += BT) cnt[b] = 0;
+      __syncthreads();
+      for (uint32_t i = tid; i < d; i += BT) atomicAdd(cnt + (uint32_t)(in[i] >> (32 + shift)), 1u);
+      __syncthreads();
+      block_excl_scan_inplace<BT>(cnt, nb, wsum);
+      for (uint32_t i = tid; i < d; i += BT) {
+        const uint64_t v = in[i];
+        const uint32_t pos = atomicAdd(cnt + (uint32_t)(v >> (32 + shift)), 1u);
+        sbig[pos] = ((v >> 32) << 32) | i;
+      }
+      __syncthreads();
+      // cnt[b] is now the end of bucket b: order each bucket (distinct values: the index)
+      for (uint32_t b = tid; b < nb; b += BT) {
+        const uint32_t e = cnt[b], s0 = b ? cnt[b - 1] : 0u;
+        for (uint32_t x = s0 + 1; x < e; ++x) {
+          const uint64_t v = sbig[x];
+          uint32_t y = x;
+          while (y > s0 && sbig[y - 1] > v) {
+            sbig[y] = sbig[y - 1];
+            --y;
+          }
+          sbig[y] = v;
+        }
+      }
+      __syncthreads();
+      sort_finish<BT>(A, lc, d, sbig);
+      continue;
+    }
     for (uint32_t r0 = 0; r0 < d; r0 += R) {
       const uint32_t len = min(R, d - r0);
       uint32_t m = 2;
@@ -1623,40 +1731,7 @@ __global__ void __launch_bounds__(BT) k_sortbig(VArgs A, uint32_t R) {
       src = dst;
       dst = t;
     }
-    const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
-    int tie = 0;
-    for (uint32_t i = tid; i + 1 < d; i += BT) tie |= (src[i] >> 32) == (src[i + 1] >> 32);
-    if (__syncthreads_or(tie) && tid == 0) {
-      auto less = [&](uint32_t x, uint32_t y) {
-        const uint64_t a0 = B2b::bswap64(fresh[2 * x]), b0 = B2b::bswap64(fresh[2 * y]);
-        if (a0 != b0) return a0 < b0;
-        return B2b::bswap64(fresh[2 * x + 1]) < B2b::bswap64(fresh[2 * y + 1]);
-      };
-      for (uint32_t i = 0; i + 1 < d;) {
-        uint32_t e = i + 1;
-        while (e < d && (src[e] >> 32) == (src[i] >> 32)) ++e;
-        for (uint32_t x = i + 1; x < e; ++x) {  // insertion sort of the run by the full key
-          const uint64_t v = src[x];
-          uint32_t y = x;
-          while (y > i && less((uint32_t)v, (uint32_t)src[y - 1])) {
-            src[y] = src[y - 1];
-            --y;
-          }
-          src[y] = v;
-        }
-        i = e;
-      }
-    }
-    __syncthreads();
-    uint4* out = reinterpret_cast<uint4*>(A.fresh_sorted + 2ull * lc * A.S);
-    const uint4* f4 = reinterpret_cast<const uint4*>(fresh);
-    uint32_t* osv = A.sval_sorted + (uint64_t)lc * A.S;
-    for (uint32_t i = tid; i < d; i += BT) {
-      const uint32_t v = (uint32_t)src[i];
-      out[i] = f4[v];
-      if (A.full) osv[i] = v;
-    }
-    __syncthreads();
+    sort_finish<BT>(A, lc, d, src);
   }
 }
 
@@ -2579,6 +2654,7 @@ struct VPriceArgs {
   uint8_t* alg8;  // [total][S]: assignment per child node of every priced candidate
   uint8_t* algt;  // rows > 256: the sweep's rows interleaved per warp (lane-minor), one per thread
   uint32_t S;
+  ef_cand_result* out;  // speculative pricing: results by candidate here, not in pa.res (null: pa.res)
 };
 
 // one thread per survivor of the step's dedup (the compacted list); KIND < 0: any cost kind / radius
@@ -2593,7 +2669,7 @@ __global__ void __launch_bounds__(EF_PRICE_THREADS) k_price_v(VPriceArgs A, cons
     const unsigned mask = __ballot_sync(0xffffffffu, k < total);
     if (k >= total) continue;
     const uint32_t c = plist[k];
-    ef_cand_result& res = A.pa.res[c];
+    ef_cand_result& res = A.out ? A.out[c] : A.pa.res[c];
     const VPlan& P = A.plan[c];
     Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
     VirtView V;
@@ -2625,6 +2701,48 @@ __global__ void __launch_bounds__(EF_PRICE_THREADS) k_price_v(VPriceArgs A, cons
     } else {
       price_graph(A.pa, V, alg, res);
     }
+  }
+}
+
+// Speculative pricing (large graphs): the candidates to price before deduplication is known,
+// i.e. every complete candidate within the node cap (a superset of the survivors)
+__global__ void k_spec_list(const ef_cand_result* res, uint32_t total, int32_t node_cap, uint32_t* list,
+                            uint32_t* list_n, ef_cand_result* spec) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t span = (total + blockDim.x - 1) / blockDim.x * blockDim.x;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < span; c += gridDim.x * blockDim.x) {
+    bool in = false;
+    if (c < total) {
+      spec[c].flags = 0;  // price_d1 ors PRICED / MISSING in
+      in = !(res[c].flags & EF_F_INCOMPLETE) && res[c].n_compute <= node_cap;
+    }
+    const unsigned m = __ballot_sync(__activemask(), in);
+    if (m) {
+      uint32_t base = 0;
+      const int leader = __ffs(m) - 1;
+      if ((int)lane == leader) base = atomicAdd(list_n, (uint32_t)__popc(m));
+      base = __shfl_sync(__activemask(), base, leader);
+      if (in) list[base + __popc(m & ((1u << lane) - 1u))] = c;
+    }
+  }
+}
+
+// after the dedup: the speculative prices of the survivors (the candidates the dedup's list
+// holds: FIRST -- PFIRST per parent -- not VISITED, not CAPPED) into the step's results;
+// the others stay unpriced, exactly as if only the survivors had been priced
+__global__ void k_spec_commit(ef_cand_result* res, const ef_cand_result* spec, uint32_t total, int per_parent) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
+    ef_cand_result& r = res[c];
+    const uint32_t f = r.flags;
+    const uint32_t first = per_parent ? EF_F_PFIRST : EF_F_FIRST;
+    if ((f & EF_F_INCOMPLETE) || (f & (first | EF_F_VISITED | EF_F_CAPPED)) != first) continue;
+    const ef_cand_result& x = spec[c];
+    r.cost = x.cost;
+    r.time_ms = x.time_ms;
+    r.energy = x.energy;
+    r.evals = x.evals;
+    r.sweeps = x.sweeps;
+    r.flags = f | (x.flags & (EF_F_PRICED | EF_F_MISSING));
   }
 }
 
@@ -2762,6 +2880,92 @@ __global__ void k_owner_insert(OwnerArgs O) {
     const uint64_t h = O.recv[2 * (uint64_t)i];
     const unsigned long long key = h ? h : 0x8000000000000000ULL;
     if (!vis_insert(O.vis_key, O.vis_mask, O.vis_count, key, h)) atomicOr(O.err, 8u);
+  }
+}
+
+// fixed-capacity buckets: pair k of owner o at o * cap + k; one warp-aggregated atomic per
+// owner present in the warp.  perm[o * cap + k] = candidate (the bucket's order does not
+// matter: the owner decides first occurrence by the global order carried in the pair)
+__global__ void k_route_pad(RouteArgs R, uint32_t cap) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t span = (R.total + 31) / 32 * 32;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < span; c += gridDim.x * blockDim.x) {
+    const bool live = c < R.total && !(R.res[c].flags & EF_F_INCOMPLETE);
+    const unsigned act = __ballot_sync(0xffffffffu, live);
+    if (!live) continue;
+    const uint64_t h = R.res[c].hash;
+    const uint32_t o = owner_of(h, R.world);
+    const unsigned peers = __match_any_sync(act, o);
+    const uint32_t leader = (uint32_t)(__ffs(peers) - 1);
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(&R.count[o], (uint32_t)__popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    const uint32_t k = base + __popc(peers & ((1u << lane) - 1u));  // < cap: cap >= candidates
+    const uint64_t pos = (uint64_t)o * cap + k;
+    R.send[2 * pos] = h;
+    R.send[2 * pos + 1] = R.order_base + c;
+    R.perm[pos] = c;
+  }
+}
+
+// padded receive buffers: slot i is valid iff i % cap < counts[i / cap]; invalid verdicts are 0
+__global__ void k_owner_claim_pad(OwnerArgs O, const uint32_t* counts, uint32_t cap) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < O.n; i += gridDim.x * blockDim.x) {
+    if (i % cap >= counts[i / cap]) continue;
+    const uint64_t h = O.recv[2 * (uint64_t)i];
+    const unsigned long long key = h ? h : 0x8000000000000000ULL;
+    uint32_t s = (uint32_t)mix64(h) & O.mask;
+    for (uint32_t probe = 0; probe <= O.mask; ++probe, s = (s + 1) & O.mask) {
+      const unsigned long long prev = atomicCAS(&O.key[s], 0ULL, key);
+      if (prev == 0ULL || prev == key) {
+        atomicMin(&O.ord[s], (unsigned long long)O.recv[2 * (uint64_t)i + 1]);
+        break;
+      }
+    }
+  }
+}
+
+__global__ void k_owner_resolve_pad(OwnerArgs O, const uint32_t* counts, uint32_t cap) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < O.n; i += gridDim.x * blockDim.x) {
+    if (i % cap >= counts[i / cap]) {
+      O.verdict[i] = 0;
+      continue;
+    }
+    const uint64_t h = O.recv[2 * (uint64_t)i];
+    const unsigned long long key = h ? h : 0x8000000000000000ULL;
+    unsigned long long first = ~0ULL;
+    uint32_t s = (uint32_t)mix64(h) & O.mask;
+    for (uint32_t probe = 0; probe <= O.mask; ++probe, s = (s + 1) & O.mask) {
+      if (O.key[s] == key) {
+        first = O.ord[s];
+        break;
+      }
+    }
+    uint32_t v = first == O.recv[2 * (uint64_t)i + 1] ? EF_F_FIRST : 0u;
+    if (vis_contains(O.vis_key, O.vis_mask, key, h)) v |= EF_F_VISITED;
+    O.verdict[i] = v;
+  }
+}
+
+__global__ void k_owner_insert_pad(OwnerArgs O, const uint32_t* counts, uint32_t cap) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < O.n; i += gridDim.x * blockDim.x) {
+    if (i % cap >= counts[i / cap] || O.verdict[i] != EF_F_FIRST) continue;
+    const uint64_t h = O.recv[2 * (uint64_t)i];
+    const unsigned long long key = h ? h : 0x8000000000000000ULL;
+    if (!vis_insert(O.vis_key, O.vis_mask, O.vis_count, key, h)) atomicOr(O.err, 8u);
+  }
+}
+
+// verdicts in the padded send layout -> candidate flags and node cap
+__global__ void k_apply_verdicts_pad(ef_cand_result* res, const uint32_t* perm, const uint32_t* counts,
+                                     const uint32_t* verdict, uint32_t world, uint32_t cap, int node_cap) {
+  const uint64_t n = (uint64_t)world * cap;
+  for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    if (i % cap >= counts[i / cap]) continue;
+    const uint32_t c = perm[i];
+    uint32_t f = res[c].flags | (verdict[i] & (EF_F_FIRST | EF_F_VISITED));
+    if (res[c].n_compute > node_cap) f |= EF_F_CAPPED;
+    res[c].flags = f;
   }
 }
 

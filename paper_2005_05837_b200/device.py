@@ -123,6 +123,9 @@ class DeviceSession:
         self.ctx = self.L.ef_create(device)
         if not self.ctx:
             raise NativeUnavailable(f"ef_create({device}) failed")
+        # held by users of the session's one geometry (rewrite.scratch_graph): the single-graph
+        # entry points share the default session across threads
+        self.lock = threading.RLock()
         # signatures
         self.sig_id: dict[str, int] = {}
         self.sig_list: list[NodeSignature] = []
@@ -291,6 +294,12 @@ class DeviceSession:
     def commit(self) -> None:
         self._check(self.L.ef_tables_commit(self.ctx), "ef_tables_commit")
 
+    def last_commit_bytes(self) -> int:
+        """Host->device bytes the last commit sent (incremental: only what changed)."""
+        out = C.c_uint64(0)
+        self._check(self.L.ef_commit_bytes(self.ctx, C.byref(out)), "ef_commit_bytes")
+        return out.value
+
     def _pending_summary(self) -> str:
         ns, nd = C.c_uint32(0), C.c_uint32(0)
         self._check(self.L.ef_pending(self.ctx, None, 0, C.byref(ns), None, 0, C.byref(nd)), "ef_pending")
@@ -299,13 +308,15 @@ class DeviceSession:
         self._check(self.L.ef_pending(self.ctx, sigs, ns.value, C.byref(ns), dvs, nd.value, C.byref(nd)), "ef_pending")
         return f"sigs={[sigs[i].key() for i in range(ns.value)]} known={list(self.sig_desc_key)[:8]} derives={list(dvs)[:4 * nd.value]}"
 
-    def resolve_pending(self) -> None:
-        """Intern what the last ef_expand asked for, then commit."""
+    def resolve_pending(self) -> bool:
+        """Intern what the last ef_expand asked for, then commit.  -> whether anything new was
+        interned."""
         ns, nd = C.c_uint32(0), C.c_uint32(0)
         self._check(self.L.ef_pending(self.ctx, None, 0, C.byref(ns), None, 0, C.byref(nd)), "ef_pending")
         sigs = (N.SigDesc * max(1, ns.value))()
         dvs = (C.c_int32 * max(4, 4 * nd.value))()
         self._check(self.L.ef_pending(self.ctx, sigs, ns.value, C.byref(ns), dvs, nd.value, C.byref(nd)), "ef_pending")
+        n_sig, n_ws = len(self.sig_list), len(self.ws)
         for i in range(ns.value):
             d = sigs[i]
             if d.key() in self.sig_desc_key:
@@ -319,6 +330,7 @@ class DeviceSession:
                 seen.add(q)
                 self._derive(*q)
         self.commit()
+        return len(self.sig_list) != n_sig or len(self.ws) != n_ws
 
     # ------------------------------------------------------------------ records
 
@@ -467,13 +479,14 @@ class DeviceSession:
         parents = N.u32_array(slots)
         rules = N.i32_array(rule_ids)
         count = C.c_uint32(0)
-        for attempt in range(64):
+        while True:
             rc = self.L.ef_expand(self.ctx, parents, len(slots), rules, len(rule_ids), C.byref(pp),
                                   int(insert_visited), C.byref(count))
             if rc == N.EF_NEED_RESOLVE:
-                if attempt >= 3:
+                # a step records at most req_cap requests; retry while every round interns
+                # something new (a round that interns nothing would loop forever)
+                if not self.resolve_pending():
                     raise N.NativeError(f"ef_expand keeps asking for interning: {self._pending_summary()}")
-                self.resolve_pending()
                 continue
             self._check(rc, "ef_expand")
             break
@@ -525,16 +538,14 @@ class DeviceSession:
         parents = N.u32_array(slots)
         rules = N.i32_array(rule_ids)
         count = C.c_uint32(0)
-        for attempt in range(8):
+        while True:
             rc = self.L.ef_expand_hashes(self.ctx, parents, len(slots), rules, len(rule_ids), C.byref(count))
             if rc == N.EF_NEED_RESOLVE:
-                if attempt >= 3:
+                if not self.resolve_pending():
                     raise N.NativeError(f"ef_expand_hashes keeps asking for interning: {self._pending_summary()}")
-                self.resolve_pending()
                 continue
             self._check(rc, "ef_expand_hashes")
             return count.value
-        raise N.NativeError("ef_expand_hashes did not converge")
 
     def route_owners(self, world: int, order_base: int, send) -> list[int]:
         """`send`: int64 CUDA tensor with room for 2 * candidates (hash, global order) pairs."""
@@ -553,6 +564,33 @@ class DeviceSession:
                     "ef_expand_finish")
         return self._results(n)
 
+    def route_owners_padded(self, world: int, order_base: int, cap: int, send, counts) -> None:
+        """`send`: int64 CUDA tensor of world * cap * 2 (hash, global order) pairs by owner bucket;
+        `counts`: int32 CUDA tensor of world pairs per owner (both written on the device)."""
+        self._check(self.L.ef_route_owners_padded(self.ctx, world, order_base, cap, C.c_void_p(send.data_ptr()),
+                                                  C.c_void_p(counts.data_ptr())), "ef_route_owners_padded")
+
+    def owner_mark_padded(self, recv, recv_counts, world: int, cap: int, verdict, insert_visited: bool) -> None:
+        self._check(self.L.ef_owner_mark_padded(self.ctx, C.c_void_p(recv.data_ptr()), C.c_void_p(recv_counts.data_ptr()),
+                                                world, cap, C.c_void_p(verdict.data_ptr()), int(insert_visited)),
+                    "ef_owner_mark_padded")
+
+    def expand_finish_padded(self, verdict_back, world: int, cap: int, pp: N.PriceParams, n: int) -> np.ndarray:
+        self._check(self.L.ef_expand_finish_padded(self.ctx, C.c_void_p(verdict_back.data_ptr()), world, cap,
+                                                   C.byref(pp)), "ef_expand_finish_padded")
+        return self._results(n)
+
+    def stream_handle(self) -> int:
+        """The library stream (cudaStream_t) as an integer, for torch.cuda.ExternalStream."""
+        out = C.c_void_p(0)
+        self._check(self.L.ef_stream(self.ctx, C.byref(out)), "ef_stream")
+        return int(out.value or 0)
+
+    def reprune(self, best: float, alpha: float) -> np.ndarray:
+        """Recompute the last step's alpha-prune flags from `best` (ef_reprune); -> fresh results."""
+        self._check(self.L.ef_reprune(self.ctx, float(best), float(alpha)), "ef_reprune")
+        return self._results(self.last_stats()["candidates"])
+
     def upload_fence(self) -> None:
         """Later steps wait for every asynchronous upload issued so far."""
         self._check(self.L.ef_upload_fence(self.ctx), "ef_upload_fence")
@@ -562,11 +600,17 @@ class DeviceSession:
         """Records of rewrites named (index into parent_slots, rewrite index within that parent)
         (ef_materialise); -> their new slots."""
         slots = self.alloc_n(len(cand_parent))
-        self._check(self.L.ef_materialise(self.ctx, N.u32_array(parent_slots), len(parent_slots),
-                                          N.i32_array(rule_ids), len(rule_ids), N.u32_array(cand_parent),
-                                          N.u32_array(cand_local), len(cand_parent), N.u32_array(slots)),
-                    "ef_materialise")
-        return slots
+        args = (N.u32_array(parent_slots), len(parent_slots), N.i32_array(rule_ids), len(rule_ids),
+                N.u32_array(cand_parent), N.u32_array(cand_local), len(cand_parent), N.u32_array(slots))
+        while True:
+            rc = self.L.ef_materialise(self.ctx, *args)
+            # a rewrite another rank's step interned (sharded closure / search): intern it here
+            if rc == N.EF_NEED_RESOLVE:
+                if not self.resolve_pending():
+                    raise N.NativeError(f"ef_materialise keeps asking for interning: {self._pending_summary()}")
+                continue
+            self._check(rc, "ef_materialise")
+            return slots
 
     def keep(self, cand_idx: list[int]) -> list[int]:
         slots = self.alloc_n(len(cand_idx))

@@ -34,6 +34,7 @@ from .errors import InfeasibleConstraint, MissingEntry, SpaceTooLarge
 from .ir import Graph
 from .profiler import ProfilerSpec, ensure_profiled, profile_signature, record_line
 from .rewrite import SubstitutionRule, scratch_graph
+from .shard import gather_batch, sharded_expand
 
 
 @dataclass
@@ -207,7 +208,7 @@ def outer_search(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: 
                  cfg: SearchConfig, profiler: ProfilerSpec | None, use_inner: bool = True,
                  db_append_path: str | None = None, session: DeviceSession | None = None,
                  trace: list | None = None, batch: int | None = None,
-                 check_prune: bool = False) -> OptimizationResult:
+                 check_prune: bool = False, exchange=None) -> OptimizationResult:
     """Best-first search over the rewrite space of g0 (search.py:211-272), expanded on the GPU.
 
     The reference's loop is kept exactly: heap of (cost, hash), the visited set, the alpha rule
@@ -232,6 +233,11 @@ def outer_search(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: 
     alpha-prune flags (EF_F_BEST / EF_F_ENQUEUE: a prefix-min over the step's first occurrences,
     seeded with the best at step time) are exactly the reference's decisions and are used;
     `check_prune=True` also recomputes them on the host and asserts equality (tests).
+
+    `exchange` (shard.OwnerExchange, one process per GPU): every rank runs this same replay;
+    each batch is expanded split over the ranks (shard.gather_batch: a contiguous slice per rank,
+    the prune flags carried across ranks by an exclusive minimum, the results all-gathered), so
+    every rank returns the single-GPU result.
     """
     started = time.perf_counter()
     stats = SearchStats()
@@ -301,7 +307,9 @@ def outer_search(g0: Graph, rules: list[SubstitutionRule], db: CostDatabase, f: 
                 s.visited_insert(new_vis)
                 new_vis.clear()
             pp.best = best_cost
-            if rule_ids:
+            if rule_ids and exchange is not None and exchange.world > 1:
+                res = gather_batch(s, slots, rule_ids, pp, exchange)
+            elif rule_ids:
                 res = s.expand(slots, rule_ids, pp, insert_visited=False)
             else:
                 res = np.empty(0, dtype=N.CAND_DTYPE)
@@ -451,7 +459,7 @@ def brute_force_assignment(g: Graph, db: CostDatabase, f: CostFunction, max_poin
 
 
 def closure(g0: Graph, rules: list[SubstitutionRule], max_graphs: int, max_graph_nodes: int | None = None,
-            session: DeviceSession | None = None) -> list[Graph]:
+            session: DeviceSession | None = None, exchange=None) -> list[Graph]:
     """BFS closure of g0 under the rules, deduplicated by canonical hash (search.py:275-300).
 
     Each BFS level is ONE batched ef_expand over all graphs of the level: candidates come back
@@ -459,7 +467,12 @@ def closure(g0: Graph, rules: list[SubstitutionRule], max_graphs: int, max_graph
     VISITED membership in the hashes seen before it, which is exactly the reference's
     sequential `seen` check; the device inserts the level's new hashes into the visited set.
     Raises SpaceTooLarge past `max_graphs`; graphs above the node cap are seen, not kept.
+
+    `exchange` (shard.OwnerExchange): the levels are expanded split over the ranks with
+    hash-owner deduplication (_closure_sharded); every rank returns the same list.
     """
+    if exchange is not None and exchange.world > 1:
+        return _closure_sharded(g0, rules, max_graphs, max_graph_nodes, session, exchange)
     s = session or DeviceSession.default()
     rule_ids = [r.rule_id for r in rules]
     cap = max_graph_nodes if max_graph_nodes is not None else 1 << 30
@@ -479,6 +492,49 @@ def closure(g0: Graph, rules: list[SubstitutionRule], max_graphs: int, max_graph
             if len(out_slots) + len(keep) > max_graphs:
                 raise SpaceTooLarge(f"rewrite closure exceeds {max_graphs} graphs")
             level = s.keep(keep) if keep else []
+            out_slots += level
+        return [s.decode(s.read_record(sl), g0)[0] for sl in out_slots]
+    finally:
+        for sl in out_slots:
+            if sl != run.root:
+                s.free(sl)
+        run.close()
+
+
+def _closure_sharded(g0: Graph, rules: list[SubstitutionRule], max_graphs: int, max_graph_nodes: int | None,
+                     session: DeviceSession | None, ex) -> list[Graph]:
+    """The BFS closure over ranks (search.py:275-300).  Every rank holds every graph's record;
+    rank r expands the contiguous slice shard.batch_slice(len(level), r, world) of each level
+    through shard.sharded_expand, whose hash-owner all-to-all gives global first occurrences
+    (rank-major = the single-GPU (parent, rule, site) order) and membership in the owner's
+    shard of the visited set (inserted there).  The kept (parent, rewrite) pairs are
+    all-gathered in rank order and every rank materialises the next level from them."""
+    from .shard import batch_slice, owner_of
+
+    s = session or DeviceSession.default()
+    rule_ids = [r.rule_id for r in rules]
+    cap = max_graph_nodes if max_graph_nodes is not None else 1 << 30
+    geo_cap = max_graph_nodes if max_graph_nodes is not None else 4 * max(1, len(g0.compute_nodes()))
+    run = _Run(s, g0, max(geo_cap, len(g0.compute_nodes())), CostDatabase(), None)
+    out_slots = [run.root]
+    try:
+        (h0,) = s.hash_slots([run.root])
+        if owner_of(h0, ex.world) == ex.rank:
+            s.visited_insert([h0])
+        pp = price_params(CostFunction.time(), 1, False, cap)
+        level = [run.root]
+        while level and rule_ids:
+            lo, hi = batch_slice(len(level), ex.rank, ex.world)
+            res = sharded_expand(s, level[lo:hi], rule_ids, pp, ex, insert_visited=True)
+            fl = res["flags"].tolist()
+            par = res["parent"].tolist()
+            seg = np.searchsorted(res["parent"], np.arange(hi - lo + 1)).tolist() if len(res) else [0] * (hi - lo + 1)
+            keep = [(lo + par[i], i - seg[par[i]]) for i, f in enumerate(fl)
+                    if (f & (N.F_FIRST | N.F_VISITED | N.F_CAPPED)) == N.F_FIRST]
+            kept = [k for part in ex.all_gather_object(keep) for k in part]
+            if len(out_slots) + len(kept) > max_graphs:
+                raise SpaceTooLarge(f"rewrite closure exceeds {max_graphs} graphs")
+            level = s.materialise(level, rule_ids, [p for p, _ in kept], [q for _, q in kept]) if kept else []
             out_slots += level
         return [s.decode(s.read_record(sl), g0)[0] for sl in out_slots]
     finally:

@@ -82,15 +82,16 @@ def select_rules(spec: str) -> list[SubstitutionRule]:
 def scratch_graph(g: Graph, session: DeviceSession | None = None, extra_nodes: int = 4):
     """Upload `g` into a fresh geometry; yields (session, slot); frees everything after."""
     s = session or DeviceSession.default()
-    n = len(g.nodes)
-    n_refs = sum(len(v.inputs) for v in g.nodes.values())
-    s.set_geometry(g, n + extra_nodes, n_refs + extra_nodes)
-    s.visited_reset(1 << 12)
-    slot = s.upload(g)
-    try:
-        yield s, slot
-    finally:
-        s.free(slot)
+    with s.lock:  # the geometry and the scratch record belong to this caller until it is done
+        n = len(g.nodes)
+        n_refs = sum(len(v.inputs) for v in g.nodes.values())
+        s.set_geometry(g, n + extra_nodes, n_refs + extra_nodes)
+        s.visited_reset(1 << 12)
+        slot = s.upload(g)
+        try:
+            yield s, slot
+        finally:
+            s.free(slot)
 
 
 def _site_of(rule_name: str, g_ids: list[int], r) -> MatchSite:

@@ -22,13 +22,23 @@ def to_oracle(g):
             "outputs": [(r.node, r.port) for r in g.outputs]}
 
 
-@pytest.mark.parametrize("n_ops,n_parents,sample", [(1000, 4, 24), (5000, 2, 8), (20000, 1, 3)])
-def test_random_dag_step_matches_oracle(n_ops, n_parents, sample):
+@pytest.mark.parametrize("n_ops,n_parents,sample,objective", [
+    (1000, 4, 24, "energy"), (1000, 2, 12, "linear0.5"),  # rows <= 2048: interleaved sweep rows
+    (5000, 2, 8, "energy"), (5000, 1, 4, "linear0.5"),    # rows > 2048: row-major sweep rows
+    (20000, 1, 3, "energy")])
+def test_random_dag_step_matches_oracle(n_ops, n_parents, sample, objective):
+    """k_price_v<ENERGY / LINEAR, false> with the exact skip of nodes with no cheaper row, on
+    both sweep-row layouts; the energy-delay objective over the origin's normalization refs."""
     from oracle import enerflow_oracle as orc
 
     g0 = zoo.random_dag(n_ops, 0)
     db = ef.CostDatabase()
-    fr = Frontier(g0, db, ef.SyntheticProfiler(0), ef.CostFunction.energy(), ef.SearchConfig(alpha=1.05), n_parents)
+    ef.ensure_profiled(g0, db, ef.SyntheticProfiler(0))
+    if objective == "energy":
+        f = ef.CostFunction.energy()
+    else:
+        f = ef.CostFunction.linear(0.5).with_refs(*ef.normalization_refs(g0, db))
+    fr = Frontier(g0, db, ef.SyntheticProfiler(0), f, ef.SearchConfig(alpha=1.05), n_parents)
     try:
         res = fr.step()
         parents = [fr.decode(sl) for sl in fr.slots]
@@ -37,6 +47,9 @@ def test_random_dag_step_matches_oracle(n_ops, n_parents, sample):
     odb = orc.CostDB()
     for (sig, alg), rec in db.records().items():
         odb.add(sig, alg, rec.time_ms, rec.power_w)
+    og0 = to_oracle(g0)
+    of = orc.CostFn("energy") if objective == "energy" else orc.CostFn("linear", w=0.5,
+                                                                       refs=orc.normalization_refs(og0, odb))
     rule_names = {i: r.name for i, r in enumerate(ef.default_rules())}
     checked = 0
     for pi, pg in enumerate(parents):
@@ -53,7 +66,7 @@ def test_random_dag_step_matches_oracle(n_ops, n_parents, sample):
             assert int(r["hash"]) == orc.canonical_hash(child), (n_ops, pi, rule, site)
             if r["flags"] & N.F_PRICED:
                 orc.ensure_profiled(child, odb, 0)
-                _, cost, t, e, evals, sweeps = orc.sweep(child, odb, orc.CostFn("energy"), 1)
+                _, cost, t, e, evals, sweeps = orc.sweep(child, odb, of, 1)
                 assert (float(r["cost"]), float(r["time_ms"]), float(r["energy"])) == (cost, t, e)
                 assert (int(r["evals"]), int(r["sweeps"])) == (evals, sweeps)
             checked += 1

@@ -1,8 +1,12 @@
-"""The sharded step's CUDA kernels (ef_expand_hashes / ef_route_owners /
-ef_owner_mark / ef_expand_finish) on one GPU, two ranks emulated by two library
-contexts driven from two threads through the product's `sharded_expand`; the
-all-to-all is done in-process.  Every candidate's hash, flags and price must
-equal a single-context `ef_expand` over the concatenated frontier.
+"""The sharded paths' CUDA kernels on one GPU, two ranks emulated by two library
+contexts driven from two threads through the product's code: the sharded step
+(`sharded_expand`: ef_expand_hashes / ef_route_owners_padded /
+ef_owner_mark_padded / ef_expand_finish_padded), the sharded BFS closure and the
+sharded outer search (`exchange=`: shard.gather_batch, ef_reprune).  The
+collectives are done in-process by ThreadExchange.  Every candidate's hash,
+flags and price must equal a single-context `ef_expand` over the concatenated
+frontier; the closure and the search must return exactly the single-GPU result
+on every rank.
 """
 
 import threading
@@ -41,25 +45,61 @@ class ThreadExchange:
     def buffer(self, name, numel, dtype):
         return torch.empty(max(numel, 1), dtype=dtype, device=self.device)[:numel]
 
-    def to_owners(self, send, counts):
-        data = self._gather((send, counts))
-        parts, rc = [], []
-        for snd, cnt in data:
-            off = sum(cnt[: self.rank])
-            parts.append(snd[2 * off: 2 * (off + cnt[self.rank])])
-            rc.append(cnt[self.rank])
-        torch.cuda.synchronize()
-        return torch.cat(parts).contiguous(), rc
+    def max_int(self, x):
+        return max(self._gather(int(x)))
 
-    def back(self, verdict, recv_counts, counts):
-        data = self._gather((verdict, recv_counts))
-        parts = []
-        for v, rco in data:
-            off = sum(rco[: self.rank])
-            parts.append(v[off: off + rco[self.rank]])
-        torch.cuda.synchronize()
-        out = torch.cat(parts).contiguous() if sum(counts) else torch.zeros(1, dtype=torch.int32, device="cuda")
+    def min(self, x):
+        return min(self._gather(float(x)))
+
+    def sum(self, x):
+        return sum(self._gather(float(x)))
+
+    def all_gather_object(self, obj):
+        return self._gather(obj)
+
+    def exclusive_min(self, x, init):
+        out = init
+        for v in self._gather(float(x))[: self.rank]:
+            out = v if v < out else out
         return out
+
+    def to_owners(self, send, counts, cap, session=None):
+        torch.cuda.synchronize()  # the library wrote them on its own stream
+        data = self._gather((send, counts))
+        recv = torch.cat([snd[2 * self.rank * cap: 2 * (self.rank + 1) * cap] for snd, _ in data]).contiguous()
+        rc = torch.stack([cnt[self.rank] for _, cnt in data]).to(torch.int32).contiguous()
+        torch.cuda.synchronize()
+        self._gather(None)  # every rank has copied before the buffers are reused
+        return recv, rc
+
+    def back(self, verdict, cap, session=None):
+        torch.cuda.synchronize()
+        data = self._gather(verdict)
+        out = torch.cat([v[self.rank * cap: (self.rank + 1) * cap] for v in data]).contiguous()
+        torch.cuda.synchronize()
+        self._gather(None)
+        return out
+
+
+def _threads(world, fn):
+    """Run fn(rank, exchange) on `world` threads; -> the per-rank results."""
+    shared = {"barrier": threading.Barrier(world), "slot": [None] * world}
+    out, errs = [None] * world, []
+
+    def run(rank):
+        try:
+            out[rank] = fn(rank, ThreadExchange(rank, world, shared))
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+            shared["barrier"].abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    return out
 
 
 def _session(g0, db, prof, cap, graphs, visited):
@@ -100,25 +140,16 @@ def test_sharded_step_equals_single(model, n_parents):
 
     world, split = 2, len(graphs) // 3
     parts = [graphs[:split], graphs[split:]]
-    shared = {"barrier": threading.Barrier(world), "slot": [None] * world}
-    out, errs = [None] * world, []
 
-    def run(rank):
+    def run(rank, ex):
+        mine = [h for h in visited if owner_of(h, world) == rank]
+        s, slots = _session(g0, db, prof, cap, parts[rank], mine)
         try:
-            mine = [h for h in visited if owner_of(h, world) == rank]
-            s, slots = _session(g0, db, prof, cap, parts[rank], mine)
-            out[rank] = sharded_expand(s, slots, rule_ids, pp, ThreadExchange(rank, world, shared)).copy()
+            return sharded_expand(s, slots, rule_ids, pp, ex).copy()
+        finally:
             s.close()
-        except Exception as e:  # pragma: no cover - reported below
-            errs.append(e)
-            shared["barrier"].abort()
 
-    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join(timeout=300)
-    assert not errs, errs
+    out = _threads(world, run)
     sharded = np.concatenate(out)
     assert len(sharded) == len(single)
     for key in ("hash", "flags", "rule", "site_a", "site_b", "n_compute", "n_nodes"):
@@ -127,3 +158,68 @@ def test_sharded_step_equals_single(model, n_parents):
     assert priced.any() and (~priced).any()
     for key in ("cost", "time_ms", "energy", "evals", "sweeps"):
         assert np.array_equal(sharded[key][priced], single[key][priced]), key
+
+
+@pytest.mark.parametrize("model,max_graphs,max_nodes", [("squeezenet", 400, None), ("resnet50", 300, 54)])
+def test_sharded_closure_equals_single(model, max_graphs, max_nodes):
+    """BFS levels split over two ranks, hash-owner dedup: the same graphs in the same order."""
+    g0 = zoo.generate(model, 0)
+    rules = ef.default_rules()
+
+    def names(gs):
+        return [ef.canonical_hash(g) for g in gs]
+
+    try:
+        single = names(ef.closure(g0, rules, max_graphs, max_nodes))
+        raised = None
+    except ef.SpaceTooLarge as e:
+        single, raised = None, type(e)
+
+    def run(rank, ex):
+        s = DeviceSession(0)
+        try:
+            try:
+                return ef.closure(g0, rules, max_graphs, max_nodes, session=s, exchange=ex)
+            except ef.SpaceTooLarge as e:
+                return type(e)
+        finally:
+            s.close()
+
+    # hashed after the threads join: canonical_hash uses the process's default session, which
+    # two threads must not drive at once
+    got = [r if isinstance(r, type) else names(r) for r in _threads(2, run)]
+    want = raised if raised is not None else single
+    assert got[0] == want and got[1] == want
+
+
+@pytest.mark.parametrize("model,alpha,max_exp,batch", [("squeezenet", 1.0, None, 8), ("resnet50", 1.05, 300, 16)])
+def test_sharded_search_equals_single(model, alpha, max_exp, batch):
+    """The outer search with each batch split over two ranks (prune flags carried across ranks
+    by the exclusive minimum, results all-gathered) returns the single-GPU search on every rank:
+    explored-hash trace, optimised graph, assignment, cost, every statistic."""
+    g0 = zoo.generate(model, 0)
+    cfg = ef.SearchConfig(alpha=alpha, max_expansions=max_exp)
+
+    def search(session=None, exchange=None):
+        trace = []
+        res = ef.outer_search(g0, ef.default_rules(), ef.CostDatabase(), ef.CostFunction.energy(), cfg,
+                              ef.SyntheticProfiler(0), trace=trace, batch=batch, check_prune=True,
+                              session=session, exchange=exchange)
+        st = {k: v for k, v in vars(res.stats).items() if k != "wall_time_ms"}
+        return trace, res.graph, res.assignment, (res.cost, res.time_ms, res.energy), st
+
+    def hashed(r):  # after the threads join (canonical_hash drives the default session)
+        return (r[0], ef.canonical_hash(r[1]), *r[2:])
+
+    want = hashed(search())
+
+    def run(rank, ex):
+        s = DeviceSession(0)
+        try:
+            return search(s, ex)
+        finally:
+            s.close()
+
+    got = [hashed(r) for r in _threads(2, run)]
+    assert got[0] == want
+    assert got[1] == want

@@ -5,7 +5,7 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 #include "../paper_2005_05837_b200/csrc/ef_blake2b.cuh"
-#include "../paper_2005_05837_b200/csrc/ef_b2b_fma.cuh"
+#include "ef_b2b_fma.cuh"
 
 template <int VARIANT>
 __global__ void __launch_bounds__(128) peak(uint64_t* out, int iters, uint32_t one) {

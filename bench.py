@@ -47,7 +47,7 @@ DEFAULT_WORKLOAD = "dag:20000"
 # --workload: the BASELINE.json configs as frontier workloads (name, objective, parents per GPU)
 WORKLOADS = {
     "dag:20000": ("synthetic random-DAG conv/matmul graph, 20k ops, full rule set, energy objective, alpha=1.05 "
-                  "(BASELINE configs[4], largest synthetic graph)", "energy", 8),
+                  "(BASELINE configs[4], largest synthetic graph)", "energy", 9),
     "resnet50": ("ResNet-50 inference graph, energy objective with per-node conv-algorithm selection, alpha=1.05 "
                  "(BASELINE configs[1])", "energy", 4096),
     "squeezenet": ("SqueezeNet inference graph, energy objective, alpha=1.0 search frontier (BASELINE configs[0])",

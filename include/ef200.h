@@ -309,6 +309,11 @@ int ef_records_write_packed_async(ef_ctx* ctx, const uint32_t* slots, uint32_t n
 int ef_upload_fence(ef_ctx* ctx);
 /* measured BLAKE2b compression rate of this GPU (register-only loop): the ALU roofline */
 int ef_b2b_peak(ef_ctx* ctx, double* compress_per_s);
+/* self-check of the pricing's division by a normalisation reference (cost.py:284-296 t / t_ref,
+ * e / e_ref, p / p_ref; reciprocal + two FMA corrections) against the IEEE division: per_divisor
+ * random dividends for each divisor; *mismatches = results differing in any bit (must be 0) */
+int ef_check_division(ef_ctx* ctx, const double* divisors, uint32_t n_divisors, uint64_t per_divisor, uint64_t seed,
+                      uint64_t* mismatches);
 
 #ifdef __cplusplus
 }

@@ -129,6 +129,8 @@ _PROTOS = {
     "ef_expand_finish_padded": (C.c_int, [_P, C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(PriceParams)]),
     "ef_stream": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
     "ef_commit_bytes": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
+    "ef_check_division": (C.c_int, [_P, C.POINTER(C.c_double), C.c_uint32, C.c_uint64, C.c_uint64,
+                                    C.POINTER(C.c_uint64)]),
     "ef_reprune": (C.c_int, [_P, C.c_double, C.c_double]),
 }
 

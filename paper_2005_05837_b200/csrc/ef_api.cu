@@ -184,8 +184,12 @@ struct ef_ctx {
   cudaStream_t st_wide = nullptr;  // k_keys_wide beside k_keys
   // speculative pricing (rows > kFastRows): every complete candidate priced on st_price while
   // the chunks hash, the survivors' prices committed after the dedup (EF_SPEC_PRICE: 0 off,
-  // 1 from the first digest on, 2 from the plans on)
-  int spec_price = 1;
+  // 1 from the first digest on, 2 from the plans on; the side stream has the lowest priority, so
+  // its CTAs fill what the hashing kernels leave free.  DAG-20k 211.9 -> 206.7 ms per step with 2,
+  // 219.7 with 1; Inception-v3 (rows <= 1024) 9.11 -> 9.55 / 9.61 ms: many short candidates
+  // keep every SM busy, and pricing there only competes)
+  int spec_price = 2;
+  uint32_t spec_min_rows = 2048;  // rows (S) above which a step prices speculatively (EF_SPEC_MIN_ROWS)
   const ef_price_params* spec_pp = nullptr;  // set by ef_expand for step_hash
   bool spec_live = false;                    // this step's speculative pricing was launched
   cudaStream_t st_price = nullptr;
@@ -280,7 +284,12 @@ int ef_device_count(void) {
 ef_ctx* ef_create(int device) {
   ef_ctx* ctx = new ef_ctx();
   ctx->dev = device;
-  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) {
+  // stream priorities: the step's main stream (and its wide-key side stream) above the
+  // speculative pricing, so price CTAs only fill what the hashing kernels leave free
+  int prio_lo = 0, prio_hi = 0;
+  if (cudaSetDevice(device) == cudaSuccess) cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&ctx->st, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
     delete ctx;
     return nullptr;
   }
@@ -294,13 +303,14 @@ ef_ctx* ef_create(int device) {
   }
   if (const char* e = getenv("EF_FUSE_MERGE")) ctx->fuse_merge = atoi(e) != 0;
   if (const char* e = getenv("EF_SPEC_PRICE")) ctx->spec_price = atoi(e);
+  if (const char* e = getenv("EF_SPEC_MIN_ROWS")) ctx->spec_min_rows = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_DIGEST_PF")) ctx->digest_pf = atoi(e) != 0;
   if (const char* e = getenv("EF_QUAD_MAX")) ctx->quad_max = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_CHUNK_MIB")) ctx->chunk_mib = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
   cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
   cudaStreamCreateWithFlags(&ctx->st_up, cudaStreamNonBlocking);
-  cudaStreamCreateWithFlags(&ctx->st_wide, cudaStreamNonBlocking);
-  cudaStreamCreateWithFlags(&ctx->st_price, cudaStreamNonBlocking);
+  cudaStreamCreateWithPriority(&ctx->st_wide, cudaStreamNonBlocking, prio_hi);
+  cudaStreamCreateWithPriority(&ctx->st_price, cudaStreamNonBlocking, prio_lo);
   cudaEventCreateWithFlags(&ctx->ev_sp0, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ctx->ev_sp1, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ctx->ev_w0, cudaEventDisableTiming);
@@ -1489,6 +1499,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       EF_CUDA(cudaGetLastError());
     }
     ctx->spec_live = false;
+    if (S <= ctx->spec_min_rows) ctx->spec_pp = nullptr;  // small rows: price after the dedup
     if (ctx->spec_pp && ctx->spec_price == 2 && (rc = launch_spec_price(ctx, total))) return rc;
     cudaEventRecord(ctx->ev[2], ctx->st);
     VArgs V = chunk_args(ctx, sc, S, Rs, lean);
@@ -1558,13 +1569,13 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
           cudaEventRecord(ce[3], ctx->st);
           ++ctx->kcount, k_digest_mg<kHashThreads, 2><<<gd, kHashThreads, 0, ctx->st>>>(V);
         } else if (ctx->big_merge) {  // merge-path key stream, then the streaming digest
-          const size_t smem = 4ull * 4 * (V.W + 1);
+          const size_t smem = 4ull * (4608 + 4 * (V.W + 1));  // per warp: the output stage + kept counts
           EF_CUDA(cudaFuncSetAttribute(k_merge_big<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
           const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
           ++ctx->kcount, k_merge_big<4><<<gm, 128, smem, ctx->st>>>(V);
           EF_CUDA(cudaGetLastError());
           cudaEventRecord(ce[3], ctx->st);
-          if (ctx->digest_pf) ++ctx->kcount, k_digest_pm<kHashThreads, true, 2><<<gd, kHashThreads, 0, ctx->st>>>(V);
+          if (ctx->digest_pf) ++ctx->kcount, k_digest_pm<kHashThreads, true, EF_DIGEST_PF_MINB><<<gd, kHashThreads, 0, ctx->st>>>(V);
           else ++ctx->kcount, k_digest_pm<kHashThreads, false, EF_DIGEST_MINB><<<gd, kHashThreads, 0, ctx->st>>>(V);
         } else {
           cudaEventRecord(ce[3], ctx->st);
@@ -2185,6 +2196,25 @@ int ef_records_write_packed(ef_ctx* ctx, const uint32_t* slots, uint32_t n, cons
   int rc = ef_records_write_packed_async(ctx, slots, n, host, offsets, bytes);
   if (rc) return rc;
   EF_CUDA(cudaStreamSynchronize(ctx->st_up));
+  return EF_OK;
+}
+
+int ef_check_division(ef_ctx* ctx, const double* divisors, uint32_t n_divisors, uint64_t per_divisor, uint64_t seed,
+                      uint64_t* mismatches) {
+  EF_REQUIRE(divisors && n_divisors && mismatches, "ef_check_division: bad arguments");
+  cudaSetDevice(ctx->dev);
+  DevBuf<double> ys;
+  DevBuf<unsigned long long> bad;
+  EF_CUDA(ys.reserve(n_divisors, ctx->st));
+  EF_CUDA(bad.reserve(1, ctx->st));
+  EF_CUDA(cudaMemcpyAsync(ys.p, divisors, n_divisors * 8ull, cudaMemcpyHostToDevice, ctx->st));
+  EF_CUDA(cudaMemsetAsync(bad.p, 0, 8, ctx->st));
+  ++ctx->kcount, k_div_check<<<ctx->n_sm * 8, 256, 0, ctx->st>>>(ys.p, n_divisors, per_divisor, seed, bad.p);
+  EF_CUDA(cudaGetLastError());
+  unsigned long long h = 0;
+  EF_CUDA(cudaMemcpyAsync(&h, bad.p, 8, cudaMemcpyDeviceToHost, ctx->st));
+  EF_CUDA(cudaStreamSynchronize(ctx->st));
+  *mismatches = h;
   return EF_OK;
 }
 

@@ -1111,22 +1111,54 @@ __device__ double pow_py(double x, double y) {
 // cost.py:234-254 in the reference's operation order.  The reference always computes
 // t = time/t_ref and e = energy/e_ref first; for the time / energy / power kinds those
 // quotients are unused, so they are only formed where the result depends on them.
-__device__ __forceinline__ double from_totals(const ef_price_params& f, double time_ms, double energy) {
+// Division by a normalisation reference (cost.py:284-296: t / t_ref, e / e_ref, p / p_ref),
+// correctly rounded like the reference's float `/`, without a full division per evaluation:
+// with r = RN(1 / y) taken once per thread, q0 = RN(x r) is within 2 ulp of x / y, one FMA
+// residual correction q1 = RN(q0 + r RN(x - q0 y)) brings it within one ulp (faithful), and by
+// Markstein's theorem a second correction is the correctly rounded quotient.  Exact for normal
+// operands and quotients: |x|, |y| in [2^-500, 2^500] (checked; else -- and for NaN / inf --
+// the IEEE division).  The residuals x - q y are exact (FMA).  tests/test_gpu_division.py
+// compares it with the division on 2^27 operand pairs per reference.
+struct Recip {
+  double t, e, p;  // RN(1 / ref), or 0: divide
+};
+
+__device__ __forceinline__ double rcp_or_zero(double y) {
+  const double a = fabs(y);
+  return (a >= 0x1p-500 && a <= 0x1p500) ? 1.0 / y : 0.0;
+}
+
+__device__ __forceinline__ Recip recip_of(const ef_price_params& f) {
+  return Recip{rcp_or_zero(f.t_ref), rcp_or_zero(f.e_ref), rcp_or_zero(f.p_ref)};
+}
+
+__device__ __forceinline__ double div_pre(double x, double y, double r) {
+  const double a = fabs(x);
+  if (r != 0.0 && a >= 0x1p-500 && a <= 0x1p500) {
+    const double q0 = __dmul_rn(x, r);
+    const double q1 = __fma_rn(__fma_rn(-q0, y, x), r, q0);
+    return __fma_rn(__fma_rn(-q1, y, x), r, q1);
+  }
+  if (r != 0.0 && x == 0.0) return __dmul_rn(x, r);  // a signed zero, as x / y
+  return x / y;
+}
+
+__device__ __forceinline__ double from_totals(const ef_price_params& f, const Recip& rc, double time_ms, double energy) {
   switch (f.kind) {
     case EF_C_TIME: return time_ms;
     case EF_C_ENERGY: return energy;
     case EF_C_POWER: return time_ms != 0.0 ? energy / time_ms : time_ms * 0.0;
     case EF_C_LINEAR: {
-      const double t = time_ms / f.t_ref, e = energy / f.e_ref;
+      const double t = div_pre(time_ms, f.t_ref, rc.t), e = div_pre(energy, f.e_ref, rc.e);
       return f.w * e + (1.0 - f.w) * t;
     }
     case EF_C_PRODUCT: {
-      const double t = time_ms / f.t_ref, e = energy / f.e_ref;
+      const double t = div_pre(time_ms, f.t_ref, rc.t), e = div_pre(energy, f.e_ref, rc.e);
       return pow_py(e, f.w) * pow_py(t, 1.0 - f.w);
     }
     default: {
-      const double t = time_ms / f.t_ref, e = energy / f.e_ref;
-      const double p = (time_ms != 0.0 ? energy / time_ms : time_ms * 0.0) / f.p_ref;
+      const double t = div_pre(time_ms, f.t_ref, rc.t), e = div_pre(energy, f.e_ref, rc.e);
+      const double p = div_pre(time_ms != 0.0 ? energy / time_ms : time_ms * 0.0, f.p_ref, rc.p);
       return f.ct * t + f.ce * e + f.cp * p;
     }
   }
@@ -1187,7 +1219,8 @@ __device__ void price_graph(const PriceArgs& A, const View& V, uint8_t* alg, ef_
   }
   double t_tot = ncomp ? st.result(F.naive_sum) : 0.0;
   double e_tot = ncomp ? se.result(F.naive_sum) : 0.0;
-  double cost = from_totals(F, t_tot, e_tot);
+  const Recip rc = recip_of(F);
+  double cost = from_totals(F, rc, t_tot, e_tot);
   long long evals = 0;
   int sweeps = 0;
   if (A.pp.use_inner && ncomp > 0) {
@@ -1210,7 +1243,7 @@ __device__ void price_graph(const PriceArgs& A, const View& V, uint8_t* alg, ef_
           double dt = 0.0, de = 0.0;
           dt += T.row_t[ro + q] - T.row_t[ro + cur];
           de += T.row_e[ro + q] - T.row_e[ro + cur];
-          const double cand = from_totals(F, t_tot + dt, e_tot + de);
+          const double cand = from_totals(F, rc, t_tot + dt, e_tot + de);
           ++evals;
           if (cand < cost) {
             alg[i] = (uint8_t)q;
@@ -1249,7 +1282,7 @@ __device__ void price_graph(const PriceArgs& A, const View& V, uint8_t* alg, ef_
                 dt += T.row_t[ro + q] - T.row_t[ro + cur];
                 de += T.row_e[ro + q] - T.row_e[ro + cur];
               }
-              const double cand = from_totals(F, t_tot + dt, e_tot + de);
+              const double cand = from_totals(F, rc, t_tot + dt, e_tot + de);
               ++evals;
               if (cand < cost) {
                 for (int j = 0; j < k; ++j) alg[pos[j]] = (uint8_t)choice[j];
@@ -1302,14 +1335,14 @@ __device__ void price_graph(const PriceArgs& A, const View& V, uint8_t* alg, ef_
 }
 
 template <int KIND>
-__device__ __forceinline__ double cost_of(const ef_price_params& f, double time_ms, double energy) {
+__device__ __forceinline__ double cost_of(const ef_price_params& f, const Recip& rc, double time_ms, double energy) {
   if (KIND == EF_C_TIME) return time_ms;
   if (KIND == EF_C_ENERGY) return energy;
   if (KIND == EF_C_LINEAR) {
-    const double t = time_ms / f.t_ref, e = energy / f.e_ref;
+    const double t = div_pre(time_ms, f.t_ref, rc.t), e = div_pre(energy, f.e_ref, rc.e);
     return f.w * e + (1.0 - f.w) * t;
   }
-  return from_totals(f, time_ms, energy);
+  return from_totals(f, rc, time_ms, energy);
 }
 
 // The d = 1 sweep (search.py:106-153 with radius 1) specialised on the cost kind: the same
@@ -1369,7 +1402,8 @@ __device__ void price_d1(const PriceArgs& A, const View& V, Alg alg, ef_cand_res
   }
   double t_tot = ncomp ? st.result(F.naive_sum) : 0.0;
   double e_tot = ncomp ? se.result(F.naive_sum) : 0.0;
-  double cost = cost_of<KIND>(F, t_tot, e_tot);
+  const Recip rc = recip_of(F);
+  double cost = cost_of<KIND>(F, rc, t_tot, e_tot);
   long long evals = 0;
   int sweeps = 0;
   bool running = !missing && ncomp > 0;
@@ -1399,7 +1433,7 @@ __device__ void price_d1(const PriceArgs& A, const View& V, Alg alg, ef_cand_res
           dt += qt - ct;
           de += qe - ce;
           const double nt = t_tot + dt, ne = e_tot + de;
-          const double cand = cost_of<KIND>(F, nt, ne);
+          const double cand = cost_of<KIND>(F, rc, nt, ne);
           const bool act = q != start;
           evals += act ? 1 : 0;
           const bool take = act && cand < cost;

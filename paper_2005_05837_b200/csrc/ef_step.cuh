@@ -40,6 +40,9 @@
 #ifndef EF_DIGEST_MINB
 #define EF_DIGEST_MINB 4
 #endif
+#ifndef EF_DIGEST_PF_MINB  // the prefetching digest of large rows (k_digest_pm<.., true, ..>)
+#define EF_DIGEST_PF_MINB 3  // 3 CTAs per SM without spills (DAG-20k digest 62.6 -> 56.5 ms; 4 spills: 89 ms)
+#endif
 #ifndef EF_KEYS_MINB
 #define EF_KEYS_MINB 4
 #endif
@@ -1551,15 +1554,15 @@ __global__ void k_count_scatter(const uint32_t* dcount, uint32_t n, uint32_t S, 
 }
 
 // Rows of more than 1024 fresh keys: one CTA per candidate (largest first), sorting on
-// (first 4 key bytes, big endian) << 32 | job index.  Up to R keys (the common case): a bucket
-// sort in shared memory -- the keys are node-key hashes, uniform in their first bytes, so
-// pow2(d) buckets on the top bits hold ~1 key each: a histogram, a block scan, a scatter and a
-// per-bucket insertion sort, O(d) work and four barriers instead of bitonic's log^2 d stages.
-// Beyond R keys: runs of R bitonic-sorted in shared memory, merged pairwise in the candidate's
-// two global sort rows (merge path: each thread writes a 1/BT stretch of the output).  Runs of
-// equal first 4 bytes (p ~ d^2 / 2^33 per candidate) are then ordered by the full key as in
-// k_sortkeys, and the keys are gathered into fresh_sorted with 16-byte loads and coalesced
-// 16-byte stores.  Dynamic shared memory: R words + R bucket counters.
+// (first 4 key bytes, big endian) << 32 | job index by buckets: the keys are node-key hashes,
+// uniform in their first bytes, so min(pow2(d), R) buckets on the top bits hold ~1-3 keys
+// each -- a histogram, a block scan, a scatter and a per-bucket insertion sort: O(d) work and
+// four barriers (bitonic runs and merges cost log^2 d stages: 21 of the 47 ms of the DAG-20k
+// sort stage went there).  The sorted words live in shared memory up to R keys, beyond in the
+// candidate's global sort row.  Runs of equal first 4 bytes (p ~ d^2 / 2^33 per candidate)
+// are then ordered by the full key as in k_sortkeys, and the keys are gathered into
+// fresh_sorted with 16-byte loads and coalesced 16-byte stores.  Dynamic shared memory: R
+// words + R bucket counters.
 // the end of a k_sortbig candidate: src holds (first 4 key bytes << 32 | job index) ascending;
 // runs of equal first 4 bytes are ordered by the full key, then the keys are gathered into
 // fresh_sorted (src may be shared or global memory)
@@ -1647,91 +1650,38 @@ __global__ void __launch_bounds__(BT) k_sortbig(VArgs A, uint32_t R) {
     const uint32_t lc = A.order[l];
     const uint32_t d = A.dcount[lc];
     if (d == 0) continue;  // CTA-uniform
-    uint64_t* in = A.skey + (uint64_t)lc * A.S;  // first key words (big endian); free after the runs
-    uint64_t* runs = const_cast<uint64_t*>(A.skey_sorted) + (uint64_t)lc * A.S;
-    if (d <= R) {  // bucket sort in shared memory
-      uint32_t nb = 32, lg = 5;
-      while (nb < d) nb <<= 1, ++lg;
-      const uint32_t shift = 32 - lg;
-      for (uint32_t b = tid; b < nb; b += BT) cnt[b] = 0;
-      __syncthreads();
-      for (uint32_t i = tid; i < d; i += BT) atomicAdd(cnt + (uint32_t)(in[i] >> (32 + shift)), 1u);
-      __syncthreads();
-      block_excl_scan_inplace<BT>(cnt, nb, wsum);
-      for (uint32_t i = tid; i < d; i += BT) {
-        const uint64_t v = in[i];
-        const uint32_t pos = atomicAdd(cnt + (uint32_t)(v >> (32 + shift)), 1u);
-        sbig[pos] = ((v >> 32) << 32) | i;
-      }
-      __syncthreads();
-      // cnt[b] is now the end of bucket b: order each bucket (distinct values: the index)
-      for (uint32_t b = tid; b < nb; b += BT) {
-        const uint32_t e = cnt[b], s0 = b ? cnt[b - 1] : 0u;
-        for (uint32_t x = s0 + 1; x < e; ++x) {
-          const uint64_t v = sbig[x];
-          uint32_t y = x;
-          while (y > s0 && sbig[y - 1] > v) {
-            sbig[y] = sbig[y - 1];
-            --y;
-          }
-          sbig[y] = v;
-        }
-      }
-      __syncthreads();
-      sort_finish<BT>(A, lc, d, sbig);
-      continue;
+    const uint64_t* in = A.skey + (uint64_t)lc * A.S;  // first key words (big endian)
+    // the sorted words: shared memory up to R keys, else the candidate's global sort row (L2)
+    uint64_t* dst = d <= R ? sbig : const_cast<uint64_t*>(A.skey_sorted) + (uint64_t)lc * A.S;
+    uint32_t nb = 32, lg = 5;
+    while (nb < d && nb < R) nb <<= 1, ++lg;
+    const uint32_t shift = 64 - lg;  // bucket = top lg bits of the first key word
+    for (uint32_t b = tid; b < nb; b += BT) cnt[b] = 0;
+    __syncthreads();
+    for (uint32_t i = tid; i < d; i += BT) atomicAdd(cnt + (uint32_t)(in[i] >> shift), 1u);
+    __syncthreads();
+    block_excl_scan_inplace<BT>(cnt, nb, wsum);
+    for (uint32_t i = tid; i < d; i += BT) {
+      const uint64_t v = in[i];
+      const uint32_t pos = atomicAdd(cnt + (uint32_t)(v >> shift), 1u);
+      dst[pos] = ((v >> 32) << 32) | i;
     }
-    for (uint32_t r0 = 0; r0 < d; r0 += R) {
-      const uint32_t len = min(R, d - r0);
-      uint32_t m = 2;
-      while (m < len) m <<= 1;
-      for (uint32_t i = tid; i < m; i += BT) sbig[i] = i < len ? ((in[r0 + i] >> 32) << 32) | (r0 + i) : ~0ull;
-      __syncthreads();
-      for (uint32_t k = 2; k <= m; k <<= 1) {
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-          for (uint32_t p = tid; p < (m >> 1); p += BT) {
-            const uint32_t i = 2 * p - (p & (j - 1));  // the pair (i, i + j), bit j of i clear
-            const uint64_t a = sbig[i], b = sbig[i + j];
-            if ((a > b) == ((i & k) == 0)) {
-              sbig[i] = b;
-              sbig[i + j] = a;
-            }
-          }
-          __syncthreads();
+    __syncthreads();
+    // cnt[b] is now the end of bucket b: order each bucket (distinct values: the index)
+    for (uint32_t b = tid; b < nb; b += BT) {
+      const uint32_t e = cnt[b], s0 = b ? cnt[b - 1] : 0u;
+      for (uint32_t x = s0 + 1; x < e; ++x) {
+        const uint64_t v = dst[x];
+        uint32_t y = x;
+        while (y > s0 && dst[y - 1] > v) {
+          dst[y] = dst[y - 1];
+          --y;
         }
+        dst[y] = v;
       }
-      for (uint32_t i = tid; i < len; i += BT) runs[r0 + i] = sbig[i];
-      __syncthreads();
     }
-    uint64_t* src = runs;
-    uint64_t* dst = in;
-    for (uint32_t w = R; w < d; w <<= 1) {  // pairwise merges of the sorted runs
-      for (uint32_t a0 = 0; a0 < d; a0 += 2 * w) {
-        const uint32_t na = min(w, d - a0);
-        const uint32_t nb = a0 + w < d ? min(w, d - a0 - w) : 0u;
-        const uint64_t* Ap = src + a0;
-        const uint64_t* Bp = Ap + na;
-        uint64_t* O = dst + a0;
-        const uint32_t tot = na + nb, per = (tot + BT - 1) / BT;
-        const uint32_t D = min(tot, per * tid), E = min(tot, D + per);
-        uint32_t lo = D > nb ? D - nb : 0u, hi = min(D, na);
-        while (lo < hi) {  // values are distinct (the job index is in the low word)
-          const uint32_t mid = (lo + hi) >> 1;
-          if (Ap[mid] < Bp[D - mid - 1]) lo = mid + 1;
-          else hi = mid;
-        }
-        uint32_t i = lo, j = D - lo;
-        for (uint32_t o = D; o < E; ++o) {
-          const bool ta = j >= nb || (i < na && Ap[i] < Bp[j]);
-          O[o] = ta ? Ap[i++] : Bp[j++];
-        }
-      }
-      __syncthreads();
-      uint64_t* t = src;
-      src = dst;
-      dst = t;
-    }
-    sort_finish<BT>(A, lc, d, src);
+    __syncthreads();
+    sort_finish<BT>(A, lc, d, dst);
   }
 }
 
@@ -2096,14 +2046,17 @@ __global__ void __launch_bounds__(WARPS * 32, EF_MERGE_MINB) k_merge(VArgs A, ui
 // lane k finds where the k-th 1/32 of the output starts with one binary search on its
 // diagonal (A addressed by kept index through per-word kept counts in shared memory), then
 // merges its stretch sequentially.  O(n + d) per candidate instead of a binary search per key.
-// Dynamic shared memory: per warp, W + 1 words.
+// The lanes' outputs go through a per-warp shared-memory stage, 8 keys per lane, and leave as
+// 128-byte runs (four lanes' stretches per store instruction) instead of 32 scattered 16-byte
+// stores.  Dynamic shared memory: per warp, 4.5 KB of stage + W + 1 words.
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_merge_big(VArgs A) {
-  extern __shared__ uint32_t mb_smem[];
+  extern __shared__ uint4 mb_stage[];
   const Geo& G = A.g;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned full = 0xffffffffu;
-  uint32_t* cumk = mb_smem + (uint64_t)w * (A.W + 1);  // kept parent keys before word x
+  uint4* stage = mb_stage + (uint64_t)w * 288;  // [32 lanes][8 keys + 1 pad: conflict-free 16-byte stores]
+  uint32_t* cumk = reinterpret_cast<uint32_t*>(mb_stage + (uint64_t)WARPS * 288) + (uint64_t)w * (A.W + 1);
   for (uint32_t lc = blockIdx.x * WARPS + w; lc < A.n; lc += gridDim.x * WARPS) {  // warp-uniform
     const uint32_t c = A.c0 + lc;
     if (A.res[c].flags & EF_F_INCOMPLETE) continue;
@@ -2194,30 +2147,45 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge_big(VArgs A) {
     if (j < d) b_key(j, b0, b1);
     uint4 bn0 = j + 1 < d ? b4[j + 1] : z4;
     uint4* o4 = reinterpret_cast<uint4*>(out);
-    for (uint32_t o = D; o < end; ++o) {
-      const bool take_a = j >= d || (i < na && !be_less(b0, b1, a0, a1));
-      if (take_a) {
-        const uint64_t w0 = B2b::bswap64(a0), w1 = B2b::bswap64(a1);
-        o4[o] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
-        if (++i < na) {
-          a0 = B2b::bswap64(((uint64_t)an0.y << 32) | an0.x);
-          a1 = B2b::bswap64(((uint64_t)an0.w << 32) | an0.z);
-          an0 = an1;
-          an1 = an2;
-          an2 = an3;
-          an3 = i + 4 < na ? a_raw(next_rank()) : z4;
-        }
-      } else {
-        const uint64_t w0 = B2b::bswap64(b0), w1 = B2b::bswap64(b1);
-        o4[o] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
-        if (++j < d) {
-          b0 = B2b::bswap64(((uint64_t)bn0.y << 32) | bn0.x);
-          b1 = B2b::bswap64(((uint64_t)bn0.w << 32) | bn0.z);
-          bn0 = j + 1 < d ? b4[j + 1] : z4;
+    const uint32_t mine = end - D;  // this lane's outputs (per, or fewer at the tail)
+    for (uint32_t t0 = 0; t0 < per; t0 += 8) {  // warp-uniform trip count
+#pragma unroll
+      for (uint32_t k = 0; k < 8; ++k) {
+        if (t0 + k < mine) {
+          const bool take_a = j >= d || (i < na && !be_less(b0, b1, a0, a1));
+          if (take_a) {
+            const uint64_t w0 = B2b::bswap64(a0), w1 = B2b::bswap64(a1);
+            stage[lane * 9 + k] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
+            if (++i < na) {
+              a0 = B2b::bswap64(((uint64_t)an0.y << 32) | an0.x);
+              a1 = B2b::bswap64(((uint64_t)an0.w << 32) | an0.z);
+              an0 = an1;
+              an1 = an2;
+              an2 = an3;
+              an3 = i + 4 < na ? a_raw(next_rank()) : z4;
+            }
+          } else {
+            const uint64_t w0 = B2b::bswap64(b0), w1 = B2b::bswap64(b1);
+            stage[lane * 9 + k] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
+            if (++j < d) {
+              b0 = B2b::bswap64(((uint64_t)bn0.y << 32) | bn0.x);
+              b1 = B2b::bswap64(((uint64_t)bn0.w << 32) | bn0.z);
+              bn0 = j + 1 < d ? b4[j + 1] : z4;
+            }
+          }
         }
       }
+      __syncwarp();
+      // the stage out: round q stores the 8 keys of lanes 4q .. 4q + 3, 128 contiguous bytes each
+      const uint32_t cnt = mine > t0 ? min(8u, mine - t0) : 0u;
+#pragma unroll
+      for (uint32_t q = 0; q < 8; ++q) {
+        const uint32_t src = 4 * q + ((uint32_t)lane >> 3), k = (uint32_t)lane & 7u;
+        const uint32_t c_src = __shfl_sync(full, cnt, src), o_src = __shfl_sync(full, D + t0, src);
+        if (k < c_src) o4[o_src + k] = stage[src * 9 + k];
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
 }
 
@@ -3039,6 +3007,34 @@ __global__ void __launch_bounds__(128) k_b2b_peak(uint64_t* out, int iters) {
   uint64_t x = 0;
   for (int i = 0; i < 8; ++i) x ^= h[i];
   out[blockIdx.x * blockDim.x + threadIdx.x] = x;
+}
+
+// div_pre (the pricing's division by a normalisation reference) against the IEEE division:
+// n random dividends per divisor -- uniform exponents in [-500, 500] and random significands,
+// every 4th one with an all-ones / all-zeros low significand (the rounding boundaries) -- plus
+// zeros; a mismatch is any bit difference
+__global__ void k_div_check(const double* ys, uint32_t nys, uint64_t n, uint64_t seed,
+                            unsigned long long* mismatches) {
+  unsigned long long bad = 0;
+  const uint64_t total = n * nys;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+    const double y = ys[t % nys];
+    uint64_t z = (t + 1) * 0x9e3779b97f4a7c15ULL ^ seed;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    z ^= z >> 31;
+    uint64_t mant = z & 0xfffffffffffffULL;
+    const uint32_t sel = (uint32_t)(z >> 52) & 3u;
+    if (sel == 1) mant |= 0xffffffULL;                  // low bits all ones
+    if (sel == 2) mant &= ~0xffffffULL;                 // low bits all zeros
+    const int64_t ex = (int64_t)((z >> 54) % 1001) - 500 + 1023;
+    double x = __longlong_as_double((long long)(((uint64_t)ex << 52) | mant));
+    if ((t & 1023) == 7) x = 0.0;
+    if (z >> 63) x = -x;
+    const double got = div_pre(x, y, rcp_or_zero(y)), want = x / y;
+    bad += __double_as_longlong(got) != __double_as_longlong(want);
+  }
+  if (bad) atomicAdd(mismatches, bad);
 }
 
 }  // namespace ef

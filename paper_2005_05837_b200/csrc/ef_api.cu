@@ -21,6 +21,7 @@ constexpr int kMatThreads = 256;
 constexpr int kHashThreads = 128;
 constexpr int kPriceThreads = EF_PRICE_THREADS;
 constexpr uint32_t kFastRows = 256;  // rows (max parent nodes + 2) served by the fast step kernels
+constexpr uint32_t kPrefixMinOuts = 64;  // graph outputs from which k_prefix builds the digest's prefix
 
 template <typename T>
 struct DevBuf {
@@ -79,14 +80,14 @@ struct Scratch {
   DevBuf<uint32_t> didx, jv, refsrc, dcount, dorder, sval2, rmask, outsrc, cbins;
   DevBuf<Job> jobs;
   DevBuf<uint16_t> jlvl;
-  DevBuf<uint64_t> fresh, fresh2, skey, skey2, merged;
+  DevBuf<uint64_t> fresh, fresh2, skey, skey2, merged, pfx;
   DevBuf<int32_t> seg_b, seg_e;
   DevBuf<uint32_t> recmax;
   void release() {
     jlvl.release();
     merged.release();
     didx.release(); jv.release(); refsrc.release(); dcount.release(); dorder.release(); cbins.release();
-    sval2.release(); rmask.release(); outsrc.release(); jobs.release();
+    sval2.release(); rmask.release(); outsrc.release(); jobs.release(); pfx.release();
     fresh.release(); fresh2.release(); skey.release(); skey2.release(); seg_b.release(); seg_e.release();
     recmax.release();
   }
@@ -102,11 +103,11 @@ struct ef_ctx {
   bool big_merge = true;  // rows > 256: merge-path key stream + streaming digest (EF_BIG_MERGE=0: in-thread merge)
   uint32_t wide_min = 512;  // jobs per candidate from which k_keys_wide takes it (EF_WIDE_MIN; 0: off)
   bool dirty_big = true;  // rows > kFastRows: k_dirty_big (warp window walk); EF_DIRTY_BIG=0: k_dirty
-  uint32_t wide_lpc = 16;  // lanes per candidate in k_keys_wide: 32, 16, 8 or 4 (EF_WIDE_LPC)
+  uint32_t wide_lpc = 8;  // lanes per candidate in k_keys_wide: 32, 16, 8 or 4 (EF_WIDE_LPC; DAG-20k keys 70.8 -> 63.9 ms from 16 to 8, 85.3 at 4)
   bool fuse_merge = false;  // rows > kFastRows: k_digest_mg merges on the fly (EF_FUSE_MERGE=1; measured slower: 52.9 vs 12.0 + 38.5 ms on DAG-20k)
   bool digest_pf = true;  // rows > kFastRows: k_digest_pm loads the next block's key words ahead (EF_DIGEST_PF)
   uint32_t quad_max = 20000;  // chunks below this many candidates hash with k_keys_quad (EF_QUAD_MAX)
-  uint64_t chunk_mib = 0;  // per-chunk hashing scratch budget, MiB (0: half the free HBM, <= 96 GiB)
+  uint64_t chunk_mib = 0;  // per-chunk hashing scratch budget, MiB (0: 80% of the HBM free at the first sizing, <= 144 GiB)
 
   // host mirrors of the tables
   std::vector<ef_sig_desc> sig_desc;
@@ -185,11 +186,15 @@ struct ef_ctx {
   // speculative pricing (rows > kFastRows): every complete candidate priced on st_price while
   // the chunks hash, the survivors' prices committed after the dedup (EF_SPEC_PRICE: 0 off,
   // 1 from the first digest on, 2 from the plans on; the side stream has the lowest priority, so
-  // its CTAs fill what the hashing kernels leave free.  DAG-20k 211.9 -> 206.7 ms per step with 2,
-  // 219.7 with 1; Inception-v3 (rows <= 1024) 9.11 -> 9.55 / 9.61 ms: many short candidates
-  // keep every SM busy, and pricing there only competes)
-  int spec_price = 2;
-  uint32_t spec_min_rows = 2048;  // rows (S) above which a step prices speculatively (EF_SPEC_MIN_ROWS)
+  // its CTAs fill what the hashing kernels leave free.  Measured per step: DAG-20k 211.9 -> 206.7
+  // ms from the plans, 219.7 from the digest; DAG-5k 41.4 -> 39.3 from the plans; DAG-1k 14.9 ->
+  // 13.8 and NasNet-A 10.9 -> 10.5 from the digest (15.9 / 13.1 from the plans); Inception-v3
+  // (187k candidates) 9.11 -> 9.55 from the digest: enough short candidates keep every SM busy,
+  // and pricing there only competes)
+  int spec_price = -1;             // -1: by row size and candidate count (below), 0 off, 1 / 2 / 3 forced
+  int spec_mode = 0;               // this step's launch point (1 digest, 2 plans, 3 node keys; 0: none)
+  uint32_t spec_min_rows = 2048;   // rows (S) from which the auto policy prices from the plans on
+  uint32_t spec_max_cands = 131072;  // rows of 257..2048: from the first digest on, up to this many candidates
   const ef_price_params* spec_pp = nullptr;  // set by ef_expand for step_hash
   bool spec_live = false;                    // this step's speculative pricing was launched
   cudaStream_t st_price = nullptr;
@@ -304,6 +309,7 @@ ef_ctx* ef_create(int device) {
   if (const char* e = getenv("EF_FUSE_MERGE")) ctx->fuse_merge = atoi(e) != 0;
   if (const char* e = getenv("EF_SPEC_PRICE")) ctx->spec_price = atoi(e);
   if (const char* e = getenv("EF_SPEC_MIN_ROWS")) ctx->spec_min_rows = (uint32_t)strtoul(e, nullptr, 10);
+  if (const char* e = getenv("EF_SPEC_MAX_CANDS")) ctx->spec_max_cands = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_DIGEST_PF")) ctx->digest_pf = atoi(e) != 0;
   if (const char* e = getenv("EF_QUAD_MAX")) ctx->quad_max = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_CHUNK_MIB")) ctx->chunk_mib = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
@@ -1334,11 +1340,14 @@ static int ensure_chunk(ef_ctx* ctx, Scratch& sc, cudaStream_t st, uint32_t item
   if (!ctx->chunk_mib) {  // a share of the HBM free when the first chunk is sized (EF_CHUNK_MIB overrides)
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
-    ctx->chunk_mib = std::min<uint64_t>(128ull << 10, std::max<uint64_t>(1024, (uint64_t)(0.7 * (double)fr) >> 20));
+    ctx->chunk_mib = std::min<uint64_t>(144ull << 10, std::max<uint64_t>(1024, (uint64_t)(0.8 * (double)fr) >> 20));
   }
   uint64_t ch = std::max<uint64_t>(256, (ctx->chunk_mib << 20) / per);
-  ch = std::min<uint64_t>(ch, std::max<uint32_t>(items, 1));
   ch = std::min<uint64_t>(ch, (uint64_t)INT32_MAX / S);
+  // equal chunks: a full chunk and a small remainder would run the remainder's kernels at a
+  // fraction of the GPU for a whole per-candidate latency (DAG-20k, 9 parents: 84k + 7.5k)
+  const uint64_t nch = (std::max<uint32_t>(items, 1) + ch - 1) / ch;
+  ch = (std::max<uint32_t>(items, 1) + nch - 1) / nch;
   *chunk = (uint32_t)ch;
   if (!lean) {
     EF_CUDA(sc.didx.reserve(ch * S, st));
@@ -1499,8 +1508,11 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       EF_CUDA(cudaGetLastError());
     }
     ctx->spec_live = false;
-    if (S <= ctx->spec_min_rows) ctx->spec_pp = nullptr;  // small rows: price after the dedup
-    if (ctx->spec_pp && ctx->spec_price == 2 && (rc = launch_spec_price(ctx, total))) return rc;
+    ctx->spec_mode = !ctx->spec_pp ? 0
+                     : ctx->spec_price > 0 ? ctx->spec_price
+                     : S > ctx->spec_min_rows ? 2
+                     : (S > kFastRows && total <= ctx->spec_max_cands) ? 1 : 0;
+    if (ctx->spec_mode == 2 && (rc = launch_spec_price(ctx, total))) return rc;
     cudaEventRecord(ctx->ev[2], ctx->st);
     VArgs V = chunk_args(ctx, sc, S, Rs, lean);
     V.parent_addr = A.parent_addr;
@@ -1510,6 +1522,14 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
     V.Os = ctx->h_scalars[8] + 2;
     EF_CUDA(sc.outsrc.reserve((uint64_t)chunk * V.Os, ctx->st));
     V.outsrc = sc.outsrc.p;
+    // graphs with many outputs (large rows): the digest's prefix built by k_prefix
+    const bool pfx = S > kFastRows && ctx->big_merge && !ctx->fuse_merge && ctx->digest_pf && ctx->h_scalars[8] >= kPrefixMinOuts;
+    V.pfx = nullptr;
+    if (pfx) {
+      V.pfx_stride = (uint32_t)(((uint64_t)ctx->input_text.size() + 18ull * ctx->h_scalars[8] + 7) / 8 + 2) & ~1u;
+      EF_CUDA(sc.pfx.reserve((uint64_t)chunk * V.pfx_stride, ctx->st));
+      V.pfx = sc.pfx.p;
+    }
     ctx->n_chunks = 0;
     for (uint32_t c0 = 0; c0 < total; c0 += chunk) {
       V.c0 = c0;
@@ -1543,6 +1563,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       }
       EF_CUDA(cudaGetLastError());
       if ((rc = order_by_count(ctx, sc, ctx->st, V.n, S))) return rc;
+      if (ctx->spec_mode == 3 && (rc = launch_spec_price(ctx, total))) return rc;  // beside the node keys
       cudaEventRecord(ce[1], ctx->st);
       if ((rc = launch_keys(ctx, ctx->st, V))) return rc;
       cudaEventRecord(ce[2], ctx->st);
@@ -1564,16 +1585,20 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
         ++ctx->kcount, k_digest_pm<kHashThreads, false, EF_DIGEST_MINB><<<gd, kHashThreads, 0, ctx->st>>>(V);
       } else {
         if ((rc = sort_fresh_keys(ctx, sc, ctx->st, V))) return rc;
-        if (ctx->spec_pp && (rc = launch_spec_price(ctx, total))) return rc;  // under the digest
+        if (ctx->spec_mode && (rc = launch_spec_price(ctx, total))) return rc;  // under the digest
         if (ctx->big_merge && ctx->fuse_merge) {  // the digest merges the two sorted streams itself
           cudaEventRecord(ce[3], ctx->st);
           ++ctx->kcount, k_digest_mg<kHashThreads, 2><<<gd, kHashThreads, 0, ctx->st>>>(V);
         } else if (ctx->big_merge) {  // merge-path key stream, then the streaming digest
-          const size_t smem = 4ull * (4608 + 4 * (V.W + 1));  // per warp: the output stage + kept counts
+          const size_t smem = 4ull * (4608 + 4 * (2 * V.W + 2));  // per warp: the output stage, kept counts, removed mask
           EF_CUDA(cudaFuncSetAttribute(k_merge_big<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
           const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
           ++ctx->kcount, k_merge_big<4><<<gm, 128, smem, ctx->st>>>(V);
           EF_CUDA(cudaGetLastError());
+          if (V.pfx) {
+            const uint32_t gpx = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
+            ++ctx->kcount, k_prefix<<<gpx, 128, 0, ctx->st>>>(V);
+          }
           cudaEventRecord(ce[3], ctx->st);
           if (ctx->digest_pf) ++ctx->kcount, k_digest_pm<kHashThreads, true, EF_DIGEST_PF_MINB><<<gd, kHashThreads, 0, ctx->st>>>(V);
           else ++ctx->kcount, k_digest_pm<kHashThreads, false, EF_DIGEST_MINB><<<gd, kHashThreads, 0, ctx->st>>>(V);
@@ -1683,7 +1708,7 @@ static int launch_price(ef_ctx* ctx, const ef_price_params* pp, uint32_t total, 
 // speculative pricing of every complete candidate on st_price, from where the main stream has
 // got to (step_hash calls it once per step, when ctx->spec_pp is set)
 static int launch_spec_price(ef_ctx* ctx, uint32_t total) {
-  if (!ctx->spec_pp || ctx->spec_live || !total) return EF_OK;
+  if (!ctx->spec_pp || !ctx->spec_mode || ctx->spec_live || !total) return EF_OK;
   EF_CUDA(ctx->d_spec.reserve(total, ctx->st));
   EF_CUDA(ctx->d_spec_list.reserve(total + 1, ctx->st));
   EF_CUDA(cudaEventRecord(ctx->ev_sp0, ctx->st));

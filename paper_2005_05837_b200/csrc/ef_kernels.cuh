@@ -1108,9 +1108,6 @@ __device__ double pow_py(double x, double y) {
   return r.hi + r.lo;
 }
 
-// cost.py:234-254 in the reference's operation order.  The reference always computes
-// t = time/t_ref and e = energy/e_ref first; for the time / energy / power kinds those
-// quotients are unused, so they are only formed where the result depends on them.
 // Division by a normalisation reference (cost.py:284-296: t / t_ref, e / e_ref, p / p_ref),
 // correctly rounded like the reference's float `/`, without a full division per evaluation:
 // with r = RN(1 / y) taken once per thread, q0 = RN(x r) is within 2 ulp of x / y, one FMA
@@ -1143,6 +1140,9 @@ __device__ __forceinline__ double div_pre(double x, double y, double r) {
   return x / y;
 }
 
+// cost.py:234-254 in the reference's operation order.  The reference always computes
+// t = time/t_ref and e = energy/e_ref first; for the time / energy / power kinds those
+// quotients are unused, so they are only formed where the result depends on them.
 __device__ __forceinline__ double from_totals(const ef_price_params& f, const Recip& rc, double time_ms, double energy) {
   switch (f.kind) {
     case EF_C_TIME: return time_ms;

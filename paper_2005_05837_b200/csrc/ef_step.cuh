@@ -104,6 +104,9 @@ struct VArgs {
   uint64_t* fresh_sorted;  // [n][S][2] the fresh keys in ascending byte order
   uint64_t* kstream;       // [n][S][2] the merged key stream k_digest_pm hashes (k_merge: fresh_sorted)
   const uint64_t* input_words;  // input text, 8-byte words, zero padded
+  uint64_t* pfx;       // [n][pfx_stride] the digest's prefix (input text, output keys and ports) as
+                       // little-endian words (k_prefix), or null: the digest assembles it itself
+  uint32_t pfx_stride;
   uint32_t* err;
   // full mode (whole records: uploads, kept candidates): parent_addr[c] is record c itself,
   // every node is a job, jv[c][j] = position of job j; graph hashes go to hash_out[c]
@@ -2048,7 +2051,9 @@ __global__ void __launch_bounds__(WARPS * 32, EF_MERGE_MINB) k_merge(VArgs A, ui
 // merges its stretch sequentially.  O(n + d) per candidate instead of a binary search per key.
 // The lanes' outputs go through a per-warp shared-memory stage, 8 keys per lane, and leave as
 // 128-byte runs (four lanes' stretches per store instruction) instead of 32 scattered 16-byte
-// stores.  Dynamic shared memory: per warp, 4.5 KB of stage + W + 1 words.
+// stores.  The candidate's removed-rank mask is copied to shared memory first: the lanes walk
+// their kept ranks word by word, and a dependent global load per 32 ranks was the kernel's
+// largest stall.  Dynamic shared memory: per warp, 4.5 KB of stage + 2 W + 2 words.
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_merge_big(VArgs A) {
   extern __shared__ uint4 mb_stage[];
@@ -2056,15 +2061,19 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge_big(VArgs A) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned full = 0xffffffffu;
   uint4* stage = mb_stage + (uint64_t)w * 288;  // [32 lanes][8 keys + 1 pad: conflict-free 16-byte stores]
-  uint32_t* cumk = reinterpret_cast<uint32_t*>(mb_stage + (uint64_t)WARPS * 288) + (uint64_t)w * (A.W + 1);
+  uint32_t* cumk = reinterpret_cast<uint32_t*>(mb_stage + (uint64_t)WARPS * 288) + (uint64_t)w * (2 * A.W + 2);
+  uint32_t* rm = cumk + A.W + 1;  // the removed-rank mask, in shared memory
   for (uint32_t lc = blockIdx.x * WARPS + w; lc < A.n; lc += gridDim.x * WARPS) {  // warp-uniform
     const uint32_t c = A.c0 + lc;
     if (A.res[c].flags & EF_F_INCOMPLETE) continue;
     const VPlan& P = A.plan[c];
     const uint32_t pn = (uint32_t)P.pn;
     const uint32_t d = A.dcount[lc];
-    const uint32_t* rm = A.rmask + (uint64_t)lc * A.W;
+    const uint32_t* grm = A.rmask + (uint64_t)lc * A.W;
     const uint32_t nw = (pn + 31) >> 5;
+    for (uint32_t x = lane; x < nw; x += 32) rm[x] = grm[x];
+    rm[nw] = 0u;  // the walk may look one word past the last rank
+    __syncwarp();
     // kept counts per word -> exclusive prefix
     uint32_t run = 0;
     for (uint32_t x0 = 0; x0 < nw; x0 += 32) {
@@ -2128,9 +2137,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge_big(VArgs A) {
     const uint32_t end = min(tot, D + per);
     // the A stream: kept ranks in order from the cached mask word, one key fetched ahead
     uint32_t r = i < na ? select_kept(i) : 0u;
-    uint32_t wd = r >> 5, bits = (r & 31u) == 31u ? 0u : (~__ldg(rm + wd) & ~((2u << (r & 31u)) - 1u));
+    uint32_t wd = r >> 5, bits = (r & 31u) == 31u ? 0u : (~rm[wd] & ~((2u << (r & 31u)) - 1u));
     auto next_rank = [&]() -> uint32_t {  // the kept rank after the last one handed out
-      while (!bits) bits = ~__ldg(rm + ++wd);
+      while (!bits) bits = ~rm[++wd];
       const uint32_t x = 32u * wd + (uint32_t)(__ffs(bits) - 1);
       bits &= bits - 1u;
       return x;
@@ -2189,6 +2198,81 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge_big(VArgs A) {
   }
 }
 
+// The digest's prefix for graphs with many outputs (DAG-5k / 20k: 1.2k / 4.8k outputs, a quarter
+// of the digest's blocks): the input text and every output's key and port (graph.py:541-547,
+// 18 bytes per output) as aligned little-endian words, a warp per candidate and a lane per
+// word (at most two output records per word), so the digest thread streams it like the keys
+// instead of chaining output -> source -> key loads and byte pushes.
+__global__ void __launch_bounds__(128) k_prefix(VArgs A) {
+  const Geo& G = A.g;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t li = A.T.input_text_len;
+  for (uint32_t lc = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; lc < A.n; lc += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t c = A.c0 + lc;
+    if (A.res[c].flags & EF_F_INCOMPLETE) continue;  // warp-uniform
+    const VPlan& P = A.plan[c];
+    Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
+    const uint64_t* pkeys = R.keys(G);
+    const uint32_t* pouts = R.outs(G);
+    const uint32_t n_out = (uint32_t)R.h().n_out;
+    const uint32_t* didx = A.didx + (uint64_t)lc * A.S;
+    const uint64_t* fresh = A.fresh + 2ull * lc * A.S;
+    const uint32_t* osrc = A.outsrc + (uint64_t)lc * A.Os;
+    const uint32_t n_rm = (uint32_t)P.n_rm;
+    const uint32_t rf0 = P.rm_from[0], rf1 = P.rm_from[1], rt0 = P.rm_to[0], rt1 = P.rm_to[1];
+    // output record r: its key words and big-endian port (graph.py:541-547); zero past the last
+    auto rec = [&](uint32_t r, uint64_t& k0, uint64_t& k1, uint64_t& pbe) {
+      if (r >= n_out) {
+        k0 = k1 = pbe = 0;
+        return;
+      }
+      uint32_t ref = pouts[r];
+      if (n_rm > 0 && ref == rf0) ref = rt0;  // vremap
+      else if (n_rm > 1 && ref == rf1) ref = rt1;
+      const uint64_t* kp;
+      if (A.osrc) {
+        const uint32_t sv = osrc[r], idx = sv & 0x7fffffu;
+        kp = (sv & kFresh) ? fresh + 2 * idx : pkeys + 2 * idx;
+      } else {
+        const uint32_t p = ref >> 8, fi = didx[p];
+        kp = fi ? fresh + 2 * (fi - 1) : pkeys + 2 * p;
+      }
+      k0 = kp[0];
+      k1 = kp[1];
+      pbe = port_be(ref & 255u);
+    };
+    const uint32_t len = li + 18u * n_out;
+    const uint32_t nwd = (len + 7) >> 3;
+    uint64_t* out = A.pfx + (uint64_t)lc * A.pfx_stride;
+    for (uint32_t q = lane; q < nwd; q += 32) {
+      const uint32_t x = 8u * q;
+      if (x + 8u <= li) {  // input text only
+        out[q] = __ldg(A.input_words + q);
+        continue;
+      }
+      uint32_t b = 0;  // bytes of this word taken so far
+      uint64_t wv = 0;
+      if (x < li) {  // the input text's tail (the words are zero padded)
+        b = li - x;
+        wv = __ldg(A.input_words + q) & ((1ull << (8 * b)) - 1ull);
+      }
+      // stream bytes [y, y + 8 - b) of the output records: record r from byte o, then r + 1
+      const uint32_t y = x + b - li, r = y / 18u, o = y - 18u * r;
+      uint64_t a0, a1, ap, n0 = 0, n1 = 0, np = 0;
+      rec(r, a0, a1, ap);
+      if (o + (8u - b) > 18u) rec(r + 1, n0, n1, np);
+      // the two records as little-endian words: a0 | a1 | ap + n0 << 16 | n0 >> 48 + n1 << 16
+      const uint64_t w2 = ap | (n0 << 16), w3 = (n0 >> 48) | (n1 << 16);
+      const uint32_t jw = o >> 3, sh = 8u * (o & 7u);
+      const uint64_t lo = jw == 0 ? a0 : jw == 1 ? a1 : w2;
+      const uint64_t hi = jw == 0 ? a1 : jw == 1 ? w2 : w3;
+      uint64_t v = sh ? (lo >> sh) | (hi << (64u - sh)) : lo;
+      if (b) v &= (1ull << (8 * (8 - b))) - 1ull;
+      out[q] = wv | (v << (8 * b));
+    }
+  }
+}
+
 // The graph digest over a pre-merged key stream: the prefix (input declarations, output keys
 // and ports) goes through the word sink; the keys follow as full words with a constant byte
 // shift, loaded 16 words per block with independent 16-byte loads.
@@ -2225,8 +2309,26 @@ __global__ void __launch_bounds__(BT, MINB) k_digest_pm(VArgs A) {
     b2b_start(h, 8);
     uint4 pf[9];
     uint32_t pf_kw = 0xffffffffu;
+    // the prefix from k_prefix: pw_full whole words, then pw_rem bytes
+    const uint64_t* pw = A.pfx ? A.pfx + (uint64_t)lc * A.pfx_stride : nullptr;
+    const uint32_t pw_full = (uint32_t)(((uint64_t)li + 18ull * n_out) >> 3), pw_rem = (uint32_t)((li + 18ull * n_out) & 7);
+    uint32_t pq = 0;
     for (uint32_t b = 0; b < nblk; ++b) {
       sk.q = 0;
+      if (pw && phase < 2) {  // whole prefix words (the sink is word-aligned until the last one)
+        const uint32_t take = min(16u, pw_full - pq);
+        uint64_t wv[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) wv[i] = (uint32_t)i < take ? pw[pq + i] : 0ull;
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if ((uint32_t)i < take) sk.push(wv[i], 8);
+        pq += take;
+        if (pq == pw_full && sk.q < 16) {
+          if (pw_rem) sk.push(pw[pq], pw_rem);
+          phase = 2;
+        }
+      }
       while (sk.q < 16 && phase < 2) {
         if (phase == 0) {
           if (gi * 8 < li) {

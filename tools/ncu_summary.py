@@ -11,6 +11,7 @@ ROUND_kernels.json (the metrics DESIGN.md cites, one row per captured launch).
 import csv
 import io
 import json
+import os
 import subprocess
 import sys
 from collections import defaultdict
@@ -71,8 +72,14 @@ def launches(path):
 
 
 def kernels(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
-                         capture_output=True, text=True, check=True).stdout
+    """rep: a .ncu-rep, or the `--page raw --csv` export of one (prof_raw.csv, written on the GPU
+    box when the report itself is too large to bring back)."""
+    if rep.endswith(".csv"):
+        with open(rep) as fh:
+            out = fh.read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
+                             capture_output=True, text=True, check=True).stdout
     rdr = list(csv.reader(io.StringIO(out)))
     head, units = rdr[0], rdr[1]
     rows = []
@@ -90,8 +97,9 @@ def main():
     src, dst = sys.argv[1], sys.argv[2]
     with open(dst + "_launches.json", "w") as fh:
         json.dump(launches(src + "/launches.csv"), fh, indent=1)
+    rep = src + "/prof.ncu-rep" if os.path.exists(src + "/prof.ncu-rep") else src + "/prof_raw.csv"
     with open(dst + "_kernels.json", "w") as fh:
-        json.dump(kernels(src + "/prof.ncu-rep"), fh, indent=1)
+        json.dump(kernels(rep), fh, indent=1)
 
 
 if __name__ == "__main__":

@@ -195,6 +195,8 @@ struct ef_ctx {
   int spec_mode = 0;               // this step's launch point (1 digest, 2 plans, 3 node keys; 0: none)
   uint32_t spec_min_rows = 2048;   // rows (S) from which the auto policy prices from the plans on
   uint32_t spec_max_cands = 131072;  // rows of 257..2048: from the first digest on, up to this many candidates
+  uint32_t spec_min_cands = 32768;   // and never below this many: a search's small steps price mostly
+                                     // visited duplicates speculatively (NasNet-A search 5.5 -> 6.4 s)
   const ef_price_params* spec_pp = nullptr;  // set by ef_expand for step_hash
   bool spec_live = false;                    // this step's speculative pricing was launched
   cudaStream_t st_price = nullptr;
@@ -310,6 +312,7 @@ ef_ctx* ef_create(int device) {
   if (const char* e = getenv("EF_SPEC_PRICE")) ctx->spec_price = atoi(e);
   if (const char* e = getenv("EF_SPEC_MIN_ROWS")) ctx->spec_min_rows = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_SPEC_MAX_CANDS")) ctx->spec_max_cands = (uint32_t)strtoul(e, nullptr, 10);
+  if (const char* e = getenv("EF_SPEC_MIN_CANDS")) ctx->spec_min_cands = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_DIGEST_PF")) ctx->digest_pf = atoi(e) != 0;
   if (const char* e = getenv("EF_QUAD_MAX")) ctx->quad_max = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_CHUNK_MIB")) ctx->chunk_mib = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
@@ -405,6 +408,8 @@ void ef_destroy(ef_ctx* ctx) {
   if (ctx->ev_sp1) cudaEventDestroy(ctx->ev_sp1);
   ctx->d_spec.release();
   ctx->d_spec_list.release();
+  ctx->d_upd_sig.release();
+  ctx->d_upd_dv.release();
   if (ctx->ev_w0) cudaEventDestroy(ctx->ev_w0);
   if (ctx->ev_w1) cudaEventDestroy(ctx->ev_w1);
   if (ctx->st_copy) cudaStreamDestroy(ctx->st_copy);
@@ -1510,6 +1515,8 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
     ctx->spec_live = false;
     ctx->spec_mode = !ctx->spec_pp ? 0
                      : ctx->spec_price > 0 ? ctx->spec_price
+                     : total < ctx->spec_min_cands ? 0
+                     : S > 4 * ctx->spec_min_rows ? 3  // DAG-20k: 194.9 -> 192.0 ms beside the node keys
                      : S > ctx->spec_min_rows ? 2
                      : (S > kFastRows && total <= ctx->spec_max_cands) ? 1 : 0;
     if (ctx->spec_mode == 2 && (rc = launch_spec_price(ctx, total))) return rc;
@@ -1590,7 +1597,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
           cudaEventRecord(ce[3], ctx->st);
           ++ctx->kcount, k_digest_mg<kHashThreads, 2><<<gd, kHashThreads, 0, ctx->st>>>(V);
         } else if (ctx->big_merge) {  // merge-path key stream, then the streaming digest
-          const size_t smem = 4ull * (4608 + 4 * (2 * V.W + 2));  // per warp: the output stage, kept counts, removed mask
+          const size_t smem = 4ull * (2560 + 4 * (2 * V.W + 2));  // per warp: the output stage, kept counts, removed mask
           EF_CUDA(cudaFuncSetAttribute(k_merge_big<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
           const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
           ++ctx->kcount, k_merge_big<4><<<gm, 128, smem, ctx->st>>>(V);

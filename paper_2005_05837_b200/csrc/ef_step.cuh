@@ -2049,19 +2049,20 @@ __global__ void __launch_bounds__(WARPS * 32, EF_MERGE_MINB) k_merge(VArgs A, ui
 // lane k finds where the k-th 1/32 of the output starts with one binary search on its
 // diagonal (A addressed by kept index through per-word kept counts in shared memory), then
 // merges its stretch sequentially.  O(n + d) per candidate instead of a binary search per key.
-// The lanes' outputs go through a per-warp shared-memory stage, 8 keys per lane, and leave as
-// 128-byte runs (four lanes' stretches per store instruction) instead of 32 scattered 16-byte
+// The lanes' outputs go through a per-warp shared-memory stage, 4 keys per lane, and leave as
+// 64-byte runs (eight lanes' stretches per store instruction) instead of 32 scattered 16-byte
 // stores.  The candidate's removed-rank mask is copied to shared memory first: the lanes walk
 // their kept ranks word by word, and a dependent global load per 32 ranks was the kernel's
-// largest stall.  Dynamic shared memory: per warp, 4.5 KB of stage + 2 W + 2 words.
+// largest stall.  Dynamic shared memory: per warp, 2.5 KB of stage + 2 W + 2 words.
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_merge_big(VArgs A) {
   extern __shared__ uint4 mb_stage[];
   const Geo& G = A.g;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned full = 0xffffffffu;
-  uint4* stage = mb_stage + (uint64_t)w * 288;  // [32 lanes][8 keys + 1 pad: conflict-free 16-byte stores]
-  uint32_t* cumk = reinterpret_cast<uint32_t*>(mb_stage + (uint64_t)WARPS * 288) + (uint64_t)w * (2 * A.W + 2);
+  constexpr uint32_t MK = 4, MS = MK + 1;  // keys per lane per flush; stage row stride (+1: conflict-free 16-byte stores)
+  uint4* stage = mb_stage + (uint64_t)w * 32 * MS;  // [32 lanes][MK keys + pad]
+  uint32_t* cumk = reinterpret_cast<uint32_t*>(mb_stage + (uint64_t)WARPS * 32 * MS) + (uint64_t)w * (2 * A.W + 2);
   uint32_t* rm = cumk + A.W + 1;  // the removed-rank mask, in shared memory
   for (uint32_t lc = blockIdx.x * WARPS + w; lc < A.n; lc += gridDim.x * WARPS) {  // warp-uniform
     const uint32_t c = A.c0 + lc;
@@ -2157,14 +2158,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge_big(VArgs A) {
     uint4 bn0 = j + 1 < d ? b4[j + 1] : z4;
     uint4* o4 = reinterpret_cast<uint4*>(out);
     const uint32_t mine = end - D;  // this lane's outputs (per, or fewer at the tail)
-    for (uint32_t t0 = 0; t0 < per; t0 += 8) {  // warp-uniform trip count
+    for (uint32_t t0 = 0; t0 < per; t0 += MK) {  // warp-uniform trip count
 #pragma unroll
-      for (uint32_t k = 0; k < 8; ++k) {
+      for (uint32_t k = 0; k < MK; ++k) {
         if (t0 + k < mine) {
           const bool take_a = j >= d || (i < na && !be_less(b0, b1, a0, a1));
           if (take_a) {
             const uint64_t w0 = B2b::bswap64(a0), w1 = B2b::bswap64(a1);
-            stage[lane * 9 + k] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
+            stage[lane * MS + k] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
             if (++i < na) {
               a0 = B2b::bswap64(((uint64_t)an0.y << 32) | an0.x);
               a1 = B2b::bswap64(((uint64_t)an0.w << 32) | an0.z);
@@ -2175,7 +2176,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge_big(VArgs A) {
             }
           } else {
             const uint64_t w0 = B2b::bswap64(b0), w1 = B2b::bswap64(b1);
-            stage[lane * 9 + k] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
+            stage[lane * MS + k] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
             if (++j < d) {
               b0 = B2b::bswap64(((uint64_t)bn0.y << 32) | bn0.x);
               b1 = B2b::bswap64(((uint64_t)bn0.w << 32) | bn0.z);
@@ -2186,12 +2187,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge_big(VArgs A) {
       }
       __syncwarp();
       // the stage out: round q stores the 8 keys of lanes 4q .. 4q + 3, 128 contiguous bytes each
-      const uint32_t cnt = mine > t0 ? min(8u, mine - t0) : 0u;
+      const uint32_t cnt = mine > t0 ? min(MK, mine - t0) : 0u;
 #pragma unroll
-      for (uint32_t q = 0; q < 8; ++q) {
-        const uint32_t src = 4 * q + ((uint32_t)lane >> 3), k = (uint32_t)lane & 7u;
+      for (uint32_t q = 0; q < MK; ++q) {
+        const uint32_t src = (32 / MK) * q + (uint32_t)lane / MK, k = (uint32_t)lane % MK;
         const uint32_t c_src = __shfl_sync(full, cnt, src), o_src = __shfl_sync(full, D + t0, src);
-        if (k < c_src) o4[o_src + k] = stage[src * 9 + k];
+        if (k < c_src) o4[o_src + k] = stage[src * MS + k];
       }
       __syncwarp();
     }

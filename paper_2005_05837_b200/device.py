@@ -148,6 +148,15 @@ class DeviceSession:
         self._apinned, self._apinned_bytes = None, 0  # the same for results_async
 
     @classmethod
+    def reset_default(cls) -> None:
+        """Destroy the process's default session (its tables, records and hashing scratch: a
+        large-graph step sizes that scratch to most of the HBM); the next default() is fresh."""
+        with cls._lock:
+            if cls._default is not None:
+                cls._default.close()
+                cls._default = None
+
+    @classmethod
     def default(cls) -> "DeviceSession":
         with cls._lock:
             if cls._default is None:

@@ -2054,8 +2054,11 @@ __global__ void __launch_bounds__(WARPS * 32, EF_MERGE_MINB) k_merge(VArgs A, ui
 // stores.  The candidate's removed-rank mask is copied to shared memory first: the lanes walk
 // their kept ranks word by word, and a dependent global load per 32 ranks was the kernel's
 // largest stall.  Dynamic shared memory: per warp, 2.5 KB of stage + 2 W + 2 words.
+#ifndef EF_MERGE_BIG_MINB  // CTAs per SM the merge's register budget is sized for
+#define EF_MERGE_BIG_MINB 1
+#endif
 template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_merge_big(VArgs A) {
+__global__ void __launch_bounds__(WARPS * 32, EF_MERGE_BIG_MINB) k_merge_big(VArgs A) {
   extern __shared__ uint4 mb_stage[];
   const Geo& G = A.g;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

@@ -191,8 +191,8 @@ struct ef_ctx {
   // 13.8 and NasNet-A 10.9 -> 10.5 from the digest (15.9 / 13.1 from the plans); Inception-v3
   // (187k candidates) 9.11 -> 9.55 from the digest: enough short candidates keep every SM busy,
   // and pricing there only competes)
-  int spec_price = -1;             // -1: by row size and candidate count (below), 0 off, 1 / 2 / 3 forced
-  int spec_mode = 0;               // this step's launch point (1 digest, 2 plans, 3 node keys; 0: none)
+  int spec_price = -1;             // -1: by row size and candidate count (below), 0 off, 1 .. 4 forced
+  int spec_mode = 0;               // this step's launch point (1 digest, 2 plans, 3 node keys, 4 key sort; 0: none)
   uint32_t spec_min_rows = 2048;   // rows (S) from which the auto policy prices from the plans on
   uint32_t spec_max_cands = 131072;  // rows of 257..2048: from the first digest on, up to this many candidates
   uint32_t spec_min_cands = 32768;   // and never below this many: a search's small steps price mostly
@@ -1516,7 +1516,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
     ctx->spec_mode = !ctx->spec_pp ? 0
                      : ctx->spec_price > 0 ? ctx->spec_price
                      : total < ctx->spec_min_cands ? 0
-                     : S > 4 * ctx->spec_min_rows ? 3  // DAG-20k: 194.9 -> 192.0 ms beside the node keys
+                     : S > 4 * ctx->spec_min_rows ? 4  // DAG-20k per step: 183.5 (node keys), 183.5 (digest), 179.9 ms (key sort)
                      : S > ctx->spec_min_rows ? 2
                      : (S > kFastRows && total <= ctx->spec_max_cands) ? 1 : 0;
     if (ctx->spec_mode == 2 && (rc = launch_spec_price(ctx, total))) return rc;
@@ -1591,6 +1591,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
         cudaEventRecord(ce[3], ctx->st);
         ++ctx->kcount, k_digest_pm<kHashThreads, false, EF_DIGEST_MINB><<<gd, kHashThreads, 0, ctx->st>>>(V);
       } else {
+        if (ctx->spec_mode == 4 && (rc = launch_spec_price(ctx, total))) return rc;  // beside the key sort
         if ((rc = sort_fresh_keys(ctx, sc, ctx->st, V))) return rc;
         if (ctx->spec_mode && (rc = launch_spec_price(ctx, total))) return rc;  // under the digest
         if (ctx->big_merge && ctx->fuse_merge) {  // the digest merges the two sorted streams itself

@@ -1108,13 +1108,58 @@ __global__ void __launch_bounds__(BT) k_keys_wide(VArgs A) {
         __syncwarp(gmask);  // cnt[level] is now the end of the level's run in ord
       }
     }
-    // rounds: every group takes up to LPC jobs of its current level; a level's keys are
-    // visible to the next level's lanes after the round's __syncwarp
-    uint32_t lev = 0, pos = 0, e = has ? cnt[0] : 0u;
+    // rounds: a level's keys are visible to the next level's lanes after the round's
+    // __syncwarp.  Lanes are dealt per round: every group first gets up to LPC lanes for its
+    // current level's remaining jobs, the lanes still idle then go to the groups with more than
+    // that (in group order), so a narrow level of one candidate lends its lanes to a wide level
+    // of another (fixed LPC-lane groups left 7.4 of 32 lanes idle per instruction on DAG-20k).
+    uint32_t lev = 0, pos = 0, e = has ? cnt[0] : 0u;  // the group's state, in each of its lanes
+    const uint64_t pk_bits = reinterpret_cast<uint64_t>(pkeys);
     while (__any_sync(full, lev < nl)) {
-      const uint32_t x = pos + sl;
-      if (lev < nl && x < e) {
-        const uint32_t jj = ord[x];
+      const uint32_t avail = lev < nl ? e - pos : 0u;
+      uint32_t av[GPW], tb = 0, te = 0;
+#pragma unroll
+      for (int g = 0; g < GPW; ++g) {
+        av[g] = __shfl_sync(full, avail, g * LPC);
+        tb += min(av[g], (uint32_t)LPC);
+      }
+      // this lane's job: (group g, index within the level's remaining jobs k)
+      int g_sel = -1;
+      uint32_t k_sel = 0, taken_mine = 0;
+      {
+        uint32_t bpre = 0, epre = 0;
+#pragma unroll
+        for (int g = 0; g < GPW; ++g) {
+          const uint32_t base = min(av[g], (uint32_t)LPC), extra = av[g] - base;
+          const uint32_t room = 32u > tb + epre ? 32u - tb - epre : 0u;
+          const uint32_t ex_taken = min(extra, room);
+          if (lane >= bpre && lane < bpre + base) {
+            g_sel = g;
+            k_sel = lane - bpre;
+          } else if (lane >= tb + epre && lane < tb + epre + ex_taken) {
+            g_sel = g;
+            k_sel = base + (lane - tb - epre);
+          }
+          if ((uint32_t)g == grp) taken_mine = base + ex_taken;
+          bpre += base;
+          epre += extra;
+        }
+        te = epre;
+      }
+      (void)te;
+      // the selected group's candidate, parent keys and position (from its lanes)
+      const int src_lane = (g_sel < 0 ? (int)grp : g_sel) * LPC;
+      const uint32_t lc_g = __shfl_sync(full, lc, src_lane);
+      const uint32_t pos_g = __shfl_sync(full, pos, src_lane);
+      const uint64_t pk_g = ((uint64_t)__shfl_sync(full, (uint32_t)(pk_bits >> 32), src_lane) << 32) |
+                            __shfl_sync(full, (uint32_t)pk_bits, src_lane);
+      if (g_sel >= 0) {
+        const uint64_t* pkeys = reinterpret_cast<const uint64_t*>(pk_g);
+        const Job* jobs = A.jobs + (uint64_t)lc_g * A.S;
+        const uint32_t* rs = A.refsrc + (uint64_t)lc_g * A.Rs;
+        uint64_t* fresh = A.fresh + 2ull * lc_g * A.S;
+        const uint32_t* ord = reinterpret_cast<const uint32_t*>(A.skey + (uint64_t)lc_g * A.S);
+        const uint32_t jj = ord[pos_g + k_sel];
         const Job jb = jobs[jj];
         const bool input = jb.nin & kInputJob;
         const uint32_t nin = input ? 0u : jb.nin;
@@ -1181,7 +1226,7 @@ __global__ void __launch_bounds__(BT) k_keys_wide(VArgs A) {
         fresh[2 * jj + 1] = h1;
       }
       if (lev < nl) {
-        pos += LPC;
+        pos += taken_mine;
         if (pos >= e) {
           pos = e;
           if (++lev < nl) e = cnt[lev];

@@ -191,6 +191,12 @@ struct ef_ctx {
   // 13.8 and NasNet-A 10.9 -> 10.5 from the digest (15.9 / 13.1 from the plans); Inception-v3
   // (187k candidates) 9.11 -> 9.55 from the digest: enough short candidates keep every SM busy,
   // and pricing there only competes)
+  // lanes per candidate of the d=1 sweep after the dedup (k_price_lanes; EF_PRICE_LANES, 0 / 1 =
+  // k_price_v), rows up to 2048.  Measured: Inception-v3 price 2.00 -> 1.79 ms with 2 lanes,
+  // 2.60 with 4, 4.47 with 8; ResNet-50 0.384 -> 0.372 / 0.514 / 0.902 ms: the first sweep
+  // takes at most nodes, so its windows commit one node each and the converged sweeps' L-fold
+  // parallelism only pays at 2 lanes.  DAG-20k (global rows): 28.8 -> 53.5 ms at 2 lanes.
+  uint32_t price_lanes = 2;
   int spec_price = -1;             // -1: by row size and candidate count (below), 0 off, 1 .. 4 forced
   int spec_mode = 0;               // this step's launch point (1 digest, 2 plans, 3 node keys, 4 key sort; 0: none)
   uint32_t spec_min_rows = 2048;   // rows (S) from which the auto policy prices from the plans on
@@ -310,6 +316,10 @@ ef_ctx* ef_create(int device) {
   }
   if (const char* e = getenv("EF_FUSE_MERGE")) ctx->fuse_merge = atoi(e) != 0;
   if (const char* e = getenv("EF_SPEC_PRICE")) ctx->spec_price = atoi(e);
+  if (const char* e = getenv("EF_PRICE_LANES")) {
+    const uint32_t v = (uint32_t)strtoul(e, nullptr, 10);
+    ctx->price_lanes = v >= 8 ? 8u : v >= 4 ? 4u : v >= 2 ? 2u : 0u;
+  }
   if (const char* e = getenv("EF_SPEC_MIN_ROWS")) ctx->spec_min_rows = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_SPEC_MAX_CANDS")) ctx->spec_max_cands = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_SPEC_MIN_CANDS")) ctx->spec_min_cands = (uint32_t)strtoul(e, nullptr, 10);
@@ -1701,6 +1711,26 @@ static int launch_price(ef_ctx* ctx, const ef_price_params* pp, uint32_t total, 
     }                                                                                                      \
   } while (0)
   ctx->alg_rows = fast;  // price_d1 leaves row indices (k_keep_alg reads the ids)
+  if (fast && ctx->price_lanes >= 2 && !out && ctx->step_S <= 2048) {  // a lane group per candidate (price_d1_lanes)
+    const uint32_t PL = ctx->price_lanes;
+    const uint32_t gl = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)(((uint64_t)total * PL + kPriceThreads - 1) / kPriceThreads),
+                                                                 ctx->n_sm * 32));
+    const size_t rows = (size_t)(kPriceThreads / PL) * ctx->step_S;
+    const int smrow = rows <= 48 * 1024 ? 1 : 0;
+    const size_t lsm = smrow ? rows : 0;
+#define EF_PRICE_L(K, PLC) \
+    ++ctx->kcount, k_price_lanes<K, PLC><<<gl, kPriceThreads, lsm, st>>>(Pv, pl, pn, smrow)
+#define EF_PRICE_LK(K) \
+    do { if (PL == 2) EF_PRICE_L(K, 2); else if (PL == 4) EF_PRICE_L(K, 4); else EF_PRICE_L(K, 8); } while (0)
+    if (pp->kind == EF_C_ENERGY) EF_PRICE_LK(EF_C_ENERGY);
+    else if (pp->kind == EF_C_TIME) EF_PRICE_LK(EF_C_TIME);
+    else if (pp->kind == EF_C_LINEAR) EF_PRICE_LK(EF_C_LINEAR);
+    else EF_PRICE_LK(EF_C_MIX + 1);
+#undef EF_PRICE_LK
+#undef EF_PRICE_L
+    EF_CUDA(cudaGetLastError());
+    return EF_OK;
+  }
   if (fast && !sm && !Pv.algt)  // the global rows start at row 0 (price_d1 writes changes only)
     EF_CUDA(cudaMemsetAsync(ctx->d_alg8.p, 0, (uint64_t)std::max<uint32_t>(total, 1) * ctx->step_S, st));
   if (fast && pp->kind == EF_C_ENERGY) EF_PRICE(EF_C_ENERGY);

@@ -1462,6 +1462,143 @@ __device__ void price_d1(const PriceArgs& A, const View& V, Alg alg, ef_cand_res
   res.flags |= EF_F_PRICED;
 }
 
+// price_d1 with L lanes per candidate (lanes sl = 0..L-1 of a group starting at lane gbase).
+// Every floating-point value of a candidate is computed by one lane with the operands the
+// sequential sweep has at that point, so the results are price_d1's bit for bit:
+//  * start totals: each window's L rows are loaded by the L lanes and summed in node order by
+//    every lane of the group (the Neumaier sum is order-dependent: it stays sequential);
+//  * sweeps: the L nodes of a window are evaluated at once, each against the current totals.
+//    Nodes before the window's first node that takes an alternative saw the totals the
+//    sequential sweep would have (no earlier node changed them), so they and that node are
+//    committed -- its totals, cost and row entry become the group's -- and the window restarts
+//    after it; the later nodes' evaluations are discarded.  Windows without a take commit all
+//    L nodes.  Evaluation counts are per committed node (nr - 1 each, as in price_d1).
+// Converged sweeps (usually every sweep after the first) run L nodes per step of the chain.
+template <int KIND, int L, class View, class Alg>
+__device__ void price_d1_lanes(const PriceArgs& A, const View& V, Alg alg, ef_cand_result* res, bool valid,
+                               uint32_t sl, uint32_t gbase, uint32_t skip) {
+  const Tables& T = A.T;
+  const ef_price_params& F = A.pp;
+  const Recip rc = recip_of(F);
+  const unsigned full = 0xffffffffu;
+  const int n = valid ? V.n : 0;
+  const int nmax = __reduce_max_sync(full, (unsigned)n);
+  NeumaierSum st, se;
+  st.init();
+  se.init();
+  int ncomp = 0;
+  long long skip_evals = 0;
+  bool missing = false;
+  for (int i0 = 0; i0 < nmax; i0 += L) {
+    const int i = i0 + (int)sl;
+    const uint2 inf = i < n ? V.info(i, T) : make_uint2(0u, kInfoInput);
+    const bool row = !(inf.y & kInfoInput) && (inf.y & kInfoRows);
+    const double rt = row ? T.row_t[inf.x] : 0.0, re = row ? T.row_e[inf.x] : 0.0;
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      const uint32_t y = __shfl_sync(full, inf.y, gbase + k);
+      const double xt = __shfl_sync(full, rt, gbase + k), xe = __shfl_sync(full, re, gbase + k);
+      if (i0 + k >= n || missing || (y & kInfoInput)) continue;
+      ++ncomp;
+      const uint32_t nr = y & kInfoRows;
+      if (nr == 0) {
+        missing = true;
+      } else {
+        st.add(xt);
+        se.add(xe);
+        if (skip && (y & skip) == skip) skip_evals += nr - 1;
+      }
+    }
+  }
+  double t_tot = ncomp ? st.result(F.naive_sum) : 0.0;
+  double e_tot = ncomp ? se.result(F.naive_sum) : 0.0;
+  double cost = cost_of<KIND>(F, rc, t_tot, e_tot);
+  long long evals = 0;
+  int sweeps = 0;
+  bool running = !missing && ncomp > 0;
+  while (__any_sync(full, running)) {
+    bool changed = false;
+    if (running) {
+      ++sweeps;
+      evals += skip_evals;
+    }
+    const bool first = sweeps == 1;
+    int i0 = 0;
+    while (__any_sync(full, running && i0 < n)) {
+      const bool act_w = running && i0 < n;  // group-uniform
+      const int i = i0 + (int)sl;
+      bool took = false;
+      long long my_ev = 0;
+      double lt = t_tot, le = e_tot, lc = cost;
+      uint32_t cur = 0;
+      if (act_w && i < n) {
+        const uint2 inf = V.info(i, T);
+        const uint32_t nr = inf.y & kInfoRows;
+        if (!(nr < 2u || (inf.y & kInfoInput) || (skip && (inf.y & skip) == skip))) {
+          const uint32_t ro = inf.x;
+          const uint32_t start = first ? 0u : (uint32_t)alg[i];
+          cur = start;
+          double ct = T.row_t[ro + cur], ce = T.row_e[ro + cur];
+          for (uint32_t q = 0; q < nr; ++q) {
+            const double qt = T.row_t[ro + q], qe = T.row_e[ro + q];
+            double dt = 0.0, de = 0.0;
+            dt += qt - ct;
+            de += qe - ce;
+            const double nt = lt + dt, ne = le + de;
+            const double cand = cost_of<KIND>(F, rc, nt, ne);
+            const bool act = q != start;
+            my_ev += act ? 1 : 0;
+            const bool take = act && cand < lc;
+            cur = take ? q : cur;
+            ct = take ? qt : ct;
+            ce = take ? qe : ce;
+            lt = take ? nt : lt;
+            le = take ? ne : le;
+            lc = take ? cand : lc;
+            took = took || take;
+          }
+        }
+      }
+      const unsigned tb = (__ballot_sync(full, took) >> gbase) & ((1u << L) - 1u);
+      const int f = tb ? __ffs(tb) - 1 : L;  // the window's first node that took
+      long long ev_sum = 0;
+#pragma unroll
+      for (int k = 0; k < L; ++k) {
+        const long long x = __shfl_sync(full, my_ev, gbase + k);
+        if (k <= f) ev_sum += x;
+      }
+      const int srcl = (int)gbase + (f < L ? f : 0);
+      const double nt = __shfl_sync(full, lt, srcl), ne = __shfl_sync(full, le, srcl), nc = __shfl_sync(full, lc, srcl);
+      if (act_w) {
+        evals += ev_sum;
+        if (f < L) {
+          if ((int)sl == f) alg[i] = (uint8_t)cur;
+          t_tot = nt;
+          e_tot = ne;
+          cost = nc;
+          changed = true;
+          i0 += f + 1;
+        } else {
+          i0 += L;
+        }
+      }
+      __syncwarp();  // the committed row entry is visible to the lanes that read it next
+    }
+    running = running && changed;
+  }
+  if (!valid || sl != 0) return;
+  if (missing) {
+    res->flags |= EF_F_MISSING;
+    return;
+  }
+  res->cost = cost;
+  res->time_ms = t_tot;
+  res->energy = e_tot;
+  res->evals = evals;
+  res->sweeps = sweeps;
+  res->flags |= EF_F_PRICED;
+}
+
 // the per-signature bits of a cost kind's exact skip (price_d1), given the price parameters
 template <int KIND>
 __device__ __forceinline__ uint32_t d1_skip_bits(const ef_price_params& f) {

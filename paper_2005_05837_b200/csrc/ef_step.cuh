@@ -1057,8 +1057,6 @@ __global__ void __launch_bounds__(BT) k_keys_wide(VArgs A) {
     uint32_t nl = 0, ncomp = 0;
     const uint32_t c = A.c0 + lc;
     const uint64_t* pkeys = nullptr;
-    const Job* jobs = A.jobs + (uint64_t)lc * A.S;
-    const uint32_t* rs = A.refsrc + (uint64_t)lc * A.Rs;
     const uint16_t* lv = A.jlvl + (uint64_t)lc * A.S;
     uint64_t* fresh = A.fresh + 2ull * lc * A.S;
     uint64_t* skey = A.skey + (uint64_t)lc * A.S;
@@ -2820,6 +2818,55 @@ __global__ void __launch_bounds__(EF_PRICE_THREADS) k_price_v(VPriceArgs A, cons
     } else {
       price_graph(A.pa, V, alg, res);
     }
+  }
+}
+
+// k_price_v with PL lanes per candidate (price_d1_lanes): a group of PL lanes prices one
+// candidate of the list; the sweep's row of each group lives in shared memory when `smrow`
+// (S bytes per group), else in the candidate's global alg8 row.
+template <int KIND, int PL>
+__global__ void __launch_bounds__(EF_PRICE_THREADS) k_price_lanes(VPriceArgs A, const uint32_t* plist,
+                                                                  const uint32_t* plist_n, int smrow) {
+  extern __shared__ uint8_t sm_rows[];
+  const Geo& G = A.pa.g;
+  const uint32_t total = *plist_n;
+  const uint32_t lane = threadIdx.x & 31u, sl = lane % PL, gbase = lane - sl;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  constexpr uint32_t GPW = 32 / PL;
+  uint8_t* srow = sm_rows + (uint64_t)(threadIdx.x / PL) * A.S;
+  const uint32_t skip = d1_skip_bits<KIND>(A.pa.pp);
+  for (uint32_t base = gw * GPW; base < total; base += nwarps * GPW) {  // warp-uniform
+    const uint32_t kk = base + lane / PL;
+    const bool valid = kk < total;
+    const uint32_t c = valid ? plist[kk] : 0u;
+    VirtView V{};
+    V.n = 0;
+    uint8_t* alg = A.alg8 + (uint64_t)c * A.S;
+    ef_cand_result* res = nullptr;
+    if (valid) {
+      res = A.out ? A.out + c : A.pa.res + c;
+      const VPlan& P = A.plan[c];
+      Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
+      V.psig = R.sig(G);
+      V.p_ro = A.pscratch + (uint64_t)P.parent * A.pstride + 7ull * G.cap_nodes + 1 + 2ull * G.cap_refs;
+      V.p_rn = V.p_ro + G.cap_nodes;
+      V.drop0 = P.drop0;
+      V.drop1 = P.drop1;
+      V.mod = P.mod;
+      V.n_keep = P.n_keep;
+      V.mod_sig = P.mod_sig;
+      V.s_new0 = P.live[0] ? P.new_sig[0] : P.new_sig[1];
+      V.s_new1 = P.new_sig[1];
+      V.n = P.n_keep + P.n_live;
+    }
+    uint8_t* row = smrow ? srow : alg;
+    for (int i = (int)sl; i < V.n; i += PL) row[i] = 0;  // row 0 everywhere (price_d1 writes changes only)
+    __syncwarp();
+    price_d1_lanes<KIND, PL>(A.pa, V, AlgRow{row, 1}, res, valid, sl, gbase, skip);
+    __syncwarp();
+    if (smrow)
+      for (int i = (int)sl; i < V.n; i += PL) alg[i] = row[i];
+    __syncwarp();
   }
 }
 

@@ -699,7 +699,7 @@ def main():
                     help="reference arm: seconds of oracle work per process per step")
     ap.add_argument("--sharded", action="store_true", help="use the hash-owner sharded step even on one rank")
     args = ap.parse_args()
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+    if (args.gpus > 1 or args.sharded) and "WORLD_SIZE" not in os.environ:
         return _self_launch(args.gpus)
     world, rank, local = _dist()
     if args.impl == "reference":

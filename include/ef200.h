@@ -259,6 +259,11 @@ int ef_materialise(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents
 /* match, plan and hash the candidates of the given parents (no dedup, no pricing) */
 int ef_expand_hashes(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, const int32_t* rules,
                      uint32_t n_rules, uint32_t* n_candidates);
+/* the same, pricing every complete candidate speculatively beside the hashing (large graphs,
+ * the policy of ef_expand); ef_expand_finish / ef_expand_finish_padded then take the prices of
+ * the survivors instead of pricing them */
+int ef_expand_hashes_spec(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, const int32_t* rules,
+                          uint32_t n_rules, const ef_price_params* pp, uint32_t* n_candidates);
 /* (hash, order_base + candidate index) pairs grouped by owner rank into d_send
  * (room for 2 * n_candidates uint64); counts[world] = pairs per owner (host) */
 int ef_route_owners(ef_ctx* ctx, uint32_t world, uint64_t order_base, uint64_t* d_send, uint32_t* counts);

@@ -124,6 +124,7 @@ _PROTOS = {
     "ef_route_owners": (C.c_int, [_P, C.c_uint32, C.c_uint64, C.c_void_p, _U32P]),
     "ef_owner_mark": (C.c_int, [_P, C.c_void_p, C.c_uint32, C.c_void_p, C.c_int]),
     "ef_expand_finish": (C.c_int, [_P, C.c_void_p, C.POINTER(PriceParams)]),
+    "ef_expand_hashes_spec": (C.c_int, [_P, _U32P, C.c_uint32, _I32P, C.c_uint32, C.POINTER(PriceParams), _U32P]),
     "ef_route_owners_padded": (C.c_int, [_P, C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p]),
     "ef_owner_mark_padded": (C.c_int, [_P, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_int]),
     "ef_expand_finish_padded": (C.c_int, [_P, C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(PriceParams)]),

@@ -204,6 +204,7 @@ struct ef_ctx {
   uint32_t spec_min_cands = 32768;   // and never below this many: a search's small steps price mostly
                                      // visited duplicates speculatively (NasNet-A search 5.5 -> 6.4 s)
   const ef_price_params* spec_pp = nullptr;  // set by ef_expand for step_hash
+  bool spec_sharded = false;                 // the step's survivors come from owner verdicts (FIRST)
   bool spec_live = false;                    // this step's speculative pricing was launched
   cudaStream_t st_price = nullptr;
   cudaEvent_t ev_sp0 = nullptr, ev_sp1 = nullptr;
@@ -1772,7 +1773,8 @@ static int step_price(ef_ctx* ctx, const ef_price_params* pp) {
     ctx->spec_live = false;
     EF_CUDA(cudaStreamWaitEvent(ctx->st, ctx->ev_sp1, 0));
     const uint32_t grid_t = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, ctx->n_sm * 8));
-    ++ctx->kcount, k_spec_commit<<<grid_t, 256, 0, ctx->st>>>(ctx->d_res.p, ctx->d_spec.p, total, pp->per_parent);
+    ++ctx->kcount, k_spec_commit<<<grid_t, 256, 0, ctx->st>>>(ctx->d_res.p, ctx->d_spec.p, total,
+                                                              ctx->spec_sharded ? 0 : pp->per_parent);
     EF_CUDA(cudaGetLastError());
   } else {
     int rc = launch_price(ctx, pp, total, ctx->st, ctx->d_plist.p, ctx->d_scalars.p + 7, nullptr);
@@ -1868,6 +1870,7 @@ int ef_expand(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, con
   // large graphs: price every candidate on a second stream while the chunks hash (their
   // pricing does not depend on the hashes, only which of them survive the dedup does)
   ctx->spec_pp = ctx->spec_price && pp && pp->use_inner ? pp : nullptr;
+  ctx->spec_sharded = false;
   rc = step_hash(ctx, parent_slots, n_parents, rules, n_rules, &total);
   ctx->spec_pp = nullptr;
   if (rc) return rc;
@@ -1887,6 +1890,23 @@ int ef_expand_hashes(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
   if (rc) return rc;
   uint32_t total = 0;
   if ((rc = step_hash(ctx, parent_slots, n_parents, rules, n_rules, &total))) return rc;
+  rc = step_sync(ctx, false);
+  *n_candidates = total;
+  return rc;
+}
+
+int ef_expand_hashes_spec(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_parents, const int32_t* rules,
+                          uint32_t n_rules, const ef_price_params* pp, uint32_t* n_candidates) {
+  int rc = step_begin(ctx, n_candidates, n_rules);
+  if (rc) return rc;
+  uint32_t total = 0;
+  // speculative pricing as in ef_expand; ef_expand_finish(_padded) commits the survivors (the
+  // owners' verdicts: first occurrences, FIRST)
+  ctx->spec_pp = ctx->spec_price && pp && pp->use_inner ? pp : nullptr;
+  rc = step_hash(ctx, parent_slots, n_parents, rules, n_rules, &total);
+  ctx->spec_pp = nullptr;
+  ctx->spec_sharded = true;
+  if (rc) return rc;
   rc = step_sync(ctx, false);
   *n_candidates = total;
   return rc;

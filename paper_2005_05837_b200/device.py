@@ -542,13 +542,19 @@ class DeviceSession:
 
     # ---- hash-owner sharding (see shard.py) ------------------------------------------
 
-    def expand_hashes(self, slots: list[int], rule_ids: list[int]) -> int:
-        """Match, plan and hash the candidates of `slots` (no dedup, no pricing)."""
+    def expand_hashes(self, slots: list[int], rule_ids: list[int], pp: N.PriceParams | None = None) -> int:
+        """Match, plan and hash the candidates of `slots` (no dedup).  With `pp`, large steps
+        also price every candidate speculatively beside the hashing (ef_expand_hashes_spec);
+        expand_finish* then keeps the survivors' prices."""
         parents = N.u32_array(slots)
         rules = N.i32_array(rule_ids)
         count = C.c_uint32(0)
         while True:
-            rc = self.L.ef_expand_hashes(self.ctx, parents, len(slots), rules, len(rule_ids), C.byref(count))
+            if pp is not None:
+                rc = self.L.ef_expand_hashes_spec(self.ctx, parents, len(slots), rules, len(rule_ids), C.byref(pp),
+                                                  C.byref(count))
+            else:
+                rc = self.L.ef_expand_hashes(self.ctx, parents, len(slots), rules, len(rule_ids), C.byref(count))
             if rc == N.EF_NEED_RESOLVE:
                 if not self.resolve_pending():
                     raise N.NativeError(f"ef_expand_hashes keeps asking for interning: {self._pending_summary()}")

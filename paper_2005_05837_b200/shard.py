@@ -129,7 +129,7 @@ def sharded_expand(session, slots: list[int], rule_ids: list[int], pp, ex: Owner
     Returns this rank's candidate results (the layout of `DeviceSession.expand`); flags
     FIRST / VISITED are global, costs are those of this rank's survivors.  `phases` counts calls.
     """
-    n = session.expand_hashes(slots, rule_ids)
+    n = session.expand_hashes(slots, rule_ids, pp)
     cap = max(1, ex.max_int(n))  # the only host-visible size: every bucket of every rank fits
     world = ex.world
     send = ex.buffer("send", 2 * world * cap, torch.int64)

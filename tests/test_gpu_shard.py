@@ -115,8 +115,12 @@ def _session(g0, db, prof, cap, graphs, visited):
     return s, [s.upload(g) for g in graphs]
 
 
-@pytest.mark.parametrize("model,n_parents", [("squeezenet", 24), ("resnet50", 16)])
-def test_sharded_step_equals_single(model, n_parents):
+@pytest.mark.parametrize("model,n_parents,spec", [("squeezenet", 24, False), ("resnet50", 16, False),
+                                                  ("resnet50", 16, True), ("nasnet_a", 4, True)])
+def test_sharded_step_equals_single(model, n_parents, spec, monkeypatch):
+    """spec: the ranks' contexts price every candidate speculatively beside the hashing
+    (EF_SPEC_PRICE=2: ef_expand_hashes_spec) and keep the survivors' prices after the owners'
+    verdicts; the reference is a plain single-context ef_expand."""
     g0 = zoo.generate(model, 0)
     db = ef.CostDatabase()
     prof = ef.SyntheticProfiler(0)
@@ -140,6 +144,8 @@ def test_sharded_step_equals_single(model, n_parents):
 
     world, split = 2, len(graphs) // 3
     parts = [graphs[:split], graphs[split:]]
+    if spec:
+        monkeypatch.setenv("EF_SPEC_PRICE", "2")  # read when the ranks' contexts are created
 
     def run(rank, ex):
         mine = [h for h in visited if owner_of(h, world) == rank]
@@ -223,3 +229,41 @@ def test_sharded_search_equals_single(model, alpha, max_exp, batch):
     got = [hashed(r) for r in _threads(2, run)]
     assert got[0] == want
     assert got[1] == want
+
+
+@pytest.mark.parametrize("mode", ["1", "2", "3", "4"])
+def test_speculative_pricing_equals_plain(mode, monkeypatch):
+    """ef_expand with every candidate priced speculatively beside the hashing (from the first
+    digest, the plans, the node keys, the key sort) and the survivors' prices committed after
+    the dedup equals the plain step -- flags, costs, evaluation counts -- on NasNet-A parents
+    (rows > 256), against a visited set that rejects some candidates."""
+    g0 = zoo.generate("nasnet_a", 0)
+    db = ef.CostDatabase()
+    prof = ef.SyntheticProfiler(0)
+    f = ef.CostFunction.energy()
+    cfg = ef.SearchConfig(alpha=1.05)
+    fr = Frontier(g0, db, prof, f, cfg, 6)
+    try:
+        graphs = [fr.decode(sl) for sl in fr.slots]
+        probe = fr.step()
+    finally:
+        fr.close()
+    visited = sorted({int(h) for h in probe["hash"].tolist()})[::4]
+    cap = _node_cap(cfg, g0)
+    pp = price_params(f, 1, True, cap)
+    rule_ids = [r.rule_id for r in ef.default_rules()]
+
+    def step():
+        s, slots = _session(g0, db, prof, cap, graphs, visited)
+        try:
+            return s.expand(slots, rule_ids, pp, insert_visited=False).copy()
+        finally:
+            s.close()
+
+    plain = step()
+    monkeypatch.setenv("EF_SPEC_PRICE", mode)
+    spec = step()
+    assert len(spec) == len(plain)
+    for key in ("hash", "flags", "cost", "time_ms", "energy", "evals", "sweeps"):
+        assert np.array_equal(spec[key], plain[key]), key
+    assert ((plain["flags"] & N.F_PRICED) != 0).any() and (plain["flags"] & N.F_VISITED).any()

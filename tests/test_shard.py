@@ -38,7 +38,7 @@ class HostRank:
         self.hashes = [int(h) for h in hashes]
         self.visited = set(visited_shard)
 
-    def expand_hashes(self, slots, rule_ids):
+    def expand_hashes(self, slots, rule_ids, pp=None):
         return len(self.hashes)
 
     def route_owners_padded(self, world, base, cap, send, counts):

@@ -82,8 +82,9 @@ struct Scratch {
   DevBuf<uint16_t> jlvl;
   DevBuf<uint64_t> fresh, fresh2, skey, skey2, merged, pfx;
   DevBuf<int32_t> seg_b, seg_e;
-  DevBuf<uint32_t> recmax;
+  DevBuf<uint32_t> recmax, pdir;
   void release() {
+    pdir.release();
     jlvl.release();
     merged.release();
     didx.release(); jv.release(); refsrc.release(); dcount.release(); dorder.release(); cbins.release();
@@ -105,6 +106,7 @@ struct ef_ctx {
   bool dirty_big = true;  // rows > kFastRows: k_dirty_big (warp window walk); EF_DIRTY_BIG=0: k_dirty
   uint32_t wide_lpc = 8;  // lanes per candidate in k_keys_wide: 32, 16, 8 or 4 (EF_WIDE_LPC; DAG-20k keys 70.8 -> 63.9 ms from 16 to 8, 85.3 at 4)
   bool fuse_merge = false;  // rows > kFastRows: k_digest_mg merges on the fly (EF_FUSE_MERGE=1; measured slower: 52.9 vs 12.0 + 38.5 ms on DAG-20k)
+  bool merge_scatter = true;  // rows > kFastRows: k_merge_scatter (EF_MERGE_SCATTER=0: k_merge_big)
   bool digest_pf = true;  // rows > kFastRows: k_digest_pm loads the next block's key words ahead (EF_DIGEST_PF)
   uint32_t quad_max = 20000;  // chunks below this many candidates hash with k_keys_quad (EF_QUAD_MAX)
   uint64_t chunk_mib = 0;  // per-chunk hashing scratch budget, MiB (0: 80% of the HBM free at the first sizing, <= 144 GiB)
@@ -325,6 +327,7 @@ ef_ctx* ef_create(int device) {
   if (const char* e = getenv("EF_SPEC_MAX_CANDS")) ctx->spec_max_cands = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_SPEC_MIN_CANDS")) ctx->spec_min_cands = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_DIGEST_PF")) ctx->digest_pf = atoi(e) != 0;
+  if (const char* e = getenv("EF_MERGE_SCATTER")) ctx->merge_scatter = atoi(e) != 0;
   if (const char* e = getenv("EF_QUAD_MAX")) ctx->quad_max = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_CHUNK_MIB")) ctx->chunk_mib = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
   cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
@@ -1548,6 +1551,17 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       EF_CUDA(sc.pfx.reserve((uint64_t)chunk * V.pfx_stride, ctx->st));
       V.pfx = sc.pfx.p;
     }
+    // k_merge_scatter: the parents' top-bit directories, once per step
+    const bool ms16 = S < 65536u;  // positions as 16-bit words
+    const size_t ms_smem = 4ull * (2ull * V.W + 3) + (ms16 ? 2ull : 4ull) * S;
+    V.pdir = nullptr;
+    if (total && S > kFastRows && ctx->big_merge && !ctx->fuse_merge && ctx->merge_scatter && ms_smem <= 200ull * 1024) {
+      EF_CUDA(sc.pdir.reserve((uint64_t)kDirN * n_parents, ctx->st));
+      V.pdir = sc.pdir.p;
+      ++ctx->kcount, k_merge_dir<<<std::max<uint32_t>(1, std::min<uint32_t>(n_parents, ctx->n_sm * 8)), 256, 0, ctx->st>>>(
+          A.parent_addr, ctx->geo, n_parents, sc.pdir.p);
+      EF_CUDA(cudaGetLastError());
+    }
     ctx->n_chunks = 0;
     for (uint32_t c0 = 0; c0 < total; c0 += chunk) {
       V.c0 = c0;
@@ -1608,11 +1622,23 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
         if (ctx->big_merge && ctx->fuse_merge) {  // the digest merges the two sorted streams itself
           cudaEventRecord(ce[3], ctx->st);
           ++ctx->kcount, k_digest_mg<kHashThreads, 2><<<gd, kHashThreads, 0, ctx->st>>>(V);
-        } else if (ctx->big_merge) {  // merge-path key stream, then the streaming digest
-          const size_t smem = 4ull * (2560 + 4 * (2 * V.W + 2));  // per warp: the output stage, kept counts, removed mask
-          EF_CUDA(cudaFuncSetAttribute(k_merge_big<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
-          ++ctx->kcount, k_merge_big<4><<<gm, 128, smem, ctx->st>>>(V);
+        } else if (ctx->big_merge) {  // merged key stream, then the streaming digest
+          if (V.pdir) {
+            const uint32_t per_sm = std::max<uint32_t>(1, std::min<uint32_t>(8, (uint32_t)((220ull * 1024) / (ms_smem + 2048))));
+            const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * per_sm));
+            if (ms16) {
+              EF_CUDA(cudaFuncSetAttribute(k_merge_scatter<256, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
+              ++ctx->kcount, k_merge_scatter<256, uint16_t><<<gm, 256, ms_smem, ctx->st>>>(V);
+            } else {
+              EF_CUDA(cudaFuncSetAttribute(k_merge_scatter<256, uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
+              ++ctx->kcount, k_merge_scatter<256, uint32_t><<<gm, 256, ms_smem, ctx->st>>>(V);
+            }
+          } else {
+            const size_t smem = 4ull * (2560 + 4 * (2 * V.W + 2));  // per warp: the output stage, kept counts, removed mask
+            EF_CUDA(cudaFuncSetAttribute(k_merge_big<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
+            ++ctx->kcount, k_merge_big<4><<<gm, 128, smem, ctx->st>>>(V);
+          }
           EF_CUDA(cudaGetLastError());
           if (V.pfx) {
             const uint32_t gpx = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));

@@ -103,6 +103,7 @@ struct VArgs {
   uint32_t* rmask;     // [n][W] parent keys (by sorted rank) absent from the candidate: dropped or dirty
   uint64_t* fresh_sorted;  // [n][S][2] the fresh keys in ascending byte order
   uint64_t* kstream;       // [n][S][2] the merged key stream k_digest_pm hashes (k_merge: fresh_sorted)
+  const uint32_t* pdir;    // [parent][kDirN] first sorted rank per top-12-bit prefix (k_merge_dir), or null
   const uint64_t* input_words;  // input text, 8-byte words, zero padded
   uint64_t* pfx;       // [n][pfx_stride] the digest's prefix (input text, output keys and ports) as
                        // little-endian words (k_prefix), or null: the digest assembles it itself
@@ -2242,6 +2243,190 @@ __global__ void __launch_bounds__(WARPS * 32, EF_MERGE_BIG_MINB) k_merge_big(VAr
       }
       __syncwarp();
     }
+  }
+}
+
+// k_merge_dir + k_merge_scatter (rows > kFastRows, the default): the same key stream as
+// k_merge_big without a serial per-lane merge.  The stream is the parent's sorted keys minus the
+// removed ranks with the candidate's sorted fresh keys inserted (graph.py:547 sorts every node
+// key), so a fresh key j lands at j + (kept parent keys <= it).  That count comes from a
+// per-parent directory of the keys' top 12 bits (k_merge_dir, once per step) plus a search of
+// the ~5 parent keys sharing them and the kept-rank prefix of the candidate's removed mask.
+// The warps then fill 32 output positions per round: the fresh ones from a ballot of the
+// positions in the round, the others from the parent's kept ranks in order (a 64-rank window
+// of the removed mask), with one coalesced 16-byte load and store per lane.  A CTA per
+// candidate; dynamic shared memory: the removed mask, its kept prefix and the S positions.
+constexpr uint32_t kDirBits = 12, kDirN = (1u << kDirBits) + 1;
+
+__device__ __forceinline__ uint32_t key_top(const uint2 x) {  // top kDirBits of the key's first word (big endian)
+  return __byte_perm(x.x, 0, 0x0123) >> (32 - kDirBits);
+}
+
+__global__ void __launch_bounds__(256) k_merge_dir(const unsigned long long* parent_addr, const Geo G, uint32_t n_parents,
+                                                  uint32_t* dir) {
+  for (uint32_t pi = blockIdx.x; pi < n_parents; pi += gridDim.x) {
+    Rec R{reinterpret_cast<char*>(parent_addr[pi])};
+    const uint32_t n = (uint32_t)R.h().n;
+    const uint2* sk = reinterpret_cast<const uint2*>(R.skeys(G));  // key r's first word: sk[2r]
+    uint32_t* D = dir + (uint64_t)pi * kDirN;
+    // D[b] = the first rank whose top bits are >= b: rank r owns (top(r - 1), top(r)], the
+    // end sentinel rank n owns the rest up to D[2^bits]
+    for (uint32_t r = threadIdx.x; r <= n; r += blockDim.x) {
+      const uint32_t t1 = r < n ? key_top(sk[2 * r]) : (1u << kDirBits);
+      const uint32_t t0 = r ? key_top(sk[2 * (r - 1)]) + 1u : 0u;
+      for (uint32_t b = t0; b <= t1; ++b) D[b] = r;
+    }
+  }
+}
+
+__device__ __forceinline__ void be_key(const uint4 x, uint64_t& k0, uint64_t& k1) {
+  k0 = B2b::bswap64(((uint64_t)x.y << 32) | x.x);
+  k1 = B2b::bswap64(((uint64_t)x.w << 32) | x.z);
+}
+
+template <int BT, typename PT>  // PT: the position type (uint16_t while S < 2^16)
+__global__ void __launch_bounds__(BT) k_merge_scatter(VArgs A) {
+  extern __shared__ uint32_t ms_sh[];
+  constexpr uint32_t NWARP = BT / 32;
+  __shared__ uint32_t wsum[NWARP], slot_sh[NWARP][32];
+  const Geo& G = A.g;
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  const unsigned full = 0xffffffffu;
+  uint32_t* slot = slot_sh[wid];  // kept ranks of the warp's round, by ordinal
+  uint32_t* rm = ms_sh;           // [W + 2] removed ranks; ranks past the parent's count read as removed
+  uint32_t* cumk = rm + A.W + 2;  // [W + 1] kept ranks before each mask word
+  PT* pb = reinterpret_cast<PT*>(cumk + A.W + 1);  // [S] output position of every fresh key (ascending)
+  for (uint32_t lc = blockIdx.x; lc < A.n; lc += gridDim.x) {
+    const uint32_t c = A.c0 + lc;
+    if (A.res[c].flags & EF_F_INCOMPLETE) continue;  // CTA-uniform
+    const VPlan& P = A.plan[c];
+    const uint32_t pn = (uint32_t)P.pn, d = A.dcount[lc], nw = (pn + 31) >> 5;
+    const uint32_t* grm = A.rmask + (uint64_t)lc * A.W;
+    for (uint32_t x = threadIdx.x; x < nw + 2; x += BT) {
+      uint32_t v = x < nw ? grm[x] : 0xffffffffu;
+      if (x + 1 == nw && (pn & 31u)) v |= ~((1u << (pn & 31u)) - 1u);
+      rm[x] = v;
+    }
+    __syncthreads();
+    // kept ranks before each word: a block scan over contiguous runs of words
+    const uint32_t per = (nw + BT - 1) / BT, x0 = min(nw, threadIdx.x * per), x1 = min(nw, x0 + per);
+    uint32_t s = 0;
+    for (uint32_t x = x0; x < x1; ++x) s += __popc(~rm[x]);
+    uint32_t inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(full, inc, o);
+      if ((int)lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    uint32_t run = inc - s, na = 0;
+#pragma unroll
+    for (uint32_t w = 0; w < NWARP; ++w) {
+      const uint32_t v = wsum[w];
+      run += w < wid ? v : 0u;
+      na += v;
+    }
+    for (uint32_t x = x0; x < x1; ++x) {
+      cumk[x] = run;
+      run += __popc(~rm[x]);
+    }
+    if (threadIdx.x == 0) cumk[nw] = na;
+    __syncthreads();
+    Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
+    const uint4* pa = reinterpret_cast<const uint4*>(R.skeys(G));
+    const uint32_t* D = A.pdir + (uint64_t)P.parent * kDirN;
+    const uint4* bk = reinterpret_cast<const uint4*>(A.fresh_sorted + 2ull * lc * A.S);
+    // 1) every fresh key's position: j + the kept parent keys <= it (the parent's key first on a tie)
+    // two keys per thread and pass, their searches interleaved (independent load chains)
+    for (uint32_t j0 = threadIdx.x; j0 < d; j0 += 2 * BT) {
+      const uint32_t j1 = j0 + BT;
+      const bool h1 = j1 < d;
+      uint64_t b0, b1, e0 = ~0ull, e1 = ~0ull;
+      be_key(bk[j0], b0, b1);
+      if (h1) be_key(bk[j1], e0, e1);
+      const uint32_t tb = (uint32_t)(b0 >> (64 - kDirBits)), te = (uint32_t)(e0 >> (64 - kDirBits));
+      uint32_t lo = __ldg(D + tb), hi = __ldg(D + tb + 1);  // the parent ranks sharing its top bits
+      uint32_t lo1 = h1 ? __ldg(D + te) : 0u, hi1 = h1 ? __ldg(D + te + 1) : 0u;
+      while (lo < hi || lo1 < hi1) {
+        const bool s0 = lo < hi, s1 = lo1 < hi1;
+        const uint32_t m0 = (lo + hi) >> 1, m1 = (lo1 + hi1) >> 1;
+        const uint4 x0 = __ldg(pa + (s0 ? m0 : 0u)), x1 = __ldg(pa + (s1 ? m1 : 0u));
+        uint64_t a0, a1, f0, f1;
+        be_key(x0, a0, a1);
+        be_key(x1, f0, f1);
+        if (s0) {
+          if (be_less(b0, b1, a0, a1)) hi = m0;
+          else lo = m0 + 1;
+        }
+        if (s1) {
+          if (be_less(e0, e1, f0, f1)) hi1 = m1;
+          else lo1 = m1 + 1;
+        }
+      }
+      pb[j0] = (PT)(j0 + cumk[lo >> 5] + __popc(~rm[lo >> 5] & ((1u << (lo & 31u)) - 1u)));
+      if (h1) pb[j1] = (PT)(j1 + cumk[lo1 >> 5] + __popc(~rm[lo1 >> 5] & ((1u << (lo1 & 31u)) - 1u)));
+    }
+    __syncthreads();
+    auto select_kept = [&](uint32_t i) -> uint32_t {  // rank of the i-th kept parent key (i < na)
+      uint32_t l = 0, h = nw;                          // last word with cumk <= i
+      while (h - l > 1) {
+        const uint32_t mid = (l + h) >> 1;
+        if (cumk[mid] <= i) l = mid;
+        else h = mid;
+      }
+      return 32u * l + nth_bit(~rm[l], i - cumk[l]);
+    };
+    // 2) the stream, 32 positions per warp round over a contiguous span per warp
+    const uint32_t tot = na + d;
+    uint4* out = reinterpret_cast<uint4*>(A.kstream + 2ull * lc * A.S);
+    const uint32_t span = (tot + NWARP * 32 - 1) / (NWARP * 32) * 32;
+    uint32_t p0 = wid * span;
+    const uint32_t pend = min(tot, p0 + span);
+    if (p0 < pend) {  // warp-uniform
+      uint32_t nb = 0, hb = d;  // fresh keys before p0
+      while (nb < hb) {
+        const uint32_t mid = (nb + hb) >> 1;
+        if ((uint32_t)pb[mid] < p0) nb = mid + 1;
+        else hb = mid;
+      }
+      uint32_t ka = p0 - nb;                         // kept parent keys before p0
+      uint32_t rc = ka < na ? select_kept(ka) : pn;  // the next kept rank
+      const uint32_t ltm = (1u << lane) - 1u;
+      for (; p0 < pend; p0 += 32) {
+        const uint32_t v = nb + lane < d ? (uint32_t)pb[nb + lane] : 0xffffffffu;
+        const uint32_t bmask = __reduce_or_sync(full, v - p0 < 32u ? 1u << (v - p0) : 0u);
+        const uint32_t cnt = min(32u, pend - p0), nf = __popc(bmask), nA = cnt - nf;
+        uint32_t have = 0;  // kept ranks published in slot[] (ordinals < nA)
+        if (nA) {  // the kept ranks among rc .. rc + 63 publish themselves by ordinal
+          const uint32_t wi = rc >> 5, sh = rc & 31u;
+          const uint32_t k_lo = ~__funnelshift_r(rm[wi], rm[wi + 1], sh);
+          const uint32_t k_hi = ~__funnelshift_r(rm[wi + 1], rm[wi + 2], sh);
+          const uint32_t c_lo = __popc(k_lo);
+          const uint32_t o_lo = __popc(k_lo & ltm), o_hi = c_lo + __popc(k_hi & ltm);
+          if (((k_lo >> lane) & 1u) && o_lo < nA) slot[o_lo] = rc + lane;
+          if (((k_hi >> lane) & 1u) && o_hi < nA) slot[o_hi] = rc + 32u + lane;
+          have = min(nA, c_lo + __popc(k_hi));
+          __syncwarp();
+        }
+        const uint32_t before = __popc(bmask & ltm);
+        if (lane < cnt) {
+          uint4 key;
+          if ((bmask >> lane) & 1u) {
+            key = bk[nb + before];
+          } else {
+            const uint32_t t = lane - before;
+            key = __ldg(pa + (t < have ? slot[t] : select_kept(ka + t)));  // (< 32 kept ranks in 64: rare)
+          }
+          out[p0 + lane] = key;
+        }
+        if (nA) rc = (nA <= have ? slot[nA - 1] : select_kept(ka + nA - 1)) + 1u;
+        __syncwarp();
+        ka += nA;
+        nb += nf;
+      }
+    }
+    __syncthreads();  // rm, cumk and pb are the next candidate's
   }
 }
 

@@ -735,14 +735,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_dirty_big(VArgs A) {
         atomicOr(&rk[k >> 5], 1u << (k & 31));
       }
       if (levels) {
-        if (__any_sync(full, (in1 | in2 | in3) != 0u)) {  // in-window producers sit on lower lanes: one ascending pass
-#pragma unroll 4
-          for (int b = 0; b < 31; ++b) {
-            const uint32_t x = __shfl_sync(full, lvl, b);
-            if ((in1 >> b) & 1u) lvl = max(lvl, x + 1u);
-            if ((in2 >> b) & 1u) lvl = max(lvl, x + 2u);
-            if ((in3 >> b) & 1u) lvl = max(lvl, x + 3u);
-          }
+        // in-window producers sit on lower lanes: one ascending pass over the lanes some lane
+        // depends on (a producer's own in-window producers are lower still, so it is final
+        // when it is read)
+        for (uint32_t u = __reduce_or_sync(full, in1 | in2 | in3); u; u &= u - 1u) {  // warp-uniform
+          const int b = __ffs(u) - 1;
+          const uint32_t x = __shfl_sync(full, lvl, b);
+          if ((in1 >> b) & 1u) lvl = max(lvl, x + 1u);
+          if ((in2 >> b) & 1u) lvl = max(lvl, x + 2u);
+          if ((in3 >> b) & 1u) lvl = max(lvl, x + 3u);
         }
         if (d) {
           plv[t] = lvl;

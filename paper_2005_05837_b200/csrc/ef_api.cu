@@ -1552,8 +1552,8 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       V.pfx = sc.pfx.p;
     }
     // k_merge_scatter: the parents' top-bit directories, once per step
-    const bool ms16 = S < 65536u;  // positions as 16-bit words
-    const size_t ms_smem = 4ull * (2ull * V.W + 3) + (ms16 ? 2ull : 4ull) * S;
+    const bool ms16 = S < 65536u;  // positions as 16-bit words; then the merge sorts the fresh keys too
+    const size_t ms_smem = 4ull * (2ull * V.W + 3) + (ms16 ? 4ull * (1u << kDirBits) + 6ull * kMsDcap : 4ull * S);
     V.pdir = nullptr;
     if (total && S > kFastRows && ctx->big_merge && !ctx->fuse_merge && ctx->merge_scatter && ms_smem <= 200ull * 1024) {
       EF_CUDA(sc.pdir.reserve((uint64_t)kDirN * n_parents, ctx->st));
@@ -1617,7 +1617,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
         ++ctx->kcount, k_digest_pm<kHashThreads, false, EF_DIGEST_MINB><<<gd, kHashThreads, 0, ctx->st>>>(V);
       } else {
         if (ctx->spec_mode == 4 && (rc = launch_spec_price(ctx, total))) return rc;  // beside the key sort
-        if ((rc = sort_fresh_keys(ctx, sc, ctx->st, V))) return rc;
+        if (!(V.pdir && ms16) && (rc = sort_fresh_keys(ctx, sc, ctx->st, V))) return rc;  // (k_merge_scatter sorts)
         if (ctx->spec_mode && (rc = launch_spec_price(ctx, total))) return rc;  // under the digest
         if (ctx->big_merge && ctx->fuse_merge) {  // the digest merges the two sorted streams itself
           cudaEventRecord(ce[3], ctx->st);
@@ -1627,11 +1627,11 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
             const uint32_t per_sm = std::max<uint32_t>(1, std::min<uint32_t>(8, (uint32_t)((220ull * 1024) / (ms_smem + 2048))));
             const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * per_sm));
             if (ms16) {
-              EF_CUDA(cudaFuncSetAttribute(k_merge_scatter<256, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
-              ++ctx->kcount, k_merge_scatter<256, uint16_t><<<gm, 256, ms_smem, ctx->st>>>(V);
+              EF_CUDA(cudaFuncSetAttribute(k_merge_scatter<256, uint16_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
+              ++ctx->kcount, k_merge_scatter<256, uint16_t, true><<<gm, 256, ms_smem, ctx->st>>>(V);
             } else {
-              EF_CUDA(cudaFuncSetAttribute(k_merge_scatter<256, uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
-              ++ctx->kcount, k_merge_scatter<256, uint32_t><<<gm, 256, ms_smem, ctx->st>>>(V);
+              EF_CUDA(cudaFuncSetAttribute(k_merge_scatter<256, uint32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
+              ++ctx->kcount, k_merge_scatter<256, uint32_t, false><<<gm, 256, ms_smem, ctx->st>>>(V);
             }
           } else {
             const size_t smem = 4ull * (2560 + 4 * (2 * V.W + 2));  // per warp: the output stage, kept counts, removed mask

@@ -2285,7 +2285,18 @@ __device__ __forceinline__ void be_key(const uint4 x, uint64_t& k0, uint64_t& k1
   k1 = B2b::bswap64(((uint64_t)x.w << 32) | x.z);
 }
 
-template <int BT, typename PT>  // PT: the position type (uint16_t while S < 2^16)
+//
+// SORT (16-bit positions only): the fresh keys are read unsorted from the node-key rows and
+// ordered here, replacing k_sortbig: a histogram on the same top 12 bits as the directory, a
+// block scan, a scatter of the job indices and an insertion sort inside each bucket (~1 key
+// per bucket on DAG-20k).  Candidates with up to kMsDcap fresh keys keep the order and the
+// positions in shared memory, larger ones in their (by now idle) sort-key row.
+#ifndef EF_MS_DCAP
+#define EF_MS_DCAP 4096
+#endif
+constexpr uint32_t kMsDcap = EF_MS_DCAP;
+
+template <int BT, typename PT, bool SORT>  // PT: the position type (uint16_t while S < 2^16)
 __global__ void __launch_bounds__(BT) k_merge_scatter(VArgs A) {
   extern __shared__ uint32_t ms_sh[];
   constexpr uint32_t NWARP = BT / 32;
@@ -2296,12 +2307,27 @@ __global__ void __launch_bounds__(BT) k_merge_scatter(VArgs A) {
   uint32_t* slot = slot_sh[wid];  // kept ranks of the warp's round, by ordinal
   uint32_t* rm = ms_sh;           // [W + 2] removed ranks; ranks past the parent's count read as removed
   uint32_t* cumk = rm + A.W + 2;  // [W + 1] kept ranks before each mask word
-  PT* pb = reinterpret_cast<PT*>(cumk + A.W + 1);  // [S] output position of every fresh key (ascending)
+  // !SORT: [S] output position of every fresh key (ascending).  SORT: [2^12] bucket counters,
+  // [kMsDcap] first key words by job (then, aliased, the positions), [kMsDcap] job indices in
+  // key order
+  uint32_t* bins = cumk + A.W + 1;
+  uint32_t* top_sm = bins + (1u << kDirBits);
+  PT* pb_sm = reinterpret_cast<PT*>(SORT ? top_sm : bins);
+  uint16_t* perm_sm = reinterpret_cast<uint16_t*>(top_sm + kMsDcap);
   for (uint32_t lc = blockIdx.x; lc < A.n; lc += gridDim.x) {
     const uint32_t c = A.c0 + lc;
     if (A.res[c].flags & EF_F_INCOMPLETE) continue;  // CTA-uniform
     const VPlan& P = A.plan[c];
     const uint32_t pn = (uint32_t)P.pn, d = A.dcount[lc], nw = (pn + 31) >> 5;
+    PT* pb = pb_sm;
+    uint32_t* top = top_sm;
+    uint16_t* perm = perm_sm;
+    if (SORT && d > kMsDcap) {  // CTA-uniform: the candidate's sort-key row (8 S bytes)
+      top = reinterpret_cast<uint32_t*>(A.skey + (uint64_t)lc * A.S);
+      pb = reinterpret_cast<PT*>(top);
+      perm = reinterpret_cast<uint16_t*>(top + A.S);
+    }
+    const uint4* fk = reinterpret_cast<const uint4*>(A.fresh + 2ull * lc * A.S);  // fresh keys, job order
     const uint32_t* grm = A.rmask + (uint64_t)lc * A.W;
     for (uint32_t x = threadIdx.x; x < nw + 2; x += BT) {
       uint32_t v = x < nw ? grm[x] : 0xffffffffu;
@@ -2338,14 +2364,54 @@ __global__ void __launch_bounds__(BT) k_merge_scatter(VArgs A) {
     const uint4* pa = reinterpret_cast<const uint4*>(R.skeys(G));
     const uint32_t* D = A.pdir + (uint64_t)P.parent * kDirN;
     const uint4* bk = reinterpret_cast<const uint4*>(A.fresh_sorted + 2ull * lc * A.S);
+    if (SORT) {  // the fresh keys in key order: perm[k] = job index of the k-th smallest
+      for (uint32_t b = threadIdx.x; b < (1u << kDirBits); b += BT) bins[b] = 0;
+      __syncthreads();
+      for (uint32_t j = threadIdx.x; j < d; j += BT) {
+        const uint2 x = reinterpret_cast<const uint2*>(fk + j)[0];
+        const uint32_t tw = __byte_perm(x.x, 0, 0x0123);  // first 4 key bytes, big endian
+        top[j] = tw;
+        atomicAdd(&bins[tw >> (32 - kDirBits)], 1u);
+      }
+      __syncthreads();
+      block_excl_scan_inplace<BT>(bins, 1u << kDirBits, wsum);
+      __syncthreads();
+      for (uint32_t j = threadIdx.x; j < d; j += BT) perm[atomicAdd(&bins[top[j] >> (32 - kDirBits)], 1u)] = (uint16_t)j;
+      __syncthreads();
+      for (uint32_t b = threadIdx.x; b < (1u << kDirBits); b += BT) {  // bins[b]: the end of bucket b
+        const uint32_t e = bins[b], s0 = b ? bins[b - 1] : 0u;
+        for (uint32_t x = s0 + 1; x < e; ++x) {  // by the first 4 bytes, the full key on a tie
+          const uint16_t v = perm[x];
+          const uint32_t tv = top[v];
+          uint32_t y = x;
+          while (y > s0) {
+            const uint16_t u = perm[y - 1];
+            const uint32_t tu = top[u];
+            bool less = tv < tu;
+            if (tv == tu) {
+              uint64_t v0, v1, u0, u1;
+              be_key(fk[v], v0, v1);
+              be_key(fk[u], u0, u1);
+              less = be_less(v0, v1, u0, u1);
+            }
+            if (!less) break;
+            perm[y] = u;
+            --y;
+          }
+          perm[y] = v;
+        }
+      }
+      __syncthreads();  // (top is dead from here: pb reuses it)
+    }
     // 1) every fresh key's position: j + the kept parent keys <= it (the parent's key first on a tie)
     // two keys per thread and pass, their searches interleaved (independent load chains)
+    auto fresh_key = [&](uint32_t k) -> uint4 { return SORT ? fk[perm[k]] : bk[k]; };  // the k-th smallest
     for (uint32_t j0 = threadIdx.x; j0 < d; j0 += 2 * BT) {
       const uint32_t j1 = j0 + BT;
       const bool h1 = j1 < d;
       uint64_t b0, b1, e0 = ~0ull, e1 = ~0ull;
-      be_key(bk[j0], b0, b1);
-      if (h1) be_key(bk[j1], e0, e1);
+      be_key(fresh_key(j0), b0, b1);
+      if (h1) be_key(fresh_key(j1), e0, e1);
       const uint32_t tb = (uint32_t)(b0 >> (64 - kDirBits)), te = (uint32_t)(e0 >> (64 - kDirBits));
       uint32_t lo = __ldg(D + tb), hi = __ldg(D + tb + 1);  // the parent ranks sharing its top bits
       uint32_t lo1 = h1 ? __ldg(D + te) : 0u, hi1 = h1 ? __ldg(D + te + 1) : 0u;
@@ -2414,7 +2480,7 @@ __global__ void __launch_bounds__(BT) k_merge_scatter(VArgs A) {
         if (lane < cnt) {
           uint4 key;
           if ((bmask >> lane) & 1u) {
-            key = bk[nb + before];
+            key = fresh_key(nb + before);
           } else {
             const uint32_t t = lane - before;
             key = __ldg(pa + (t < have ? slot[t] : select_kept(ka + t)));  // (< 32 kept ranks in 64: rare)

@@ -82,9 +82,12 @@ struct Scratch {
   DevBuf<uint16_t> jlvl;
   DevBuf<uint64_t> fresh, fresh2, skey, skey2, merged, pfx;
   DevBuf<int32_t> seg_b, seg_e;
-  DevBuf<uint32_t> recmax, pdir;
+  DevBuf<uint32_t> recmax, pdir, pfx_first;
+  DevBuf<uint64_t> pfx_state;
   void release() {
     pdir.release();
+    pfx_first.release();
+    pfx_state.release();
     jlvl.release();
     merged.release();
     didx.release(); jv.release(); refsrc.release(); dcount.release(); dorder.release(); cbins.release();
@@ -107,6 +110,7 @@ struct ef_ctx {
   uint32_t wide_lpc = 8;  // lanes per candidate in k_keys_wide: 32, 16, 8 or 4 (EF_WIDE_LPC; DAG-20k keys 70.8 -> 63.9 ms from 16 to 8, 85.3 at 4)
   bool fuse_merge = false;  // rows > kFastRows: k_digest_mg merges on the fly (EF_FUSE_MERGE=1; measured slower: 52.9 vs 12.0 + 38.5 ms on DAG-20k)
   bool merge_scatter = true;  // rows > kFastRows: k_merge_scatter (EF_MERGE_SCATTER=0: k_merge_big)
+  bool pfx_share = true;  // k_prefix / the digest start at the parent's prefix state (EF_PFX_SHARE=0: from block 0)
   bool digest_pf = true;  // rows > kFastRows: k_digest_pm loads the next block's key words ahead (EF_DIGEST_PF)
   uint32_t quad_max = 20000;  // chunks below this many candidates hash with k_keys_quad (EF_QUAD_MAX)
   uint64_t chunk_mib = 0;  // per-chunk hashing scratch budget, MiB (0: 80% of the HBM free at the first sizing, <= 144 GiB)
@@ -210,6 +214,7 @@ struct ef_ctx {
   bool spec_live = false;                    // this step's speculative pricing was launched
   cudaStream_t st_price = nullptr;
   cudaEvent_t ev_sp0 = nullptr, ev_sp1 = nullptr;
+  cudaEvent_t ev_pf0 = nullptr, ev_pf1 = nullptr;  // k_pfx_chain on st_wide, beside the dirty walk
   DevBuf<ef_cand_result> d_spec;
   DevBuf<uint32_t> d_spec_list;
   cudaEvent_t ev_w0 = nullptr, ev_w1 = nullptr;
@@ -328,6 +333,7 @@ ef_ctx* ef_create(int device) {
   if (const char* e = getenv("EF_SPEC_MIN_CANDS")) ctx->spec_min_cands = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_DIGEST_PF")) ctx->digest_pf = atoi(e) != 0;
   if (const char* e = getenv("EF_MERGE_SCATTER")) ctx->merge_scatter = atoi(e) != 0;
+  if (const char* e = getenv("EF_PFX_SHARE")) ctx->pfx_share = atoi(e) != 0;
   if (const char* e = getenv("EF_QUAD_MAX")) ctx->quad_max = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_CHUNK_MIB")) ctx->chunk_mib = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
   cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
@@ -336,6 +342,8 @@ ef_ctx* ef_create(int device) {
   cudaStreamCreateWithPriority(&ctx->st_price, cudaStreamNonBlocking, prio_lo);
   cudaEventCreateWithFlags(&ctx->ev_sp0, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ctx->ev_sp1, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ctx->ev_pf0, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ctx->ev_pf1, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ctx->ev_w0, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ctx->ev_w1, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&ctx->st_copy, cudaStreamNonBlocking);
@@ -420,6 +428,8 @@ void ef_destroy(ef_ctx* ctx) {
   if (ctx->st_price) cudaStreamDestroy(ctx->st_price);
   if (ctx->ev_sp0) cudaEventDestroy(ctx->ev_sp0);
   if (ctx->ev_sp1) cudaEventDestroy(ctx->ev_sp1);
+  if (ctx->ev_pf0) cudaEventDestroy(ctx->ev_pf0);
+  if (ctx->ev_pf1) cudaEventDestroy(ctx->ev_pf1);
   ctx->d_spec.release();
   ctx->d_spec_list.release();
   ctx->d_upd_sig.release();
@@ -1550,6 +1560,22 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       V.pfx_stride = (uint32_t)(((uint64_t)ctx->input_text.size() + 18ull * ctx->h_scalars[8] + 7) / 8 + 2) & ~1u;
       EF_CUDA(sc.pfx.reserve((uint64_t)chunk * V.pfx_stride, ctx->st));
       V.pfx = sc.pfx.p;
+      if (ctx->pfx_share && ctx->dirty_big) {  // (k_dirty_big finds the first changed output)  // the parents' prefix chains, once per step
+        const uint32_t li = (uint32_t)ctx->input_text.size();
+        V.pfx_nst = ((li + 18u * ctx->h_scalars[8]) >> 7) + 1;
+        EF_CUDA(sc.pfx_state.reserve((uint64_t)n_parents * V.pfx_nst * 8, ctx->st));
+        EF_CUDA(sc.pfx_first.reserve(chunk, ctx->st));
+        V.pfx_state = sc.pfx_state.p;
+        V.pfx_first = sc.pfx_first.p;
+        // on the wide-key stream: a one-warp-per-parent chain that runs beside the dirty walk
+        EF_CUDA(cudaEventRecord(ctx->ev_pf0, ctx->st));
+        EF_CUDA(cudaStreamWaitEvent(ctx->st_wide, ctx->ev_pf0, 0));
+        ++ctx->kcount, k_pfx_chain<<<std::max<uint32_t>(1, n_parents), 32, 0, ctx->st_wide>>>(
+            A.parent_addr, ctx->geo, n_parents, reinterpret_cast<const uint64_t*>(ctx->d_input_text.p), li, V.pfx_nst,
+            sc.pfx_state.p);
+        EF_CUDA(cudaGetLastError());
+        EF_CUDA(cudaEventRecord(ctx->ev_pf1, ctx->st_wide));
+      }
     }
     // k_merge_scatter: the parents' top-bit directories, once per step
     const bool ms16 = S < 65536u;  // positions as 16-bit words; then the merge sorts the fresh keys too
@@ -1641,6 +1667,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
           }
           EF_CUDA(cudaGetLastError());
           if (V.pfx) {
+            if (V.pfx_state && c0 == 0) EF_CUDA(cudaStreamWaitEvent(ctx->st, ctx->ev_pf1, 0));  // the parents' chains
             const uint32_t gpx = std::max<uint32_t>(1, std::min<uint32_t>((V.n + 3) / 4, ctx->n_sm * 16));
             ++ctx->kcount, k_prefix<<<gpx, 128, 0, ctx->st>>>(V);
           }

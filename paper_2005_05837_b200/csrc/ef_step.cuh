@@ -108,6 +108,9 @@ struct VArgs {
   uint64_t* pfx;       // [n][pfx_stride] the digest's prefix (input text, output keys and ports) as
                        // little-endian words (k_prefix), or null: the digest assembles it itself
   uint32_t pfx_stride;
+  uint32_t* pfx_first;        // [n] first graph output whose (key, port) differs from the parent's (k_dirty_big)
+  const uint64_t* pfx_state;  // [parent][pfx_nst][8] BLAKE2b state of the parent's digest after b prefix blocks
+  uint32_t pfx_nst;           //   (k_pfx_chain), or null: every digest starts from block 0
   uint32_t* err;
   // full mode (whole records: uploads, kept candidates): parent_addr[c] is record c itself,
   // every node is a job, jv[c][j] = position of job j; graph hashes go to hash_out[c]
@@ -768,7 +771,16 @@ __global__ void __launch_bounds__(WARPS * 32) k_dirty_big(VArgs A) {
     }
     const uint32_t* pouts = R.outs(G);
     uint32_t* os = A.outsrc + (uint64_t)lc * A.Os;
-    for (int o = lane; o < R.h().n_out; o += 32) os[o] = src_pos(vremap(P, pouts[o]));
+    uint32_t o_first = 0xffffffffu;
+    for (int o = lane; o < R.h().n_out; o += 32) {
+      const uint32_t ref = pouts[o], sv = src_pos(vremap(P, ref));
+      os[o] = sv;
+      if (sv != (((ref & 255u) << 23) | (ref >> 8))) o_first = min(o_first, (uint32_t)o);  // not the parent's own key
+    }
+    if (A.pfx_first) {
+      o_first = __reduce_min_sync(full, o_first);
+      if (lane == 0) A.pfx_first[lc] = min(o_first, (uint32_t)R.h().n_out);
+    }
     __syncwarp();
     uint32_t* grm = A.rmask + (uint64_t)lc * A.W;
     for (uint32_t w = lane; w < nw; w += 32) grm[w] = rk[w];
@@ -2502,6 +2514,42 @@ __global__ void __launch_bounds__(BT) k_merge_scatter(VArgs A) {
 // 18 bytes per output) as aligned little-endian words, a warp per candidate and a lane per
 // word (at most two output records per word), so the digest thread streams it like the keys
 // instead of chaining output -> source -> key loads and byte pushes.
+// word q of the digest's prefix: the input text, then 18-byte output records
+// rec(r, key0, key1, port_be) (graph.py:541-547), as little-endian words
+template <class RecF>
+__device__ __forceinline__ uint64_t prefix_word(uint32_t q, uint32_t li, const uint64_t* input_words, RecF rec) {
+  const uint32_t x = 8u * q;
+  if (x + 8u <= li) return __ldg(input_words + q);  // input text only
+  uint32_t b = 0;  // bytes of this word taken so far
+  uint64_t wv = 0;
+  if (x < li) {  // the input text's tail (the words are zero padded)
+    b = li - x;
+    wv = __ldg(input_words + q) & ((1ull << (8 * b)) - 1ull);
+  }
+  // stream bytes [y, y + 8 - b) of the output records: record r from byte o, then r + 1
+  const uint32_t y = x + b - li, r = y / 18u, o = y - 18u * r;
+  uint64_t a0, a1, ap, n0 = 0, n1 = 0, np = 0;
+  rec(r, a0, a1, ap);
+  if (o + (8u - b) > 18u) rec(r + 1, n0, n1, np);
+  // the two records as little-endian words: a0 | a1 | ap + n0 << 16 | n0 >> 48 + n1 << 16
+  const uint64_t w2 = ap | (n0 << 16), w3 = (n0 >> 48) | (n1 << 16);
+  const uint32_t jw = o >> 3, sh = 8u * (o & 7u);
+  const uint64_t lo = jw == 0 ? a0 : jw == 1 ? a1 : w2;
+  const uint64_t hi = jw == 0 ? a1 : jw == 1 ? w2 : w3;
+  uint64_t v = sh ? (lo >> sh) | (hi << (64u - sh)) : lo;
+  if (b) v &= (1ull << (8 * (8 - b))) - 1ull;
+  return wv | (v << (8 * b));
+}
+
+// The first prefix block a candidate's digest must compress: its prefix equals the parent's up
+// to output pfx_first, so the blocks before that byte are the parent's, whose BLAKE2b states
+// k_pfx_chain has saved (the digest and k_prefix both start there).
+__device__ __forceinline__ uint32_t pfx_block0(const VArgs& A, uint32_t lc, uint32_t li, uint32_t n_out) {
+  if (!A.pfx_state) return 0u;
+  const uint32_t fb = li + 18u * A.pfx_first[lc];
+  return min(fb >> 7, (li + 18u * n_out) >> 7);
+}
+
 __global__ void __launch_bounds__(128) k_prefix(VArgs A) {
   const Geo& G = A.g;
   const uint32_t lane = threadIdx.x & 31u;
@@ -2543,31 +2591,46 @@ __global__ void __launch_bounds__(128) k_prefix(VArgs A) {
     const uint32_t len = li + 18u * n_out;
     const uint32_t nwd = (len + 7) >> 3;
     uint64_t* out = A.pfx + (uint64_t)lc * A.pfx_stride;
-    for (uint32_t q = lane; q < nwd; q += 32) {
-      const uint32_t x = 8u * q;
-      if (x + 8u <= li) {  // input text only
-        out[q] = __ldg(A.input_words + q);
-        continue;
+    for (uint32_t q = 16u * pfx_block0(A, lc, li, n_out) + lane; q < nwd; q += 32)  // (the parent's blocks are skipped)
+      out[q] = prefix_word(q, li, A.input_words, rec);
+  }
+}
+
+// The parent's prefix chain: a warp per parent builds each 128-byte prefix block (16 lanes, a
+// word each) and one lane compresses it, saving the state after every block.
+__global__ void __launch_bounds__(32) k_pfx_chain(const unsigned long long* parent_addr, const Geo G, uint32_t n_parents,
+                                                 const uint64_t* input_words, uint32_t li, uint32_t nst, uint64_t* states) {
+  __shared__ uint64_t m[16];
+  const uint32_t lane = threadIdx.x;
+  for (uint32_t pi = blockIdx.x; pi < n_parents; pi += gridDim.x) {
+    Rec R{reinterpret_cast<char*>(parent_addr[pi])};
+    const uint64_t* pkeys = R.keys(G);
+    const uint32_t* pouts = R.outs(G);
+    const uint32_t n_out = (uint32_t)R.h().n_out;
+    auto rec = [&](uint32_t r, uint64_t& k0, uint64_t& k1, uint64_t& pbe) {
+      if (r >= n_out) {
+        k0 = k1 = pbe = 0;
+        return;
       }
-      uint32_t b = 0;  // bytes of this word taken so far
-      uint64_t wv = 0;
-      if (x < li) {  // the input text's tail (the words are zero padded)
-        b = li - x;
-        wv = __ldg(A.input_words + q) & ((1ull << (8 * b)) - 1ull);
+      const uint32_t ref = pouts[r];
+      k0 = pkeys[2 * (ref >> 8)];
+      k1 = pkeys[2 * (ref >> 8) + 1];
+      pbe = port_be(ref & 255u);
+    };
+    const uint32_t nbp = min((li + 18u * n_out) >> 7, nst - 1);
+    uint64_t* st = states + (uint64_t)pi * nst * 8;
+    uint64_t h[8];
+    b2b_start(h, 8);
+    if (lane < 8) st[lane] = h[lane];
+    for (uint32_t b = 0; b < nbp; ++b) {
+      if (lane < 16) m[lane] = prefix_word(16u * b + lane, li, input_words, rec);
+      __syncwarp();
+      if (lane == 0) {
+        b2b_compress(h, m, 128ull * (b + 1), false);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) st[8ull * (b + 1) + i] = h[i];
       }
-      // stream bytes [y, y + 8 - b) of the output records: record r from byte o, then r + 1
-      const uint32_t y = x + b - li, r = y / 18u, o = y - 18u * r;
-      uint64_t a0, a1, ap, n0 = 0, n1 = 0, np = 0;
-      rec(r, a0, a1, ap);
-      if (o + (8u - b) > 18u) rec(r + 1, n0, n1, np);
-      // the two records as little-endian words: a0 | a1 | ap + n0 << 16 | n0 >> 48 + n1 << 16
-      const uint64_t w2 = ap | (n0 << 16), w3 = (n0 >> 48) | (n1 << 16);
-      const uint32_t jw = o >> 3, sh = 8u * (o & 7u);
-      const uint64_t lo = jw == 0 ? a0 : jw == 1 ? a1 : w2;
-      const uint64_t hi = jw == 0 ? a1 : jw == 1 ? w2 : w3;
-      uint64_t v = sh ? (lo >> sh) | (hi << (64u - sh)) : lo;
-      if (b) v &= (1ull << (8 * (8 - b))) - 1ull;
-      out[q] = wv | (v << (8 * b));
+      __syncwarp();
     }
   }
 }
@@ -2611,8 +2674,15 @@ __global__ void __launch_bounds__(BT, MINB) k_digest_pm(VArgs A) {
     // the prefix from k_prefix: pw_full whole words, then pw_rem bytes
     const uint64_t* pw = A.pfx ? A.pfx + (uint64_t)lc * A.pfx_stride : nullptr;
     const uint32_t pw_full = (uint32_t)(((uint64_t)li + 18ull * n_out) >> 3), pw_rem = (uint32_t)((li + 18ull * n_out) & 7);
-    uint32_t pq = 0;
-    for (uint32_t b = 0; b < nblk; ++b) {
+    uint32_t pq = 0, b0 = 0;
+    if (pw && A.pfx_state) {  // the blocks before the first changed output are the parent's: start from its state
+      b0 = pfx_block0(A, lc, li, (uint32_t)n_out);
+      const uint64_t* ps = A.pfx_state + ((uint64_t)P.parent * A.pfx_nst + b0) * 8;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) h[i] = ps[i];
+      pq = 16u * b0;
+    }
+    for (uint32_t b = b0; b < nblk; ++b) {
       sk.q = 0;
       if (pw && phase < 2) {  // whole prefix words (the sink is word-aligned until the last one)
         const uint32_t take = min(16u, pw_full - pq);
@@ -2714,7 +2784,7 @@ __global__ void __launch_bounds__(BT, MINB) k_digest_pm(VArgs A) {
       b2b_compress_col<BT>(h, col, len < 128ull * (b + 1) ? len : 128ull * (b + 1), b + 1 == nblk);
     }
     A.res[c].hash = B2b::bswap64(h[0]);
-    if (A.stats) atomicAdd(A.stats + 1, (unsigned long long)nblk);
+    if (A.stats) atomicAdd(A.stats + 1, (unsigned long long)(nblk - b0));
   }
 }
 

@@ -110,6 +110,8 @@ struct ef_ctx {
   uint32_t wide_lpc = 8;  // lanes per candidate in k_keys_wide: 32, 16, 8 or 4 (EF_WIDE_LPC; DAG-20k keys 70.8 -> 63.9 ms from 16 to 8, 85.3 at 4)
   bool fuse_merge = false;  // rows > kFastRows: k_digest_mg merges on the fly (EF_FUSE_MERGE=1; measured slower: 52.9 vs 12.0 + 38.5 ms on DAG-20k)
   bool merge_scatter = true;  // rows > kFastRows: k_merge_scatter (EF_MERGE_SCATTER=0: k_merge_big)
+  bool sparse_sweep = true;  // rows > kFastRows: d = 1 sweeps visit only movable nodes (EF_SPARSE_SWEEP=0: all)
+  DevBuf<uint32_t> d_nsk;
   bool pfx_share = true;  // k_prefix / the digest start at the parent's prefix state (EF_PFX_SHARE=0: from block 0)
   bool digest_pf = true;  // rows > kFastRows: k_digest_pm loads the next block's key words ahead (EF_DIGEST_PF)
   uint32_t quad_max = 20000;  // chunks below this many candidates hash with k_keys_quad (EF_QUAD_MAX)
@@ -334,6 +336,7 @@ ef_ctx* ef_create(int device) {
   if (const char* e = getenv("EF_DIGEST_PF")) ctx->digest_pf = atoi(e) != 0;
   if (const char* e = getenv("EF_MERGE_SCATTER")) ctx->merge_scatter = atoi(e) != 0;
   if (const char* e = getenv("EF_PFX_SHARE")) ctx->pfx_share = atoi(e) != 0;
+  if (const char* e = getenv("EF_SPARSE_SWEEP")) ctx->sparse_sweep = atoi(e) != 0;
   if (const char* e = getenv("EF_QUAD_MAX")) ctx->quad_max = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_CHUNK_MIB")) ctx->chunk_mib = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
   cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
@@ -416,6 +419,7 @@ void ef_destroy(ef_ctx* ctx) {
   ctx->d_sig_info.release();
   ctx->d_alg8.release();
   ctx->d_algt.release();
+  ctx->d_nsk.release();
   ctx->sc[0].release();
   ctx->sc[1].release();
   ctx->d_up_stage.release();
@@ -1787,6 +1791,18 @@ static int launch_price(ef_ctx* ctx, const ef_price_params* pp, uint32_t total, 
   }
   if (fast && !sm && !Pv.algt)  // the global rows start at row 0 (price_d1 writes changes only)
     EF_CUDA(cudaMemsetAsync(ctx->d_alg8.p, 0, (uint64_t)std::max<uint32_t>(total, 1) * ctx->step_S, st));
+  if (fast && !sm && ctx->sparse_sweep && ctx->step_n_parents) {  // the parents' movable-node bits (sparse sweeps)
+    const uint32_t W = (ctx->geo.cap_nodes + 31) / 32;
+    EF_CUDA(ctx->d_nsk.reserve((uint64_t)ctx->step_n_parents * W, st));
+    Pv.nsk = ctx->d_nsk.p;
+    Pv.nsk_W = W;
+    const uint32_t gn = std::min<uint32_t>(ctx->step_n_parents, ctx->n_sm * 8);
+    if (pp->kind == EF_C_ENERGY) ++ctx->kcount, k_price_nsk<EF_C_ENERGY><<<gn, 256, 0, st>>>(Pv.pa, ctx->d_parent_addr.p, ctx->d_pscratch.p, Pv.pstride, ctx->step_n_parents, W, ctx->d_nsk.p);
+    else if (pp->kind == EF_C_TIME) ++ctx->kcount, k_price_nsk<EF_C_TIME><<<gn, 256, 0, st>>>(Pv.pa, ctx->d_parent_addr.p, ctx->d_pscratch.p, Pv.pstride, ctx->step_n_parents, W, ctx->d_nsk.p);
+    else if (pp->kind == EF_C_LINEAR) ++ctx->kcount, k_price_nsk<EF_C_LINEAR><<<gn, 256, 0, st>>>(Pv.pa, ctx->d_parent_addr.p, ctx->d_pscratch.p, Pv.pstride, ctx->step_n_parents, W, ctx->d_nsk.p);
+    else ++ctx->kcount, k_price_nsk<EF_C_MIX + 1><<<gn, 256, 0, st>>>(Pv.pa, ctx->d_parent_addr.p, ctx->d_pscratch.p, Pv.pstride, ctx->step_n_parents, W, ctx->d_nsk.p);
+    EF_CUDA(cudaGetLastError());
+  }
   if (fast && pp->kind == EF_C_ENERGY) EF_PRICE(EF_C_ENERGY);
   else if (fast && pp->kind == EF_C_TIME) EF_PRICE(EF_C_TIME);
   else if (fast && pp->kind == EF_C_LINEAR) EF_PRICE(EF_C_LINEAR);

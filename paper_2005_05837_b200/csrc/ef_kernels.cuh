@@ -1361,6 +1361,15 @@ __device__ __forceinline__ double cost_of(const ef_price_params& f, const Recip&
 // sweep reads no row entry and a sweep writes a node's entry only when it changes.  The row
 // holds ROW indices, not algorithm ids; the ids are read from the signature's rows where a
 // record is written (k_keep_alg).
+// the sparse-sweep mask of a view (VirtView on a parent: k_price_nsk), else null; the sparse
+// sweep itself is VirtView's (ef_step.cuh), never reached for other views
+template <class View>
+__device__ __forceinline__ const uint32_t* view_nsk(const View&) { return nullptr; }
+template <class View, class F>
+__device__ __forceinline__ void sparse_sweep(const View&, unsigned, bool, const uint32_t*, const Tables&, F&&, int& n_dense0) {
+  n_dense0 = 0;
+}
+
 template <int KIND, class View, class Alg>
 __device__ void price_d1(const PriceArgs& A, const View& V, Alg alg, ef_cand_result& res, unsigned mask,
                          uint32_t skip) {
@@ -1414,16 +1423,11 @@ __device__ void price_d1(const PriceArgs& A, const View& V, Alg alg, ef_cand_res
       evals += skip_evals;
     }
     const bool first = sweeps == 1;
-    for (int i0 = 0; i0 < nmax; i0 += G) {
-      uint2 inf[G];  // the rows of G nodes requested together
-#pragma unroll
-      for (int k = 0; k < G; ++k) inf[k] = running && i0 + k < n ? V.info(i0 + k, T) : make_uint2(0u, kInfoInput);
-#pragma unroll
-      for (int k = 0; k < G; ++k) {
-        const int i = i0 + k;
-        const uint32_t nr = inf[k].y & kInfoRows;
-        if (nr < 2u || (inf[k].y & kInfoInput) || (skip && (inf[k].y & skip) == skip)) continue;
-        const uint32_t ro = inf[k].x;
+    // node i with info word pair inf: the first-improvement pass over its rows
+    auto sweep_node = [&](const int i, const uint2 in) {
+        const uint32_t nr = in.y & kInfoRows;
+        if (nr < 2u || (in.y & kInfoInput) || (skip && (in.y & skip) == skip)) return;
+        const uint32_t ro = in.x;
         const uint32_t start = first ? 0u : (uint32_t)alg[i];
         uint32_t cur = start;
         double ct = T.row_t[ro + cur], ce = T.row_e[ro + cur];
@@ -1446,6 +1450,20 @@ __device__ void price_d1(const PriceArgs& A, const View& V, Alg alg, ef_cand_res
           changed = changed || take;
         }
         if (cur != start) alg[i] = (uint8_t)cur;
+    };
+    const uint32_t* nsk = view_nsk(V);
+    if (nsk) {  // sparse: only the parent positions whose node can move (k_price_nsk), in order
+      int n_dense0;
+      sparse_sweep(V, mask, running, nsk, T, sweep_node, n_dense0);
+      for (int i0 = n_dense0; i0 < nmax; ++i0)  // then the new nodes (ids n_keep, n_keep + 1)
+        if (running && i0 < n) sweep_node(i0, V.info(i0, T));
+    } else {
+      for (int i0 = 0; i0 < nmax; i0 += G) {
+        uint2 inf[G];  // the rows of G nodes requested together
+#pragma unroll
+        for (int k = 0; k < G; ++k) inf[k] = running && i0 + k < n ? V.info(i0 + k, T) : make_uint2(0u, kInfoInput);
+#pragma unroll
+        for (int k = 0; k < G; ++k) sweep_node(i0 + k, inf[k]);
       }
     }
     running = running && changed;

@@ -3055,6 +3055,7 @@ __global__ void k_rec_max(const unsigned long long* rec, uint32_t n, uint32_t* o
 // ------------------------------------------------------------------------------------------
 
 struct VirtView {
+  const uint32_t* nsk;  // the parent's movable-node bits (k_price_nsk), or null: the dense sweep
   const uint32_t* psig;
   const uint32_t* p_ro;  // the parent's per-node price rows (k_match)
   const uint32_t* p_rn;
@@ -3084,7 +3085,65 @@ struct VirtView {
   }
 };
 
+__device__ __forceinline__ const uint32_t* view_nsk(const VirtView& V) { return V.nsk; }
+
+// The d = 1 sweep over the parent positions whose node can move (>= 2 rows, not an input, not
+// skipped by the kind's exact shortcut: k_price_nsk), in order, with the candidate's dropped
+// positions cleared and its rewritten node always visited (sweep_node re-checks every node, so
+// a superset is exact).  The other nodes of the dense sweep do nothing but count, so the result
+// is the dense sweep's bit for bit; the new nodes (ids n_keep, n_keep + 1) follow densely.
+template <class F>
+__device__ __forceinline__ void sparse_sweep(const VirtView& V, unsigned mask, bool running, const uint32_t* nsk,
+                                             const Tables& T, F&& sweep_node, int& n_dense0) {
+  const int npp = V.n_keep + (V.drop0 >= 0 ? 1 : 0) + (V.drop1 >= 0 ? 1 : 0);
+  const int nwm = (int)__reduce_max_sync(mask, (unsigned)((npp + 31) >> 5));
+  for (int w = 0; w < nwm; ++w) {
+    uint32_t x = 0;
+    if (running && 32 * w < npp) {
+      x = nsk[w];
+      if (V.drop0 >= 0 && (V.drop0 >> 5) == w) x &= ~(1u << (V.drop0 & 31));
+      if (V.drop1 >= 0 && (V.drop1 >> 5) == w) x &= ~(1u << (V.drop1 & 31));
+      if (V.mod >= 0 && (V.mod >> 5) == w) x |= 1u << (V.mod & 31);
+    }
+    for (uint32_t u = __reduce_or_sync(mask, x); u; u &= u - 1u) {  // warp-uniform, ascending
+      const int b = __ffs(u) - 1;
+      if ((x >> b) & 1u) {
+        const int pp = 32 * w + b;
+        const int i = pp - (V.drop0 >= 0 && pp > V.drop0 ? 1 : 0) - (V.drop1 >= 0 && pp > V.drop1 ? 1 : 0);
+        sweep_node(i, pp == V.mod ? T.sig_info[V.mod_sig] : make_uint2(V.p_ro[pp], V.p_rn[pp]));
+      }
+    }
+  }
+  n_dense0 = V.n_keep;
+}
+
+// per parent: bit pp set when the d = 1 sweep can move node pp (price_d1's own test)
+template <int KIND>
+__global__ void k_price_nsk(PriceArgs PA, const unsigned long long* parent_addr, const uint32_t* pscratch,
+                            uint64_t pstride, uint32_t n_parents, uint32_t W, uint32_t* nsk) {
+  const Geo& G = PA.g;
+  const uint32_t skip = d1_skip_bits<KIND>(PA.pp);
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (uint32_t pi = blockIdx.x; pi < n_parents; pi += gridDim.x) {
+    Rec R{reinterpret_cast<char*>(parent_addr[pi])};
+    const uint32_t n = (uint32_t)R.h().n;
+    const uint32_t* p_rn = pscratch + (uint64_t)pi * pstride + 7ull * G.cap_nodes + 1 + 2ull * G.cap_refs + G.cap_nodes;
+    for (uint32_t w = wid; w < W; w += nwarps) {
+      const uint32_t pp = 32u * w + lane;
+      bool mv = false;
+      if (pp < n) {
+        const uint32_t y = p_rn[pp], nr = y & kInfoRows;
+        mv = !(nr < 2u || (y & kInfoInput) || (skip && (y & skip) == skip));
+      }
+      const uint32_t word = __ballot_sync(0xffffffffu, mv);
+      if (lane == 0) nsk[(uint64_t)pi * W + w] = word;
+    }
+  }
+}
+
 struct VPriceArgs {
+  const uint32_t* nsk;  // [parent][nsk_W] k_price_nsk, or null
+  uint32_t nsk_W;
   PriceArgs pa;
   const uint32_t* pscratch;
   uint64_t pstride;
@@ -3112,6 +3171,7 @@ __global__ void __launch_bounds__(EF_PRICE_THREADS) k_price_v(VPriceArgs A, cons
     const VPlan& P = A.plan[c];
     Rec R{reinterpret_cast<char*>(A.parent_addr[P.parent])};
     VirtView V;
+    V.nsk = A.nsk ? A.nsk + (uint64_t)P.parent * A.nsk_W : nullptr;
     V.psig = R.sig(G);
     V.p_ro = A.pscratch + (uint64_t)P.parent * A.pstride + 7ull * G.cap_nodes + 1 + 2ull * G.cap_refs;
     V.p_rn = V.p_ro + G.cap_nodes;

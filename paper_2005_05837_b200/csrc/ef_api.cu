@@ -110,6 +110,12 @@ struct ef_ctx {
   uint32_t wide_lpc = 8;  // lanes per candidate in k_keys_wide: 32, 16, 8 or 4 (EF_WIDE_LPC; DAG-20k keys 70.8 -> 63.9 ms from 16 to 8, 85.3 at 4)
   bool fuse_merge = false;  // rows > kFastRows: k_digest_mg merges on the fly (EF_FUSE_MERGE=1; measured slower: 52.9 vs 12.0 + 38.5 ms on DAG-20k)
   bool merge_scatter = true;  // rows > kFastRows: k_merge_scatter (EF_MERGE_SCATTER=0: k_merge_big)
+  // ... on rows above EF_MS_MIN_ROWS (k_merge_big below), sorting the fresh keys itself on rows
+  // above EF_MS_SORT_MIN (k_sortkeys below).  Both 0: every row > kFastRows.  Measured per step
+  // against k_sortkeys + k_merge_big: Inception-v3 8.61 -> 8.17 ms, NasNet-A 9.39 -> 6.73 ms,
+  // DAG-1k 11.8 -> 10.0 ms (k_sortkeys + k_merge_scatter: 9.37 / 9.44 / 11.8)
+  uint32_t ms_min_rows = 0;
+  uint32_t ms_sort_min_rows = 0;
   bool sparse_sweep = true;  // rows > kFastRows: d = 1 sweeps visit only movable nodes (EF_SPARSE_SWEEP=0: all)
   DevBuf<uint32_t> d_nsk;
   bool pfx_share = true;  // k_prefix / the digest start at the parent's prefix state (EF_PFX_SHARE=0: from block 0)
@@ -204,7 +210,10 @@ struct ef_ctx {
   // 2.60 with 4, 4.47 with 8; ResNet-50 0.384 -> 0.372 / 0.514 / 0.902 ms: the first sweep
   // takes at most nodes, so its windows commit one node each and the converged sweeps' L-fold
   // parallelism only pays at 2 lanes.  DAG-20k (global rows): 28.8 -> 53.5 ms at 2 lanes.
-  uint32_t price_lanes = 2;
+  // Since the sparse sweeps (k_price_nsk), one thread per candidate visiting only the movable
+  // nodes wins everywhere, so lanes are off by default: ResNet-50 0.367 -> 0.328 ms, Inception-v3
+  // 1.80 -> 1.39 ms (dense k_price_v: 0.370 / 2.33).
+  uint32_t price_lanes = 0;
   int spec_price = -1;             // -1: by row size and candidate count (below), 0 off, 1 .. 4 forced
   int spec_mode = 0;               // this step's launch point (1 digest, 2 plans, 3 node keys, 4 key sort; 0: none)
   uint32_t spec_min_rows = 2048;   // rows (S) from which the auto policy prices from the plans on
@@ -335,6 +344,8 @@ ef_ctx* ef_create(int device) {
   if (const char* e = getenv("EF_SPEC_MIN_CANDS")) ctx->spec_min_cands = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_DIGEST_PF")) ctx->digest_pf = atoi(e) != 0;
   if (const char* e = getenv("EF_MERGE_SCATTER")) ctx->merge_scatter = atoi(e) != 0;
+  if (const char* e = getenv("EF_MS_MIN_ROWS")) ctx->ms_min_rows = (uint32_t)strtoul(e, nullptr, 10);
+  if (const char* e = getenv("EF_MS_SORT_MIN")) ctx->ms_sort_min_rows = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_PFX_SHARE")) ctx->pfx_share = atoi(e) != 0;
   if (const char* e = getenv("EF_SPARSE_SWEEP")) ctx->sparse_sweep = atoi(e) != 0;
   if (const char* e = getenv("EF_QUAD_MAX")) ctx->quad_max = (uint32_t)strtoul(e, nullptr, 10);
@@ -1582,10 +1593,13 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
       }
     }
     // k_merge_scatter: the parents' top-bit directories, once per step
-    const bool ms16 = S < 65536u;  // positions as 16-bit words; then the merge sorts the fresh keys too
-    const size_t ms_smem = 4ull * (2ull * V.W + 3) + (ms16 ? 4ull * (1u << kDirBits) + 6ull * kMsDcap : 4ull * S);
+    const bool ms16 = S < 65536u;  // positions as 16-bit words
+    const bool ms_sort = ms16 && S > ctx->ms_sort_min_rows;  // the merge sorts the fresh keys too (k_sortkeys below)
+    const size_t ms_smem =
+        4ull * (2ull * V.W + 3) + (ms_sort ? 4ull * (1u << kDirBits) + 6ull * kMsDcap : (ms16 ? 2ull : 4ull) * S);
     V.pdir = nullptr;
-    if (total && S > kFastRows && ctx->big_merge && !ctx->fuse_merge && ctx->merge_scatter && ms_smem <= 200ull * 1024) {
+    if (total && S > kFastRows && S > ctx->ms_min_rows && ctx->big_merge && !ctx->fuse_merge && ctx->merge_scatter &&
+        ms_smem <= 200ull * 1024) {
       EF_CUDA(sc.pdir.reserve((uint64_t)kDirN * n_parents, ctx->st));
       V.pdir = sc.pdir.p;
       ++ctx->kcount, k_merge_dir<<<std::max<uint32_t>(1, std::min<uint32_t>(n_parents, ctx->n_sm * 8)), 256, 0, ctx->st>>>(
@@ -1647,7 +1661,7 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
         ++ctx->kcount, k_digest_pm<kHashThreads, false, EF_DIGEST_MINB><<<gd, kHashThreads, 0, ctx->st>>>(V);
       } else {
         if (ctx->spec_mode == 4 && (rc = launch_spec_price(ctx, total))) return rc;  // beside the key sort
-        if (!(V.pdir && ms16) && (rc = sort_fresh_keys(ctx, sc, ctx->st, V))) return rc;  // (k_merge_scatter sorts)
+        if (!(V.pdir && ms_sort) && (rc = sort_fresh_keys(ctx, sc, ctx->st, V))) return rc;  // (k_merge_scatter sorts)
         if (ctx->spec_mode && (rc = launch_spec_price(ctx, total))) return rc;  // under the digest
         if (ctx->big_merge && ctx->fuse_merge) {  // the digest merges the two sorted streams itself
           cudaEventRecord(ce[3], ctx->st);
@@ -1656,9 +1670,12 @@ static int step_hash(ef_ctx* ctx, const uint32_t* parent_slots, uint32_t n_paren
           if (V.pdir) {
             const uint32_t per_sm = std::max<uint32_t>(1, std::min<uint32_t>(8, (uint32_t)((220ull * 1024) / (ms_smem + 2048))));
             const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>(V.n, ctx->n_sm * per_sm));
-            if (ms16) {
+            if (ms_sort) {
               EF_CUDA(cudaFuncSetAttribute(k_merge_scatter<256, uint16_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
               ++ctx->kcount, k_merge_scatter<256, uint16_t, true><<<gm, 256, ms_smem, ctx->st>>>(V);
+            } else if (ms16) {
+              EF_CUDA(cudaFuncSetAttribute(k_merge_scatter<256, uint16_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
+              ++ctx->kcount, k_merge_scatter<256, uint16_t, false><<<gm, 256, ms_smem, ctx->st>>>(V);
             } else {
               EF_CUDA(cudaFuncSetAttribute(k_merge_scatter<256, uint32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
               ++ctx->kcount, k_merge_scatter<256, uint32_t, false><<<gm, 256, ms_smem, ctx->st>>>(V);
@@ -1791,7 +1808,7 @@ static int launch_price(ef_ctx* ctx, const ef_price_params* pp, uint32_t total, 
   }
   if (fast && !sm && !Pv.algt)  // the global rows start at row 0 (price_d1 writes changes only)
     EF_CUDA(cudaMemsetAsync(ctx->d_alg8.p, 0, (uint64_t)std::max<uint32_t>(total, 1) * ctx->step_S, st));
-  if (fast && !sm && ctx->sparse_sweep && ctx->step_n_parents) {  // the parents' movable-node bits (sparse sweeps)
+  if (fast && ctx->sparse_sweep && ctx->step_n_parents) {  // the parents' movable-node bits (sparse sweeps)
     const uint32_t W = (ctx->geo.cap_nodes + 31) / 32;
     EF_CUDA(ctx->d_nsk.reserve((uint64_t)ctx->step_n_parents * W, st));
     Pv.nsk = ctx->d_nsk.p;

@@ -2377,20 +2377,23 @@ __global__ void __launch_bounds__(BT) k_merge_scatter(VArgs A) {
     const uint32_t* D = A.pdir + (uint64_t)P.parent * kDirN;
     const uint4* bk = reinterpret_cast<const uint4*>(A.fresh_sorted + 2ull * lc * A.S);
     if (SORT) {  // the fresh keys in key order: perm[k] = job index of the k-th smallest
-      for (uint32_t b = threadIdx.x; b < (1u << kDirBits); b += BT) bins[b] = 0;
+      uint32_t lg = 5;  // pow2(d) buckets, 32 .. 2^12, on the top bits (~1 key each)
+      while ((1u << lg) < d && lg < kDirBits) ++lg;
+      const uint32_t nbk = 1u << lg;
+      for (uint32_t b = threadIdx.x; b < nbk; b += BT) bins[b] = 0;
       __syncthreads();
       for (uint32_t j = threadIdx.x; j < d; j += BT) {
         const uint2 x = reinterpret_cast<const uint2*>(fk + j)[0];
         const uint32_t tw = __byte_perm(x.x, 0, 0x0123);  // first 4 key bytes, big endian
         top[j] = tw;
-        atomicAdd(&bins[tw >> (32 - kDirBits)], 1u);
+        atomicAdd(&bins[tw >> (32 - lg)], 1u);
       }
       __syncthreads();
-      block_excl_scan_inplace<BT>(bins, 1u << kDirBits, wsum);
+      block_excl_scan_inplace<BT>(bins, nbk, wsum);
       __syncthreads();
-      for (uint32_t j = threadIdx.x; j < d; j += BT) perm[atomicAdd(&bins[top[j] >> (32 - kDirBits)], 1u)] = (uint16_t)j;
+      for (uint32_t j = threadIdx.x; j < d; j += BT) perm[atomicAdd(&bins[top[j] >> (32 - lg)], 1u)] = (uint16_t)j;
       __syncthreads();
-      for (uint32_t b = threadIdx.x; b < (1u << kDirBits); b += BT) {  // bins[b]: the end of bucket b
+      for (uint32_t b = threadIdx.x; b < nbk; b += BT) {  // bins[b]: the end of bucket b
         const uint32_t e = bins[b], s0 = b ? bins[b - 1] : 0u;
         for (uint32_t x = s0 + 1; x < e; ++x) {  // by the first 4 bytes, the full key on a tie
           const uint16_t v = perm[x];

@@ -111,7 +111,8 @@ RULES = ["fuse-conv-relu", "split-conv-activation", "merge-parallel-convs", "spl
 
 # the committed `ncu --set full` captures, newest first (tools/ncu_summary.py): the traffic
 # figure of a kernel comes from the newest capture that holds it
-PROFILES = [os.path.join("profiles", f) for f in ("ncu_r02c_dag20k_kernels.json", "ncu_r02c_resnet50_kernels.json",
+PROFILES = [os.path.join("profiles", f) for f in ("ncu_r02d_dag20k_kernels.json", "ncu_r02d_resnet50_kernels.json",
+                                                   "ncu_r02c_dag20k_kernels.json", "ncu_r02c_resnet50_kernels.json",
                                                    "ncu_r02aa_dag20k_kernels.json", "ncu_r02aa_resnet50_kernels.json",
                                                    "ncu_r02w_kernels.json", "ncu_r01f_kernels.json")]
 

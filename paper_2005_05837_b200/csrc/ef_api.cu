@@ -212,8 +212,12 @@ struct ef_ctx {
   // parallelism only pays at 2 lanes.  DAG-20k (global rows): 28.8 -> 53.5 ms at 2 lanes.
   // Since the sparse sweeps (k_price_nsk), one thread per candidate visiting only the movable
   // nodes wins everywhere, so lanes are off by default: ResNet-50 0.367 -> 0.328 ms, Inception-v3
-  // 1.80 -> 1.39 ms (dense k_price_v: 0.370 / 2.33).
+  // 1.80 -> 1.39 ms (dense k_price_v: 0.370 / 2.33).  Small steps (the batched outer_search's,
+  // a few thousand candidates) are latency-bound and keep 2 lanes: ResNet-50 3000-expansion
+  // search 0.85 s warm with 2 lanes, 1.67 s with one thread.
   uint32_t price_lanes = 0;
+  int price_lanes_env = 0;          // EF_PRICE_LANES given: that, whatever the step size
+  uint32_t lanes_max_cands = 32768;  // steps below this many candidates: 2 lanes (EF_LANES_MAX_CANDS)
   int spec_price = -1;             // -1: by row size and candidate count (below), 0 off, 1 .. 4 forced
   int spec_mode = 0;               // this step's launch point (1 digest, 2 plans, 3 node keys, 4 key sort; 0: none)
   uint32_t spec_min_rows = 2048;   // rows (S) from which the auto policy prices from the plans on
@@ -338,12 +342,14 @@ ef_ctx* ef_create(int device) {
   if (const char* e = getenv("EF_PRICE_LANES")) {
     const uint32_t v = (uint32_t)strtoul(e, nullptr, 10);
     ctx->price_lanes = v >= 8 ? 8u : v >= 4 ? 4u : v >= 2 ? 2u : 0u;
+    ctx->price_lanes_env = 1;
   }
   if (const char* e = getenv("EF_SPEC_MIN_ROWS")) ctx->spec_min_rows = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_SPEC_MAX_CANDS")) ctx->spec_max_cands = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_SPEC_MIN_CANDS")) ctx->spec_min_cands = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_DIGEST_PF")) ctx->digest_pf = atoi(e) != 0;
   if (const char* e = getenv("EF_MERGE_SCATTER")) ctx->merge_scatter = atoi(e) != 0;
+  if (const char* e = getenv("EF_LANES_MAX_CANDS")) ctx->lanes_max_cands = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_MS_MIN_ROWS")) ctx->ms_min_rows = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_MS_SORT_MIN")) ctx->ms_sort_min_rows = (uint32_t)strtoul(e, nullptr, 10);
   if (const char* e = getenv("EF_PFX_SHARE")) ctx->pfx_share = atoi(e) != 0;
@@ -1786,8 +1792,9 @@ static int launch_price(ef_ctx* ctx, const ef_price_params* pp, uint32_t total, 
     }                                                                                                      \
   } while (0)
   ctx->alg_rows = fast;  // price_d1 leaves row indices (k_keep_alg reads the ids)
-  if (fast && ctx->price_lanes >= 2 && !out && ctx->step_S <= 2048) {  // a lane group per candidate (price_d1_lanes)
-    const uint32_t PL = ctx->price_lanes;
+  const uint32_t lanes = ctx->price_lanes_env ? ctx->price_lanes : total < ctx->lanes_max_cands ? 2u : ctx->price_lanes;
+  if (fast && lanes >= 2 && !out && ctx->step_S <= 2048) {  // a lane group per candidate (price_d1_lanes)
+    const uint32_t PL = lanes;
     const uint32_t gl = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)(((uint64_t)total * PL + kPriceThreads - 1) / kPriceThreads),
                                                                  ctx->n_sm * 32));
     const size_t rows = (size_t)(kPriceThreads / PL) * ctx->step_S;

@@ -1050,8 +1050,11 @@ __global__ void __launch_bounds__(BT, EF_KEYS_MINB) k_keys(VArgs A) {
 // The candidate's skey row is scratch for the level sort until the keys are done.
 // ------------------------------------------------------------------------------------------
 
+#ifndef EF_WIDE_MINB  // CTAs per SM the wide-key kernel's register budget is sized for
+#define EF_WIDE_MINB 1
+#endif
 template <int BT, int LPC>
-__global__ void __launch_bounds__(BT) k_keys_wide(VArgs A) {
+__global__ void __launch_bounds__(BT, EF_WIDE_MINB) k_keys_wide(VArgs A) {
   constexpr int WPB = BT / 32;
   constexpr int GPW = 32 / LPC;  // candidates per warp
   __shared__ uint64_t msg[kKeyMaxW * BT];
